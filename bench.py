@@ -1,0 +1,335 @@
+"""Benchmark: load steps of BASELINE configs[1] (512x512 notched tension, 790k DOFs, FP64).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--case cfg2] [--scheme S1]
+
+A "step" is one load step (``staggered_step``, reference schemes.py:332-392) of the case's own
+schedule: W untimed warm-up load steps advance the state, then K load steps are timed.
+
+* ``value``   — DOF-iterations/s (SURVEY.md §8(d) reading 1a: 3*N_nodes * sum n_stag / time),
+  device-resident state, CUDA events on the solver stream around each load step, L2 flushed
+  (256 MiB write) before every timed step, outside the timed region.
+* ``e2e``     — the same metric through the reference-facing drop-in
+  ``paper_2209_07969_b200.schemes.staggered_step`` with the caller's HOST SolverState: every
+  step uploads the state, solves, and downloads the state (all copies inside the timed region).
+* ``roofline``— the dominant kernel (``k_cg``, momentum PCG): algorithmic bytes
+  168 B * N_nodes per PCG iteration / its CUDA-event time.
+* ``cpu_baseline`` — the CPU oracle port (oracle/phasefield_oracle.py, SuperLU like the
+  reference default) on the first load step of the same case, rank 0 only.
+* ``--impl reference`` — the reference's CPU algorithm (the oracle port; the Python reference
+  does not travel to the GPU box) on the same case/metric; load steps until K are done or a
+  time budget is spent.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MOM_BYTES_PER_NODE = 168.0          # momentum PCG iteration
+EVO_BYTES_PER_NODE, EVO_BYTES_PER_ELEM = 72.0, 32.0
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -------------------------------------------------------------------------------------------
+def run_ours(args, ws, rank, local):
+    from paper_2209_07969_b200 import configs as C
+    from paper_2209_07969_b200 import schemes
+    from paper_2209_07969_b200.session import DeviceSession
+
+    case = C.get_case(args.case)
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pb = C.setup(case, C.b200_api())
+    n_nodes, n_elems = pb.mesh.n_nodes, pb.mesh.n_elems
+    sess = DeviceSession(pb.disc.layout, pb.params, pb.config, device=local)
+    sess.push_state(pb.state)
+    for _ in range(args.warmup):
+        sess.step(args.scheme, pb.bcs, pb.pins)
+    sess.synchronize()
+    barrier(ws)
+    tot = dict(ms=0.0, n_stag=0, cg_u=0, cg_d=0, ms_u=0.0, ms_d=0.0, dofit=0.0, launches=0,
+               cgl_u=0, cgl_d=0)
+    per_step = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            sess.flush_l2()  # inputs of a 512^2 load step fit in L2: flush between steps
+            st = sess.step(args.scheme, pb.bcs, pb.pins)  # synchronizes at its end
+            ms = st.step_ms  # CUDA events on the solver stream around the whole load step
+            per_step.append(ms)
+            tot["ms"] += ms
+            tot["n_stag"] += st.n_stag
+            tot["cg_u"] += st.cg_iters_u
+            tot["cg_d"] += st.cg_iters_d
+            tot["ms_u"] += st.kernel_ms_u
+            tot["ms_d"] += st.kernel_ms_d
+            tot["dofit"] += st.cg_dofiters_u + st.cg_dofiters_d
+            tot["launches"] += st.launches
+            tot["cgl_u"] += st.cg_launches_u
+            tot["cgl_d"] += st.cg_launches_d
+    sess.synchronize()
+    barrier(ws)
+    t_max = allreduce_max(ws, tot["ms"])
+    # e2e: the reference-facing drop-in with host SolverState, copies inside the timed region
+    pb2 = C.setup(case, C.b200_api())
+    kind = schemes.SchemeKind(args.scheme)
+    for _ in range(args.warmup):
+        schemes.staggered_step(pb2.disc, pb2.state, kind, pb2.bcs, pb2.params, pb2.config,
+                               pb2.pins)
+    e2e_stag = 0
+    barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s2 = schemes.staggered_step(pb2.disc, pb2.state, kind, pb2.bcs, pb2.params, pb2.config,
+                                    pb2.pins)
+        e2e_stag += s2.n_stag
+    e2e_ms = allreduce_max(ws, (time.perf_counter() - t0) * 1e3)
+    h2d = 8 * (2 * n_nodes + 2 * n_nodes + 4 * 4 * n_elems)  # u, d, d_prev, 4 GP arrays
+    d2h = h2d + 8 * (16 + 4) * n_elems if schemes.SYNC_GP_STRAIN else h2d
+    ndof = 3 * n_nodes
+    value = ws * ndof * tot["n_stag"] / (t_max / 1e3)
+    peak, peak_src = peaks()
+    mom_bytes = MOM_BYTES_PER_NODE * n_nodes
+    achieved = (tot["cg_u"] * mom_bytes / 1e9) / (tot["ms_u"] / 1e3) if tot["ms_u"] else 0.0
+    evo_bytes = EVO_BYTES_PER_NODE * n_nodes + EVO_BYTES_PER_ELEM * n_elems
+    evo_achieved = (tot["cg_d"] * evo_bytes / 1e9) / (tot["ms_d"] / 1e3) if tot["ms_d"] else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k_cg_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        if tj.get("case") == args.case and tot["cgl_u"]:
+            traffic = tj["dram_bytes_per_iter"] * tot["cg_u"] / tot["cgl_u"]
+    res = {
+        "metric": "DOF-iterations/s of staggered solve (FP64)",
+        "value": value,
+        "unit": "DOF-iter/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (BASELINE configs[1] recipe: seeded structured mesh, no dataset)",
+        "config": {
+            "workload": f"{args.case}: {case.note}; scheme {args.scheme}; load steps "
+                        f"{args.warmup + 1}..{args.warmup + args.steps}",
+            "n_nodes": n_nodes, "n_elems": n_elems, "dofs": ndof,
+            "parallelism": "replicas" if ws > 1 else "single-gpu",
+            "l2": "flushed (256 MiB write) before each timed load step, outside the timing",
+            "timing": "CUDA events on the solver stream around each pf_staggered_step",
+        },
+        "load_steps_per_s": ws * args.steps / (t_max / 1e3),
+        "solver_dof_iter_per_s": ws * tot["dofit"] / (t_max / 1e3),
+        "n_stag_total": tot["n_stag"],
+        "pcg_iters": {"momentum": tot["cg_u"], "phase_field": tot["cg_d"],
+                      "momentum_launches": tot["cgl_u"], "phase_field_launches": tot["cgl_d"]},
+        "kernel_ms": {"momentum_pcg": tot["ms_u"], "phase_field_pcg": tot["ms_d"]},
+        "roofline": {
+            "kernel": "k_cg (momentum PCG, persistent cooperative)",
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "peak_source": peak_src,
+            "algorithmic_bytes": "168 B x N_nodes per momentum PCG iteration",
+            "phase_field_achieved": evo_achieved,
+        },
+        "e2e": {"value": ws * ndof * e2e_stag / (e2e_ms / 1e3), "unit": "DOF-iter/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_ms / args.steps,
+                "path": "paper_2209_07969_b200.schemes.staggered_step with host SolverState"},
+        "gpu_launches": tot["launches"],
+        "clocks": clk.summary(),
+        "per_step_ms": [round(x, 3) for x in per_step],
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(args, case)
+    sess.close()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return res if rank == 0 else None
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(ws, v):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# -------------------------------------------------------------------------------------------
+def oracle_steps(case_name, scheme, max_steps, budget_s):
+    """Run the CPU oracle port from load step 1 until max_steps or the time budget."""
+    from oracle.phasefield_oracle import oracle_api
+    from paper_2209_07969_b200 import configs as C
+
+    case = C.get_case(case_name)
+    pb = C.setup(case, oracle_api())
+    n_stag, wall, steps = 0, 0.0, 0
+    while steps < max_steps and (steps == 0 or wall < budget_s):
+        t0 = time.perf_counter()
+        st = pb.api.staggered_step(pb.disc, pb.state, scheme, pb.bcs, pb.params, pb.config,
+                                   pb.pins)
+        wall += time.perf_counter() - t0
+        n_stag += st.n_stag
+        steps += 1
+    ndof = 3 * pb.mesh.n_nodes
+    return ndof * n_stag / wall, steps, n_stag, wall
+
+
+def cpu_baseline(args, case):
+    v, steps, n_stag, wall = oracle_steps(args.case, args.scheme, 1, 0.0)
+    return {"value": v, "unit": "DOF-iter/s", "cores": 1, "kind": "port",
+            "sample": f"oracle port (SuperLU, like the reference default) on load step 1 of "
+                      f"{args.case} ({n_stag} staggered iteration(s), {wall:.1f} s)"}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return None
+    budget = float(os.environ.get("PFB200_REF_BUDGET_S", "150"))
+    v, steps, n_stag, wall = oracle_steps(args.case, args.scheme, args.steps, budget)
+    from paper_2209_07969_b200 import configs as C
+
+    case = C.get_case(args.case)
+    cores = os.cpu_count() or 1
+    sample = (f"CPU oracle port of the reference algorithm (SuperLU direct solves; SuperLU is "
+              f"single-threaded, numpy may use {cores} threads) on load steps 1..{steps} of "
+              f"{args.case} ({n_stag} staggered iterations, {wall:.1f} s); warm-up steps "
+              f"skipped and steps capped by a {budget:.0f} s budget")
+    return {
+        "impl": "reference",
+        "metric": "DOF-iterations/s of staggered solve (FP64)",
+        "value": v, "unit": "DOF-iter/s", "n_gpus": ws, "steps": steps,
+        "requested_steps": args.steps, "warmup": 0, "ms_per_step": wall * 1e3 / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE configs[1] recipe)",
+        "config": {"workload": f"{args.case}: {case.note}; scheme {args.scheme}"},
+        "cpu_baseline": {"value": v, "unit": "DOF-iter/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "DOF-iter/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--case", default="cfg2")
+    ap.add_argument("--scheme", default="S1")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup < 3 violates the timing rules", file=sys.stderr)
+    ws, rank, local = dist_env()
+    res = run_reference(args, ws, rank) if args.impl == "reference" else run_ours(
+        args, ws, rank, local)
+    if rank == 0 and res is not None:
+        print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()

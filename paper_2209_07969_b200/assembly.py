@@ -1,0 +1,101 @@
+"""Discretisation handle, Gauss-point state and the force functionals (interface mirror).
+
+``Discretization`` keeps the reference's public attributes (``mesh``, ``n_gp``, ``n_u_dofs``,
+``n_d_dofs``; ``assembly.py:92-143``) but precomputes nothing per element: the B200 operators
+are matrix-free and need only the row-compact layout (``meshing.StructuredLayout``).  At 8192^2
+the reference's ``b_u`` alone would need ~51 GB.
+
+``reaction_force`` / ``internal_force`` (``assembly.py:161-171``, ``:315-326``) evaluate the
+internal force on the GPU (``pf_reaction_force`` / ``pf_internal_force``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .material import material_key
+from .meshing import StructuredLayout
+from .session import DeviceSession
+
+
+@dataclass
+class GaussPointState:
+    """Per-Gauss-point scalars, arrays shaped (n_elems, 4) (reference assembly.py:46-72)."""
+
+    strain: np.ndarray
+    tr_eps: np.ndarray
+    tr_eps_plus: np.ndarray
+    dev_dot_dev: np.ndarray
+    psi_plus: np.ndarray
+    psi_max: np.ndarray
+
+    @classmethod
+    def zeros(cls, n_elems: int, n_gp: int) -> "GaussPointState":
+        return cls(strain=np.zeros((n_elems, n_gp, 4)), tr_eps=np.zeros((n_elems, n_gp)),
+                   tr_eps_plus=np.zeros((n_elems, n_gp)), dev_dot_dev=np.zeros((n_elems, n_gp)),
+                   psi_plus=np.zeros((n_elems, n_gp)), psi_max=np.zeros((n_elems, n_gp)))
+
+
+class Discretization:
+    """Bilinear quads with 2x2 Gauss points on a structured uniform grid."""
+
+    def __init__(self, mesh):
+        if np.asarray(mesh.elements).shape[1] != 4:
+            raise ValueError("only 4-node quadrilaterals are supported here")
+        self.mesh = mesh
+        self.n_gp = 4
+        self.layout = StructuredLayout.from_mesh(mesh)
+        self.n_u_dofs = 2 * mesh.n_nodes
+        self.n_d_dofs = mesh.n_nodes
+
+
+def _layout_of(disc) -> StructuredLayout:
+    lay = getattr(disc, "layout", None)
+    if isinstance(lay, StructuredLayout):
+        return lay
+    cache = disc.__dict__.setdefault("_pfb200_layout", [])
+    if not cache:
+        cache.append(StructuredLayout.from_mesh(disc.mesh))
+    return cache[0]
+
+
+def _config_key(cfg) -> tuple:
+    return (float(cfg.tol_nr), float(cfg.tol_st), int(cfg.max_nr), int(cfg.max_stag),
+            float(cfg.d_cap), float(cfg.res_floor))
+
+
+class _DefaultConfig:
+    tol_nr, tol_st, max_nr, max_stag, d_cap, res_floor, lin_method = (
+        1.0e-7, 1.0e-6, 50, 2000, 0.95, 1.0e-12, "direct")
+
+
+def session_for(disc, params, config=None) -> DeviceSession:
+    """The cached ``DeviceSession`` of a discretisation (ours or the reference's)."""
+    sessions = disc.__dict__.setdefault("_pfb200_sessions", {})
+    if config is None:
+        mk = material_key(params)
+        for (m, _), s in sessions.items():
+            if m == mk:
+                return s
+        config = _DefaultConfig()
+    key = (material_key(params), _config_key(config))
+    sess = sessions.get(key)
+    if sess is None:
+        sess = DeviceSession(_layout_of(disc), params, config)
+        sessions[key] = sess
+    return sess
+
+
+def internal_force(disc, u, d, params) -> np.ndarray:
+    sess = session_for(disc, params)
+    sess.push(u=u, d=d)
+    return sess.internal_force()
+
+
+def reaction_force(disc, u, d, params, node_set, component: int) -> float:
+    """Resultant of the internal force over a node set (per unit thickness)."""
+    sess = session_for(disc, params)
+    sess.push(u=u, d=d)
+    return float(sess.reaction_force(node_set, component))

@@ -1,0 +1,1001 @@
+// pf_api.cu — C-ABI (include/pf_b200.h) and host orchestration of the staggered hot path.
+//
+// Control flow mirrors the reference driver exactly (schemes.py:192-392): the Newton and
+// staggered loops run on the host and read back ONE scalar block per Newton iteration
+// (residual norm, gate count, SPD flag) through mapped pinned memory; every linear solve is ONE
+// cooperative persistent PCG launch (pf_kernels.cuh: k_cg) with device-side stopping, so no
+// host round trip happens inside a solve.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pf_b200.h"
+#include "pf_kernels.cuh"
+
+using pfb::CgResult;
+
+struct pf_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  pfb::DMesh dm{};
+  pfb::Consts C{};
+  pf_config cfg{};
+  pf_material mat{};
+  int n_nodes = 0, n_elems = 0, nx = 0, ny = 0;
+  std::vector<int> h_nlo, h_nhi, h_nst, h_elo, h_ehi, h_est;
+  // device row tables and tiles
+  int *d_nlo = nullptr, *d_nhi = nullptr, *d_nst = nullptr;
+  int *d_elo = nullptr, *d_ehi = nullptr, *d_est = nullptr;
+  int2* d_tiles = nullptr;
+  int n_tiles = 0;
+  // state
+  double *u = nullptr, *d = nullptr, *dprev = nullptr;
+  double *trp = nullptr, *dev2 = nullptr, *psi = nullptr, *psimax = nullptr;
+  // momentum work
+  double *Ru = nullptr, *ru = nullptr, *xu = nullptr, *qu = nullptr, *p0u = nullptr,
+         *p1u = nullptr, *dinvu = nullptr, *diagu = nullptr;
+  uint8_t* flags = nullptr;
+  uint8_t* umask = nullptr;
+  // phase-field work
+  double *Rd = nullptr, *rd = nullptr, *xd = nullptr, *qd = nullptr, *p0d = nullptr,
+         *p1d = nullptr, *dinvd = nullptr, *diagd = nullptr, *b = nullptr;
+  uint8_t* pmask = nullptr;
+  // scratch
+  double* partials = nullptr;
+  double* scratch = nullptr;   // [n_elems*16] strain / gate / extra outputs
+  long long* d_idx = nullptr;  // index list scratch (BC dofs, reaction nodes)
+  size_t d_idx_cap = 0;
+  double* flushbuf = nullptr;
+  size_t flush_n = 0;
+  CgResult* h_cgres = nullptr;  // mapped pinned
+  CgResult* d_cgres = nullptr;
+  double* h_scal = nullptr;     // mapped pinned scalars
+  double* d_scal = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
+  int cg_grid = 1, sm_count = 0;
+  long long l2_bytes = 0;
+  // cached masks
+  std::vector<int64_t> cons_key, pins_key;
+  bool umask_all_free = true, pmask_all_free = true;
+  int64_t n_pinned = 0;
+  // accounting of the current call
+  pf_stats acc{};
+  std::string err;
+};
+
+static const char* kVersion = "paper_2209_07969_b200 0.1 (sm_100a FP64 matrix-free PCG)";
+
+// ------------------------------------------------------------------------------------------
+#define PF_CUDA(expr)                                                                \
+  do {                                                                               \
+    cudaError_t e__ = (expr);                                                        \
+    if (e__ != cudaSuccess) {                                                        \
+      h->err = std::string("CUDA error: ") + cudaGetErrorString(e__) + " at " #expr; \
+      return PF_ERR_CUDA;                                                            \
+    }                                                                                \
+  } while (0)
+
+#define PF_TRY(expr)                   \
+  do {                                 \
+    pf_status s__ = (expr);            \
+    if (s__ != PF_OK) return s__;      \
+  } while (0)
+
+static pf_status fail(pf_handle* h, pf_status s, const std::string& msg) {
+  h->err = msg;
+  return s;
+}
+
+static pf_status launched(pf_handle* h) {
+  h->acc.launches += 1;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+  return PF_OK;
+}
+
+template <class T>
+static pf_status dalloc(pf_handle* h, T** p, size_t n) {
+  PF_CUDA(cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T)));
+  PF_CUDA(cudaMemsetAsync(*p, 0, std::max<size_t>(n, 1) * sizeof(T), h->stream));
+  return PF_OK;
+}
+
+static double now_s() {
+  using namespace std::chrono;
+  return duration<double>(steady_clock::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------------------------------------
+// constants (restating the reference's shape-function arithmetic, assembly.py:28-43,108-129)
+static void build_consts(pf_handle* h, double hx, double hy) {
+  pfb::Consts& C = h->C;
+  const double c = 1.0 / std::sqrt(3.0);
+  const double gp[4][2] = {{-c, -c}, {c, -c}, {c, c}, {-c, c}};
+  double dNx[4][4], dNy[4][4];
+  for (int g = 0; g < 4; ++g) {
+    const double xi = gp[g][0], et = gp[g][1];
+    C.N[g][0] = 0.25 * ((1 - xi) * (1 - et));
+    C.N[g][1] = 0.25 * ((1 + xi) * (1 - et));
+    C.N[g][2] = 0.25 * ((1 + xi) * (1 + et));
+    C.N[g][3] = 0.25 * ((1 - xi) * (1 + et));
+    const double sx[4] = {-(1 - et), (1 - et), (1 + et), -(1 + et)};
+    const double sy[4] = {-(1 - xi), -(1 + xi), (1 + xi), (1 - xi)};
+    for (int a = 0; a < 4; ++a) {
+      dNx[g][a] = (2.0 / hx) * (0.25 * sx[a]);
+      dNy[g][a] = (2.0 / hy) * (0.25 * sy[a]);
+    }
+  }
+  const double w = (hx * 0.5) * (hy * 0.5);
+  C.w = w;
+  C.Px = (1.0 + c) / (2.0 * hx);
+  C.Mx = (1.0 - c) / (2.0 * hx);
+  C.Py = (1.0 + c) / (2.0 * hy);
+  C.My = (1.0 - c) / (2.0 * hy);
+  C.Pxw = C.Px * w;
+  C.Mxw = C.Mx * w;
+  C.Pyw = C.Py * w;
+  C.Myw = C.My * w;
+  C.P2xw = C.Px * C.Px * w;
+  C.M2xw = C.Mx * C.Mx * w;
+  C.P2yw = C.Py * C.Py * w;
+  C.M2yw = C.My * C.My * w;
+  const pf_material& m = h->mat;
+  const double grad_w = 2.0 * m.g_c * m.length_l / m.c_w;
+  for (int g = 0; g < 4; ++g)
+    for (int a = 0; a < 4; ++a) C.Nw[g][a] = C.N[g][a] * w;
+  for (int a = 0; a < 4; ++a)
+    for (int bb = 0; bb < 4; ++bb) {
+      double s = 0.0;
+      for (int g = 0; g < 4; ++g) s += (dNx[g][a] * dNx[g][bb] + dNy[g][a] * dNy[g][bb]) * w;
+      C.lap[a][bb] = grad_w * s;
+    }
+  C.mu = m.mu;
+  C.k = m.bulk_k;
+  C.two_mu = 2.0 * m.mu;
+  C.mu43 = 2.0 * m.mu * (1.0 - 1.0 / 3.0);
+  C.eta = m.eta;
+  C.gamma = m.gamma;
+  C.src_base = m.g_c / (m.c_w * m.length_l);
+  C.grad_w = grad_w;
+  C.psi_crit = m.g_c / (m.c_w * m.length_l);
+  C.d_cap = h->cfg.d_cap;
+  C.at2 = m.at2;
+}
+
+// ------------------------------------------------------------------------------------------
+extern "C" const char* pf_version(void) { return kVersion; }
+
+extern "C" const char* pf_last_error(const pf_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+extern "C" void pf_destroy(pf_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  void* ptrs[] = {h->d_nlo, h->d_nhi, h->d_nst, h->d_elo, h->d_ehi, h->d_est, h->d_tiles,
+                  h->u, h->d, h->dprev, h->trp, h->dev2, h->psi, h->psimax,
+                  h->Ru, h->ru, h->xu, h->qu, h->p0u, h->p1u, h->dinvu, h->diagu, h->flags,
+                  h->umask, h->Rd, h->rd, h->xd, h->qd, h->p0d, h->p1d, h->dinvd, h->diagd,
+                  h->b, h->pmask, h->partials, h->scratch, h->d_idx, h->flushbuf};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h->h_cgres) cudaFreeHost(h->h_cgres);
+  if (h->h_scal) cudaFreeHost(h->h_scal);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->evs0) cudaEventDestroy(h->evs0);
+  if (h->evs1) cudaEventDestroy(h->evs1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+static pf_status validate_mesh(pf_handle* h, const pf_mesh* m) {
+  if (m->nx < 1 || m->ny < 1 || m->ny > 65535 || !(m->hx > 0.0) || !(m->hy > 0.0))
+    return fail(h, PF_ERR_INVALID, "mesh: need 1 <= nx, 1 <= ny <= 65535 and hx, hy > 0");
+  if (m->n_nodes <= 0 || 2 * m->n_nodes >= (int64_t)INT32_MAX || m->n_elems <= 0 ||
+      4 * m->n_elems >= (int64_t)INT32_MAX)
+    return fail(h, PF_ERR_INVALID, "mesh: sizes out of range for 32-bit device indexing");
+  int64_t nn = 0, ne = 0;
+  for (int j = 0; j <= m->ny; ++j) {
+    if (m->node_lo[j] < 0 || m->node_hi[j] > m->nx + 1 || m->node_hi[j] < m->node_lo[j])
+      return fail(h, PF_ERR_INVALID, "mesh: bad node row range");
+    if (m->node_hi[j] > m->node_lo[j] && m->node_start[j] != nn)
+      return fail(h, PF_ERR_INVALID, "mesh: node rows are not row-major compact");
+    nn += m->node_hi[j] - m->node_lo[j];
+  }
+  if (m->notch_row >= 0) {
+    if (m->notch_row > m->ny || m->notch_lo < 0 || m->notch_hi <= m->notch_lo ||
+        m->dup_start != nn)
+      return fail(h, PF_ERR_INVALID, "mesh: bad notch description");
+    nn += m->notch_hi - m->notch_lo;
+  }
+  if (nn != m->n_nodes) return fail(h, PF_ERR_INVALID, "mesh: node count mismatch");
+  for (int j = 0; j < m->ny; ++j) {
+    const int lo = m->elem_lo[j], hi = m->elem_hi[j];
+    if (hi < lo) return fail(h, PF_ERR_INVALID, "mesh: bad cell row range");
+    if (hi > lo) {
+      if (m->elem_start[j] != ne) return fail(h, PF_ERR_INVALID, "mesh: cells not row-major compact");
+      // every corner must exist
+      if (lo < m->node_lo[j] || hi + 1 > m->node_hi[j] || lo < m->node_lo[j + 1] ||
+          hi + 1 > m->node_hi[j + 1])
+        return fail(h, PF_ERR_INVALID, "mesh: cell corner outside node rows");
+    }
+    ne += hi - lo;
+  }
+  if (ne != m->n_elems) return fail(h, PF_ERR_INVALID, "mesh: element count mismatch");
+  return PF_OK;
+}
+
+extern "C" pf_status pf_create(const pf_mesh* mesh, const pf_material* mat, const pf_config* cfg,
+                               int device, pf_handle** out) {
+  if (!out || !mesh || !mat || !cfg) return PF_ERR_INVALID;
+  *out = nullptr;
+  pf_handle* h = new pf_handle();
+  h->device = device;
+  h->cfg = *cfg;
+  h->mat = *mat;
+  pf_status st = validate_mesh(h, mesh);
+  if (st != PF_OK) {
+    fprintf(stderr, "pf_create: %s\n", h->err.c_str());
+    delete h;
+    return st;
+  }
+  auto bail = [&](pf_status s) {
+    fprintf(stderr, "pf_create: %s\n", h->err.c_str());
+    pf_destroy(h);
+    return s;
+  };
+#define CREATE_CUDA(expr)                                                          \
+  do {                                                                             \
+    cudaError_t e__ = (expr);                                                      \
+    if (e__ != cudaSuccess) {                                                      \
+      h->err = std::string("CUDA error: ") + cudaGetErrorString(e__) + " at " #expr; \
+      return bail(PF_ERR_CUDA);                                                    \
+    }                                                                              \
+  } while (0)
+  CREATE_CUDA(cudaSetDevice(device));
+  CREATE_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  CREATE_CUDA(cudaEventCreate(&h->ev0));
+  CREATE_CUDA(cudaEventCreate(&h->ev1));
+  CREATE_CUDA(cudaEventCreate(&h->evs0));
+  CREATE_CUDA(cudaEventCreate(&h->evs1));
+  h->nx = mesh->nx;
+  h->ny = mesh->ny;
+  h->n_nodes = (int)mesh->n_nodes;
+  h->n_elems = (int)mesh->n_elems;
+  const int nx = h->nx, ny = h->ny;
+  h->h_nlo.assign(mesh->node_lo, mesh->node_lo + ny + 1);
+  h->h_nhi.assign(mesh->node_hi, mesh->node_hi + ny + 1);
+  h->h_nst.resize(ny + 1);
+  for (int j = 0; j <= ny; ++j) h->h_nst[j] = (int)mesh->node_start[j];
+  h->h_elo.assign(mesh->elem_lo, mesh->elem_lo + ny);
+  h->h_ehi.assign(mesh->elem_hi, mesh->elem_hi + ny);
+  h->h_est.resize(ny);
+  for (int j = 0; j < ny; ++j) h->h_est[j] = (int)mesh->elem_start[j];
+  // active tiles: tiles owning at least one node
+  std::vector<int2> tiles;
+  const int tiles_x = (nx + 1 + pfb::TX - 1) / pfb::TX, tiles_y = (ny + 1 + pfb::TY - 1) / pfb::TY;
+  for (int ty = 0; ty < tiles_y; ++ty)
+    for (int tx = 0; tx < tiles_x; ++tx) {
+      bool any = false;
+      for (int j = ty * pfb::TY; j < std::min((ty + 1) * pfb::TY, ny + 1) && !any; ++j) {
+        const int lo = std::max(h->h_nlo[j], tx * pfb::TX), hi = std::min(h->h_nhi[j], (tx + 1) * pfb::TX);
+        any = hi > lo;
+      }
+      if (any) tiles.push_back(make_int2(tx, ty));
+    }
+  h->n_tiles = (int)tiles.size();
+  auto up_int = [&](int** dptr, const std::vector<int>& v) -> cudaError_t {
+    cudaError_t e = cudaMalloc((void**)dptr, std::max<size_t>(v.size(), 1) * sizeof(int));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpy(*dptr, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice);
+  };
+  CREATE_CUDA(up_int(&h->d_nlo, h->h_nlo));
+  CREATE_CUDA(up_int(&h->d_nhi, h->h_nhi));
+  CREATE_CUDA(up_int(&h->d_nst, h->h_nst));
+  CREATE_CUDA(up_int(&h->d_elo, h->h_elo));
+  CREATE_CUDA(up_int(&h->d_ehi, h->h_ehi));
+  CREATE_CUDA(up_int(&h->d_est, h->h_est));
+  CREATE_CUDA(cudaMalloc((void**)&h->d_tiles, tiles.size() * sizeof(int2)));
+  CREATE_CUDA(cudaMemcpy(h->d_tiles, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  pfb::DMesh& dm = h->dm;
+  dm.nx = nx; dm.ny = ny;
+  dm.nlo = h->d_nlo; dm.nhi = h->d_nhi; dm.nst = h->d_nst;
+  dm.elo = h->d_elo; dm.ehi = h->d_ehi; dm.est = h->d_est;
+  dm.notch_row = mesh->notch_row;
+  dm.notch_lo = mesh->notch_row >= 0 ? mesh->notch_lo : 0;
+  dm.notch_hi = mesh->notch_row >= 0 ? mesh->notch_hi : 0;
+  dm.dup_start = mesh->notch_row >= 0 ? (int)mesh->dup_start : 0;
+  dm.n_nodes = h->n_nodes; dm.n_elems = h->n_elems;
+  dm.n_tiles = h->n_tiles; dm.tiles = h->d_tiles;
+  build_consts(h, mesh->hx, mesh->hy);
+  const size_t nn = h->n_nodes, ne = h->n_elems;
+  pf_status s2 = PF_OK;
+#define CREATE_ALLOC(ptr, n) \
+  if ((s2 = dalloc(h, &(ptr), (n))) != PF_OK) return bail(s2)
+  CREATE_ALLOC(h->u, 2 * nn);
+  CREATE_ALLOC(h->d, nn);
+  CREATE_ALLOC(h->dprev, nn);
+  CREATE_ALLOC(h->trp, 4 * ne);
+  CREATE_ALLOC(h->dev2, 4 * ne);
+  CREATE_ALLOC(h->psi, 4 * ne);
+  CREATE_ALLOC(h->psimax, 4 * ne);
+  CREATE_ALLOC(h->Ru, 2 * nn);
+  CREATE_ALLOC(h->ru, 2 * nn);
+  CREATE_ALLOC(h->xu, 2 * nn);
+  CREATE_ALLOC(h->qu, 2 * nn);
+  CREATE_ALLOC(h->p0u, 2 * nn);
+  CREATE_ALLOC(h->p1u, 2 * nn);
+  CREATE_ALLOC(h->dinvu, 2 * nn);
+  CREATE_ALLOC(h->diagu, 2 * nn);
+  CREATE_ALLOC(h->flags, ne);
+  CREATE_ALLOC(h->umask, 2 * nn);
+  CREATE_ALLOC(h->Rd, nn);
+  CREATE_ALLOC(h->rd, nn);
+  CREATE_ALLOC(h->xd, nn);
+  CREATE_ALLOC(h->qd, nn);
+  CREATE_ALLOC(h->p0d, nn);
+  CREATE_ALLOC(h->p1d, nn);
+  CREATE_ALLOC(h->dinvd, nn);
+  CREATE_ALLOC(h->diagd, nn);
+  CREATE_ALLOC(h->b, 4 * ne);
+  CREATE_ALLOC(h->pmask, nn);
+  CREATE_ALLOC(h->scratch, 16 * ne);
+  CREATE_CUDA(cudaMemsetAsync(h->umask, 1, 2 * nn, h->stream));
+  CREATE_CUDA(cudaMemsetAsync(h->pmask, 1, nn, h->stream));
+  int dev_sms = 0, occ = 0, l2 = 0;
+  CREATE_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
+  CREATE_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+  CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pfb::k_cg, pfb::NT, 0));
+  h->sm_count = dev_sms;
+  h->l2_bytes = l2;
+  if (occ < 1) {
+    h->err = "k_cg cannot be resident (occupancy 0)";
+    return bail(PF_ERR_CUDA);
+  }
+  h->cg_grid = std::max(1, std::min(occ * dev_sms, h->n_tiles));
+  const size_t npart = std::max<size_t>((size_t)h->n_tiles, (size_t)h->cg_grid) * 4;
+  CREATE_ALLOC(h->partials, npart);
+  CREATE_CUDA(cudaHostAlloc((void**)&h->h_cgres, sizeof(CgResult), cudaHostAllocMapped));
+  CREATE_CUDA(cudaHostGetDevicePointer((void**)&h->d_cgres, h->h_cgres, 0));
+  CREATE_CUDA(cudaHostAlloc((void**)&h->h_scal, 16 * sizeof(double), cudaHostAllocMapped));
+  CREATE_CUDA(cudaHostGetDevicePointer((void**)&h->d_scal, h->h_scal, 0));
+  CREATE_CUDA(cudaStreamSynchronize(h->stream));
+  *out = h;
+  return PF_OK;
+#undef CREATE_ALLOC
+#undef CREATE_CUDA
+}
+
+// ------------------------------------------------------------------------------------------
+// state transfer
+static pf_status h2d(pf_handle* h, double* dst, const double* src, size_t n) {
+  if (!src) return PF_OK;
+  PF_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  return PF_OK;
+}
+static pf_status d2h(pf_handle* h, double* dst, const double* src, size_t n) {
+  if (!dst) return PF_OK;
+  PF_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  return PF_OK;
+}
+
+extern "C" pf_status pf_set_state(pf_handle* h, const double* u, const double* d,
+                                  const double* d_prev, const double* trp, const double* dev2,
+                                  const double* psi, const double* psimax) {
+  PF_CUDA(cudaSetDevice(h->device));
+  const size_t nn = h->n_nodes, ng = 4 * (size_t)h->n_elems;
+  PF_TRY(h2d(h, h->u, u, 2 * nn));
+  PF_TRY(h2d(h, h->d, d, nn));
+  PF_TRY(h2d(h, h->dprev, d_prev, nn));
+  PF_TRY(h2d(h, h->trp, trp, ng));
+  PF_TRY(h2d(h, h->dev2, dev2, ng));
+  PF_TRY(h2d(h, h->psi, psi, ng));
+  PF_TRY(h2d(h, h->psimax, psimax, ng));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+extern "C" pf_status pf_get_state(pf_handle* h, double* u, double* d, double* d_prev,
+                                  double* trp, double* dev2, double* psi, double* psimax) {
+  PF_CUDA(cudaSetDevice(h->device));
+  const size_t nn = h->n_nodes, ng = 4 * (size_t)h->n_elems;
+  PF_TRY(d2h(h, u, h->u, 2 * nn));
+  PF_TRY(d2h(h, d, h->d, nn));
+  PF_TRY(d2h(h, d_prev, h->dprev, nn));
+  PF_TRY(d2h(h, trp, h->trp, ng));
+  PF_TRY(d2h(h, dev2, h->dev2, ng));
+  PF_TRY(d2h(h, psi, h->psi, ng));
+  PF_TRY(d2h(h, psimax, h->psimax, ng));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+static dim3 cell_grid(const pf_handle* h) { return dim3((h->nx + 127) / 128, h->ny); }
+
+static pfb::GpArgs gp_args(pf_handle* h) {
+  pfb::GpArgs g{};
+  g.m = h->dm;
+  g.C = h->C;
+  g.u = reinterpret_cast<const double2*>(h->u);
+  g.d = h->d;
+  g.trp = h->trp;
+  g.dev2 = h->dev2;
+  g.psi = h->psi;
+  g.psimax = h->psimax;
+  return g;
+}
+
+extern "C" pf_status pf_get_gp_strain(pf_handle* h, double* strain, double* tr_eps) {
+  PF_CUDA(cudaSetDevice(h->device));
+  const size_t ne = h->n_elems;
+  double* tr_dev = h->scratch;  // tr first (4 ne), then strain needs 16 ne: do two passes
+  pfb::GpArgs g = gp_args(h);
+  g.trp = nullptr; g.dev2 = nullptr; g.psi = nullptr;
+  if (tr_eps) {
+    g.tr = tr_dev;
+    pfb::k_refresh_gp<<<cell_grid(h), 128, 0, h->stream>>>(g);
+    PF_TRY(launched(h));
+    PF_TRY(d2h(h, tr_eps, tr_dev, 4 * ne));
+    PF_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  if (strain) {
+    g.tr = nullptr;
+    g.strain = h->scratch;
+    pfb::k_refresh_gp<<<cell_grid(h), 128, 0, h->stream>>>(g);
+    PF_TRY(launched(h));
+    PF_TRY(d2h(h, strain, h->scratch, 16 * ne));
+    PF_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  return PF_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// masks
+static pf_status set_umask(pf_handle* h, const std::vector<int64_t>& cons) {
+  if (cons == h->cons_key) return PF_OK;
+  const size_t n = 2 * (size_t)h->n_nodes;
+  std::vector<uint8_t> m(n, 1);
+  for (int64_t k : cons) {
+    if (k < 0 || (size_t)k >= n) return fail(h, PF_ERR_INDEX, "constrained node outside the system");
+    m[k] = 0;
+  }
+  PF_CUDA(cudaMemcpyAsync(h->umask, m.data(), n, cudaMemcpyHostToDevice, h->stream));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  h->cons_key = cons;
+  h->umask_all_free = cons.empty();
+  return PF_OK;
+}
+
+static pf_status set_pmask(pf_handle* h, const int64_t* pins, int64_t n_pins) {
+  std::vector<int64_t> key(pins, pins + (pins ? n_pins : 0));
+  if (key == h->pins_key) return PF_OK;
+  const size_t n = h->n_nodes;
+  std::vector<uint8_t> m(n, 1);
+  for (int64_t k : key) {
+    if (k < 0 || (size_t)k >= n) return fail(h, PF_ERR_INDEX, "constrained node outside the system");
+    m[k] = 0;
+  }
+  PF_CUDA(cudaMemcpyAsync(h->pmask, m.data(), n, cudaMemcpyHostToDevice, h->stream));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  h->n_pinned = (int64_t)std::count(m.begin(), m.end(), (uint8_t)0);
+  h->pins_key = key;
+  h->pmask_all_free = key.empty();
+  return PF_OK;
+}
+
+static pf_status ensure_idx(pf_handle* h, size_t n) {
+  if (n <= h->d_idx_cap) return PF_OK;
+  if (h->d_idx) cudaFree(h->d_idx);
+  h->d_idx_cap = std::max<size_t>(n, 1024);
+  PF_CUDA(cudaMalloc((void**)&h->d_idx, h->d_idx_cap * sizeof(long long)));
+  return PF_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// kernel launch helpers
+static pf_status launch_mom_prepare(pf_handle* h, int full) {
+  pfb::MomPrepArgs a{};
+  a.m = h->dm;
+  a.C = h->C;
+  a.u = reinterpret_cast<const double2*>(h->u);
+  a.d = h->d;
+  a.umask = reinterpret_cast<const uchar2*>(h->umask);
+  a.R = reinterpret_cast<double2*>(h->Ru);
+  a.r = reinterpret_cast<double2*>(h->ru);
+  a.x = reinterpret_cast<double2*>(h->xu);
+  a.dinv = reinterpret_cast<double2*>(h->dinvu);
+  a.flags = h->flags;
+  a.diag = reinterpret_cast<double2*>(h->diagu);
+  a.partials = h->partials;
+  a.full = full;
+  pfb::k_mom_prepare<<<h->n_tiles, pfb::NT, 0, h->stream>>>(a);
+  return launched(h);
+}
+
+static pf_status launch_evo_prepare(pf_handle* h, int full, int extra_scheme) {
+  pfb::EvoPrepArgs a{};
+  a.m = h->dm;
+  a.C = h->C;
+  a.d = h->d;
+  a.dprev = h->dprev;
+  a.psi = h->psi;
+  a.trp = h->trp;
+  a.dev2 = h->dev2;
+  a.psimax = h->psimax;
+  a.pmask = h->pmask;
+  a.R = h->Rd;
+  a.r = h->rd;
+  a.x = h->xd;
+  a.dinv = h->dinvd;
+  a.b = h->b;
+  a.diag = h->diagd;
+  a.partials = h->partials;
+  a.full = full;
+  a.extra_scheme = extra_scheme;
+  pfb::k_evo_prepare<<<h->n_tiles, pfb::NT, 0, h->stream>>>(a);
+  return launched(h);
+}
+
+// sums nv partial streams of n_tiles CTAs into h_scal[0..nv) and waits for them
+static pf_status finalize(pf_handle* h, int nv) {
+  pfb::k_finalize<<<1, 256, 0, h->stream>>>(h->partials, h->n_tiles, nv, h->d_scal);
+  PF_TRY(launched(h));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+// one persistent PCG solve; returns the CG status
+static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
+                        long long* iters) {
+  pfb::CgArgs a{};
+  a.m = h->dm;
+  a.C = h->C;
+  a.vec2 = mom ? 1 : 0;
+  a.ndof = mom ? 2LL * h->n_nodes : (long long)h->n_nodes;
+  a.d = h->d;
+  a.flags = h->flags;
+  a.b = h->b;
+  a.x = mom ? h->xu : h->xd;
+  a.r = mom ? h->ru : h->rd;
+  a.q = mom ? h->qu : h->qd;
+  a.p0 = mom ? h->p0u : h->p0d;
+  a.p1 = mom ? h->p1u : h->p1d;
+  a.dinv = mom ? h->dinvu : h->dinvd;
+  a.target = target;
+  a.partials = h->partials;
+  a.result = h->d_cgres;
+  a.rtol = h->cfg.cg_rtol;
+  a.maxiter = (long long)h->cfg.cg_maxiter_factor * a.ndof;  // 20 * matrix.shape[0]
+  a.probe = probe ? 1 : 0;
+  void* args[] = {&a};
+  PF_CUDA(cudaEventRecord(h->ev0, h->stream));
+  PF_CUDA(cudaLaunchCooperativeKernel((const void*)pfb::k_cg, dim3(h->cg_grid), dim3(pfb::NT),
+                                      args, 0, h->stream));
+  PF_TRY(launched(h));
+  PF_CUDA(cudaEventRecord(h->ev1, h->stream));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  *status = h->h_cgres->status;
+  *iters = h->h_cgres->iters;
+  const double nfree_u = 2.0 * h->n_nodes - (double)h->cons_key.size();
+  const double nfree_d = (double)h->n_nodes - (double)h->n_pinned;
+  if (mom) {
+    h->acc.cg_iters_u += *iters;
+    h->acc.cg_dofiters_u += (double)*iters * nfree_u;
+    h->acc.kernel_ms_u += ms;
+    h->acc.cg_launches_u += 1;
+  } else {
+    h->acc.cg_iters_d += *iters;
+    h->acc.cg_dofiters_d += (double)*iters * nfree_d;
+    h->acc.kernel_ms_d += ms;
+    h->acc.cg_launches_d += 1;
+  }
+  if (*status == pfb::CG_MAXITER)
+    return fail(h, PF_ERR_SINGULAR, "cg failed to converge (info=" + std::to_string(*iters) + ")");
+  if (*status == pfb::CG_NAN) return fail(h, PF_ERR_SINGULAR, "cg produced a non-finite residual");
+  return PF_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// solve_momentum (schemes.py:192-239)
+struct BcView {
+  const int64_t* dofs;
+  const int64_t* offsets;
+  const double* incs;
+  int n;
+};
+
+static pf_status momentum(pf_handle* h, const BcView& bc, bool apply_inc, double* r0,
+                          int* n_nr_out, double* last_ratio) {
+  // kinematic increments (schemes.py:207-209): u[dofs] += inc for unique dofs of each pair
+  std::vector<int64_t> cons;
+  for (int k = 0; k < bc.n; ++k) {
+    std::vector<int64_t> dofs(bc.dofs + bc.offsets[k], bc.dofs + bc.offsets[k + 1]);
+    for (int64_t v : dofs)
+      if (v < 0 || v >= 2LL * h->n_nodes)
+        return fail(h, PF_ERR_INDEX, "index out of bounds in boundary-condition dofs");
+    std::sort(dofs.begin(), dofs.end());
+    dofs.erase(std::unique(dofs.begin(), dofs.end()), dofs.end());
+    cons.insert(cons.end(), dofs.begin(), dofs.end());
+    if (apply_inc && bc.incs[k] != 0.0 && !dofs.empty()) {
+      PF_TRY(ensure_idx(h, dofs.size()));
+      PF_CUDA(cudaMemcpyAsync(h->d_idx, dofs.data(), dofs.size() * sizeof(long long),
+                              cudaMemcpyHostToDevice, h->stream));
+      const long long n = (long long)dofs.size();
+      pfb::k_add_inc<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(h->u, h->d_idx, n,
+                                                                          bc.incs[k]);
+      PF_TRY(launched(h));
+      PF_CUDA(cudaStreamSynchronize(h->stream));  // d_idx is reused by the next pair
+    }
+  }
+  std::sort(cons.begin(), cons.end());
+  cons.erase(std::unique(cons.begin(), cons.end()), cons.end());
+  PF_TRY(set_umask(h, cons));
+  const pf_config& cfg = h->cfg;
+  int n_nr = 0;
+  double rnorm = 0.0;
+  for (int it = 0; it <= cfg.max_nr; ++it) {
+    PF_TRY(launch_mom_prepare(h, 1));
+    PF_TRY(finalize(h, 1));
+    rnorm = std::sqrt(h->h_scal[0]);
+    if (std::isnan(*r0)) *r0 = rnorm;
+    if (rnorm <= std::max(cfg.tol_nr * *r0, cfg.res_floor)) break;
+    if (it == cfg.max_nr) {
+      char buf[256];
+      snprintf(buf, sizeof buf,
+               "momentum Newton loop did not converge in %d iterations (relative residual %.3e)",
+               cfg.max_nr, rnorm / std::max(*r0, cfg.res_floor));
+      return fail(h, PF_ERR_CONV_MOMENTUM, buf);
+    }
+    int status;
+    long long iters;
+    PF_TRY(run_cg(h, true, h->u, false, &status, &iters));
+    n_nr += 1;
+  }
+  // refresh_gp_from_displacement (assembly.py:260-269)
+  pfb::GpArgs g = gp_args(h);
+  pfb::k_refresh_gp<<<cell_grid(h), 128, 0, h->stream>>>(g);
+  PF_TRY(launched(h));
+  *n_nr_out = n_nr;
+  *last_ratio = rnorm / std::max(*r0, cfg.res_floor);
+  return PF_OK;
+}
+
+// solve_evolution (schemes.py:242-313)
+static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, int* fallbacks) {
+  const pf_config& cfg = h->cfg;
+  int n_nr = 0;
+  for (int it = 0; it <= cfg.max_nr; ++it) {
+    const int extra = (it == 0 && scheme != PF_ST) ? scheme : 0;
+    PF_TRY(launch_evo_prepare(h, 1, extra));
+    PF_TRY(finalize(h, 3));
+    const double rnorm = std::sqrt(h->h_scal[0]);
+    const bool gated = extra != 0 && h->h_scal[1] > 0.0;
+    const bool nonpos_diag = h->h_scal[2] > 0.0;
+    if (std::isnan(*r0)) *r0 = rnorm;
+    if (rnorm <= std::max(cfg.tol_nr * *r0, cfg.res_floor)) break;
+    if (it == cfg.max_nr) {
+      char buf[256];
+      snprintf(buf, sizeof buf,
+               "evolution Newton loop did not converge in %d iterations (relative residual %.3e)",
+               cfg.max_nr, rnorm / std::max(*r0, cfg.res_floor));
+      return fail(h, PF_ERR_CONV_EVOLUTION, buf);
+    }
+    int status = pfb::CG_CONVERGED;
+    long long iters = 0;
+    if (gated) {
+      // SPD predicate for K_dd + K~ (replaces check_spd, linsolve.py:58-77): a non-positive
+      // diagonal, or non-positive curvature p.Ap inside PCG, means "not positive definite"
+      bool fallback = nonpos_diag;
+      if (!fallback) {
+        PF_TRY(run_cg(h, false, nullptr, true, &status, &iters));
+        fallback = status == pfb::CG_INDEFINITE;
+      }
+      if (fallback) {  // plain tangent for this staggered iteration (schemes.py:293-301)
+        PF_TRY(launch_evo_prepare(h, 1, 0));
+        PF_TRY(run_cg(h, false, nullptr, false, &status, &iters));
+        *fallbacks += 1;
+      }
+      // one-time half-step energy update from this increment (schemes.py:303-310)
+      pfb::GpArgs g = gp_args(h);
+      g.dd = h->xd;
+      g.scheme = scheme;
+      pfb::k_update_energy<<<cell_grid(h), 128, 0, h->stream>>>(g);
+      PF_TRY(launched(h));
+      const long long n = h->n_nodes;
+      pfb::k_axpy<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(h->d, h->xd, n);
+      PF_TRY(launched(h));
+    } else {
+      PF_TRY(run_cg(h, false, h->d, false, &status, &iters));
+    }
+    n_nr += 1;
+  }
+  *n_nr_out = n_nr;
+  return PF_OK;
+}
+
+static pf_status evo_norm(pf_handle* h, double* out) {
+  PF_TRY(launch_evo_prepare(h, 0, 0));
+  PF_TRY(finalize(h, 3));
+  *out = std::sqrt(h->h_scal[0]);
+  return PF_OK;
+}
+
+static pf_status commit(pf_handle* h) {
+  const long long ngp = 4LL * h->n_elems, nn = h->n_nodes;
+  const long long n = std::max(ngp, nn);
+  pfb::k_commit<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(h->psimax, h->psi, ngp,
+                                                                    h->dprev, h->d, nn);
+  return launched(h);
+}
+
+// ------------------------------------------------------------------------------------------
+extern "C" pf_status pf_staggered_step(pf_handle* h, int scheme, const int64_t* bc_dofs,
+                                       const int64_t* bc_offsets, const double* bc_incs,
+                                       int32_t n_bc, const int64_t* pins, int64_t n_pins,
+                                       pf_stats* out, double* hist, int32_t hist_cap) {
+  if (!h) return PF_ERR_INVALID;
+  PF_CUDA(cudaSetDevice(h->device));
+  if (scheme < PF_ST || scheme > PF_S3) return fail(h, PF_ERR_INVALID, "unknown scheme");
+  h->acc = pf_stats{};
+  pf_stats& st = h->acc;
+  const pf_config& cfg = h->cfg;
+  BcView bc{bc_dofs, bc_offsets, bc_incs, n_bc};
+  PF_TRY(set_pmask(h, pins, n_pins));
+  std::vector<double> history;
+  double r0_u = NAN, r0_d = NAN, last_u_ratio = 0.0;
+  PF_CUDA(cudaEventRecord(h->evs0, h->stream));
+  double t0 = now_s();
+  int nnr = 0;
+  PF_TRY(momentum(h, bc, true, &r0_u, &nnr, &last_u_ratio));
+  st.n_nr_u += nnr;
+  st.wall_u += now_s() - t0;
+  double snorm;
+  PF_TRY(evo_norm(h, &snorm));
+  r0_d = snorm;
+  history.push_back(1.0);
+  bool converged = snorm <= cfg.res_floor;
+  while (!converged) {
+    if (st.n_stag >= cfg.max_stag) {
+      char buf[128];
+      snprintf(buf, sizeof buf, "staggered loop did not converge in %d iterations", cfg.max_stag);
+      h->err = buf;
+      st.n_hist = (int)std::min<size_t>(history.size(), (size_t)std::max(hist_cap, 0));
+      if (hist) std::copy(history.begin(), history.begin() + st.n_hist, hist);
+      if (out) *out = st;
+      return PF_ERR_CONV_STAGGERED;
+    }
+    st.n_stag += 1;
+    t0 = now_s();
+    int nd = 0;
+    PF_TRY(evolution(h, scheme, &r0_d, &nd, &st.spd_fallbacks));
+    st.n_nr_d += nd;
+    st.wall_d += now_s() - t0;
+    t0 = now_s();
+    PF_TRY(momentum(h, bc, false, &r0_u, &nnr, &last_u_ratio));
+    st.n_nr_u += nnr;
+    st.wall_u += now_s() - t0;
+    PF_TRY(evo_norm(h, &snorm));
+    const double ratio = snorm / std::max(r0_d, cfg.res_floor);
+    history.push_back(ratio);
+    converged = snorm <= std::max(cfg.tol_st * r0_d, cfg.res_floor);
+  }
+  st.final_rd_ratio = st.n_stag ? history.back() : 0.0;
+  st.final_ru_ratio = last_u_ratio;
+  PF_TRY(commit(h));
+  PF_CUDA(cudaEventRecord(h->evs1, h->stream));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  {
+    float ms = 0.f;
+    PF_CUDA(cudaEventElapsedTime(&ms, h->evs0, h->evs1));
+    st.step_ms = ms;
+  }
+  st.n_hist = (int)std::min<size_t>(history.size(), (size_t)std::max(hist_cap, 0));
+  if (hist) std::copy(history.begin(), history.begin() + st.n_hist, hist);
+  if (out) *out = st;
+  return PF_OK;
+}
+
+extern "C" pf_status pf_solve_momentum(pf_handle* h, const int64_t* bc_dofs,
+                                       const int64_t* bc_offsets, const double* bc_incs,
+                                       int32_t n_bc, double* r0_u, int32_t* n_nr,
+                                       double* last_ratio) {
+  PF_CUDA(cudaSetDevice(h->device));
+  h->acc = pf_stats{};
+  BcView bc{bc_dofs, bc_offsets, bc_incs, n_bc};
+  int nnr = 0;
+  double lr = 0.0;
+  PF_TRY(momentum(h, bc, true, r0_u, &nnr, &lr));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  if (n_nr) *n_nr = nnr;
+  if (last_ratio) *last_ratio = lr;
+  return PF_OK;
+}
+
+extern "C" pf_status pf_solve_evolution(pf_handle* h, int scheme, const int64_t* pins,
+                                        int64_t n_pins, double* r0_d, int32_t* n_nr,
+                                        int32_t* spd_fallbacks) {
+  PF_CUDA(cudaSetDevice(h->device));
+  h->acc = pf_stats{};
+  PF_TRY(set_pmask(h, pins, n_pins));
+  int nd = 0, fb = 0;
+  PF_TRY(evolution(h, scheme, r0_d, &nd, &fb));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  if (n_nr) *n_nr = nd;
+  if (spd_fallbacks) *spd_fallbacks += fb;
+  return PF_OK;
+}
+
+extern "C" pf_status pf_evolution_residual_norm(pf_handle* h, const int64_t* pins,
+                                                int64_t n_pins, double* out) {
+  PF_CUDA(cudaSetDevice(h->device));
+  PF_TRY(set_pmask(h, pins, n_pins));
+  return evo_norm(h, out);
+}
+
+extern "C" pf_status pf_commit_step(pf_handle* h) {
+  PF_CUDA(cudaSetDevice(h->device));
+  PF_TRY(commit(h));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// operators at the current state
+extern "C" pf_status pf_internal_force(pf_handle* h, double* f_out) {
+  PF_CUDA(cudaSetDevice(h->device));
+  PF_TRY(launch_mom_prepare(h, 0));
+  PF_TRY(d2h(h, f_out, h->Ru, 2 * (size_t)h->n_nodes));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+extern "C" pf_status pf_reaction_force(pf_handle* h, const int64_t* nodes, int64_t n,
+                                       int component, double* out) {
+  PF_CUDA(cudaSetDevice(h->device));
+  if (component < 0 || component > 1) return fail(h, PF_ERR_INVALID, "component must be 0 or 1");
+  for (int64_t i = 0; i < n; ++i)
+    if (nodes[i] < 0 || nodes[i] >= h->n_nodes)
+      return fail(h, PF_ERR_INDEX, "reaction node outside the mesh");
+  PF_TRY(launch_mom_prepare(h, 0));
+  PF_TRY(ensure_idx(h, (size_t)n));
+  if (n > 0)
+    PF_CUDA(cudaMemcpyAsync(h->d_idx, nodes, n * sizeof(long long), cudaMemcpyHostToDevice,
+                            h->stream));
+  pfb::k_reaction<<<1, 256, 0, h->stream>>>(h->Ru, h->d_idx, n, component, h->d_scal);
+  PF_TRY(launched(h));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  *out = h->h_scal[0];
+  return PF_OK;
+}
+
+extern "C" pf_status pf_momentum_tangent_apply(pf_handle* h, const double* x, double* y,
+                                               double* diag) {
+  PF_CUDA(cudaSetDevice(h->device));
+  PF_TRY(launch_mom_prepare(h, 1));  // branch flags and raw diagonal at the current u
+  PF_TRY(h2d(h, h->p0u, x, 2 * (size_t)h->n_nodes));
+  pfb::ApplyArgs a{};
+  a.m = h->dm;
+  a.C = h->C;
+  a.d = h->d;
+  a.flags = h->flags;
+  a.x = h->p0u;
+  a.y = h->qu;
+  a.vec2 = 1;
+  pfb::k_apply<<<h->n_tiles, pfb::NT, 0, h->stream>>>(a);
+  PF_TRY(launched(h));
+  PF_TRY(d2h(h, y, h->qu, 2 * (size_t)h->n_nodes));
+  PF_TRY(d2h(h, diag, h->diagu, 2 * (size_t)h->n_nodes));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+extern "C" pf_status pf_evolution_residual(pf_handle* h, double* r_out) {
+  PF_CUDA(cudaSetDevice(h->device));
+  PF_TRY(launch_evo_prepare(h, 0, 0));
+  PF_TRY(d2h(h, r_out, h->Rd, (size_t)h->n_nodes));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+extern "C" pf_status pf_evolution_tangent_apply(pf_handle* h, int scheme, const double* x,
+                                                double* y, double* diag) {
+  PF_CUDA(cudaSetDevice(h->device));
+  if (scheme < PF_ST || scheme > PF_S3) return fail(h, PF_ERR_INVALID, "unknown scheme");
+  PF_TRY(launch_evo_prepare(h, 1, scheme));
+  PF_TRY(h2d(h, h->p0d, x, (size_t)h->n_nodes));
+  pfb::ApplyArgs a{};
+  a.m = h->dm;
+  a.C = h->C;
+  a.b = h->b;
+  a.x = h->p0d;
+  a.y = h->qd;
+  a.vec2 = 0;
+  pfb::k_apply<<<h->n_tiles, pfb::NT, 0, h->stream>>>(a);
+  PF_TRY(launched(h));
+  PF_TRY(d2h(h, y, h->qd, (size_t)h->n_nodes));
+  PF_TRY(d2h(h, diag, h->diagd, (size_t)h->n_nodes));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+extern "C" pf_status pf_refresh_gp(pf_handle* h) {
+  PF_CUDA(cudaSetDevice(h->device));
+  pfb::GpArgs g = gp_args(h);
+  pfb::k_refresh_gp<<<cell_grid(h), 128, 0, h->stream>>>(g);
+  PF_TRY(launched(h));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+extern "C" pf_status pf_softening_gate(pf_handle* h, uint8_t* gate_out) {
+  PF_CUDA(cudaSetDevice(h->device));
+  pfb::GpArgs g = gp_args(h);
+  g.gate = reinterpret_cast<uint8_t*>(h->scratch);
+  pfb::k_gate_extra<<<cell_grid(h), 128, 0, h->stream>>>(g);
+  PF_TRY(launched(h));
+  PF_CUDA(cudaMemcpyAsync(gate_out, h->scratch, 4 * (size_t)h->n_elems, cudaMemcpyDeviceToHost,
+                          h->stream));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+extern "C" pf_status pf_extra_stiffness(pf_handle* h, int scheme, double* extra_out) {
+  PF_CUDA(cudaSetDevice(h->device));
+  if (scheme < PF_ST || scheme > PF_S3) return fail(h, PF_ERR_INVALID, "unknown scheme");
+  pfb::GpArgs g = gp_args(h);
+  g.extra = h->scratch;
+  g.scheme = scheme;
+  pfb::k_gate_extra<<<cell_grid(h), 128, 0, h->stream>>>(g);
+  PF_TRY(launched(h));
+  PF_TRY(d2h(h, extra_out, h->scratch, 4 * (size_t)h->n_elems));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+extern "C" pf_status pf_update_active_energy(pf_handle* h, int scheme, const double* dd) {
+  PF_CUDA(cudaSetDevice(h->device));
+  if (scheme < PF_ST || scheme > PF_S3) return fail(h, PF_ERR_INVALID, "unknown scheme");
+  if (scheme == PF_ST) return PF_OK;  // schemes.py:162-163
+  PF_TRY(h2d(h, h->xd, dd, (size_t)h->n_nodes));
+  pfb::GpArgs g = gp_args(h);
+  g.dd = h->xd;
+  g.scheme = scheme;
+  pfb::k_update_energy<<<cell_grid(h), 128, 0, h->stream>>>(g);
+  PF_TRY(launched(h));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+extern "C" pf_status pf_device_info(pf_handle* h, int32_t* cg_grid, int32_t* sm_count,
+                                    int64_t* l2_bytes) {
+  if (cg_grid) *cg_grid = h->cg_grid;
+  if (sm_count) *sm_count = h->sm_count;
+  if (l2_bytes) *l2_bytes = h->l2_bytes;
+  return PF_OK;
+}
+
+extern "C" pf_status pf_flush_l2(pf_handle* h) {
+  PF_CUDA(cudaSetDevice(h->device));
+  if (!h->flushbuf) {
+    h->flush_n = (size_t)std::max<long long>(2 * h->l2_bytes, 256LL << 20) / sizeof(double);
+    PF_CUDA(cudaMalloc((void**)&h->flushbuf, h->flush_n * sizeof(double)));
+  }
+  pfb::k_flush<<<h->sm_count * 4, 256, 0, h->stream>>>(h->flushbuf, (long long)h->flush_n, 1.0);
+  PF_TRY(launched(h));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}
+
+extern "C" pf_status pf_synchronize(pf_handle* h) {
+  PF_CUDA(cudaSetDevice(h->device));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
+}

@@ -1,0 +1,175 @@
+"""End-to-end and solver-level parity of the B200 path against the reference.
+
+Golden per-step tables come from the unmodified reference (tests/golden/run_*.npz).  The bar
+(BASELINE.json north_star): per-step staggered iterations equal within +-1,
+reaction force within 1e-6 of the peak force, phase field within 1e-6 in L-infinity.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_err
+from paper_2209_07969_b200 import configs as C
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("tension16", s) for s in ("ST", "S1", "S2", "S3")] + [
+    ("tension32", "ST"), ("tension32", "S1"), ("tension32", "S3"),
+    ("shear32", "ST"), ("shear32", "S2"), ("shear32", "S3"),
+    ("lpanel25", "ST"), ("lpanel25", "S1"),
+    ("multicrack32", "ST"), ("multicrack32", "S1"),
+]
+
+
+def run_case(case, scheme, steps=None):
+    pb = C.setup(C.get_case(case), C.b200_api())
+    recs = C.run(pb, scheme, n_steps=steps)
+    return pb, recs
+
+
+def check_against_golden(recs, z, state, fcol=7):
+    tab = z["table"]
+    assert len(recs) == len(tab)
+    fpeak = np.abs(tab[:, fcol]).max()
+    worst = dict(stag=0, force=0.0)
+    for r, row in zip(recs, tab):
+        d_stag = abs(r.n_stag - int(row[1]))
+        d_force = abs(r.reactions[0] - row[fcol]) / fpeak
+        worst["stag"] = max(worst["stag"], d_stag)
+        worst["force"] = max(worst["force"], d_force)
+        assert d_stag <= 1, f"step {r.step}: n_stag {r.n_stag} vs reference {int(row[1])}"
+        assert d_force <= 1e-6, f"step {r.step}: force {r.reactions[0]} vs {row[fcol]}"
+    dinf = float(np.abs(state.d - z["final_d"]).max())
+    assert dinf <= 1e-6, dinf
+    return worst, dinf
+
+
+@pytest.mark.parametrize("case,scheme", CASES)
+def test_end_to_end_matches_reference(case, scheme, cuda_ok):
+    z = golden(f"run_{case}_{scheme}.npz")
+    pb, recs = run_case(case, scheme)
+    check_against_golden(recs, z, pb.state)
+    # fast schemes must take fewer staggered iterations at the crack than ST (paper Fig. 4b)
+    if scheme != "ST":
+        assert sum(r.spd_fallbacks for r in recs) == pytest.approx(
+            z["table"][:, 4].sum(), rel=0.15, abs=3)
+
+
+@pytest.mark.parametrize("scheme", ["ST", "S1", "S2", "S3"])
+def test_cfg1_full_run(scheme, cuda_ok):
+    """BASELINE configs[0]: 64x64 tension, 65 steps, against the reference's own run."""
+    z = golden(f"run_cfg1_{scheme}.npz")
+    snaps = {}
+
+    def cb(rec, pb):
+        if f"d_step{rec.step}" in z.files:
+            snaps[rec.step] = pb.state.d.copy()
+
+    pb = C.setup(C.get_case("cfg1"), C.b200_api())
+    recs = C.run(pb, scheme, on_step=cb)
+    check_against_golden(recs, z, pb.state)
+    for step, d in snaps.items():
+        assert np.abs(d - z[f"d_step{step}"]).max() <= 1e-6, step
+
+
+def test_cfg2_first_steps(cuda_ok):
+    """BASELINE configs[1] at full size (512x512, 790k DOFs): first two load steps."""
+    z = golden("run_cfg2_ST_2steps.npz")
+    pb, recs = run_case("cfg2", "ST", steps=2)
+    check_against_golden(recs, z, pb.state)
+
+
+@pytest.mark.parametrize("case,scheme", [("tension16", "S1"), ("tension16", "S2"),
+                                         ("tension16", "S3"), ("shear32", "S3")])
+def test_spd_predicate_agrees_with_check_spd(case, scheme, cuda_ok):
+    """The curvature SPD predicate reproduces the reference's SuperLU check_spd decisions."""
+    import json
+
+    from paper_2209_07969_b200.session import DeviceSession
+
+    z = golden(f"spd_{case}_{scheme}.npz")
+    meta = json.loads(str(z["meta"]))
+    pb = C.setup(C.get_case(case), C.b200_api())
+    s = DeviceSession(pb.disc.layout, pb.params, pb.config, device=0)
+    agree = total = 0
+    for key, n, want in (("fallback", meta["n_fallback"], 1), ("spd", meta["n_spd"], 0)):
+        for i in range(n):
+            g = lambda k: z[f"{key}{i}_{k}"]  # noqa: E731
+            s.push(u=np.zeros(2 * pb.mesh.n_nodes), d=g("d"), d_prev=g("d_prev"),
+                   tr_eps_plus=g("trp"), dev_dot_dev=g("dev2"), psi_plus=g("psi"),
+                   psi_max=g("psimax"))
+            _, _, fb = s.solve_evolution(scheme, pb.pins)
+            agree += int(fb == want)
+            total += 1
+    assert agree == total, f"{agree}/{total} decisions agree"
+
+
+def test_solver_level_parity_with_oracle(cuda_ok):
+    """solve_momentum / solve_evolution NR counts and fields vs the CPU oracle."""
+    from oracle.phasefield_oracle import Oracle
+    from paper_2209_07969_b200.session import DeviceSession
+
+    case = C.get_case("tension16")
+    ref = C.setup(case, __import__("oracle.phasefield_oracle", fromlist=["x"]).oracle_api())
+    pb = C.setup(case, C.b200_api())
+    C.run(ref, "S1", n_steps=9)
+    st = ref.state
+    s = DeviceSession(pb.disc.layout, pb.params, pb.config, device=0)
+    s.push(st.u, st.d, st.d_prev, st.gp.tr_eps_plus, st.gp.dev_dot_dev, st.gp.psi_plus,
+           st.gp.psi_max)
+    o = Oracle(ref.disc, ref.params, ref.config)
+    ctx = {"r0_u": None, "r0_d": None, "u_ratio": 0.0}
+    n_u_ref = o.momentum(st, ref.bcs, ctx)
+    n_u, r0_u, _ = s.solve_momentum(pb.bcs)
+    assert n_u == n_u_ref and abs(r0_u - ctx["r0_u"]) <= 1e-10 * ctx["r0_u"]
+    got = s.pull()
+    assert rel_err(got["u"], st.u) < 1e-9
+    assert rel_err(got["psi_plus"], st.gp.psi_plus) < 1e-8
+
+    class _S:
+        spd_fallbacks = 0
+
+    n_d_ref = o.evolution(st, "S1", np.zeros(0, np.int64), ctx, _S)
+    n_d, _, fb = s.solve_evolution("S1", None, ctx["r0_d"])
+    assert n_d == n_d_ref and fb == _S.spd_fallbacks
+    got = s.pull()
+    assert np.abs(got["d"] - st.d).max() < 1e-9
+    assert rel_err(got["psi_plus"], st.gp.psi_plus) < 1e-8
+
+
+def test_determinism_and_dropin_equivalence(cuda_ok):
+    """Bitwise-identical reruns (SURVEY.md §7 hard part 6); drop-in == device session."""
+    from paper_2209_07969_b200.session import DeviceSession
+
+    case = C.get_case("tension16")
+    outs = []
+    for _ in range(2):
+        pb = C.setup(case, C.b200_api())
+        C.run(pb, "S3", n_steps=11)
+        outs.append((pb.state.u.copy(), pb.state.d.copy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    pb = C.setup(case, C.b200_api())
+    s = DeviceSession(pb.disc.layout, pb.params, pb.config, device=0)
+    s.push_state(pb.state)
+    for _ in range(11):
+        s.step("S3", pb.bcs, pb.pins)
+    got = s.pull()
+    assert np.array_equal(got["u"], outs[0][0]) and np.array_equal(got["d"], outs[0][1])
+
+
+def test_errors_map_to_reference_exceptions(cuda_ok):
+    from paper_2209_07969_b200 import schemes
+    from paper_2209_07969_b200.session import ConvergenceError
+
+    case = C.get_case("tension16")
+    pb = C.setup(case, C.b200_api())
+    bad = [(np.array([10 ** 9], dtype=np.int64), 0.0)]
+    with pytest.raises(IndexError):
+        schemes.staggered_step(pb.disc, pb.state, schemes.SchemeKind.ST, bad, pb.params,
+                               pb.config)
+    cfg = schemes.SolverConfig(tol_st=1e-5, max_stag=2)
+    pb = C.setup(case, C.b200_api())
+    C.run(pb, "ST", n_steps=10)
+    with pytest.raises(ConvergenceError) as ei:
+        schemes.staggered_step(pb.disc, pb.state, "ST", pb.bcs, pb.params, cfg)
+    assert len(ei.value.residual_history) >= 2
