@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpfb200.so")
+LIB_PATH = os.environ.get("PFB200_LIB") or os.path.join(HERE, "libpfb200.so")
 
 PF_OK, PF_ERR_INVALID, PF_ERR_INDEX = 0, 1, 2
 PF_ERR_CONV_MOMENTUM, PF_ERR_CONV_EVOLUTION, PF_ERR_CONV_STAGGERED = 3, 4, 5

@@ -58,7 +58,7 @@ struct pf_handle {
   double* h_scal = nullptr;     // mapped pinned scalars
   double* d_scal = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
-  int cg_grid = 1, sm_count = 0;
+  int cg_grid = 1, cg_grid_evo = 1, sm_count = 0;
   long long l2_bytes = 0;
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
@@ -347,18 +347,27 @@ extern "C" pf_status pf_create(const pf_mesh* mesh, const pf_material* mat, cons
   CREATE_ALLOC(h->scratch, 16 * ne);
   CREATE_CUDA(cudaMemsetAsync(h->umask, 1, 2 * nn, h->stream));
   CREATE_CUDA(cudaMemsetAsync(h->pmask, 1, nn, h->stream));
-  int dev_sms = 0, occ = 0, l2 = 0;
+  int dev_sms = 0, occ = 0, occ_evo = 0, l2 = 0;
   CREATE_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
   CREATE_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
-  CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pfb::k_cg, pfb::NT, 0));
+  CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pfb::k_cg<true>, pfb::NT, 0));
+  CREATE_CUDA(
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_evo, pfb::k_cg<false>, pfb::NT, 0));
   h->sm_count = dev_sms;
   h->l2_bytes = l2;
-  if (occ < 1) {
+  if (occ < 1 || occ_evo < 1) {
     h->err = "k_cg cannot be resident (occupancy 0)";
     return bail(PF_ERR_CUDA);
   }
-  h->cg_grid = std::max(1, std::min(occ * dev_sms, h->n_tiles));
-  const size_t npart = std::max<size_t>((size_t)h->n_tiles, (size_t)h->cg_grid) * 4;
+  // balanced persistent grid: the fewest CTAs that keep the per-CTA tile count minimal
+  auto balanced = [&](int resident) {
+    const int per = (h->n_tiles + resident - 1) / resident;
+    return std::max(1, (h->n_tiles + per - 1) / per);
+  };
+  h->cg_grid = balanced(occ * dev_sms);
+  h->cg_grid_evo = balanced(occ_evo * dev_sms);
+  const size_t npart =
+      std::max<size_t>((size_t)h->n_tiles, (size_t)std::max(h->cg_grid, h->cg_grid_evo)) * 4;
   CREATE_ALLOC(h->partials, npart);
   CREATE_CUDA(cudaHostAlloc((void**)&h->h_cgres, sizeof(CgResult), cudaHostAllocMapped));
   CREATE_CUDA(cudaHostGetDevicePointer((void**)&h->d_cgres, h->h_cgres, 0));
@@ -549,13 +558,10 @@ static pf_status finalize(pf_handle* h, int nv) {
   return PF_OK;
 }
 
-// one persistent PCG solve; returns the CG status
-static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
-                        long long* iters) {
+static pfb::CgArgs cg_args(pf_handle* h, bool mom) {
   pfb::CgArgs a{};
   a.m = h->dm;
   a.C = h->C;
-  a.vec2 = mom ? 1 : 0;
   a.ndof = mom ? 2LL * h->n_nodes : (long long)h->n_nodes;
   a.d = h->d;
   a.flags = h->flags;
@@ -566,16 +572,24 @@ static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int*
   a.p0 = mom ? h->p0u : h->p0d;
   a.p1 = mom ? h->p1u : h->p1d;
   a.dinv = mom ? h->dinvu : h->dinvd;
-  a.target = target;
   a.partials = h->partials;
   a.result = h->d_cgres;
   a.rtol = h->cfg.cg_rtol;
   a.maxiter = (long long)h->cfg.cg_maxiter_factor * a.ndof;  // 20 * matrix.shape[0]
+  return a;
+}
+
+// one persistent PCG solve; returns the CG status
+static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
+                        long long* iters) {
+  pfb::CgArgs a = cg_args(h, mom);
+  a.target = target;
   a.probe = probe ? 1 : 0;
   void* args[] = {&a};
+  const void* fn = mom ? (const void*)pfb::k_cg<true> : (const void*)pfb::k_cg<false>;
+  const int grid = mom ? h->cg_grid : h->cg_grid_evo;
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
-  PF_CUDA(cudaLaunchCooperativeKernel((const void*)pfb::k_cg, dim3(h->cg_grid), dim3(pfb::NT),
-                                      args, 0, h->stream));
+  PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(pfb::NT), args, 0, h->stream));
   PF_TRY(launched(h));
   PF_CUDA(cudaEventRecord(h->ev1, h->stream));
   PF_CUDA(cudaStreamSynchronize(h->stream));
@@ -880,15 +894,8 @@ extern "C" pf_status pf_momentum_tangent_apply(pf_handle* h, const double* x, do
   PF_CUDA(cudaSetDevice(h->device));
   PF_TRY(launch_mom_prepare(h, 1));  // branch flags and raw diagonal at the current u
   PF_TRY(h2d(h, h->p0u, x, 2 * (size_t)h->n_nodes));
-  pfb::ApplyArgs a{};
-  a.m = h->dm;
-  a.C = h->C;
-  a.d = h->d;
-  a.flags = h->flags;
-  a.x = h->p0u;
-  a.y = h->qu;
-  a.vec2 = 1;
-  pfb::k_apply<<<h->n_tiles, pfb::NT, 0, h->stream>>>(a);
+  pfb::CgArgs a = cg_args(h, true);
+  pfb::k_apply<true><<<h->n_tiles, pfb::NT, 0, h->stream>>>(a, h->p0u);
   PF_TRY(launched(h));
   PF_TRY(d2h(h, y, h->qu, 2 * (size_t)h->n_nodes));
   PF_TRY(d2h(h, diag, h->diagu, 2 * (size_t)h->n_nodes));
@@ -910,14 +917,8 @@ extern "C" pf_status pf_evolution_tangent_apply(pf_handle* h, int scheme, const 
   if (scheme < PF_ST || scheme > PF_S3) return fail(h, PF_ERR_INVALID, "unknown scheme");
   PF_TRY(launch_evo_prepare(h, 1, scheme));
   PF_TRY(h2d(h, h->p0d, x, (size_t)h->n_nodes));
-  pfb::ApplyArgs a{};
-  a.m = h->dm;
-  a.C = h->C;
-  a.b = h->b;
-  a.x = h->p0d;
-  a.y = h->qd;
-  a.vec2 = 0;
-  pfb::k_apply<<<h->n_tiles, pfb::NT, 0, h->stream>>>(a);
+  pfb::CgArgs a = cg_args(h, false);
+  pfb::k_apply<false><<<h->n_tiles, pfb::NT, 0, h->stream>>>(a, h->p0d);
   PF_TRY(launched(h));
   PF_TRY(d2h(h, y, h->qd, (size_t)h->n_nodes));
   PF_TRY(d2h(h, diag, h->diagd, (size_t)h->n_nodes));

@@ -1,0 +1,465 @@
+// pf_cg.cuh — K4/K8 + K5 (+K10): persistent Jacobi-PCG, one cooperative launch per linear solve.
+//
+// Mirrors scipy.sparse.linalg.cg (SciPy 1.18.1, called at linsolve.py:51): x0 = 0, stop when the
+// recursive residual satisfies ||r|| < rtol*||b||, z = D^-1 r, maxiter = 20 n, no breakdown test
+// (the reference's bounded matrix keeps constrained components at zero, assembly.py:299-308,
+// which the masked operator reproduces exactly).  Per iteration there are two grid barriers:
+//   phase A (tiles): p_k = z_k + beta p_{k-1} evaluated on the fly for tile+halo nodes (p is
+//                    double-buffered so neighbours read p_{k-1} while owners write p_k),
+//                    x += alpha_{k-1} p_{k-1} on owned nodes, q = A p_k (masked), partial p.q
+//   phase B (flat):  r -= alpha q, partials r.r and r.D^-1.r
+// The SPD probe (K10, SURVEY.md §7 hard part 1) aborts at p.q <= 0.
+//
+// Latency structure: thread t owns node slot t of its tile (TX x TY = NT), so the owned node's
+// r, D^-1 and p stay in registers from the halo phase to the gather; the halo border and the slit
+// duplicates are spread over the first threads; node/cell ids come from the row tables through
+// the read-only path (L1-resident), so a tile needs three CTA barriers.
+#pragma once
+#include <type_traits>
+
+namespace pfb {
+
+constexpr int NBORDER = 2 * HX + 2 * TY;  // halo ring slots around the TX x TY owned block
+#ifndef PFB_CG_MINB_MOM
+#define PFB_CG_MINB_MOM 2
+#endif
+#ifndef PFB_CG_MINB_EVO
+#define PFB_CG_MINB_EVO 3
+#endif
+
+struct SmemMomA {
+  double2 p[HY][HX];
+  double2 pdup[HX];
+  double d[HY][HX];
+  double ddup[HX];
+  double2 f[4][EY][EX];
+};
+
+struct SmemEvoA {
+  double p[HY][HX];
+  double pdup[HX];
+  double f[4][EY][EX];
+};
+
+// extra slot e (0 .. NBORDER + HX) -> halo position; returns false for the dup row
+__device__ __forceinline__ bool border_pos(int e, int& hx, int& hy) {
+  if (e < HX) { hx = e; hy = 0; return true; }
+  e -= HX;
+  if (e < HX) { hx = e; hy = HY - 1; return true; }
+  e -= HX;
+  if (e < 2 * TY) { hx = (e & 1) ? HX - 1 : 0; hy = 1 + (e >> 1); return true; }
+  hx = e - 2 * TY;
+  hy = -1;
+  return false;
+}
+
+enum CgStatus { CG_CONVERGED = 0, CG_MAXITER = 1, CG_INDEFINITE = 2, CG_NAN = 3 };
+
+struct CgResult {
+  long long iters;
+  int status;
+  int pad;
+  double bnorm, rnorm;
+};
+
+struct CgArgs {
+  DMesh m;
+  Consts C;
+  long long ndof;        // flat length (2*n_nodes or n_nodes)
+  const double* d;       // momentum: nodal d
+  const uint8_t* flags;  // momentum: per-element tangent branch bits
+  const double* b;       // phase field: [n_elems*4] Newton coefficient
+  double* x;
+  double* r;
+  double* q;
+  double* p0;
+  double* p1;
+  const double* dinv;
+  double* target;        // optional: target += x at the end
+  double* partials;      // >= 2*gridDim.x
+  CgResult* result;
+  double rtol;
+  long long maxiter;
+  int probe;
+};
+
+template <bool MOM>
+struct Node;
+template <>
+struct Node<true> {
+  using T = double2;
+  __device__ static T zero() { return make_double2(0.0, 0.0); }
+  __device__ static T ld_cg(const double* p, int id) {
+    return __ldcg(reinterpret_cast<const double2*>(p) + id);
+  }
+  __device__ static T ld_ro(const double* p, int id) {
+    return __ldg(reinterpret_cast<const double2*>(p) + id);
+  }
+  __device__ static void st(double* p, int id, T v) { reinterpret_cast<double2*>(p)[id] = v; }
+  __device__ static T mul(T a, T b) { return make_double2(a.x * b.x, a.y * b.y); }
+  __device__ static T axpy(double s, T x, T y) { return make_double2(s * x.x + y.x, s * x.y + y.y); }
+  __device__ static T mask(T v, T di) {
+    return make_double2(di.x != 0.0 ? v.x : 0.0, di.y != 0.0 ? v.y : 0.0);
+  }
+  __device__ static double dot(T a, T b) { return a.x * b.x + a.y * b.y; }
+};
+template <>
+struct Node<false> {
+  using T = double;
+  __device__ static T zero() { return 0.0; }
+  __device__ static T ld_cg(const double* p, int id) { return __ldcg(p + id); }
+  __device__ static T ld_ro(const double* p, int id) { return __ldg(p + id); }
+  __device__ static void st(double* p, int id, T v) { p[id] = v; }
+  __device__ static T mul(T a, T b) { return a * b; }
+  __device__ static T axpy(double s, T x, T y) { return s * x + y; }
+  __device__ static T mask(T v, T di) { return di != 0.0 ? v : 0.0; }
+  __device__ static double dot(T a, T b) { return a * b; }
+};
+
+// ---------------------------------------------------------------------------------------
+// register-lean element operators (per Gauss point accumulation)
+__device__ __forceinline__ void mom_cell_apply_lean(const Consts& C, const double2 (&pc)[4],
+                                                    const double (&dc)[4], unsigned flags,
+                                                    double2 (&f)[4]) {
+  const double bx = pc[1].x - pc[0].x, tx = pc[2].x - pc[3].x;
+  const double by = pc[1].y - pc[0].y, ty = pc[2].y - pc[3].y;
+  const double lx = pc[3].x - pc[0].x, rx = pc[2].x - pc[1].x;
+  const double ly = pc[3].y - pc[0].y, ry = pc[2].y - pc[1].y;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) f[q] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    // dN/dx = [-A, A, B, -B], dN/dy = [-Cc, -D, D, Cc] at this Gauss point
+    const double A = g < 2 ? C.Px : C.Mx, B = g < 2 ? C.Mx : C.Px;
+    const double Cc = (g == 0 || g == 3) ? C.Py : C.My, D = (g == 0 || g == 3) ? C.My : C.Py;
+    const double dg = C.N[g][0] * dc[0] + C.N[g][1] * dc[1] + C.N[g][2] * dc[2] +
+                      C.N[g][3] * dc[3];
+    const double gg = degradation(C, dg);
+    const double exx = A * bx + B * tx;
+    const double eyy = Cc * ly + D * ry;
+    const double gxy = Cc * lx + D * rx + A * by + B * ty;
+    double sxx, syy, sxy;
+    tangent_gp(C, exx, eyy, gxy, gg, (flags >> g) & 1u, sxx, syy, sxy);
+    sxx *= C.w;
+    syy *= C.w;
+    sxy *= C.w;
+    f[0].x += -A * sxx - Cc * sxy;
+    f[1].x += A * sxx - D * sxy;
+    f[2].x += B * sxx + D * sxy;
+    f[3].x += -B * sxx + Cc * sxy;
+    f[0].y += -Cc * syy - A * sxy;
+    f[1].y += -D * syy + A * sxy;
+    f[2].y += D * syy + B * sxy;
+    f[3].y += Cc * syy - B * sxy;
+  }
+}
+
+__device__ __forceinline__ void evo_cell_apply(const Consts& C, const double (&pc)[4],
+                                               const double (&bq)[4], double (&f)[4]) {
+  double t4[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+    t4[g] = bq[g] * (C.N[g][0] * pc[0] + C.N[g][1] * pc[1] + C.N[g][2] * pc[2] +
+                     C.N[g][3] * pc[3]);
+#pragma unroll
+  for (int aa = 0; aa < 4; ++aa)
+    f[aa] = C.Nw[0][aa] * t4[0] + C.Nw[1][aa] * t4[1] + C.Nw[2][aa] * t4[2] +
+            C.Nw[3][aa] * t4[3] + C.lap[aa][0] * pc[0] + C.lap[aa][1] * pc[1] +
+            C.lap[aa][2] * pc[2] + C.lap[aa][3] * pc[3];
+}
+
+// ---------------------------------------------------------------------------------------
+// Phase A of one tile.  APPLY=true: plain y = A x (x from `pold`, y to a.q, unmasked, no
+// p/x bookkeeping) — used by pf_*_tangent_apply.
+template <bool MOM, bool APPLY, class SM>
+__device__ __forceinline__ void phase_a_tile(const CgArgs& a, SM& S, int tile, bool first,
+                                             double beta, double alpha_prev,
+                                             const double* __restrict__ pold,
+                                             double* __restrict__ pnew, double& pq) {
+  using NT_ = Node<MOM>;
+  using T = typename NT_::T;
+  const DMesh& m = a.m;
+  const Consts& C = a.C;
+  const int2 tl = m.tiles[tile];
+  const int tx0 = tl.x * TX, ty0 = tl.y * TY;
+  const int tid = threadIdx.x;
+  // ---- owned slot of this thread
+  const int ox = tid % TX, oy = tid / TX;
+  const int oi = tx0 + ox, oj = ty0 + oy;
+  const int oid = node_at(m, oi, oj);
+  T own_di = NT_::zero(), own_p = NT_::zero();
+  if (oid >= 0) {
+    if (APPLY) {
+      own_p = NT_::ld_ro(pold, oid);
+    } else {
+      own_di = NT_::ld_ro(a.dinv, oid);
+      own_p = NT_::mul(own_di, NT_::ld_cg(a.r, oid));
+      if (!first) {
+        const T po = NT_::ld_cg(pold, oid);
+        own_p = NT_::axpy(beta, po, own_p);
+        NT_::st(a.x, oid, NT_::axpy(alpha_prev, po, NT_::ld_cg(a.x, oid)));
+      }
+      NT_::st(pnew, oid, own_p);
+    }
+  }
+  S.p[oy + 1][ox + 1] = own_p;
+  if constexpr (MOM) S.d[oy + 1][ox + 1] = oid >= 0 ? __ldg(a.d + oid) : 0.0;
+  // ---- halo ring and slit duplicates
+  const bool dup = tile_has_dup(m, ty0);
+  const int nextra = NBORDER + (dup ? HX : 0);
+  for (int e = tid; e < nextra; e += NT) {
+    int hx, hy;
+    const bool ring = border_pos(e, hx, hy);
+    const int i = tx0 - 1 + hx;
+    int id;
+    bool owned = false;
+    if (ring) {
+      id = node_at(m, i, ty0 - 1 + hy);
+    } else {
+      id = is_dup_col(m, i) ? m.dup_start + (i - m.notch_lo) : -1;
+      owned = m.notch_row >= ty0 && m.notch_row < ty0 + TY && hx >= 1 && hx <= TX;
+    }
+    T pn = NT_::zero();
+    double dv = 0.0;
+    if (id >= 0) {
+      if (APPLY) {
+        pn = NT_::ld_ro(pold, id);
+      } else {
+        pn = NT_::mul(NT_::ld_ro(a.dinv, id), NT_::ld_cg(a.r, id));
+        if (!first) {
+          const T po = NT_::ld_cg(pold, id);
+          pn = NT_::axpy(beta, po, pn);
+          if (owned) NT_::st(a.x, id, NT_::axpy(alpha_prev, po, NT_::ld_cg(a.x, id)));
+        }
+        if (owned) NT_::st(pnew, id, pn);
+      }
+      if constexpr (MOM) dv = __ldg(a.d + id);
+    }
+    if (ring) {
+      S.p[hy][hx] = pn;
+      if constexpr (MOM) S.d[hy][hx] = dv;
+    } else {
+      S.pdup[hx] = pn;
+      if constexpr (MOM) S.ddup[hx] = dv;
+    }
+  }
+  __syncthreads();
+  // ---- cells touching an owned node
+  for (int c = tid; c < EX * EY; c += NT) {
+    const int ex = c % EX, ey = c / EX;
+    const int ci = tx0 - 1 + ex, cj = ty0 - 1 + ey;
+    const int eid = cell_at(m, ci, cj);
+    T f[4];
+    if constexpr (MOM) {
+      f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
+      if (eid >= 0) {
+        double2 pc[4];
+        double dc[4];
+        cell_corners(m, S.p, S.pdup, ex, ey, ci, cj, pc);
+        cell_corners(m, S.d, S.ddup, ex, ey, ci, cj, dc);
+        mom_cell_apply_lean(C, pc, dc, __ldg(a.flags + eid), f);
+      }
+    } else {
+      f[0] = f[1] = f[2] = f[3] = 0.0;
+      if (eid >= 0) {
+        double pc[4], bq[4];
+        cell_corners(m, S.p, S.pdup, ex, ey, ci, cj, pc);
+        load4(a.b, eid, bq);
+        evo_cell_apply(C, pc, bq, f);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) S.f[q][ey][ex] = f[q];
+  }
+  __syncthreads();
+  // ---- owned gather (reference element order), mask, p.q
+  if (oid >= 0) {
+    const bool split = owned_split(m, oi, oj);
+    T below, above;
+    gather_corners(S.f, ox, oy, below, above);
+    T qv = split ? below : gather_all(S.f, ox, oy);
+    if (!APPLY) {
+      qv = NT_::mask(qv, own_di);
+      pq += NT_::dot(own_p, qv);
+    }
+    NT_::st(a.q, oid, qv);
+    if (split) {
+      const int idd = m.dup_start + (oi - m.notch_lo);
+      T qd = above;
+      if (!APPLY) {
+        qd = NT_::mask(qd, NT_::ld_ro(a.dinv, idd));
+        pq += NT_::dot(S.pdup[ox + 1], qd);
+      }
+      NT_::st(a.q, idd, qd);
+    }
+  }
+  __syncthreads();
+}
+
+// partial k of CTA i lives at part[stride*i + k]; every CTA sums in the same fixed order
+template <int NV>
+__device__ __forceinline__ void grid_reduce(const double* part, int stride, double* bc,
+                                            double (&out)[NV]) {
+  if (threadIdx.x < 32) {
+    double s[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) s[k] = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) s[k] += __ldcg(part + stride * i + k);
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) s[k] = warp_sum(s[k]);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) bc[k] = s[k];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = bc[k];
+}
+
+// flat pass over double2 pairs: r -= alpha q (update), partials r.r and r.D^-1.r
+__device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, bool update, double& rr,
+                                        double& rz) {
+  constexpr int U = 4;
+  const long long n2 = a.ndof >> 1;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  double2* r2 = reinterpret_cast<double2*>(a.r);
+  const double2* q2 = reinterpret_cast<const double2*>(a.q);
+  const double2* d2 = reinterpret_cast<const double2*>(a.dinv);
+  for (long long base = (long long)blockIdx.x * blockDim.x + threadIdx.x; base < n2;
+       base += U * stride) {
+    // loads are issued unconditionally (clamped index) so the unrolled arrays stay in registers
+    double2 rv[U], qv[U], dv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = min(base + u * stride, n2 - 1);
+      rv[u] = __ldcg(r2 + i);
+      dv[u] = __ldg(d2 + i);
+      qv[u] = update ? __ldcg(q2 + i) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = base + u * stride;
+      if (i < n2) {
+        if (update) {
+          rv[u].x -= alpha * qv[u].x;
+          rv[u].y -= alpha * qv[u].y;
+          r2[i] = rv[u];
+        }
+        rr += rv[u].x * rv[u].x + rv[u].y * rv[u].y;
+        rz += rv[u].x * (dv[u].x * rv[u].x) + rv[u].y * (dv[u].y * rv[u].y);
+      }
+    }
+  }
+  if ((a.ndof & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long i = a.ndof - 1;
+    double rv = __ldcg(a.r + i);
+    if (update) {
+      rv -= alpha * __ldcg(a.q + i);
+      a.r[i] = rv;
+    }
+    rr += rv * rv;
+    rz += rv * (__ldg(a.dinv + i) * rv);
+  }
+}
+
+template <bool MOM>
+struct CgSmem {
+  using SM = typename std::conditional<MOM, SmemMomA, SmemEvoA>::type;
+  SM t;
+  double red[NT / 32 * 2];
+  double bc[4];
+};
+
+template <bool MOM>
+__global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k_cg(CgArgs a) {
+  __shared__ CgSmem<MOM> S;
+  cg::grid_group grid = cg::this_grid();
+  double* part = a.partials;
+  double rr = 0.0, rz = 0.0;
+  phase_b(a, 0.0, false, rr, rz);  // ||b||^2 and b.D^-1.b (r = b on entry)
+  {
+    double v[2] = {rr, rz};
+    block_sum<2>(v, S.red);
+    if (threadIdx.x == 0) { part[2 * blockIdx.x] = v[0]; part[2 * blockIdx.x + 1] = v[1]; }
+  }
+  grid.sync();
+  double red[2];
+  grid_reduce<2>(part, 2, S.bc, red);
+  rr = red[0];
+  double rho = red[1];
+  const double bnorm = sqrt(rr);
+  const double atol = a.rtol * bnorm;
+  long long k = 0;
+  int status = CG_CONVERGED;
+  double alpha = 0.0, rho_prev = 0.0;
+  if (bnorm != 0.0) {
+    for (;;) {
+      const double rn = sqrt(rr);
+      if (rn < atol) break;
+      if (!(rn == rn)) { status = CG_NAN; break; }
+      if (k >= a.maxiter) { status = CG_MAXITER; break; }
+      const bool first = (k == 0);
+      const double beta = first ? 0.0 : rho / rho_prev;
+      double* pnew = (k & 1) ? a.p1 : a.p0;
+      const double* pold = (k & 1) ? a.p0 : a.p1;
+      double pq = 0.0;
+      for (int tile = blockIdx.x; tile < a.m.n_tiles; tile += gridDim.x)
+        phase_a_tile<MOM, false>(a, S.t, tile, first, beta, alpha, pold, pnew, pq);
+      {
+        double v[1] = {pq};
+        block_sum<1>(v, S.red);
+        if (threadIdx.x == 0) part[2 * blockIdx.x] = v[0];
+      }
+      grid.sync();
+      double pqr[1];
+      grid_reduce<1>(part, 2, S.bc, pqr);
+      if (a.probe && !(pqr[0] > 0.0)) { status = CG_INDEFINITE; k += 1; break; }
+      alpha = rho / pqr[0];
+      rho_prev = rho;
+      rr = 0.0;
+      rz = 0.0;
+      phase_b(a, alpha, true, rr, rz);
+      {
+        double v[2] = {rr, rz};
+        block_sum<2>(v, S.red);
+        if (threadIdx.x == 0) { part[2 * blockIdx.x] = v[0]; part[2 * blockIdx.x + 1] = v[1]; }
+      }
+      grid.sync();
+      grid_reduce<2>(part, 2, S.bc, red);
+      rr = red[0];
+      rho = red[1];
+      ++k;
+    }
+  }
+  if (status != CG_INDEFINITE) {  // x += alpha_{k-1} p_{k-1}; target += x
+    const double* plast = (k & 1) ? a.p0 : a.p1;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.ndof;
+         i += stride) {
+      double xv = __ldcg(a.x + i);
+      if (k > 0) xv += alpha * __ldcg(plast + i);
+      a.x[i] = xv;
+      if (a.target) a.target[i] += xv;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.result->iters = k;
+    a.result->status = status;
+    a.result->bnorm = bnorm;
+    a.result->rnorm = sqrt(rr);
+  }
+}
+
+// y = A x (unmasked) at the current state: one CTA per tile
+template <bool MOM>
+__global__ void __launch_bounds__(NT) k_apply(CgArgs a, const double* x) {
+  __shared__ typename CgSmem<MOM>::SM S;
+  double pq = 0.0;
+  phase_a_tile<MOM, true>(a, S, blockIdx.x, true, 0.0, 0.0, x, nullptr, pq);
+}
+
+}  // namespace pfb

@@ -93,21 +93,30 @@ __device__ __forceinline__ double2 add2(double2 a, double2 b) {
   return make_double2(a.x + b.x, a.y + b.y);
 }
 
-// owned node (ox, oy): contributions of the cells below (corners 2, 3) and above (0, 1)
+// Owned node (ox, oy) sums its (up to four) cell contributions SEQUENTIALLY in the reference's
+// element order -- (i-1,j-1) corner 2, (i,j-1) corner 3, (i-1,j) corner 1, (i,j) corner 0 --
+// i.e. exactly the accumulation order of np.add.at / COO->CSR duplicate summation
+// (assembly.py:188, :195-197).  The order matters beyond round-off: the symmetric tension test
+// bifurcates at the crack step and the side the crack takes is decided by this bias.
+// `below` = first two terms (cells of row j-1), `above` = last two (cells of row j), used
+// separately at slit nodes, which belong to one side only.
+template <class T>
+__device__ __forceinline__ T add_t(T a, T b);
+template <>
+__device__ __forceinline__ double add_t<double>(double a, double b) { return a + b; }
+template <>
+__device__ __forceinline__ double2 add_t<double2>(double2 a, double2 b) { return add2(a, b); }
+
 template <class T>
 __device__ __forceinline__ void gather_corners(const T (&f)[4][EY][EX], int ox, int oy,
-                                               T& below, T& above);
-template <>
-__device__ __forceinline__ void gather_corners<double2>(const double2 (&f)[4][EY][EX], int ox,
-                                                        int oy, double2& below, double2& above) {
-  below = add2(f[2][oy][ox], f[3][oy][ox + 1]);
-  above = add2(f[0][oy + 1][ox + 1], f[1][oy + 1][ox]);
+                                               T& below, T& above) {
+  below = add_t(f[2][oy][ox], f[3][oy][ox + 1]);
+  above = add_t(f[1][oy + 1][ox], f[0][oy + 1][ox + 1]);
 }
-template <>
-__device__ __forceinline__ void gather_corners<double>(const double (&f)[4][EY][EX], int ox,
-                                                       int oy, double& below, double& above) {
-  below = f[2][oy][ox] + f[3][oy][ox + 1];
-  above = f[0][oy + 1][ox + 1] + f[1][oy + 1][ox];
+template <class T>
+__device__ __forceinline__ T gather_all(const T (&f)[4][EY][EX], int ox, int oy) {
+  return add_t(add_t(add_t(f[2][oy][ox], f[3][oy][ox + 1]), f[1][oy + 1][ox]),
+               f[0][oy + 1][ox + 1]);
 }
 
 __device__ __forceinline__ bool owned_split(const DMesh& m, int i, int j) {
@@ -224,7 +233,7 @@ __global__ void __launch_bounds__(NT) k_mom_prepare(MomPrepArgs a) {
         idown[0] = id;
         idown[1] = m.dup_start + (oi - m.notch_lo);
       } else {
-        Rown[0] = add2(below, above);
+        Rown[0] = gather_all(S.f, ox, oy);
         idown[0] = id;
       }
     }
@@ -277,7 +286,7 @@ __global__ void __launch_bounds__(NT) k_mom_prepare(MomPrepArgs a) {
       double2 below, above, dg[2];
       gather_corners(S.f, ox, oy, below, above);
       if (idown[1] >= 0) { dg[0] = below; dg[1] = above; }
-      else dg[0] = add2(below, above);
+      else dg[0] = gather_all(S.f, ox, oy);
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         if (idown[k] < 0) continue;
@@ -421,7 +430,7 @@ __global__ void __launch_bounds__(NT) k_evo_prepare(EvoPrepArgs a) {
         Rown[0] = below; Rown[1] = above;
         idown[0] = id; idown[1] = m.dup_start + (oi - m.notch_lo);
       } else {
-        Rown[0] = below + above;
+        Rown[0] = gather_all(S.f, ox, oy);
         idown[0] = id;
       }
     }
@@ -482,7 +491,7 @@ __global__ void __launch_bounds__(NT) k_evo_prepare(EvoPrepArgs a) {
       double below, above, dg[2];
       gather_corners(S.f, ox, oy, below, above);
       if (idown[1] >= 0) { dg[0] = below; dg[1] = above; }
-      else dg[0] = below + above;
+      else dg[0] = gather_all(S.f, ox, oy);
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         if (idown[k] < 0) continue;
@@ -503,467 +512,9 @@ __global__ void __launch_bounds__(NT) k_evo_prepare(EvoPrepArgs a) {
   }
 }
 
-// ========================================================================================
-// K4/K8 + K5 (+K10): persistent Jacobi-PCG, one cooperative launch per linear solve.
-// Mirrors scipy.sparse.linalg.cg (SciPy 1.18.1, called at linsolve.py:51): x0 = 0,
-// stop when ||r|| < rtol*||b|| (recursive residual), z = D^-1 r, maxiter = 20 n.
-// Per iteration, two grid barriers:
-//   phase A (tiles): p_k = z + beta p_{k-1} evaluated on the fly for tile+halo nodes
-//                    (p double-buffered), x += alpha_{k-1} p_{k-1} on owned nodes,
-//                    q = A p_k (masked), partial p.q
-//   phase B (flat):  r -= alpha q, partial r.r and r.D^-1.r
-// The curvature probe (SPD predicate, SURVEY.md §7 hard part 1) aborts at p.q <= 0.
-enum CgStatus { CG_CONVERGED = 0, CG_MAXITER = 1, CG_INDEFINITE = 2, CG_NAN = 3 };
-
-struct CgResult {
-  long long iters;
-  int status;
-  int pad;
-  double bnorm, rnorm;
-};
-
-struct CgArgs {
-  DMesh m;
-  Consts C;
-  int vec2;              // 1: momentum (double2 nodes), 0: phase field (double nodes)
-  long long ndof;        // flat length (2*n_nodes or n_nodes)
-  // momentum operator data
-  const double* d;       // nodal d
-  const uint8_t* flags;  // per element
-  // phase-field operator data
-  const double* b;       // [n_elems*4]
-  // PCG vectors (flat doubles, length ndof)
-  double* x;
-  double* r;
-  double* q;
-  double* p0;
-  double* p1;
-  const double* dinv;
-  double* target;        // optional: target += x at the end
-  double* partials;      // >= 2*gridDim.x
-  CgResult* result;
-  double rtol;
-  long long maxiter;
-  int probe;             // abort on non-positive curvature
-};
-
-struct __align__(16) SmemCg {
-  union {
-    SmemVec2Tile v2;
-    SmemScalTile s;
-  };
-  double bc[4];
-};
-
-// ---- phase A, momentum tile
-__device__ __forceinline__ void cg_phaseA_mom(const CgArgs& a, SmemVec2Tile& S, int tile,
-                                              bool first, double beta, double alpha_prev,
-                                              const double2* __restrict__ pold,
-                                              double2* __restrict__ pnew, double& pq) {
-  const DMesh& m = a.m;
-  const Consts& C = a.C;
-  const int2 t = m.tiles[tile];
-  const int tx0 = t.x * TX, ty0 = t.y * TY;
-  load_tile_rows(m, ty0, S.R);
-  __syncthreads();
-  const bool dup = tile_has_dup(m, ty0);
-  const int nslots = HX * HY + (dup ? HX : 0);
-  const double2* r2 = reinterpret_cast<const double2*>(a.r);
-  const double2* di2 = reinterpret_cast<const double2*>(a.dinv);
-  double2* x2 = reinterpret_cast<double2*>(a.x);
-  for (int s = threadIdx.x; s < nslots; s += NT) {
-    const Slot sl = tile_slot(m, S.R, tx0, ty0, s);
-    double2 pn = make_double2(0.0, 0.0);
-    double dv = 0.0;
-    if (sl.id >= 0) {
-      const double2 rv = ldcg(r2 + sl.id);
-      const double2 dv2 = ldro(di2 + sl.id);
-      pn = make_double2(dv2.x * rv.x, dv2.y * rv.y);
-      if (!first) {
-        const double2 po = ldcg(pold + sl.id);
-        pn.x = beta * po.x + pn.x;
-        pn.y = beta * po.y + pn.y;
-        if (sl.owned) {
-          double2 xv = ldcg(x2 + sl.id);
-          xv.x += alpha_prev * po.x;
-          xv.y += alpha_prev * po.y;
-          x2[sl.id] = xv;
-        }
-      }
-      if (sl.owned) pnew[sl.id] = pn;
-      dv = ldro(a.d + sl.id);
-    }
-    if (sl.hy >= 0) { S.p[sl.hy][sl.hx] = pn; S.d[sl.hy][sl.hx] = dv; }
-    else { S.pdup[sl.hx] = pn; S.ddup[sl.hx] = dv; }
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < EX * EY; c += NT) {
-    const int ex = c % EX, ey = c / EX;
-    const int ci = tx0 - 1 + ex, cj = ty0 - 1 + ey;
-    const int eid = tile_cell(S.R, ey, ci);
-    double2 f[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-    if (eid >= 0) {
-      double2 pc[4];
-      double dc[4], g[4];
-      cell_corners(m, S.p, S.pdup, ex, ey, ci, cj, pc);
-      cell_corners(m, S.d, S.ddup, ex, ey, ci, cj, dc);
-      mom_cell_g(C, dc, g);
-      mom_cell_apply(C, pc, g, __ldg(a.flags + eid), f);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) S.f[q][ey][ex] = f[q];
-  }
-  __syncthreads();
-  double2* q2 = reinterpret_cast<double2*>(a.q);
-  {
-    const int o = threadIdx.x;
-    const int ox = o % TX, oy = o / TX;
-    const int oi = tx0 + ox, oj = ty0 + oy;
-    const int id = tile_node(S.R, oy + 1, oi);
-    if (id >= 0) {
-      double2 below, above;
-      gather_corners(S.f, ox, oy, below, above);
-      const bool split = owned_split(m, oi, oj);
-      double2 qv = split ? below : add2(below, above);
-      double2 dv = ldro(di2 + id);
-      qv.x = dv.x != 0.0 ? qv.x : 0.0;
-      qv.y = dv.y != 0.0 ? qv.y : 0.0;
-      q2[id] = qv;
-      const double2 pv = S.p[oy + 1][ox + 1];
-      pq += pv.x * qv.x + pv.y * qv.y;
-      if (split) {
-        const int idd = m.dup_start + (oi - m.notch_lo);
-        double2 qd = above;
-        dv = ldro(di2 + idd);
-        qd.x = dv.x != 0.0 ? qd.x : 0.0;
-        qd.y = dv.y != 0.0 ? qd.y : 0.0;
-        q2[idd] = qd;
-        const double2 pd = S.pdup[ox + 1];
-        pq += pd.x * qd.x + pd.y * qd.y;
-      }
-    }
-  }
-  __syncthreads();
-}
-
-// ---- phase A, phase-field tile
-__device__ __forceinline__ void cg_phaseA_evo(const CgArgs& a, SmemScalTile& S, int tile,
-                                              bool first, double beta, double alpha_prev,
-                                              const double* __restrict__ pold,
-                                              double* __restrict__ pnew, double& pq) {
-  const DMesh& m = a.m;
-  const Consts& C = a.C;
-  const int2 t = m.tiles[tile];
-  const int tx0 = t.x * TX, ty0 = t.y * TY;
-  load_tile_rows(m, ty0, S.R);
-  __syncthreads();
-  const bool dup = tile_has_dup(m, ty0);
-  const int nslots = HX * HY + (dup ? HX : 0);
-  for (int s = threadIdx.x; s < nslots; s += NT) {
-    const Slot sl = tile_slot(m, S.R, tx0, ty0, s);
-    double pn = 0.0;
-    if (sl.id >= 0) {
-      pn = ldro(a.dinv + sl.id) * ldcg(a.r + sl.id);
-      if (!first) {
-        const double po = ldcg(pold + sl.id);
-        pn = beta * po + pn;
-        if (sl.owned) a.x[sl.id] = ldcg(a.x + sl.id) + alpha_prev * po;
-      }
-      if (sl.owned) pnew[sl.id] = pn;
-    }
-    if (sl.hy >= 0) S.p[sl.hy][sl.hx] = pn;
-    else S.pdup[sl.hx] = pn;
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < EX * EY; c += NT) {
-    const int ex = c % EX, ey = c / EX;
-    const int ci = tx0 - 1 + ex, cj = ty0 - 1 + ey;
-    const int eid = tile_cell(S.R, ey, ci);
-    double f[4] = {0, 0, 0, 0};
-    if (eid >= 0) {
-      double pc[4], pg[4], bq[4];
-      cell_corners(m, S.p, S.pdup, ex, ey, ci, cj, pc);
-      interp_q4(C, pc[0], pc[1], pc[2], pc[3], pg);
-      load4(a.b, eid, bq);
-      double t4[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) t4[q] = bq[q] * pg[q];
-#pragma unroll
-      for (int aa = 0; aa < 4; ++aa)
-        f[aa] = C.Nw[0][aa] * t4[0] + C.Nw[1][aa] * t4[1] + C.Nw[2][aa] * t4[2] +
-                C.Nw[3][aa] * t4[3] + C.lap[aa][0] * pc[0] + C.lap[aa][1] * pc[1] +
-                C.lap[aa][2] * pc[2] + C.lap[aa][3] * pc[3];
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) S.f[q][ey][ex] = f[q];
-  }
-  __syncthreads();
-  {
-    const int o = threadIdx.x;
-    const int ox = o % TX, oy = o / TX;
-    const int oi = tx0 + ox, oj = ty0 + oy;
-    const int id = tile_node(S.R, oy + 1, oi);
-    if (id >= 0) {
-      double below, above;
-      gather_corners(S.f, ox, oy, below, above);
-      const bool split = owned_split(m, oi, oj);
-      double qv = split ? below : below + above;
-      qv = ldro(a.dinv + id) != 0.0 ? qv : 0.0;
-      a.q[id] = qv;
-      pq += S.p[oy + 1][ox + 1] * qv;
-      if (split) {
-        const int idd = m.dup_start + (oi - m.notch_lo);
-        const double qd = ldro(a.dinv + idd) != 0.0 ? above : 0.0;
-        a.q[idd] = qd;
-        pq += S.pdup[ox + 1] * qd;
-      }
-    }
-  }
-  __syncthreads();
-}
-
-// grid-wide deterministic reduction of NV partials per CTA (called right after grid.sync)
-// partial k of CTA i lives at part[stride*i + k]
-template <int NV>
-__device__ __forceinline__ void grid_reduce(const double* part, int stride, double* bc,
-                                            double (&out)[NV]) {
-  if (threadIdx.x < 32) {
-    double s[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) s[k] = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) {
-#pragma unroll
-      for (int k = 0; k < NV; ++k) s[k] += __ldcg(part + stride * i + k);
-    }
-#pragma unroll
-    for (int k = 0; k < NV; ++k) s[k] = warp_sum(s[k]);
-    if (threadIdx.x == 0) {
-#pragma unroll
-      for (int k = 0; k < NV; ++k) bc[k] = s[k];
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < NV; ++k) out[k] = bc[k];
-}
-
-// flat pass: r -= alpha q (alpha = 0 for the initial reduction); partials (r.r, r.Dinv.r)
-__device__ __forceinline__ void cg_phaseB(const CgArgs& a, double alpha, bool update,
-                                          double& rr, double& rz) {
-  const long long n2 = a.ndof >> 1;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  double2* r2 = reinterpret_cast<double2*>(a.r);
-  const double2* q2 = reinterpret_cast<const double2*>(a.q);
-  const double2* d2 = reinterpret_cast<const double2*>(a.dinv);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
-    double2 rv = ldcg(r2 + i);
-    if (update) {
-      const double2 qv = ldcg(q2 + i);
-      rv.x -= alpha * qv.x;
-      rv.y -= alpha * qv.y;
-      r2[i] = rv;
-    }
-    const double2 dv = ldro(d2 + i);
-    rr += rv.x * rv.x + rv.y * rv.y;
-    rz += rv.x * (dv.x * rv.x) + rv.y * (dv.y * rv.y);
-  }
-  if ((a.ndof & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-    const long long i = a.ndof - 1;
-    double rv = __ldcg(a.r + i);
-    if (update) {
-      rv -= alpha * __ldcg(a.q + i);
-      a.r[i] = rv;
-    }
-    rr += rv * rv;
-    rz += rv * (__ldg(a.dinv + i) * rv);
-  }
-}
-
-__global__ void __launch_bounds__(NT) k_cg(CgArgs a) {
-  __shared__ SmemCg S;
-  cg::grid_group grid = cg::this_grid();
-  double* part = a.partials;
-  // initial reduction: ||b||^2 and b.D^-1.b (r = b on entry)
-  double rr = 0.0, rz = 0.0;
-  cg_phaseB(a, 0.0, false, rr, rz);
-  {
-    double v[2] = {rr, rz};
-    block_sum<2>(v, a.vec2 ? S.v2.red : S.s.red);
-    if (threadIdx.x == 0) { part[2 * blockIdx.x] = v[0]; part[2 * blockIdx.x + 1] = v[1]; }
-  }
-  grid.sync();
-  double red[2];
-  grid_reduce<2>(part, 2, S.bc, red);
-  rr = red[0];
-  double rho = red[1];
-  const double bnorm = sqrt(rr);
-  const double atol = a.rtol * bnorm;
-  long long k = 0;
-  int status = CG_CONVERGED;
-  double alpha = 0.0, rho_prev = 0.0;
-  if (bnorm != 0.0) {
-    for (;;) {
-      const double rn = sqrt(rr);
-      if (rn < atol) break;
-      if (!(rn == rn)) { status = CG_NAN; break; }
-      if (k >= a.maxiter) { status = CG_MAXITER; break; }
-      const bool first = (k == 0);
-      const double beta = first ? 0.0 : rho / rho_prev;
-      double* pnew = (k & 1) ? a.p1 : a.p0;
-      const double* pold = (k & 1) ? a.p0 : a.p1;
-      double pq = 0.0;
-      for (int tile = blockIdx.x; tile < a.m.n_tiles; tile += gridDim.x) {
-        if (a.vec2)
-          cg_phaseA_mom(a, S.v2, tile, first, beta, alpha,
-                        reinterpret_cast<const double2*>(pold),
-                        reinterpret_cast<double2*>(pnew), pq);
-        else
-          cg_phaseA_evo(a, S.s, tile, first, beta, alpha, pold, pnew, pq);
-      }
-      {
-        double v[1] = {pq};
-        block_sum<1>(v, a.vec2 ? S.v2.red : S.s.red);
-        if (threadIdx.x == 0) part[2 * blockIdx.x] = v[0];
-      }
-      grid.sync();
-      double pqr[1];
-      grid_reduce<1>(part, 2, S.bc, pqr);
-      const double pqv = pqr[0];
-      if (a.probe && !(pqv > 0.0)) { status = CG_INDEFINITE; k += 1; break; }
-      alpha = rho / pqv;
-      rho_prev = rho;
-      rr = 0.0; rz = 0.0;
-      cg_phaseB(a, alpha, true, rr, rz);
-      {
-        double v[2] = {rr, rz};
-        block_sum<2>(v, a.vec2 ? S.v2.red : S.s.red);
-        if (threadIdx.x == 0) { part[2 * blockIdx.x] = v[0]; part[2 * blockIdx.x + 1] = v[1]; }
-      }
-      grid.sync();
-      grid_reduce<2>(part, 2, S.bc, red);
-      rr = red[0];
-      rho = red[1];
-      ++k;
-    }
-  }
-  // finalize: x += alpha_{k-1} p_{k-1}; target += x
-  if (status != CG_INDEFINITE) {
-    const double* plast = (k & 1) ? a.p0 : a.p1;  // p_{k-1} lives in buffer (k-1)&1
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.ndof;
-         i += stride) {
-      double xv = __ldcg(a.x + i);
-      if (k > 0) xv += alpha * __ldcg(plast + i);
-      a.x[i] = xv;
-      if (a.target) a.target[i] += xv;
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.result->iters = k;
-    a.result->status = status;
-    a.result->bnorm = bnorm;
-    a.result->rnorm = sqrt(rr);
-  }
-}
-
-// ========================================================================================
-// matrix-free tangent apply (tests / pf_*_tangent_apply): y = K x, unmasked, at current state
-struct ApplyArgs {
-  DMesh m;
-  Consts C;
-  const double* d;       // momentum: nodal d
-  const uint8_t* flags;  // momentum: branch flags
-  const double* b;       // phase field: Newton coefficient
-  const double* x;
-  double* y;
-  int vec2;
-};
-
-__global__ void __launch_bounds__(NT) k_apply(ApplyArgs a) {
-  __shared__ SmemCg S;
-  const DMesh& m = a.m;
-  const Consts& C = a.C;
-  const int2 t = m.tiles[blockIdx.x];
-  const int tx0 = t.x * TX, ty0 = t.y * TY;
-  TileRows& R = a.vec2 ? S.v2.R : S.s.R;
-  load_tile_rows(m, ty0, R);
-  __syncthreads();
-  const bool dup = tile_has_dup(m, ty0);
-  const int nslots = HX * HY + (dup ? HX : 0);
-  for (int s = threadIdx.x; s < nslots; s += NT) {
-    const Slot sl = tile_slot(m, R, tx0, ty0, s);
-    if (a.vec2) {
-      double2 pv = make_double2(0, 0);
-      double dv = 0.0;
-      if (sl.id >= 0) {
-        pv = ldro(reinterpret_cast<const double2*>(a.x) + sl.id);
-        dv = ldro(a.d + sl.id);
-      }
-      if (sl.hy >= 0) { S.v2.p[sl.hy][sl.hx] = pv; S.v2.d[sl.hy][sl.hx] = dv; }
-      else { S.v2.pdup[sl.hx] = pv; S.v2.ddup[sl.hx] = dv; }
-    } else {
-      const double pv = sl.id >= 0 ? ldro(a.x + sl.id) : 0.0;
-      if (sl.hy >= 0) S.s.p[sl.hy][sl.hx] = pv;
-      else S.s.pdup[sl.hx] = pv;
-    }
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < EX * EY; c += NT) {
-    const int ex = c % EX, ey = c / EX;
-    const int ci = tx0 - 1 + ex, cj = ty0 - 1 + ey;
-    const int eid = tile_cell(R, ey, ci);
-    if (a.vec2) {
-      double2 f[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-      if (eid >= 0) {
-        double2 pc[4];
-        double dc[4], g[4];
-        cell_corners(m, S.v2.p, S.v2.pdup, ex, ey, ci, cj, pc);
-        cell_corners(m, S.v2.d, S.v2.ddup, ex, ey, ci, cj, dc);
-        mom_cell_g(C, dc, g);
-        mom_cell_apply(C, pc, g, __ldg(a.flags + eid), f);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) S.v2.f[q][ey][ex] = f[q];
-    } else {
-      double f[4] = {0, 0, 0, 0};
-      if (eid >= 0) {
-        double pc[4], pg[4], bq[4], t4[4];
-        cell_corners(m, S.s.p, S.s.pdup, ex, ey, ci, cj, pc);
-        interp_q4(C, pc[0], pc[1], pc[2], pc[3], pg);
-        load4(a.b, eid, bq);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) t4[q] = bq[q] * pg[q];
-#pragma unroll
-        for (int aa = 0; aa < 4; ++aa)
-          f[aa] = C.Nw[0][aa] * t4[0] + C.Nw[1][aa] * t4[1] + C.Nw[2][aa] * t4[2] +
-                  C.Nw[3][aa] * t4[3] + C.lap[aa][0] * pc[0] + C.lap[aa][1] * pc[1] +
-                  C.lap[aa][2] * pc[2] + C.lap[aa][3] * pc[3];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) S.s.f[q][ey][ex] = f[q];
-    }
-  }
-  __syncthreads();
-  const int o = threadIdx.x;
-  const int ox = o % TX, oy = o / TX;
-  const int oi = tx0 + ox, oj = ty0 + oy;
-  const int id = tile_node(R, oy + 1, oi);
-  if (id < 0) return;
-  const bool split = owned_split(m, oi, oj);
-  const int idd = split ? m.dup_start + (oi - m.notch_lo) : -1;
-  if (a.vec2) {
-    double2 below, above;
-    gather_corners(S.v2.f, ox, oy, below, above);
-    double2* y2 = reinterpret_cast<double2*>(a.y);
-    y2[id] = split ? below : add2(below, above);
-    if (split) y2[idd] = above;
-  } else {
-    double below, above;
-    gather_corners(S.s.f, ox, oy, below, above);
-    a.y[id] = split ? below : below + above;
-    if (split) a.y[idd] = above;
-  }
-}
+}  // namespace pfb
+#include "pf_cg.cuh"
+namespace pfb {
 
 // ========================================================================================
 // cell-parallel GP kernels (2-D grid over the bounding cell grid)

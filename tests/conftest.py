@@ -37,7 +37,48 @@ def rel_err(a, b) -> float:
     return float(np.abs(a - b).max() / scale)
 
 
-KAT_MESHES = ("notched8", "notched12x6", "plain10", "lshape")
+def mirror_perm(mesh) -> np.ndarray:
+    """Node permutation of the reflection y -> side - y of a notched square.
+
+    Grid node (i, j) maps to (i, ny - j); on the slit row the lower-face node (i, ny/2) and its
+    duplicate (upper face) swap.  The tension load case (bottom fixed, top pulled) is
+    invariant under this reflection up to a rigid translation, so a phase field and its
+    mirror image are equally valid solutions (the crack-step bifurcation picks one by
+    round-off; DESIGN.md "Parity").
+    """
+    from paper_2209_07969_b200.meshing import StructuredLayout
+
+    lay = StructuredLayout.from_mesh(mesh)
+    nx, ny = lay.nx, lay.ny
+    ids = np.arange((nx + 1) * (ny + 1)).reshape(ny + 1, nx + 1)
+    perm = np.arange(mesh.n_nodes)
+    perm[: ids.size] = ids[::-1].ravel()
+    if lay.notch_row >= 0:
+        cols = np.arange(lay.notch_lo, lay.notch_hi)
+        orig = lay.notch_row * (nx + 1) + cols
+        dup = lay.dup_start + (cols - lay.notch_lo)
+        perm[orig], perm[dup] = dup, orig
+    return perm
+
+
+def stag_band(case: str, scheme: str, n_steps: int) -> np.ndarray:
+    """Per-step allowed |n_stag - reference|: 1 + spread of the round-off ensemble."""
+    path = os.path.join(GOLDEN, f"sens_{case}_{scheme}.json")
+    if not os.path.exists(path):
+        return np.ones(n_steps, dtype=int)
+    with open(path) as f:
+        sens = json.load(f)["n_stag"]
+    z = np.load(os.path.join(GOLDEN, f"run_{case}_{scheme}.npz"))
+    ref = z["table"][:n_steps, 1].astype(int)
+    spread = np.zeros(n_steps, dtype=int)
+    for v in sens.values():
+        v = np.asarray(v[:n_steps])
+        spread[: v.size] = np.maximum(spread[: v.size], np.abs(v - ref[: v.size]))
+    return 1 + spread
+
+
+KAT_MESHES = ("notched8", "notched12x6", "plain10", "lshape", "notched16", "notched80x16",
+              "lshape12p5")
 
 
 def kat_mesh(name):
@@ -48,6 +89,9 @@ def kat_mesh(name):
         "notched12x6": lambda: meshing.build_notched_square(12, 6, 2.0),
         "plain10": lambda: meshing.build_notched_square(10, 10, 1000.0, False),
         "lshape": lambda: meshing.build_lshape_mesh(62.5),
+        "notched16": lambda: meshing.build_notched_square(16, 16, 1.0),
+        "notched80x16": lambda: meshing.build_notched_square(80, 16, 5.0),
+        "lshape12p5": lambda: meshing.build_lshape_mesh(12.5),
     }[name]()
 
 

@@ -47,7 +47,7 @@ def _ref():
 
 
 # -------------------------------------------------------------------------------------------
-def kat() -> None:
+def kat(only=None) -> None:
     """Kernel-level known answers on small meshes from seeded random states."""
     assembly, linsolve, material, meshing, schemes = _ref()
     meshes = {
@@ -55,12 +55,18 @@ def kat() -> None:
         "notched12x6": lambda: meshing.build_notched_square(12, 6, 2.0),
         "plain10": lambda: meshing.build_notched_square(10, 10, 1000.0, False),
         "lshape": lambda: meshing.build_lshape_mesh(62.5),
+        # slit row on a tile boundary (TY = 8) and a slit spanning two tile columns (TX = 32)
+        "notched16": lambda: meshing.build_notched_square(16, 16, 1.0),
+        "notched80x16": lambda: meshing.build_notched_square(80, 16, 5.0),
+        "lshape12p5": lambda: meshing.build_lshape_mesh(12.5),
     }
     params = material.MaterialParams.from_young_poisson(
         210000.0, 0.3, g_c=2.7, length_l=0.05, at_model="AT2")
     params_at1 = material.MaterialParams.from_young_poisson(
         210000.0, 0.3, g_c=2.7, length_l=0.05, at_model="AT1")
     for name, build in meshes.items():
+        if only and name not in only:
+            continue
         rng = np.random.default_rng(1234)
         mesh = build()
         disc = assembly.Discretization(mesh)
@@ -208,7 +214,8 @@ def spd(case_name: str, scheme: str, max_each: int) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     sub = ap.add_subparsers(dest="cmd", required=True)
-    sub.add_parser("kat")
+    k = sub.add_parser("kat")
+    k.add_argument("only", nargs="*")
     r = sub.add_parser("run")
     r.add_argument("case")
     r.add_argument("scheme")
@@ -222,7 +229,7 @@ def main() -> None:
     a = ap.parse_args()
     t0 = time.time()
     if a.cmd == "kat":
-        kat()
+        kat(a.only)
     elif a.cmd == "run":
         snaps = [int(x) for x in a.snap.split(",") if x]
         run(a.case, a.scheme, a.steps, snaps, a.lin)
