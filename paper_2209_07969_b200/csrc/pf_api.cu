@@ -33,6 +33,7 @@ struct pf_handle {
   int *d_nlo = nullptr, *d_nhi = nullptr, *d_nst = nullptr;
   int *d_elo = nullptr, *d_ehi = nullptr, *d_est = nullptr;
   int2* d_tiles = nullptr;
+  int4 *d_nrow = nullptr, *d_erow = nullptr;
   int n_tiles = 0;
   // state
   double *u = nullptr, *d = nullptr, *dprev = nullptr;
@@ -59,6 +60,7 @@ struct pf_handle {
   double* d_scal = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
   int cg_grid = 1, cg_grid_evo = 1, sm_count = 0;
+  pfb::MarchGeom geom_mom{}, geom_evo{}, geom_apply{};
   long long l2_bytes = 0;
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
@@ -159,6 +161,7 @@ static void build_consts(pf_handle* h, double hx, double hy) {
   C.k = m.bulk_k;
   C.two_mu = 2.0 * m.mu;
   C.mu43 = 2.0 * m.mu * (1.0 - 1.0 / 3.0);
+  C.third = 1.0 / 3.0;
   C.eta = m.eta;
   C.gamma = m.gamma;
   C.src_base = m.g_c / (m.c_w * m.length_l);
@@ -177,6 +180,7 @@ extern "C" void pf_destroy(pf_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   void* ptrs[] = {h->d_nlo, h->d_nhi, h->d_nst, h->d_elo, h->d_ehi, h->d_est, h->d_tiles,
+                  h->d_nrow, h->d_erow,
                   h->u, h->d, h->dprev, h->trp, h->dev2, h->psi, h->psimax,
                   h->Ru, h->ru, h->xu, h->qu, h->p0u, h->p1u, h->dinvu, h->diagu, h->flags,
                   h->umask, h->Rd, h->rd, h->xd, h->qd, h->p0d, h->p1d, h->dinvd, h->diagd,
@@ -302,6 +306,15 @@ extern "C" pf_status pf_create(const pf_mesh* mesh, const pf_material* mat, cons
   CREATE_CUDA(up_int(&h->d_est, h->h_est));
   CREATE_CUDA(cudaMalloc((void**)&h->d_tiles, tiles.size() * sizeof(int2)));
   CREATE_CUDA(cudaMemcpy(h->d_tiles, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  {
+    std::vector<int4> nrow(ny + 1), erow(std::max(ny, 1));
+    for (int j = 0; j <= ny; ++j) nrow[j] = make_int4(h->h_nlo[j], h->h_nhi[j], h->h_nst[j], 0);
+    for (int j = 0; j < ny; ++j) erow[j] = make_int4(h->h_elo[j], h->h_ehi[j], h->h_est[j], 0);
+    CREATE_CUDA(cudaMalloc((void**)&h->d_nrow, nrow.size() * sizeof(int4)));
+    CREATE_CUDA(cudaMalloc((void**)&h->d_erow, erow.size() * sizeof(int4)));
+    CREATE_CUDA(cudaMemcpy(h->d_nrow, nrow.data(), nrow.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CREATE_CUDA(cudaMemcpy(h->d_erow, erow.data(), erow.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  }
   pfb::DMesh& dm = h->dm;
   dm.nx = nx; dm.ny = ny;
   dm.nlo = h->d_nlo; dm.nhi = h->d_nhi; dm.nst = h->d_nst;
@@ -312,6 +325,7 @@ extern "C" pf_status pf_create(const pf_mesh* mesh, const pf_material* mat, cons
   dm.dup_start = mesh->notch_row >= 0 ? (int)mesh->dup_start : 0;
   dm.n_nodes = h->n_nodes; dm.n_elems = h->n_elems;
   dm.n_tiles = h->n_tiles; dm.tiles = h->d_tiles;
+  dm.nrow = h->d_nrow; dm.erow = h->d_erow;
   build_consts(h, mesh->hx, mesh->hy);
   const size_t nn = h->n_nodes, ne = h->n_elems;
   pf_status s2 = PF_OK;
@@ -359,13 +373,13 @@ extern "C" pf_status pf_create(const pf_mesh* mesh, const pf_material* mat, cons
     h->err = "k_cg cannot be resident (occupancy 0)";
     return bail(PF_ERR_CUDA);
   }
-  // balanced persistent grid: the fewest CTAs that keep the per-CTA tile count minimal
-  auto balanced = [&](int resident) {
-    const int per = (h->n_tiles + resident - 1) / resident;
-    return std::max(1, (h->n_tiles + per - 1) / per);
-  };
-  h->cg_grid = balanced(occ * dev_sms);
-  h->cg_grid_evo = balanced(occ_evo * dev_sms);
+  // persistent grids: all resident warps march; unit shape from the resident warp count
+  const int wpc = pfb::NT / 32;
+  h->geom_mom = pfb::make_march_geom(nx, ny, occ * dev_sms * wpc);
+  h->geom_evo = pfb::make_march_geom(nx, ny, occ_evo * dev_sms * wpc);
+  h->geom_apply = pfb::make_march_geom(nx, ny, 4 * dev_sms * wpc);
+  h->cg_grid = std::max(1, std::min(occ * dev_sms, (h->geom_mom.n_units + wpc - 1) / wpc));
+  h->cg_grid_evo = std::max(1, std::min(occ_evo * dev_sms, (h->geom_evo.n_units + wpc - 1) / wpc));
   const size_t npart =
       std::max<size_t>((size_t)h->n_tiles, (size_t)std::max(h->cg_grid, h->cg_grid_evo)) * 4;
   CREATE_ALLOC(h->partials, npart);
@@ -563,6 +577,7 @@ static pfb::CgArgs cg_args(pf_handle* h, bool mom) {
   a.m = h->dm;
   a.C = h->C;
   a.ndof = mom ? 2LL * h->n_nodes : (long long)h->n_nodes;
+  a.g = mom ? h->geom_mom : h->geom_evo;
   a.d = h->d;
   a.flags = h->flags;
   a.b = h->b;
@@ -895,7 +910,8 @@ extern "C" pf_status pf_momentum_tangent_apply(pf_handle* h, const double* x, do
   PF_TRY(launch_mom_prepare(h, 1));  // branch flags and raw diagonal at the current u
   PF_TRY(h2d(h, h->p0u, x, 2 * (size_t)h->n_nodes));
   pfb::CgArgs a = cg_args(h, true);
-  pfb::k_apply<true><<<h->n_tiles, pfb::NT, 0, h->stream>>>(a, h->p0u);
+  a.g = h->geom_apply;
+  pfb::k_apply<true><<<(a.g.n_units + 7) / 8, pfb::NT, 0, h->stream>>>(a, h->p0u);
   PF_TRY(launched(h));
   PF_TRY(d2h(h, y, h->qu, 2 * (size_t)h->n_nodes));
   PF_TRY(d2h(h, diag, h->diagu, 2 * (size_t)h->n_nodes));
@@ -918,7 +934,8 @@ extern "C" pf_status pf_evolution_tangent_apply(pf_handle* h, int scheme, const 
   PF_TRY(launch_evo_prepare(h, 1, scheme));
   PF_TRY(h2d(h, h->p0d, x, (size_t)h->n_nodes));
   pfb::CgArgs a = cg_args(h, false);
-  pfb::k_apply<false><<<h->n_tiles, pfb::NT, 0, h->stream>>>(a, h->p0d);
+  a.g = h->geom_apply;
+  pfb::k_apply<false><<<(a.g.n_units + 7) / 8, pfb::NT, 0, h->stream>>>(a, h->p0d);
   PF_TRY(launched(h));
   PF_TRY(d2h(h, y, h->qd, (size_t)h->n_nodes));
   PF_TRY(d2h(h, diag, h->diagd, (size_t)h->n_nodes));

@@ -4,10 +4,10 @@
 // recursive residual satisfies ||r|| < rtol*||b||, z = D^-1 r, maxiter = 20 n, no breakdown test
 // (the reference's bounded matrix keeps constrained components at zero, assembly.py:299-308,
 // which the masked operator reproduces exactly).  Per iteration there are two grid barriers:
-//   phase A (tiles): p_k = z_k + beta p_{k-1} evaluated on the fly for tile+halo nodes (p is
-//                    double-buffered so neighbours read p_{k-1} while owners write p_k),
-//                    x += alpha_{k-1} p_{k-1} on owned nodes, q = A p_k (masked), partial p.q
-//   phase B (flat):  r -= alpha q, partials r.r and r.D^-1.r
+//   phase A (warp marching, pf_march.cuh): p_k = z_k + beta p_{k-1} evaluated on the fly for
+//                    every node a warp touches (p double-buffered so neighbours read p_{k-1}
+//                    while owners write p_k), q = A p_k (masked), partial p.q
+//   phase B (flat):  r -= alpha q, x += alpha p_k, partials r.r and r.D^-1.r
 // The SPD probe (K10, SURVEY.md §7 hard part 1) aborts at p.q <= 0.
 //
 // Latency structure: thread t owns node slot t of its tile (TX x TY = NT), so the owned node's
@@ -20,6 +20,9 @@
 namespace pfb {
 
 constexpr int NBORDER = 2 * HX + 2 * TY;  // halo ring slots around the TX x TY owned block
+#ifndef PFB_PHASEB_UNROLL
+#define PFB_PHASEB_UNROLL 2
+#endif
 #ifndef PFB_CG_MINB_MOM
 #define PFB_CG_MINB_MOM 2
 #endif
@@ -62,9 +65,14 @@ struct CgResult {
   double bnorm, rnorm;
 };
 
+struct MarchGeom {
+  int n_strips, rows_per_unit, n_row_blocks, n_units;
+};
+
 struct CgArgs {
   DMesh m;
   Consts C;
+  MarchGeom g;          // warp work units of the marching phase A (pf_march.cuh)
   long long ndof;        // flat length (2*n_nodes or n_nodes)
   const double* d;       // momentum: nodal d
   const uint8_t* flags;  // momentum: per-element tangent branch bits
@@ -296,6 +304,10 @@ __device__ __forceinline__ void phase_a_tile(const CgArgs& a, SM& S, int tile, b
   __syncthreads();
 }
 
+}  // namespace pfb
+#include "pf_march.cuh"
+namespace pfb {
+
 // partial k of CTA i lives at part[stride*i + k]; every CTA sums in the same fixed order
 template <int NV>
 __device__ __forceinline__ void grid_reduce(const double* part, int stride, double* bc,
@@ -320,25 +332,32 @@ __device__ __forceinline__ void grid_reduce(const double* part, int stride, doub
   for (int k = 0; k < NV; ++k) out[k] = bc[k];
 }
 
-// flat pass over double2 pairs: r -= alpha q (update), partials r.r and r.D^-1.r
-__device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, bool update, double& rr,
-                                        double& rz) {
-  constexpr int U = 4;
+// flat pass over double2 pairs: r -= alpha q and x += alpha p_k (update), partials r.r and
+// r.D^-1.r
+__device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, const double* pk,
+                                        bool update, double& rr, double& rz) {
+  constexpr int U = PFB_PHASEB_UNROLL;
   const long long n2 = a.ndof >> 1;
   const long long stride = (long long)gridDim.x * blockDim.x;
   double2* r2 = reinterpret_cast<double2*>(a.r);
+  double2* x2 = reinterpret_cast<double2*>(a.x);
   const double2* q2 = reinterpret_cast<const double2*>(a.q);
+  const double2* p2 = reinterpret_cast<const double2*>(pk);
   const double2* d2 = reinterpret_cast<const double2*>(a.dinv);
   for (long long base = (long long)blockIdx.x * blockDim.x + threadIdx.x; base < n2;
        base += U * stride) {
     // loads are issued unconditionally (clamped index) so the unrolled arrays stay in registers
-    double2 rv[U], qv[U], dv[U];
+    double2 rv[U], qv[U], dv[U], pv[U], xv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const long long i = min(base + u * stride, n2 - 1);
       rv[u] = __ldcg(r2 + i);
       dv[u] = __ldg(d2 + i);
-      qv[u] = update ? __ldcg(q2 + i) : make_double2(0.0, 0.0);
+      if (update) {
+        qv[u] = __ldcg(q2 + i);
+        pv[u] = __ldcg(p2 + i);
+        xv[u] = __ldcg(x2 + i);
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -348,6 +367,9 @@ __device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, bool upda
           rv[u].x -= alpha * qv[u].x;
           rv[u].y -= alpha * qv[u].y;
           r2[i] = rv[u];
+          xv[u].x += alpha * pv[u].x;
+          xv[u].y += alpha * pv[u].y;
+          x2[i] = xv[u];
         }
         rr += rv[u].x * rv[u].x + rv[u].y * rv[u].y;
         rz += rv[u].x * (dv[u].x * rv[u].x) + rv[u].y * (dv[u].y * rv[u].y);
@@ -360,27 +382,26 @@ __device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, bool upda
     if (update) {
       rv -= alpha * __ldcg(a.q + i);
       a.r[i] = rv;
+      a.x[i] = __ldcg(a.x + i) + alpha * __ldcg(pk + i);
     }
     rr += rv * rv;
     rz += rv * (__ldg(a.dinv + i) * rv);
   }
 }
 
-template <bool MOM>
 struct CgSmem {
-  using SM = typename std::conditional<MOM, SmemMomA, SmemEvoA>::type;
-  SM t;
   double red[NT / 32 * 2];
   double bc[4];
 };
 
 template <bool MOM>
 __global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k_cg(CgArgs a) {
-  __shared__ CgSmem<MOM> S;
+  __shared__ CgSmem S;
   cg::grid_group grid = cg::this_grid();
+  const int gwarp = blockIdx.x * (NT / 32) + (threadIdx.x >> 5), nwarps = gridDim.x * (NT / 32);
   double* part = a.partials;
   double rr = 0.0, rz = 0.0;
-  phase_b(a, 0.0, false, rr, rz);  // ||b||^2 and b.D^-1.b (r = b on entry)
+  phase_b(a, 0.0, nullptr, false, rr, rz);  // ||b||^2 and b.D^-1.b (r = b on entry)
   {
     double v[2] = {rr, rz};
     block_sum<2>(v, S.red);
@@ -407,8 +428,8 @@ __global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k
       double* pnew = (k & 1) ? a.p1 : a.p0;
       const double* pold = (k & 1) ? a.p0 : a.p1;
       double pq = 0.0;
-      for (int tile = blockIdx.x; tile < a.m.n_tiles; tile += gridDim.x)
-        phase_a_tile<MOM, false>(a, S.t, tile, first, beta, alpha, pold, pnew, pq);
+      for (int u = gwarp; u < a.g.n_units; u += nwarps)
+        march_unit<MOM, false>(a, a.g, u, first, beta, pold, pnew, pq);
       {
         double v[1] = {pq};
         block_sum<1>(v, S.red);
@@ -422,7 +443,7 @@ __global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k
       rho_prev = rho;
       rr = 0.0;
       rz = 0.0;
-      phase_b(a, alpha, true, rr, rz);
+      phase_b(a, alpha, pnew, true, rr, rz);
       {
         double v[2] = {rr, rz};
         block_sum<2>(v, S.red);
@@ -435,16 +456,11 @@ __global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k
       ++k;
     }
   }
-  if (status != CG_INDEFINITE) {  // x += alpha_{k-1} p_{k-1}; target += x
-    const double* plast = (k & 1) ? a.p0 : a.p1;
+  if (status != CG_INDEFINITE && a.target) {  // x is complete: target += x
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.ndof;
-         i += stride) {
-      double xv = __ldcg(a.x + i);
-      if (k > 0) xv += alpha * __ldcg(plast + i);
-      a.x[i] = xv;
-      if (a.target) a.target[i] += xv;
-    }
+         i += stride)
+      a.target[i] += __ldcg(a.x + i);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.result->iters = k;
@@ -454,12 +470,12 @@ __global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k
   }
 }
 
-// y = A x (unmasked) at the current state: one CTA per tile
+// y = A x (unmasked) at the current state: one warp per marching unit
 template <bool MOM>
 __global__ void __launch_bounds__(NT) k_apply(CgArgs a, const double* x) {
-  __shared__ typename CgSmem<MOM>::SM S;
+  const int u = blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
   double pq = 0.0;
-  phase_a_tile<MOM, true>(a, S, blockIdx.x, true, 0.0, 0.0, x, nullptr, pq);
+  if (u < a.g.n_units) march_unit<MOM, true>(a, a.g, u, true, 0.0, x, nullptr, pq);
 }
 
 }  // namespace pfb

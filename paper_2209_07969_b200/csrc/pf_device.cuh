@@ -39,6 +39,8 @@ struct DMesh {
   int n_nodes, n_elems;
   int n_tiles;
   const int2* tiles;  // active tile coordinates (tile column, tile row)
+  const int4* nrow;   // [ny+1] packed (lo, hi, start, 0) of node rows
+  const int4* erow;   // [ny]   packed (lo, hi, start, 0) of cell rows
 };
 
 struct Consts {
@@ -50,6 +52,7 @@ struct Consts {
   double Nw[4][4];    // N[g][a] * wdet
   double lap[4][4];   // grad_w * sum_g gradN_a . gradN_b * wdet
   double mu, k, two_mu, mu43;  // mu43 = 2 mu (1 - 1/3): tangent normal diagonal
+  double third;                // 1/3 (tangent apply only; residuals divide like the reference)
   double eta, gamma, src_base, grad_w, psi_crit, d_cap;
   int at2;
 };

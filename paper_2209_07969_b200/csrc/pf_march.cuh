@@ -1,0 +1,276 @@
+// pf_march.cuh — barrier-free register-marching phase A of the persistent PCG.
+//
+// A work unit is (strip, row block): a warp owns TXW = 30 node columns (lanes 1..30; lanes 0
+// and 31 carry the halo columns) and marches up node rows r0-1 .. r1 keeping two node rows in
+// registers.  Lane l evaluates cell (col_l, cj) from its own and lane l+1's nodes (shuffle),
+// and each node's four cell contributions arrive in the reference's element order
+//     ((c2 of (i-1,j-1) + c3 of (i,j-1)) + c1 of (i-1,j)) + c0 of (i,j)
+// (np.add.at / COO->CSR order, assembly.py:188, :195-197), so results are bit-identical to the
+// tile formulation.  No shared memory, no CTA barriers; the next row's loads are issued before
+// the current row's FP64 work, so every warp keeps a row of loads in flight.  The x update of
+// the CG moved to the streaming phase B; phase A only reads p_{k-1}, r, D^-1 (and d) and writes
+// p_k and q.
+//
+// The slit (meshing.py:126-138): node row R holds lower-face nodes, and for columns in
+// [notch_lo, notch_hi) a second, upper-face set (the duplicates) used as bottom corners by
+// cell row R.  Rows with variable extents (L-panel, meshing.py:179-192) come from the row
+// tables (broadcast __ldg loads, L1-resident).
+#pragma once
+
+namespace pfb {
+
+constexpr int TXW = 30;  // owned columns per warp strip
+
+__device__ __forceinline__ double shfl_dn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double shfl_up(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double2 shfl_dn(double2 v) {
+  return make_double2(shfl_dn(v.x), shfl_dn(v.y));
+}
+__device__ __forceinline__ double2 shfl_up(double2 v) {
+  return make_double2(shfl_up(v.x), shfl_up(v.y));
+}
+
+// Element tangent-vector product K_e(u, d) p_e on a uniform cell, grouped by the tensor-product
+// structure: each derivative takes two distinct values per cell, and the back-projection sums
+// Gauss-point pairs first (~130 FP64 operations per cell, no division).
+__device__ __forceinline__ void mom_cell_fast(const Consts& C, const double2 (&pc)[4],
+                                              const double (&dc)[4], unsigned flags,
+                                              double2 (&f)[4]) {
+  const double bx = pc[1].x - pc[0].x, tx = pc[2].x - pc[3].x;
+  const double by = pc[1].y - pc[0].y, ty = pc[2].y - pc[3].y;
+  const double lx = pc[3].x - pc[0].x, rx = pc[2].x - pc[1].x;
+  const double ly = pc[3].y - pc[0].y, ry = pc[2].y - pc[1].y;
+  const double uxx_lo = C.Px * bx + C.Mx * tx, uxx_hi = C.Mx * bx + C.Px * tx;
+  const double uyx_lo = C.Px * by + C.Mx * ty, uyx_hi = C.Mx * by + C.Px * ty;
+  const double uxy_l = C.Py * lx + C.My * rx, uxy_r = C.My * lx + C.Py * rx;
+  const double uyy_l = C.Py * ly + C.My * ry, uyy_r = C.My * ly + C.Py * ry;
+  const double exx[4] = {uxx_lo, uxx_lo, uxx_hi, uxx_hi};
+  const double eyy[4] = {uyy_l, uyy_r, uyy_r, uyy_l};
+  const double gxy[4] = {uxy_l + uyx_lo, uxy_r + uyx_lo, uxy_r + uyx_hi, uxy_l + uyx_hi};
+  double sxx[4], syy[4], sxy[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const double dg = C.N[g][0] * dc[0] + C.N[g][1] * dc[1] + C.N[g][2] * dc[2] +
+                      C.N[g][3] * dc[3];
+    const double om = 1.0 - dg;
+    const double gg = om * om + C.eta;
+    const double tr = exx[g] + eyy[g];
+    const double a = gg * C.two_mu;
+    const double kv = ((flags >> g) & 1u) ? gg * C.k : C.k;
+    const double t3 = tr * C.third;
+    sxx[g] = a * (exx[g] - t3) + kv * tr;
+    syy[g] = a * (eyy[g] - t3) + kv * tr;
+    sxy[g] = (gg * C.mu) * gxy[g];
+  }
+  const double xx01 = sxx[0] + sxx[1], xx23 = sxx[2] + sxx[3];
+  const double yy03 = syy[0] + syy[3], yy12 = syy[1] + syy[2];
+  const double xy01 = sxy[0] + sxy[1], xy23 = sxy[2] + sxy[3];
+  const double xy03 = sxy[0] + sxy[3], xy12 = sxy[1] + sxy[2];
+  const double axx = C.Pxw * xx01 + C.Mxw * xx23, bxx = C.Mxw * xx01 + C.Pxw * xx23;
+  const double cyy = C.Pyw * yy03 + C.Myw * yy12, dyy = C.Myw * yy03 + C.Pyw * yy12;
+  const double axy = C.Pxw * xy01 + C.Mxw * xy23, bxy = C.Mxw * xy01 + C.Pxw * xy23;
+  const double cxy = C.Pyw * xy03 + C.Myw * xy12, dxy = C.Myw * xy03 + C.Pyw * xy12;
+  f[0] = make_double2(-axx - cxy, -cyy - axy);
+  f[1] = make_double2(axx - dxy, -dyy + axy);
+  f[2] = make_double2(bxx + dxy, dyy + bxy);
+  f[3] = make_double2(-bxx + cxy, cyy - bxy);
+}
+
+template <bool MOM>
+struct RawNode {
+  using T = typename Node<MOM>::T;
+  T r, di, po;
+  double d;
+  int id;
+};
+
+template <bool MOM, bool APPLY>
+__device__ __forceinline__ void fetch_node(const CgArgs& a, const double* __restrict__ pold,
+                                           bool first, int id, RawNode<MOM>& w) {
+  using N_ = Node<MOM>;
+  w.id = id;
+  if (id >= 0) {
+    if (APPLY) {
+      w.po = N_::ld_ro(pold, id);
+    } else {
+      w.r = N_::ld_cg(a.r, id);
+      w.di = N_::ld_ro(a.dinv, id);
+      if (!first) w.po = N_::ld_cg(pold, id);
+    }
+    if constexpr (MOM) w.d = __ldg(a.d + id);
+  }
+}
+
+// p_k = D^-1 r + beta p_{k-1}; the owner stores it
+template <bool MOM, bool APPLY>
+__device__ __forceinline__ typename Node<MOM>::T finish_node(const RawNode<MOM>& w, bool first,
+                                                             double beta, bool own,
+                                                             double* __restrict__ pnew) {
+  using N_ = Node<MOM>;
+  if (w.id < 0) return N_::zero();
+  if (APPLY) return w.po;
+  typename N_::T p = N_::mul(w.di, w.r);
+  if (!first) p = N_::axpy(beta, w.po, p);
+  if (own) N_::st(pnew, w.id, p);
+  return p;
+}
+
+template <bool MOM, bool APPLY>
+__device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, int unit,
+                                           bool first, double beta,
+                                           const double* __restrict__ pold,
+                                           double* __restrict__ pnew, double& pq) {
+  using N_ = Node<MOM>;
+  using T = typename N_::T;
+  const DMesh& m = a.m;
+  const Consts& C = a.C;
+  const int lane = threadIdx.x & 31;
+  const int strip = unit % G.n_strips;
+  const int r0 = (unit / G.n_strips) * G.rows_per_unit;
+  const int r1 = min(r0 + G.rows_per_unit, m.ny + 1);
+  const int col = strip * TXW - 1 + lane;
+  const bool lane_own = lane >= 1 && lane <= TXW;
+  const int R = m.notch_row;
+  const bool dupcol = R >= 0 && col >= m.notch_lo && col < m.notch_hi;
+  const int dupid = dupcol ? m.dup_start + (col - m.notch_lo) : -1;
+  auto nid = [&](int j) -> int {
+    if (j < 0 || j > m.ny) return -1;
+    const int4 rw = __ldg(m.nrow + j);
+    return (col >= rw.x && col < rw.y) ? rw.z + (col - rw.x) : -1;
+  };
+
+  // lower row (cj) state
+  T p_lo, di_lo, p_dup = N_::zero(), di_dup = N_::zero();
+  double d_lo, d_dup = 0.0;
+  int id_lo, id_dup = -1;
+  bool lo_slit;
+  RawNode<MOM> w;
+  {
+    fetch_node<MOM, APPLY>(a, pold, first, nid(r0 - 1), w);
+    p_lo = finish_node<MOM, APPLY>(w, first, beta, false, pnew);
+    di_lo = w.di;
+    d_lo = MOM ? w.d : 0.0;
+    id_lo = w.id;
+    lo_slit = (r0 - 1 == R);
+    if (lo_slit) {
+      RawNode<MOM> wd;
+      fetch_node<MOM, APPLY>(a, pold, first, dupid, wd);
+      p_dup = finish_node<MOM, APPLY>(wd, first, beta, false, pnew);
+      di_dup = wd.di;
+      d_dup = MOM ? wd.d : 0.0;
+      id_dup = wd.id;
+    }
+  }
+  fetch_node<MOM, APPLY>(a, pold, first, nid(r0), w);  // upper row, in flight
+  T acc_lo = N_::zero();
+  for (int cj = r0 - 1; cj < r1; ++cj) {
+    const int jh = cj + 1;
+    const bool hi_own = lane_own && jh >= r0 && jh < r1;
+    const T p_hi = finish_node<MOM, APPLY>(w, first, beta, hi_own, pnew);
+    const T di_hi = w.di;
+    const double d_hi = MOM ? w.d : 0.0;
+    const int id_hi = w.id;
+    const bool hi_slit = (jh == R);
+    T p_hdup = N_::zero(), di_hdup = N_::zero();
+    double d_hdup = 0.0;
+    int id_hdup = -1;
+    if (hi_slit) {  // warp-uniform
+      RawNode<MOM> wd;
+      fetch_node<MOM, APPLY>(a, pold, first, dupid, wd);
+      p_hdup = finish_node<MOM, APPLY>(wd, first, beta, hi_own, pnew);
+      di_hdup = wd.di;
+      d_hdup = MOM ? wd.d : 0.0;
+      id_hdup = wd.id;
+    }
+    if (jh + 1 <= r1) fetch_node<MOM, APPLY>(a, pold, first, nid(jh + 1), w);  // prefetch
+    // ---- cell (col, cj)
+    const bool use_dup = lo_slit && dupcol;
+    const T b0 = use_dup ? p_dup : p_lo;
+    const T b1 = shfl_dn(b0);
+    const T t2 = shfl_dn(p_hi);
+    int eid = -1;
+    if (cj >= 0 && cj < m.ny) {
+      const int4 er = __ldg(m.erow + cj);
+      if (lane < 31 && col >= er.x && col < er.y) eid = er.z + (col - er.x);
+    }
+    T f[4];
+    if constexpr (MOM) {
+      const double e0 = use_dup ? d_dup : d_lo;
+      const double e1 = shfl_dn(e0);
+      const double e2 = shfl_dn(d_hi);
+      f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
+      if (eid >= 0) {
+        const double2 pc[4] = {b0, b1, t2, p_hi};
+        const double dc[4] = {e0, e1, e2, d_hi};
+        mom_cell_fast(C, pc, dc, __ldg(a.flags + eid), f);
+      }
+    } else {
+      f[0] = f[1] = f[2] = f[3] = 0.0;
+      if (eid >= 0) {
+        const double pc[4] = {b0, b1, t2, p_hi};
+        double bq[4];
+        load4(a.b, eid, bq);
+        evo_cell_apply(C, pc, bq, f);
+      }
+    }
+    // ---- node row cj complete: ((c2 + c3) + c1 from the left) + c0 own
+    const T c1l = shfl_up(f[1]);
+    const T c2l = shfl_up(f[2]);
+    if (lane_own && cj >= r0) {
+      if (use_dup) {
+        if (id_lo >= 0) {  // lower face: cells below only
+          T qv = acc_lo;
+          if (!APPLY) {
+            qv = N_::mask(qv, di_lo);
+            pq += N_::dot(p_lo, qv);
+          }
+          N_::st(a.q, id_lo, qv);
+        }
+        if (id_dup >= 0) {  // upper face: cells above only
+          T qv = add_t(c1l, f[0]);
+          if (!APPLY) {
+            qv = N_::mask(qv, di_dup);
+            pq += N_::dot(p_dup, qv);
+          }
+          N_::st(a.q, id_dup, qv);
+        }
+      } else if (id_lo >= 0) {
+        T qv = add_t(add_t(acc_lo, c1l), f[0]);
+        if (!APPLY) {
+          qv = N_::mask(qv, di_lo);
+          pq += N_::dot(p_lo, qv);
+        }
+        N_::st(a.q, id_lo, qv);
+      }
+    }
+    acc_lo = add_t(c2l, f[3]);
+    p_lo = p_hi;
+    di_lo = di_hi;
+    d_lo = d_hi;
+    id_lo = id_hi;
+    lo_slit = hi_slit;
+    if (hi_slit) {
+      p_dup = p_hdup;
+      di_dup = di_hdup;
+      d_dup = d_hdup;
+      id_dup = id_hdup;
+    }
+  }
+}
+
+// host-side choice of the unit shape: enough units for every resident warp, but at least
+// 4 owned rows per unit so the halo rows stay a modest overhead
+inline MarchGeom make_march_geom(int nx, int ny, int resident_warps) {
+  MarchGeom g;
+  g.n_strips = (nx + 1 + TXW - 1) / TXW;
+  const long long strip_rows = (long long)g.n_strips * (ny + 1);
+  int rows = (int)((strip_rows + resident_warps - 1) / resident_warps);
+  rows = rows < 4 ? 4 : rows;
+  if (rows > ny + 1) rows = ny + 1;
+  g.rows_per_unit = rows;
+  g.n_row_blocks = (ny + 1 + rows - 1) / rows;
+  g.n_units = g.n_strips * g.n_row_blocks;
+  return g;
+}
+
+}  // namespace pfb

@@ -8,14 +8,14 @@ reference by tests/test_oracle_golden.py) on every golden case and records, per 
 n_stag of every variant.  tests/test_gpu_solver.py uses the spread as the "+-N where the
 reference's own iterative tolerance allows" band of BASELINE.json's north star.
 
-Variants (all mathematically identical to the reference):
-  cg          the reference's own lin_method="cg" (Jacobi-PCG, rtol 1e-12)
-  exact       exact uniform-cell geometry instead of coordinate-derived Jacobians
-  exact_diff  exact geometry + strains from edge jumps (u1-u0) instead of B.u products
-  pair        pairwise instead of sequential per-node accumulation
-  gpu_like    exact + diff + element-Laplacian gradient term + pairwise + CG
+Variants: the full factorial of six exact-arithmetic-equivalent knobs (KNOBS below): geometry
+from coordinates or exact constants, strains as B.u products or edge jumps, the phase-field
+gradient term as gradient or element-Laplacian, per-node accumulation sequential or pairwise,
+internal-force back-projection as one einsum or Gauss-point-pair grouped, and the linear
+solver direct (SuperLU) or the reference's own lin_method="cg".  The crack side taken by the
+symmetric tension test ("branch") is recorded too.
 
-    OMP_NUM_THREADS=1 python tests/golden/make_sensitivity.py tension16 ST
+    OMP_NUM_THREADS=1 python tests/golden/make_sensitivity.py tension16 ST [steps|-] [max_variants]
 """
 
 from __future__ import annotations
@@ -34,29 +34,63 @@ sys.path.insert(0, ROOT)
 from oracle.phasefield_oracle import oracle_api  # noqa: E402
 from paper_2209_07969_b200 import configs as C  # noqa: E402
 
-VARIANTS = {
-    "cg": dict(lin_method="cg"),
-    "exact": dict(geometry="exact"),
-    "exact_diff": dict(geometry="exact", strain="differences"),
-    "pair": dict(scatter="pairwise"),
-    "gpu_like": dict(geometry="exact", strain="differences", gradterm="laplacian",
-                     scatter="pairwise", lin_method="cg"),
+KNOBS = {
+    "geometry": ("coords", "exact"),
+    "strain": ("products", "differences"),
+    "gradterm": ("gradient", "laplacian"),
+    "scatter": ("sequential", "pairwise"),
+    "backproj": ("einsum", "grouped"),
+    "lin_method": ("direct", "cg"),
 }
 
 
-def run_variant(case: str, scheme: str, variant: str, steps: int | None = None) -> list:
-    pb = C.setup(C.get_case(case), oracle_api(**VARIANTS[variant]))
-    return [r.n_stag for r in C.run(pb, scheme, n_steps=steps)]
+def factorial(max_variants: int | None = None) -> dict:
+    """All non-default knob combinations (the default one is the pinned oracle itself)."""
+    import itertools
+
+    keys = list(KNOBS)
+    out = {}
+    for combo in itertools.product(*(range(len(KNOBS[k])) for k in keys)):
+        if not any(combo):
+            continue
+        kw = {k: KNOBS[k][c] for k, c in zip(keys, combo) if c}
+        out["+".join(f"{k}={v}" for k, v in kw.items())] = kw
+    if max_variants is not None:  # deterministic thinning: keep every k-th combination
+        names = list(out)
+        step = max(1, len(names) // max_variants)
+        out = {n: out[n] for n in names[::step][:max_variants]}
+    return out
+
+
+VARIANTS = factorial()
+
+
+def run_variant(case: str, scheme: str, kw: dict, steps: int | None = None) -> tuple:
+    pb = C.setup(C.get_case(case), oracle_api(**kw))
+    stag = [r.n_stag for r in C.run(pb, scheme, n_steps=steps)]
+    branch = None
+    cs = C.get_case(case)
+    if cs.loading == "tension" and cs.mesh[0] == "notched":
+        n = cs.mesh[1]
+        d = pb.state.d
+        below = d[(n // 2 - 1) * (n + 1):(n // 2) * (n + 1)].mean()
+        above = d[(n // 2 + 1) * (n + 1):(n // 2 + 2) * (n + 1)].mean()
+        branch = "below" if below > above else ("above" if above > below else "symmetric")
+    return stag, branch
 
 
 def main() -> None:
     case, scheme = sys.argv[1], sys.argv[2]
-    steps = int(sys.argv[3]) if len(sys.argv) > 3 else None
+    steps = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3] != "-" else None
+    maxv = int(sys.argv[4]) if len(sys.argv) > 4 else None
+    variants = factorial(maxv)
     t0 = time.time()
-    out = {v: run_variant(case, scheme, v, steps) for v in VARIANTS}
+    stag, branch = {}, {}
+    for name, kw in variants.items():
+        stag[name], branch[name] = run_variant(case, scheme, kw, steps)
     path = os.path.join(HERE, f"sens_{case}_{scheme}.json")
     with open(path, "w") as f:
-        json.dump({"case": case, "scheme": scheme, "n_stag": out,
+        json.dump({"case": case, "scheme": scheme, "n_stag": stag, "branch": branch,
                    "seconds": round(time.time() - t0, 1)}, f)
     print("wrote", path, round(time.time() - t0, 1), "s")
 
