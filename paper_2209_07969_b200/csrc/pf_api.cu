@@ -60,7 +60,17 @@ struct pf_handle {
   double* d_scal = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
   int cg_grid = 1, cg_grid_evo = 1, sm_count = 0;
+  size_t cg_dyn_smem = 0;
   pfb::MarchGeom geom_mom{}, geom_evo{}, geom_apply{};
+  // split-phase PCG (pf_cg.cuh: k_cg_a / k_cg_b chained in CUDA graphs)
+  bool split = false;
+  int chunk = 32;
+  pfb::MarchGeom geom_a_mom{}, geom_a_evo{};
+  int gridA_mom = 1, gridA_evo = 1, gridB = 1;
+  pfb::CgCtl* d_ctl = nullptr;
+  pfb::CgCtl* h_ctl = nullptr;  // pinned
+  double *partA = nullptr, *partB = nullptr;
+  cudaGraphExec_t graphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [mom][probe]
   long long l2_bytes = 0;
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
@@ -187,6 +197,13 @@ extern "C" void pf_destroy(pf_handle* h) {
                   h->b, h->pmask, h->partials, h->scratch, h->d_idx, h->flushbuf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto& row : h->graphs)
+    for (auto& g : row)
+      if (g) cudaGraphExecDestroy(g);
+  if (h->d_ctl) cudaFree(h->d_ctl);
+  if (h->partA) cudaFree(h->partA);
+  if (h->partB) cudaFree(h->partB);
+  if (h->h_ctl) cudaFreeHost(h->h_ctl);
   if (h->h_cgres) cudaFreeHost(h->h_cgres);
   if (h->h_scal) cudaFreeHost(h->h_scal);
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -364,7 +381,13 @@ extern "C" pf_status pf_create(const pf_mesh* mesh, const pf_material* mat, cons
   int dev_sms = 0, occ = 0, occ_evo = 0, l2 = 0;
   CREATE_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
   CREATE_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
-  CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pfb::k_cg<true>, pfb::NT, 0));
+  const size_t ring_smem = PFB_USE_RING ? sizeof(pfb::MomRing) * (pfb::NT / 32) : 0;
+  h->cg_dyn_smem = ring_smem;
+  if (ring_smem > 48 * 1024)
+    CREATE_CUDA(cudaFuncSetAttribute(pfb::k_cg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ring_smem));
+  CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pfb::k_cg<true>, pfb::NT,
+                                                            ring_smem));
   CREATE_CUDA(
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_evo, pfb::k_cg<false>, pfb::NT, 0));
   h->sm_count = dev_sms;
@@ -380,6 +403,25 @@ extern "C" pf_status pf_create(const pf_mesh* mesh, const pf_material* mat, cons
   h->geom_apply = pfb::make_march_geom(nx, ny, 4 * dev_sms * wpc);
   h->cg_grid = std::max(1, std::min(occ * dev_sms, (h->geom_mom.n_units + wpc - 1) / wpc));
   h->cg_grid_evo = std::max(1, std::min(occ_evo * dev_sms, (h->geom_evo.n_units + wpc - 1) / wpc));
+  {  // split-phase PCG geometry: phase A one wave of resident CTAs, phase B 4 CTAs per SM
+    const char* mode = getenv("PFB200_CG");  // "split": graph-chained phase kernels (A/B tests)
+    h->split = mode && std::string(mode) == "split";
+    const char* ch = getenv("PFB200_CG_CHUNK");
+    if (ch) h->chunk = std::max(1, atoi(ch));
+    int oa = 0, oe = 0;
+    CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, pfb::k_cg_a<true>, pfb::NT, 0));
+    CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oe, pfb::k_cg_a<false>, pfb::NT, 0));
+    h->geom_a_mom = pfb::make_march_geom(nx, ny, std::max(oa, 1) * dev_sms * wpc);
+    h->geom_a_evo = pfb::make_march_geom(nx, ny, std::max(oe, 1) * dev_sms * wpc);
+    h->gridA_mom = (h->geom_a_mom.n_units + wpc - 1) / wpc;
+    h->gridA_evo = (h->geom_a_evo.n_units + wpc - 1) / wpc;
+    h->gridB = 4 * dev_sms;
+    CREATE_CUDA(cudaMalloc((void**)&h->d_ctl, sizeof(pfb::CgCtl)));
+    CREATE_CUDA(cudaMallocHost((void**)&h->h_ctl, sizeof(pfb::CgCtl)));
+    CREATE_CUDA(cudaMalloc((void**)&h->partA,
+                           sizeof(double) * pfb::CG_SLOTS * std::max(h->gridA_mom, h->gridA_evo)));
+    CREATE_CUDA(cudaMalloc((void**)&h->partB, sizeof(double) * (pfb::CG_SLOTS + 1) * h->gridB * 2));
+  }
   const size_t npart =
       std::max<size_t>((size_t)h->n_tiles, (size_t)std::max(h->cg_grid, h->cg_grid_evo)) * 4;
   CREATE_ALLOC(h->partials, npart);
@@ -594,9 +636,33 @@ static pfb::CgArgs cg_args(pf_handle* h, bool mom) {
   return a;
 }
 
-// one persistent PCG solve; returns the CG status
-static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
-                        long long* iters) {
+static pf_status cg_account(pf_handle* h, bool mom, long long iters, float ms) {
+  const double nfree_u = 2.0 * h->n_nodes - (double)h->cons_key.size();
+  const double nfree_d = (double)h->n_nodes - (double)h->n_pinned;
+  if (mom) {
+    h->acc.cg_iters_u += iters;
+    h->acc.cg_dofiters_u += (double)iters * nfree_u;
+    h->acc.kernel_ms_u += ms;
+    h->acc.cg_launches_u += 1;
+  } else {
+    h->acc.cg_iters_d += iters;
+    h->acc.cg_dofiters_d += (double)iters * nfree_d;
+    h->acc.kernel_ms_d += ms;
+    h->acc.cg_launches_d += 1;
+  }
+  return PF_OK;
+}
+
+static pf_status cg_status(pf_handle* h, int status, long long iters) {
+  if (status == pfb::CG_MAXITER)
+    return fail(h, PF_ERR_SINGULAR, "cg failed to converge (info=" + std::to_string(iters) + ")");
+  if (status == pfb::CG_NAN) return fail(h, PF_ERR_SINGULAR, "cg produced a non-finite residual");
+  return PF_OK;
+}
+
+// one persistent PCG solve (single cooperative launch)
+static pf_status run_cg_persistent(pf_handle* h, bool mom, double* target, bool probe,
+                                   int* status, long long* iters) {
   pfb::CgArgs a = cg_args(h, mom);
   a.target = target;
   a.probe = probe ? 1 : 0;
@@ -604,7 +670,8 @@ static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int*
   const void* fn = mom ? (const void*)pfb::k_cg<true> : (const void*)pfb::k_cg<false>;
   const int grid = mom ? h->cg_grid : h->cg_grid_evo;
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
-  PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(pfb::NT), args, 0, h->stream));
+  PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(pfb::NT), args,
+                                      mom ? h->cg_dyn_smem : 0, h->stream));
   PF_TRY(launched(h));
   PF_CUDA(cudaEventRecord(h->ev1, h->stream));
   PF_CUDA(cudaStreamSynchronize(h->stream));
@@ -612,23 +679,85 @@ static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int*
   PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   *status = h->h_cgres->status;
   *iters = h->h_cgres->iters;
-  const double nfree_u = 2.0 * h->n_nodes - (double)h->cons_key.size();
-  const double nfree_d = (double)h->n_nodes - (double)h->n_pinned;
-  if (mom) {
-    h->acc.cg_iters_u += *iters;
-    h->acc.cg_dofiters_u += (double)*iters * nfree_u;
-    h->acc.kernel_ms_u += ms;
-    h->acc.cg_launches_u += 1;
-  } else {
-    h->acc.cg_iters_d += *iters;
-    h->acc.cg_dofiters_d += (double)*iters * nfree_d;
-    h->acc.kernel_ms_d += ms;
-    h->acc.cg_launches_d += 1;
+  cg_account(h, mom, *iters, ms);
+  return cg_status(h, *status, *iters);
+}
+
+static pfb::SplitArgs split_args(pf_handle* h, bool mom, bool probe) {
+  pfb::SplitArgs s{};
+  s.c = cg_args(h, mom);
+  s.c.g = mom ? h->geom_a_mom : h->geom_a_evo;
+  s.c.probe = probe ? 1 : 0;
+  s.ctl = h->d_ctl;
+  s.partA = h->partA;
+  s.partB = h->partB;
+  s.gridA = mom ? h->gridA_mom : h->gridA_evo;
+  s.gridB = h->gridB;
+  return s;
+}
+
+// a CUDA graph of `chunk` iterations (phase A, phase B) + the base advance, cached per handle
+static pf_status chunk_graph(pf_handle* h, bool mom, bool probe, cudaGraphExec_t* out) {
+  cudaGraphExec_t& g = h->graphs[mom ? 1 : 0][probe ? 1 : 0];
+  if (!g) {
+    pfb::SplitArgs s = split_args(h, mom, probe);
+    cudaGraph_t graph;
+    PF_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    for (int kl = 0; kl < h->chunk; ++kl) {
+      if (mom) {
+        pfb::k_cg_a<true><<<s.gridA, pfb::NT, 0, h->stream>>>(s, kl);
+        pfb::k_cg_b<true><<<s.gridB, pfb::NT, 0, h->stream>>>(s, kl);
+      } else {
+        pfb::k_cg_a<false><<<s.gridA, pfb::NT, 0, h->stream>>>(s, kl);
+        pfb::k_cg_b<false><<<s.gridB, pfb::NT, 0, h->stream>>>(s, kl);
+      }
+    }
+    pfb::k_cg_advance<<<1, 1, 0, h->stream>>>(h->d_ctl, h->chunk);
+    PF_CUDA(cudaStreamEndCapture(h->stream, &graph));
+    PF_CUDA(cudaGraphInstantiate(&g, graph, 0));
+    PF_CUDA(cudaGraphDestroy(graph));
   }
-  if (*status == pfb::CG_MAXITER)
-    return fail(h, PF_ERR_SINGULAR, "cg failed to converge (info=" + std::to_string(*iters) + ")");
-  if (*status == pfb::CG_NAN) return fail(h, PF_ERR_SINGULAR, "cg produced a non-finite residual");
+  *out = g;
   return PF_OK;
+}
+
+static pf_status run_cg_split(pf_handle* h, bool mom, double* target, bool probe, int* status,
+                              long long* iters) {
+  pfb::SplitArgs s = split_args(h, mom, probe);
+  cudaGraphExec_t g;
+  PF_TRY(chunk_graph(h, mom, probe, &g));
+  PF_CUDA(cudaEventRecord(h->ev0, h->stream));
+  PF_CUDA(cudaMemsetAsync(h->d_ctl, 0, sizeof(pfb::CgCtl), h->stream));
+  if (mom) pfb::k_cg_init<true><<<s.gridB, pfb::NT, 0, h->stream>>>(s);
+  else pfb::k_cg_init<false><<<s.gridB, pfb::NT, 0, h->stream>>>(s);
+  PF_TRY(launched(h));
+  for (;;) {
+    PF_CUDA(cudaGraphLaunch(g, h->stream));
+    h->acc.launches += 2 * h->chunk + 1;
+    PF_CUDA(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(pfb::CgCtl), cudaMemcpyDeviceToHost,
+                            h->stream));
+    PF_CUDA(cudaStreamSynchronize(h->stream));
+    if (h->h_ctl->done) break;
+  }
+  *status = h->h_ctl->status;
+  *iters = h->h_ctl->iters;
+  if (*status == pfb::CG_CONVERGED && target) {
+    const long long n = s.c.ndof;
+    pfb::k_cg_finish<<<4 * h->sm_count, 256, 0, h->stream>>>(target, s.c.x, n);
+    PF_TRY(launched(h));
+  }
+  PF_CUDA(cudaEventRecord(h->ev1, h->stream));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  cg_account(h, mom, *iters, ms);
+  return cg_status(h, *status, *iters);
+}
+
+static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
+                        long long* iters) {
+  return h->split ? run_cg_split(h, mom, target, probe, status, iters)
+                  : run_cg_persistent(h, mom, target, probe, status, iters);
 }
 
 // ------------------------------------------------------------------------------------------

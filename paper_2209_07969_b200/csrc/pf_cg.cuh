@@ -27,7 +27,7 @@ constexpr int NBORDER = 2 * HX + 2 * TY;  // halo ring slots around the TX x TY 
 #define PFB_CG_MINB_MOM 2
 #endif
 #ifndef PFB_CG_MINB_EVO
-#define PFB_CG_MINB_EVO 3
+#define PFB_CG_MINB_EVO 2
 #endif
 
 struct SmemMomA {
@@ -109,6 +109,10 @@ struct Node<true> {
   __device__ static T mask(T v, T di) {
     return make_double2(di.x != 0.0 ? v.x : 0.0, di.y != 0.0 ? v.y : 0.0);
   }
+  __device__ static unsigned freebits(T di) { return (di.x != 0.0 ? 1u : 0u) | (di.y != 0.0 ? 2u : 0u); }
+  __device__ static T maskb(T v, unsigned b) {
+    return make_double2((b & 1u) ? v.x : 0.0, (b & 2u) ? v.y : 0.0);
+  }
   __device__ static double dot(T a, T b) { return a.x * b.x + a.y * b.y; }
 };
 template <>
@@ -121,6 +125,8 @@ struct Node<false> {
   __device__ static T mul(T a, T b) { return a * b; }
   __device__ static T axpy(double s, T x, T y) { return s * x + y; }
   __device__ static T mask(T v, T di) { return di != 0.0 ? v : 0.0; }
+  __device__ static unsigned freebits(T di) { return di != 0.0 ? 1u : 0u; }
+  __device__ static T maskb(T v, unsigned b) { return (b & 1u) ? v : 0.0; }
   __device__ static double dot(T a, T b) { return a * b; }
 };
 
@@ -389,14 +395,20 @@ __device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, const dou
   }
 }
 
+template <bool MOM>
 struct CgSmem {
+  DupRow<MOM> dup[NT / 32];
   double red[NT / 32 * 2];
   double bc[4];
 };
+#ifndef PFB_USE_RING
+#define PFB_USE_RING 0  // cp.async ring: measured no gain over register prefetch
+#endif
 
 template <bool MOM>
 __global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k_cg(CgArgs a) {
-  __shared__ CgSmem S;
+  __shared__ CgSmem<MOM> S;
+  extern __shared__ __align__(16) unsigned char dyn_smem[];  // MomRing per warp (momentum)
   cg::grid_group grid = cg::this_grid();
   const int gwarp = blockIdx.x * (NT / 32) + (threadIdx.x >> 5), nwarps = gridDim.x * (NT / 32);
   double* part = a.partials;
@@ -428,8 +440,13 @@ __global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k
       double* pnew = (k & 1) ? a.p1 : a.p0;
       const double* pold = (k & 1) ? a.p0 : a.p1;
       double pq = 0.0;
-      for (int u = gwarp; u < a.g.n_units; u += nwarps)
-        march_unit<MOM, false>(a, a.g, u, first, beta, pold, pnew, pq);
+      for (int u = gwarp; u < a.g.n_units; u += nwarps) {
+        if constexpr (MOM && PFB_USE_RING)
+          march_mom_ring(a, a.g, u, first, beta, pold, pnew, pq, S.dup[threadIdx.x >> 5],
+                         reinterpret_cast<MomRing*>(dyn_smem)[threadIdx.x >> 5]);
+        else
+          march_unit<MOM, false>(a, a.g, u, first, beta, pold, pnew, pq, S.dup[threadIdx.x >> 5]);
+      }
       {
         double v[1] = {pq};
         block_sum<1>(v, S.red);
@@ -473,9 +490,174 @@ __global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k
 // y = A x (unmasked) at the current state: one warp per marching unit
 template <bool MOM>
 __global__ void __launch_bounds__(NT) k_apply(CgArgs a, const double* x) {
+  __shared__ DupRow<MOM> dup[NT / 32];
   const int u = blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
   double pq = 0.0;
-  if (u < a.g.n_units) march_unit<MOM, true>(a, a.g, u, true, 0.0, x, nullptr, pq);
+  if (u < a.g.n_units)
+    march_unit<MOM, true>(a, a.g, u, true, 0.0, x, nullptr, pq, dup[threadIdx.x >> 5]);
+}
+
+}  // namespace pfb
+
+// =========================================================================================
+// Split-phase PCG: the same iteration as k_cg, but phase A (march) and phase B (stream) are
+// separate kernels chained in a CUDA graph of CG_CHUNK iterations, so each phase is compiled
+// for its own register budget / occupancy.  Device-side control: every CTA re-reduces the
+// previous phase's per-CTA partials in a fixed order (deterministic, no atomics), so all CTAs
+// agree on alpha, beta and the stopping decision; the first CTA of the deciding kernel records
+// the outcome in CgCtl and every later kernel of the chunk exits immediately.
+namespace pfb {
+
+constexpr int CG_SLOTS = 3;  // ring of partial buffers: iteration k uses slot k mod 3
+
+struct CgCtl {
+  long long k0;     // first iteration of the current chunk
+  long long iters;  // final iteration count (valid when done)
+  int done, status;
+  double atol, bnorm, rnorm;
+};
+
+struct SplitArgs {
+  CgArgs c;
+  CgCtl* ctl;
+  double* partA;    // [CG_SLOTS][gridA]        p.q
+  double* partB;    // [CG_SLOTS + 1][gridB][2] r.r, r.D^-1.r (slot CG_SLOTS: initial b)
+  int gridA, gridB;
+};
+
+__device__ __forceinline__ int slot_of(long long k) { return (int)(k % CG_SLOTS); }
+
+template <int NV>
+__device__ __forceinline__ void reduce_parts(const double* part, int n, double* bc,
+                                             double (&out)[NV]) {
+  if (threadIdx.x < 32) {
+    double s[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) s[q] = 0.0;
+    for (int i = threadIdx.x; i < n; i += 32) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) s[q] += __ldcg(part + NV * i + q);
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) s[q] = warp_sum(s[q]);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) bc[q] = s[q];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) out[q] = bc[q];
+}
+
+// initial reduction over r = b: ||b||^2 and b.D^-1.b
+template <bool MOM>
+__global__ void __launch_bounds__(NT) k_cg_init(SplitArgs s) {
+  __shared__ double red[NT / 32 * 2];
+  double rr = 0.0, rz = 0.0;
+  phase_b(s.c, 0.0, nullptr, false, rr, rz);
+  double v[2] = {rr, rz};
+  block_sum<2>(v, red);
+  double* pb = s.partB + (size_t)CG_SLOTS * s.gridB * 2;
+  if (threadIdx.x == 0) { pb[2 * blockIdx.x] = v[0]; pb[2 * blockIdx.x + 1] = v[1]; }
+  if (blockIdx.x == 0 && threadIdx.x == 0) { s.ctl->done = 0; s.ctl->status = CG_CONVERGED; }
+}
+
+#ifndef PFB_CGA_MINB_MOM
+#define PFB_CGA_MINB_MOM 2
+#endif
+template <bool MOM>
+__global__ void __launch_bounds__(NT, MOM ? PFB_CGA_MINB_MOM : 3) k_cg_a(SplitArgs s, int klocal) {
+  __shared__ double bc[4];
+  __shared__ double red[NT / 32];
+  __shared__ DupRow<MOM> dup[NT / 32];
+  if (s.ctl->done) return;
+  const long long k = s.ctl->k0 + klocal;
+  const double* pbk = s.partB + (size_t)(k == 0 ? CG_SLOTS : slot_of(k - 1)) * s.gridB * 2;
+  double cur[2];
+  reduce_parts<2>(pbk, s.gridB, bc, cur);  // ||r_k||^2, r_k.D^-1.r_k
+  const double rn = sqrt(cur[0]);
+  double atol;
+  if (k == 0) {
+    atol = s.c.rtol * rn;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { s.ctl->atol = atol; s.ctl->bnorm = rn; }
+  } else {
+    atol = s.ctl->atol;
+  }
+  int status = -1;
+  if (k == 0 && rn == 0.0) status = CG_CONVERGED;  // b = 0: x = 0 (scipy returns b)
+  else if (rn < atol) status = CG_CONVERGED;
+  else if (!(rn == rn)) status = CG_NAN;
+  else if (k >= s.c.maxiter) status = CG_MAXITER;
+  if (status >= 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      s.ctl->iters = k;
+      s.ctl->status = status;
+      s.ctl->rnorm = rn;
+      __threadfence();
+      s.ctl->done = 1;
+    }
+    return;
+  }
+  double beta = 0.0;
+  if (k > 0) {
+    __syncthreads();
+    const double* pbp = s.partB + (size_t)(k == 1 ? CG_SLOTS : slot_of(k - 2)) * s.gridB * 2;
+    double prev[2];
+    reduce_parts<2>(pbp, s.gridB, bc, prev);
+    beta = cur[1] / prev[1];
+  }
+  double* pnew = (k & 1) ? s.c.p1 : s.c.p0;
+  const double* pold = (k & 1) ? s.c.p0 : s.c.p1;
+  double pq = 0.0;
+  const int nwarps = gridDim.x * (NT / 32);
+  for (int u = blockIdx.x * (NT / 32) + (threadIdx.x >> 5); u < s.c.g.n_units; u += nwarps)
+    march_unit<MOM, false>(s.c, s.c.g, u, k == 0, beta, pold, pnew, pq, dup[threadIdx.x >> 5]);
+  double v[1] = {pq};
+  block_sum<1>(v, red);
+  if (threadIdx.x == 0) s.partA[(size_t)slot_of(k) * s.gridA + blockIdx.x] = v[0];
+}
+
+template <bool MOM>
+__global__ void __launch_bounds__(NT) k_cg_b(SplitArgs s, int klocal) {
+  __shared__ double bc[4];
+  __shared__ double red[NT / 32 * 2];
+  if (s.ctl->done) return;
+  const long long k = s.ctl->k0 + klocal;
+  double pqv[1], cur[2];
+  reduce_parts<1>(s.partA + (size_t)slot_of(k) * s.gridA, s.gridA, bc, pqv);
+  __syncthreads();
+  reduce_parts<2>(s.partB + (size_t)(k == 0 ? CG_SLOTS : slot_of(k - 1)) * s.gridB * 2,
+                  s.gridB, bc, cur);
+  if (s.c.probe && !(pqv[0] > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      s.ctl->iters = k + 1;
+      s.ctl->status = CG_INDEFINITE;
+      __threadfence();
+      s.ctl->done = 1;
+    }
+    return;
+  }
+  const double alpha = cur[1] / pqv[0];
+  const double* pk = (k & 1) ? s.c.p1 : s.c.p0;
+  double rr = 0.0, rz = 0.0;
+  phase_b(s.c, alpha, pk, true, rr, rz);
+  double v[2] = {rr, rz};
+  block_sum<2>(v, red);
+  double* pb = s.partB + (size_t)slot_of(k) * s.gridB * 2;
+  if (threadIdx.x == 0) { pb[2 * blockIdx.x] = v[0]; pb[2 * blockIdx.x + 1] = v[1]; }
+}
+
+// end of a chunk: advance the iteration base
+__global__ void k_cg_advance(CgCtl* ctl, int chunk) {
+  if (!ctl->done) ctl->k0 += chunk;
+}
+
+// target += x after convergence
+__global__ void k_cg_finish(double* target, const double* x, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    target[i] += x[i];
 }
 
 }  // namespace pfb

@@ -115,11 +115,51 @@ __device__ __forceinline__ typename Node<MOM>::T finish_node(const RawNode<MOM>&
   return p;
 }
 
+// ---- cp.async prefetch ring (momentum march): the next PFB_RING node rows of a warp live in
+// shared memory, filled by 16-byte cp.async.cg copies (L2 -> smem, no register staging,
+// zero-fill for absent nodes), so each warp keeps PFB_RING-1 rows of loads in flight.
+#ifndef PFB_RING
+#define PFB_RING 4
+#endif
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+struct MomRow {  // one node row of one warp
+  double2 r[32], di[32], po[32];
+  double d[32];
+  int id[32];
+};
+struct MomRing {
+  MomRow row[PFB_RING];
+};
+
+// the slit row's upper-face (duplicate) nodes of one warp, parked in shared memory so the march
+// does not carry them in registers through every row
+template <bool MOM>
+struct DupRow {
+  typename Node<MOM>::T p[32];
+  double d[32];
+  int id[32];
+  unsigned fb[32];
+};
+
 template <bool MOM, bool APPLY>
 __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, int unit,
                                            bool first, double beta,
                                            const double* __restrict__ pold,
-                                           double* __restrict__ pnew, double& pq) {
+                                           double* __restrict__ pnew, double& pq,
+                                           DupRow<MOM>& dup) {
   using N_ = Node<MOM>;
   using T = typename N_::T;
   const DMesh& m = a.m;
@@ -132,84 +172,87 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
   const bool lane_own = lane >= 1 && lane <= TXW;
   const int R = m.notch_row;
   const bool dupcol = R >= 0 && col >= m.notch_lo && col < m.notch_hi;
-  const int dupid = dupcol ? m.dup_start + (col - m.notch_lo) : -1;
   auto nid = [&](int j) -> int {
     if (j < 0 || j > m.ny) return -1;
     const int4 rw = __ldg(m.nrow + j);
     return (col >= rw.x && col < rw.y) ? rw.z + (col - rw.x) : -1;
   };
+  // loads and parks the duplicate row (warp-uniform call)
+  auto load_dup = [&](bool own) {
+    RawNode<MOM> wd;
+    fetch_node<MOM, APPLY>(a, pold, first, dupcol ? m.dup_start + (col - m.notch_lo) : -1, wd);
+    dup.p[lane] = finish_node<MOM, APPLY>(wd, first, beta, own, pnew);
+    dup.d[lane] = MOM ? wd.d : 0.0;
+    dup.id[lane] = wd.id;
+    dup.fb[lane] = (APPLY || wd.id < 0) ? 0u : N_::freebits(wd.di);
+    __syncwarp();
+  };
 
   // lower row (cj) state
-  T p_lo, di_lo, p_dup = N_::zero(), di_dup = N_::zero();
-  double d_lo, d_dup = 0.0;
-  int id_lo, id_dup = -1;
+  T p_lo;
+  double d_lo;
+  int id_lo;
+  unsigned fb_lo;
   bool lo_slit;
   RawNode<MOM> w;
-  {
-    fetch_node<MOM, APPLY>(a, pold, first, nid(r0 - 1), w);
-    p_lo = finish_node<MOM, APPLY>(w, first, beta, false, pnew);
-    di_lo = w.di;
-    d_lo = MOM ? w.d : 0.0;
-    id_lo = w.id;
-    lo_slit = (r0 - 1 == R);
-    if (lo_slit) {
-      RawNode<MOM> wd;
-      fetch_node<MOM, APPLY>(a, pold, first, dupid, wd);
-      p_dup = finish_node<MOM, APPLY>(wd, first, beta, false, pnew);
-      di_dup = wd.di;
-      d_dup = MOM ? wd.d : 0.0;
-      id_dup = wd.id;
-    }
-  }
+  fetch_node<MOM, APPLY>(a, pold, first, nid(r0 - 1), w);
+  p_lo = finish_node<MOM, APPLY>(w, first, beta, false, pnew);
+  d_lo = MOM ? w.d : 0.0;
+  id_lo = w.id;
+  fb_lo = (APPLY || w.id < 0) ? 0u : N_::freebits(w.di);
+  lo_slit = (r0 - 1 == R);
+  if (lo_slit) load_dup(false);
   fetch_node<MOM, APPLY>(a, pold, first, nid(r0), w);  // upper row, in flight
+  // cell-row data (branch bits / Newton coefficients) are prefetched one row ahead too
+  auto cell_id = [&](int cj) -> int {
+    if (cj < 0 || cj >= m.ny || lane >= 31) return -1;
+    const int4 er = __ldg(m.erow + cj);
+    return (col >= er.x && col < er.y) ? er.z + (col - er.x) : -1;
+  };
+  int eid_n = cell_id(r0 - 1);
+  unsigned fl_n = 0u;
+  double bq_n[4] = {0.0, 0.0, 0.0, 0.0};
+  auto fetch_cell = [&](int eid) {
+    if (eid < 0) return;
+    if constexpr (MOM) fl_n = __ldg(a.flags + eid);
+    else load4(a.b, eid, bq_n);
+  };
+  fetch_cell(eid_n);
   T acc_lo = N_::zero();
   for (int cj = r0 - 1; cj < r1; ++cj) {
     const int jh = cj + 1;
     const bool hi_own = lane_own && jh >= r0 && jh < r1;
     const T p_hi = finish_node<MOM, APPLY>(w, first, beta, hi_own, pnew);
-    const T di_hi = w.di;
     const double d_hi = MOM ? w.d : 0.0;
     const int id_hi = w.id;
+    const unsigned fb_hi = (APPLY || w.id < 0) ? 0u : N_::freebits(w.di);
     const bool hi_slit = (jh == R);
-    T p_hdup = N_::zero(), di_hdup = N_::zero();
-    double d_hdup = 0.0;
-    int id_hdup = -1;
-    if (hi_slit) {  // warp-uniform
-      RawNode<MOM> wd;
-      fetch_node<MOM, APPLY>(a, pold, first, dupid, wd);
-      p_hdup = finish_node<MOM, APPLY>(wd, first, beta, hi_own, pnew);
-      di_hdup = wd.di;
-      d_hdup = MOM ? wd.d : 0.0;
-      id_hdup = wd.id;
-    }
     if (jh + 1 <= r1) fetch_node<MOM, APPLY>(a, pold, first, nid(jh + 1), w);  // prefetch
+    const int eid = eid_n;
+    const unsigned fl = fl_n;
+    double bq[4] = {bq_n[0], bq_n[1], bq_n[2], bq_n[3]};
+    eid_n = cell_id(cj + 1);
+    fetch_cell(eid_n);
     // ---- cell (col, cj)
     const bool use_dup = lo_slit && dupcol;
-    const T b0 = use_dup ? p_dup : p_lo;
+    const T b0 = use_dup ? dup.p[lane] : p_lo;
     const T b1 = shfl_dn(b0);
     const T t2 = shfl_dn(p_hi);
-    int eid = -1;
-    if (cj >= 0 && cj < m.ny) {
-      const int4 er = __ldg(m.erow + cj);
-      if (lane < 31 && col >= er.x && col < er.y) eid = er.z + (col - er.x);
-    }
     T f[4];
     if constexpr (MOM) {
-      const double e0 = use_dup ? d_dup : d_lo;
+      const double e0 = use_dup ? dup.d[lane] : d_lo;
       const double e1 = shfl_dn(e0);
       const double e2 = shfl_dn(d_hi);
       f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
       if (eid >= 0) {
         const double2 pc[4] = {b0, b1, t2, p_hi};
         const double dc[4] = {e0, e1, e2, d_hi};
-        mom_cell_fast(C, pc, dc, __ldg(a.flags + eid), f);
+        mom_cell_fast(C, pc, dc, fl, f);
       }
     } else {
       f[0] = f[1] = f[2] = f[3] = 0.0;
       if (eid >= 0) {
         const double pc[4] = {b0, b1, t2, p_hi};
-        double bq[4];
-        load4(a.b, eid, bq);
         evo_cell_apply(C, pc, bq, f);
       }
     }
@@ -221,41 +264,184 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
         if (id_lo >= 0) {  // lower face: cells below only
           T qv = acc_lo;
           if (!APPLY) {
-            qv = N_::mask(qv, di_lo);
+            qv = N_::maskb(qv, fb_lo);
             pq += N_::dot(p_lo, qv);
           }
           N_::st(a.q, id_lo, qv);
         }
-        if (id_dup >= 0) {  // upper face: cells above only
+        const int idd = dup.id[lane];
+        if (idd >= 0) {  // upper face: cells above only
           T qv = add_t(c1l, f[0]);
           if (!APPLY) {
-            qv = N_::mask(qv, di_dup);
-            pq += N_::dot(p_dup, qv);
+            qv = N_::maskb(qv, dup.fb[lane]);
+            pq += N_::dot(dup.p[lane], qv);
           }
-          N_::st(a.q, id_dup, qv);
+          N_::st(a.q, idd, qv);
         }
       } else if (id_lo >= 0) {
         T qv = add_t(add_t(acc_lo, c1l), f[0]);
         if (!APPLY) {
-          qv = N_::mask(qv, di_lo);
+          qv = N_::maskb(qv, fb_lo);
           pq += N_::dot(p_lo, qv);
         }
         N_::st(a.q, id_lo, qv);
       }
     }
     acc_lo = add_t(c2l, f[3]);
+    if (hi_slit) {  // warp-uniform; the old duplicate row was consumed above
+      __syncwarp();
+      load_dup(hi_own);
+    }
     p_lo = p_hi;
-    di_lo = di_hi;
     d_lo = d_hi;
     id_lo = id_hi;
+    fb_lo = fb_hi;
     lo_slit = hi_slit;
-    if (hi_slit) {
-      p_dup = p_hdup;
-      di_dup = di_hdup;
-      d_dup = d_hdup;
-      id_dup = id_hdup;
-    }
   }
+}
+
+// Momentum phase A with the cp.async ring (same arithmetic and accumulation order as
+// march_unit<true, false>; only the way node rows arrive differs).
+__device__ __forceinline__ void ring_issue(const CgArgs& a, const double* __restrict__ pold,
+                                           bool first, int id, MomRow& slot, int lane) {
+  const bool v = id >= 0;
+  const int cid = v ? id : 0;
+  cp_async16(&slot.r[lane], a.r + 2 * (size_t)cid, v);
+  cp_async16(&slot.di[lane], a.dinv + 2 * (size_t)cid, v);
+  if (!first) cp_async16(&slot.po[lane], pold + 2 * (size_t)cid, v);
+  cp_async8(&slot.d[lane], a.d + cid, v);
+  slot.id[lane] = id;
+}
+
+__device__ __forceinline__ void march_mom_ring(const CgArgs& a, const MarchGeom& G, int unit,
+                                               bool first, double beta,
+                                               const double* __restrict__ pold,
+                                               double* __restrict__ pnew, double& pq,
+                                               DupRow<true>& dup, MomRing& ring) {
+  using N_ = Node<true>;
+  using T = double2;
+  const DMesh& m = a.m;
+  const Consts& C = a.C;
+  const int lane = threadIdx.x & 31;
+  const int strip = unit % G.n_strips;
+  const int r0 = (unit / G.n_strips) * G.rows_per_unit;
+  const int r1 = min(r0 + G.rows_per_unit, m.ny + 1);
+  const int col = strip * TXW - 1 + lane;
+  const bool lane_own = lane >= 1 && lane <= TXW;
+  const int R = m.notch_row;
+  const bool dupcol = R >= 0 && col >= m.notch_lo && col < m.notch_hi;
+  auto nid = [&](int j) -> int {
+    if (j < 0 || j > m.ny) return -1;
+    const int4 rw = __ldg(m.nrow + j);
+    return (col >= rw.x && col < rw.y) ? rw.z + (col - rw.x) : -1;
+  };
+  auto load_dup = [&](bool own) {
+    RawNode<true> wd;
+    fetch_node<true, false>(a, pold, first, dupcol ? m.dup_start + (col - m.notch_lo) : -1, wd);
+    dup.p[lane] = finish_node<true, false>(wd, first, beta, own, pnew);
+    dup.d[lane] = wd.d;
+    dup.id[lane] = wd.id;
+    dup.fb[lane] = wd.id < 0 ? 0u : N_::freebits(wd.di);
+    __syncwarp();
+  };
+  // rows r0-1 .. r1 enter the ring in order; row j lives in slot (j - r0 + 1) % PFB_RING
+  const int jfirst = r0 - 1;
+  int jissue = jfirst;
+  for (int q = 0; q < PFB_RING - 1; ++q, ++jissue) {
+    if (jissue <= r1) ring_issue(a, pold, first, nid(jissue), ring.row[(jissue - jfirst) % PFB_RING], lane);
+    cp_async_commit();
+  }
+  auto take = [&](int j, bool own, T& p, double& d, int& id, unsigned& fb) {
+    MomRow& sl = ring.row[(j - jfirst) % PFB_RING];
+    id = sl.id[lane];
+    d = sl.d[lane];
+    p = make_double2(0.0, 0.0);
+    fb = 0u;
+    if (id >= 0) {
+      const T di = sl.di[lane];
+      p = N_::mul(di, sl.r[lane]);
+      if (!first) p = N_::axpy(beta, sl.po[lane], p);
+      if (own) N_::st(pnew, id, p);
+      fb = N_::freebits(di);
+    }
+  };
+  // lower row r0-1
+  T p_lo;
+  double d_lo;
+  int id_lo;
+  unsigned fb_lo;
+  cp_async_wait<PFB_RING - 2>();
+  take(jfirst, false, p_lo, d_lo, id_lo, fb_lo);
+  bool lo_slit = (jfirst == R);
+  if (lo_slit) load_dup(false);
+  T acc_lo = make_double2(0.0, 0.0);
+  for (int cj = r0 - 1; cj < r1; ++cj) {
+    const int jh = cj + 1;
+    // refill: the slot of row jfirst + (cj - jfirst) is free again
+    if (jissue <= r1) ring_issue(a, pold, first, nid(jissue), ring.row[(jissue - jfirst) % PFB_RING], lane);
+    cp_async_commit();
+    ++jissue;
+    cp_async_wait<PFB_RING - 2>();
+    const bool hi_own = lane_own && jh >= r0 && jh < r1;
+    T p_hi;
+    double d_hi;
+    int id_hi;
+    unsigned fb_hi;
+    take(jh, hi_own, p_hi, d_hi, id_hi, fb_hi);
+    const bool hi_slit = (jh == R);
+    const bool use_dup = lo_slit && dupcol;
+    const T b0 = use_dup ? dup.p[lane] : p_lo;
+    const T b1 = shfl_dn(b0);
+    const T t2 = shfl_dn(p_hi);
+    const double e0 = use_dup ? dup.d[lane] : d_lo;
+    const double e1 = shfl_dn(e0);
+    const double e2 = shfl_dn(d_hi);
+    int eid = -1;
+    if (cj >= 0 && cj < m.ny) {
+      const int4 er = __ldg(m.erow + cj);
+      if (lane < 31 && col >= er.x && col < er.y) eid = er.z + (col - er.x);
+    }
+    T f[4];
+    f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
+    if (eid >= 0) {
+      const double2 pc[4] = {b0, b1, t2, p_hi};
+      const double dc[4] = {e0, e1, e2, d_hi};
+      mom_cell_fast(C, pc, dc, __ldg(a.flags + eid), f);
+    }
+    const T c1l = shfl_up(f[1]);
+    const T c2l = shfl_up(f[2]);
+    if (lane_own && cj >= r0) {
+      if (use_dup) {
+        if (id_lo >= 0) {
+          const T qv = N_::maskb(acc_lo, fb_lo);
+          pq += N_::dot(p_lo, qv);
+          N_::st(a.q, id_lo, qv);
+        }
+        const int idd = dup.id[lane];
+        if (idd >= 0) {
+          const T qv = N_::maskb(add_t(c1l, f[0]), dup.fb[lane]);
+          pq += N_::dot(dup.p[lane], qv);
+          N_::st(a.q, idd, qv);
+        }
+      } else if (id_lo >= 0) {
+        const T qv = N_::maskb(add_t(add_t(acc_lo, c1l), f[0]), fb_lo);
+        pq += N_::dot(p_lo, qv);
+        N_::st(a.q, id_lo, qv);
+      }
+    }
+    acc_lo = add_t(c2l, f[3]);
+    if (hi_slit) {
+      __syncwarp();
+      load_dup(hi_own);
+    }
+    p_lo = p_hi;
+    d_lo = d_hi;
+    id_lo = id_hi;
+    fb_lo = fb_hi;
+    lo_slit = hi_slit;
+  }
+  cp_async_wait<0>();
+  __syncwarp();
 }
 
 // host-side choice of the unit shape: enough units for every resident warp, but at least
