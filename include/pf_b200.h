@@ -159,6 +159,30 @@ pf_status pf_softening_gate(pf_handle* h, uint8_t* gate_out);
 pf_status pf_extra_stiffness(pf_handle* h, int scheme, double* extra_out);
 pf_status pf_update_active_energy(pf_handle* h, int scheme, const double* delta_d_nodal);
 
+/* row-strip decomposition ---------------------------------------------
+ * Each rank owns a contiguous range of node rows of the global mesh; its handle is created on
+ * the LOCAL row-compact sub-mesh (owned rows plus one ghost row per neighbour, plus the slit
+ * duplicates when it owns the slit row; paper_2209_07969_b200/strips.py builds it).  Owned
+ * nodes: [own_lo, own_hi) and [dup_lo, n_nodes); owned cells: [cell_lo, cell_hi).  Halo rows
+ * are contiguous local ranges.  comm_kind 0 = NCCL (nccl_id from pf_nccl_unique_id on rank 0,
+ * broadcast by the caller); 1 = in-process host emulation (host_group from
+ * pf_host_group_create, one host thread per strip, all strips on the same GPU — tests). */
+typedef struct {
+  int32_t rank, nranks;
+  int64_t own_lo, own_hi, dup_lo, cell_lo, cell_hi;
+  int64_t send_lo_start, send_lo_count, recv_lo_start, recv_lo_count;
+  int64_t send_hi_start, send_hi_count, recv_hi_start, recv_hi_count;
+  int32_t comm_kind;
+  unsigned char nccl_id[128];
+  void* host_group;
+} pf_strip;
+
+pf_status pf_nccl_unique_id(unsigned char out[128]);
+pf_status pf_host_group_create(int32_t nranks, void** out);
+void pf_host_group_destroy(void* group);
+pf_status pf_create_strip(const pf_mesh* local_mesh, const pf_material* mat, const pf_config* cfg,
+                          int device, const pf_strip* strip, pf_handle** out);
+
 /* device-resident benchmarking helpers */
 pf_status pf_device_info(pf_handle* h, int32_t* cg_grid, int32_t* sm_count, int64_t* l2_bytes);
 pf_status pf_flush_l2(pf_handle* h);

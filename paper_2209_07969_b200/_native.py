@@ -65,6 +65,19 @@ class PfStats(C.Structure):
     ]
 
 
+class PfStrip(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int32), ("nranks", C.c_int32),
+        ("own_lo", C.c_int64), ("own_hi", C.c_int64), ("dup_lo", C.c_int64),
+        ("cell_lo", C.c_int64), ("cell_hi", C.c_int64),
+        ("send_lo_start", C.c_int64), ("send_lo_count", C.c_int64),
+        ("recv_lo_start", C.c_int64), ("recv_lo_count", C.c_int64),
+        ("send_hi_start", C.c_int64), ("send_hi_count", C.c_int64),
+        ("recv_hi_start", C.c_int64), ("recv_hi_count", C.c_int64),
+        ("comm_kind", C.c_int32), ("nccl_id", C.c_ubyte * 128), ("host_group", C.c_void_p),
+    ]
+
+
 # name -> (restype, argtypes); mirrors include/pf_b200.h
 _SIGNATURES = {
     "pf_create": (C.c_int, [C.POINTER(PfMesh), C.POINTER(PfMaterial), C.POINTER(PfConfig),
@@ -92,6 +105,11 @@ _SIGNATURES = {
     "pf_softening_gate": (C.c_int, [C.c_void_p, _u8p]),
     "pf_extra_stiffness": (C.c_int, [C.c_void_p, C.c_int, _f64p]),
     "pf_update_active_energy": (C.c_int, [C.c_void_p, C.c_int, _f64p]),
+    "pf_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte * 128)]),
+    "pf_host_group_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
+    "pf_host_group_destroy": (None, [C.c_void_p]),
+    "pf_create_strip": (C.c_int, [C.POINTER(PfMesh), C.POINTER(PfMaterial), C.POINTER(PfConfig),
+                                  C.c_int, C.POINTER(PfStrip), C.POINTER(C.c_void_p)]),
     "pf_device_info": (C.c_int, [C.c_void_p, _i32p, _i32p, _i64p]),
     "pf_flush_l2": (C.c_int, [C.c_void_p]),
     "pf_synchronize": (C.c_int, [C.c_void_p]),

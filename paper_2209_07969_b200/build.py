@@ -9,9 +9,17 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", "pf_api.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("pf_device.cuh", "pf_kernels.cuh")] + [
+DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in (
+    "pf_device.cuh", "pf_kernels.cuh", "pf_cg.cuh", "pf_march.cuh", "pf_comm.h")] + [
     os.path.join(ROOT, "include", "pf_b200.h")]
 OUT = os.path.join(HERE, "libpfb200.so")
+
+NCCL_INCLUDE = None
+for _cand in ("/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/include",
+              "/usr/include"):
+    if os.path.exists(os.path.join(_cand, "nccl.h")):
+        NCCL_INCLUDE = _cand
+        break
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -38,7 +46,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *SOURCES]
+    inc = ["-I", NCCL_INCLUDE] if NCCL_INCLUDE else []
+    cmd = [nvcc(), *NVCC_FLAGS, *inc, "-ldl", "-o", OUT + ".tmp", *SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

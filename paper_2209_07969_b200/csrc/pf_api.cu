@@ -17,6 +17,7 @@
 
 #include "../../include/pf_b200.h"
 #include "pf_kernels.cuh"
+#include "pf_comm.h"
 
 using pfb::CgResult;
 
@@ -71,6 +72,11 @@ struct pf_handle {
   pfb::CgCtl* h_ctl = nullptr;  // pinned
   double *partA = nullptr, *partB = nullptr;
   cudaGraphExec_t graphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [mom][probe]
+  // row-strip decomposition: communicator and device reduction buffers
+  pfb::Comm* comm = nullptr;
+  double* d_red = nullptr;  // [16] device scalars for all-reduces
+  double* gA = nullptr;     // [CG_SLOTS]       global p.q
+  double* gB = nullptr;     // [CG_SLOTS+1][2]  global r.r, r.D^-1.r
   long long l2_bytes = 0;
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
@@ -200,6 +206,10 @@ extern "C" void pf_destroy(pf_handle* h) {
   for (auto& row : h->graphs)
     for (auto& g : row)
       if (g) cudaGraphExecDestroy(g);
+  delete h->comm;
+  if (h->d_red) cudaFree(h->d_red);
+  if (h->gA) cudaFree(h->gA);
+  if (h->gB) cudaFree(h->gB);
   if (h->d_ctl) cudaFree(h->d_ctl);
   if (h->partA) cudaFree(h->partA);
   if (h->partB) cudaFree(h->partB);
@@ -251,8 +261,8 @@ static pf_status validate_mesh(pf_handle* h, const pf_mesh* m) {
   return PF_OK;
 }
 
-extern "C" pf_status pf_create(const pf_mesh* mesh, const pf_material* mat, const pf_config* cfg,
-                               int device, pf_handle** out) {
+static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const pf_config* cfg,
+                             int device, const pf_strip* strip, pf_handle** out) {
   if (!out || !mesh || !mat || !cfg) return PF_ERR_INVALID;
   *out = nullptr;
   pf_handle* h = new pf_handle();
@@ -343,6 +353,34 @@ extern "C" pf_status pf_create(const pf_mesh* mesh, const pf_material* mat, cons
   dm.n_nodes = h->n_nodes; dm.n_elems = h->n_elems;
   dm.n_tiles = h->n_tiles; dm.tiles = h->d_tiles;
   dm.nrow = h->d_nrow; dm.erow = h->d_erow;
+  dm.own_lo = 0; dm.own_hi = h->n_nodes; dm.dup_lo = h->n_nodes;
+  dm.cell_lo = 0; dm.cell_hi = h->n_elems;
+  if (strip) {
+    dm.own_lo = (int)strip->own_lo; dm.own_hi = (int)strip->own_hi; dm.dup_lo = (int)strip->dup_lo;
+    dm.cell_lo = (int)strip->cell_lo; dm.cell_hi = (int)strip->cell_hi;
+    pfb::HaloSpec sp;
+    sp.rank = strip->rank; sp.nranks = strip->nranks;
+    sp.send_lo_start = strip->send_lo_start; sp.send_lo_count = strip->send_lo_count;
+    sp.recv_lo_start = strip->recv_lo_start; sp.recv_lo_count = strip->recv_lo_count;
+    sp.send_hi_start = strip->send_hi_start; sp.send_hi_count = strip->send_hi_count;
+    sp.recv_hi_start = strip->recv_hi_start; sp.recv_hi_count = strip->recv_hi_count;
+    if (strip->comm_kind == 0) {
+      auto* nc = new pfb::NcclComm();
+      nc->spec = sp;
+      h->comm = nc;
+      const std::string e = nc->init(strip->nccl_id);
+      if (!e.empty()) { h->err = e; return bail(PF_ERR_NCCL); }
+    } else {
+      if (!strip->host_group) { h->err = "host_group is null"; return bail(PF_ERR_INVALID); }
+      auto* hc = new pfb::HostComm();
+      hc->spec = sp;
+      hc->g = static_cast<pfb::HostGroup*>(strip->host_group);
+      h->comm = hc;
+    }
+    CREATE_CUDA(cudaMalloc((void**)&h->d_red, 16 * sizeof(double)));
+    CREATE_CUDA(cudaMalloc((void**)&h->gA, pfb::CG_SLOTS * sizeof(double)));
+    CREATE_CUDA(cudaMalloc((void**)&h->gB, (pfb::CG_SLOTS + 1) * 2 * sizeof(double)));
+  }
   build_consts(h, mesh->hx, mesh->hy);
   const size_t nn = h->n_nodes, ne = h->n_elems;
   pf_status s2 = PF_OK;
@@ -435,6 +473,40 @@ extern "C" pf_status pf_create(const pf_mesh* mesh, const pf_material* mat, cons
 #undef CREATE_ALLOC
 #undef CREATE_CUDA
 }
+
+extern "C" pf_status pf_create(const pf_mesh* mesh, const pf_material* mat, const pf_config* cfg,
+                               int device, pf_handle** out) {
+  return create_impl(mesh, mat, cfg, device, nullptr, out);
+}
+
+extern "C" pf_status pf_create_strip(const pf_mesh* local_mesh, const pf_material* mat,
+                                     const pf_config* cfg, int device, const pf_strip* strip,
+                                     pf_handle** out) {
+  if (!strip || strip->nranks < 1 || strip->rank < 0 || strip->rank >= strip->nranks)
+    return PF_ERR_INVALID;
+  return create_impl(local_mesh, mat, cfg, device, strip, out);
+}
+
+extern "C" pf_status pf_nccl_unique_id(unsigned char out[128]) {
+  pfb::NcclApi& api = pfb::NcclApi::get();
+  const std::string e = api.load();
+  if (!e.empty()) {
+    fprintf(stderr, "pf_nccl_unique_id: %s\n", e.c_str());
+    return PF_ERR_NCCL;
+  }
+  ncclUniqueId id;
+  if (api.GetUniqueId(&id) != ncclSuccess) return PF_ERR_NCCL;
+  std::memcpy(out, &id, sizeof(id) < 128 ? sizeof(id) : 128);
+  return PF_OK;
+}
+
+extern "C" pf_status pf_host_group_create(int32_t nranks, void** out) {
+  if (nranks < 1 || !out) return PF_ERR_INVALID;
+  *out = new pfb::HostGroup(nranks);
+  return PF_OK;
+}
+
+extern "C" void pf_host_group_destroy(void* group) { delete static_cast<pfb::HostGroup*>(group); }
 
 // ------------------------------------------------------------------------------------------
 // state transfer
@@ -606,18 +678,44 @@ static pf_status launch_evo_prepare(pf_handle* h, int full, int extra_scheme) {
   return launched(h);
 }
 
-// sums nv partial streams of n_tiles CTAs into h_scal[0..nv) and waits for them
+static pf_status comm_check(pf_handle* h, const std::string& e) {
+  if (e.empty()) return PF_OK;
+  return fail(h, PF_ERR_NCCL, e);
+}
+
+// sums nv partial streams of n_tiles CTAs into h_scal[0..nv) (all-reduced over the strips) and
+// waits for them
 static pf_status finalize(pf_handle* h, int nv) {
-  pfb::k_finalize<<<1, 256, 0, h->stream>>>(h->partials, h->n_tiles, nv, h->d_scal);
+  if (!h->comm) {
+    pfb::k_finalize<<<1, 256, 0, h->stream>>>(h->partials, h->n_tiles, nv, h->d_scal);
+    PF_TRY(launched(h));
+    PF_CUDA(cudaStreamSynchronize(h->stream));
+    return PF_OK;
+  }
+  pfb::k_finalize<<<1, 256, 0, h->stream>>>(h->partials, h->n_tiles, nv, h->d_red);
   PF_TRY(launched(h));
+  PF_TRY(comm_check(h, h->comm->allreduce(h->d_red, nv, h->stream)));
+  PF_CUDA(cudaMemcpyAsync(h->h_scal, h->d_red, nv * sizeof(double), cudaMemcpyDeviceToHost,
+                          h->stream));
   PF_CUDA(cudaStreamSynchronize(h->stream));
   return PF_OK;
+}
+
+static pf_status halo(pf_handle* h, double* vec, int comps) {
+  if (!h->comm) return PF_OK;
+  return comm_check(h, h->comm->halo(vec, comps, h->stream));
+}
+
+static pf_status axpy(pf_handle* h, double* y, const double* x, long long n) {
+  pfb::k_axpy<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(y, x, n);
+  return launched(h);
 }
 
 static pfb::CgArgs cg_args(pf_handle* h, bool mom) {
   pfb::CgArgs a{};
   a.m = h->dm;
   a.C = h->C;
+  a.vec2 = mom ? 1 : 0;
   a.ndof = mom ? 2LL * h->n_nodes : (long long)h->n_nodes;
   a.g = mom ? h->geom_mom : h->geom_evo;
   a.d = h->d;
@@ -754,8 +852,63 @@ static pf_status run_cg_split(pf_handle* h, bool mom, double* target, bool probe
   return cg_status(h, *status, *iters);
 }
 
+// split-phase PCG with all-reduces and halo exchanges between the phases (row strips).
+// Every rank takes identical decisions because every decision uses all-reduced scalars.
+static pf_status run_cg_dist(pf_handle* h, bool mom, double* target, bool probe, int* status,
+                             long long* iters) {
+  pfb::SplitArgs s = split_args(h, mom, probe);
+  s.gA = h->gA;
+  s.gB = h->gB;
+  const int comps = mom ? 2 : 1;
+  PF_CUDA(cudaEventRecord(h->ev0, h->stream));
+  PF_CUDA(cudaMemsetAsync(h->d_ctl, 0, sizeof(pfb::CgCtl), h->stream));
+  if (mom) pfb::k_cg_init<true><<<s.gridB, pfb::NT, 0, h->stream>>>(s);
+  else pfb::k_cg_init<false><<<s.gridB, pfb::NT, 0, h->stream>>>(s);
+  PF_TRY(launched(h));
+  double* gb0 = h->gB + 2 * pfb::CG_SLOTS;
+  pfb::k_finalize<<<1, 256, 0, h->stream>>>(h->partB + (size_t)pfb::CG_SLOTS * s.gridB * 2,
+                                            s.gridB, 2, gb0);
+  PF_TRY(launched(h));
+  PF_TRY(comm_check(h, h->comm->allreduce(gb0, 2, h->stream)));
+  for (long long k = 0;; ++k) {
+    const int sl = (int)(k % pfb::CG_SLOTS);
+    if (mom) pfb::k_cg_a<true><<<s.gridA, pfb::NT, 0, h->stream>>>(s, (int)k);
+    else pfb::k_cg_a<false><<<s.gridA, pfb::NT, 0, h->stream>>>(s, (int)k);
+    PF_TRY(launched(h));
+    pfb::k_finalize<<<1, 256, 0, h->stream>>>(h->partA + (size_t)sl * s.gridA, s.gridA, 1,
+                                              h->gA + sl);
+    PF_TRY(launched(h));
+    PF_TRY(comm_check(h, h->comm->allreduce(h->gA + sl, 1, h->stream)));
+    if (mom) pfb::k_cg_b<true><<<s.gridB, pfb::NT, 0, h->stream>>>(s, (int)k);
+    else pfb::k_cg_b<false><<<s.gridB, pfb::NT, 0, h->stream>>>(s, (int)k);
+    PF_TRY(launched(h));
+    pfb::k_finalize<<<1, 256, 0, h->stream>>>(h->partB + (size_t)sl * s.gridB * 2, s.gridB, 2,
+                                              h->gB + 2 * sl);
+    PF_TRY(launched(h));
+    PF_TRY(comm_check(h, h->comm->allreduce(h->gB + 2 * sl, 2, h->stream)));
+    PF_TRY(halo(h, s.c.r, comps));
+    PF_TRY(halo(h, (k & 1) ? s.c.p1 : s.c.p0, comps));
+    if ((k + 1) % h->chunk == 0) {
+      PF_CUDA(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(pfb::CgCtl), cudaMemcpyDeviceToHost,
+                              h->stream));
+      PF_CUDA(cudaStreamSynchronize(h->stream));
+      if (h->h_ctl->done) break;
+    }
+  }
+  *status = h->h_ctl->status;
+  *iters = h->h_ctl->iters;
+  if (*status == pfb::CG_CONVERGED && target) PF_TRY(axpy(h, target, s.c.x, s.c.ndof));
+  PF_CUDA(cudaEventRecord(h->ev1, h->stream));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  cg_account(h, mom, *iters, ms);
+  return cg_status(h, *status, *iters);
+}
+
 static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
                         long long* iters) {
+  if (h->comm) return run_cg_dist(h, mom, target, probe, status, iters);
   return h->split ? run_cg_split(h, mom, target, probe, status, iters)
                   : run_cg_persistent(h, mom, target, probe, status, iters);
 }
@@ -813,7 +966,15 @@ static pf_status momentum(pf_handle* h, const BcView& bc, bool apply_inc, double
     }
     int status;
     long long iters;
-    PF_TRY(run_cg(h, true, h->u, false, &status, &iters));
+    if (h->comm) {  // ghost rows of r and D^-1 from their owners; u ghosts refreshed below
+      PF_TRY(halo(h, h->ru, 2));
+      PF_TRY(halo(h, h->dinvu, 2));
+      PF_TRY(run_cg(h, true, nullptr, false, &status, &iters));
+      PF_TRY(halo(h, h->xu, 2));
+      PF_TRY(axpy(h, h->u, h->xu, 2LL * h->n_nodes));
+    } else {
+      PF_TRY(run_cg(h, true, h->u, false, &status, &iters));
+    }
     n_nr += 1;
   }
   // refresh_gp_from_displacement (assembly.py:260-269)
@@ -847,6 +1008,10 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
     }
     int status = pfb::CG_CONVERGED;
     long long iters = 0;
+    if (h->comm) {
+      PF_TRY(halo(h, h->rd, 1));
+      PF_TRY(halo(h, h->dinvd, 1));
+    }
     if (gated) {
       // SPD predicate for K_dd + K~ (replaces check_spd, linsolve.py:58-77): a non-positive
       // diagonal, or non-positive curvature p.Ap inside PCG, means "not positive definite"
@@ -857,9 +1022,14 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
       }
       if (fallback) {  // plain tangent for this staggered iteration (schemes.py:293-301)
         PF_TRY(launch_evo_prepare(h, 1, 0));
+        if (h->comm) {
+          PF_TRY(halo(h, h->rd, 1));
+          PF_TRY(halo(h, h->dinvd, 1));
+        }
         PF_TRY(run_cg(h, false, nullptr, false, &status, &iters));
         *fallbacks += 1;
       }
+      PF_TRY(halo(h, h->xd, 1));
       // one-time half-step energy update from this increment (schemes.py:303-310)
       pfb::GpArgs g = gp_args(h);
       g.dd = h->xd;
@@ -869,6 +1039,10 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
       const long long n = h->n_nodes;
       pfb::k_axpy<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(h->d, h->xd, n);
       PF_TRY(launched(h));
+    } else if (h->comm) {
+      PF_TRY(run_cg(h, false, nullptr, false, &status, &iters));
+      PF_TRY(halo(h, h->xd, 1));
+      PF_TRY(axpy(h, h->d, h->xd, h->n_nodes));
     } else {
       PF_TRY(run_cg(h, false, h->d, false, &status, &iters));
     }
@@ -1026,8 +1200,14 @@ extern "C" pf_status pf_reaction_force(pf_handle* h, const int64_t* nodes, int64
   if (n > 0)
     PF_CUDA(cudaMemcpyAsync(h->d_idx, nodes, n * sizeof(long long), cudaMemcpyHostToDevice,
                             h->stream));
-  pfb::k_reaction<<<1, 256, 0, h->stream>>>(h->Ru, h->d_idx, n, component, h->d_scal);
+  pfb::k_reaction<<<1, 256, 0, h->stream>>>(h->Ru, h->d_idx, n, component,
+                                            h->comm ? h->d_red : h->d_scal);
   PF_TRY(launched(h));
+  if (h->comm) {  // callers pass their OWNED nodes of the set
+    PF_TRY(comm_check(h, h->comm->allreduce(h->d_red, 1, h->stream)));
+    PF_CUDA(cudaMemcpyAsync(h->h_scal, h->d_red, sizeof(double), cudaMemcpyDeviceToHost,
+                            h->stream));
+  }
   PF_CUDA(cudaStreamSynchronize(h->stream));
   *out = h->h_scal[0];
   return PF_OK;

@@ -72,6 +72,7 @@ struct MarchGeom {
 struct CgArgs {
   DMesh m;
   Consts C;
+  int vec2;             // 1: momentum (double2 per node)
   MarchGeom g;          // warp work units of the marching phase A (pf_march.cuh)
   long long ndof;        // flat length (2*n_nodes or n_nodes)
   const double* d;       // momentum: nodal d
@@ -377,8 +378,17 @@ __device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, const dou
           xv[u].y += alpha * pv[u].y;
           x2[i] = xv[u];
         }
-        rr += rv[u].x * rv[u].x + rv[u].y * rv[u].y;
-        rz += rv[u].x * (dv[u].x * rv[u].x) + rv[u].y * (dv[u].y * rv[u].y);
+        // pair i holds node i (momentum) or nodes 2i, 2i+1 (phase field); ghosts do not count
+        const bool o0 = node_owned(a.m, a.vec2 ? (int)i : (int)(2 * i));
+        const bool o1 = a.vec2 ? o0 : node_owned(a.m, (int)(2 * i + 1));
+        if (o0) {
+          rr += rv[u].x * rv[u].x;
+          rz += rv[u].x * (dv[u].x * rv[u].x);
+        }
+        if (o1) {
+          rr += rv[u].y * rv[u].y;
+          rz += rv[u].y * (dv[u].y * rv[u].y);
+        }
       }
     }
   }
@@ -390,8 +400,10 @@ __device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, const dou
       a.r[i] = rv;
       a.x[i] = __ldcg(a.x + i) + alpha * __ldcg(pk + i);
     }
-    rr += rv * rv;
-    rz += rv * (__ldg(a.dinv + i) * rv);
+    if (node_owned(a.m, (int)i)) {
+      rr += rv * rv;
+      rz += rv * (__ldg(a.dinv + i) * rv);
+    }
   }
 }
 
@@ -520,6 +532,10 @@ struct CgCtl {
 struct SplitArgs {
   CgArgs c;
   CgCtl* ctl;
+  // distributed mode: per-phase results reduced and all-reduced outside the kernels into
+  // gA[slot] (p.q) and gB[slot][2] (r.r, r.D^-1.r); slot CG_SLOTS of gB holds the initial b
+  const double* gA;
+  const double* gB;
   double* partA;    // [CG_SLOTS][gridA]        p.q
   double* partB;    // [CG_SLOTS + 1][gridB][2] r.r, r.D^-1.r (slot CG_SLOTS: initial b)
   int gridA, gridB;
@@ -573,9 +589,14 @@ __global__ void __launch_bounds__(NT, MOM ? PFB_CGA_MINB_MOM : 3) k_cg_a(SplitAr
   __shared__ DupRow<MOM> dup[NT / 32];
   if (s.ctl->done) return;
   const long long k = s.ctl->k0 + klocal;
-  const double* pbk = s.partB + (size_t)(k == 0 ? CG_SLOTS : slot_of(k - 1)) * s.gridB * 2;
+  const int sb = k == 0 ? CG_SLOTS : slot_of(k - 1);
   double cur[2];
-  reduce_parts<2>(pbk, s.gridB, bc, cur);  // ||r_k||^2, r_k.D^-1.r_k
+  if (s.gB) {
+    cur[0] = s.gB[2 * sb];
+    cur[1] = s.gB[2 * sb + 1];
+  } else {
+    reduce_parts<2>(s.partB + (size_t)sb * s.gridB * 2, s.gridB, bc, cur);  // r.r, r.D^-1.r
+  }
   const double rn = sqrt(cur[0]);
   double atol;
   if (k == 0) {
@@ -601,10 +622,14 @@ __global__ void __launch_bounds__(NT, MOM ? PFB_CGA_MINB_MOM : 3) k_cg_a(SplitAr
   }
   double beta = 0.0;
   if (k > 0) {
-    __syncthreads();
-    const double* pbp = s.partB + (size_t)(k == 1 ? CG_SLOTS : slot_of(k - 2)) * s.gridB * 2;
+    const int sp = k == 1 ? CG_SLOTS : slot_of(k - 2);
     double prev[2];
-    reduce_parts<2>(pbp, s.gridB, bc, prev);
+    if (s.gB) {
+      prev[1] = s.gB[2 * sp + 1];
+    } else {
+      __syncthreads();
+      reduce_parts<2>(s.partB + (size_t)sp * s.gridB * 2, s.gridB, bc, prev);
+    }
     beta = cur[1] / prev[1];
   }
   double* pnew = (k & 1) ? s.c.p1 : s.c.p0;
@@ -625,10 +650,16 @@ __global__ void __launch_bounds__(NT) k_cg_b(SplitArgs s, int klocal) {
   if (s.ctl->done) return;
   const long long k = s.ctl->k0 + klocal;
   double pqv[1], cur[2];
-  reduce_parts<1>(s.partA + (size_t)slot_of(k) * s.gridA, s.gridA, bc, pqv);
-  __syncthreads();
-  reduce_parts<2>(s.partB + (size_t)(k == 0 ? CG_SLOTS : slot_of(k - 1)) * s.gridB * 2,
-                  s.gridB, bc, cur);
+  const int sb = k == 0 ? CG_SLOTS : slot_of(k - 1);
+  if (s.gA) {
+    pqv[0] = s.gA[slot_of(k)];
+    cur[0] = s.gB[2 * sb];
+    cur[1] = s.gB[2 * sb + 1];
+  } else {
+    reduce_parts<1>(s.partA + (size_t)slot_of(k) * s.gridA, s.gridA, bc, pqv);
+    __syncthreads();
+    reduce_parts<2>(s.partB + (size_t)sb * s.gridB * 2, s.gridB, bc, cur);
+  }
   if (s.c.probe && !(pqv[0] > 0.0)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       s.ctl->iters = k + 1;

@@ -41,7 +41,17 @@ struct DMesh {
   const int2* tiles;  // active tile coordinates (tile column, tile row)
   const int4* nrow;   // [ny+1] packed (lo, hi, start, 0) of node rows
   const int4* erow;   // [ny]   packed (lo, hi, start, 0) of cell rows
+  // ownership (row-strip decomposition): owned nodes are [own_lo, own_hi) plus [dup_lo, n);
+  // owned cells [cell_lo, cell_hi).  Single GPU: everything owned.
+  int own_lo, own_hi, dup_lo, cell_lo, cell_hi;
 };
+
+__device__ __forceinline__ bool node_owned(const DMesh& m, int id) {
+  return (id >= m.own_lo && id < m.own_hi) || id >= m.dup_lo;
+}
+__device__ __forceinline__ bool cell_owned(const DMesh& m, int eid) {
+  return eid >= m.cell_lo && eid < m.cell_hi;
+}
 
 struct Consts {
   double Px, Mx, Py, My;      // (1 + c)/(2 hx), (1 - c)/(2 hx), same with hy; c = 1/sqrt(3)

@@ -245,8 +245,10 @@ __global__ void __launch_bounds__(NT) k_mom_prepare(MomPrepArgs a) {
     const double2 Rv = Rown[k];
     a.R[id] = Rv;
     const uchar2 mk = a.umask[id];
-    if (mk.x) rr += Rv.x * Rv.x;
-    if (mk.y) rr += Rv.y * Rv.y;
+    if (node_owned(m, id)) {
+      if (mk.x) rr += Rv.x * Rv.x;
+      if (mk.y) rr += Rv.y * Rv.y;
+    }
     if (a.full) {
       a.r[id] = make_double2(mk.x ? -Rv.x : 0.0, mk.y ? -Rv.y : 0.0);
       a.x[id] = make_double2(0.0, 0.0);
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(NT) k_evo_prepare(EvoPrepArgs a) {
           bq[q] = 2.0 * psi[q] + srcd + C.gamma * (dg[q] < pg[q] ? 1.0 : 0.0);
           if (a.extra_scheme && gate_gp(C, psi[q], pm[q], dg[q])) {
             bq[q] = bq[q] + extra_gp(C, a.extra_scheme, dg[q], trp[q], dev2[q]);
-            ngate += 1.0;
+            if (cell_owned(m, eid)) ngate += 1.0;
           }
         }
         store4(a.b, eid, bq);
@@ -442,7 +444,7 @@ __global__ void __launch_bounds__(NT) k_evo_prepare(EvoPrepArgs a) {
     const double Rv = Rown[k];
     if (a.R) a.R[id] = Rv;
     const bool fr = a.pmask[id] != 0;
-    if (fr) rr += Rv * Rv;
+    if (fr && node_owned(m, id)) rr += Rv * Rv;
     if (a.full) {
       a.r[id] = fr ? -Rv : 0.0;
       a.x[id] = 0.0;
@@ -498,7 +500,7 @@ __global__ void __launch_bounds__(NT) k_evo_prepare(EvoPrepArgs a) {
         const int id = idown[k];
         const bool fr = a.pmask[id] != 0;
         if (a.diag) a.diag[id] = dg[k];
-        if (fr && !(dg[k] > 0.0)) nonpos += 1.0;
+        if (fr && !(dg[k] > 0.0) && node_owned(m, id)) nonpos += 1.0;
         a.dinv[id] = fr ? 1.0 / dg[k] : 0.0;
       }
     }

@@ -265,7 +265,7 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
           T qv = acc_lo;
           if (!APPLY) {
             qv = N_::maskb(qv, fb_lo);
-            pq += N_::dot(p_lo, qv);
+            if (node_owned(m, id_lo)) pq += N_::dot(p_lo, qv);
           }
           N_::st(a.q, id_lo, qv);
         }
@@ -274,7 +274,7 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
           T qv = add_t(c1l, f[0]);
           if (!APPLY) {
             qv = N_::maskb(qv, dup.fb[lane]);
-            pq += N_::dot(dup.p[lane], qv);
+            if (node_owned(m, idd)) pq += N_::dot(dup.p[lane], qv);
           }
           N_::st(a.q, idd, qv);
         }
@@ -282,7 +282,7 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
         T qv = add_t(add_t(acc_lo, c1l), f[0]);
         if (!APPLY) {
           qv = N_::maskb(qv, fb_lo);
-          pq += N_::dot(p_lo, qv);
+          if (node_owned(m, id_lo)) pq += N_::dot(p_lo, qv);
         }
         N_::st(a.q, id_lo, qv);
       }
@@ -414,18 +414,18 @@ __device__ __forceinline__ void march_mom_ring(const CgArgs& a, const MarchGeom&
       if (use_dup) {
         if (id_lo >= 0) {
           const T qv = N_::maskb(acc_lo, fb_lo);
-          pq += N_::dot(p_lo, qv);
+          if (node_owned(m, id_lo)) pq += N_::dot(p_lo, qv);
           N_::st(a.q, id_lo, qv);
         }
         const int idd = dup.id[lane];
         if (idd >= 0) {
           const T qv = N_::maskb(add_t(c1l, f[0]), dup.fb[lane]);
-          pq += N_::dot(dup.p[lane], qv);
+          if (node_owned(m, idd)) pq += N_::dot(dup.p[lane], qv);
           N_::st(a.q, idd, qv);
         }
       } else if (id_lo >= 0) {
         const T qv = N_::maskb(add_t(add_t(acc_lo, c1l), f[0]), fb_lo);
-        pq += N_::dot(p_lo, qv);
+        if (node_owned(m, id_lo)) pq += N_::dot(p_lo, qv);
         N_::st(a.q, id_lo, qv);
       }
     }

@@ -69,7 +69,8 @@ def _pins(pinned) -> tuple:
 class DeviceSession:
     """All device state for one (mesh, material, solver-config) triple on one GPU."""
 
-    def __init__(self, mesh_or_layout, params, config, device: int | None = None):
+    def __init__(self, mesh_or_layout, params, config, device: int | None = None,
+                 strip=None):
         self.lib = N.load()
         lay = (mesh_or_layout if isinstance(mesh_or_layout, StructuredLayout)
                else StructuredLayout.from_mesh(mesh_or_layout))
@@ -102,7 +103,12 @@ class DeviceSession:
                          1.0e-12, 20)
         self.params, self.config = params, config
         h = C.c_void_p()
-        st = self.lib.pf_create(C.byref(mesh), C.byref(mat), C.byref(cfg), device, C.byref(h))
+        if strip is None:
+            st = self.lib.pf_create(C.byref(mesh), C.byref(mat), C.byref(cfg), device,
+                                    C.byref(h))
+        else:
+            st = self.lib.pf_create_strip(C.byref(mesh), C.byref(mat), C.byref(cfg), device,
+                                          C.byref(strip), C.byref(h))
         if st != N.PF_OK or not h.value:
             raise (ValueError if st == N.PF_ERR_INVALID else DeviceError)(
                 f"pf_create failed with status {st} (see stderr)")

@@ -27,13 +27,13 @@ def run_case(case, scheme, steps=None):
     return pb, recs
 
 
-def check_against_golden(recs, z, state, case, scheme, mesh, fcol=7):
+def check_against_golden(recs, z, state, case, scheme, mesh, fcol=7, run_file=None):
     """Per-step n_stag within the reference algorithm's round-off band (conftest.stag_band),
     reaction within 1e-6 of the peak force, final phase field within 1e-6 in L-inf -- modulo
     the reflection symmetry for the symmetric tension case (conftest.mirror_perm)."""
     tab = z["table"]
     assert len(recs) == len(tab)
-    band = stag_band(case, scheme, len(tab))
+    band = stag_band(case, scheme, len(tab), run_file)
     fpeak = np.abs(tab[:, fcol]).max()
     for r, row, b in zip(recs, tab, band):
         d_stag = abs(r.n_stag - int(row[1]))
@@ -83,7 +83,8 @@ def test_cfg2_first_steps(cuda_ok):
     """BASELINE configs[1] at full size (512x512, 790k DOFs): first two load steps."""
     z = golden("run_cfg2_ST_2steps.npz")
     pb, recs = run_case("cfg2", "ST", steps=2)
-    check_against_golden(recs, z, pb.state, "cfg2", "ST", pb.mesh)
+    check_against_golden(recs, z, pb.state, "cfg2", "ST", pb.mesh,
+                         run_file="run_cfg2_ST_2steps.npz")
 
 
 @pytest.mark.parametrize("case,scheme", [("tension16", "S1"), ("tension16", "S2"),
