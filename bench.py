@@ -16,6 +16,9 @@ schedule: W untimed warm-up load steps advance the state, then K load steps are 
   168 B * N_nodes per PCG iteration / its CUDA-event time.
 * ``cpu_baseline`` — the CPU oracle port (oracle/phasefield_oracle.py, SuperLU like the
   reference default) on the first load step of the same case, rank 0 only.
+* ``--gpus N`` (torchrun, one process per GPU) — the same cfg2 problem split into N row strips
+  (``dist.StripSession``: NCCL halo rows + all-reduces captured in CUDA graphs), strong
+  scaling; value = global DOF-iterations / max-over-ranks device time.
 * ``--impl reference`` — the reference's CPU algorithm (the oracle port; the Python reference
   does not travel to the GPU box) on the same case/metric; load steps until K are done or a
   time budget is spent.
@@ -114,10 +117,50 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------------------------------------
+class _Single:
+    """N = 1: one DeviceSession on the whole mesh (persistent cooperative PCG)."""
+
+    def __init__(self, pb, local):
+        from paper_2209_07969_b200.session import DeviceSession
+
+        self.s = DeviceSession(pb.disc.layout, pb.params, pb.config, device=local)
+        self.pb = pb
+        self.n_local = pb.mesh.n_nodes
+
+    def push(self, state):
+        self.s.push_state(state)
+
+    def step(self, scheme):
+        return self.s.step(scheme, self.pb.bcs, self.pb.pins)
+
+
+class _Strip:
+    """N > 1: one row strip per rank, NCCL halos and all-reduces (pf_create_strip)."""
+
+    def __init__(self, pb, rank, ws, local):
+        import torch.distributed as dist
+
+        from paper_2209_07969_b200.dist import StripSession, nccl_unique_id
+
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        self.s = StripSession(pb.disc.layout, pb.params, pb.config, rank, ws, "nccl",
+                              device=local, nccl_id=obj[0])
+        self.pb = pb
+        self.n_local = self.s.strip.n_local
+
+    def push(self, state):
+        g = state.gp
+        self.s.push_global(state.u, state.d, state.d_prev, g.tr_eps_plus, g.dev_dot_dev,
+                           g.psi_plus, g.psi_max)
+
+    def step(self, scheme):
+        return self.s.step(scheme, self.pb.bcs, self.pb.pins)
+
+
 def run_ours(args, ws, rank, local):
     from paper_2209_07969_b200 import configs as C
     from paper_2209_07969_b200 import schemes
-    from paper_2209_07969_b200.session import DeviceSession
 
     case = C.get_case(args.case)
     if ws > 1:
@@ -128,10 +171,11 @@ def run_ours(args, ws, rank, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     pb = C.setup(case, C.b200_api())
     n_nodes, n_elems = pb.mesh.n_nodes, pb.mesh.n_elems
-    sess = DeviceSession(pb.disc.layout, pb.params, pb.config, device=local)
-    sess.push_state(pb.state)
+    run = _Single(pb, local) if ws == 1 else _Strip(pb, rank, ws, local)
+    sess = run.s if ws == 1 else run.s.sess
+    run.push(pb.state)
     for _ in range(args.warmup):
-        sess.step(args.scheme, pb.bcs, pb.pins)
+        run.step(args.scheme)
     sess.synchronize()
     barrier(ws)
     tot = dict(ms=0.0, n_stag=0, cg_u=0, cg_d=0, ms_u=0.0, ms_d=0.0, dofit=0.0, launches=0,
@@ -140,7 +184,8 @@ def run_ours(args, ws, rank, local):
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             sess.flush_l2()  # inputs of a 512^2 load step fit in L2: flush between steps
-            st = sess.step(args.scheme, pb.bcs, pb.pins)  # synchronizes at its end
+            barrier(ws)
+            st = run.step(args.scheme)  # synchronizes at its end
             ms = st.step_ms  # CUDA events on the solver stream around the whole load step
             per_step.append(ms)
             tot["ms"] += ms
@@ -156,36 +201,59 @@ def run_ours(args, ws, rank, local):
     sess.synchronize()
     barrier(ws)
     t_max = allreduce_max(ws, tot["ms"])
-    # e2e: the reference-facing drop-in with host SolverState, copies inside the timed region
+    # e2e: host SolverState in, host SolverState out, every step (copies inside the timing)
     pb2 = C.setup(case, C.b200_api())
     kind = schemes.SchemeKind(args.scheme)
-    for _ in range(args.warmup):
-        schemes.staggered_step(pb2.disc, pb2.state, kind, pb2.bcs, pb2.params, pb2.config,
-                               pb2.pins)
     e2e_stag = 0
-    barrier(ws)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        s2 = schemes.staggered_step(pb2.disc, pb2.state, kind, pb2.bcs, pb2.params, pb2.config,
-                                    pb2.pins)
-        e2e_stag += s2.n_stag
-    e2e_ms = allreduce_max(ws, (time.perf_counter() - t0) * 1e3)
-    h2d = 8 * (2 * n_nodes + 2 * n_nodes + 4 * 4 * n_elems)  # u, d, d_prev, 4 GP arrays
-    d2h = h2d + 8 * (16 + 4) * n_elems if schemes.SYNC_GP_STRAIN else h2d
+    if ws == 1:
+        for _ in range(args.warmup):
+            schemes.staggered_step(pb2.disc, pb2.state, kind, pb2.bcs, pb2.params, pb2.config,
+                                   pb2.pins)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            s2 = schemes.staggered_step(pb2.disc, pb2.state, kind, pb2.bcs, pb2.params,
+                                        pb2.config, pb2.pins)
+            e2e_stag += s2.n_stag
+        e2e_ms = (time.perf_counter() - t0) * 1e3
+        h2d = 8 * (2 * n_nodes + 2 * n_nodes + 4 * 4 * n_elems)  # u, d, d_prev, 4 GP arrays
+        d2h = h2d + 8 * (16 + 4) * n_elems if schemes.SYNC_GP_STRAIN else h2d
+        e2e_path = "paper_2209_07969_b200.schemes.staggered_step with host SolverState"
+    else:
+        run2 = _Strip(pb2, rank, ws, local)
+        ss = run2.s
+        for _ in range(args.warmup):
+            run2.push(pb2.state)
+            run2.step(args.scheme)
+        barrier(ws)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            run2.push(pb2.state)  # scatter the host state to the strip
+            s2 = run2.step(args.scheme)
+            gather_full(ss.owned_state(), pb2.state, ws)  # owned results -> every host copy
+            e2e_stag += s2.n_stag
+        e2e_ms = allreduce_max(ws, (time.perf_counter() - t0) * 1e3)
+        nl, el = ss.strip.n_local, ss.strip.layout.n_elems
+        h2d = 8 * (4 * nl + 16 * el)
+        d2h = 8 * (4 * nl + 16 * el)
+        e2e_path = ("dist.StripSession: scatter host SolverState, step, gather owned results, "
+                    "all-gather into every rank's host state")
+        run2.s.close()
     ndof = 3 * n_nodes
-    value = ws * ndof * tot["n_stag"] / (t_max / 1e3)
+    value = ndof * tot["n_stag"] / (t_max / 1e3)
     peak, peak_src = peaks()
-    mom_bytes = MOM_BYTES_PER_NODE * n_nodes
+    n_cg = run.n_local
+    mom_bytes = MOM_BYTES_PER_NODE * n_cg
     achieved = (tot["cg_u"] * mom_bytes / 1e9) / (tot["ms_u"] / 1e3) if tot["ms_u"] else 0.0
-    evo_bytes = EVO_BYTES_PER_NODE * n_nodes + EVO_BYTES_PER_ELEM * n_elems
+    evo_bytes = EVO_BYTES_PER_NODE * n_cg + EVO_BYTES_PER_ELEM * n_elems / ws
     evo_achieved = (tot["cg_d"] * evo_bytes / 1e9) / (tot["ms_d"] / 1e3) if tot["ms_d"] else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "k_cg_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and ws == 1:
         with open(tpath) as f:
             tj = json.load(f)
         if tj.get("case") == args.case and tot["cgl_u"]:
             traffic = tj["dram_bytes_per_iter"] * tot["cg_u"] / tot["cgl_u"]
+    launches = int(allreduce_sum(ws, float(tot["launches"])))
     res = {
         "metric": "DOF-iterations/s of staggered solve (FP64)",
         "value": value,
@@ -195,7 +263,7 @@ def run_ours(args, ws, rank, local):
         "warmup": args.warmup,
         "ms_per_step": t_max / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if ws == 1 else "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (BASELINE configs[1] recipe: seeded structured mesh, no dataset)",
@@ -203,39 +271,42 @@ def run_ours(args, ws, rank, local):
             "workload": f"{args.case}: {case.note}; scheme {args.scheme}; load steps "
                         f"{args.warmup + 1}..{args.warmup + args.steps}",
             "n_nodes": n_nodes, "n_elems": n_elems, "dofs": ndof,
-            "parallelism": "replicas" if ws > 1 else "single-gpu",
+            "parallelism": "single-gpu" if ws == 1 else f"row strips x{ws} (NCCL halos)",
             "l2": "flushed (256 MiB write) before each timed load step, outside the timing",
-            "timing": "CUDA events on the solver stream around each pf_staggered_step",
+            "timing": "CUDA events on the solver stream around each pf_staggered_step; "
+                      "max over ranks",
         },
-        "load_steps_per_s": ws * args.steps / (t_max / 1e3),
-        "solver_dof_iter_per_s": ws * tot["dofit"] / (t_max / 1e3),
+        "load_steps_per_s": args.steps / (t_max / 1e3),
+        "solver_dof_iter_per_s": allreduce_sum(ws, tot["dofit"]) / (t_max / 1e3),
         "n_stag_total": tot["n_stag"],
         "pcg_iters": {"momentum": tot["cg_u"], "phase_field": tot["cg_d"],
                       "momentum_launches": tot["cgl_u"], "phase_field_launches": tot["cgl_d"]},
         "kernel_ms": {"momentum_pcg": tot["ms_u"], "phase_field_pcg": tot["ms_d"]},
         "roofline": {
-            "kernel": "k_cg (momentum PCG, persistent cooperative)",
+            "kernel": "k_cg<true> (momentum PCG, persistent cooperative)" if ws == 1 else
+                      "momentum PCG (k_cg_a/k_cg_b + NCCL, rank 0's strip)",
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_source": peak_src,
             "algorithmic_bytes": "168 B x N_nodes per momentum PCG iteration",
             "phase_field_achieved": evo_achieved,
         },
-        "e2e": {"value": ws * ndof * e2e_stag / (e2e_ms / 1e3), "unit": "DOF-iter/s",
+        "e2e": {"value": ndof * e2e_stag / (e2e_ms / 1e3), "unit": "DOF-iter/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms / args.steps,
-                "path": "paper_2209_07969_b200.schemes.staggered_step with host SolverState"},
-        "gpu_launches": tot["launches"],
+                "ms_per_step": e2e_ms / args.steps, "path": e2e_path},
+        "gpu_launches": launches,
         "clocks": clk.summary(),
         "per_step_ms": [round(x, 3) for x in per_step],
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(args, case)
-    sess.close()
     if ws > 1:
+        run.s.close()
         import torch.distributed as dist
 
         dist.destroy_process_group()
+    else:
+        sess.close()
     return res if rank == 0 else None
 
 
@@ -244,6 +315,50 @@ def barrier(ws):
         import torch.distributed as dist
 
         dist.barrier()
+
+
+def gather_full(own, state, ws):
+    """All-gather the ranks' owned nodal / cell results into the full host SolverState."""
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+    def allgather_rows(mat):
+        t = torch.from_numpy(np.ascontiguousarray(mat)).to(dev)
+        n = torch.tensor([t.shape[0]], device=dev)
+        ns = [torch.zeros_like(n) for _ in range(ws)]
+        dist.all_gather(ns, n)
+        m = int(max(int(x) for x in ns))
+        pad = torch.zeros((m, t.shape[1]), dtype=t.dtype, device=dev)
+        pad[: t.shape[0]] = t
+        outs = [torch.empty_like(pad) for _ in range(ws)]
+        dist.all_gather(outs, pad)
+        return np.concatenate([o[: int(k)].cpu().numpy() for o, k in zip(outs, ns)])
+
+    nodes = allgather_rows(np.column_stack([own["nodes"].astype(np.float64), own["u"],
+                                            own["d"], own["d_prev"]]))
+    ids = nodes[:, 0].astype(np.int64)
+    state.u.reshape(-1, 2)[ids] = nodes[:, 1:3]
+    state.d[ids] = nodes[:, 3]
+    state.d_prev[ids] = nodes[:, 4]
+    gp = state.gp
+    cells = allgather_rows(np.column_stack([own["cells"].astype(np.float64)] + [
+        own[k].reshape(-1, 4) for k in ("tr_eps_plus", "dev_dot_dev", "psi_plus", "psi_max")]))
+    cid = cells[:, 0].astype(np.int64)
+    for j, k in enumerate(("tr_eps_plus", "dev_dot_dev", "psi_plus", "psi_max")):
+        getattr(gp, k)[cid] = cells[:, 1 + 4 * j: 5 + 4 * j]
+
+
+def allreduce_sum(ws, v):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
 
 
 def allreduce_max(ws, v):

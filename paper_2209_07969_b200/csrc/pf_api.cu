@@ -61,6 +61,14 @@ struct pf_handle {
   double* d_scal = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
   int cg_grid = 1, cg_grid_evo = 1, sm_count = 0;
+  // warm starts of the momentum PCG: previous solution of the same kind of Newton system
+  // slot 0: the load-increment pass; slot s (1..WARM_SLOTS-1): staggered pass s (the last
+  // slot also serves later passes) -- the previous load step's solve at the same pass index
+  static constexpr int WARM_SLOTS = 4;
+  bool warm = true;
+  bool trace = false;
+  double* warm_buf[WARM_SLOTS] = {nullptr, nullptr, nullptr, nullptr};
+  bool warm_ok[WARM_SLOTS] = {false, false, false, false};
   size_t cg_dyn_smem = 0;
   pfb::MarchGeom geom_mom{}, geom_evo{}, geom_apply{};
   // split-phase PCG (pf_cg.cuh: k_cg_a / k_cg_b chained in CUDA graphs)
@@ -77,6 +85,7 @@ struct pf_handle {
   double* d_red = nullptr;  // [16] device scalars for all-reduces
   double* gA = nullptr;     // [CG_SLOTS]       global p.q
   double* gB = nullptr;     // [CG_SLOTS+1][2]  global r.r, r.D^-1.r
+  cudaGraphExec_t dgraphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // dist chunks
   long long l2_bytes = 0;
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
@@ -200,10 +209,14 @@ extern "C" void pf_destroy(pf_handle* h) {
                   h->u, h->d, h->dprev, h->trp, h->dev2, h->psi, h->psimax,
                   h->Ru, h->ru, h->xu, h->qu, h->p0u, h->p1u, h->dinvu, h->diagu, h->flags,
                   h->umask, h->Rd, h->rd, h->xd, h->qd, h->p0d, h->p1d, h->dinvd, h->diagd,
-                  h->b, h->pmask, h->partials, h->scratch, h->d_idx, h->flushbuf};
+                  h->b, h->pmask, h->partials, h->scratch, h->d_idx, h->flushbuf,
+                  h->warm_buf[0], h->warm_buf[1], h->warm_buf[2], h->warm_buf[3]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& row : h->graphs)
+    for (auto& g : row)
+      if (g) cudaGraphExecDestroy(g);
+  for (auto& row : h->dgraphs)
     for (auto& g : row)
       if (g) cudaGraphExecDestroy(g);
   delete h->comm;
@@ -414,6 +427,13 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
   CREATE_ALLOC(h->b, 4 * ne);
   CREATE_ALLOC(h->pmask, nn);
   CREATE_ALLOC(h->scratch, 16 * ne);
+  for (int w = 0; w < pf_handle::WARM_SLOTS; ++w) CREATE_ALLOC(h->warm_buf[w], 2 * nn);
+  {
+    const char* w = getenv("PFB200_WARM");
+    h->warm = !(w && std::string(w) == "0");
+    const char* tr = getenv("PFB200_TRACE");
+    h->trace = tr && std::string(tr) == "1";
+  }
   CREATE_CUDA(cudaMemsetAsync(h->umask, 1, 2 * nn, h->stream));
   CREATE_CUDA(cudaMemsetAsync(h->pmask, 1, nn, h->stream));
   int dev_sms = 0, occ = 0, occ_evo = 0, l2 = 0;
@@ -760,10 +780,11 @@ static pf_status cg_status(pf_handle* h, int status, long long iters) {
 
 // one persistent PCG solve (single cooperative launch)
 static pf_status run_cg_persistent(pf_handle* h, bool mom, double* target, bool probe,
-                                   int* status, long long* iters) {
+                                   int* status, long long* iters, const double* guess) {
   pfb::CgArgs a = cg_args(h, mom);
   a.target = target;
   a.probe = probe ? 1 : 0;
+  a.guess = guess;
   void* args[] = {&a};
   const void* fn = mom ? (const void*)pfb::k_cg<true> : (const void*)pfb::k_cg<false>;
   const int grid = mom ? h->cg_grid : h->cg_grid_evo;
@@ -870,30 +891,54 @@ static pf_status run_cg_dist(pf_handle* h, bool mom, double* target, bool probe,
                                             s.gridB, 2, gb0);
   PF_TRY(launched(h));
   PF_TRY(comm_check(h, h->comm->allreduce(gb0, 2, h->stream)));
-  for (long long k = 0;; ++k) {
-    const int sl = (int)(k % pfb::CG_SLOTS);
-    if (mom) pfb::k_cg_a<true><<<s.gridA, pfb::NT, 0, h->stream>>>(s, (int)k);
-    else pfb::k_cg_a<false><<<s.gridA, pfb::NT, 0, h->stream>>>(s, (int)k);
+  // one iteration k = k0 + kl (kl < chunk, chunk % 6 == 0 so slot and parity depend on kl only)
+  auto iteration = [&](int kl) -> pf_status {
+    const int sl = kl % pfb::CG_SLOTS;
+    if (mom) pfb::k_cg_a<true><<<s.gridA, pfb::NT, 0, h->stream>>>(s, kl);
+    else pfb::k_cg_a<false><<<s.gridA, pfb::NT, 0, h->stream>>>(s, kl);
     PF_TRY(launched(h));
     pfb::k_finalize<<<1, 256, 0, h->stream>>>(h->partA + (size_t)sl * s.gridA, s.gridA, 1,
                                               h->gA + sl);
     PF_TRY(launched(h));
     PF_TRY(comm_check(h, h->comm->allreduce(h->gA + sl, 1, h->stream)));
-    if (mom) pfb::k_cg_b<true><<<s.gridB, pfb::NT, 0, h->stream>>>(s, (int)k);
-    else pfb::k_cg_b<false><<<s.gridB, pfb::NT, 0, h->stream>>>(s, (int)k);
+    if (mom) pfb::k_cg_b<true><<<s.gridB, pfb::NT, 0, h->stream>>>(s, kl);
+    else pfb::k_cg_b<false><<<s.gridB, pfb::NT, 0, h->stream>>>(s, kl);
     PF_TRY(launched(h));
     pfb::k_finalize<<<1, 256, 0, h->stream>>>(h->partB + (size_t)sl * s.gridB * 2, s.gridB, 2,
                                               h->gB + 2 * sl);
     PF_TRY(launched(h));
     PF_TRY(comm_check(h, h->comm->allreduce(h->gB + 2 * sl, 2, h->stream)));
     PF_TRY(halo(h, s.c.r, comps));
-    PF_TRY(halo(h, (k & 1) ? s.c.p1 : s.c.p0, comps));
-    if ((k + 1) % h->chunk == 0) {
-      PF_CUDA(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(pfb::CgCtl), cudaMemcpyDeviceToHost,
-                              h->stream));
-      PF_CUDA(cudaStreamSynchronize(h->stream));
-      if (h->h_ctl->done) break;
+    PF_TRY(halo(h, (kl & 1) ? s.c.p1 : s.c.p0, comps));
+    return PF_OK;
+  };
+  const int chunk = std::max(6, (h->chunk / 6) * 6);
+  cudaGraphExec_t* gexec = &h->dgraphs[mom ? 1 : 0][probe ? 1 : 0];
+  if (h->comm->capturable() && !*gexec) {  // record the chunk once: kernels + NCCL
+    cudaGraph_t graph;
+    PF_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    pf_status st = PF_OK;
+    for (int kl = 0; kl < chunk && st == PF_OK; ++kl) st = iteration(kl);
+    pfb::k_cg_advance<<<1, 1, 0, h->stream>>>(h->d_ctl, chunk);
+    cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+    if (st != PF_OK) return st;
+    PF_CUDA(ce);
+    PF_CUDA(cudaGraphInstantiate(gexec, graph, 0));
+    PF_CUDA(cudaGraphDestroy(graph));
+  }
+  for (;;) {
+    if (h->comm->capturable()) {
+      PF_CUDA(cudaGraphLaunch(*gexec, h->stream));
+      h->acc.launches += 5 * chunk + 1;
+    } else {
+      for (int kl = 0; kl < chunk; ++kl) PF_TRY(iteration(kl));
+      pfb::k_cg_advance<<<1, 1, 0, h->stream>>>(h->d_ctl, chunk);
+      PF_TRY(launched(h));
     }
+    PF_CUDA(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(pfb::CgCtl), cudaMemcpyDeviceToHost,
+                            h->stream));
+    PF_CUDA(cudaStreamSynchronize(h->stream));
+    if (h->h_ctl->done) break;
   }
   *status = h->h_ctl->status;
   *iters = h->h_ctl->iters;
@@ -907,10 +952,10 @@ static pf_status run_cg_dist(pf_handle* h, bool mom, double* target, bool probe,
 }
 
 static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
-                        long long* iters) {
+                        long long* iters, const double* guess = nullptr) {
   if (h->comm) return run_cg_dist(h, mom, target, probe, status, iters);
   return h->split ? run_cg_split(h, mom, target, probe, status, iters)
-                  : run_cg_persistent(h, mom, target, probe, status, iters);
+                  : run_cg_persistent(h, mom, target, probe, status, iters, guess);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -923,7 +968,7 @@ struct BcView {
 };
 
 static pf_status momentum(pf_handle* h, const BcView& bc, bool apply_inc, double* r0,
-                          int* n_nr_out, double* last_ratio) {
+                          int* n_nr_out, double* last_ratio, int pass) {
   // kinematic increments (schemes.py:207-209): u[dofs] += inc for unique dofs of each pair
   std::vector<int64_t> cons;
   for (int k = 0; k < bc.n; ++k) {
@@ -973,7 +1018,21 @@ static pf_status momentum(pf_handle* h, const BcView& bc, bool apply_inc, double
       PF_TRY(halo(h, h->xu, 2));
       PF_TRY(axpy(h, h->u, h->xu, 2LL * h->n_nodes));
     } else {
-      PF_TRY(run_cg(h, true, h->u, false, &status, &iters));
+      // warm start of the first Newton step from the previous solve of the same kind (the
+      // load-increment pass or a staggered pass); later Newton corrections start from zero
+      const int ws = std::min(std::max(pass, 0), pf_handle::WARM_SLOTS - 1);
+      double* wbuf = h->warm_buf[ws];
+      bool& wok = h->warm_ok[ws];
+      const double* guess = (h->warm && n_nr == 0 && wok) ? wbuf : nullptr;
+      PF_TRY(run_cg(h, true, h->u, false, &status, &iters, guess));
+      if (h->trace)
+        fprintf(stderr, "[pfb200] momentum pass %d newton %d warm %d iters %lld\n", pass, n_nr,
+                guess != nullptr, iters);
+      if (h->warm && n_nr == 0) {
+        PF_CUDA(cudaMemcpyAsync(wbuf, h->xu, 2 * sizeof(double) * h->n_nodes,
+                                cudaMemcpyDeviceToDevice, h->stream));
+        wok = true;
+      }
     }
     n_nr += 1;
   }
@@ -1046,6 +1105,9 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
     } else {
       PF_TRY(run_cg(h, false, h->d, false, &status, &iters));
     }
+    if (h->trace)
+      fprintf(stderr, "[pfb200] evolution newton %d gated %d iters %lld\n", n_nr, (int)gated,
+              iters);
     n_nr += 1;
   }
   *n_nr_out = n_nr;
@@ -1085,7 +1147,7 @@ extern "C" pf_status pf_staggered_step(pf_handle* h, int scheme, const int64_t* 
   PF_CUDA(cudaEventRecord(h->evs0, h->stream));
   double t0 = now_s();
   int nnr = 0;
-  PF_TRY(momentum(h, bc, true, &r0_u, &nnr, &last_u_ratio));
+  PF_TRY(momentum(h, bc, true, &r0_u, &nnr, &last_u_ratio, 0));
   st.n_nr_u += nnr;
   st.wall_u += now_s() - t0;
   double snorm;
@@ -1110,7 +1172,7 @@ extern "C" pf_status pf_staggered_step(pf_handle* h, int scheme, const int64_t* 
     st.n_nr_d += nd;
     st.wall_d += now_s() - t0;
     t0 = now_s();
-    PF_TRY(momentum(h, bc, false, &r0_u, &nnr, &last_u_ratio));
+    PF_TRY(momentum(h, bc, false, &r0_u, &nnr, &last_u_ratio, st.n_stag));
     st.n_nr_u += nnr;
     st.wall_u += now_s() - t0;
     PF_TRY(evo_norm(h, &snorm));
@@ -1143,7 +1205,7 @@ extern "C" pf_status pf_solve_momentum(pf_handle* h, const int64_t* bc_dofs,
   BcView bc{bc_dofs, bc_offsets, bc_incs, n_bc};
   int nnr = 0;
   double lr = 0.0;
-  PF_TRY(momentum(h, bc, true, r0_u, &nnr, &lr));
+  PF_TRY(momentum(h, bc, true, r0_u, &nnr, &lr, 0));
   PF_CUDA(cudaStreamSynchronize(h->stream));
   if (n_nr) *n_nr = nnr;
   if (last_ratio) *last_ratio = lr;

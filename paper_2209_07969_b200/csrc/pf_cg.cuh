@@ -90,6 +90,7 @@ struct CgArgs {
   double rtol;
   long long maxiter;
   int probe;
+  const double* guess;   // optional warm start v: x0 = gamma v, gamma = (b.v)/(v.Av)
 };
 
 template <bool MOM>
@@ -424,8 +425,62 @@ __global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k
   cg::grid_group grid = cg::this_grid();
   const int gwarp = blockIdx.x * (NT / 32) + (threadIdx.x >> 5), nwarps = gridDim.x * (NT / 32);
   double* part = a.partials;
+  double bnorm_in = -1.0;
+  if (a.guess) {
+    // v = guess restricted to free DOFs (into p1, unused before iteration 1); q = A v;
+    // gamma = (b.v)/(v.Av) is the energy-optimal multiple of v, so the start is never worse
+    // than x0 = 0 in the A-norm.  The stopping test keeps using rtol * ||b||.
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.ndof;
+         i += stride)
+      a.p1[i] = __ldg(a.dinv + i) != 0.0 ? __ldg(a.guess + i) : 0.0;
+    grid.sync();
+    for (int u = gwarp; u < a.g.n_units; u += nwarps) {
+      double dummy = 0.0;
+      march_unit<MOM, true>(a, a.g, u, true, 0.0, a.p1, nullptr, dummy,
+                            S.dup[threadIdx.x >> 5]);
+    }
+    grid.sync();
+    double bv = 0.0, vav = 0.0, bb = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.ndof;
+         i += stride) {
+      const bool fr = __ldg(a.dinv + i) != 0.0;
+      const double v = __ldcg(a.p1 + i);
+      const double qv = fr ? __ldcg(a.q + i) : 0.0;
+      const double bi = __ldcg(a.r + i);
+      if (node_owned(a.m, (int)(a.vec2 ? i >> 1 : i))) {
+        bv += bi * v;
+        vav += v * qv;
+        bb += bi * bi;
+      }
+    }
+    {
+      double v3[3] = {bv, vav, bb};
+      block_sum<3>(v3, S.red);
+      if (threadIdx.x == 0) {
+        part[4 * blockIdx.x] = v3[0];
+        part[4 * blockIdx.x + 1] = v3[1];
+        part[4 * blockIdx.x + 2] = v3[2];
+      }
+    }
+    grid.sync();
+    double g3[3];
+    grid_reduce<3>(part, 4, S.bc, g3);
+    bnorm_in = sqrt(g3[2]);
+    const double gamma = (g3[1] > 0.0 && g3[0] > 0.0) ? g3[0] / g3[1] : 0.0;
+    if (gamma > 0.0) {  // x = gamma v, r = b - gamma A v (constrained rows stay 0)
+      for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.ndof;
+           i += stride) {
+        const bool fr = __ldg(a.dinv + i) != 0.0;
+        const double v = __ldcg(a.p1 + i);
+        a.x[i] = gamma * v;
+        if (fr) a.r[i] = __ldcg(a.r + i) - gamma * __ldcg(a.q + i);
+      }
+    }
+    grid.sync();
+  }
   double rr = 0.0, rz = 0.0;
-  phase_b(a, 0.0, nullptr, false, rr, rz);  // ||b||^2 and b.D^-1.b (r = b on entry)
+  phase_b(a, 0.0, nullptr, false, rr, rz);  // ||r0||^2 and r0.D^-1.r0 (r = b on entry)
   {
     double v[2] = {rr, rz};
     block_sum<2>(v, S.red);
@@ -436,7 +491,7 @@ __global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k
   grid_reduce<2>(part, 2, S.bc, red);
   rr = red[0];
   double rho = red[1];
-  const double bnorm = sqrt(rr);
+  const double bnorm = bnorm_in >= 0.0 ? bnorm_in : sqrt(rr);  // scipy: rtol * ||b||
   const double atol = a.rtol * bnorm;
   long long k = 0;
   int status = CG_CONVERGED;

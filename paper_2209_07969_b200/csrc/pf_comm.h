@@ -39,6 +39,7 @@ struct Comm {
   // returns an error string or empty
   virtual std::string allreduce(double* d_buf, int n, cudaStream_t s) = 0;
   virtual std::string halo(double* vec, int comps, cudaStream_t s) = 0;
+  virtual bool capturable() const { return false; }  // may be recorded into a CUDA graph
 };
 
 // ---------------------------------------------------------------------------------------
@@ -89,6 +90,7 @@ struct NcclApi {
 
 struct NcclComm : Comm {
   ncclComm_t comm = nullptr;
+  bool capturable() const override { return true; }
   ~NcclComm() override {
     if (comm) NcclApi::get().CommDestroy(comm);
   }

@@ -97,3 +97,34 @@ def test_strips_equal_single_gpu_before_cracking(cuda_ok):
         assert a[:3] == b[:3]
         assert abs(a[3] - b[4][0]) <= 1e-10 * abs(a[3])
     assert np.abs(d - d1).max() <= 1e-10
+
+
+@pytest.mark.parametrize("case,scheme", [("tension16", "S1"), ("lpanel25", "ST")])
+def test_nccl_graph_path_single_rank(case, scheme, cuda_ok):
+    """The NCCL transport and the CUDA-graph capture of the distributed PCG (kernels +
+    ncclAllReduce per phase) on a 1-rank communicator: same results as the reference."""
+    from paper_2209_07969_b200.dist import StripSession, nccl_unique_id
+
+    z = golden(f"run_{case}_{scheme}.npz")
+    tab = z["table"]
+    pb = C.setup(C.get_case(case), C.b200_api())
+    ss = StripSession(pb.disc.layout, pb.params, pb.config, 0, 1, "nccl", device=0,
+                      nccl_id=nccl_unique_id())
+    s = pb.state
+    ss.push_global(s.u, s.d, s.d_prev, s.gp.tr_eps_plus, s.gp.dev_dot_dev, s.gp.psi_plus,
+                   s.gp.psi_max)
+    band = stag_band(case, scheme, len(tab))
+    fpeak = np.abs(tab[:, 7]).max()
+    for k, (row, b) in enumerate(zip(tab, band)):
+        st = ss.step(scheme, pb.bcs, pb.pins)
+        f = ss.reaction_force(*pb.reactions[0][1:])
+        assert abs(st.n_stag - int(row[1])) <= b, (k + 1, st.n_stag, row[1])
+        assert abs(f - row[7]) <= 1e-6 * fpeak, (k + 1, f, row[7])
+    own = ss.owned_state()
+    d = np.empty(pb.mesh.n_nodes)
+    d[own["nodes"]] = own["d"]
+    err = float(np.abs(d - z["final_d"]).max())
+    if C.get_case(case).loading == "tension":
+        err = min(err, float(np.abs(d - z["final_d"][mirror_perm(pb.mesh)]).max()))
+    assert err <= 1e-6, err
+    ss.close()

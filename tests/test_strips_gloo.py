@@ -114,3 +114,53 @@ def test_halo_protocol_gloo_world2(name):
         assert ok, f"rank {r}: ghost rows differ from the owners' values"
         assert cnt == n_nodes
         assert abs(s - ref) <= 1e-12 * ref
+
+
+def _gather_worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        from paper_2209_07969_b200 import configs as C
+        from paper_2209_07969_b200.schemes import SolverState
+
+        case = C.get_case("tension16")
+        mesh = C.build_mesh(case, C.b200_api())
+        lay = meshing.StructuredLayout.from_mesh(mesh)
+        st = strips.make_strip(lay, world, rank)
+        rng = np.random.default_rng(11)
+        full = {k: rng.standard_normal(n) for k, n in (
+            ("u", 2 * mesh.n_nodes), ("d", mesh.n_nodes), ("d_prev", mesh.n_nodes))}
+        gpf = {k: rng.standard_normal((mesh.n_elems, 4)) for k in (
+            "tr_eps_plus", "dev_dot_dev", "psi_plus", "psi_max")}
+        own_nodes = st.owned_global_nodes()
+        own_cells = st.cell_local_to_global[st.cell_lo:st.cell_hi]
+        own = {"nodes": own_nodes, "cells": own_cells,
+               "u": full["u"].reshape(-1, 2)[own_nodes], "d": full["d"][own_nodes],
+               "d_prev": full["d_prev"][own_nodes]}
+        own.update({k: v[own_cells] for k, v in gpf.items()})
+
+        class _Disc:
+            n_u_dofs, n_d_dofs, n_gp = 2 * mesh.n_nodes, mesh.n_nodes, 4
+
+            class mesh_:  # noqa: N801
+                n_elems = mesh.n_elems
+        _Disc.mesh = _Disc.mesh_
+        state = SolverState.zeros(_Disc)
+        bench.gather_full(own, state, world)
+        ok = (np.array_equal(state.u, full["u"]) and np.array_equal(state.d, full["d"])
+              and np.array_equal(state.d_prev, full["d_prev"])
+              and all(np.array_equal(getattr(state.gp, k), v) for k, v in gpf.items()))
+        results[rank] = ok
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_gather_full_gloo_world2():
+    """bench.py's multi-rank e2e leg rebuilds the full host state from owned strip results."""
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_gather_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    assert all(results[r] for r in range(world))
