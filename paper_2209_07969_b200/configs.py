@@ -90,6 +90,10 @@ _add(LoadCase("shear32", ("notched", 32, 32, 1.0, True), {**_TENSION_MAT, "lengt
 _add(LoadCase("lpanel25", ("lshape", 25.0),
               dict(e_mod=25850.0, nu=0.18, g_c=0.089, length_l=40.0, at_model="AT2"),
               "lpanel", 0.1, 12, ("ST", "S1"), note="cfg4 analogue (20x20 bounding grid)"))
+_add(LoadCase("multicrack256", ("notched", 256, 256, 1000.0, False),
+              dict(e_mod=10000.0, nu=0.25, g_c=0.01, length_l=2.0, at_model="AT2"),
+              "biaxial", 2.0e-3, 50, ("ST", "S1"), precracks=(8, 20220916, 5.0, 20.0),
+              note="cfg5 analogue of SURVEY.md App. B (256^2, 8 cracks, same seed logic)"))
 _add(LoadCase("multicrack32", ("notched", 32, 32, 1000.0, False),
               dict(e_mod=10000.0, nu=0.25, g_c=0.01, length_l=60.0, at_model="AT2"),
               "biaxial", 0.1, 10, ("ST", "S1"), precracks=(6, 20220916, 60.0, 160.0),

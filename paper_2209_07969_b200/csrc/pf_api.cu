@@ -439,15 +439,15 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
   int dev_sms = 0, occ = 0, occ_evo = 0, l2 = 0;
   CREATE_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
   CREATE_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
-  const size_t ring_smem = PFB_USE_RING ? sizeof(pfb::MomRing) * (pfb::NT / 32) : 0;
+  const size_t ring_smem = PFB_USE_RING ? sizeof(pfb::MomRing) * (pfb::CG_NT / 32) : 0;
   h->cg_dyn_smem = ring_smem;
   if (ring_smem > 48 * 1024)
     CREATE_CUDA(cudaFuncSetAttribute(pfb::k_cg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)ring_smem));
-  CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pfb::k_cg<true>, pfb::NT,
+  CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pfb::k_cg<true>, pfb::CG_NT,
                                                             ring_smem));
   CREATE_CUDA(
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_evo, pfb::k_cg<false>, pfb::NT, 0));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_evo, pfb::k_cg<false>, pfb::CG_NT, 0));
   h->sm_count = dev_sms;
   h->l2_bytes = l2;
   if (occ < 1 || occ_evo < 1) {
@@ -455,12 +455,13 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
     return bail(PF_ERR_CUDA);
   }
   // persistent grids: all resident warps march; unit shape from the resident warp count
-  const int wpc = pfb::NT / 32;
-  h->geom_mom = pfb::make_march_geom(nx, ny, occ * dev_sms * wpc);
-  h->geom_evo = pfb::make_march_geom(nx, ny, occ_evo * dev_sms * wpc);
+  const int wpc = pfb::NT / 32, cwpc = pfb::CG_NT / 32;
+  h->geom_mom = pfb::make_march_geom(nx, ny, occ * dev_sms * cwpc);
+  h->geom_evo = pfb::make_march_geom(nx, ny, occ_evo * dev_sms * cwpc);
   h->geom_apply = pfb::make_march_geom(nx, ny, 4 * dev_sms * wpc);
-  h->cg_grid = std::max(1, std::min(occ * dev_sms, (h->geom_mom.n_units + wpc - 1) / wpc));
-  h->cg_grid_evo = std::max(1, std::min(occ_evo * dev_sms, (h->geom_evo.n_units + wpc - 1) / wpc));
+  h->cg_grid = std::max(1, std::min(occ * dev_sms, (h->geom_mom.n_units + cwpc - 1) / cwpc));
+  h->cg_grid_evo =
+      std::max(1, std::min(occ_evo * dev_sms, (h->geom_evo.n_units + cwpc - 1) / cwpc));
   {  // split-phase PCG geometry: phase A one wave of resident CTAs, phase B 4 CTAs per SM
     const char* mode = getenv("PFB200_CG");  // "split": graph-chained phase kernels (A/B tests)
     h->split = mode && std::string(mode) == "split";
@@ -789,7 +790,7 @@ static pf_status run_cg_persistent(pf_handle* h, bool mom, double* target, bool 
   const void* fn = mom ? (const void*)pfb::k_cg<true> : (const void*)pfb::k_cg<false>;
   const int grid = mom ? h->cg_grid : h->cg_grid_evo;
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
-  PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(pfb::NT), args,
+  PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(pfb::CG_NT), args,
                                       mom ? h->cg_dyn_smem : 0, h->stream));
   PF_TRY(launched(h));
   PF_CUDA(cudaEventRecord(h->ev1, h->stream));

@@ -10,51 +10,26 @@
 //   phase B (flat):  r -= alpha q, x += alpha p_k, partials r.r and r.D^-1.r
 // The SPD probe (K10, SURVEY.md §7 hard part 1) aborts at p.q <= 0.
 //
-// Latency structure: thread t owns node slot t of its tile (TX x TY = NT), so the owned node's
-// r, D^-1 and p stay in registers from the halo phase to the gather; the halo border and the slit
-// duplicates are spread over the first threads; node/cell ids come from the row tables through
-// the read-only path (L1-resident), so a tile needs three CTA barriers.
+// Phase A is the barrier-free warp march of pf_march.cuh (the first version of this kernel used
+// 32x8 shared-memory tiles with three CTA barriers per tile; profiles/README.md has the history).
 #pragma once
 #include <type_traits>
 
 namespace pfb {
 
-constexpr int NBORDER = 2 * HX + 2 * TY;  // halo ring slots around the TX x TY owned block
 #ifndef PFB_PHASEB_UNROLL
 #define PFB_PHASEB_UNROLL 2
 #endif
+#ifndef PFB_CG_NT
+#define PFB_CG_NT 256
+#endif
+constexpr int CG_NT = PFB_CG_NT;  // block size of the persistent PCG kernel
 #ifndef PFB_CG_MINB_MOM
 #define PFB_CG_MINB_MOM 2
 #endif
 #ifndef PFB_CG_MINB_EVO
 #define PFB_CG_MINB_EVO 2
 #endif
-
-struct SmemMomA {
-  double2 p[HY][HX];
-  double2 pdup[HX];
-  double d[HY][HX];
-  double ddup[HX];
-  double2 f[4][EY][EX];
-};
-
-struct SmemEvoA {
-  double p[HY][HX];
-  double pdup[HX];
-  double f[4][EY][EX];
-};
-
-// extra slot e (0 .. NBORDER + HX) -> halo position; returns false for the dup row
-__device__ __forceinline__ bool border_pos(int e, int& hx, int& hy) {
-  if (e < HX) { hx = e; hy = 0; return true; }
-  e -= HX;
-  if (e < HX) { hx = e; hy = HY - 1; return true; }
-  e -= HX;
-  if (e < 2 * TY) { hx = (e & 1) ? HX - 1 : 0; hy = 1 + (e >> 1); return true; }
-  hx = e - 2 * TY;
-  hy = -1;
-  return false;
-}
 
 enum CgStatus { CG_CONVERGED = 0, CG_MAXITER = 1, CG_INDEFINITE = 2, CG_NAN = 3 };
 
@@ -133,43 +108,7 @@ struct Node<false> {
 };
 
 // ---------------------------------------------------------------------------------------
-// register-lean element operators (per Gauss point accumulation)
-__device__ __forceinline__ void mom_cell_apply_lean(const Consts& C, const double2 (&pc)[4],
-                                                    const double (&dc)[4], unsigned flags,
-                                                    double2 (&f)[4]) {
-  const double bx = pc[1].x - pc[0].x, tx = pc[2].x - pc[3].x;
-  const double by = pc[1].y - pc[0].y, ty = pc[2].y - pc[3].y;
-  const double lx = pc[3].x - pc[0].x, rx = pc[2].x - pc[1].x;
-  const double ly = pc[3].y - pc[0].y, ry = pc[2].y - pc[1].y;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) f[q] = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    // dN/dx = [-A, A, B, -B], dN/dy = [-Cc, -D, D, Cc] at this Gauss point
-    const double A = g < 2 ? C.Px : C.Mx, B = g < 2 ? C.Mx : C.Px;
-    const double Cc = (g == 0 || g == 3) ? C.Py : C.My, D = (g == 0 || g == 3) ? C.My : C.Py;
-    const double dg = C.N[g][0] * dc[0] + C.N[g][1] * dc[1] + C.N[g][2] * dc[2] +
-                      C.N[g][3] * dc[3];
-    const double gg = degradation(C, dg);
-    const double exx = A * bx + B * tx;
-    const double eyy = Cc * ly + D * ry;
-    const double gxy = Cc * lx + D * rx + A * by + B * ty;
-    double sxx, syy, sxy;
-    tangent_gp(C, exx, eyy, gxy, gg, (flags >> g) & 1u, sxx, syy, sxy);
-    sxx *= C.w;
-    syy *= C.w;
-    sxy *= C.w;
-    f[0].x += -A * sxx - Cc * sxy;
-    f[1].x += A * sxx - D * sxy;
-    f[2].x += B * sxx + D * sxy;
-    f[3].x += -B * sxx + Cc * sxy;
-    f[0].y += -Cc * syy - A * sxy;
-    f[1].y += -D * syy + A * sxy;
-    f[2].y += D * syy + B * sxy;
-    f[3].y += Cc * syy - B * sxy;
-  }
-}
-
+// phase-field element operator: (sum_g N b N^T w + grad_w L) p_e
 __device__ __forceinline__ void evo_cell_apply(const Consts& C, const double (&pc)[4],
                                                const double (&bq)[4], double (&f)[4]) {
   double t4[4];
@@ -182,134 +121,6 @@ __device__ __forceinline__ void evo_cell_apply(const Consts& C, const double (&p
     f[aa] = C.Nw[0][aa] * t4[0] + C.Nw[1][aa] * t4[1] + C.Nw[2][aa] * t4[2] +
             C.Nw[3][aa] * t4[3] + C.lap[aa][0] * pc[0] + C.lap[aa][1] * pc[1] +
             C.lap[aa][2] * pc[2] + C.lap[aa][3] * pc[3];
-}
-
-// ---------------------------------------------------------------------------------------
-// Phase A of one tile.  APPLY=true: plain y = A x (x from `pold`, y to a.q, unmasked, no
-// p/x bookkeeping) — used by pf_*_tangent_apply.
-template <bool MOM, bool APPLY, class SM>
-__device__ __forceinline__ void phase_a_tile(const CgArgs& a, SM& S, int tile, bool first,
-                                             double beta, double alpha_prev,
-                                             const double* __restrict__ pold,
-                                             double* __restrict__ pnew, double& pq) {
-  using NT_ = Node<MOM>;
-  using T = typename NT_::T;
-  const DMesh& m = a.m;
-  const Consts& C = a.C;
-  const int2 tl = m.tiles[tile];
-  const int tx0 = tl.x * TX, ty0 = tl.y * TY;
-  const int tid = threadIdx.x;
-  // ---- owned slot of this thread
-  const int ox = tid % TX, oy = tid / TX;
-  const int oi = tx0 + ox, oj = ty0 + oy;
-  const int oid = node_at(m, oi, oj);
-  T own_di = NT_::zero(), own_p = NT_::zero();
-  if (oid >= 0) {
-    if (APPLY) {
-      own_p = NT_::ld_ro(pold, oid);
-    } else {
-      own_di = NT_::ld_ro(a.dinv, oid);
-      own_p = NT_::mul(own_di, NT_::ld_cg(a.r, oid));
-      if (!first) {
-        const T po = NT_::ld_cg(pold, oid);
-        own_p = NT_::axpy(beta, po, own_p);
-        NT_::st(a.x, oid, NT_::axpy(alpha_prev, po, NT_::ld_cg(a.x, oid)));
-      }
-      NT_::st(pnew, oid, own_p);
-    }
-  }
-  S.p[oy + 1][ox + 1] = own_p;
-  if constexpr (MOM) S.d[oy + 1][ox + 1] = oid >= 0 ? __ldg(a.d + oid) : 0.0;
-  // ---- halo ring and slit duplicates
-  const bool dup = tile_has_dup(m, ty0);
-  const int nextra = NBORDER + (dup ? HX : 0);
-  for (int e = tid; e < nextra; e += NT) {
-    int hx, hy;
-    const bool ring = border_pos(e, hx, hy);
-    const int i = tx0 - 1 + hx;
-    int id;
-    bool owned = false;
-    if (ring) {
-      id = node_at(m, i, ty0 - 1 + hy);
-    } else {
-      id = is_dup_col(m, i) ? m.dup_start + (i - m.notch_lo) : -1;
-      owned = m.notch_row >= ty0 && m.notch_row < ty0 + TY && hx >= 1 && hx <= TX;
-    }
-    T pn = NT_::zero();
-    double dv = 0.0;
-    if (id >= 0) {
-      if (APPLY) {
-        pn = NT_::ld_ro(pold, id);
-      } else {
-        pn = NT_::mul(NT_::ld_ro(a.dinv, id), NT_::ld_cg(a.r, id));
-        if (!first) {
-          const T po = NT_::ld_cg(pold, id);
-          pn = NT_::axpy(beta, po, pn);
-          if (owned) NT_::st(a.x, id, NT_::axpy(alpha_prev, po, NT_::ld_cg(a.x, id)));
-        }
-        if (owned) NT_::st(pnew, id, pn);
-      }
-      if constexpr (MOM) dv = __ldg(a.d + id);
-    }
-    if (ring) {
-      S.p[hy][hx] = pn;
-      if constexpr (MOM) S.d[hy][hx] = dv;
-    } else {
-      S.pdup[hx] = pn;
-      if constexpr (MOM) S.ddup[hx] = dv;
-    }
-  }
-  __syncthreads();
-  // ---- cells touching an owned node
-  for (int c = tid; c < EX * EY; c += NT) {
-    const int ex = c % EX, ey = c / EX;
-    const int ci = tx0 - 1 + ex, cj = ty0 - 1 + ey;
-    const int eid = cell_at(m, ci, cj);
-    T f[4];
-    if constexpr (MOM) {
-      f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
-      if (eid >= 0) {
-        double2 pc[4];
-        double dc[4];
-        cell_corners(m, S.p, S.pdup, ex, ey, ci, cj, pc);
-        cell_corners(m, S.d, S.ddup, ex, ey, ci, cj, dc);
-        mom_cell_apply_lean(C, pc, dc, __ldg(a.flags + eid), f);
-      }
-    } else {
-      f[0] = f[1] = f[2] = f[3] = 0.0;
-      if (eid >= 0) {
-        double pc[4], bq[4];
-        cell_corners(m, S.p, S.pdup, ex, ey, ci, cj, pc);
-        load4(a.b, eid, bq);
-        evo_cell_apply(C, pc, bq, f);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) S.f[q][ey][ex] = f[q];
-  }
-  __syncthreads();
-  // ---- owned gather (reference element order), mask, p.q
-  if (oid >= 0) {
-    const bool split = owned_split(m, oi, oj);
-    T below, above;
-    gather_corners(S.f, ox, oy, below, above);
-    T qv = split ? below : gather_all(S.f, ox, oy);
-    if (!APPLY) {
-      qv = NT_::mask(qv, own_di);
-      pq += NT_::dot(own_p, qv);
-    }
-    NT_::st(a.q, oid, qv);
-    if (split) {
-      const int idd = m.dup_start + (oi - m.notch_lo);
-      T qd = above;
-      if (!APPLY) {
-        qd = NT_::mask(qd, NT_::ld_ro(a.dinv, idd));
-        pq += NT_::dot(S.pdup[ox + 1], qd);
-      }
-      NT_::st(a.q, idd, qd);
-    }
-  }
-  __syncthreads();
 }
 
 }  // namespace pfb
@@ -410,8 +221,8 @@ __device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, const dou
 
 template <bool MOM>
 struct CgSmem {
-  DupRow<MOM> dup[NT / 32];
-  double red[NT / 32 * 2];
+  DupRow<MOM> dup[CG_NT / 32];
+  double red[CG_NT / 32 * 3];
   double bc[4];
 };
 #ifndef PFB_USE_RING
@@ -419,11 +230,12 @@ struct CgSmem {
 #endif
 
 template <bool MOM>
-__global__ void __launch_bounds__(NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k_cg(CgArgs a) {
+__global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k_cg(CgArgs a) {
   __shared__ CgSmem<MOM> S;
   extern __shared__ __align__(16) unsigned char dyn_smem[];  // MomRing per warp (momentum)
   cg::grid_group grid = cg::this_grid();
-  const int gwarp = blockIdx.x * (NT / 32) + (threadIdx.x >> 5), nwarps = gridDim.x * (NT / 32);
+  const int gwarp = blockIdx.x * (CG_NT / 32) + (threadIdx.x >> 5),
+            nwarps = gridDim.x * (CG_NT / 32);
   double* part = a.partials;
   double bnorm_in = -1.0;
   if (a.guess) {
