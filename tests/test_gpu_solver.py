@@ -181,3 +181,27 @@ def test_errors_map_to_reference_exceptions(cuda_ok):
     with pytest.raises(ConvergenceError) as ei:
         schemes.staggered_step(pb.disc, pb.state, "ST", pb.bcs, pb.params, cfg)
     assert len(ei.value.residual_history) >= 2
+
+
+@pytest.mark.parametrize("case", ["cfg3", "cfg4"])
+def test_full_size_first_step(case, cuda_ok):
+    """BASELINE configs[2] (1024^2 shear, 3.15 M DOFs) and configs[3] (L-panel h = 0.5,
+    2.26 M DOFs) at full size: the reference's first load step (fixtures store d as float32)."""
+    z = golden(f"run_{case}_ST_1steps.npz")
+    pb, recs = run_case(case, "ST", steps=1)
+    row = z["table"][0]
+    assert recs[0].n_stag == int(row[1]) and recs[0].n_nr_u == int(row[2])
+    assert abs(recs[0].reactions[0] - row[7]) <= 1e-6 * abs(row[7])
+    d_ref = z["final_d_f32"].astype(np.float64)
+    assert np.abs(pb.state.d - d_ref).max() <= 1e-6
+    umax, unorm, _ = z["final_u_stats"]
+    assert abs(np.abs(pb.state.u).max() - umax) <= 1e-8 * umax
+    assert abs(np.linalg.norm(pb.state.u) - unorm) <= 1e-8 * unorm
+
+
+def test_multicrack256_analogue(cuda_ok):
+    """SURVEY App. B cfg5 analogue: 256^2, 8 seeded pre-cracks (d = d_prev = 1), biaxial."""
+    z = golden("run_multicrack256_ST_10steps.npz")
+    pb, recs = run_case("multicrack256", "ST", steps=10)
+    check_against_golden(recs, z, pb.state, "multicrack256", "ST", pb.mesh,
+                         run_file="run_multicrack256_ST_10steps.npz")
