@@ -83,6 +83,10 @@ _add(LoadCase("cfg5", ("notched", 8192, 8192, 1000.0, False),
 _add(LoadCase("tension16", ("notched", 16, 16, 1.0, True), {**_TENSION_MAT, "length_l": 0.08},
               "tension", 6.0e-4, 16, ("ST", "S1", "S2", "S3"),
               note="cfg1/cfg2 analogue, cracks within 16 steps"))
+_add(LoadCase("tension16_at1", ("notched", 16, 16, 1.0, True),
+              {**_TENSION_MAT, "length_l": 0.08, "at_model": "AT1"},
+              "tension", 6.0e-4, 16, ("ST", "S1", "S3"),
+              note="AT1 (the reference default model) on the tension16 analogue"))
 _add(LoadCase("tension32", ("notched", 32, 32, 1.0, True), {**_TENSION_MAT, "length_l": 0.04},
               "tension", 4.0e-4, 18, ("ST", "S1", "S2", "S3"), note="cfg2 analogue"))
 _add(LoadCase("shear32", ("notched", 32, 32, 1.0, True), {**_TENSION_MAT, "length_l": 0.04},

@@ -456,8 +456,10 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
   }
   // persistent grids: all resident warps march; unit shape from the resident warp count
   const int wpc = pfb::NT / 32, cwpc = pfb::CG_NT / 32;
-  h->geom_mom = pfb::make_march_geom(nx, ny, occ * dev_sms * cwpc);
-  h->geom_evo = pfb::make_march_geom(nx, ny, occ_evo * dev_sms * cwpc);
+  const char* mr = getenv("PFB200_MIN_ROWS");
+  const int min_rows = mr ? std::max(1, atoi(mr)) : 4;
+  h->geom_mom = pfb::make_march_geom(nx, ny, occ * dev_sms * cwpc, min_rows);
+  h->geom_evo = pfb::make_march_geom(nx, ny, occ_evo * dev_sms * cwpc, min_rows);
   h->geom_apply = pfb::make_march_geom(nx, ny, 4 * dev_sms * wpc);
   h->cg_grid = std::max(1, std::min(occ * dev_sms, (h->geom_mom.n_units + cwpc - 1) / cwpc));
   h->cg_grid_evo =

@@ -446,12 +446,12 @@ __device__ __forceinline__ void march_mom_ring(const CgArgs& a, const MarchGeom&
 
 // host-side choice of the unit shape: enough units for every resident warp, but at least
 // 4 owned rows per unit so the halo rows stay a modest overhead
-inline MarchGeom make_march_geom(int nx, int ny, int resident_warps) {
+inline MarchGeom make_march_geom(int nx, int ny, int resident_warps, int min_rows = 4) {
   MarchGeom g;
   g.n_strips = (nx + 1 + TXW - 1) / TXW;
   const long long strip_rows = (long long)g.n_strips * (ny + 1);
   int rows = (int)((strip_rows + resident_warps - 1) / resident_warps);
-  rows = rows < 4 ? 4 : rows;
+  rows = rows < min_rows ? min_rows : rows;
   if (rows > ny + 1) rows = ny + 1;
   g.rows_per_unit = rows;
   g.n_row_blocks = (ny + 1 + rows - 1) / rows;

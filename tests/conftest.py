@@ -63,11 +63,16 @@ def mirror_perm(mesh) -> np.ndarray:
 
 def stag_band(case: str, scheme: str, n_steps: int, run_file: str | None = None) -> np.ndarray:
     """Per-step allowed |n_stag - reference|: 1 + spread of the round-off ensemble."""
-    path = os.path.join(GOLDEN, f"sens_{case}_{scheme}.json")
-    if not os.path.exists(path):
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(GOLDEN, f"sens_{case}_{scheme}.json")) +
+                   glob.glob(os.path.join(GOLDEN, f"sens_{case}_{scheme}_part*.json")))
+    if not paths:
         return np.ones(n_steps, dtype=int)
-    with open(path) as f:
-        sens = json.load(f)["n_stag"]
+    sens = {}
+    for path in paths:
+        with open(path) as f:
+            sens.update(json.load(f)["n_stag"])
     z = np.load(os.path.join(GOLDEN, run_file or f"run_{case}_{scheme}.npz"))
     ref = z["table"][:n_steps, 1].astype(int)
     spread = np.zeros(n_steps, dtype=int)

@@ -15,7 +15,7 @@ internal-force back-projection as one einsum or Gauss-point-pair grouped, and th
 solver direct (SuperLU) or the reference's own lin_method="cg".  The crack side taken by the
 symmetric tension test ("branch") is recorded too.
 
-    OMP_NUM_THREADS=1 python tests/golden/make_sensitivity.py tension16 ST [steps|-] [max_variants]
+    OMP_NUM_THREADS=1 python tests/golden/make_sensitivity.py tension16 ST [steps|-] [max_variants|-] [a:b]
 """
 
 from __future__ import annotations
@@ -82,13 +82,19 @@ def run_variant(case: str, scheme: str, kw: dict, steps: int | None = None) -> t
 def main() -> None:
     case, scheme = sys.argv[1], sys.argv[2]
     steps = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3] != "-" else None
-    maxv = int(sys.argv[4]) if len(sys.argv) > 4 else None
+    maxv = int(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4] != "-" else None
     variants = factorial(maxv)
+    suffix = ""
+    if len(sys.argv) > 5:  # "a:b" slice of the full factorial, written to its own part file
+        a, b = (int(x) for x in sys.argv[5].split(":"))
+        names = list(factorial())[a:b]
+        variants = {n: factorial()[n] for n in names}
+        suffix = f"_part{a}_{b}"
     t0 = time.time()
     stag, branch = {}, {}
     for name, kw in variants.items():
         stag[name], branch[name] = run_variant(case, scheme, kw, steps)
-    path = os.path.join(HERE, f"sens_{case}_{scheme}.json")
+    path = os.path.join(HERE, f"sens_{case}_{scheme}{suffix}.json")
     with open(path, "w") as f:
         json.dump({"case": case, "scheme": scheme, "n_stag": stag, "branch": branch,
                    "seconds": round(time.time() - t0, 1)}, f)
