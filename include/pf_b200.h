@@ -184,6 +184,11 @@ pf_status pf_create_strip(const pf_mesh* local_mesh, const pf_material* mat, con
                           int device, const pf_strip* strip, pf_handle** out);
 
 /* device-resident benchmarking helpers */
+/* n_iter PCG iterations of the momentum (physics 0) or phase-field (1) operator at the current
+ * state with the stopping test disabled (rtol 0): per-iteration cost at any mesh size without
+ * solving to convergence.  ms_out = CUDA-event time of the PCG launch. */
+pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, double* ms_out,
+                      int64_t* iters_out);
 pf_status pf_device_info(pf_handle* h, int32_t* cg_grid, int32_t* sm_count, int64_t* l2_bytes);
 pf_status pf_flush_l2(pf_handle* h);
 pf_status pf_synchronize(pf_handle* h);

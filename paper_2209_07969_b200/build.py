@@ -43,16 +43,22 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile libpfb200.so.  `defines`/`out`: experiment variants (e.g. -DPFB_USE_RING=1 into
+    another file, loaded through PFB200_LIB); the default library never uses them."""
+    if out is None and not defines and not force and up_to_date():
         return OUT
+    target = out or OUT
     inc = ["-I", NCCL_INCLUDE] if NCCL_INCLUDE else []
-    cmd = [nvcc(), *NVCC_FLAGS, *inc, "-ldl", "-o", OUT + ".tmp", *SOURCES]
+    cmd = [nvcc(), *NVCC_FLAGS, *inc, *[f"-D{d}" for d in defines], "-ldl",
+           "-o", target + ".tmp", *SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError(f"nvcc failed ({res.returncode}): {' '.join(cmd)}")
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(target + ".tmp", target)
+    if out is not None:
+        return target
     log = os.path.join(HERE, "csrc", "ptxas_sm100a.log")
     with open(log, "w") as f:
         f.write(res.stderr)
@@ -62,4 +68,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    argv = sys.argv[1:]
+    defs = [a[2:] for a in argv if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in argv if a.startswith("--out=")]
+    print(build(force="--force" in argv, verbose=True, defines=defs,
+                out=outs[0] if outs else None))

@@ -69,7 +69,7 @@ struct pf_handle {
   bool trace = false;
   double* warm_buf[WARM_SLOTS] = {nullptr, nullptr, nullptr, nullptr};
   bool warm_ok[WARM_SLOTS] = {false, false, false, false};
-  size_t cg_dyn_smem = 0;
+  bool xupd_mom = false, xupd_evo = false;  // lazy-x PCG variants (k_cg<MOM, true>)
   pfb::MarchGeom geom_mom{}, geom_evo{}, geom_apply{};
   // split-phase PCG (pf_cg.cuh: k_cg_a / k_cg_b chained in CUDA graphs)
   bool split = false;
@@ -439,15 +439,19 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
   int dev_sms = 0, occ = 0, occ_evo = 0, l2 = 0;
   CREATE_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
   CREATE_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
-  const size_t ring_smem = PFB_USE_RING ? sizeof(pfb::MomRing) * (pfb::CG_NT / 32) : 0;
-  h->cg_dyn_smem = ring_smem;
-  if (ring_smem > 48 * 1024)
-    CREATE_CUDA(cudaFuncSetAttribute(pfb::k_cg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)ring_smem));
-  CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pfb::k_cg<true>, pfb::CG_NT,
-                                                            ring_smem));
-  CREATE_CUDA(
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_evo, pfb::k_cg<false>, pfb::CG_NT, 0));
+  {  // both variants of each persistent kernel must be co-resident at the same grid size
+    int o1 = 0, o2 = 0;
+    CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, pfb::k_cg<true, false>,
+                                                              pfb::CG_NT, 0));
+    CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_cg<true, true>,
+                                                              pfb::CG_NT, 0));
+    occ = std::min(o1, o2);
+    CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, pfb::k_cg<false, false>,
+                                                              pfb::CG_NT, 0));
+    CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_cg<false, true>,
+                                                              pfb::CG_NT, 0));
+    occ_evo = std::min(o1, o2);
+  }
   h->sm_count = dev_sms;
   h->l2_bytes = l2;
   if (occ < 1 || occ_evo < 1) {
@@ -461,6 +465,14 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
   h->geom_mom = pfb::make_march_geom(nx, ny, occ * dev_sms * cwpc, min_rows);
   h->geom_evo = pfb::make_march_geom(nx, ny, occ_evo * dev_sms * cwpc, min_rows);
   h->geom_apply = pfb::make_march_geom(nx, ny, 4 * dev_sms * wpc);
+  {  // lazy x update only where one PCG iteration streams far more than L2 holds (measured:
+     // 8192^2 -6.5% time per iteration, 1024^2 +2.5% momentum / +10% phase field)
+    const double big = 4.0 * (double)l2;
+    h->xupd_mom = 168.0 * (double)nn > big;
+    h->xupd_evo = 72.0 * (double)nn + 32.0 * (double)ne > big;
+    const char* xu = getenv("PFB200_XUPD");  // "0" / "1": force (A/B tests)
+    if (xu) h->xupd_mom = h->xupd_evo = std::string(xu) == "1";
+  }
   h->cg_grid = std::max(1, std::min(occ * dev_sms, (h->geom_mom.n_units + cwpc - 1) / cwpc));
   h->cg_grid_evo =
       std::max(1, std::min(occ_evo * dev_sms, (h->geom_evo.n_units + cwpc - 1) / cwpc));
@@ -734,6 +746,11 @@ static pf_status axpy(pf_handle* h, double* y, const double* x, long long n) {
   return launched(h);
 }
 
+static const void* cg_kernel(pf_handle* h, bool mom) {
+  if (mom) return h->xupd_mom ? (const void*)pfb::k_cg<true, true> : (const void*)pfb::k_cg<true, false>;
+  return h->xupd_evo ? (const void*)pfb::k_cg<false, true> : (const void*)pfb::k_cg<false, false>;
+}
+
 static pfb::CgArgs cg_args(pf_handle* h, bool mom) {
   pfb::CgArgs a{};
   a.m = h->dm;
@@ -789,11 +806,11 @@ static pf_status run_cg_persistent(pf_handle* h, bool mom, double* target, bool 
   a.probe = probe ? 1 : 0;
   a.guess = guess;
   void* args[] = {&a};
-  const void* fn = mom ? (const void*)pfb::k_cg<true> : (const void*)pfb::k_cg<false>;
+  const void* fn = cg_kernel(h, mom);
   const int grid = mom ? h->cg_grid : h->cg_grid_evo;
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
   PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(pfb::CG_NT), args,
-                                      mom ? h->cg_dyn_smem : 0, h->stream));
+                                      0, h->stream));
   PF_TRY(launched(h));
   PF_CUDA(cudaEventRecord(h->ev1, h->stream));
   PF_CUDA(cudaStreamSynchronize(h->stream));
@@ -1366,6 +1383,33 @@ extern "C" pf_status pf_update_active_energy(pf_handle* h, int scheme, const dou
 }
 
 // ------------------------------------------------------------------------------------------
+extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, double* ms_out,
+                                 int64_t* iters_out) {
+  PF_CUDA(cudaSetDevice(h->device));
+  if (n_iter < 1 || physics < 0 || physics > 1) return fail(h, PF_ERR_INVALID, "bad arguments");
+  const bool mom = physics == 0;
+  if (mom) PF_TRY(launch_mom_prepare(h, 1));
+  else PF_TRY(launch_evo_prepare(h, 1, 0));
+  pfb::CgArgs a = cg_args(h, mom);
+  a.rtol = 0.0;  // never converges: exactly n_iter iterations
+  a.maxiter = n_iter;
+  void* args[] = {&a};
+  const void* fn = cg_kernel(h, mom);
+  PF_CUDA(cudaEventRecord(h->ev0, h->stream));
+  PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(mom ? h->cg_grid : h->cg_grid_evo),
+                                      dim3(pfb::CG_NT), args, 0,
+                                      h->stream));
+  PF_TRY(launched(h));
+  PF_CUDA(cudaEventRecord(h->ev1, h->stream));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  if (ms_out) *ms_out = ms;
+  if (iters_out) *iters_out = h->h_cgres->iters;
+  if (h->h_cgres->status == pfb::CG_NAN) return fail(h, PF_ERR_SINGULAR, "non-finite residual");
+  return PF_OK;
+}
+
 extern "C" pf_status pf_device_info(pf_handle* h, int32_t* cg_grid, int32_t* sm_count,
                                     int64_t* l2_bytes) {
   if (cg_grid) *cg_grid = h->cg_grid;

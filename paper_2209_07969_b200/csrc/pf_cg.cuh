@@ -151,8 +151,10 @@ __device__ __forceinline__ void grid_reduce(const double* part, int stride, doub
   for (int k = 0; k < NV; ++k) out[k] = bc[k];
 }
 
-// flat pass over double2 pairs: r -= alpha q and x += alpha p_k (update), partials r.r and
-// r.D^-1.r
+// flat pass over double2 pairs: r -= alpha q and, XU, x += alpha p_k (update), partials r.r
+// and r.D^-1.r.  The persistent kernel passes XU = false: its march applies the x update one
+// iteration late (march_unit XUPD).
+template <bool XU>
 __device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, const double* pk,
                                         bool update, double& rr, double& rz) {
   constexpr int U = PFB_PHASEB_UNROLL;
@@ -174,8 +176,10 @@ __device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, const dou
       dv[u] = __ldg(d2 + i);
       if (update) {
         qv[u] = __ldcg(q2 + i);
-        pv[u] = __ldcg(p2 + i);
-        xv[u] = __ldcg(x2 + i);
+        if (XU) {
+          pv[u] = __ldcg(p2 + i);
+          xv[u] = __ldcg(x2 + i);
+        }
       }
     }
 #pragma unroll
@@ -186,9 +190,11 @@ __device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, const dou
           rv[u].x -= alpha * qv[u].x;
           rv[u].y -= alpha * qv[u].y;
           r2[i] = rv[u];
-          xv[u].x += alpha * pv[u].x;
-          xv[u].y += alpha * pv[u].y;
-          x2[i] = xv[u];
+          if (XU) {
+            xv[u].x += alpha * pv[u].x;
+            xv[u].y += alpha * pv[u].y;
+            x2[i] = xv[u];
+          }
         }
         // pair i holds node i (momentum) or nodes 2i, 2i+1 (phase field); ghosts do not count
         const bool o0 = node_owned(a.m, a.vec2 ? (int)i : (int)(2 * i));
@@ -210,7 +216,7 @@ __device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, const dou
     if (update) {
       rv -= alpha * __ldcg(a.q + i);
       a.r[i] = rv;
-      a.x[i] = __ldcg(a.x + i) + alpha * __ldcg(pk + i);
+      if (XU) a.x[i] = __ldcg(a.x + i) + alpha * __ldcg(pk + i);
     }
     if (node_owned(a.m, (int)i)) {
       rr += rv * rv;
@@ -225,14 +231,12 @@ struct CgSmem {
   double red[CG_NT / 32 * 3];
   double bc[4];
 };
-#ifndef PFB_USE_RING
-#define PFB_USE_RING 0  // cp.async ring: measured no gain over register prefetch
-#endif
 
-template <bool MOM>
+// XUPD: lazy x update inside the march (fewer bytes, longer march): chosen by the host for
+// meshes whose working set is far beyond L2 (pf_api.cu create_impl)
+template <bool MOM, bool XUPD>
 __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO) k_cg(CgArgs a) {
   __shared__ CgSmem<MOM> S;
-  extern __shared__ __align__(16) unsigned char dyn_smem[];  // MomRing per warp (momentum)
   cg::grid_group grid = cg::this_grid();
   const int gwarp = blockIdx.x * (CG_NT / 32) + (threadIdx.x >> 5),
             nwarps = gridDim.x * (CG_NT / 32);
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO
     grid.sync();
   }
   double rr = 0.0, rz = 0.0;
-  phase_b(a, 0.0, nullptr, false, rr, rz);  // ||r0||^2 and r0.D^-1.r0 (r = b on entry)
+  phase_b<!XUPD>(a, 0.0, nullptr, false, rr, rz);  // ||r0||^2 and r0.D^-1.r0 (r = b on entry)
   {
     double v[2] = {rr, rz};
     block_sum<2>(v, S.red);
@@ -320,11 +324,8 @@ __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO
       const double* pold = (k & 1) ? a.p0 : a.p1;
       double pq = 0.0;
       for (int u = gwarp; u < a.g.n_units; u += nwarps) {
-        if constexpr (MOM && PFB_USE_RING)
-          march_mom_ring(a, a.g, u, first, beta, pold, pnew, pq, S.dup[threadIdx.x >> 5],
-                         reinterpret_cast<MomRing*>(dyn_smem)[threadIdx.x >> 5]);
-        else
-          march_unit<MOM, false>(a, a.g, u, first, beta, pold, pnew, pq, S.dup[threadIdx.x >> 5]);
+        march_unit<MOM, false, XUPD>(a, a.g, u, first, beta, pold, pnew, pq,
+                                       S.dup[threadIdx.x >> 5], alpha);
       }
       {
         double v[1] = {pq};
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO
       rho_prev = rho;
       rr = 0.0;
       rz = 0.0;
-      phase_b(a, alpha, pnew, true, rr, rz);
+      phase_b<!XUPD>(a, alpha, pnew, true, rr, rz);
       {
         double v[2] = {rr, rz};
         block_sum<2>(v, S.red);
@@ -352,11 +353,20 @@ __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO
       ++k;
     }
   }
-  if (status != CG_INDEFINITE && a.target) {  // x is complete: target += x
+  const bool xlast = XUPD && k > 0;
+  if (status != CG_INDEFINITE && (xlast || a.target)) {
+    // the last iteration's x += alpha p_{k-1} (deferred by the lazy update), then target += x
+    const double* plast = ((k - 1) & 1) ? a.p1 : a.p0;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.ndof;
-         i += stride)
-      a.target[i] += __ldcg(a.x + i);
+         i += stride) {
+      double xv = __ldcg(a.x + i);
+      if (xlast) {
+        xv += alpha * __ldcg(plast + i);
+        a.x[i] = xv;
+      }
+      if (a.target) a.target[i] += xv;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.result->iters = k;
@@ -438,7 +448,7 @@ template <bool MOM>
 __global__ void __launch_bounds__(NT) k_cg_init(SplitArgs s) {
   __shared__ double red[NT / 32 * 2];
   double rr = 0.0, rz = 0.0;
-  phase_b(s.c, 0.0, nullptr, false, rr, rz);
+  phase_b<true>(s.c, 0.0, nullptr, false, rr, rz);
   double v[2] = {rr, rz};
   block_sum<2>(v, red);
   double* pb = s.partB + (size_t)CG_SLOTS * s.gridB * 2;
@@ -539,7 +549,7 @@ __global__ void __launch_bounds__(NT) k_cg_b(SplitArgs s, int klocal) {
   const double alpha = cur[1] / pqv[0];
   const double* pk = (k & 1) ? s.c.p1 : s.c.p0;
   double rr = 0.0, rz = 0.0;
-  phase_b(s.c, alpha, pk, true, rr, rz);
+  phase_b<true>(s.c, alpha, pk, true, rr, rz);
   double v[2] = {rr, rz};
   block_sum<2>(v, red);
   double* pb = s.partB + (size_t)slot_of(k) * s.gridB * 2;

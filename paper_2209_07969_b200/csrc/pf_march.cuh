@@ -79,14 +79,18 @@ __device__ __forceinline__ void mom_cell_fast(const Consts& C, const double2 (&p
 template <bool MOM>
 struct RawNode {
   using T = typename Node<MOM>::T;
-  T r, di, po;
+  T r, di, po, x;
   double d;
   int id;
 };
 
-template <bool MOM, bool APPLY>
+// XUPD (lazy solution update): the owner of a node also loads x so that finish_node can apply
+// x += alpha_{k-1} p_{k-1} with the p_{k-1} the march reads anyway (phase B then no longer
+// streams p and x: 32 B per node and iteration less)
+template <bool MOM, bool APPLY, bool XUPD = false>
 __device__ __forceinline__ void fetch_node(const CgArgs& a, const double* __restrict__ pold,
-                                           bool first, int id, RawNode<MOM>& w) {
+                                           bool first, int id, RawNode<MOM>& w,
+                                           bool xown = false) {
   using N_ = Node<MOM>;
   w.id = id;
   if (id >= 0) {
@@ -96,53 +100,28 @@ __device__ __forceinline__ void fetch_node(const CgArgs& a, const double* __rest
       w.r = N_::ld_cg(a.r, id);
       w.di = N_::ld_ro(a.dinv, id);
       if (!first) w.po = N_::ld_cg(pold, id);
+      if (XUPD && !first && xown) w.x = N_::ld_cg(a.x, id);
     }
     if constexpr (MOM) w.d = __ldg(a.d + id);
   }
 }
 
-// p_k = D^-1 r + beta p_{k-1}; the owner stores it
-template <bool MOM, bool APPLY>
+// p_k = D^-1 r + beta p_{k-1}; the owner stores it (and, XUPD, x += alpha_{k-1} p_{k-1})
+template <bool MOM, bool APPLY, bool XUPD = false>
 __device__ __forceinline__ typename Node<MOM>::T finish_node(const RawNode<MOM>& w, bool first,
                                                              double beta, bool own,
-                                                             double* __restrict__ pnew) {
+                                                             double* __restrict__ pnew,
+                                                             double* __restrict__ x = nullptr,
+                                                             double xalpha = 0.0) {
   using N_ = Node<MOM>;
   if (w.id < 0) return N_::zero();
   if (APPLY) return w.po;
   typename N_::T p = N_::mul(w.di, w.r);
   if (!first) p = N_::axpy(beta, w.po, p);
   if (own) N_::st(pnew, w.id, p);
+  if (XUPD && !first && own) N_::st(x, w.id, N_::axpy(xalpha, w.po, w.x));
   return p;
 }
-
-// ---- cp.async prefetch ring (momentum march): the next PFB_RING node rows of a warp live in
-// shared memory, filled by 16-byte cp.async.cg copies (L2 -> smem, no register staging,
-// zero-fill for absent nodes), so each warp keeps PFB_RING-1 rows of loads in flight.
-#ifndef PFB_RING
-#define PFB_RING 4
-#endif
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
-               "r"(valid ? 16 : 0));
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
-               "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-struct MomRow {  // one node row of one warp
-  double2 r[32], di[32], po[32];
-  double d[32];
-  int id[32];
-};
-struct MomRing {
-  MomRow row[PFB_RING];
-};
 
 // the slit row's upper-face (duplicate) nodes of one warp, parked in shared memory so the march
 // does not carry them in registers through every row
@@ -154,12 +133,12 @@ struct DupRow {
   unsigned fb[32];
 };
 
-template <bool MOM, bool APPLY>
+template <bool MOM, bool APPLY, bool XUPD = false>
 __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, int unit,
                                            bool first, double beta,
                                            const double* __restrict__ pold,
                                            double* __restrict__ pnew, double& pq,
-                                           DupRow<MOM>& dup) {
+                                           DupRow<MOM>& dup, double xalpha = 0.0) {
   using N_ = Node<MOM>;
   using T = typename N_::T;
   const DMesh& m = a.m;
@@ -180,8 +159,9 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
   // loads and parks the duplicate row (warp-uniform call)
   auto load_dup = [&](bool own) {
     RawNode<MOM> wd;
-    fetch_node<MOM, APPLY>(a, pold, first, dupcol ? m.dup_start + (col - m.notch_lo) : -1, wd);
-    dup.p[lane] = finish_node<MOM, APPLY>(wd, first, beta, own, pnew);
+    fetch_node<MOM, APPLY, XUPD>(a, pold, first, dupcol ? m.dup_start + (col - m.notch_lo) : -1,
+                                 wd, own);
+    dup.p[lane] = finish_node<MOM, APPLY, XUPD>(wd, first, beta, own, pnew, a.x, xalpha);
     dup.d[lane] = MOM ? wd.d : 0.0;
     dup.id[lane] = wd.id;
     dup.fb[lane] = (APPLY || wd.id < 0) ? 0u : N_::freebits(wd.di);
@@ -202,7 +182,7 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
   fb_lo = (APPLY || w.id < 0) ? 0u : N_::freebits(w.di);
   lo_slit = (r0 - 1 == R);
   if (lo_slit) load_dup(false);
-  fetch_node<MOM, APPLY>(a, pold, first, nid(r0), w);  // upper row, in flight
+  fetch_node<MOM, APPLY, XUPD>(a, pold, first, nid(r0), w, lane_own && r0 < r1);  // in flight
   // cell-row data (branch bits / Newton coefficients) are prefetched one row ahead too
   auto cell_id = [&](int cj) -> int {
     if (cj < 0 || cj >= m.ny || lane >= 31) return -1;
@@ -222,12 +202,13 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
   for (int cj = r0 - 1; cj < r1; ++cj) {
     const int jh = cj + 1;
     const bool hi_own = lane_own && jh >= r0 && jh < r1;
-    const T p_hi = finish_node<MOM, APPLY>(w, first, beta, hi_own, pnew);
+    const T p_hi = finish_node<MOM, APPLY, XUPD>(w, first, beta, hi_own, pnew, a.x, xalpha);
     const double d_hi = MOM ? w.d : 0.0;
     const int id_hi = w.id;
     const unsigned fb_hi = (APPLY || w.id < 0) ? 0u : N_::freebits(w.di);
     const bool hi_slit = (jh == R);
-    if (jh + 1 <= r1) fetch_node<MOM, APPLY>(a, pold, first, nid(jh + 1), w);  // prefetch
+    if (jh + 1 <= r1)  // prefetch
+      fetch_node<MOM, APPLY, XUPD>(a, pold, first, nid(jh + 1), w, lane_own && jh + 1 < r1);
     const int eid = eid_n;
     const unsigned fl = fl_n;
     double bq[4] = {bq_n[0], bq_n[1], bq_n[2], bq_n[3]};
@@ -300,157 +281,17 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
   }
 }
 
-// Momentum phase A with the cp.async ring (same arithmetic and accumulation order as
-// march_unit<true, false>; only the way node rows arrive differs).
-__device__ __forceinline__ void ring_issue(const CgArgs& a, const double* __restrict__ pold,
-                                           bool first, int id, MomRow& slot, int lane) {
-  const bool v = id >= 0;
-  const int cid = v ? id : 0;
-  cp_async16(&slot.r[lane], a.r + 2 * (size_t)cid, v);
-  cp_async16(&slot.di[lane], a.dinv + 2 * (size_t)cid, v);
-  if (!first) cp_async16(&slot.po[lane], pold + 2 * (size_t)cid, v);
-  cp_async8(&slot.d[lane], a.d + cid, v);
-  slot.id[lane] = id;
-}
-
-__device__ __forceinline__ void march_mom_ring(const CgArgs& a, const MarchGeom& G, int unit,
-                                               bool first, double beta,
-                                               const double* __restrict__ pold,
-                                               double* __restrict__ pnew, double& pq,
-                                               DupRow<true>& dup, MomRing& ring) {
-  using N_ = Node<true>;
-  using T = double2;
-  const DMesh& m = a.m;
-  const Consts& C = a.C;
-  const int lane = threadIdx.x & 31;
-  const int strip = unit % G.n_strips;
-  const int r0 = (unit / G.n_strips) * G.rows_per_unit;
-  const int r1 = min(r0 + G.rows_per_unit, m.ny + 1);
-  const int col = strip * TXW - 1 + lane;
-  const bool lane_own = lane >= 1 && lane <= TXW;
-  const int R = m.notch_row;
-  const bool dupcol = R >= 0 && col >= m.notch_lo && col < m.notch_hi;
-  auto nid = [&](int j) -> int {
-    if (j < 0 || j > m.ny) return -1;
-    const int4 rw = __ldg(m.nrow + j);
-    return (col >= rw.x && col < rw.y) ? rw.z + (col - rw.x) : -1;
-  };
-  auto load_dup = [&](bool own) {
-    RawNode<true> wd;
-    fetch_node<true, false>(a, pold, first, dupcol ? m.dup_start + (col - m.notch_lo) : -1, wd);
-    dup.p[lane] = finish_node<true, false>(wd, first, beta, own, pnew);
-    dup.d[lane] = wd.d;
-    dup.id[lane] = wd.id;
-    dup.fb[lane] = wd.id < 0 ? 0u : N_::freebits(wd.di);
-    __syncwarp();
-  };
-  // rows r0-1 .. r1 enter the ring in order; row j lives in slot (j - r0 + 1) % PFB_RING
-  const int jfirst = r0 - 1;
-  int jissue = jfirst;
-  for (int q = 0; q < PFB_RING - 1; ++q, ++jissue) {
-    if (jissue <= r1) ring_issue(a, pold, first, nid(jissue), ring.row[(jissue - jfirst) % PFB_RING], lane);
-    cp_async_commit();
-  }
-  auto take = [&](int j, bool own, T& p, double& d, int& id, unsigned& fb) {
-    MomRow& sl = ring.row[(j - jfirst) % PFB_RING];
-    id = sl.id[lane];
-    d = sl.d[lane];
-    p = make_double2(0.0, 0.0);
-    fb = 0u;
-    if (id >= 0) {
-      const T di = sl.di[lane];
-      p = N_::mul(di, sl.r[lane]);
-      if (!first) p = N_::axpy(beta, sl.po[lane], p);
-      if (own) N_::st(pnew, id, p);
-      fb = N_::freebits(di);
-    }
-  };
-  // lower row r0-1
-  T p_lo;
-  double d_lo;
-  int id_lo;
-  unsigned fb_lo;
-  cp_async_wait<PFB_RING - 2>();
-  take(jfirst, false, p_lo, d_lo, id_lo, fb_lo);
-  bool lo_slit = (jfirst == R);
-  if (lo_slit) load_dup(false);
-  T acc_lo = make_double2(0.0, 0.0);
-  for (int cj = r0 - 1; cj < r1; ++cj) {
-    const int jh = cj + 1;
-    // refill: the slot of row jfirst + (cj - jfirst) is free again
-    if (jissue <= r1) ring_issue(a, pold, first, nid(jissue), ring.row[(jissue - jfirst) % PFB_RING], lane);
-    cp_async_commit();
-    ++jissue;
-    cp_async_wait<PFB_RING - 2>();
-    const bool hi_own = lane_own && jh >= r0 && jh < r1;
-    T p_hi;
-    double d_hi;
-    int id_hi;
-    unsigned fb_hi;
-    take(jh, hi_own, p_hi, d_hi, id_hi, fb_hi);
-    const bool hi_slit = (jh == R);
-    const bool use_dup = lo_slit && dupcol;
-    const T b0 = use_dup ? dup.p[lane] : p_lo;
-    const T b1 = shfl_dn(b0);
-    const T t2 = shfl_dn(p_hi);
-    const double e0 = use_dup ? dup.d[lane] : d_lo;
-    const double e1 = shfl_dn(e0);
-    const double e2 = shfl_dn(d_hi);
-    int eid = -1;
-    if (cj >= 0 && cj < m.ny) {
-      const int4 er = __ldg(m.erow + cj);
-      if (lane < 31 && col >= er.x && col < er.y) eid = er.z + (col - er.x);
-    }
-    T f[4];
-    f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
-    if (eid >= 0) {
-      const double2 pc[4] = {b0, b1, t2, p_hi};
-      const double dc[4] = {e0, e1, e2, d_hi};
-      mom_cell_fast(C, pc, dc, __ldg(a.flags + eid), f);
-    }
-    const T c1l = shfl_up(f[1]);
-    const T c2l = shfl_up(f[2]);
-    if (lane_own && cj >= r0) {
-      if (use_dup) {
-        if (id_lo >= 0) {
-          const T qv = N_::maskb(acc_lo, fb_lo);
-          if (node_owned(m, id_lo)) pq += N_::dot(p_lo, qv);
-          N_::st(a.q, id_lo, qv);
-        }
-        const int idd = dup.id[lane];
-        if (idd >= 0) {
-          const T qv = N_::maskb(add_t(c1l, f[0]), dup.fb[lane]);
-          if (node_owned(m, idd)) pq += N_::dot(dup.p[lane], qv);
-          N_::st(a.q, idd, qv);
-        }
-      } else if (id_lo >= 0) {
-        const T qv = N_::maskb(add_t(add_t(acc_lo, c1l), f[0]), fb_lo);
-        if (node_owned(m, id_lo)) pq += N_::dot(p_lo, qv);
-        N_::st(a.q, id_lo, qv);
-      }
-    }
-    acc_lo = add_t(c2l, f[3]);
-    if (hi_slit) {
-      __syncwarp();
-      load_dup(hi_own);
-    }
-    p_lo = p_hi;
-    d_lo = d_hi;
-    id_lo = id_hi;
-    fb_lo = fb_hi;
-    lo_slit = hi_slit;
-  }
-  cp_async_wait<0>();
-  __syncwarp();
-}
-
-// host-side choice of the unit shape: enough units for every resident warp, but at least
-// 4 owned rows per unit so the halo rows stay a modest overhead
 inline MarchGeom make_march_geom(int nx, int ny, int resident_warps, int min_rows = 4) {
+  // At most one unit per resident warp: phase A lasts as long as its busiest warp, so the row
+  // blocks per strip are floor(warps / strips).  (A ceil split that leaves some warps with two
+  // units doubles the phase: 8192^2 had 2466 units for 2368 warps.)  Units never cross a strip:
+  // the 8 warps of a CTA march 8 adjacent strips in lockstep and share their halo columns in L2
+  // (runs laid end to end over the strips balanced better but measured slower).
   MarchGeom g;
   g.n_strips = (nx + 1 + TXW - 1) / TXW;
-  const long long strip_rows = (long long)g.n_strips * (ny + 1);
-  int rows = (int)((strip_rows + resident_warps - 1) / resident_warps);
+  int blocks = resident_warps / g.n_strips;
+  blocks = blocks < 1 ? 1 : blocks;
+  int rows = (ny + 1 + blocks - 1) / blocks;
   rows = rows < min_rows ? min_rows : rows;
   if (rows > ny + 1) rows = ny + 1;
   g.rows_per_unit = rows;

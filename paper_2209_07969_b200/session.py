@@ -267,6 +267,13 @@ class DeviceSession:
         self._check(self.lib.pf_update_active_energy(self.h, scheme_code(scheme), N.f64(dd)))
 
     # -- benchmarking helpers ------------------------------------------------------------
+    def bench_cg(self, physics: str, n_iter: int) -> tuple:
+        """(ms, iterations) of a fixed-length PCG run at the current state (no convergence)."""
+        ms, it = C.c_double(), C.c_int64()
+        self._check(self.lib.pf_bench_cg(self.h, 0 if physics == "momentum" else 1,
+                                         int(n_iter), C.byref(ms), C.byref(it)))
+        return ms.value, it.value
+
     def device_info(self) -> dict:
         g, s, l2 = C.c_int32(), C.c_int32(), C.c_int64()
         self._check(self.lib.pf_device_info(self.h, C.byref(g), C.byref(s), C.byref(l2)))

@@ -97,3 +97,23 @@ def test_operator_symmetry_and_rigid_modes(cuda_ok):
     Kb, _ = s.evolution_tangent_apply("ST", b)
     assert abs(b @ Ka - a @ Kb) <= 1e-12 * abs(b @ Ka)
     s.close()
+
+
+def test_fixed_length_pcg_benchmark_entry(cuda_ok):
+    """pf_bench_cg runs exactly n PCG iterations (stopping test off) on the rectangle layout
+    used for the cfg5-size measurements; the layout equals the one derived from the mesh."""
+    from paper_2209_07969_b200 import meshing
+    from paper_2209_07969_b200.session import DeviceSession
+
+    lay = meshing.StructuredLayout.rectangle(40, 24, 1.0 / 40, 1.0 / 24)
+    ref = meshing.StructuredLayout.from_mesh(meshing.build_notched_square(40, 24, 1.0, False))
+    assert np.array_equal(lay.node_start, ref.node_start) and lay.n_elems == ref.n_elems
+    s = DeviceSession(lay, kat_params("at2"), _Cfg(), device=0)
+    rng = np.random.default_rng(3)
+    nn = lay.n_nodes
+    s.push(u=1e-3 * rng.standard_normal(2 * nn), d=0.5 * rng.random(nn), d_prev=np.zeros(nn))
+    s.refresh_gp()
+    for phys in ("momentum", "evolution"):
+        ms, it = s.bench_cg(phys, 7)
+        assert it == 7 and ms > 0.0
+    s.close()

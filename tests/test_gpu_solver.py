@@ -186,6 +186,30 @@ def test_determinism_and_dropin_equivalence(cuda_ok):
     assert np.array_equal(got["u"], outs[0][0]) and np.array_equal(got["d"], outs[0][1])
 
 
+@pytest.mark.parametrize("case_name", ["tension16", "lpanel25"])
+def test_lazy_x_variant_matches_default(cuda_ok, monkeypatch, case_name):
+    """The lazy-x PCG variant (x += alpha p folded into the next march; chosen automatically
+    only for meshes far beyond L2, e.g. cfg5) computes the same iterates: forced on for a
+    small mesh, every staggered iteration count and the final fields match the default."""
+    from paper_2209_07969_b200.session import DeviceSession
+
+    case = C.get_case(case_name)
+    runs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PFB200_XUPD", flag)
+        pb = C.setup(case, C.b200_api())
+        s = DeviceSession(pb.disc.layout, pb.params, pb.config, device=0)
+        s.push_state(pb.state)
+        stats = [s.step("S1", pb.bcs, pb.pins) for _ in range(6)]
+        got = s.pull()
+        runs.append(([(st.n_stag, st.cg_iters_u, st.cg_iters_d) for st in stats], got))
+        s.close()
+    assert runs[0][0] == runs[1][0]
+    for k in ("u", "d"):
+        a, b = runs[0][1][k], runs[1][1][k]
+        assert np.max(np.abs(a - b)) <= 1e-12 * max(1.0, np.max(np.abs(a))), k
+
+
 def test_errors_map_to_reference_exceptions(cuda_ok):
     from paper_2209_07969_b200 import schemes
     from paper_2209_07969_b200.session import ConvergenceError
