@@ -64,11 +64,15 @@ struct pf_handle {
   // warm starts of the momentum PCG: previous solution of the same kind of Newton system
   // slot 0: the load-increment pass; slot s (1..WARM_SLOTS-1): staggered pass s (the last
   // slot also serves later passes) -- the previous load step's solve at the same pass index
+  // Each slot keeps the backward-difference table of its last warm_depth (<= pfb::WARM_MAX)
+  // solutions; the PCG starts from their energy-optimal combination (pf_cg.cuh warm_start).
   static constexpr int WARM_SLOTS = 4;
   bool warm = true;
   bool trace = false;
-  double* warm_buf[WARM_SLOTS] = {nullptr, nullptr, nullptr, nullptr};
-  bool warm_ok[WARM_SLOTS] = {false, false, false, false};
+  // cfg2 load steps 4..13, momentum PCG iterations: depth 1 69634, 3 52336, 4 52151, 5 51805
+  int warm_depth = 3;
+  double* warm_buf[WARM_SLOTS][pfb::WARM_MAX] = {};
+  int warm_n[WARM_SLOTS] = {};
   bool xupd_mom = false, xupd_evo = false;  // lazy-x PCG variants (k_cg<MOM, true>)
   pfb::MarchGeom geom_mom{}, geom_evo{}, geom_apply{};
   // split-phase PCG (pf_cg.cuh: k_cg_a / k_cg_b chained in CUDA graphs)
@@ -209,10 +213,12 @@ extern "C" void pf_destroy(pf_handle* h) {
                   h->u, h->d, h->dprev, h->trp, h->dev2, h->psi, h->psimax,
                   h->Ru, h->ru, h->xu, h->qu, h->p0u, h->p1u, h->dinvu, h->diagu, h->flags,
                   h->umask, h->Rd, h->rd, h->xd, h->qd, h->p0d, h->p1d, h->dinvd, h->diagd,
-                  h->b, h->pmask, h->partials, h->scratch, h->d_idx, h->flushbuf,
-                  h->warm_buf[0], h->warm_buf[1], h->warm_buf[2], h->warm_buf[3]};
+                  h->b, h->pmask, h->partials, h->scratch, h->d_idx, h->flushbuf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto& row : h->warm_buf)
+    for (double* p : row)
+      if (p) cudaFree(p);
   for (auto& row : h->graphs)
     for (auto& g : row)
       if (g) cudaGraphExecDestroy(g);
@@ -427,10 +433,14 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
   CREATE_ALLOC(h->b, 4 * ne);
   CREATE_ALLOC(h->pmask, nn);
   CREATE_ALLOC(h->scratch, 16 * ne);
-  for (int w = 0; w < pf_handle::WARM_SLOTS; ++w) CREATE_ALLOC(h->warm_buf[w], 2 * nn);
   {
     const char* w = getenv("PFB200_WARM");
-    h->warm = !(w && std::string(w) == "0");
+    h->warm = !(w && std::string(w) == "0") && !strip;  // strips: cold starts
+    const char* wd = getenv("PFB200_WARM_DEPTH");  // 1..WARM_MAX (A/B tests)
+    if (wd) h->warm_depth = std::min(std::max(atoi(wd), 1), pfb::WARM_MAX);
+    if (h->warm)
+      for (int sl = 0; sl < pf_handle::WARM_SLOTS; ++sl)
+        for (int k = 0; k < h->warm_depth; ++k) CREATE_ALLOC(h->warm_buf[sl][k], 2 * nn);
     const char* tr = getenv("PFB200_TRACE");
     h->trace = tr && std::string(tr) == "1";
   }
@@ -496,7 +506,8 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
     CREATE_CUDA(cudaMalloc((void**)&h->partB, sizeof(double) * (pfb::CG_SLOTS + 1) * h->gridB * 2));
   }
   const size_t npart =
-      std::max<size_t>((size_t)h->n_tiles, (size_t)std::max(h->cg_grid, h->cg_grid_evo)) * 4;
+      std::max<size_t>((size_t)h->n_tiles * 4,
+                       (size_t)std::max(h->cg_grid, h->cg_grid_evo) * pfb::CG_PART_STRIDE);
   CREATE_ALLOC(h->partials, npart);
   CREATE_CUDA(cudaHostAlloc((void**)&h->h_cgres, sizeof(CgResult), cudaHostAllocMapped));
   CREATE_CUDA(cudaHostGetDevicePointer((void**)&h->d_cgres, h->h_cgres, 0));
@@ -800,11 +811,13 @@ static pf_status cg_status(pf_handle* h, int status, long long iters) {
 
 // one persistent PCG solve (single cooperative launch)
 static pf_status run_cg_persistent(pf_handle* h, bool mom, double* target, bool probe,
-                                   int* status, long long* iters, const double* guess) {
+                                   int* status, long long* iters, double* const* guess,
+                                   int n_guess) {
   pfb::CgArgs a = cg_args(h, mom);
   a.target = target;
   a.probe = probe ? 1 : 0;
-  a.guess = guess;
+  for (int k = 0; k < n_guess && k < pfb::WARM_MAX; ++k) a.guess[k] = guess[k];
+  a.n_guess = guess ? std::min(n_guess, pfb::WARM_MAX) : 0;
   void* args[] = {&a};
   const void* fn = cg_kernel(h, mom);
   const int grid = mom ? h->cg_grid : h->cg_grid_evo;
@@ -972,10 +985,10 @@ static pf_status run_cg_dist(pf_handle* h, bool mom, double* target, bool probe,
 }
 
 static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
-                        long long* iters, const double* guess = nullptr) {
+                        long long* iters, double* const* guess = nullptr, int n_guess = 0) {
   if (h->comm) return run_cg_dist(h, mom, target, probe, status, iters);
   return h->split ? run_cg_split(h, mom, target, probe, status, iters)
-                  : run_cg_persistent(h, mom, target, probe, status, iters, guess);
+                  : run_cg_persistent(h, mom, target, probe, status, iters, guess, n_guess);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1041,17 +1054,21 @@ static pf_status momentum(pf_handle* h, const BcView& bc, bool apply_inc, double
       // warm start of the first Newton step from the previous solve of the same kind (the
       // load-increment pass or a staggered pass); later Newton corrections start from zero
       const int ws = std::min(std::max(pass, 0), pf_handle::WARM_SLOTS - 1);
-      double* wbuf = h->warm_buf[ws];
-      bool& wok = h->warm_ok[ws];
-      const double* guess = (h->warm && n_nr == 0 && wok) ? wbuf : nullptr;
-      PF_TRY(run_cg(h, true, h->u, false, &status, &iters, guess));
+      double* guess[pfb::WARM_MAX] = {};
+      const int ng = (h->warm && n_nr == 0) ? h->warm_n[ws] : 0;
+      for (int k = 0; k < ng; ++k) guess[k] = h->warm_buf[ws][k];
+      PF_TRY(run_cg(h, true, h->u, false, &status, &iters, guess, ng));
       if (h->trace)
         fprintf(stderr, "[pfb200] momentum pass %d newton %d warm %d iters %lld\n", pass, n_nr,
-                guess != nullptr, iters);
-      if (h->warm && n_nr == 0) {
-        PF_CUDA(cudaMemcpyAsync(wbuf, h->xu, 2 * sizeof(double) * h->n_nodes,
-                                cudaMemcpyDeviceToDevice, h->stream));
-        wok = true;
+                ng, iters);
+      if (h->warm && n_nr == 0) {  // the solution joins the difference table
+        pfb::WarmTable t{};
+        for (int k = 0; k < h->warm_depth; ++k) t.d[k] = h->warm_buf[ws][k];
+        const long long n = 2LL * h->n_nodes;
+        pfb::k_warm_push<<<4 * h->sm_count, 256, 0, h->stream>>>(t, h->warm_n[ws],
+                                                              h->warm_depth, h->xu, n);
+        PF_TRY(launched(h));
+        h->warm_n[ws] = std::min(h->warm_n[ws] + 1, h->warm_depth);
       }
     }
     n_nr += 1;

@@ -40,6 +40,12 @@ struct CgResult {
   double bnorm, rnorm;
 };
 
+constexpr int WARM_MAX = 5;         // depth of the warm-start difference table
+constexpr int CG_PART_STRIDE = 12;  // doubles per CTA in the partials buffer (warm start)
+struct WarmTable {
+  double* d[WARM_MAX];
+};
+
 struct MarchGeom {
   int n_strips, rows_per_unit, n_row_blocks, n_units;
 };
@@ -65,7 +71,10 @@ struct CgArgs {
   double rtol;
   long long maxiter;
   int probe;
-  const double* guess;   // optional warm start v: x0 = gamma v, gamma = (b.v)/(v.Av)
+  // optional warm start: backward-difference table of the last n_guess <= WARM_MAX solutions
+  // (guess[0] = newest, guess[k] = k-th difference); x0 = their energy-optimal combination
+  const double* guess[WARM_MAX];
+  int n_guess;
 };
 
 template <bool MOM>
@@ -228,9 +237,160 @@ __device__ __forceinline__ void phase_b(const CgArgs& a, double alpha, const dou
 template <bool MOM>
 struct CgSmem {
   DupRow<MOM> dup[CG_NT / 32];
-  double red[CG_NT / 32 * 3];
-  double bc[4];
+  double red[CG_NT / 32 * CG_PART_STRIDE];
+  double bc[CG_PART_STRIDE];
+  double gram[WARM_MAX * WARM_MAX + WARM_MAX + 1];  // warm start: G, U^T b, b.b
 };
+
+
+// Galerkin warm start.  The host keeps, per kind of Newton system, the backward-difference
+// table u_1 = v_1, u_2 = v_1 - v_2, u_3 = u_2(v_1,v_2) - u_2(v_2,v_3), ... of its last m
+// solutions (k_warm_push).  Differences of consecutive solutions (which agree to ~1e-6) carry
+// the trend at full relative precision, so the coefficients below stay O(1).  x0 = U y with
+// (U^T A U) y = U^T b is the A-norm-closest point of span(U) to the solution: never worse than
+// x0 = 0.  Directions whose Cholesky pivot falls below 1e-6 of their diagonal are dropped.
+// r0 = b - A x0 is then formed by one more operator application, so it is consistent with x0
+// whatever y is.  Returns ||b||; x and r are set for the PCG loop (r = b on entry).
+template <bool MOM>
+__device__ __forceinline__ double warm_start(const CgArgs& a, CgSmem<MOM>& S) {
+  cg::grid_group grid = cg::this_grid();
+  constexpr int M = WARM_MAX;
+  const int gwarp = blockIdx.x * (CG_NT / 32) + (threadIdx.x >> 5),
+            nwarps = gridDim.x * (CG_NT / 32);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double* part = a.partials;
+  const int m = a.n_guess < M ? a.n_guess : M;
+  // column k of G = U^T (A u_k) (free rows only); with k = 0 also c = U^T b and b.b
+#pragma unroll 1
+  for (int k = 0; k < m; ++k) {
+    const double* uk = a.guess[0];
+#pragma unroll
+    for (int t = 1; t < M; ++t)
+      if (k == t) uk = a.guess[t];
+    for (int u = gwarp; u < a.g.n_units; u += nwarps) {
+      double dummy = 0.0;
+      march_unit<MOM, true>(a, a.g, u, true, 0.0, uk, nullptr, dummy, S.dup[threadIdx.x >> 5]);
+    }
+    grid.sync();
+    double acc[CG_PART_STRIDE];
+#pragma unroll
+    for (int t = 0; t < CG_PART_STRIDE; ++t) acc[t] = 0.0;
+    for (long long i = i0; i < a.ndof; i += stride) {
+      if (!node_owned(a.m, (int)(a.vec2 ? i >> 1 : i)) || __ldg(a.dinv + i) == 0.0) continue;
+      const double qi = __ldcg(a.q + i), bi = k == 0 ? __ldcg(a.r + i) : 0.0;
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        if (j < m && (j <= k || k == 0)) {
+          const double uj = __ldg(a.guess[j] + i);
+          if (j <= k) acc[j] += uj * qi;
+          if (k == 0) acc[M + j] += uj * bi;
+        }
+      }
+      if (k == 0) acc[2 * M] += bi * bi;
+    }
+    block_sum<CG_PART_STRIDE>(acc, S.red);
+    if (threadIdx.x == 0)
+      for (int t = 0; t < CG_PART_STRIDE; ++t) part[CG_PART_STRIDE * blockIdx.x + t] = acc[t];
+    grid.sync();
+    double g[CG_PART_STRIDE];
+    grid_reduce<CG_PART_STRIDE>(part, CG_PART_STRIDE, S.bc, g);
+    if (threadIdx.x == 0) {
+      for (int j = 0; j <= k; ++j) S.gram[j * M + k] = S.gram[k * M + j] = g[j];
+      if (k == 0)
+        for (int j = 0; j <= M; ++j) S.gram[M * M + j] = g[M + j];
+    }
+    grid.sync();  // partials and S.bc are reused by the next column
+  }
+  double G[M][M], c[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    c[j] = j < m ? S.gram[M * M + j] : 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) G[j][k] = (j < m && k < m) ? S.gram[j * M + k] : 0.0;
+  }
+  const double bb = m > 0 ? S.gram[M * M + M] : 0.0;
+  // pivot-dropping Cholesky G = L L^T (identical arithmetic in every thread, compile-time
+  // bounds so the arrays stay in registers)
+  double L[M][M], z[M], y[M];
+  bool keep[M];
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) L[i][j] = 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    double d = G[i][i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) d -= L[i][k] * L[i][k];
+    keep[i] = i < m && G[i][i] > 0.0 && d > 1e-6 * G[i][i];
+    const double lii = keep[i] ? sqrt(d) : 1.0;
+    L[i][i] = keep[i] ? lii : 0.0;
+#pragma unroll
+    for (int j = i + 1; j < M; ++j) {
+      double e = G[j][i];
+#pragma unroll
+      for (int k = 0; k < i; ++k) e -= L[j][k] * L[i][k];
+      L[j][i] = keep[i] ? e / lii : 0.0;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    double e = c[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) e -= L[i][k] * z[k];
+    z[i] = keep[i] ? e / L[i][i] : 0.0;
+  }
+  bool any = false;
+#pragma unroll
+  for (int i = M - 1; i >= 0; --i) {
+    double e = z[i];
+#pragma unroll
+    for (int k = i + 1; k < M; ++k) e -= L[k][i] * y[k];
+    y[i] = keep[i] ? e / L[i][i] : 0.0;
+    any = any || y[i] != 0.0;
+  }
+  if (any) {
+    for (long long i = i0; i < a.ndof; i += stride) {  // x0 = U y on the free DOFs
+      double xv = 0.0;
+      if (__ldg(a.dinv + i) != 0.0) {
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          if (k < m) xv += y[k] * __ldg(a.guess[k] + i);
+      }
+      a.x[i] = xv;
+    }
+    grid.sync();
+    for (int u = gwarp; u < a.g.n_units; u += nwarps) {  // q = A x0
+      double dummy = 0.0;
+      march_unit<MOM, true>(a, a.g, u, true, 0.0, a.x, nullptr, dummy, S.dup[threadIdx.x >> 5]);
+    }
+    grid.sync();
+    for (long long i = i0; i < a.ndof; i += stride)  // r0 = b - A x0 (constrained rows stay 0)
+      if (__ldg(a.dinv + i) != 0.0) a.r[i] = __ldcg(a.r + i) - __ldcg(a.q + i);
+  }
+  grid.sync();
+  return sqrt(bb);
+}
+
+// warm-start history update after a solve: the difference table (guess[0] = newest solution,
+// guess[k] = k-th backward difference) absorbs x in place; n_valid = entries before the push
+__global__ void k_warm_push(WarmTable t, int n_valid, int depth, const double* __restrict__ x,
+                            long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double cur = x[i];
+#pragma unroll
+    for (int k = 0; k < WARM_MAX; ++k) {
+      if (k >= depth) break;
+      const double old = k < n_valid ? t.d[k][i] : 0.0;
+      t.d[k][i] = cur;
+      if (k >= n_valid) break;
+      cur = cur - old;
+    }
+  }
+}
 
 // XUPD: lazy x update inside the march (fewer bytes, longer march): chosen by the host for
 // meshes whose working set is far beyond L2 (pf_api.cu create_impl)
@@ -242,59 +402,8 @@ __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO
             nwarps = gridDim.x * (CG_NT / 32);
   double* part = a.partials;
   double bnorm_in = -1.0;
-  if (a.guess) {
-    // v = guess restricted to free DOFs (into p1, unused before iteration 1); q = A v;
-    // gamma = (b.v)/(v.Av) is the energy-optimal multiple of v, so the start is never worse
-    // than x0 = 0 in the A-norm.  The stopping test keeps using rtol * ||b||.
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.ndof;
-         i += stride)
-      a.p1[i] = __ldg(a.dinv + i) != 0.0 ? __ldg(a.guess + i) : 0.0;
-    grid.sync();
-    for (int u = gwarp; u < a.g.n_units; u += nwarps) {
-      double dummy = 0.0;
-      march_unit<MOM, true>(a, a.g, u, true, 0.0, a.p1, nullptr, dummy,
-                            S.dup[threadIdx.x >> 5]);
-    }
-    grid.sync();
-    double bv = 0.0, vav = 0.0, bb = 0.0;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.ndof;
-         i += stride) {
-      const bool fr = __ldg(a.dinv + i) != 0.0;
-      const double v = __ldcg(a.p1 + i);
-      const double qv = fr ? __ldcg(a.q + i) : 0.0;
-      const double bi = __ldcg(a.r + i);
-      if (node_owned(a.m, (int)(a.vec2 ? i >> 1 : i))) {
-        bv += bi * v;
-        vav += v * qv;
-        bb += bi * bi;
-      }
-    }
-    {
-      double v3[3] = {bv, vav, bb};
-      block_sum<3>(v3, S.red);
-      if (threadIdx.x == 0) {
-        part[4 * blockIdx.x] = v3[0];
-        part[4 * blockIdx.x + 1] = v3[1];
-        part[4 * blockIdx.x + 2] = v3[2];
-      }
-    }
-    grid.sync();
-    double g3[3];
-    grid_reduce<3>(part, 4, S.bc, g3);
-    bnorm_in = sqrt(g3[2]);
-    const double gamma = (g3[1] > 0.0 && g3[0] > 0.0) ? g3[0] / g3[1] : 0.0;
-    if (gamma > 0.0) {  // x = gamma v, r = b - gamma A v (constrained rows stay 0)
-      for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.ndof;
-           i += stride) {
-        const bool fr = __ldg(a.dinv + i) != 0.0;
-        const double v = __ldcg(a.p1 + i);
-        a.x[i] = gamma * v;
-        if (fr) a.r[i] = __ldcg(a.r + i) - gamma * __ldcg(a.q + i);
-      }
-    }
-    grid.sync();
-  }
+  if constexpr (MOM)  // phase-field solves start cold (SPD predicate semantics)
+    if (a.n_guess > 0) bnorm_in = warm_start<MOM>(a, S);
   double rr = 0.0, rz = 0.0;
   phase_b<!XUPD>(a, 0.0, nullptr, false, rr, rz);  // ||r0||^2 and r0.D^-1.r0 (r = b on entry)
   {
