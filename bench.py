@@ -283,7 +283,7 @@ def run_ours(args, ws, rank, local):
                       "momentum_launches": tot["cgl_u"], "phase_field_launches": tot["cgl_d"]},
         "kernel_ms": {"momentum_pcg": tot["ms_u"], "phase_field_pcg": tot["ms_d"]},
         "roofline": {
-            "kernel": "k_cg<true> (momentum PCG, persistent cooperative)" if ws == 1 else
+            "kernel": "k_cg<true, *> (momentum PCG, persistent cooperative)" if ws == 1 else
                       "momentum PCG (k_cg_a/k_cg_b + NCCL, rank 0's strip)",
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
