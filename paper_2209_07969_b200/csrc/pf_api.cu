@@ -42,6 +42,7 @@ struct pf_handle {
   // momentum work
   double *Ru = nullptr, *ru = nullptr, *xu = nullptr, *qu = nullptr, *p0u = nullptr,
          *p1u = nullptr, *dinvu = nullptr, *diagu = nullptr;
+  double *r1u = nullptr, *w1u = nullptr, *pcu = nullptr;  // single-reduction PCG (k_cg_sr)
   uint8_t* flags = nullptr;
   uint8_t* umask = nullptr;
   // phase-field work
@@ -74,6 +75,8 @@ struct pf_handle {
   double* warm_buf[WARM_SLOTS][pfb::WARM_MAX] = {};
   int warm_n[WARM_SLOTS] = {};
   bool xupd_mom = false, xupd_evo = false;  // lazy-x PCG variants (k_cg<MOM, true>)
+  bool sr_mom = false;  // momentum solves by the single-reduction PCG (k_cg_sr<true>)
+  size_t sr_smem = 0;   // its dynamic shared memory (cp.async staging slots)
   pfb::MarchGeom geom_mom{}, geom_evo{}, geom_apply{};
   // split-phase PCG (pf_cg.cuh: k_cg_a / k_cg_b chained in CUDA graphs)
   bool split = false;
@@ -212,6 +215,7 @@ extern "C" void pf_destroy(pf_handle* h) {
                   h->d_nrow, h->d_erow,
                   h->u, h->d, h->dprev, h->trp, h->dev2, h->psi, h->psimax,
                   h->Ru, h->ru, h->xu, h->qu, h->p0u, h->p1u, h->dinvu, h->diagu, h->flags,
+                  h->r1u, h->w1u, h->pcu,
                   h->umask, h->Rd, h->rd, h->xd, h->qd, h->p0d, h->p1d, h->dinvd, h->diagd,
                   h->b, h->pmask, h->partials, h->scratch, h->d_idx, h->flushbuf};
   for (void* p : ptrs)
@@ -418,6 +422,22 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
   CREATE_ALLOC(h->qu, 2 * nn);
   CREATE_ALLOC(h->p0u, 2 * nn);
   CREATE_ALLOC(h->p1u, 2 * nn);
+  {
+    // single-reduction momentum PCG where the iteration is latency-bound (working set in L2:
+    // cfg1 -11%, cfg2 -8% per iteration); the two-barrier form where bytes dominate (cfg4 +12%,
+    // cfg3 +8%, cfg5 +5% with the single-reduction form).  PFB200_SR=0/1 forces (A/B tests).
+    int l2b = 0;
+    CREATE_CUDA(cudaDeviceGetAttribute(&l2b, cudaDevAttrL2CacheSize, device));
+    h->sr_mom = 168.0 * (double)nn <= (double)l2b;
+    const char* srv = getenv("PFB200_SR");
+    if (srv) h->sr_mom = std::string(srv) == "1";
+    h->sr_mom = h->sr_mom && !strip;  // strips: split-phase kernels
+    if (h->sr_mom) {
+      CREATE_ALLOC(h->r1u, 2 * nn);
+      CREATE_ALLOC(h->w1u, 2 * nn);
+      CREATE_ALLOC(h->pcu, 2 * nn);
+    }
+  }
   CREATE_ALLOC(h->dinvu, 2 * nn);
   CREATE_ALLOC(h->diagu, 2 * nn);
   CREATE_ALLOC(h->flags, ne);
@@ -456,6 +476,15 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
     CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_cg<true, true>,
                                                               pfb::CG_NT, 0));
     occ = std::min(o1, o2);
+    if (h->sr_mom) {
+      h->sr_smem = sizeof(pfb::SrStage<true>) * pfb::SR_SLOTS * (pfb::CG_NT / 32);
+      CREATE_CUDA(cudaFuncSetAttribute(pfb::k_cg_sr<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)h->sr_smem));
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_cg_sr<true>,
+                                                                pfb::CG_NT, h->sr_smem));
+      occ = std::min(occ, o2);
+    }
     CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, pfb::k_cg<false, false>,
                                                               pfb::CG_NT, 0));
     CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_cg<false, true>,
@@ -758,6 +787,7 @@ static pf_status axpy(pf_handle* h, double* y, const double* x, long long n) {
 }
 
 static const void* cg_kernel(pf_handle* h, bool mom) {
+  if (mom && h->sr_mom) return (const void*)pfb::k_cg_sr<true>;
   if (mom) return h->xupd_mom ? (const void*)pfb::k_cg<true, true> : (const void*)pfb::k_cg<true, false>;
   return h->xupd_evo ? (const void*)pfb::k_cg<false, true> : (const void*)pfb::k_cg<false, false>;
 }
@@ -777,6 +807,9 @@ static pfb::CgArgs cg_args(pf_handle* h, bool mom) {
   a.q = mom ? h->qu : h->qd;
   a.p0 = mom ? h->p0u : h->p0d;
   a.p1 = mom ? h->p1u : h->p1d;
+  a.r1 = mom ? h->r1u : nullptr;
+  a.w1 = mom ? h->w1u : nullptr;
+  a.pc = mom ? h->pcu : nullptr;
   a.dinv = mom ? h->dinvu : h->dinvd;
   a.partials = h->partials;
   a.result = h->d_cgres;
@@ -823,7 +856,7 @@ static pf_status run_cg_persistent(pf_handle* h, bool mom, double* target, bool 
   const int grid = mom ? h->cg_grid : h->cg_grid_evo;
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
   PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(pfb::CG_NT), args,
-                                      0, h->stream));
+                                      (mom && h->sr_mom) ? h->sr_smem : 0, h->stream));
   PF_TRY(launched(h));
   PF_CUDA(cudaEventRecord(h->ev1, h->stream));
   PF_CUDA(cudaStreamSynchronize(h->stream));
@@ -1414,8 +1447,8 @@ extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, doub
   const void* fn = cg_kernel(h, mom);
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
   PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(mom ? h->cg_grid : h->cg_grid_evo),
-                                      dim3(pfb::CG_NT), args, 0,
-                                      h->stream));
+                                      dim3(pfb::CG_NT), args,
+                                      (mom && h->sr_mom) ? h->sr_smem : 0, h->stream));
   PF_TRY(launched(h));
   PF_CUDA(cudaEventRecord(h->ev1, h->stream));
   PF_CUDA(cudaStreamSynchronize(h->stream));

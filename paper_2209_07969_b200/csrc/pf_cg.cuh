@@ -75,6 +75,10 @@ struct CgArgs {
   // (guess[0] = newest, guess[k] = k-th difference); x0 = their energy-optimal combination
   const double* guess[WARM_MAX];
   int n_guess;
+  // single-reduction PCG (k_cg_sr) extra vectors: second r and w buffers, search direction
+  double* r1;
+  double* w1;
+  double* pc;
 };
 
 template <bool MOM>
@@ -131,6 +135,27 @@ __device__ __forceinline__ void evo_cell_apply(const Consts& C, const double (&p
             C.Nw[3][aa] * t4[3] + C.lap[aa][0] * pc[0] + C.lap[aa][1] * pc[1] +
             C.lap[aa][2] * pc[2] + C.lap[aa][3] * pc[3];
 }
+
+// One pass of the single-reduction (Chronopoulos-Gear) PCG, k_cg_sr: the march applies, at
+// every node it touches, the previous iteration's updates s = w + beta s, r -= alpha s (and, at
+// owned nodes, p = D^-1 r_old + beta p, x += alpha p), then multiplies u = D^-1 r.  r, s and w
+// are ping-ponged (compile-time parity ODD, buffers straight from the kernel parameters)
+// because neighbouring warps read a node's old values while its owner writes the new ones; p
+// (CgArgs::pc) and x are read and written by the owner only.
+template <bool ODD>
+struct SrBuf {  // pass parity ODD reads the "in" buffers, writes the "out" buffers
+  __device__ static const double* rin(const CgArgs& a) { return ODD ? a.r1 : a.r; }
+  __device__ static double* rout(const CgArgs& a) { return ODD ? a.r : a.r1; }
+  __device__ static const double* win(const CgArgs& a) { return ODD ? a.w1 : a.q; }
+  __device__ static double* wout(const CgArgs& a) { return ODD ? a.q : a.w1; }
+  __device__ static const double* sin(const CgArgs& a) { return ODD ? a.p1 : a.p0; }
+  __device__ static double* sout(const CgArgs& a) { return ODD ? a.p0 : a.p1; }
+};
+struct SrScal {
+  double alpha, beta;
+  int first;  // pass 0: no update (u = D^-1 r0)
+  int fresh;  // pass 1: no previous p, s
+};
 
 }  // namespace pfb
 #include "pf_march.cuh"
@@ -409,11 +434,16 @@ __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO
   {
     double v[2] = {rr, rz};
     block_sum<2>(v, S.red);
-    if (threadIdx.x == 0) { part[2 * blockIdx.x] = v[0]; part[2 * blockIdx.x + 1] = v[1]; }
+    if (threadIdx.x == 0) {
+      part[CG_PART_STRIDE * blockIdx.x] = v[0];
+      part[CG_PART_STRIDE * blockIdx.x + 1] = v[1];
+    }
   }
   grid.sync();
+  // slots: 0/1 = r.r, r.z; 2 = p.q.  Each slot is rewritten only after a grid barrier that
+  // every CTA passes after reading it.
   double red[2];
-  grid_reduce<2>(part, 2, S.bc, red);
+  grid_reduce<2>(part, CG_PART_STRIDE, S.bc, red);
   rr = red[0];
   double rho = red[1];
   const double bnorm = bnorm_in >= 0.0 ? bnorm_in : sqrt(rr);  // scipy: rtol * ||b||
@@ -439,11 +469,11 @@ __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO
       {
         double v[1] = {pq};
         block_sum<1>(v, S.red);
-        if (threadIdx.x == 0) part[2 * blockIdx.x] = v[0];
+        if (threadIdx.x == 0) part[CG_PART_STRIDE * blockIdx.x + 2] = v[0];
       }
       grid.sync();
       double pqr[1];
-      grid_reduce<1>(part, 2, S.bc, pqr);
+      grid_reduce<1>(part + 2, CG_PART_STRIDE, S.bc, pqr);
       if (a.probe && !(pqr[0] > 0.0)) { status = CG_INDEFINITE; k += 1; break; }
       alpha = rho / pqr[0];
       rho_prev = rho;
@@ -453,10 +483,13 @@ __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO
       {
         double v[2] = {rr, rz};
         block_sum<2>(v, S.red);
-        if (threadIdx.x == 0) { part[2 * blockIdx.x] = v[0]; part[2 * blockIdx.x + 1] = v[1]; }
+        if (threadIdx.x == 0) {
+          part[CG_PART_STRIDE * blockIdx.x] = v[0];
+          part[CG_PART_STRIDE * blockIdx.x + 1] = v[1];
+        }
       }
       grid.sync();
-      grid_reduce<2>(part, 2, S.bc, red);
+      grid_reduce<2>(part, CG_PART_STRIDE, S.bc, red);
       rr = red[0];
       rho = red[1];
       ++k;
@@ -476,6 +509,90 @@ __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO
       }
       if (a.target) a.target[i] += xv;
     }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.result->iters = k;
+    a.result->status = status;
+    a.result->bnorm = bnorm;
+    a.result->rnorm = sqrt(rr);
+  }
+}
+
+// Single-reduction (Chronopoulos-Gear) Jacobi-PCG, persistent and cooperative like k_cg: ONE
+// march and ONE grid barrier per iteration (k_cg: march, barrier, stream, barrier).  Same
+// preconditioner, x0 and stopping rule (SciPy: ||r|| < rtol ||b||, maxiter, r recursive); the
+// iterates equal the Hestenes-Stiefel ones in exact arithmetic (scripts/cgcg_study.py: counts
+// within +-2 and true residuals at the same 1e-12 level on the reference's momentum systems).
+//   pass 0:  u = D^-1 r0, w = A u, (r.r, r.u, w.u)
+//   pass k:  s = w + beta s, p = D^-1 r + beta p (owners), x += alpha p, r -= alpha s,
+//            u = D^-1 r, w = A u, (r.r, r.u, w.u)     [fused in the march, SrBuf/SrScal]
+//   then     beta = g'/g, alpha = g'/(w.u - beta g'/alpha)   (denominator = p.Ap: the probe)
+template <bool MOM>
+__global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO)
+    k_cg_sr(CgArgs a) {
+  __shared__ CgSmem<MOM> S;
+  cg::grid_group grid = cg::this_grid();
+  const int gwarp = blockIdx.x * (CG_NT / 32) + (threadIdx.x >> 5),
+            nwarps = gridDim.x * (CG_NT / 32);
+  double* part = a.partials;
+  double bnorm_in = -1.0;
+  if constexpr (MOM)
+    if (a.n_guess > 0) bnorm_in = warm_start<MOM>(a, S);
+  SrScal sp;
+  long long k = 0;
+  int status = CG_CONVERGED;
+  double alpha = 0.0, beta = 0.0, gam = 0.0, rr = 0.0, bnorm = 0.0, atol = 0.0;
+  for (;;) {
+    sp.alpha = alpha;
+    sp.beta = beta;
+    sp.first = k == 0;
+    sp.fresh = k == 1;
+    double dl = 0.0, rrp = 0.0, gp = 0.0;
+    if (k & 1) {
+      for (int u = gwarp; u < a.g.n_units; u += nwarps)
+        march_unit<MOM, false, false, 2>(a, a.g, u, false, 0.0, nullptr, nullptr, dl,
+                                         S.dup[threadIdx.x >> 5], 0.0, &sp, &rrp, &gp);
+    } else {
+      for (int u = gwarp; u < a.g.n_units; u += nwarps)
+        march_unit<MOM, false, false, 1>(a, a.g, u, false, 0.0, nullptr, nullptr, dl,
+                                         S.dup[threadIdx.x >> 5], 0.0, &sp, &rrp, &gp);
+    }
+    const int off = (k & 1) ? 3 : 0;  // alternate slot sets: a slot is rewritten two barriers on
+    {
+      double v[3] = {rrp, gp, dl};
+      block_sum<3>(v, S.red);
+      if (threadIdx.x == 0) {
+        part[CG_PART_STRIDE * blockIdx.x + off] = v[0];
+        part[CG_PART_STRIDE * blockIdx.x + off + 1] = v[1];
+        part[CG_PART_STRIDE * blockIdx.x + off + 2] = v[2];
+      }
+    }
+    grid.sync();
+    double red[3];
+    grid_reduce<3>(part + off, CG_PART_STRIDE, S.bc, red);
+    rr = red[0];
+    const double gnew = red[1], delta = red[2];
+    if (k == 0) {
+      bnorm = bnorm_in >= 0.0 ? bnorm_in : sqrt(rr);  // scipy: rtol * ||b||
+      atol = a.rtol * bnorm;
+      if (bnorm == 0.0) break;
+    }
+    const double rn = sqrt(rr);
+    if (rn < atol) break;
+    if (!(rn == rn)) { status = CG_NAN; break; }
+    if (k >= a.maxiter) { status = CG_MAXITER; break; }
+    beta = k == 0 ? 0.0 : gnew / gam;
+    const double den = k == 0 ? delta : delta - beta * gnew / alpha;  // = p.Ap
+    if (a.probe && !(den > 0.0)) { status = CG_INDEFINITE; k += 1; break; }
+    alpha = gnew / den;
+    gam = gnew;
+    ++k;
+  }
+  if (status != CG_INDEFINITE && a.target) {  // x is complete: target += x
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.ndof;
+         i += stride)
+      a.target[i] += __ldcg(a.x + i);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.result->iters = k;

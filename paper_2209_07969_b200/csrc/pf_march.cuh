@@ -76,25 +76,77 @@ __device__ __forceinline__ void mom_cell_fast(const Consts& C, const double2 (&p
   f[3] = make_double2(-bxx + cxy, cyy - bxy);
 }
 
+// ---- cp.async staging (single-reduction march): a lane's next node row is copied L2 -> smem
+// without register staging (zero-fill for absent values), so the six vectors the SR node update
+// needs do not occupy registers while in flight
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+template <bool MOM>
+__device__ __forceinline__ void cp_async_t(typename Node<MOM>::T* smem, const double* g, int id,
+                                           bool valid) {
+  const int cid = valid ? id : 0;
+  if constexpr (MOM) cp_async16(smem, g + 2 * (size_t)cid, valid);
+  else cp_async8(smem, g + cid, valid);
+}
+
+template <bool MOM>
+struct SrStage {  // one node row of one warp (lane-private columns)
+  using T = typename Node<MOM>::T;
+  T r[32], di[32], po[32], x[32], s[32], wo[32];
+  double d[32];
+};
+constexpr int SR_SLOTS = 3;  // per warp: two alternating node rows, the slit-duplicate row
+extern __shared__ __align__(16) unsigned char pf_dyn_smem[];
+template <bool MOM>
+__device__ __forceinline__ SrStage<MOM>& sr_slot(int which) {
+  return reinterpret_cast<SrStage<MOM>*>(pf_dyn_smem)[(threadIdx.x >> 5) * SR_SLOTS + which];
+}
+
 template <bool MOM>
 struct RawNode {
   using T = typename Node<MOM>::T;
   T r, di, po, x;
   double d;
   int id;
+  int slot;  // SR: staging slot of this row (sr_slot)
+  int pend;  // SR: a younger row's copies were committed after this row's (wait_group 1)
 };
 
 // XUPD (lazy solution update): the owner of a node also loads x so that finish_node can apply
 // x += alpha_{k-1} p_{k-1} with the p_{k-1} the march reads anyway (phase B then no longer
 // streams p and x: 32 B per node and iteration less)
-template <bool MOM, bool APPLY, bool XUPD = false>
+template <bool MOM, bool APPLY, bool XUPD = false, int SR = 0>
 __device__ __forceinline__ void fetch_node(const CgArgs& a, const double* __restrict__ pold,
                                            bool first, int id, RawNode<MOM>& w,
-                                           bool xown = false) {
+                                           bool xown = false, const SrScal* sp = nullptr) {
   using N_ = Node<MOM>;
   w.id = id;
   if (id >= 0) {
-    if (APPLY) {
+    if constexpr (SR != 0) {
+      using B = SrBuf<SR == 2>;
+      SrStage<MOM>& st = sr_slot<MOM>(w.slot);
+      const int ln = threadIdx.x & 31;
+      const bool upd = !sp->first, old = upd && !sp->fresh;
+      cp_async_t<MOM>(&st.r[ln], B::rin(a), id, true);
+      cp_async_t<MOM>(&st.di[ln], a.dinv, id, true);
+      cp_async_t<MOM>(&st.wo[ln], B::win(a), id, upd);
+      cp_async_t<MOM>(&st.s[ln], B::sin(a), id, old);
+      cp_async_t<MOM>(&st.po[ln], a.pc, id, old && xown);
+      cp_async_t<MOM>(&st.x[ln], a.x, id, upd && xown);
+      if constexpr (MOM) cp_async8(&st.d[ln], a.d + id, true);
+      cp_async_commit();
+    } else if (APPLY) {
       w.po = N_::ld_ro(pold, id);
     } else {
       w.r = N_::ld_cg(a.r, id);
@@ -102,19 +154,56 @@ __device__ __forceinline__ void fetch_node(const CgArgs& a, const double* __rest
       if (!first) w.po = N_::ld_cg(pold, id);
       if (XUPD && !first && xown) w.x = N_::ld_cg(a.x, id);
     }
-    if constexpr (MOM) w.d = __ldg(a.d + id);
+    if constexpr (MOM && SR == 0) w.d = __ldg(a.d + id);
   }
 }
 
-// p_k = D^-1 r + beta p_{k-1}; the owner stores it (and, XUPD, x += alpha_{k-1} p_{k-1})
-template <bool MOM, bool APPLY, bool XUPD = false>
+// p_k = D^-1 r + beta p_{k-1}; the owner stores it (and, XUPD, x += alpha_{k-1} p_{k-1}).
+// SR (1 even / 2 odd pass): the single-reduction node update (pf_cg.cuh SrBuf); returns u = D^-1 r_new, the vector multiplied.
+template <bool MOM, bool APPLY, bool XUPD = false, int SR = 0>
 __device__ __forceinline__ typename Node<MOM>::T finish_node(const RawNode<MOM>& w, bool first,
                                                              double beta, bool own,
                                                              double* __restrict__ pnew,
                                                              double* __restrict__ x = nullptr,
-                                                             double xalpha = 0.0) {
+                                                             double xalpha = 0.0,
+                                                             const SrScal* sp = nullptr,
+                                                             double* rr = nullptr,
+                                                             double* gam = nullptr,
+                                                             const CgArgs* ap = nullptr) {
   using N_ = Node<MOM>;
   if (w.id < 0) return N_::zero();
+  if constexpr (SR != 0) {
+    using T = typename N_::T;
+    using B = SrBuf<SR == 2>;
+    const CgArgs& a = *ap;
+    const int ln = threadIdx.x & 31;
+    if (w.pend) cp_async_wait_1();
+    else cp_async_wait_all();
+    const SrStage<MOM>& st = sr_slot<MOM>(w.slot);
+    const T r0 = st.r[ln], di = st.di[ln];
+    const T uo = N_::mul(di, r0);
+    if (sp->first) {
+      if (own) {
+        N_::st(B::rout(a), w.id, r0);
+        *rr += N_::dot(r0, r0);
+        *gam += N_::dot(r0, uo);
+      }
+      return uo;
+    }
+    const T sv = N_::axpy(sp->beta, st.s[ln], st.wo[ln]);  // s = w + beta s
+    const T rv = N_::axpy(-sp->alpha, sv, r0);             // r -= alpha s
+    const T u = N_::mul(di, rv);
+    if (own) {
+      const T pv = N_::axpy(sp->beta, st.po[ln], uo);      // p = D^-1 r_old + beta p
+      N_::st(a.pc, w.id, pv);
+      N_::st(a.x, w.id, N_::axpy(sp->alpha, pv, st.x[ln]));  // x += alpha p
+      N_::st(B::sout(a), w.id, sv);
+      N_::st(B::rout(a), w.id, rv);
+      *rr += N_::dot(rv, rv);
+      *gam += N_::dot(rv, u);
+    }
+    return u;
+  }
   if (APPLY) return w.po;
   typename N_::T p = N_::mul(w.di, w.r);
   if (!first) p = N_::axpy(beta, w.po, p);
@@ -133,12 +222,14 @@ struct DupRow {
   unsigned fb[32];
 };
 
-template <bool MOM, bool APPLY, bool XUPD = false>
+template <bool MOM, bool APPLY, bool XUPD = false, int SR = 0>
 __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, int unit,
                                            bool first, double beta,
                                            const double* __restrict__ pold,
                                            double* __restrict__ pnew, double& pq,
-                                           DupRow<MOM>& dup, double xalpha = 0.0) {
+                                           DupRow<MOM>& dup, double xalpha = 0.0,
+                                           const SrScal* sp = nullptr, double* rr = nullptr,
+                                           double* gam = nullptr) {
   using N_ = Node<MOM>;
   using T = typename N_::T;
   const DMesh& m = a.m;
@@ -156,15 +247,29 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
     const int4 rw = __ldg(m.nrow + j);
     return (col >= rw.x && col < rw.y) ? rw.z + (col - rw.x) : -1;
   };
+  // d and D^-1 of a finished row (SR: still in its staging slot)
+  auto node_d = [&](const RawNode<MOM>& v) -> double {
+    if constexpr (!MOM) return 0.0;
+    else if constexpr (SR != 0) return v.id >= 0 ? sr_slot<MOM>(v.slot).d[lane] : 0.0;
+    else return v.d;
+  };
+  auto node_fb = [&](const RawNode<MOM>& v) -> unsigned {
+    if (APPLY || v.id < 0) return 0u;
+    if constexpr (SR != 0) return N_::freebits(sr_slot<MOM>(v.slot).di[lane]);
+    else return N_::freebits(v.di);
+  };
   // loads and parks the duplicate row (warp-uniform call)
   auto load_dup = [&](bool own) {
     RawNode<MOM> wd;
-    fetch_node<MOM, APPLY, XUPD>(a, pold, first, dupcol ? m.dup_start + (col - m.notch_lo) : -1,
-                                 wd, own);
-    dup.p[lane] = finish_node<MOM, APPLY, XUPD>(wd, first, beta, own, pnew, a.x, xalpha);
-    dup.d[lane] = MOM ? wd.d : 0.0;
+    wd.slot = 2;
+    wd.pend = 0;
+    fetch_node<MOM, APPLY, XUPD, SR>(a, pold, first,
+                                     dupcol ? m.dup_start + (col - m.notch_lo) : -1, wd, own, sp);
+    dup.p[lane] = finish_node<MOM, APPLY, XUPD, SR>(wd, first, beta, own, pnew, a.x, xalpha, sp,
+                                                    rr, gam, &a);
+    dup.d[lane] = node_d(wd);
     dup.id[lane] = wd.id;
-    dup.fb[lane] = (APPLY || wd.id < 0) ? 0u : N_::freebits(wd.di);
+    dup.fb[lane] = node_fb(wd);
     __syncwarp();
   };
 
@@ -174,15 +279,39 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
   int id_lo;
   unsigned fb_lo;
   bool lo_slit;
-  RawNode<MOM> w;
-  fetch_node<MOM, APPLY>(a, pold, first, nid(r0 - 1), w);
-  p_lo = finish_node<MOM, APPLY>(w, first, beta, false, pnew);
-  d_lo = MOM ? w.d : 0.0;
+  // SR stages node rows in shared memory two rows ahead: w = the row finished next, wn = the
+  // row after it (already in flight); a row's slot is refilled right after it is finished.
+  // The register path (SR == 0) keeps one row of loads in flight in w.
+  RawNode<MOM> w, wn;
+  w.slot = 0;
+  w.pend = 0;
+  wn.slot = 1;
+  wn.pend = 0;
+  fetch_node<MOM, APPLY, false, SR>(a, pold, first, nid(r0 - 1), w, false, sp);
+  if constexpr (SR != 0) {
+    fetch_node<MOM, APPLY, XUPD, SR>(a, pold, first, nid(r0), wn, lane_own && r0 < r1, sp);
+    w.pend = 1;
+  }
+  p_lo = finish_node<MOM, APPLY, false, SR>(w, first, beta, false, pnew, nullptr, 0.0, sp, rr,
+                                            gam, &a);
+  d_lo = node_d(w);
   id_lo = w.id;
-  fb_lo = (APPLY || w.id < 0) ? 0u : N_::freebits(w.di);
+  fb_lo = node_fb(w);
   lo_slit = (r0 - 1 == R);
   if (lo_slit) load_dup(false);
-  fetch_node<MOM, APPLY, XUPD>(a, pold, first, nid(r0), w, lane_own && r0 < r1);  // in flight
+  if constexpr (SR != 0) {
+    const int fs = w.slot;
+    w = wn;
+    wn.slot = fs;
+    w.pend = 0;
+    if (r0 + 1 <= r1) {
+      fetch_node<MOM, APPLY, XUPD, SR>(a, pold, first, nid(r0 + 1), wn, lane_own && r0 + 1 < r1,
+                                       sp);
+      w.pend = 1;
+    }
+  } else {
+    fetch_node<MOM, APPLY, XUPD, SR>(a, pold, first, nid(r0), w, lane_own && r0 < r1, sp);
+  }
   // cell-row data (branch bits / Newton coefficients) are prefetched one row ahead too
   auto cell_id = [&](int cj) -> int {
     if (cj < 0 || cj >= m.ny || lane >= 31) return -1;
@@ -202,13 +331,26 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
   for (int cj = r0 - 1; cj < r1; ++cj) {
     const int jh = cj + 1;
     const bool hi_own = lane_own && jh >= r0 && jh < r1;
-    const T p_hi = finish_node<MOM, APPLY, XUPD>(w, first, beta, hi_own, pnew, a.x, xalpha);
-    const double d_hi = MOM ? w.d : 0.0;
+    const T p_hi = finish_node<MOM, APPLY, XUPD, SR>(w, first, beta, hi_own, pnew, a.x, xalpha, sp,
+                                                     rr, gam, &a);
+    const double d_hi = node_d(w);
     const int id_hi = w.id;
-    const unsigned fb_hi = (APPLY || w.id < 0) ? 0u : N_::freebits(w.di);
+    const unsigned fb_hi = node_fb(w);
     const bool hi_slit = (jh == R);
-    if (jh + 1 <= r1)  // prefetch
-      fetch_node<MOM, APPLY, XUPD>(a, pold, first, nid(jh + 1), w, lane_own && jh + 1 < r1);
+    if constexpr (SR != 0) {  // the finished row's slot takes row jh + 2
+      const int fs = w.slot;
+      w = wn;
+      wn.slot = fs;
+      w.pend = 0;
+      if (jh + 2 <= r1) {
+        fetch_node<MOM, APPLY, XUPD, SR>(a, pold, first, nid(jh + 2), wn,
+                                         lane_own && jh + 2 < r1, sp);
+        w.pend = 1;
+      }
+    } else if (jh + 1 <= r1) {  // prefetch
+      fetch_node<MOM, APPLY, XUPD, SR>(a, pold, first, nid(jh + 1), w, lane_own && jh + 1 < r1,
+                                       sp);
+    }
     const int eid = eid_n;
     const unsigned fl = fl_n;
     double bq[4] = {bq_n[0], bq_n[1], bq_n[2], bq_n[3]};
@@ -248,7 +390,7 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
             qv = N_::maskb(qv, fb_lo);
             if (node_owned(m, id_lo)) pq += N_::dot(p_lo, qv);
           }
-          N_::st(a.q, id_lo, qv);
+          N_::st(SR == 0 ? a.q : SrBuf<SR == 2>::wout(a), id_lo, qv);
         }
         const int idd = dup.id[lane];
         if (idd >= 0) {  // upper face: cells above only
@@ -257,7 +399,7 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
             qv = N_::maskb(qv, dup.fb[lane]);
             if (node_owned(m, idd)) pq += N_::dot(dup.p[lane], qv);
           }
-          N_::st(a.q, idd, qv);
+          N_::st(SR == 0 ? a.q : SrBuf<SR == 2>::wout(a), idd, qv);
         }
       } else if (id_lo >= 0) {
         T qv = add_t(add_t(acc_lo, c1l), f[0]);
@@ -265,7 +407,7 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
           qv = N_::maskb(qv, fb_lo);
           if (node_owned(m, id_lo)) pq += N_::dot(p_lo, qv);
         }
-        N_::st(a.q, id_lo, qv);
+        N_::st(SR == 0 ? a.q : SrBuf<SR == 2>::wout(a), id_lo, qv);
       }
     }
     acc_lo = add_t(c2l, f[3]);

@@ -186,28 +186,33 @@ def test_determinism_and_dropin_equivalence(cuda_ok):
     assert np.array_equal(got["u"], outs[0][0]) and np.array_equal(got["d"], outs[0][1])
 
 
+@pytest.mark.parametrize("variant", ["PFB200_XUPD", "PFB200_SR"])
 @pytest.mark.parametrize("case_name", ["tension16", "lpanel25"])
-def test_lazy_x_variant_matches_default(cuda_ok, monkeypatch, case_name):
-    """The lazy-x PCG variant (x += alpha p folded into the next march; chosen automatically
-    only for meshes far beyond L2, e.g. cfg5) computes the same iterates: forced on for a
-    small mesh, every staggered iteration count and the final fields match the default."""
+def test_pcg_variants_match(cuda_ok, monkeypatch, case_name, variant):
+    """The momentum PCG variants the host picks by mesh size give the reference CG's answers:
+    lazy x (x += alpha p folded into the next march; automatic for meshes far beyond L2) has
+    the same iterates; single-reduction (Chronopoulos-Gear; automatic for L2-resident meshes)
+    has the same iterates in exact arithmetic.  Each is forced on and off for a small mesh:
+    staggered counts equal, PCG counts within 1%, fields within 1e-9."""
     from paper_2209_07969_b200.session import DeviceSession
 
     case = C.get_case(case_name)
     runs = []
     for flag in ("0", "1"):
-        monkeypatch.setenv("PFB200_XUPD", flag)
+        monkeypatch.setenv(variant, flag)
         pb = C.setup(case, C.b200_api())
         s = DeviceSession(pb.disc.layout, pb.params, pb.config, device=0)
         s.push_state(pb.state)
         stats = [s.step("S1", pb.bcs, pb.pins) for _ in range(6)]
-        got = s.pull()
-        runs.append(([(st.n_stag, st.cg_iters_u, st.cg_iters_d) for st in stats], got))
+        runs.append((stats, s.pull()))
         s.close()
-    assert runs[0][0] == runs[1][0]
+    (s0, g0), (s1, g1) = runs
+    assert [x.n_stag for x in s0] == [x.n_stag for x in s1]
+    for a, b in zip(s0, s1):
+        assert abs(a.cg_iters_u - b.cg_iters_u) <= max(2, 0.01 * a.cg_iters_u)
+        assert abs(a.cg_iters_d - b.cg_iters_d) <= max(2, 0.01 * a.cg_iters_d)
     for k in ("u", "d"):
-        a, b = runs[0][1][k], runs[1][1][k]
-        assert np.max(np.abs(a - b)) <= 1e-12 * max(1.0, np.max(np.abs(a))), k
+        assert np.max(np.abs(g0[k] - g1[k])) <= 1e-9 * max(1.0, np.max(np.abs(g0[k]))), k
 
 
 def test_errors_map_to_reference_exceptions(cuda_ok):
