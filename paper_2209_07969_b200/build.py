@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         return OUT
     target = out or OUT
     inc = ["-I", NCCL_INCLUDE] if NCCL_INCLUDE else []
-    cmd = [nvcc(), *NVCC_FLAGS, *inc, *[f"-D{d}" for d in defines], "-ldl",
+    cmd = [nvcc(), *NVCC_FLAGS, *inc, *[f"-D{d}" for d in defines], "-ldl", "-lpthread",
            "-o", target + ".tmp", *SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

@@ -8,11 +8,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pf_b200.h"
@@ -75,6 +77,8 @@ struct pf_handle {
   double* warm_buf[WARM_SLOTS][pfb::WARM_MAX] = {};
   int warm_n[WARM_SLOTS] = {};
   bool xupd_mom = false, xupd_evo = false;  // lazy-x PCG variants (k_cg<MOM, true>)
+  double* stage = nullptr;  // pinned host staging buffer for state transfers
+  size_t stage_cap = 0;     // doubles
   bool sr_mom = false;  // momentum solves by the single-reduction PCG (k_cg_sr<true>)
   size_t sr_smem = 0;   // its dynamic shared memory (cp.async staging slots)
   pfb::MarchGeom geom_mom{}, geom_evo{}, geom_apply{};
@@ -223,6 +227,7 @@ extern "C" void pf_destroy(pf_handle* h) {
   for (auto& row : h->warm_buf)
     for (double* p : row)
       if (p) cudaFree(p);
+  if (h->stage) cudaFreeHost(h->stage);
   for (auto& row : h->graphs)
     for (auto& g : row)
       if (g) cudaGraphExecDestroy(g);
@@ -584,16 +589,97 @@ extern "C" pf_status pf_host_group_create(int32_t nranks, void** out) {
 extern "C" void pf_host_group_destroy(void* group) { delete static_cast<pfb::HostGroup*>(group); }
 
 // ------------------------------------------------------------------------------------------
-// state transfer
-static pf_status h2d(pf_handle* h, double* dst, const double* src, size_t n) {
-  if (!src) return PF_OK;
-  PF_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+// state transfer.  Host arrays are ordinary (pageable) caller memory: large transfers go through
+// one pinned staging buffer, the host-side copy split over a few threads (the driver's pageable
+// path is a single-threaded staged copy; fresh output arrays also fault their pages in there).
+struct Xfer {
+  double* host;
+  double* dev;
+  size_t n;
+};
+
+// bytes-balanced parallel memcpy over a list of (dst, src, bytes) segments
+static void par_copy(const std::vector<std::array<size_t, 3>>& seg) {
+  size_t total = 0;
+  for (const auto& sg : seg) total += sg[2];
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nt = std::min<size_t>({(size_t)8, (size_t)hw, std::max<size_t>(1, total >> 22)});
+  auto run = [&](size_t lo, size_t hi) {  // global byte range [lo, hi)
+    size_t base = 0;
+    for (const auto& sg : seg) {
+      const size_t a = std::max(lo, base), b = std::min(hi, base + sg[2]);
+      if (a < b)
+        std::memcpy(reinterpret_cast<char*>(sg[0]) + (a - base),
+                    reinterpret_cast<const char*>(sg[1]) + (a - base), b - a);
+      base += sg[2];
+    }
+  };
+  if (nt <= 1) return run(0, total);
+  std::vector<std::thread> th;
+  const size_t step = (total + nt - 1) / nt;
+  for (size_t t = 1; t < nt; ++t) th.emplace_back(run, t * step, std::min(total, (t + 1) * step));
+  run(0, std::min(total, step));
+  for (auto& t : th) t.join();
+}
+
+static pf_status ensure_stage(pf_handle* h, size_t n) {
+  if (n <= h->stage_cap) return PF_OK;
+  if (h->stage) cudaFreeHost(h->stage);
+  h->stage = nullptr;
+  h->stage_cap = 0;
+  PF_CUDA(cudaHostAlloc((void**)&h->stage, n * sizeof(double), cudaHostAllocDefault));
+  h->stage_cap = n;
   return PF_OK;
 }
-static pf_status d2h(pf_handle* h, double* dst, const double* src, size_t n) {
-  if (!dst) return PF_OK;
-  PF_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+
+static constexpr size_t STAGE_MIN = 1 << 19;  // doubles (4 MB): below, plain pageable copies
+
+static pf_status transfer(pf_handle* h, const std::vector<Xfer>& items, bool to_device) {
+  size_t total = 0;
+  for (const auto& it : items)
+    if (it.host) total += it.n;
+  if (total < STAGE_MIN) {
+    for (const auto& it : items)
+      if (it.host)
+        PF_CUDA(cudaMemcpyAsync(to_device ? (void*)it.dev : (void*)it.host,
+                                to_device ? (const void*)it.host : (const void*)it.dev,
+                                it.n * sizeof(double),
+                                to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                                h->stream));
+    PF_CUDA(cudaStreamSynchronize(h->stream));
+    return PF_OK;
+  }
+  PF_TRY(ensure_stage(h, total));
+  std::vector<std::array<size_t, 3>> seg;
+  size_t off = 0;
+  for (const auto& it : items) {
+    if (!it.host) continue;
+    double* st = h->stage + off;
+    if (to_device) seg.push_back({(size_t)st, (size_t)it.host, it.n * sizeof(double)});
+    else seg.push_back({(size_t)it.host, (size_t)st, it.n * sizeof(double)});
+    off += it.n;
+  }
+  if (to_device) par_copy(seg);
+  off = 0;
+  for (const auto& it : items) {
+    if (!it.host) continue;
+    PF_CUDA(cudaMemcpyAsync(to_device ? (void*)it.dev : (void*)(h->stage + off),
+                            to_device ? (const void*)(h->stage + off) : (const void*)it.dev,
+                            it.n * sizeof(double),
+                            to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                            h->stream));
+    off += it.n;
+  }
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  if (!to_device) par_copy(seg);
   return PF_OK;
+}
+
+static pf_status h2d(pf_handle* h, double* dst, const double* src, size_t n) {
+  return transfer(h, {{const_cast<double*>(src), dst, n}}, true);
+}
+static pf_status d2h(pf_handle* h, double* dst, const double* src, size_t n) {
+  return transfer(h, {{dst, const_cast<double*>(src), n}}, false);
 }
 
 extern "C" pf_status pf_set_state(pf_handle* h, const double* u, const double* d,
@@ -601,30 +687,22 @@ extern "C" pf_status pf_set_state(pf_handle* h, const double* u, const double* d
                                   const double* psi, const double* psimax) {
   PF_CUDA(cudaSetDevice(h->device));
   const size_t nn = h->n_nodes, ng = 4 * (size_t)h->n_elems;
-  PF_TRY(h2d(h, h->u, u, 2 * nn));
-  PF_TRY(h2d(h, h->d, d, nn));
-  PF_TRY(h2d(h, h->dprev, d_prev, nn));
-  PF_TRY(h2d(h, h->trp, trp, ng));
-  PF_TRY(h2d(h, h->dev2, dev2, ng));
-  PF_TRY(h2d(h, h->psi, psi, ng));
-  PF_TRY(h2d(h, h->psimax, psimax, ng));
-  PF_CUDA(cudaStreamSynchronize(h->stream));
-  return PF_OK;
+  auto c = [](const double* p) { return const_cast<double*>(p); };
+  return transfer(h,
+                  {{c(u), h->u, 2 * nn}, {c(d), h->d, nn}, {c(d_prev), h->dprev, nn},
+                   {c(trp), h->trp, ng}, {c(dev2), h->dev2, ng}, {c(psi), h->psi, ng},
+                   {c(psimax), h->psimax, ng}},
+                  true);
 }
 
 extern "C" pf_status pf_get_state(pf_handle* h, double* u, double* d, double* d_prev,
                                   double* trp, double* dev2, double* psi, double* psimax) {
   PF_CUDA(cudaSetDevice(h->device));
   const size_t nn = h->n_nodes, ng = 4 * (size_t)h->n_elems;
-  PF_TRY(d2h(h, u, h->u, 2 * nn));
-  PF_TRY(d2h(h, d, h->d, nn));
-  PF_TRY(d2h(h, d_prev, h->dprev, nn));
-  PF_TRY(d2h(h, trp, h->trp, ng));
-  PF_TRY(d2h(h, dev2, h->dev2, ng));
-  PF_TRY(d2h(h, psi, h->psi, ng));
-  PF_TRY(d2h(h, psimax, h->psimax, ng));
-  PF_CUDA(cudaStreamSynchronize(h->stream));
-  return PF_OK;
+  return transfer(h,
+                  {{u, h->u, 2 * nn}, {d, h->d, nn}, {d_prev, h->dprev, nn}, {trp, h->trp, ng},
+                   {dev2, h->dev2, ng}, {psi, h->psi, ng}, {psimax, h->psimax, ng}},
+                  false);
 }
 
 static dim3 cell_grid(const pf_handle* h) { return dim3((h->nx + 127) / 128, h->ny); }
@@ -653,7 +731,6 @@ extern "C" pf_status pf_get_gp_strain(pf_handle* h, double* strain, double* tr_e
     pfb::k_refresh_gp<<<cell_grid(h), 128, 0, h->stream>>>(g);
     PF_TRY(launched(h));
     PF_TRY(d2h(h, tr_eps, tr_dev, 4 * ne));
-    PF_CUDA(cudaStreamSynchronize(h->stream));
   }
   if (strain) {
     g.tr = nullptr;
@@ -661,7 +738,6 @@ extern "C" pf_status pf_get_gp_strain(pf_handle* h, double* strain, double* tr_e
     pfb::k_refresh_gp<<<cell_grid(h), 128, 0, h->stream>>>(g);
     PF_TRY(launched(h));
     PF_TRY(d2h(h, strain, h->scratch, 16 * ne));
-    PF_CUDA(cudaStreamSynchronize(h->stream));
   }
   return PF_OK;
 }

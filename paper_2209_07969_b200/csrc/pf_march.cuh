@@ -220,6 +220,9 @@ struct DupRow {
   double d[32];
   int id[32];
   unsigned fb[32];
+  // 32-row windows of the node-row / cell-row tables (refilled by one coalesced load every 32
+  // rows): the per-row lookups are shared-memory broadcasts instead of dependent global loads
+  int4 nwin[32], ewin[32];
 };
 
 template <bool MOM, bool APPLY, bool XUPD = false, int SR = 0>
@@ -242,9 +245,17 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
   const bool lane_own = lane >= 1 && lane <= TXW;
   const int R = m.notch_row;
   const bool dupcol = R >= 0 && col >= m.notch_lo && col < m.notch_hi;
+  int nbase = -1000000, ebase = -1000000;  // warp-uniform window bases
   auto nid = [&](int j) -> int {
     if (j < 0 || j > m.ny) return -1;
-    const int4 rw = __ldg(m.nrow + j);
+    if (j - nbase >= 32 || j < nbase) {  // warp-uniform refill
+      __syncwarp();
+      nbase = j;
+      const int jj = j + lane;
+      dup.nwin[lane] = jj <= m.ny ? __ldg(m.nrow + jj) : make_int4(0, 0, 0, 0);
+      __syncwarp();
+    }
+    const int4 rw = dup.nwin[j - nbase];
     return (col >= rw.x && col < rw.y) ? rw.z + (col - rw.x) : -1;
   };
   // d and D^-1 of a finished row (SR: still in its staging slot)
@@ -314,8 +325,16 @@ __device__ __forceinline__ void march_unit(const CgArgs& a, const MarchGeom& G, 
   }
   // cell-row data (branch bits / Newton coefficients) are prefetched one row ahead too
   auto cell_id = [&](int cj) -> int {
-    if (cj < 0 || cj >= m.ny || lane >= 31) return -1;
-    const int4 er = __ldg(m.erow + cj);
+    if (cj < 0 || cj >= m.ny) return -1;
+    if (cj - ebase >= 32 || cj < ebase) {  // warp-uniform refill
+      __syncwarp();
+      ebase = cj;
+      const int jj = cj + lane;
+      dup.ewin[lane] = jj < m.ny ? __ldg(m.erow + jj) : make_int4(0, 0, 0, 0);
+      __syncwarp();
+    }
+    if (lane >= 31) return -1;
+    const int4 er = dup.ewin[cj - ebase];
     return (col >= er.x && col < er.y) ? er.z + (col - er.x) : -1;
   };
   int eid_n = cell_id(r0 - 1);

@@ -117,3 +117,26 @@ def test_fixed_length_pcg_benchmark_entry(cuda_ok):
         ms, it = s.bench_cg(phys, 7)
         assert it == 7 and ms > 0.0
     s.close()
+
+
+def test_state_roundtrip_through_pinned_staging(cuda_ok):
+    """pf_set_state / pf_get_state move large states through the pinned staging buffer with
+    threaded host copies (>= 4 MB); the round trip is bit-exact and fresh output arrays work."""
+    from paper_2209_07969_b200 import meshing
+    from paper_2209_07969_b200.session import DeviceSession
+
+    lay = meshing.StructuredLayout.rectangle(300, 300, 1.0 / 300, 1.0 / 300)
+    s = DeviceSession(lay, kat_params("at2"), _Cfg(), device=0)
+    rng = np.random.default_rng(9)
+    nn, ne = lay.n_nodes, lay.n_elems
+    want = dict(u=rng.standard_normal(2 * nn), d=rng.random(nn), d_prev=rng.random(nn),
+                tr_eps_plus=rng.standard_normal((ne, 4)), dev_dot_dev=rng.random((ne, 4)),
+                psi_plus=rng.random((ne, 4)), psi_max=rng.random((ne, 4)))
+    assert sum(v.size for v in want.values()) * 8 > 4 << 20
+    s.push(**want)
+    got = s.pull()
+    for k, v in want.items():
+        assert np.array_equal(got[k].reshape(v.shape), v), k
+    strain, tr = s.gp_strain()
+    assert strain.shape == (ne, 4, 4) and np.all(np.isfinite(strain)) and np.all(np.isfinite(tr))
+    s.close()
