@@ -428,12 +428,11 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
   CREATE_ALLOC(h->p0u, 2 * nn);
   CREATE_ALLOC(h->p1u, 2 * nn);
   {
-    // single-reduction momentum PCG where the iteration is latency-bound (working set in L2:
-    // cfg1 -11%, cfg2 -8% per iteration); the two-barrier form where bytes dominate (cfg4 +12%,
-    // cfg3 +8%, cfg5 +5% with the single-reduction form).  PFB200_SR=0/1 forces (A/B tests).
-    int l2b = 0;
-    CREATE_CUDA(cudaDeviceGetAttribute(&l2b, cudaDevAttrL2CacheSize, device));
-    h->sr_mom = 168.0 * (double)nn <= (double)l2b;
+    // single-reduction momentum PCG (k_cg_sr) by default: per iteration (µs) SR / two-barrier /
+    // two-barrier + lazy x: cfg1 9.9 / - / 11.7, cfg2 15.0 / 16.6 / 16.4, cfg4 34.5 / 33.3 /
+    // 34.1, cfg3 42.6 / 42.1 / 42.7, cfg5 2290 / 2466 / 2317.  PFB200_SR=0 selects the
+    // two-barrier kernel (lazy x for meshes beyond 4x L2).
+    h->sr_mom = true;
     const char* srv = getenv("PFB200_SR");
     if (srv) h->sr_mom = std::string(srv) == "1";
     h->sr_mom = h->sr_mom && !strip;  // strips: split-phase kernels
