@@ -45,6 +45,7 @@ struct pf_handle {
   double *Ru = nullptr, *ru = nullptr, *xu = nullptr, *qu = nullptr, *p0u = nullptr,
          *p1u = nullptr, *dinvu = nullptr, *diagu = nullptr;
   double *r1u = nullptr, *w1u = nullptr, *pcu = nullptr;  // single-reduction PCG (k_cg_sr)
+  double *r1d = nullptr, *w1d = nullptr, *pcd = nullptr;
   uint8_t* flags = nullptr;
   uint8_t* umask = nullptr;
   // phase-field work
@@ -80,6 +81,8 @@ struct pf_handle {
   double* stage = nullptr;  // pinned host staging buffer for state transfers
   size_t stage_cap = 0;     // doubles
   bool sr_mom = false;  // momentum solves by the single-reduction PCG (k_cg_sr<true>)
+  bool sr_evo = false;  // phase-field solves by k_cg_sr<false>
+  size_t sr_smem_evo = 0;
   size_t sr_smem = 0;   // its dynamic shared memory (cp.async staging slots)
   pfb::MarchGeom geom_mom{}, geom_evo{}, geom_apply{};
   // split-phase PCG (pf_cg.cuh: k_cg_a / k_cg_b chained in CUDA graphs)
@@ -219,7 +222,7 @@ extern "C" void pf_destroy(pf_handle* h) {
                   h->d_nrow, h->d_erow,
                   h->u, h->d, h->dprev, h->trp, h->dev2, h->psi, h->psimax,
                   h->Ru, h->ru, h->xu, h->qu, h->p0u, h->p1u, h->dinvu, h->diagu, h->flags,
-                  h->r1u, h->w1u, h->pcu,
+                  h->r1u, h->w1u, h->pcu, h->r1d, h->w1d, h->pcd,
                   h->umask, h->Rd, h->rd, h->xd, h->qd, h->p0d, h->p1d, h->dinvd, h->diagd,
                   h->b, h->pmask, h->partials, h->scratch, h->d_idx, h->flushbuf};
   for (void* p : ptrs)
@@ -436,6 +439,13 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
     const char* srv = getenv("PFB200_SR");
     if (srv) h->sr_mom = std::string(srv) == "1";
     h->sr_mom = h->sr_mom && !strip;  // strips: split-phase kernels
+    const char* sre = getenv("PFB200_SR_EVO");
+    h->sr_evo = !(sre && std::string(sre) == "0") && !strip;
+    if (h->sr_evo) {
+      CREATE_ALLOC(h->r1d, nn);
+      CREATE_ALLOC(h->w1d, nn);
+      CREATE_ALLOC(h->pcd, nn);
+    }
     if (h->sr_mom) {
       CREATE_ALLOC(h->r1u, 2 * nn);
       CREATE_ALLOC(h->w1u, 2 * nn);
@@ -494,6 +504,15 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
     CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_cg<false, true>,
                                                               pfb::CG_NT, 0));
     occ_evo = std::min(o1, o2);
+    if (h->sr_evo) {
+      h->sr_smem_evo = sizeof(pfb::SrStage<false>) * pfb::SR_SLOTS * (pfb::CG_NT / 32);
+      CREATE_CUDA(cudaFuncSetAttribute(pfb::k_cg_sr<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)h->sr_smem_evo));
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_cg_sr<false>,
+                                                                pfb::CG_NT, h->sr_smem_evo));
+      occ_evo = std::min(occ_evo, o2);
+    }
   }
   h->sm_count = dev_sms;
   h->l2_bytes = l2;
@@ -861,8 +880,13 @@ static pf_status axpy(pf_handle* h, double* y, const double* x, long long n) {
   return launched(h);
 }
 
+static size_t cg_smem(const pf_handle* h, bool mom) {  // dynamic smem of the chosen PCG kernel
+  return mom ? (h->sr_mom ? h->sr_smem : 0) : (h->sr_evo ? h->sr_smem_evo : 0);
+}
+
 static const void* cg_kernel(pf_handle* h, bool mom) {
   if (mom && h->sr_mom) return (const void*)pfb::k_cg_sr<true>;
+  if (!mom && h->sr_evo) return (const void*)pfb::k_cg_sr<false>;
   if (mom) return h->xupd_mom ? (const void*)pfb::k_cg<true, true> : (const void*)pfb::k_cg<true, false>;
   return h->xupd_evo ? (const void*)pfb::k_cg<false, true> : (const void*)pfb::k_cg<false, false>;
 }
@@ -882,9 +906,9 @@ static pfb::CgArgs cg_args(pf_handle* h, bool mom) {
   a.q = mom ? h->qu : h->qd;
   a.p0 = mom ? h->p0u : h->p0d;
   a.p1 = mom ? h->p1u : h->p1d;
-  a.r1 = mom ? h->r1u : nullptr;
-  a.w1 = mom ? h->w1u : nullptr;
-  a.pc = mom ? h->pcu : nullptr;
+  a.r1 = mom ? h->r1u : h->r1d;
+  a.w1 = mom ? h->w1u : h->w1d;
+  a.pc = mom ? h->pcu : h->pcd;
   a.dinv = mom ? h->dinvu : h->dinvd;
   a.partials = h->partials;
   a.result = h->d_cgres;
@@ -931,7 +955,7 @@ static pf_status run_cg_persistent(pf_handle* h, bool mom, double* target, bool 
   const int grid = mom ? h->cg_grid : h->cg_grid_evo;
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
   PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(pfb::CG_NT), args,
-                                      (mom && h->sr_mom) ? h->sr_smem : 0, h->stream));
+                                      cg_smem(h, mom), h->stream));
   PF_TRY(launched(h));
   PF_CUDA(cudaEventRecord(h->ev1, h->stream));
   PF_CUDA(cudaStreamSynchronize(h->stream));
@@ -1523,7 +1547,7 @@ extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, doub
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
   PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(mom ? h->cg_grid : h->cg_grid_evo),
                                       dim3(pfb::CG_NT), args,
-                                      (mom && h->sr_mom) ? h->sr_smem : 0, h->stream));
+                                      cg_smem(h, mom), h->stream));
   PF_TRY(launched(h));
   PF_CUDA(cudaEventRecord(h->ev1, h->stream));
   PF_CUDA(cudaStreamSynchronize(h->stream));

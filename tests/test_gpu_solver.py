@@ -186,14 +186,14 @@ def test_determinism_and_dropin_equivalence(cuda_ok):
     assert np.array_equal(got["u"], outs[0][0]) and np.array_equal(got["d"], outs[0][1])
 
 
-@pytest.mark.parametrize("variant", ["PFB200_XUPD", "PFB200_SR"])
+@pytest.mark.parametrize("variant", ["PFB200_XUPD", "PFB200_SR", "PFB200_SR_EVO"])
 @pytest.mark.parametrize("case_name", ["tension16", "lpanel25"])
 def test_pcg_variants_match(cuda_ok, monkeypatch, case_name, variant):
-    """The momentum PCG variants the host picks by mesh size give the reference CG's answers:
-    lazy x (x += alpha p folded into the next march; automatic for meshes far beyond L2) has
-    the same iterates; single-reduction (Chronopoulos-Gear; automatic for L2-resident meshes)
-    has the same iterates in exact arithmetic.  Each is forced on and off for a small mesh:
-    staggered counts equal, PCG counts within 1%, fields within 1e-9."""
+    """The PCG variants give the reference CG's answers: lazy x (x += alpha p folded into the
+    next march of the two-barrier kernel) has the same iterates; the single-reduction kernel
+    (Chronopoulos-Gear; the default for momentum and phase field) has the same iterates in exact
+    arithmetic.  Each is forced on and off for a small mesh: staggered counts equal, PCG counts
+    within 1%, fields within 1e-9."""
     from paper_2209_07969_b200.session import DeviceSession
 
     case = C.get_case(case_name)
