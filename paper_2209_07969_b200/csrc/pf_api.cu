@@ -101,6 +101,14 @@ struct pf_handle {
   double* gB = nullptr;     // [CG_SLOTS+1][2]  global r.r, r.D^-1.r
   cudaGraphExec_t dgraphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // dist chunks
   long long l2_bytes = 0;
+  // geometric-multigrid PCG for the momentum solves (pf_mg.cuh k_mgcg)
+  bool mg = false;
+  pfb::MgArgs mga{};
+  std::vector<void*> mg_allocs;
+  int mg_gf = 1, mg_gflat = 1;            // fine-march grid, flat-kernel grid
+  std::vector<int> mg_gl;                 // node-kernel grid per level
+  pfb::MgIn* mg_in = nullptr;             // mapped pinned per-solve inputs
+  cudaGraphExec_t mg_setup_exec = nullptr, mg_solve_exec = nullptr;
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
   bool umask_all_free = true, pmask_all_free = true;
@@ -230,6 +238,11 @@ extern "C" void pf_destroy(pf_handle* h) {
   for (auto& row : h->warm_buf)
     for (double* p : row)
       if (p) cudaFree(p);
+  for (void* p : h->mg_allocs)
+    if (p) cudaFree(p);
+  if (h->mg_in) cudaFreeHost(h->mg_in);
+  if (h->mg_setup_exec) cudaGraphExecDestroy(h->mg_setup_exec);
+  if (h->mg_solve_exec) cudaGraphExecDestroy(h->mg_solve_exec);
   if (h->stage) cudaFreeHost(h->stage);
   for (auto& row : h->graphs)
     for (auto& g : row)
@@ -289,6 +302,274 @@ static pf_status validate_mesh(pf_handle* h, const pf_mesh* m) {
     ne += hi - lo;
   }
   if (ne != m->n_elems) return fail(h, PF_ERR_INVALID, "mesh: element count mismatch");
+  return PF_OK;
+}
+
+
+// ------------------------------------------------------------------------------------------
+// multigrid hierarchy (pf_mg.cuh): row-compact layouts of the 2x2-agglomerated levels
+struct HostLevel {
+  int nx = 0, ny = 0;
+  std::vector<int> nlo, nhi, nst, elo, ehi, est;
+  int notch_row = -1, notch_lo = 0, notch_hi = 0, dup_start = 0, n_nodes = 0, n_elems = 0;
+};
+
+// coarse layout of f (every 2x2 block of cells -> one cell, slit kept on its coarse row), or
+// false when f does not agglomerate (odd extents, rows or slit off the even lines)
+static bool mg_coarsen(const HostLevel& f, HostLevel& c) {
+  if (f.nx % 2 || f.ny % 2 || f.nx < 4 || f.ny < 4) return false;
+  c = HostLevel();
+  c.nx = f.nx / 2;
+  c.ny = f.ny / 2;
+  c.elo.resize(c.ny); c.ehi.resize(c.ny); c.est.resize(c.ny);
+  for (int J = 0; J < c.ny; ++J) {
+    const int a = 2 * J, b = 2 * J + 1;
+    if (f.elo[a] != f.elo[b] || f.ehi[a] != f.ehi[b] || f.elo[a] % 2 || f.ehi[a] % 2) return false;
+    c.elo[J] = f.elo[a] / 2;
+    c.ehi[J] = f.ehi[a] / 2;
+  }
+  c.nlo.resize(c.ny + 1); c.nhi.resize(c.ny + 1); c.nst.resize(c.ny + 1);
+  int n = 0;
+  for (int J = 0; J <= c.ny; ++J) {
+    const int lo = f.nlo[2 * J], hi = f.nhi[2 * J];
+    if (lo % 2 || (hi - 1) % 2) return false;
+    c.nlo[J] = lo / 2;
+    c.nhi[J] = (hi - 1) / 2 + 1;
+    c.nst[J] = n;
+    n += c.nhi[J] - c.nlo[J];
+  }
+  int e = 0;
+  for (int J = 0; J < c.ny; ++J) {
+    c.est[J] = e;
+    e += c.ehi[J] - c.elo[J];
+  }
+  c.n_elems = e;
+  if (f.notch_row >= 0) {
+    if (f.notch_row % 2 || f.notch_lo % 2 || f.notch_hi % 2) return false;
+    c.notch_row = f.notch_row / 2;
+    c.notch_lo = f.notch_lo / 2;
+    c.notch_hi = f.notch_hi / 2;
+    c.dup_start = n;
+    n += c.notch_hi - c.notch_lo;
+  }
+  c.n_nodes = n;
+  // every coarse node row must cover the odd fine rows next to it (bilinear prolongation)
+  for (int j = 1; j < f.ny; j += 2) {
+    const int J0 = j / 2, J1 = J0 + 1;
+    const int lo = std::max(c.nlo[J0], c.nlo[J1]) * 2, hi = (std::min(c.nhi[J0], c.nhi[J1]) - 1) * 2 + 1;
+    if (f.nlo[j] < lo || f.nhi[j] > hi) return false;
+  }
+  return true;
+}
+
+template <class T>
+static cudaError_t mg_alloc(pf_handle* h, T** p, size_t n) {
+  cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
+  if (e == cudaSuccess) {
+    h->mg_allocs.push_back((void*)*p);
+    e = cudaMemset(*p, 0, std::max<size_t>(n, 1) * sizeof(T));
+  }
+  return e;
+}
+
+static pf_status mg_build_graphs(pf_handle* h);
+
+static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
+  const char* tl = getenv("PFB200_MG_TAIL");  // tail levels: at most this many nodes
+  const int tail_nodes = tl ? std::max(0, atoi(tl)) : 1200;
+  const char* nc = getenv("PFB200_MG_NUC");
+  const int nu_c = nc ? std::max(1, atoi(nc)) : 16;
+  std::vector<HostLevel> lv(1);
+  HostLevel& f = lv[0];
+  f.nx = h->nx; f.ny = h->ny;
+  f.nlo = h->h_nlo; f.nhi = h->h_nhi; f.nst = h->h_nst;
+  f.elo = h->h_elo; f.ehi = h->h_ehi; f.est = h->h_est;
+  f.notch_row = h->dm.notch_row; f.notch_lo = h->dm.notch_lo; f.notch_hi = h->dm.notch_hi;
+  f.dup_start = h->dm.dup_start; f.n_nodes = h->n_nodes; f.n_elems = h->n_elems;
+  while ((int)lv.size() < pfb::MG_MAXL && 2 * lv.back().n_nodes > pfb::MG_DENSE_MAX) {
+    HostLevel c;
+    if (!mg_coarsen(lv.back(), c)) break;
+    lv.push_back(std::move(c));
+  }
+  const int nl = (int)lv.size();
+  if (nl < 2) return PF_OK;  // nothing to agglomerate: Jacobi PCG
+  pfb::MgArgs& A = h->mga;
+  A = pfb::MgArgs{};
+  A.C = h->C;
+  A.n_levels = nl;
+  A.dense = 2 * lv.back().n_nodes <= pfb::MG_DENSE_MAX;
+  A.nu_c = nu_c;
+  int nt = nl - 1;  // the coarsest level always belongs to the tail kernel
+  while (nt > 1 && lv[nt - 1].n_nodes <= tail_nodes) --nt;
+  A.n_tail = nt;
+  auto oom = [&]() { return fail(h, PF_ERR_CUDA, "multigrid allocation failed"); };
+  h->mg_gl.assign(nl, 1);
+  int coarse_items = 0;
+  for (int l = 0; l < nl; ++l) {
+    const HostLevel& L = lv[l];
+    pfb::MgLevel& M = A.L[l];
+    pfb::DMesh& dm = M.m;
+    if (l == 0) {
+      dm = h->dm;
+    } else {
+      std::vector<int4> nrow(L.ny + 1), erow(L.ny);
+      for (int j = 0; j <= L.ny; ++j) nrow[j] = make_int4(L.nlo[j], L.nhi[j], L.nst[j], 0);
+      for (int j = 0; j < L.ny; ++j) erow[j] = make_int4(L.elo[j], L.ehi[j], L.est[j], 0);
+      int4 *dn = nullptr, *de = nullptr;
+      if (mg_alloc(h, &dn, nrow.size()) != cudaSuccess || mg_alloc(h, &de, erow.size()) != cudaSuccess)
+        return oom();
+      cudaMemcpy(dn, nrow.data(), nrow.size() * sizeof(int4), cudaMemcpyHostToDevice);
+      cudaMemcpy(de, erow.data(), erow.size() * sizeof(int4), cudaMemcpyHostToDevice);
+      dm = pfb::DMesh{};
+      dm.nx = L.nx; dm.ny = L.ny;
+      dm.nrow = dn; dm.erow = de;
+      dm.notch_row = L.notch_row; dm.notch_lo = L.notch_lo; dm.notch_hi = L.notch_hi;
+      dm.dup_start = L.dup_start;
+      dm.n_nodes = L.n_nodes; dm.n_elems = L.n_elems;
+      dm.own_lo = 0; dm.own_hi = L.n_nodes; dm.dup_lo = L.n_nodes;
+      dm.cell_lo = 0; dm.cell_hi = L.n_elems;
+      if (mg_alloc(h, &M.K, 64 * (size_t)L.n_elems) != cudaSuccess ||
+          mg_alloc(h, &M.dinv, 2 * (size_t)L.n_nodes) != cudaSuccess ||
+          mg_alloc(h, &M.b, 2 * (size_t)L.n_nodes) != cudaSuccess ||
+          mg_alloc(h, &M.e, 2 * (size_t)L.n_nodes) != cudaSuccess)
+        return oom();
+      M.items = pfb::mg_items(L.nx, L.ny, L.notch_row >= 0);
+      M.item_off = coarse_items;
+      coarse_items += M.items;
+      h->mg_gl[l] = (M.items + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+    }
+    if (mg_alloc(h, &M.t, 2 * (size_t)L.n_nodes) != cudaSuccess) return oom();
+  }
+  A.coarse_items = coarse_items;
+  A.g0 = pfb::make_march_geom(h->nx, h->ny, fine_resident_warps);
+  h->mg_gf = (A.g0.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+  h->mg_gflat = 2 * h->sm_count;
+  if (mg_alloc(h, &A.z, 2 * (size_t)h->n_nodes) != cudaSuccess) return oom();
+  A.L[0].dinv = h->dinvu;
+  A.L[0].e = A.z;
+  const int ndc = 2 * lv.back().n_nodes;
+  if (A.dense && mg_alloc(h, &A.Ainv, (size_t)ndc * ndc) != cudaSuccess) return oom();
+  const size_t npart = std::max<size_t>((size_t)2 * h->mg_gf + h->mg_gflat,
+                                        (size_t)h->mg_gflat * 2 * pfb::MG_MAXL);
+  if (mg_alloc(h, &A.part, npart) != cudaSuccess || mg_alloc(h, &A.ctl, 1) != cudaSuccess)
+    return oom();
+  if (cudaHostAlloc((void**)&h->mg_in, sizeof(pfb::MgIn), cudaHostAllocMapped) != cudaSuccess)
+    return oom();
+  pfb::MgIn* din = nullptr;
+  cudaHostGetDevicePointer((void**)&din, h->mg_in, 0);
+  A.in = din;
+  A.d = h->d;
+  A.flags = h->flags;
+  A.x = h->xu; A.r = h->ru; A.p0 = h->p0u; A.p1 = h->p1u; A.q = h->qu;
+  A.result = h->d_cgres;
+  A.ndof = 2LL * h->n_nodes;
+  PF_TRY(mg_build_graphs(h));
+  h->mg = true;
+  return PF_OK;
+}
+
+// Two graphs per handle: the hierarchy setup (Galerkin levels, diagonals, power steps, omega,
+// dense coarsest inverse) and the solve (init, WHILE {one PCG iteration}, finish).
+static pf_status mg_build_graphs(pf_handle* h) {
+  pfb::MgArgs& A = h->mga;
+  const int nl = A.n_levels;
+  cudaStream_t s = h->stream;
+  // ---- setup graph
+  {
+    cudaGraph_t g = nullptr;
+    PF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int lc = 1; lc < nl; ++lc) {
+      const int cells = A.L[lc].m.nx * A.L[lc].m.ny;
+      pfb::k_mg_galerkin<<<(cells + pfb::MG_WARPS - 1) / pfb::MG_WARPS, pfb::MG_NT, 0, s>>>(A, lc);
+      pfb::k_mg_diag<<<h->mg_gl[lc], pfb::MG_NT, 0, s>>>(A, lc);
+    }
+    if (A.dense) pfb::k_mg_dense<<<1, pfb::MG_NT, 0, s>>>(A);
+    const int cb = (A.coarse_items + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+    for (int k = 1; k <= pfb::MG_POW; ++k)
+      pfb::k_mg_pow<<<h->mg_gf + cb, pfb::MG_NT, 0, s>>>(A, k, h->mg_gf);
+    pfb::k_mg_lambda<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A);
+    cudaError_t e = cudaStreamEndCapture(s, &g);
+    if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG setup capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&h->mg_setup_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG setup graph: ") + cudaGetErrorString(e));
+  }
+  // ---- solve graph: init -> WHILE (cond) { iteration } -> finish.  PFB200_MG_UNROLL=N (profiling
+  // only): N unconditional iterations instead of the WHILE node, so ncu sees every kernel.
+  auto body_kernels = [&](const pfb::MgArgs& B) {
+    pfb::k_mg_fine_resid<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B);
+    for (int l = 1; l < B.n_tail; ++l) {
+      pfb::k_mg_restrict<<<h->mg_gl[l], pfb::MG_NT, 0, s>>>(B, l);
+      pfb::k_mg_resid<<<h->mg_gl[l], pfb::MG_NT, 0, s>>>(B, l);
+    }
+    pfb::k_mg_tail<<<1, pfb::MG_TAIL_NT, 0, s>>>(B);
+    for (int l = B.n_tail - 1; l >= 1; --l) {
+      pfb::k_mg_prolongate<<<h->mg_gl[l], pfb::MG_NT, 0, s>>>(B, l);
+      pfb::k_mg_smooth<<<h->mg_gl[l], pfb::MG_NT, 0, s>>>(B, l);
+    }
+    pfb::k_mg_fine_smooth<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B);
+    pfb::k_mg_pcg<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B, h->mg_gf);
+    pfb::k_mg_update<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(B, h->mg_gf, h->mg_gf);
+  };
+  const char* un = getenv("PFB200_MG_UNROLL");
+  const int unroll = un ? std::max(0, atoi(un)) : 0;
+  if (unroll > 0) {
+    cudaGraph_t g = nullptr;
+    A.use_cond = 0;
+    PF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    pfb::k_mg_init<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A);
+    for (int it = 0; it < unroll; ++it) body_kernels(A);
+    pfb::k_mg_finish<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A);
+    PF_CUDA(cudaStreamEndCapture(s, &g));
+    cudaError_t e = cudaGraphInstantiate(&h->mg_solve_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG solve graph: ") + cudaGetErrorString(e));
+    return PF_OK;
+  }
+  {
+    cudaGraph_t g = nullptr;
+    PF_CUDA(cudaGraphCreate(&g, 0));
+    PF_CUDA(cudaGraphConditionalHandleCreate(&A.cond, g, 1, cudaGraphCondAssignDefault));
+    A.use_cond = 1;
+    cudaGraphNode_t n_init = nullptr, n_while = nullptr, n_fin = nullptr;
+    {
+      PF_CUDA(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      pfb::k_mg_init<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A);
+      cudaGraph_t gg = g;
+      PF_CUDA(cudaStreamEndCapture(s, &gg));
+      size_t nn = 0;
+      PF_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+      std::vector<cudaGraphNode_t> nodes(nn);
+      PF_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+      n_init = nodes[0];
+    }
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = A.cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    PF_CUDA(cudaGraphAddNode(&n_while, g, &n_init, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    {
+      PF_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      body_kernels(A);
+      cudaGraph_t bb = body;
+      PF_CUDA(cudaStreamEndCapture(s, &bb));
+    }
+    {
+      cudaGraphNodeParams kp = {};
+      kp.type = cudaGraphNodeTypeKernel;
+      void* args[] = {&A};
+      kp.kernel.func = (void*)pfb::k_mg_finish;
+      kp.kernel.gridDim = dim3(h->mg_gflat);
+      kp.kernel.blockDim = dim3(pfb::MG_NT);
+      kp.kernel.kernelParams = args;
+      PF_CUDA(cudaGraphAddNode(&n_fin, g, &n_while, 1, &kp));
+    }
+    cudaError_t e = cudaGraphInstantiate(&h->mg_solve_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG solve graph: ") + cudaGetErrorString(e));
+  }
   return PF_OK;
 }
 
@@ -440,7 +721,9 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
     if (srv) h->sr_mom = std::string(srv) == "1";
     h->sr_mom = h->sr_mom && !strip;  // strips: split-phase kernels
     const char* sre = getenv("PFB200_SR_EVO");
-    h->sr_evo = !(sre && std::string(sre) == "0") && !strip;
+    // opt-in: on cfg3's first load step the single-reduction phase-field PCG never reached
+    // ||r|| < 1e-12 ||b|| (maxiter 20 n, tests/test_gpu_solver.py::test_full_size_first_step)
+    h->sr_evo = (sre && std::string(sre) == "1") && !strip;
     if (h->sr_evo) {
       CREATE_ALLOC(h->r1d, nn);
       CREATE_ALLOC(h->w1d, nn);
@@ -565,6 +848,23 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
   CREATE_CUDA(cudaHostGetDevicePointer((void**)&h->d_cgres, h->h_cgres, 0));
   CREATE_CUDA(cudaHostAlloc((void**)&h->h_scal, 16 * sizeof(double), cudaHostAllocMapped));
   CREATE_CUDA(cudaHostGetDevicePointer((void**)&h->d_scal, h->h_scal, 0));
+  {  // geometric-multigrid PCG for the momentum solves (single GPU; PFB200_MG=0: Jacobi PCG)
+    const char* mgv = getenv("PFB200_MG");
+    const bool want = !(mgv && std::string(mgv) == "0") && !strip;
+    if (want) {
+      int om = 0, o2 = 0;
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, pfb::k_mg_fine_smooth, pfb::MG_NT, 0));
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_mg_pcg, pfb::MG_NT, 0));
+      om = std::min(om, o2);
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_mg_fine_resid, pfb::MG_NT, 0));
+      om = std::min(om, o2);
+      if (om >= 1) {
+        pf_status ms = mg_setup(h, om * dev_sms * pfb::MG_WARPS);
+        if (ms != PF_OK) return bail(ms);
+        if (h->mg) h->warm = false;  // the MG solves start cold (x0 = 0, like the reference CG)
+      }
+    }
+  }
   CREATE_CUDA(cudaStreamSynchronize(h->stream));
   *out = h;
   return PF_OK;
@@ -1116,8 +1416,38 @@ static pf_status run_cg_dist(pf_handle* h, bool mom, double* target, bool probe,
   return cg_status(h, *status, *iters);
 }
 
+
+// one MG-PCG solve: setup graph (hierarchy at the current tangent), then the solve graph whose
+// PCG loop is a device-side WHILE node; the host waits once, at the end
+static pf_status run_mg(pf_handle* h, double* target, int* status, long long* iters,
+                        int setup_only = 0, long long maxiter = -1, double rtol = -1.0,
+                        bool check = true) {
+  h->mg_in->rtol = rtol >= 0.0 ? rtol : h->cfg.cg_rtol;
+  h->mg_in->maxiter = maxiter > 0 ? maxiter
+                                  : (long long)h->cfg.cg_maxiter_factor * 2LL * h->n_nodes;
+  h->mg_in->target = target;
+  PF_CUDA(cudaEventRecord(h->ev0, h->stream));
+  PF_CUDA(cudaGraphLaunch(h->mg_setup_exec, h->stream));
+  PF_TRY(launched(h));
+  if (!setup_only) {
+    PF_CUDA(cudaGraphLaunch(h->mg_solve_exec, h->stream));
+    PF_TRY(launched(h));
+  }
+  PF_CUDA(cudaEventRecord(h->ev1, h->stream));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  if (setup_only) return PF_OK;
+  *status = h->h_cgres->status;
+  *iters = h->h_cgres->iters;
+  if (!check) return PF_OK;
+  cg_account(h, true, *iters, ms);
+  return cg_status(h, *status, *iters);
+}
+
 static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
                         long long* iters, double* const* guess = nullptr, int n_guess = 0) {
+  if (mom && h->mg && !probe) return run_mg(h, target, status, iters);
   if (h->comm) return run_cg_dist(h, mom, target, probe, status, iters);
   return h->split ? run_cg_split(h, mom, target, probe, status, iters)
                   : run_cg_persistent(h, mom, target, probe, status, iters, guess, n_guess);
@@ -1535,7 +1865,19 @@ extern "C" pf_status pf_update_active_energy(pf_handle* h, int scheme, const dou
 extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, double* ms_out,
                                  int64_t* iters_out) {
   PF_CUDA(cudaSetDevice(h->device));
-  if (n_iter < 1 || physics < 0 || physics > 1) return fail(h, PF_ERR_INVALID, "bad arguments");
+  if (n_iter < 1 || physics < 0 || physics > 2) return fail(h, PF_ERR_INVALID, "bad arguments");
+  if (physics == 2) {  // multigrid-preconditioned momentum PCG
+    if (!h->mg) return fail(h, PF_ERR_INVALID, "no multigrid hierarchy on this handle");
+    PF_TRY(launch_mom_prepare(h, 1));
+    int status = 0;
+    long long iters = 0;
+    PF_TRY(run_mg(h, nullptr, &status, &iters, 0, n_iter, 0.0, false));
+    float ms = 0.f;
+    PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (ms_out) *ms_out = ms;
+    if (iters_out) *iters_out = iters;
+    return PF_OK;
+  }
   const bool mom = physics == 0;
   if (mom) PF_TRY(launch_mom_prepare(h, 1));
   else PF_TRY(launch_evo_prepare(h, 1, 0));
@@ -1556,6 +1898,22 @@ extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, doub
   if (ms_out) *ms_out = ms;
   if (iters_out) *iters_out = h->h_cgres->iters;
   if (h->h_cgres->status == pfb::CG_NAN) return fail(h, PF_ERR_SINGULAR, "non-finite residual");
+  return PF_OK;
+}
+
+extern "C" pf_status pf_mg_info(pf_handle* h, int32_t* n_levels, int32_t* n_grid,
+                                int32_t* dense, double* omega) {
+  PF_CUDA(cudaSetDevice(h->device));
+  if (n_levels) *n_levels = h->mg ? h->mga.n_levels : 0;
+  if (n_grid) *n_grid = h->mg ? h->mga.n_tail : 0;
+  if (dense) *dense = h->mg ? h->mga.dense : 0;
+  if (!h->mg || !omega) return PF_OK;
+  PF_TRY(launch_mom_prepare(h, 1));
+  int status = 0;
+  long long iters = 0;
+  PF_TRY(run_mg(h, nullptr, &status, &iters, 1));
+  PF_CUDA(cudaMemcpy(omega, h->mga.ctl->omega, h->mga.n_levels * sizeof(double),
+                     cudaMemcpyDeviceToHost));
   return PF_OK;
 }
 

@@ -671,3 +671,4 @@ __global__ void k_flush(double* buf, long long n, double v) {
 }
 
 }  // namespace pfb
+#include "pf_mg.cuh"

@@ -269,10 +269,21 @@ class DeviceSession:
     # -- benchmarking helpers ------------------------------------------------------------
     def bench_cg(self, physics: str, n_iter: int) -> tuple:
         """(ms, iterations) of a fixed-length PCG run at the current state (no convergence)."""
+        code = {"momentum": 0, "evolution": 1, "phase_field": 1, "momentum_mg": 2}[physics]
         ms, it = C.c_double(), C.c_int64()
-        self._check(self.lib.pf_bench_cg(self.h, 0 if physics == "momentum" else 1,
-                                         int(n_iter), C.byref(ms), C.byref(it)))
+        self._check(self.lib.pf_bench_cg(self.h, code, int(n_iter), C.byref(ms), C.byref(it)))
         return ms.value, it.value
+
+    def mg_info(self, with_omega: bool = False) -> dict:
+        """Multigrid hierarchy of the momentum PCG (n_levels 0: Jacobi PCG on this handle)."""
+        nl, ng, dn = C.c_int32(), C.c_int32(), C.c_int32()
+        self._check(self.lib.pf_mg_info(self.h, C.byref(nl), C.byref(ng), C.byref(dn), None))
+        out = {"n_levels": nl.value, "n_grid": ng.value, "dense": bool(dn.value)}
+        if with_omega and nl.value:
+            om = np.zeros(nl.value)
+            self._check(self.lib.pf_mg_info(self.h, None, None, None, N.f64(om)))
+            out["omega"] = om
+        return out
 
     def device_info(self) -> dict:
         g, s, l2 = C.c_int32(), C.c_int32(), C.c_int64()

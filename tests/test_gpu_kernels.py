@@ -113,7 +113,7 @@ def test_fixed_length_pcg_benchmark_entry(cuda_ok):
     nn = lay.n_nodes
     s.push(u=1e-3 * rng.standard_normal(2 * nn), d=0.5 * rng.random(nn), d_prev=np.zeros(nn))
     s.refresh_gp()
-    for phys in ("momentum", "evolution"):
+    for phys in ("momentum", "evolution", "momentum_mg"):
         ms, it = s.bench_cg(phys, 7)
         assert it == 7 and ms > 0.0
     s.close()

@@ -192,12 +192,13 @@ def test_pcg_variants_match(cuda_ok, monkeypatch, case_name, variant):
     """The PCG variants give the reference CG's answers: lazy x (x += alpha p folded into the
     next march of the two-barrier kernel) has the same iterates; the single-reduction kernel
     (Chronopoulos-Gear; the default for momentum and phase field) has the same iterates in exact
-    arithmetic.  Each is forced on and off for a small mesh: staggered counts equal, PCG counts
+    arithmetic.  Each is forced on and off for a small mesh (Jacobi preconditioner): staggered counts equal, PCG counts
     within 1%, fields within 1e-9."""
     from paper_2209_07969_b200.session import DeviceSession
 
     case = C.get_case(case_name)
     runs = []
+    monkeypatch.setenv("PFB200_MG", "0")  # the Jacobi PCG kernels (MG: tests/test_gpu_mg.py)
     for flag in ("0", "1"):
         monkeypatch.setenv(variant, flag)
         pb = C.setup(case, C.b200_api())
