@@ -192,12 +192,13 @@ pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, double* ms_out,
                       int64_t* iters_out);
 pf_status pf_device_info(pf_handle* h, int32_t* cg_grid, int32_t* sm_count, int64_t* l2_bytes);
 /* Multigrid hierarchy of the momentum PCG (replaces the Jacobi preconditioner M = D^-1 of
- * linsolve.py:49 by a Galerkin V-cycle; same system, same stopping test): level count, levels
- * on the whole grid, dense coarsest solve; omega (optional, [n_levels]) builds the hierarchy at
- * the current state and returns the damped-Jacobi weights 4 / (3 lambda_max(D^-1 A_l)).
- * n_levels = 0: this handle solves with Jacobi PCG (PFB200_MG=0, strips, tiny meshes). */
+ * linsolve.py:49 by a Galerkin V-cycle; same system, same stopping test): level count, first
+ * level of the single-CTA tail kernel (n_levels: none), dense coarsest solve, hierarchy builds
+ * so far; omega (optional, [n_levels]) builds the hierarchy at the current state and returns
+ * the damped-Jacobi weights 4 / (3 lambda_max(D^-1 A_l)).  n_levels = 0: this handle solves
+ * with Jacobi PCG (PFB200_MG=0, strips, meshes that do not agglomerate). */
 pf_status pf_mg_info(pf_handle* h, int32_t* n_levels, int32_t* n_grid, int32_t* dense,
-                     double* omega);
+                     int64_t* setups, double* omega);
 pf_status pf_flush_l2(pf_handle* h);
 pf_status pf_synchronize(pf_handle* h);
 

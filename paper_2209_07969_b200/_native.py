@@ -112,7 +112,7 @@ _SIGNATURES = {
                                   C.c_int, C.POINTER(PfStrip), C.POINTER(C.c_void_p)]),
     "pf_bench_cg": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, _f64p, _i64p]),
     "pf_device_info": (C.c_int, [C.c_void_p, _i32p, _i32p, _i64p]),
-    "pf_mg_info": (C.c_int, [C.c_void_p, _i32p, _i32p, _i32p, _f64p]),
+    "pf_mg_info": (C.c_int, [C.c_void_p, _i32p, _i32p, _i32p, _i64p, _f64p]),
     "pf_flush_l2": (C.c_int, [C.c_void_p]),
     "pf_synchronize": (C.c_int, [C.c_void_p]),
 }

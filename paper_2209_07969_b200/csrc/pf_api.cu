@@ -106,9 +106,20 @@ struct pf_handle {
   pfb::MgArgs mga{};
   std::vector<void*> mg_allocs;
   int mg_gf = 1, mg_gflat = 1;            // fine-march grid, flat-kernel grid
-  std::vector<int> mg_gl;                 // node-kernel grid per level
+  std::vector<int> mg_gl;                 // warp-item grid per level (row-chunk kernels)
+  std::vector<int> mg_gn;                 // node-parallel grid per level (assembled form)
+  std::vector<int> mg_lpn;                // lanes per node of the level's node kernels (1 | 16)
   pfb::MgIn* mg_in = nullptr;             // mapped pinned per-solve inputs
   cudaGraphExec_t mg_setup_exec = nullptr, mg_solve_exec = nullptr;
+  // hierarchy reuse: the coarse levels (Galerkin matrices, omegas) are a preconditioner only;
+  // they are rebuilt when the iteration count drifts above the count right after the last
+  // rebuild, when the Dirichlet set changes, or after mg_max_age solves (PFB200_MG_REUSE=0:
+  // rebuild at every solve).  The fine level always uses the current tangent.
+  bool mg_built = false, mg_reuse = true;
+  long long mg_ref_iters = 0, mg_last_iters = 0;
+  int mg_age = 0, mg_max_age = 64;
+  long long mg_setups = 0;
+
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
   bool umask_all_free = true, pmask_all_free = true;
@@ -362,6 +373,105 @@ static bool mg_coarsen(const HostLevel& f, HostLevel& c) {
   return true;
 }
 
+
+// node id at grid (i, j); up: the slit row's duplicates as seen from the cells above
+static int hl_node(const HostLevel& L, int i, int j, bool up) {
+  if (j < 0 || j > L.ny || i < L.nlo[j] || i >= L.nhi[j]) return -1;
+  if (up && j == L.notch_row && i >= L.notch_lo && i < L.notch_hi) return L.dup_start + (i - L.notch_lo);
+  return L.nst[j] + (i - L.nlo[j]);
+}
+static bool hl_cell(const HostLevel& L, int ci, int cj) {
+  return cj >= 0 && cj < L.ny && ci >= L.elo[cj] && ci < L.ehi[cj];
+}
+static bool hl_dup_pos(const HostLevel& L, int i, int j) {
+  return L.notch_row >= 0 && j == L.notch_row && i >= L.notch_lo && i < L.notch_hi;
+}
+template <class F>
+static void hl_for_nodes(const HostLevel& L, F&& f) {  // f(id, i, j, dup)
+  for (int j = 0; j <= L.ny; ++j)
+    for (int i = L.nlo[j]; i < L.nhi[j]; ++i) f(L.nst[j] + (i - L.nlo[j]), i, j, false);
+  if (L.notch_row >= 0)
+    for (int i = L.notch_lo; i < L.notch_hi; ++i) f(L.dup_start + (i - L.notch_lo), i, L.notch_row, true);
+}
+
+// Stencil neighbours of every node, slot-major ([MG_NS][n]; pf_mg.cuh): slots 0-2 row j-1,
+// 3-5 row j, 6-8 row j+1 (columns i-1, i, i+1), each looked up the way the cells coupling the
+// two nodes see them (bottom corners from above the slit, top corners from below); slot 9 =
+// the second face of a slit-tip neighbour (the only node coupled to both faces of one grid
+// position).  -1 = no coupling.
+static std::vector<int> hl_stencil_ids(const HostLevel& L) {
+  const size_t n = L.n_nodes;
+  std::vector<int> ids(n * pfb::MG_NS, -1);
+  hl_for_nodes(L, [&](int id, int i, int j, bool) {
+    auto o = [&](int s) -> int& { return ids[(size_t)s * n + id]; };
+    const bool below = hl_node(L, i, j, false) == id;
+    const bool above = hl_node(L, i, j, true) == id;
+    for (int a = -1; a <= 1; ++a) {
+      if (below) o(1 + a) = hl_node(L, i + a, j - 1, true);
+      if (above) o(7 + a) = hl_node(L, i + a, j + 1, false);
+      const int nb = below ? hl_node(L, i + a, j, false) : -1;
+      const int na = above ? hl_node(L, i + a, j, true) : -1;
+      if (nb >= 0 && na >= 0 && nb != na) {
+        o(4 + a) = nb;
+        o(9) = na;
+      } else {
+        o(4 + a) = nb >= 0 ? nb : na;
+      }
+    }
+  });
+  return ids;
+}
+
+// Restriction lists of coarse level c from fine level f ([12][n_c]): slot (b+1)*3 + (a+1) =
+// the fine node at (2I+a, 2J+b) that interpolates from this coarse node (the regular node, or
+// the slit duplicate on the far side), slots 9-11 = a second fine node at (2I+a, 2J) when both
+// faces interpolate from it (the coarse slit tip).  Weights follow from the slot.
+static std::vector<int> hl_restrict_ids(const HostLevel& f, const HostLevel& c) {
+  const size_t n = c.n_nodes;
+  std::vector<int> ids(n * 12, -1);
+  hl_for_nodes(c, [&](int id, int I, int J, bool up) {
+    const bool dpos = hl_dup_pos(c, I, J);
+    for (int b = -1; b <= 1; ++b)
+      for (int a = -1; a <= 1; ++a) {
+        const int i = 2 * I + a, j = 2 * J + b;
+        const int fr = hl_node(f, i, j, false);
+        if (fr < 0) continue;
+        const bool s_reg = f.notch_row >= 0 && j > f.notch_row;
+        const bool use_r = !dpos || s_reg == up;
+        const bool has_d = hl_dup_pos(f, i, j);
+        const bool use_d = has_d && (!dpos || up);
+        const int fd = has_d ? f.dup_start + (i - f.notch_lo) : -1;
+        const int s = (b + 1) * 3 + (a + 1);
+        if (use_r && use_d) {
+          ids[(size_t)s * n + id] = fr;
+          ids[(size_t)(9 + a + 1) * n + id] = fd;
+        } else if (use_r) {
+          ids[(size_t)s * n + id] = fr;
+        } else if (use_d) {
+          ids[(size_t)s * n + id] = fd;
+        }
+      }
+  });
+  return ids;
+}
+
+// Prolongation lists of fine level f from coarse level c ([4][n_f]): the coarse nodes
+// (I0,J0), (I1,J0), (I0,J1), (I1,J1) that node (i, j) interpolates from (distinct ones only;
+// weight 1 / their count), seen from the node's side of the slit.
+static std::vector<int> hl_prolong_ids(const HostLevel& f, const HostLevel& c) {
+  const size_t n = f.n_nodes;
+  std::vector<int> ids(n * 4, -1);
+  hl_for_nodes(f, [&](int id, int i, int j, bool dup) {
+    const bool up = dup || (f.notch_row >= 0 && j > f.notch_row);
+    const int I0 = i >> 1, J0 = j >> 1, I1 = I0 + (i & 1), J1 = J0 + (j & 1);
+    ids[0 * n + id] = hl_node(c, I0, J0, up);
+    if (I1 != I0) ids[1 * n + id] = hl_node(c, I1, J0, up);
+    if (J1 != J0) ids[2 * n + id] = hl_node(c, I0, J1, up);
+    if (I1 != I0 && J1 != J0) ids[3 * n + id] = hl_node(c, I1, J1, up);
+  });
+  return ids;
+}
+
 template <class T>
 static cudaError_t mg_alloc(pf_handle* h, T** p, size_t n) {
   cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
@@ -375,8 +485,9 @@ static cudaError_t mg_alloc(pf_handle* h, T** p, size_t n) {
 static pf_status mg_build_graphs(pf_handle* h);
 
 static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
+
   const char* tl = getenv("PFB200_MG_TAIL");  // tail levels: at most this many nodes
-  const int tail_nodes = tl ? std::max(0, atoi(tl)) : 1200;
+  const int tail_nodes = tl ? std::max(0, atoi(tl)) : 1 << 30;
   const char* nc = getenv("PFB200_MG_NUC");
   const int nu_c = nc ? std::max(1, atoi(nc)) : 16;
   std::vector<HostLevel> lv(1);
@@ -399,11 +510,45 @@ static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
   A.n_levels = nl;
   A.dense = 2 * lv.back().n_nodes <= pfb::MG_DENSE_MAX;
   A.nu_c = nu_c;
-  int nt = nl - 1;  // the coarsest level always belongs to the tail kernel
-  while (nt > 1 && lv[nt - 1].n_nodes <= tail_nodes) --nt;
-  A.n_tail = nt;
+  // tail: the coarsest levels whose row tables, cell matrices and vectors (plus the dense
+  // inverse) fit the single-CTA kernel's shared memory (PFB200_MG_TAIL_KB, default 200)
+  const char* tk = getenv("PFB200_MG_TAIL_KB");
+  const size_t budget = (size_t)(tk ? std::max(0, atoi(tk)) : 200) * 1024;
+  auto level_bytes = [&](const HostLevel& L) -> size_t {
+    return 16 * (size_t)(2 * L.ny + 1) + 8 * 64 * (size_t)L.n_elems + 8 * 2 * 4 * (size_t)L.n_nodes;
+  };
+  const size_t ainv_bytes = A.dense ? 8 * (size_t)(2 * lv.back().n_nodes) * (2 * lv.back().n_nodes) : 0;
+  int nt = nl;
+  size_t used = ainv_bytes;
+  while (nt > 1 && lv[nt - 1].n_nodes <= tail_nodes && used + level_bytes(lv[nt - 1]) <= budget) {
+    used += level_bytes(lv[nt - 1]);
+    --nt;
+  }
+  A.n_tail = nt;  // nt == nl: no tail kernel (the coarsest level is solved by grid kernels)
+  {
+    size_t off = 0;
+    auto take = [&](size_t bytes) { const size_t o = off; off += (bytes + 15) & ~size_t(15); return (int)o; };
+    for (int l = nt; l < nl; ++l) {
+      const HostLevel& L = lv[l];
+      pfb::MgTailSlot& t = A.ts[l];
+      t.nrow = take(16 * (size_t)(L.ny + 1));
+      t.erow = take(16 * (size_t)L.ny);
+      t.K = take(8 * 64 * (size_t)L.n_elems);
+      t.dinv = take(16 * (size_t)L.n_nodes);
+      t.b = take(16 * (size_t)L.n_nodes);
+      t.t = take(16 * (size_t)L.n_nodes);
+      t.e = take(16 * (size_t)L.n_nodes);
+    }
+    A.ts_ainv = take(ainv_bytes);
+    A.ts_bytes = (int)off;
+    if (nt < nl && cudaFuncSetAttribute(pfb::k_mg_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        A.ts_bytes) != cudaSuccess)
+      return fail(h, PF_ERR_CUDA, "k_mg_tail shared memory");
+  }
   auto oom = [&]() { return fail(h, PF_ERR_CUDA, "multigrid allocation failed"); };
   h->mg_gl.assign(nl, 1);
+  h->mg_gn.assign(nl, 1);
+  h->mg_lpn.assign(nl, 16);
   int coarse_items = 0;
   for (int l = 0; l < nl; ++l) {
     const HostLevel& L = lv[l];
@@ -434,9 +579,33 @@ static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
           mg_alloc(h, &M.e, 2 * (size_t)L.n_nodes) != cudaSuccess)
         return oom();
       M.items = pfb::mg_items(L.nx, L.ny, L.notch_row >= 0);
-      M.item_off = coarse_items;
-      coarse_items += M.items;
+      M.item_off = coarse_items;  // node offset in the concatenated coarse node space (even)
+      coarse_items += (L.n_nodes + 1) & ~1;
       h->mg_gl[l] = (M.items + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+      // small levels: a half-warp per node (all loads of a node in flight); large levels: a
+      // thread per node (latency hidden by occupancy).  Threshold: 16 lanes per node would
+      // exceed one wave of resident threads.
+      h->mg_lpn[l] = 16LL * L.n_nodes <= 2048LL * h->sm_count ? 16 : 1;
+      h->mg_gn[l] = std::max(1, std::min((int)((h->mg_lpn[l] * (long long)L.n_nodes + pfb::MG_NT - 1) / pfb::MG_NT),
+                                         16 * h->sm_count));
+      {  // assembled-form index tables (static per handle)
+        const std::vector<int> nb = hl_stencil_ids(L), rd = hl_restrict_ids(lv[l - 1], L);
+        int *dnb = nullptr, *drd = nullptr;
+        if (mg_alloc(h, &dnb, nb.size()) != cudaSuccess || mg_alloc(h, &drd, rd.size()) != cudaSuccess ||
+            mg_alloc(h, &M.S, (size_t)4 * pfb::MG_NS * L.n_nodes) != cudaSuccess)
+          return oom();
+        cudaMemcpy(dnb, nb.data(), nb.size() * sizeof(int), cudaMemcpyHostToDevice);
+        cudaMemcpy(drd, rd.data(), rd.size() * sizeof(int), cudaMemcpyHostToDevice);
+        M.nbr = dnb;
+        M.rid = drd;
+        if (l + 1 < nl) {
+          const std::vector<int> pd = hl_prolong_ids(L, lv[l + 1]);
+          int* dpd = nullptr;
+          if (mg_alloc(h, &dpd, pd.size()) != cudaSuccess) return oom();
+          cudaMemcpy(dpd, pd.data(), pd.size() * sizeof(int), cudaMemcpyHostToDevice);
+          M.pid = dpd;
+        }
+      }
     }
     if (mg_alloc(h, &M.t, 2 * (size_t)L.n_nodes) != cudaSuccess) return oom();
   }
@@ -481,13 +650,13 @@ static pf_status mg_build_graphs(pf_handle* h) {
     for (int lc = 1; lc < nl; ++lc) {
       const int cells = A.L[lc].m.nx * A.L[lc].m.ny;
       pfb::k_mg_galerkin<<<(cells + pfb::MG_WARPS - 1) / pfb::MG_WARPS, pfb::MG_NT, 0, s>>>(A, lc);
-      pfb::k_mg_diag<<<h->mg_gl[lc], pfb::MG_NT, 0, s>>>(A, lc);
+      pfb::k_mg_stencil<<<h->mg_gl[lc], pfb::MG_NT, 0, s>>>(A, lc);
     }
     if (A.dense) pfb::k_mg_dense<<<1, pfb::MG_NT, 0, s>>>(A);
-    const int cb = (A.coarse_items + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+    const int cb = (16 * A.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
     for (int k = 1; k <= pfb::MG_POW; ++k)
       pfb::k_mg_pow<<<h->mg_gf + cb, pfb::MG_NT, 0, s>>>(A, k, h->mg_gf);
-    pfb::k_mg_lambda<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A);
+    pfb::k_mg_lambda<<<32, pfb::MG_NT, 0, s>>>(A);  // few CTAs: 2 MG_MAXL partials each
     cudaError_t e = cudaStreamEndCapture(s, &g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG setup capture: ") + cudaGetErrorString(e));
     e = cudaGraphInstantiate(&h->mg_setup_exec, g, 0);
@@ -496,16 +665,35 @@ static pf_status mg_build_graphs(pf_handle* h) {
   }
   // ---- solve graph: init -> WHILE (cond) { iteration } -> finish.  PFB200_MG_UNROLL=N (profiling
   // only): N unconditional iterations instead of the WHILE node, so ncu sees every kernel.
+#define MG_NODE_KERNEL(K, l, ...)                                                   \
+  do {                                                                              \
+    if (h->mg_lpn[l] == 16) pfb::K<16><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__); \
+    else pfb::K<1><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__);                     \
+  } while (0)
   auto body_kernels = [&](const pfb::MgArgs& B) {
+    const int c = nl - 1, top = std::min(B.n_tail, c);  // grid levels [1, top)
     pfb::k_mg_fine_resid<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B);
-    for (int l = 1; l < B.n_tail; ++l) {
-      pfb::k_mg_restrict<<<h->mg_gl[l], pfb::MG_NT, 0, s>>>(B, l);
-      pfb::k_mg_resid<<<h->mg_gl[l], pfb::MG_NT, 0, s>>>(B, l);
+    for (int l = 1; l < top; ++l) {
+      MG_NODE_KERNEL(k_mg_srestrict, l, B, l);
+      MG_NODE_KERNEL(k_mg_sresid, l, B, l);
     }
-    pfb::k_mg_tail<<<1, pfb::MG_TAIL_NT, 0, s>>>(B);
-    for (int l = B.n_tail - 1; l >= 1; --l) {
-      pfb::k_mg_prolongate<<<h->mg_gl[l], pfb::MG_NT, 0, s>>>(B, l);
-      pfb::k_mg_smooth<<<h->mg_gl[l], pfb::MG_NT, 0, s>>>(B, l);
+    if (B.n_tail < nl) {
+      pfb::k_mg_tail<<<1, pfb::MG_TAIL_NT, B.ts_bytes, s>>>(B);
+    } else {  // coarsest level on the grid
+      MG_NODE_KERNEL(k_mg_srestrict, c, B, c);
+      if (B.dense) {
+        pfb::k_mg_coarse_dense<<<1, pfb::MG_NT, 0, s>>>(B);
+      } else {
+        double* bufs[2] = {B.L[c].e, B.L[c].t};
+        int cur = (B.nu_c - 1) % 2 == 0 ? 0 : 1;
+        pfb::k_mg_jacobi0<<<h->mg_gn[c], pfb::MG_NT, 0, s>>>(B, c, bufs[cur]);
+        for (int k = 1; k < B.nu_c; ++k, cur ^= 1)
+          MG_NODE_KERNEL(k_mg_ssweep, c, B, c, bufs[cur], bufs[cur ^ 1]);
+      }
+    }
+    for (int l = top - 1; l >= 1; --l) {
+      MG_NODE_KERNEL(k_mg_sprolongate, l, B, l);
+      MG_NODE_KERNEL(k_mg_ssmooth, l, B, l);
     }
     pfb::k_mg_fine_smooth<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B);
     pfb::k_mg_pcg<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B, h->mg_gf);
@@ -862,6 +1050,8 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
         pf_status ms = mg_setup(h, om * dev_sms * pfb::MG_WARPS);
         if (ms != PF_OK) return bail(ms);
         if (h->mg) h->warm = false;  // the MG solves start cold (x0 = 0, like the reference CG)
+        const char* ru = getenv("PFB200_MG_REUSE");
+        h->mg_reuse = !(ru && std::string(ru) == "0");
       }
     }
   }
@@ -1072,6 +1262,7 @@ static pf_status set_umask(pf_handle* h, const std::vector<int64_t>& cons) {
   }
   PF_CUDA(cudaMemcpyAsync(h->umask, m.data(), n, cudaMemcpyHostToDevice, h->stream));
   PF_CUDA(cudaStreamSynchronize(h->stream));
+  h->mg_built = false;  // the Galerkin levels are masked at the Dirichlet dofs
   h->cons_key = cons;
   h->umask_all_free = cons.empty();
   return PF_OK;
@@ -1421,14 +1612,20 @@ static pf_status run_cg_dist(pf_handle* h, bool mom, double* target, bool probe,
 // PCG loop is a device-side WHILE node; the host waits once, at the end
 static pf_status run_mg(pf_handle* h, double* target, int* status, long long* iters,
                         int setup_only = 0, long long maxiter = -1, double rtol = -1.0,
-                        bool check = true) {
+                        bool check = true, bool force_setup = false) {
   h->mg_in->rtol = rtol >= 0.0 ? rtol : h->cfg.cg_rtol;
   h->mg_in->maxiter = maxiter > 0 ? maxiter
                                   : (long long)h->cfg.cg_maxiter_factor * 2LL * h->n_nodes;
   h->mg_in->target = target;
+  const bool rebuild = force_setup || setup_only || !h->mg_reuse || !h->mg_built ||
+                       h->mg_age >= h->mg_max_age ||
+                       h->mg_last_iters > (h->mg_ref_iters * 5) / 4 + 2;
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
-  PF_CUDA(cudaGraphLaunch(h->mg_setup_exec, h->stream));
-  PF_TRY(launched(h));
+  if (rebuild) {
+    PF_CUDA(cudaGraphLaunch(h->mg_setup_exec, h->stream));
+    PF_TRY(launched(h));
+    h->mg_setups += 1;
+  }
   if (!setup_only) {
     PF_CUDA(cudaGraphLaunch(h->mg_solve_exec, h->stream));
     PF_TRY(launched(h));
@@ -1437,9 +1634,19 @@ static pf_status run_mg(pf_handle* h, double* target, int* status, long long* it
   PF_CUDA(cudaStreamSynchronize(h->stream));
   float ms = 0.f;
   PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  if (rebuild) {
+    h->mg_built = true;
+    h->mg_age = 0;
+  }
   if (setup_only) return PF_OK;
   *status = h->h_cgres->status;
   *iters = h->h_cgres->iters;
+  if (rebuild) h->mg_ref_iters = *iters;
+  h->mg_last_iters = *iters;
+  if (h->trace)
+    fprintf(stderr, "[pfb200] mg solve: %lld iterations, %.3f ms%s\n", *iters, ms,
+            rebuild ? " (hierarchy rebuilt)" : "");
+  h->mg_age += 1;
   if (!check) return PF_OK;
   cg_account(h, true, *iters, ms);
   return cg_status(h, *status, *iters);
@@ -1871,7 +2078,7 @@ extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, doub
     PF_TRY(launch_mom_prepare(h, 1));
     int status = 0;
     long long iters = 0;
-    PF_TRY(run_mg(h, nullptr, &status, &iters, 0, n_iter, 0.0, false));
+    PF_TRY(run_mg(h, nullptr, &status, &iters, 0, n_iter, 0.0, false, true));
     float ms = 0.f;
     PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
     if (ms_out) *ms_out = ms;
@@ -1902,8 +2109,9 @@ extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, doub
 }
 
 extern "C" pf_status pf_mg_info(pf_handle* h, int32_t* n_levels, int32_t* n_grid,
-                                int32_t* dense, double* omega) {
+                                int32_t* dense, int64_t* setups, double* omega) {
   PF_CUDA(cudaSetDevice(h->device));
+  if (setups) *setups = h->mg_setups;
   if (n_levels) *n_levels = h->mg ? h->mga.n_levels : 0;
   if (n_grid) *n_grid = h->mg ? h->mga.n_tail : 0;
   if (dense) *dense = h->mg ? h->mga.dense : 0;

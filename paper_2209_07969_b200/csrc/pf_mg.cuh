@@ -36,6 +36,7 @@ constexpr int MG_WARPS = MG_NT / 32;
 constexpr int MG_POW = 8;          // power steps for lambda_max(D^-1 A_l)
 constexpr int MG_DENSE_MAX = 64;   // coarsest level by a dense inverse when 2 n_nodes <= this
 constexpr int MG_TAIL_NT = 512;    // threads of the single-CTA tail kernel
+constexpr int MG_NS = 10;          // assembled stencil slots per node (3x3 + slit-tip face)
 
 struct MgLevel {
   DMesh m;        // row tables (nrow/erow), notch, n_nodes/n_elems of this level
@@ -46,6 +47,13 @@ struct MgLevel {
   double* e;      // correction / power-iteration buffer
   int items;      // node items (rows x 32-column chunks) of mg_for_nodes
   int item_off;   // offset of this level in the concatenated coarse item space (power steps)
+  // assembled form (l >= 1), slot-major: nbr [MG_NS][n] neighbour ids, S [MG_NS*4][n] 2x2
+  // blocks (xx, xy, yx, yy); rid [12][n] restriction sources on level l-1; pid [4][n]
+  // prolongation sources on level l+1 (l <= n_levels-2)
+  const int* nbr;
+  double* S;
+  const int* rid;
+  const int* pid;
 };
 
 // device-side control block of one solve
@@ -61,6 +69,10 @@ struct MgCtl {
   long long k, maxiter;
   int status, done;
   unsigned int count;  // last-block counter (reset by the last block)
+};
+
+struct MgTailSlot {  // byte offsets of one tail level in k_mg_tail's shared memory
+  int nrow, erow, K, dinv, b, t, e;
 };
 
 struct MgArgs {
@@ -80,7 +92,9 @@ struct MgArgs {
   CgResult* result;
   long long ndof;
   cudaGraphConditionalHandle cond;
-  int use_cond;          // 0: launched outside the graph (per-kernel profiling)
+  int use_cond;          // 0: launched outside the graph (unrolled profiling graph)
+  MgTailSlot ts[MG_MAXL];
+  int ts_ainv, ts_bytes;  // dense inverse offset, total shared memory of k_mg_tail
 };
 
 struct MgWarp {
@@ -97,8 +111,8 @@ struct MgGal {
 __device__ __forceinline__ double2 d2add(double2 a, double2 b) {
   return make_double2(a.x + b.x, a.y + b.y);
 }
-__device__ __forceinline__ double2 d2ldcg(const double* p, int id) {
-  return __ldcg(reinterpret_cast<const double2*>(p) + id);
+__device__ __forceinline__ double2 d2ldcg(const double* p, int id) {  // input of this kernel
+  return __ldg(reinterpret_cast<const double2*>(p) + id);
 }
 __device__ __forceinline__ void d2st(double* p, int id, double2 v) {
   reinterpret_cast<double2*>(p)[id] = v;
@@ -269,28 +283,49 @@ struct FineResid : FineBase {  // x = omega D^-1 r (pre-smoothing from zero), t 
   }
 };
 
+// ---- memory policies of the coarse-level primitives: global (every input of a kernel was
+// written by an earlier kernel, so the read-only / L1 path is coherent) or shared (the tail
+// kernel's staged levels)
+struct GMem {
+  __device__ static double2 v2(const double* p, int i) {
+    return __ldg(reinterpret_cast<const double2*>(p) + i);
+  }
+  __device__ static int4 row(const int4* p, int j) { return __ldg(p + j); }
+};
+struct SMem {
+  __device__ static double2 v2(const double* p, int i) {
+    return reinterpret_cast<const double2*>(p)[i];
+  }
+  __device__ static int4 row(const int4* p, int j) { return p[j]; }
+};
+
+// node id in a row entry (lo, hi, start); up: the slit row's duplicates as seen from above
+__device__ __forceinline__ int mg_row_node(const DMesh& m, int4 rw, int i, int j, bool up) {
+  if (i < rw.x || i >= rw.y) return -1;
+  if (up && j == m.notch_row && i >= m.notch_lo && i < m.notch_hi)
+    return m.dup_start + (i - m.notch_lo);
+  return rw.z + (i - rw.x);
+}
+
 // prolongation (P e_{l+1}) at node (i, j) of level l; dup = upper-face slit node
+template <class MC>
 __device__ __forceinline__ double2 mg_prolong(const DMesh& mf, const DMesh& mc,
                                               const double* ec, int i, int j, bool dup) {
   const bool up = dup || (mf.notch_row >= 0 && j > mf.notch_row);
-  const int I0 = i >> 1, J0 = j >> 1;
-  const bool ox = i & 1, oy = j & 1;
-  double2 s = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int bj = 0; bj < 2; ++bj) {
-    if (bj == 1 && !oy) break;
-#pragma unroll
-    for (int bi = 0; bi < 2; ++bi) {
-      if (bi == 1 && !ox) break;
-      const int c = mg_node(mc, I0 + bi, J0 + bj, up);
-      if (c < 0) continue;
-      const double w = (ox ? 0.5 : 1.0) * (oy ? 0.5 : 1.0);
-      const double2 v = d2ldcg(ec, c);
-      s.x += w * v.x;
-      s.y += w * v.y;
-    }
-  }
-  return s;
+  const int I0 = i >> 1, J0 = j >> 1, I1 = I0 + (i & 1), J1 = J0 + (j & 1);
+  const double w = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
+  const int4 r0 = MC::row(mc.nrow, J0), r1 = MC::row(mc.nrow, min(J1, mc.ny));
+  const int c00 = mg_row_node(mc, r0, I0, J0, up), c10 = mg_row_node(mc, r0, I1, J0, up);
+  const int c01 = mg_row_node(mc, r1, I0, J1, up), c11 = mg_row_node(mc, r1, I1, J1, up);
+  const double2 v00 = MC::v2(ec, max(c00, 0)), v10 = MC::v2(ec, max(c10, 0));
+  const double2 v01 = MC::v2(ec, max(c01, 0)), v11 = MC::v2(ec, max(c11, 0));
+  // distinct corners only (I1 == I0 / J1 == J0 on even positions)
+  const double a00 = c00 >= 0 ? w : 0.0;
+  const double a10 = (c10 >= 0 && I1 != I0) ? w : 0.0;
+  const double a01 = (c01 >= 0 && J1 != J0) ? w : 0.0;
+  const double a11 = (c11 >= 0 && I1 != I0 && J1 != J0) ? w : 0.0;
+  return make_double2(a00 * v00.x + a10 * v10.x + a01 * v01.x + a11 * v11.x,
+                      a00 * v00.y + a10 * v10.y + a01 * v01.y + a11 * v11.y);
 }
 
 struct FineSmooth : FineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 (r - A y); r.z
@@ -306,7 +341,7 @@ struct FineSmooth : FineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 
     if (id < 0) return make_double2(0.0, 0.0);
     aux = __ldg(d + id);
     const double2 dv = di(id), bv = d2ldcg(r, id);
-    const double2 pe = mg_prolong(*mf, *mc, ec, i, j, dup);
+    const double2 pe = mg_prolong<GMem>(*mf, *mc, ec, i, j, dup);
     return mask2(make_double2(om * dv.x * bv.x + pe.x, om * dv.y * bv.y + pe.y), dv);
   }
   __device__ void out(int id, double2 Av, double2 y) const {
@@ -367,7 +402,7 @@ struct FinePcg : FineBase {  // p = z + beta p_old (owner stores), q = A p (mask
 // ---- coarse levels: node-parallel phases ----------------------------------------------------
 // Visit every node of a level: items are (node row or the slit-duplicate row, 32-column chunk);
 // f(id, i, j, dup) per existing node.  worker/nw count warps.
-template <class F>
+template <class M, class F>
 __device__ __forceinline__ void mg_for_nodes(const DMesh& m, int worker, int nw, F&& f) {
   const int lane = threadIdx.x & 31;
   const int chunks = (m.nx + 1 + 31) / 32;
@@ -375,7 +410,7 @@ __device__ __forceinline__ void mg_for_nodes(const DMesh& m, int worker, int nw,
   for (int it = worker; it < rows * chunks; it += nw) {
     const int row = it / chunks, i = (it % chunks) * 32 + lane;
     if (row <= m.ny) {
-      const int id = mg_node(m, i, row, false);
+      const int id = mg_row_node(m, M::row(m.nrow, row), i, row, false);
       if (id >= 0) f(id, i, row, false);
     } else if (i >= m.notch_lo && i < m.notch_hi) {
       f(m.dup_start + (i - m.notch_lo), i, m.notch_row, true);
@@ -386,307 +421,392 @@ __host__ __device__ inline int mg_items(int nx, int ny, bool notch) {
   return (ny + 1 + (notch ? 1 : 0)) * ((nx + 1 + 31) / 32);
 }
 
-// restriction (P^T t_{l-1}) at node (I, J, up) of level l >= 1: gather over the <= 9 fine
-// nodes that interpolate from it (a fine node on the far side of the slit does not)
+// restriction (P^T t_{l-1}) at node (I, J, up) of level l >= 1: gather over the <= 9 fine nodes
+// that interpolate from it (a fine node on the far side of the slit does not).  Branch-free:
+// the three fine row entries, then all candidate loads at once.
+template <class MF>
 __device__ __forceinline__ double2 mg_restrict_at(const DMesh& mf, const DMesh& mc,
                                                   const double* t, int I, int J, bool up) {
   const int Rf = mf.notch_row;
   const bool dpos = mg_dup_pos(mc, I, J);
-  double2 s = make_double2(0.0, 0.0);
+  double sx = 0.0, sy = 0.0;
 #pragma unroll
   for (int b = -1; b <= 1; ++b) {
     const int j = 2 * J + b;
+    const bool jv = j >= 0 && j <= mf.ny;
+    const int4 rw = MF::row(mf.nrow, jv ? j : 2 * J);
     const double wy = b ? 0.5 : 1.0;
+    const bool s_reg = Rf >= 0 && j > Rf;
 #pragma unroll
     for (int a = -1; a <= 1; ++a) {
       const int i = 2 * I + a;
       const double w = wy * (a ? 0.5 : 1.0);
-      const int fr = mg_node(mf, i, j, false);
-      if (fr < 0) continue;
-      const bool s_reg = Rf >= 0 && j > Rf;
-      if (!dpos || s_reg == up) {
-        const double2 v = d2ldcg(t, fr);
-        s.x += w * v.x;
-        s.y += w * v.y;
-      }
-      if (mg_dup_pos(mf, i, j) && (!dpos || up)) {
-        const double2 v = d2ldcg(t, mf.dup_start + (i - mf.notch_lo));
-        s.x += w * v.x;
-        s.y += w * v.y;
-      }
+      const int fr = jv ? mg_row_node(mf, rw, i, j, false) : -1;
+      const bool use_r = fr >= 0 && (!dpos || s_reg == up);
+      const bool use_d = fr >= 0 && mg_dup_pos(mf, i, j) && (!dpos || up);
+      const double2 vr = MF::v2(t, use_r ? fr : 0);
+      const double2 vd = MF::v2(t, use_d ? mf.dup_start + (i - mf.notch_lo) : 0);
+      const double wr = use_r ? w : 0.0, wd = use_d ? w : 0.0;
+      sx += wr * vr.x + wd * vd.x;
+      sy += wr * vr.y + wd * vd.y;
     }
   }
-  return s;
+  return make_double2(sx, sy);
 }
 
 // Matrix-vector product of a coarse level at one node, gathered from its <= 4 cells (stored
-// Galerkin matrices).  The 3x3 neighbourhood is looked up the way each cell sees its corners
-// (bottom corners from above the slit, top corners from below), so the slit faces separate:
-// slots 0-2 row j-1, 3-5 row j seen from the cells below, 6-8 row j from the cells above,
-// 9-11 row j+1.  xval(id) gives the input vector at a node; the cells are summed in the fixed
-// order below-left, below-right, above-left, above-right.  xc = input at the node itself.
-template <class X>
+// 8x8 Galerkin matrices, row-major, dofs ux0 uy0 ux1 ...).  The 3x3 neighbourhood is looked up
+// the way each cell sees its corners (bottom corners from above the slit, top corners from
+// below), so the slit faces separate: slots 0-2 row j-1, 3-5 row j seen from the cells below,
+// 6-8 row j from the cells above, 9-11 row j+1.  Branch-free: row entries, then every input and
+// matrix load at once (absent nodes / cells read entry 0 with weight 0).  Cells are summed in the
+// fixed order below-left, below-right, above-left, above-right; xc = the input at the node.
+template <class M, class X>
 __device__ __forceinline__ double2 mg_gather(const DMesh& m, const double* K, int id, int i,
                                              int j, X&& xval, double2& xc) {
+  const bool jm = j >= 1, jp = j + 1 <= m.ny;
+  const int4 rm = M::row(m.nrow, jm ? j - 1 : j), r0 = M::row(m.nrow, j);
+  const int4 rp = M::row(m.nrow, jp ? j + 1 : j);
+  const bool cm = j >= 1, c0 = j < m.ny;
+  const int4 em = M::row(m.erow, cm ? j - 1 : 0), e0 = M::row(m.erow, c0 ? j : 0);
   int nid[12];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    nid[a] = mg_node(m, i + a - 1, j - 1, true);
-    nid[3 + a] = mg_node(m, i + a - 1, j, false);
-    nid[6 + a] = mg_node(m, i + a - 1, j, true);
-    nid[9 + a] = mg_node(m, i + a - 1, j + 1, false);
+    const int ii = i + a - 1;
+    nid[a] = jm ? mg_row_node(m, rm, ii, j - 1, true) : -1;
+    nid[3 + a] = mg_row_node(m, r0, ii, j, false);
+    nid[6 + a] = mg_row_node(m, r0, ii, j, true);
+    nid[9 + a] = jp ? mg_row_node(m, rp, ii, j + 1, false) : -1;
   }
   double2 xv[12];
 #pragma unroll
   for (int sl = 0; sl < 12; ++sl) {
     const int row = sl / 3;
-    if (row == 2 && nid[sl] == nid[sl - 3]) {
-      xv[sl] = xv[sl - 3];
-      continue;
-    }
-    xv[sl] = nid[sl] >= 0 ? xval(nid[sl]) : make_double2(0.0, 0.0);
+    const int jj = j + (row == 0 ? -1 : (row == 3 ? 1 : 0));
+    const int n = max(nid[sl], 0);
+    const double2 v = xval(n, i + (sl % 3) - 1, jj, mg_is_dup(m, n));
+    xv[sl] = nid[sl] >= 0 ? v : make_double2(0.0, 0.0);
   }
   const bool below = nid[4] == id, above = nid[7] == id;
   xc = below ? xv[4] : xv[7];
-  // cells: (dx, dy, corner of this node, corner slots 0..3)
-  const int cdx[4] = {-1, 0, -1, 0}, cdy[4] = {-1, -1, 0, 0}, ck[4] = {2, 3, 1, 0};
+  auto cell = [&](int4 er, bool rv, int ci) -> int {
+    return (rv && ci >= er.x && ci < er.y) ? er.z + (ci - er.x) : -1;
+  };
+  const int ce[4] = {below ? cell(em, cm, i - 1) : -1, below ? cell(em, cm, i) : -1,
+                     above ? cell(e0, c0, i - 1) : -1, above ? cell(e0, c0, i) : -1};
+  const int ck[4] = {2, 3, 1, 0};
   const int cs[4][4] = {{0, 1, 4, 3}, {1, 2, 5, 4}, {6, 7, 10, 9}, {7, 8, 11, 10}};
-  double2 acc = make_double2(0.0, 0.0);
+  double ax = 0.0, ay = 0.0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    if (q < 2 ? !below : !above) continue;
-    const int e = mg_cell(m, i + cdx[q], j + cdy[q]);
-    if (e < 0) continue;
-    const int k = ck[q];
-    const double2* Kr = reinterpret_cast<const double2*>(K + 64 * (size_t)e);
+    const int e = ce[q];
+    const double wq = e >= 0 ? 1.0 : 0.0;
+    const double* Kr = K + 64 * (size_t)max(e, 0) + 16 * ck[q];  // rows 2k, 2k+1
+    double sx = 0.0, sy = 0.0;
 #pragma unroll
     for (int bq = 0; bq < 4; ++bq) {
       const double2 v = xv[cs[q][bq]];
-      const double2 kx = __ldcg(Kr + (2 * k) * 4 + bq), ky = __ldcg(Kr + (2 * k + 1) * 4 + bq);
-      acc.x += kx.x * v.x + kx.y * v.y;
-      acc.y += ky.x * v.x + ky.y * v.y;
+      const double2 kx = M::v2(Kr, bq), ky = M::v2(Kr + 8, bq);
+      sx += kx.x * v.x + kx.y * v.y;
+      sy += ky.x * v.x + ky.y * v.y;
     }
+    ax += wq * sx;
+    ay += wq * sy;
   }
-  return acc;
+  return make_double2(ax, ay);
 }
 
-// ---- setup helpers ----------------------------------------------------------------------------
-// Galerkin cell matrices of level lc from level lc-1 (lc == 1: from the matrix-free fine
-// operator, masked at the Dirichlet dofs); one warp per coarse cell
-__device__ __forceinline__ void mg_galerkin(const MgArgs& A, int lc, int worker, int nw,
-                                            MgGal& sg) {
-  const DMesh& mc = A.L[lc].m;
-  const DMesh& mf = A.L[lc - 1].m;
-  const int lane = threadIdx.x & 31;
-  const int c = lane >> 3, bcol = lane & 7;
-  const int ox = c & 1, oy = c >> 1;
-  double* KE = A.L[lc].K;
-  for (int it = worker; it < mc.ny * mc.nx; it += nw) {  // one coarse cell per warp item
-    const int J = it / mc.nx;
-    const int4 er = __ldg(mc.erow + J);
-    {
-      const int I = it % mc.nx;
-      if (I < er.x || I >= er.y) continue;  // warp-uniform
-      const int E = er.z + (I - er.x);
-      const int ci = 2 * I + ox, cj = 2 * J + oy;
-      // column bcol of child c's (masked) cell matrix
-      double col[8];
-      if (lc == 1) {
-        int n[4];
-        n[0] = mg_node(mf, ci, cj, true);
-        n[1] = mg_node(mf, ci + 1, cj, true);
-        n[2] = mg_node(mf, ci + 1, cj + 1, false);
-        n[3] = mg_node(mf, ci, cj + 1, false);
-        const int fe = mg_cell(mf, ci, cj);
-        double2 di[4];
-        double dc[4];
-        double2 v[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          di[q] = n[q] >= 0 ? __ldg(reinterpret_cast<const double2*>(A.L[0].dinv) + n[q])
-                            : make_double2(0.0, 0.0);
-          dc[q] = n[q] >= 0 ? __ldg(A.d + n[q]) : 0.0;
-          v[q] = make_double2(bcol == 2 * q ? 1.0 : 0.0, bcol == 2 * q + 1 ? 1.0 : 0.0);
-        }
-        const double fb = (bcol & 1) ? di[bcol >> 1].y : di[bcol >> 1].x;
-        double2 f[4];
-        f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
-        if (fe >= 0 && fb != 0.0) mom_cell_fast(A.C, v, dc, __ldg(A.flags + fe), f);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          col[2 * q] = di[q].x != 0.0 ? f[q].x : 0.0;
-          col[2 * q + 1] = di[q].y != 0.0 ? f[q].y : 0.0;
-        }
-      } else {
-        const int fe = mg_cell(mf, ci, cj);
-        const double* Kf = A.L[lc - 1].K + 64 * (size_t)fe;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) col[a] = fe >= 0 ? __ldcg(Kf + a * 8 + bcol) : 0.0;
-      }
-#pragma unroll
-      for (int a = 0; a < 8; ++a) sg.Kc[c][a * 8 + bcol] = col[a];
-      __syncwarp();
-      {  // T_c = K_c Q_c: lane (c, a = bcol) computes row a
-        const int a = bcol;
-        double tr[8];
-#pragma unroll
-        for (int B = 0; B < 8; ++B) {
-          double s = 0.0;
-#pragma unroll
-          for (int k2 = 0; k2 < 4; ++k2) s += sg.Kc[c][a * 8 + 2 * k2 + (B & 1)] * mg_q(c, k2, B >> 1);
-          tr[B] = s;
-        }
-#pragma unroll
-        for (int B = 0; B < 8; ++B) sg.T[c][a * 8 + B] = tr[B];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {  // K_E = sum_c Q_c^T T_c: entries lane, lane + 32
-        const int e = lane + 32 * h;
-        const int Ar = e >> 3, B = e & 7;
-        double s = 0.0;
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-#pragma unroll
-          for (int k2 = 0; k2 < 4; ++k2)
-            s += mg_q(cc, k2, Ar >> 1) * sg.T[cc][(2 * k2 + (Ar & 1)) * 8 + B];
-        KE[64 * (size_t)E + e] = s;
-      }
-      __syncwarp();
-    }
-  }
+// A view of one coarse level (global memory, or the tail kernel's shared-memory copy)
+struct LView {
+  DMesh m;
+  const double* K;
+  const double* dinv;
+  double* b;
+  double* t;
+  double* e;
+};
+__device__ __forceinline__ LView lview(const MgLevel& L) {
+  return LView{L.m, L.K, L.dinv, L.b, L.t, L.e};
 }
 
-__device__ __forceinline__ void mg_diag(const MgArgs& A, int l, int worker, int nw) {
-  const DMesh& m = A.L[l].m;
-  const double* K = A.L[l].K;
-  mg_for_nodes(m, worker, nw, [&](int id, int i, int j, bool dup) {
-    double sx = 0.0, sy = 0.0;
-    // (cell dx, dy, corner of this node in it)
-    const int cdx[4] = {-1, 0, -1, 0}, cdy[4] = {-1, -1, 0, 0}, ck[4] = {2, 3, 1, 0};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int ci = i + cdx[q], cj = j + cdy[q];
-      const int e = mg_cell(m, ci, cj);
-      if (e < 0) continue;
-      // the node must be this cell's corner ck[q] (slit faces)
-      const int k = ck[q];
-      const int ni = ci + ((k == 1 || k == 2) ? 1 : 0), nj = cj + (k >= 2 ? 1 : 0);
-      const int nid = mg_node(m, ni, nj, k < 2);
-      if (nid != id) continue;
-      sx += __ldcg(K + 64 * (size_t)e + (2 * k) * 9);
-      sy += __ldcg(K + 64 * (size_t)e + (2 * k + 1) * 9);
-    }
-    (void)dup;
-    d2st(A.L[l].dinv, id, make_double2(sx > 0.0 ? 1.0 / sx : 0.0, sy > 0.0 ? 1.0 / sy : 0.0));
-  });
-}
-
-// ---- coarse-level phases (levels >= 1; worker / nw count warps) ------------------------------
-// restriction b_l = P^T t_{l-1} (masked at dead dofs)
-__device__ __forceinline__ void mg_restrict(const MgArgs& A, int l, int worker, int nw) {
-  const MgLevel& L = A.L[l];
-  const DMesh& mf = A.L[l - 1].m;
-  const double* tf = A.L[l - 1].t;
-  mg_for_nodes(L.m, worker, nw, [&](int id, int i, int j, bool dup) {
-    d2st(L.b, id, mask2(mg_restrict_at(mf, L.m, tf, i, j, dup), d2ldcg(L.dinv, id)));
+// restriction b = P^T t_f (masked at dead dofs)
+template <class MF, class M>
+__device__ __forceinline__ void mg_restrict(const LView& L, const DMesh& mf, const double* tf,
+                                            int worker, int nw) {
+  mg_for_nodes<M>(L.m, worker, nw, [&](int id, int i, int j, bool dup) {
+    d2st(L.b, id, mask2(mg_restrict_at<MF>(mf, L.m, tf, i, j, dup), M::v2(L.dinv, id)));
   });
 }
 // down-sweep residual t = b - A x with x = omega D^-1 b (one Jacobi sweep from zero)
-__device__ __forceinline__ void mg_resid(const MgArgs& A, int l, double om, int worker, int nw) {
-  const MgLevel& L = A.L[l];
-  mg_for_nodes(L.m, worker, nw, [&](int id, int i, int j, bool) {
-    auto xval = [&](int n) -> double2 {
-      const double2 di = d2ldcg(L.dinv, n), bv = d2ldcg(L.b, n);
+template <class M>
+__device__ __forceinline__ void mg_resid(const LView& L, double om, int worker, int nw) {
+  mg_for_nodes<M>(L.m, worker, nw, [&](int id, int i, int j, bool) {
+    auto xval = [&](int n, int, int, bool) -> double2 {
+      const double2 di = M::v2(L.dinv, n), bv = M::v2(L.b, n);
       return make_double2(om * di.x * bv.x, om * di.y * bv.y);
     };
     double2 xc;
-    const double2 Av = mg_gather(L.m, L.K, id, i, j, xval, xc);
-    const double2 di = d2ldcg(L.dinv, id), bv = d2ldcg(L.b, id);
+    const double2 Av = mg_gather<M>(L.m, L.K, id, i, j, xval, xc);
+    const double2 di = M::v2(L.dinv, id), bv = M::v2(L.b, id);
     d2st(L.t, id, mask2(make_double2(bv.x - Av.x, bv.y - Av.y), di));
   });
 }
-// prolongation y = omega D^-1 b + P e_{l+1} (into t)
-__device__ __forceinline__ void mg_prolongate(const MgArgs& A, int l, double om, int worker,
-                                              int nw) {
-  const MgLevel& L = A.L[l];
-  const MgLevel& Lc = A.L[l + 1];
-  mg_for_nodes(L.m, worker, nw, [&](int id, int i, int j, bool dup) {
-    const double2 di = d2ldcg(L.dinv, id), bv = d2ldcg(L.b, id);
-    const double2 pe = mg_prolong(L.m, Lc.m, Lc.e, i, j, dup);
+// prolongation y = omega D^-1 b + P e_c (into t)
+template <class M, class MC>
+__device__ __forceinline__ void mg_prolongate(const LView& L, const DMesh& mc, const double* ec,
+                                              double om, int worker, int nw) {
+  mg_for_nodes<M>(L.m, worker, nw, [&](int id, int i, int j, bool dup) {
+    const double2 di = M::v2(L.dinv, id), bv = M::v2(L.b, id);
+    const double2 pe = mg_prolong<MC>(L.m, mc, ec, i, j, dup);
     d2st(L.t, id, mask2(make_double2(om * di.x * bv.x + pe.x, om * di.y * bv.y + pe.y), di));
   });
 }
-// post-smoothing e = y + omega D^-1 (b - A y), y in t
-__device__ __forceinline__ void mg_smooth(const MgArgs& A, int l, double om, int worker, int nw) {
-  const MgLevel& L = A.L[l];
-  mg_for_nodes(L.m, worker, nw, [&](int id, int i, int j, bool) {
-    auto xval = [&](int n) -> double2 { return d2ldcg(L.t, n); };
+// post-smoothing e = y + omega D^-1 (b - A y), y in t; eout: where e goes
+template <class M>
+__device__ __forceinline__ void mg_smooth(const LView& L, double* eout, double om, int worker,
+                                          int nw) {
+  mg_for_nodes<M>(L.m, worker, nw, [&](int id, int i, int j, bool) {
+    auto xval = [&](int n, int, int, bool) -> double2 { return M::v2(L.t, n); };
     double2 y;
-    const double2 Av = mg_gather(L.m, L.K, id, i, j, xval, y);
-    const double2 di = d2ldcg(L.dinv, id), bv = d2ldcg(L.b, id);
-    d2st(L.e, id, make_double2(y.x + om * di.x * (bv.x - Av.x), y.y + om * di.y * (bv.y - Av.y)));
+    const double2 Av = mg_gather<M>(L.m, L.K, id, i, j, xval, y);
+    const double2 di = M::v2(L.dinv, id), bv = M::v2(L.b, id);
+    d2st(eout, id, make_double2(y.x + om * di.x * (bv.x - Av.x), y.y + om * di.y * (bv.y - Av.y)));
   });
 }
 // Jacobi sweep eout = ein + omega D^-1 (b - A ein)
-__device__ __forceinline__ void mg_sweep(const MgArgs& A, int l, double om, const double* ein,
+template <class M>
+__device__ __forceinline__ void mg_sweep(const LView& L, double om, const double* ein,
                                          double* eout, int worker, int nw) {
-  const MgLevel& L = A.L[l];
-  mg_for_nodes(L.m, worker, nw, [&](int id, int i, int j, bool) {
-    auto xval = [&](int n) -> double2 { return d2ldcg(ein, n); };
+  mg_for_nodes<M>(L.m, worker, nw, [&](int id, int i, int j, bool) {
+    auto xval = [&](int n, int, int, bool) -> double2 { return M::v2(ein, n); };
     double2 x;
-    const double2 Av = mg_gather(L.m, L.K, id, i, j, xval, x);
-    const double2 di = d2ldcg(L.dinv, id), bv = d2ldcg(L.b, id);
+    const double2 Av = mg_gather<M>(L.m, L.K, id, i, j, xval, x);
+    const double2 di = M::v2(L.dinv, id), bv = M::v2(L.b, id);
     d2st(eout, id, make_double2(x.x + om * di.x * (bv.x - Av.x), x.y + om * di.y * (bv.y - Av.y)));
   });
 }
-// power step vout = D^-1 A vin (vin == nullptr: hashed start vector)
-__device__ __forceinline__ void mg_pow(const MgArgs& A, int l, const double* vin, double* vout,
-                                       int worker, int nw) {
-  const MgLevel& L = A.L[l];
-  mg_for_nodes(L.m, worker, nw, [&](int id, int i, int j, bool) {
-    auto xval = [&](int n) -> double2 {
-      const double2 di = d2ldcg(L.dinv, n);
-      const double2 v = vin ? d2ldcg(vin, n)
-                            : make_double2(mg_hash01(2u * n + 1u), mg_hash01(2u * n + 2u));
-      return mask2(v, di);
-    };
-    double2 x;
-    const double2 Av = mg_gather(L.m, L.K, id, i, j, xval, x);
-    const double2 di = d2ldcg(L.dinv, id);
-    d2st(vout, id, make_double2(di.x * Av.x, di.y * Av.y));
-  });
+// ---- coarse levels in assembled form: one thread per node, slot-major index and stencil
+// arrays, every load independent (two dependent rounds: indices, then values) -------------------
+__device__ __forceinline__ double mg_rw(int s) {  // restriction weight of slot s
+  const int a = s < 9 ? s % 3 - 1 : s - 10, b = s < 9 ? s / 3 - 1 : 0;
+  return (a ? 0.5 : 1.0) * (b ? 0.5 : 1.0);
 }
+// Node-parallel kernels of the assembled form: a half-warp per node, one lane per stencil /
+// restriction / prolongation slot, so every index and value load of a node is in flight at
+// once (two dependent rounds); the half-warp sum is a fixed butterfly (bit-reproducible).
+__device__ __forceinline__ double2 hw_sum(double2 v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+// slot s2 of S_s x[nbr_s] at node id (zero for s2 >= MG_NS or no coupling)
+template <class X>
+__device__ __forceinline__ double2 mg_slot_apply(const MgLevel& L, int n, int id, int s2,
+                                                 X&& xval) {
+  if (s2 >= MG_NS || id >= n) return make_double2(0.0, 0.0);
+  const int k = __ldg(L.nbr + (size_t)s2 * n + id);
+  if (k < 0) return make_double2(0.0, 0.0);
+  const double* Sp = L.S + (size_t)(4 * s2) * n + id;
+  const double sxx = __ldg(Sp), sxy = __ldg(Sp + n), syx = __ldg(Sp + 2 * (size_t)n),
+               syy = __ldg(Sp + 3 * (size_t)n);
+  const double2 x = xval(k);
+  return make_double2(sxx * x.x + sxy * x.y, syx * x.x + syy * x.y);
+}
+// LPN lanes per node (16: small levels, every load of a node in flight at once; 1: large
+// levels, latency hidden by the many resident warps).  Slot partial sums are combined in a
+// fixed order either way (bit-reproducible).
+template <int LPN>
+struct NodeMap {
+  __device__ static int lane() { return LPN == 1 ? 0 : (int)(threadIdx.x & (LPN - 1)); }
+  __device__ static int first() { return (int)((blockIdx.x * blockDim.x + threadIdx.x) / LPN); }
+  __device__ static int stride() { return (int)((gridDim.x * blockDim.x) / LPN); }
+  __device__ static int end(int n) { return LPN == 1 ? n : ((n + 1) >> 1) << 1; }  // warp-uniform
+  __device__ static double2 sum(double2 v) { return LPN == 1 ? v : hw_sum(v); }
+};
+template <int LPN, class X>
+__device__ __forceinline__ double2 mg_apply(const MgLevel& L, int n, int id, X&& xval) {
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s2 = NodeMap<LPN>::lane(); s2 < MG_NS; s2 += LPN) {
+    const double2 v = mg_slot_apply(L, n, id, s2, xval);
+    acc.x += v.x;
+    acc.y += v.y;
+  }
+  return NodeMap<LPN>::sum(acc);
+}
+#define MG_FOR_NODE_L(n) \
+  for (int id = NodeMap<LPN>::first(); id < NodeMap<LPN>::end(n); id += NodeMap<LPN>::stride())
+#define MG_LEAD (NodeMap<LPN>::lane() == 0 && id < n)
 
-// coarsest level: b = P^T t, then the dense inverse or nu_c Jacobi sweeps from zero (a
-// symmetric polynomial in D^-1 A times D^-1, so the V-cycle stays symmetric); result in L.e.
-// Runs inside one CTA (the tail kernel).
-__device__ __forceinline__ void mg_coarse_cta(const MgArgs& A, double om) {
-  const int c = A.n_levels - 1;
-  const MgLevel& L = A.L[c];
-  const int nd = 2 * L.m.n_nodes;
-  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  mg_restrict(A, c, w, nw);
-  __syncthreads();
-  if (A.dense) {
-    for (int i = threadIdx.x; i < nd; i += blockDim.x) {
-      double s = 0.0;
-      for (int j = 0; j < nd; ++j) s += __ldcg(A.Ainv + (size_t)i * nd + j) * __ldcg(L.b + j);
-      L.e[i] = s;
+// restriction b = P^T t_{l-1} (masked at dead dofs)
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mg_srestrict(MgArgs A, int l) {
+  const MgLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double* tf = A.L[l - 1].t;
+  MG_FOR_NODE_L(n) {
+    double2 v = make_double2(0.0, 0.0);
+    if (id < n) {
+#pragma unroll
+      for (int s2 = NodeMap<LPN>::lane(); s2 < 12; s2 += LPN) {
+        const int f = __ldg(L.rid + (size_t)s2 * n + id);
+        if (f >= 0) {
+          const double2 t = GMem::v2(tf, f);
+          const double w = mg_rw(s2);
+          v.x += w * t.x;
+          v.y += w * t.y;
+        }
+      }
     }
-    __syncthreads();
-    return;
+    v = NodeMap<LPN>::sum(v);
+    if (MG_LEAD) d2st(L.b, id, mask2(v, GMem::v2(L.dinv, id)));
   }
-  double* bufs[2] = {L.e, L.t};
-  int cur = (A.nu_c - 1) % 2 == 0 ? 0 : 1;  // the last sweep lands in L.e
-  for (int i = threadIdx.x; i < nd; i += blockDim.x)
-    bufs[cur][i] = om * __ldcg(L.dinv + i) * __ldcg(L.b + i);
-  __syncthreads();
-  for (int s = 1; s < A.nu_c; ++s) {
-    mg_sweep(A, c, om, bufs[cur], bufs[cur ^ 1], w, nw);
-    cur ^= 1;
-    __syncthreads();
+}
+// t = b - A x, x = omega D^-1 b
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mg_sresid(MgArgs A, int l) {
+  const MgLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  MG_FOR_NODE_L(n) {
+    const double2 Av = mg_apply<LPN>(L, n, id, [&](int k) -> double2 {
+      const double2 di = GMem::v2(L.dinv, k), bv = GMem::v2(L.b, k);
+      return make_double2(om * di.x * bv.x, om * di.y * bv.y);
+    });
+    if (MG_LEAD) {
+      const double2 di = GMem::v2(L.dinv, id), bv = GMem::v2(L.b, id);
+      d2st(L.t, id, mask2(make_double2(bv.x - Av.x, bv.y - Av.y), di));
+    }
   }
+}
+// y = omega D^-1 b + P e_{l+1} (into t)
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mg_sprolongate(MgArgs A, int l) {
+  const MgLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  const double* ec = A.L[l + 1].e;
+  MG_FOR_NODE_L(n) {
+    double2 v = make_double2(0.0, 0.0), cnt = make_double2(0.0, 0.0);
+    if (id < n) {
+#pragma unroll
+      for (int s2 = NodeMap<LPN>::lane(); s2 < 4; s2 += LPN) {
+        const int c = __ldg(L.pid + (size_t)s2 * n + id);
+        if (c >= 0) {
+          const double2 e = GMem::v2(ec, c);
+          v.x += e.x;
+          v.y += e.y;
+          cnt.x += 1.0;
+        }
+      }
+    }
+    v = NodeMap<LPN>::sum(v);
+    cnt = NodeMap<LPN>::sum(cnt);
+    if (MG_LEAD) {
+      const double w = 1.0 / cnt.x;  // bilinear weights: 1, 1/2 or 1/4 (distinct sources)
+      const double2 di = GMem::v2(L.dinv, id), bv = GMem::v2(L.b, id);
+      d2st(L.t, id, mask2(make_double2(om * di.x * bv.x + w * v.x, om * di.y * bv.y + w * v.y), di));
+    }
+  }
+}
+// e = y + omega D^-1 (b - A y), y in t
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mg_ssmooth(MgArgs A, int l) {
+  const MgLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  MG_FOR_NODE_L(n) {
+    const double2 Ay = mg_apply<LPN>(L, n, id, [&](int k) -> double2 { return GMem::v2(L.t, k); });
+    if (MG_LEAD) {
+      const double2 y = GMem::v2(L.t, id), di = GMem::v2(L.dinv, id), bv = GMem::v2(L.b, id);
+      d2st(L.e, id, make_double2(y.x + om * di.x * (bv.x - Ay.x), y.y + om * di.y * (bv.y - Ay.y)));
+    }
+  }
+}
+// Jacobi sweep out = in + omega D^-1 (b - A in) (grid coarsest level)
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mg_ssweep(MgArgs A, int l, const double* in,
+                                                     double* out) {
+  const MgLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  MG_FOR_NODE_L(n) {
+    const double2 Ax = mg_apply<LPN>(L, n, id, [&](int k) -> double2 { return GMem::v2(in, k); });
+    if (MG_LEAD) {
+      const double2 x = GMem::v2(in, id), di = GMem::v2(L.dinv, id), bv = GMem::v2(L.b, id);
+      d2st(out, id, make_double2(x.x + om * di.x * (bv.x - Ax.x), x.y + om * di.y * (bv.y - Ax.y)));
+    }
+  }
+}
+// power step at one node of a coarse level (half-warp per node; every lane of the warp must
+// call it: id >= n makes the half-warp idle): vout = D^-1 A vin (vin == nullptr: hashed start)
+__device__ __forceinline__ void mg_spow(const MgLevel& L, const double* vin, double* vout, int id) {
+  const int n = L.m.n_nodes, s2 = (int)(threadIdx.x & 15);
+  const double2 Av = hw_sum(mg_slot_apply(L, n, id, s2, [&](int k) -> double2 {
+    const double2 di = GMem::v2(L.dinv, k);
+    const double2 v = vin ? GMem::v2(vin, k)
+                          : make_double2(mg_hash01(2u * k + 1u), mg_hash01(2u * k + 2u));
+    return mask2(v, di);
+  }));
+  if (s2 == 0 && id < n) {
+    const double2 di = GMem::v2(L.dinv, id);
+    d2st(vout, id, make_double2(di.x * Av.x, di.y * Av.y));
+  }
+}
+// setup: assemble the stencil of level l from its cell matrices, and its inverse diagonal
+__global__ void __launch_bounds__(MG_NT) k_mg_stencil(MgArgs A, int l) {
+  const MgLevel& L = A.L[l];
+  const DMesh& m = L.m;
+  const int n = m.n_nodes;
+  mg_for_nodes<GMem>(m, blockIdx.x * MG_WARPS + (threadIdx.x >> 5), gridDim.x * MG_WARPS,
+                     [&](int id, int i, int j, bool) {
+    int nb[MG_NS];
+#pragma unroll
+    for (int s2 = 0; s2 < MG_NS; ++s2) nb[s2] = __ldg(L.nbr + (size_t)s2 * n + id);
+    double acc[MG_NS][4];
+#pragma unroll
+    for (int s2 = 0; s2 < MG_NS; ++s2)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[s2][q] = 0.0;
+    const int cdx[4] = {-1, 0, -1, 0}, cdy[4] = {-1, -1, 0, 0}, ck[4] = {2, 3, 1, 0};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {  // below-left, below-right, above-left, above-right
+      const int ci = i + cdx[c], cj = j + cdy[c];
+      const int e = mg_cell(m, ci, cj);
+      if (e < 0) continue;
+      int cn[4];
+      cn[0] = mg_node(m, ci, cj, true);
+      cn[1] = mg_node(m, ci + 1, cj, true);
+      cn[2] = mg_node(m, ci + 1, cj + 1, false);
+      cn[3] = mg_node(m, ci, cj + 1, false);
+      const int k = ck[c];
+      if (cn[k] != id) continue;  // the cell is on the other face of the slit
+      const double* Ke = L.K + 64 * (size_t)e;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int qx = ci + ((q == 1 || q == 2) ? 1 : 0) - i, qy = cj + (q >= 2 ? 1 : 0) - j;
+        int slot = qy < 0 ? 1 + qx : (qy > 0 ? 7 + qx : 4 + qx);
+        if (qy == 0 && nb[slot] != cn[q]) slot = 9;
+        const double kxx = __ldg(Ke + (2 * k) * 8 + 2 * q), kxy = __ldg(Ke + (2 * k) * 8 + 2 * q + 1);
+        const double kyx = __ldg(Ke + (2 * k + 1) * 8 + 2 * q),
+                     kyy = __ldg(Ke + (2 * k + 1) * 8 + 2 * q + 1);
+#pragma unroll
+        for (int s2 = 0; s2 < MG_NS; ++s2)
+          if (s2 == slot) {
+            acc[s2][0] += kxx; acc[s2][1] += kxy; acc[s2][2] += kyx; acc[s2][3] += kyy;
+          }
+      }
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < MG_NS; ++s2)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) L.S[(size_t)(4 * s2 + q) * n + id] = acc[s2][q];
+    d2st(L.dinv, id, make_double2(acc[4][0] > 0.0 ? 1.0 / acc[4][0] : 0.0,
+                                  acc[4][3] > 0.0 ? 1.0 / acc[4][3] : 0.0));
+  });
 }
 
 // ---- deterministic grid reductions: per-CTA partials, the last CTA sums them in order --------
@@ -792,38 +912,108 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_fine_resid(MgArgs A) {
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
 }
 
-__global__ void __launch_bounds__(MG_NT) k_mg_restrict(MgArgs A, int l) {
-  mg_restrict(A, l, blockIdx.x * MG_WARPS + (threadIdx.x >> 5), gridDim.x * MG_WARPS);
+#define MG_GW (int)(blockIdx.x * MG_WARPS + (threadIdx.x >> 5)), (int)(gridDim.x * MG_WARPS)
+// coarsest level on the grid (it does not fit the tail kernel's shared memory): dense inverse
+// applied by one CTA, or Jacobi sweeps from zero (k_mg_jacobi0 then k_mg_ssweep ping-pong)
+__global__ void __launch_bounds__(MG_NT) k_mg_coarse_dense(MgArgs A) {
+  const MgLevel& L = A.L[A.n_levels - 1];
+  const int nd = 2 * L.m.n_nodes;
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < nd; ++j) s += __ldcg(A.Ainv + (size_t)i * nd + j) * __ldcg(L.b + j);
+    L.e[i] = s;
+  }
 }
-__global__ void __launch_bounds__(MG_NT) k_mg_resid(MgArgs A, int l) {
-  mg_resid(A, l, __ldcg(&A.ctl->omega[l]), blockIdx.x * MG_WARPS + (threadIdx.x >> 5),
-           gridDim.x * MG_WARPS);
+__global__ void __launch_bounds__(MG_NT) k_mg_jacobi0(MgArgs A, int l, double* out) {
+  const MgLevel& L = A.L[l];
+  const double om = __ldcg(&A.ctl->omega[l]);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < 2LL * L.m.n_nodes;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = om * __ldcg(L.dinv + i) * __ldcg(L.b + i);
 }
-__global__ void __launch_bounds__(MG_NT) k_mg_prolongate(MgArgs A, int l) {
-  mg_prolongate(A, l, __ldcg(&A.ctl->omega[l]), blockIdx.x * MG_WARPS + (threadIdx.x >> 5),
-                gridDim.x * MG_WARPS);
+// Tail: levels [n_tail, n_levels) staged in dynamic shared memory (row tables, cell matrices,
+// inverse diagonals, the dense coarsest inverse) and cycled by one CTA with CTA barriers:
+// restriction from level n_tail - 1 (global) down to the coarsest solve and back up to
+// e_{n_tail} (global).  Offsets (bytes) come from the host (MgArgs::ts).
+extern __shared__ __align__(16) unsigned char mg_tail_smem[];
+__device__ __forceinline__ LView mg_tail_view(const MgArgs& A, int l) {
+  unsigned char* sm = mg_tail_smem;
+  const MgTailSlot& t = A.ts[l];
+  LView v;
+  v.m = A.L[l].m;
+  v.m.nrow = reinterpret_cast<const int4*>(sm + t.nrow);
+  v.m.erow = reinterpret_cast<const int4*>(sm + t.erow);
+  v.K = reinterpret_cast<const double*>(sm + t.K);
+  v.dinv = reinterpret_cast<const double*>(sm + t.dinv);
+  v.b = reinterpret_cast<double*>(sm + t.b);
+  v.t = reinterpret_cast<double*>(sm + t.t);
+  v.e = reinterpret_cast<double*>(sm + t.e);
+  return v;
 }
-__global__ void __launch_bounds__(MG_NT) k_mg_smooth(MgArgs A, int l) {
-  mg_smooth(A, l, __ldcg(&A.ctl->omega[l]), blockIdx.x * MG_WARPS + (threadIdx.x >> 5),
-            gridDim.x * MG_WARPS);
+__device__ __forceinline__ void mg_stage(void* dst, const void* src, size_t bytes) {
+  const int4* s4 = reinterpret_cast<const int4*>(src);
+  int4* d4 = reinterpret_cast<int4*>(dst);
+  for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) d4[i] = __ldcg(s4 + i);
 }
-
-// levels [n_tail, n_levels) in one CTA: the V-cycle below level n_tail - 1 (result e_{n_tail})
 __global__ void __launch_bounds__(MG_TAIL_NT) k_mg_tail(MgArgs A) {
   const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nl = A.n_levels, l0 = A.n_tail;
-  for (int l = l0; l < nl - 1; ++l) {
-    mg_restrict(A, l, w, nw);
-    __syncthreads();
-    mg_resid(A, l, __ldcg(&A.ctl->omega[l]), w, nw);
-    __syncthreads();
+  const int nl = A.n_levels, l0 = A.n_tail, c = nl - 1;
+  for (int l = l0; l < nl; ++l) {
+    const LView v = mg_tail_view(A, l);
+    const MgLevel& G = A.L[l];
+    mg_stage((void*)v.m.nrow, G.m.nrow, sizeof(int4) * (G.m.ny + 1));
+    mg_stage((void*)v.m.erow, G.m.erow, sizeof(int4) * G.m.ny);
+    mg_stage((void*)v.K, G.K, sizeof(double) * 64 * (size_t)G.m.n_elems);
+    mg_stage((void*)v.dinv, G.dinv, sizeof(double) * 2 * (size_t)G.m.n_nodes);
   }
-  mg_coarse_cta(A, __ldcg(&A.ctl->omega[nl - 1]));
-  for (int l = nl - 2; l >= l0; --l) {
-    const double om = __ldcg(&A.ctl->omega[l]);
-    mg_prolongate(A, l, om, w, nw);
+  const int nd = 2 * A.L[c].m.n_nodes;
+  double* Ainv = reinterpret_cast<double*>(mg_tail_smem + A.ts_ainv);
+  if (A.dense) mg_stage(Ainv, A.Ainv, sizeof(double) * nd * nd);
+  __syncthreads();
+  for (int l = l0; l < nl; ++l) {
+    const LView v = mg_tail_view(A, l);
+    if (l == l0) mg_restrict<GMem, SMem>(v, A.L[l - 1].m, A.L[l - 1].t, w, nw);
+    else {
+      const LView f = mg_tail_view(A, l - 1);
+      mg_restrict<SMem, SMem>(v, f.m, f.t, w, nw);
+    }
     __syncthreads();
-    mg_smooth(A, l, om, w, nw);
+    if (l < c) {
+      mg_resid<SMem>(v, __ldcg(&A.ctl->omega[l]), w, nw);
+      __syncthreads();
+    }
+  }
+  {  // coarsest solve
+    const LView v = mg_tail_view(A, c);
+    if (A.dense) {
+      for (int i = threadIdx.x; i < nd; i += blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < nd; ++j) s += Ainv[i * nd + j] * v.b[j];
+        v.e[i] = s;
+      }
+      __syncthreads();
+    } else {
+      const double om = __ldcg(&A.ctl->omega[c]);
+      double* bufs[2] = {v.e, v.t};
+      int cur = (A.nu_c - 1) % 2 == 0 ? 0 : 1;  // the last sweep lands in e
+      for (int i = threadIdx.x; i < nd; i += blockDim.x) bufs[cur][i] = om * v.dinv[i] * v.b[i];
+      __syncthreads();
+      for (int s2 = 1; s2 < A.nu_c; ++s2) {
+        mg_sweep<SMem>(v, om, bufs[cur], bufs[cur ^ 1], w, nw);
+        cur ^= 1;
+        __syncthreads();
+      }
+    }
+    if (l0 == c)  // only the coarsest level in the tail: hand its result to the grid
+      for (int i = threadIdx.x; i < nd; i += blockDim.x) A.L[c].e[i] = v.e[i];
+  }
+  for (int l = c - 1; l >= l0; --l) {
+    const LView v = mg_tail_view(A, l);
+    const LView cv = mg_tail_view(A, l + 1);
+    const double om = __ldcg(&A.ctl->omega[l]);
+    mg_prolongate<SMem, SMem>(v, cv.m, cv.e, om, w, nw);
+    __syncthreads();
+    mg_smooth<SMem>(v, l == l0 ? A.L[l].e : v.e, om, w, nw);
     __syncthreads();
   }
 }
@@ -920,13 +1110,96 @@ __global__ void __launch_bounds__(MG_NT) k_mg_finish(MgArgs A) {
 // ================================================================================================
 // setup kernels: Galerkin cell matrices, inverse diagonals, lambda_max by power steps, dense
 // inverse of the coarsest level
+// Galerkin cell matrices of level lc from level lc-1 (lc == 1: from the matrix-free fine
+// operator, masked at the Dirichlet dofs); one warp per coarse cell
+__device__ __forceinline__ void mg_galerkin(const MgArgs& A, int lc, int worker, int nw,
+                                            MgGal& sg) {
+  const DMesh& mc = A.L[lc].m;
+  const DMesh& mf = A.L[lc - 1].m;
+  const int lane = threadIdx.x & 31;
+  const int c = lane >> 3, bcol = lane & 7;
+  const int ox = c & 1, oy = c >> 1;
+  double* KE = A.L[lc].K;
+  for (int it = worker; it < mc.ny * mc.nx; it += nw) {  // one coarse cell per warp item
+    const int J = it / mc.nx;
+    const int4 er = __ldg(mc.erow + J);
+    {
+      const int I = it % mc.nx;
+      if (I < er.x || I >= er.y) continue;  // warp-uniform
+      const int E = er.z + (I - er.x);
+      const int ci = 2 * I + ox, cj = 2 * J + oy;
+      // column bcol of child c's (masked) cell matrix
+      double col[8];
+      if (lc == 1) {
+        int n[4];
+        n[0] = mg_node(mf, ci, cj, true);
+        n[1] = mg_node(mf, ci + 1, cj, true);
+        n[2] = mg_node(mf, ci + 1, cj + 1, false);
+        n[3] = mg_node(mf, ci, cj + 1, false);
+        const int fe = mg_cell(mf, ci, cj);
+        double2 di[4];
+        double dc[4];
+        double2 v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          di[q] = n[q] >= 0 ? __ldg(reinterpret_cast<const double2*>(A.L[0].dinv) + n[q])
+                            : make_double2(0.0, 0.0);
+          dc[q] = n[q] >= 0 ? __ldg(A.d + n[q]) : 0.0;
+          v[q] = make_double2(bcol == 2 * q ? 1.0 : 0.0, bcol == 2 * q + 1 ? 1.0 : 0.0);
+        }
+        const double fb = (bcol & 1) ? di[bcol >> 1].y : di[bcol >> 1].x;
+        double2 f[4];
+        f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
+        if (fe >= 0 && fb != 0.0) mom_cell_fast(A.C, v, dc, __ldg(A.flags + fe), f);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          col[2 * q] = di[q].x != 0.0 ? f[q].x : 0.0;
+          col[2 * q + 1] = di[q].y != 0.0 ? f[q].y : 0.0;
+        }
+      } else {
+        const int fe = mg_cell(mf, ci, cj);
+        const double* Kf = A.L[lc - 1].K + 64 * (size_t)fe;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) col[a] = fe >= 0 ? __ldg(Kf + a * 8 + bcol) : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < 8; ++a) sg.Kc[c][a * 8 + bcol] = col[a];
+      __syncwarp();
+      {  // T_c = K_c Q_c: lane (c, a = bcol) computes row a
+        const int a = bcol;
+        double tr[8];
+#pragma unroll
+        for (int B = 0; B < 8; ++B) {
+          double s = 0.0;
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) s += sg.Kc[c][a * 8 + 2 * k2 + (B & 1)] * mg_q(c, k2, B >> 1);
+          tr[B] = s;
+        }
+#pragma unroll
+        for (int B = 0; B < 8; ++B) sg.T[c][a * 8 + B] = tr[B];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // K_E = sum_c Q_c^T T_c: entries lane, lane + 32
+        const int e = lane + 32 * h;
+        const int Ar = e >> 3, B = e & 7;
+        double s = 0.0;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2)
+            s += mg_q(cc, k2, Ar >> 1) * sg.T[cc][(2 * k2 + (Ar & 1)) * 8 + B];
+        KE[64 * (size_t)E + e] = s;
+      }
+      __syncwarp();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(MG_NT) k_mg_galerkin(MgArgs A, int lc) {
   __shared__ MgGal sg[MG_WARPS];
   mg_galerkin(A, lc, blockIdx.x * MG_WARPS + (threadIdx.x >> 5), gridDim.x * MG_WARPS,
               sg[threadIdx.x >> 5]);
-}
-__global__ void __launch_bounds__(MG_NT) k_mg_diag(MgArgs A, int l) {
-  mg_diag(A, l, blockIdx.x * MG_WARPS + (threadIdx.x >> 5), gridDim.x * MG_WARPS);
 }
 // power step k (1..MG_POW): blocks [0, fine_blocks) march the fine level, the rest gather the
 // coarse levels (concatenated item space)
@@ -943,12 +1216,14 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_pow(MgArgs A, int step, int fin
     if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[warp]);
     return;
   }
-  const int w = (blockIdx.x - fine_blocks) * MG_WARPS + warp;
-  if (w >= A.coarse_items) return;
+  // concatenated coarse nodes, a half-warp per node (the node pair of a warp shares a level:
+  // level offsets are even)
+  const int t = ((blockIdx.x - fine_blocks) * MG_NT + threadIdx.x) >> 4;
+  if (t >= A.coarse_items) return;  // whole warps (coarse_items is even)
   int l = 1;
-  while (l + 1 < A.n_levels && w >= A.L[l + 1].item_off) ++l;
+  while (l + 1 < A.n_levels && t >= A.L[l + 1].item_off) ++l;
   const MgLevel& L = A.L[l];
-  mg_pow(A, l, vin(L), vout(L), w - L.item_off, L.items);
+  mg_spow(L, vin(L), vout(L), t - L.item_off);
 }
 // omega_l = 4 / (3 lambda_l), lambda_l = ||v_POW|| / ||v_POW-1|| (per-level partials)
 __global__ void __launch_bounds__(MG_NT) k_mg_lambda(MgArgs A) {
@@ -987,31 +1262,38 @@ __global__ void __launch_bounds__(MG_NT) k_mg_dense(MgArgs A) {
   __shared__ double M[MG_DENSE_MAX * MG_DENSE_MAX];
   __shared__ double F[MG_DENSE_MAX];
   __shared__ int live[MG_DENSE_MAX];
+  __shared__ int cn[MG_DENSE_MAX][4];  // corner node ids of the coarsest cells (<= nodes)
+  __shared__ int ncell;
   const int c = A.n_levels - 1;
   const DMesh& m = A.L[c].m;
   const int nd = 2 * m.n_nodes;
+  if (threadIdx.x == 0) {
+    int e = 0;
+    for (int cjr = 0; cjr < m.ny; ++cjr) {
+      const int4 er = __ldg(m.erow + cjr);
+      for (int cir = er.x; cir < er.y && e < MG_DENSE_MAX; ++cir, ++e) {
+        cn[e][0] = mg_node(m, cir, cjr, true);
+        cn[e][1] = mg_node(m, cir + 1, cjr, true);
+        cn[e][2] = mg_node(m, cir + 1, cjr + 1, false);
+        cn[e][3] = mg_node(m, cir, cjr + 1, false);
+      }
+    }
+    ncell = e;
+  }
+  __syncthreads();
   for (int ij = threadIdx.x; ij < nd * nd; ij += blockDim.x) {
     const int i = ij / nd, j = ij % nd;
     const int ni = i >> 1, nj = j >> 1, ci = i & 1, cj = j & 1;
     double s = 0.0;
-    for (int cjr = 0; cjr < m.ny; ++cjr) {
-      const int4 er = __ldg(m.erow + cjr);
-      for (int cir = er.x; cir < er.y; ++cir) {
-        const int e = er.z + (cir - er.x);
-        int n[4];
-        n[0] = mg_node(m, cir, cjr, true);
-        n[1] = mg_node(m, cir + 1, cjr, true);
-        n[2] = mg_node(m, cir + 1, cjr + 1, false);
-        n[3] = mg_node(m, cir, cjr + 1, false);
-        int ka = -1, kb = -1;
+    for (int e = 0; e < ncell; ++e) {  // cells in id order (row-compact numbering)
+      int ka = -1, kb = -1;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (n[q] == ni) ka = q;
-          if (n[q] == nj) kb = q;
-        }
-        if (ka >= 0 && kb >= 0)
-          s += __ldcg(A.L[c].K + 64 * (size_t)e + (2 * ka + ci) * 8 + 2 * kb + cj);
+      for (int q = 0; q < 4; ++q) {
+        if (cn[e][q] == ni) ka = q;
+        if (cn[e][q] == nj) kb = q;
       }
+      if (ka >= 0 && kb >= 0)
+        s += __ldcg(A.L[c].K + 64 * (size_t)e + (2 * ka + ci) * 8 + 2 * kb + cj);
     }
     M[ij] = s;
   }

@@ -276,12 +276,14 @@ class DeviceSession:
 
     def mg_info(self, with_omega: bool = False) -> dict:
         """Multigrid hierarchy of the momentum PCG (n_levels 0: Jacobi PCG on this handle)."""
-        nl, ng, dn = C.c_int32(), C.c_int32(), C.c_int32()
-        self._check(self.lib.pf_mg_info(self.h, C.byref(nl), C.byref(ng), C.byref(dn), None))
-        out = {"n_levels": nl.value, "n_grid": ng.value, "dense": bool(dn.value)}
+        nl, ng, dn, su = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+        self._check(self.lib.pf_mg_info(self.h, C.byref(nl), C.byref(ng), C.byref(dn),
+                                        C.byref(su), None))
+        out = {"n_levels": nl.value, "n_grid": ng.value, "dense": bool(dn.value),
+               "setups": su.value}
         if with_omega and nl.value:
             om = np.zeros(nl.value)
-            self._check(self.lib.pf_mg_info(self.h, None, None, None, N.f64(om)))
+            self._check(self.lib.pf_mg_info(self.h, None, None, None, None, N.f64(om)))
             out["omega"] = om
         return out
 
