@@ -472,12 +472,14 @@ static std::vector<int> hl_prolong_ids(const HostLevel& f, const HostLevel& c) {
   return ids;
 }
 
+// multigrid arrays are padded to 16-byte multiples (k_mg_tail stages them with TMA bulk copies)
 template <class T>
 static cudaError_t mg_alloc(pf_handle* h, T** p, size_t n) {
-  cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
+  const size_t bytes = (std::max<size_t>(n, 1) * sizeof(T) + 15) & ~size_t(15);
+  cudaError_t e = cudaMalloc((void**)p, bytes);
   if (e == cudaSuccess) {
     h->mg_allocs.push_back((void*)*p);
-    e = cudaMemset(*p, 0, std::max<size_t>(n, 1) * sizeof(T));
+    e = cudaMemset(*p, 0, bytes);
   }
   return e;
 }
@@ -510,17 +512,23 @@ static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
   A.n_levels = nl;
   A.dense = 2 * lv.back().n_nodes <= pfb::MG_DENSE_MAX;
   A.nu_c = nu_c;
-  // tail: the coarsest levels whose row tables, cell matrices and vectors (plus the dense
-  // inverse) fit the single-CTA kernel's shared memory (PFB200_MG_TAIL_KB, default 200)
+  // tail: the coarsest levels whose assembled form (plus the dense inverse) fits the
+  // single-CTA kernel's shared memory (PFB200_MG_TAIL_KB, default 220)
   const char* tk = getenv("PFB200_MG_TAIL_KB");
-  const size_t budget = (size_t)(tk ? std::max(0, atoi(tk)) : 200) * 1024;
-  auto level_bytes = [&](const HostLevel& L) -> size_t {
-    return 16 * (size_t)(2 * L.ny + 1) + 8 * 64 * (size_t)L.n_elems + 8 * 2 * 4 * (size_t)L.n_nodes;
+  const size_t budget = (size_t)(tk ? std::max(0, atoi(tk)) : 220) * 1024;
+  auto level_bytes = [&](const HostLevel& L) -> size_t {  // assembled form, 16-B aligned arrays
+    auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
+    const size_t n = L.n_nodes;
+    return al(4 * pfb::MG_NS * n) + al(4 * 12 * n) + al(4 * 4 * n) + al(8 * 4 * pfb::MG_NS * n) +
+           4 * al(16 * n);
   };
   const size_t ainv_bytes = A.dense ? 8 * (size_t)(2 * lv.back().n_nodes) * (2 * lv.back().n_nodes) : 0;
   int nt = nl;
   size_t used = ainv_bytes;
-  while (nt > 1 && lv[nt - 1].n_nodes <= tail_nodes && used + level_bytes(lv[nt - 1]) <= budget) {
+  // (the top tail level's restriction sources are pre-loaded in registers: at most
+  // MG_TAIL_P passes of MG_TAIL_NT / 4 nodes)
+  while (nt > 1 && lv[nt - 1].n_nodes <= std::min(tail_nodes, pfb::MG_TAIL_P * pfb::MG_TAIL_NT / 4) &&
+         used + level_bytes(lv[nt - 1]) <= budget) {
     used += level_bytes(lv[nt - 1]);
     --nt;
   }
@@ -529,15 +537,16 @@ static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
     size_t off = 0;
     auto take = [&](size_t bytes) { const size_t o = off; off += (bytes + 15) & ~size_t(15); return (int)o; };
     for (int l = nt; l < nl; ++l) {
-      const HostLevel& L = lv[l];
+      const size_t n = lv[l].n_nodes;
       pfb::MgTailSlot& t = A.ts[l];
-      t.nrow = take(16 * (size_t)(L.ny + 1));
-      t.erow = take(16 * (size_t)L.ny);
-      t.K = take(8 * 64 * (size_t)L.n_elems);
-      t.dinv = take(16 * (size_t)L.n_nodes);
-      t.b = take(16 * (size_t)L.n_nodes);
-      t.t = take(16 * (size_t)L.n_nodes);
-      t.e = take(16 * (size_t)L.n_nodes);
+      t.nbr = take(4 * pfb::MG_NS * n);
+      t.rid = take(4 * 12 * n);
+      t.pid = take(4 * 4 * n);
+      t.S = take(8 * 4 * pfb::MG_NS * n);
+      t.dinv = take(16 * n);
+      t.b = take(16 * n);
+      t.t = take(16 * n);
+      t.e = take(16 * n);
     }
     A.ts_ainv = take(ainv_bytes);
     A.ts_bytes = (int)off;
@@ -585,7 +594,8 @@ static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
       // small levels: a half-warp per node (all loads of a node in flight); large levels: a
       // thread per node (latency hidden by occupancy).  Threshold: 16 lanes per node would
       // exceed one wave of resident threads.
-      h->mg_lpn[l] = 16LL * L.n_nodes <= 2048LL * h->sm_count ? 16 : 1;
+      const long long wave = 2048LL * h->sm_count;
+      h->mg_lpn[l] = 16LL * L.n_nodes <= wave ? 16 : (4LL * L.n_nodes <= wave ? 4 : 1);
       h->mg_gn[l] = std::max(1, std::min((int)((h->mg_lpn[l] * (long long)L.n_nodes + pfb::MG_NT - 1) / pfb::MG_NT),
                                          16 * h->sm_count));
       {  // assembled-form index tables (static per handle)
@@ -632,6 +642,9 @@ static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
   A.x = h->xu; A.r = h->ru; A.p0 = h->p0u; A.p1 = h->p1u; A.q = h->qu;
   A.result = h->d_cgres;
   A.ndof = 2LL * h->n_nodes;
+  if (getenv("PFB200_MG_TAILCLK")) {
+    if (mg_alloc(h, &A.tclk, 32) != cudaSuccess) return oom();
+  }
   PF_TRY(mg_build_graphs(h));
   h->mg = true;
   return PF_OK;
@@ -668,6 +681,7 @@ static pf_status mg_build_graphs(pf_handle* h) {
 #define MG_NODE_KERNEL(K, l, ...)                                                   \
   do {                                                                              \
     if (h->mg_lpn[l] == 16) pfb::K<16><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__); \
+    else if (h->mg_lpn[l] == 4) pfb::K<4><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__); \
     else pfb::K<1><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__);                     \
   } while (0)
   auto body_kernels = [&](const pfb::MgArgs& B) {
@@ -1646,6 +1660,13 @@ static pf_status run_mg(pf_handle* h, double* target, int* status, long long* it
   if (h->trace)
     fprintf(stderr, "[pfb200] mg solve: %lld iterations, %.3f ms%s\n", *iters, ms,
             rebuild ? " (hierarchy rebuilt)" : "");
+  if (h->mga.tclk) {
+    long long c[32] = {};
+    cudaMemcpy(c, h->mga.tclk, sizeof c, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[pfb200] tail phases (cycles):");
+    for (int k = 1; k < 32 && c[k]; ++k) fprintf(stderr, " %lld", c[k] - c[k - 1]);
+    fprintf(stderr, "\n");
+  }
   h->mg_age += 1;
   if (!check) return PF_OK;
   cg_account(h, true, *iters, ms);

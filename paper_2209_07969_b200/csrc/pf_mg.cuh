@@ -35,8 +35,9 @@ constexpr int MG_NT = 256;
 constexpr int MG_WARPS = MG_NT / 32;
 constexpr int MG_POW = 8;          // power steps for lambda_max(D^-1 A_l)
 constexpr int MG_DENSE_MAX = 64;   // coarsest level by a dense inverse when 2 n_nodes <= this
-constexpr int MG_TAIL_NT = 512;    // threads of the single-CTA tail kernel
+constexpr int MG_TAIL_NT = 1024;   // threads of the single-CTA tail kernel
 constexpr int MG_NS = 10;          // assembled stencil slots per node (3x3 + slit-tip face)
+constexpr int MG_TAIL_P = 2;       // node passes of the tail's top level (MG_TAIL_NT / 4 each)
 
 struct MgLevel {
   DMesh m;        // row tables (nrow/erow), notch, n_nodes/n_elems of this level
@@ -72,7 +73,7 @@ struct MgCtl {
 };
 
 struct MgTailSlot {  // byte offsets of one tail level in k_mg_tail's shared memory
-  int nrow, erow, K, dinv, b, t, e;
+  int nbr, rid, pid, S, dinv, b, t, e;
 };
 
 struct MgArgs {
@@ -93,6 +94,7 @@ struct MgArgs {
   long long ndof;
   cudaGraphConditionalHandle cond;
   int use_cond;          // 0: launched outside the graph (unrolled profiling graph)
+  long long* tclk;       // debug (PFB200_MG_TAILCLK): clock64 after each k_mg_tail phase
   MgTailSlot ts[MG_MAXL];
   int ts_ainv, ts_bytes;  // dense inverse offset, total shared memory of k_mg_tail
 };
@@ -283,20 +285,13 @@ struct FineResid : FineBase {  // x = omega D^-1 r (pre-smoothing from zero), t 
   }
 };
 
-// ---- memory policies of the coarse-level primitives: global (every input of a kernel was
-// written by an earlier kernel, so the read-only / L1 path is coherent) or shared (the tail
-// kernel's staged levels)
+// ---- global loads of the coarse-level kernels: every input of a kernel was written by an
+// earlier kernel, so the read-only / L1 path is coherent
 struct GMem {
   __device__ static double2 v2(const double* p, int i) {
     return __ldg(reinterpret_cast<const double2*>(p) + i);
   }
   __device__ static int4 row(const int4* p, int j) { return __ldg(p + j); }
-};
-struct SMem {
-  __device__ static double2 v2(const double* p, int i) {
-    return reinterpret_cast<const double2*>(p)[i];
-  }
-  __device__ static int4 row(const int4* p, int j) { return p[j]; }
 };
 
 // node id in a row entry (lo, hi, start); up: the slit row's duplicates as seen from above
@@ -421,170 +416,6 @@ __host__ __device__ inline int mg_items(int nx, int ny, bool notch) {
   return (ny + 1 + (notch ? 1 : 0)) * ((nx + 1 + 31) / 32);
 }
 
-// restriction (P^T t_{l-1}) at node (I, J, up) of level l >= 1: gather over the <= 9 fine nodes
-// that interpolate from it (a fine node on the far side of the slit does not).  Branch-free:
-// the three fine row entries, then all candidate loads at once.
-template <class MF>
-__device__ __forceinline__ double2 mg_restrict_at(const DMesh& mf, const DMesh& mc,
-                                                  const double* t, int I, int J, bool up) {
-  const int Rf = mf.notch_row;
-  const bool dpos = mg_dup_pos(mc, I, J);
-  double sx = 0.0, sy = 0.0;
-#pragma unroll
-  for (int b = -1; b <= 1; ++b) {
-    const int j = 2 * J + b;
-    const bool jv = j >= 0 && j <= mf.ny;
-    const int4 rw = MF::row(mf.nrow, jv ? j : 2 * J);
-    const double wy = b ? 0.5 : 1.0;
-    const bool s_reg = Rf >= 0 && j > Rf;
-#pragma unroll
-    for (int a = -1; a <= 1; ++a) {
-      const int i = 2 * I + a;
-      const double w = wy * (a ? 0.5 : 1.0);
-      const int fr = jv ? mg_row_node(mf, rw, i, j, false) : -1;
-      const bool use_r = fr >= 0 && (!dpos || s_reg == up);
-      const bool use_d = fr >= 0 && mg_dup_pos(mf, i, j) && (!dpos || up);
-      const double2 vr = MF::v2(t, use_r ? fr : 0);
-      const double2 vd = MF::v2(t, use_d ? mf.dup_start + (i - mf.notch_lo) : 0);
-      const double wr = use_r ? w : 0.0, wd = use_d ? w : 0.0;
-      sx += wr * vr.x + wd * vd.x;
-      sy += wr * vr.y + wd * vd.y;
-    }
-  }
-  return make_double2(sx, sy);
-}
-
-// Matrix-vector product of a coarse level at one node, gathered from its <= 4 cells (stored
-// 8x8 Galerkin matrices, row-major, dofs ux0 uy0 ux1 ...).  The 3x3 neighbourhood is looked up
-// the way each cell sees its corners (bottom corners from above the slit, top corners from
-// below), so the slit faces separate: slots 0-2 row j-1, 3-5 row j seen from the cells below,
-// 6-8 row j from the cells above, 9-11 row j+1.  Branch-free: row entries, then every input and
-// matrix load at once (absent nodes / cells read entry 0 with weight 0).  Cells are summed in the
-// fixed order below-left, below-right, above-left, above-right; xc = the input at the node.
-template <class M, class X>
-__device__ __forceinline__ double2 mg_gather(const DMesh& m, const double* K, int id, int i,
-                                             int j, X&& xval, double2& xc) {
-  const bool jm = j >= 1, jp = j + 1 <= m.ny;
-  const int4 rm = M::row(m.nrow, jm ? j - 1 : j), r0 = M::row(m.nrow, j);
-  const int4 rp = M::row(m.nrow, jp ? j + 1 : j);
-  const bool cm = j >= 1, c0 = j < m.ny;
-  const int4 em = M::row(m.erow, cm ? j - 1 : 0), e0 = M::row(m.erow, c0 ? j : 0);
-  int nid[12];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const int ii = i + a - 1;
-    nid[a] = jm ? mg_row_node(m, rm, ii, j - 1, true) : -1;
-    nid[3 + a] = mg_row_node(m, r0, ii, j, false);
-    nid[6 + a] = mg_row_node(m, r0, ii, j, true);
-    nid[9 + a] = jp ? mg_row_node(m, rp, ii, j + 1, false) : -1;
-  }
-  double2 xv[12];
-#pragma unroll
-  for (int sl = 0; sl < 12; ++sl) {
-    const int row = sl / 3;
-    const int jj = j + (row == 0 ? -1 : (row == 3 ? 1 : 0));
-    const int n = max(nid[sl], 0);
-    const double2 v = xval(n, i + (sl % 3) - 1, jj, mg_is_dup(m, n));
-    xv[sl] = nid[sl] >= 0 ? v : make_double2(0.0, 0.0);
-  }
-  const bool below = nid[4] == id, above = nid[7] == id;
-  xc = below ? xv[4] : xv[7];
-  auto cell = [&](int4 er, bool rv, int ci) -> int {
-    return (rv && ci >= er.x && ci < er.y) ? er.z + (ci - er.x) : -1;
-  };
-  const int ce[4] = {below ? cell(em, cm, i - 1) : -1, below ? cell(em, cm, i) : -1,
-                     above ? cell(e0, c0, i - 1) : -1, above ? cell(e0, c0, i) : -1};
-  const int ck[4] = {2, 3, 1, 0};
-  const int cs[4][4] = {{0, 1, 4, 3}, {1, 2, 5, 4}, {6, 7, 10, 9}, {7, 8, 11, 10}};
-  double ax = 0.0, ay = 0.0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int e = ce[q];
-    const double wq = e >= 0 ? 1.0 : 0.0;
-    const double* Kr = K + 64 * (size_t)max(e, 0) + 16 * ck[q];  // rows 2k, 2k+1
-    double sx = 0.0, sy = 0.0;
-#pragma unroll
-    for (int bq = 0; bq < 4; ++bq) {
-      const double2 v = xv[cs[q][bq]];
-      const double2 kx = M::v2(Kr, bq), ky = M::v2(Kr + 8, bq);
-      sx += kx.x * v.x + kx.y * v.y;
-      sy += ky.x * v.x + ky.y * v.y;
-    }
-    ax += wq * sx;
-    ay += wq * sy;
-  }
-  return make_double2(ax, ay);
-}
-
-// A view of one coarse level (global memory, or the tail kernel's shared-memory copy)
-struct LView {
-  DMesh m;
-  const double* K;
-  const double* dinv;
-  double* b;
-  double* t;
-  double* e;
-};
-__device__ __forceinline__ LView lview(const MgLevel& L) {
-  return LView{L.m, L.K, L.dinv, L.b, L.t, L.e};
-}
-
-// restriction b = P^T t_f (masked at dead dofs)
-template <class MF, class M>
-__device__ __forceinline__ void mg_restrict(const LView& L, const DMesh& mf, const double* tf,
-                                            int worker, int nw) {
-  mg_for_nodes<M>(L.m, worker, nw, [&](int id, int i, int j, bool dup) {
-    d2st(L.b, id, mask2(mg_restrict_at<MF>(mf, L.m, tf, i, j, dup), M::v2(L.dinv, id)));
-  });
-}
-// down-sweep residual t = b - A x with x = omega D^-1 b (one Jacobi sweep from zero)
-template <class M>
-__device__ __forceinline__ void mg_resid(const LView& L, double om, int worker, int nw) {
-  mg_for_nodes<M>(L.m, worker, nw, [&](int id, int i, int j, bool) {
-    auto xval = [&](int n, int, int, bool) -> double2 {
-      const double2 di = M::v2(L.dinv, n), bv = M::v2(L.b, n);
-      return make_double2(om * di.x * bv.x, om * di.y * bv.y);
-    };
-    double2 xc;
-    const double2 Av = mg_gather<M>(L.m, L.K, id, i, j, xval, xc);
-    const double2 di = M::v2(L.dinv, id), bv = M::v2(L.b, id);
-    d2st(L.t, id, mask2(make_double2(bv.x - Av.x, bv.y - Av.y), di));
-  });
-}
-// prolongation y = omega D^-1 b + P e_c (into t)
-template <class M, class MC>
-__device__ __forceinline__ void mg_prolongate(const LView& L, const DMesh& mc, const double* ec,
-                                              double om, int worker, int nw) {
-  mg_for_nodes<M>(L.m, worker, nw, [&](int id, int i, int j, bool dup) {
-    const double2 di = M::v2(L.dinv, id), bv = M::v2(L.b, id);
-    const double2 pe = mg_prolong<MC>(L.m, mc, ec, i, j, dup);
-    d2st(L.t, id, mask2(make_double2(om * di.x * bv.x + pe.x, om * di.y * bv.y + pe.y), di));
-  });
-}
-// post-smoothing e = y + omega D^-1 (b - A y), y in t; eout: where e goes
-template <class M>
-__device__ __forceinline__ void mg_smooth(const LView& L, double* eout, double om, int worker,
-                                          int nw) {
-  mg_for_nodes<M>(L.m, worker, nw, [&](int id, int i, int j, bool) {
-    auto xval = [&](int n, int, int, bool) -> double2 { return M::v2(L.t, n); };
-    double2 y;
-    const double2 Av = mg_gather<M>(L.m, L.K, id, i, j, xval, y);
-    const double2 di = M::v2(L.dinv, id), bv = M::v2(L.b, id);
-    d2st(eout, id, make_double2(y.x + om * di.x * (bv.x - Av.x), y.y + om * di.y * (bv.y - Av.y)));
-  });
-}
-// Jacobi sweep eout = ein + omega D^-1 (b - A ein)
-template <class M>
-__device__ __forceinline__ void mg_sweep(const LView& L, double om, const double* ein,
-                                         double* eout, int worker, int nw) {
-  mg_for_nodes<M>(L.m, worker, nw, [&](int id, int i, int j, bool) {
-    auto xval = [&](int n, int, int, bool) -> double2 { return M::v2(ein, n); };
-    double2 x;
-    const double2 Av = mg_gather<M>(L.m, L.K, id, i, j, xval, x);
-    const double2 di = M::v2(L.dinv, id), bv = M::v2(L.b, id);
-    d2st(eout, id, make_double2(x.x + om * di.x * (bv.x - Av.x), x.y + om * di.y * (bv.y - Av.y)));
-  });
-}
 // ---- coarse levels in assembled form: one thread per node, slot-major index and stencil
 // arrays, every load independent (two dependent rounds: indices, then values) -------------------
 __device__ __forceinline__ double mg_rw(int s) {  // restriction weight of slot s
@@ -594,9 +425,10 @@ __device__ __forceinline__ double mg_rw(int s) {  // restriction weight of slot 
 // Node-parallel kernels of the assembled form: a half-warp per node, one lane per stencil /
 // restriction / prolongation slot, so every index and value load of a node is in flight at
 // once (two dependent rounds); the half-warp sum is a fixed butterfly (bit-reproducible).
-__device__ __forceinline__ double2 hw_sum(double2 v) {
+template <int W = 16>
+__device__ __forceinline__ double2 hw_sum(double2 v) {  // butterfly over W aligned lanes
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) {
+  for (int o = W / 2; o > 0; o >>= 1) {
     v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
     v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
   }
@@ -615,7 +447,7 @@ __device__ __forceinline__ double2 mg_slot_apply(const MgLevel& L, int n, int id
   const double2 x = xval(k);
   return make_double2(sxx * x.x + sxy * x.y, syx * x.x + syy * x.y);
 }
-// LPN lanes per node (16: small levels, every load of a node in flight at once; 1: large
+// LPN lanes per node (16: small levels, every load of a node in flight at once; 4 / 1: larger
 // levels, latency hidden by the many resident warps).  Slot partial sums are combined in a
 // fixed order either way (bit-reproducible).
 template <int LPN>
@@ -623,8 +455,10 @@ struct NodeMap {
   __device__ static int lane() { return LPN == 1 ? 0 : (int)(threadIdx.x & (LPN - 1)); }
   __device__ static int first() { return (int)((blockIdx.x * blockDim.x + threadIdx.x) / LPN); }
   __device__ static int stride() { return (int)((gridDim.x * blockDim.x) / LPN); }
-  __device__ static int end(int n) { return LPN == 1 ? n : ((n + 1) >> 1) << 1; }  // warp-uniform
-  __device__ static double2 sum(double2 v) { return LPN == 1 ? v : hw_sum(v); }
+  __device__ static int end(int n) {  // warp-uniform trip counts (32 / LPN nodes per warp)
+    return LPN == 1 ? n : ((n + 32 / LPN - 1) / (32 / LPN)) * (32 / LPN);
+  }
+  __device__ static double2 sum(double2 v) { return LPN == 1 ? v : hw_sum<LPN>(v); }
 };
 template <int LPN, class X>
 __device__ __forceinline__ double2 mg_apply(const MgLevel& L, int n, int id, X&& xval) {
@@ -931,90 +765,251 @@ __global__ void __launch_bounds__(MG_NT) k_mg_jacobi0(MgArgs A, int l, double* o
        i += (long long)gridDim.x * blockDim.x)
     out[i] = om * __ldcg(L.dinv + i) * __ldcg(L.b + i);
 }
-// Tail: levels [n_tail, n_levels) staged in dynamic shared memory (row tables, cell matrices,
-// inverse diagonals, the dense coarsest inverse) and cycled by one CTA with CTA barriers:
-// restriction from level n_tail - 1 (global) down to the coarsest solve and back up to
-// e_{n_tail} (global).  Offsets (bytes) come from the host (MgArgs::ts).
+// Tail: levels [n_tail, n_levels) in assembled form staged in dynamic shared memory
+// (neighbour / restriction / prolongation tables, stencils, inverse diagonals, the dense
+// coarsest inverse) and cycled by one CTA with CTA barriers, a half-warp per node: from the
+// restriction of level n_tail - 1's residual (global) down to the coarsest solve and back up
+// to e_{n_tail} (global).  Byte offsets come from the host (MgArgs::ts).
 extern __shared__ __align__(16) unsigned char mg_tail_smem[];
-__device__ __forceinline__ LView mg_tail_view(const MgArgs& A, int l) {
+struct TLevel {  // shared-memory view of one tail level
+  int n;
+  const int *nbr, *rid, *pid;
+  const double *S, *dinv;
+  double *b, *t, *e;
+};
+__device__ __forceinline__ TLevel mg_tl(const MgArgs& A, int l) {
   unsigned char* sm = mg_tail_smem;
-  const MgTailSlot& t = A.ts[l];
-  LView v;
-  v.m = A.L[l].m;
-  v.m.nrow = reinterpret_cast<const int4*>(sm + t.nrow);
-  v.m.erow = reinterpret_cast<const int4*>(sm + t.erow);
-  v.K = reinterpret_cast<const double*>(sm + t.K);
-  v.dinv = reinterpret_cast<const double*>(sm + t.dinv);
-  v.b = reinterpret_cast<double*>(sm + t.b);
-  v.t = reinterpret_cast<double*>(sm + t.t);
-  v.e = reinterpret_cast<double*>(sm + t.e);
+  const MgTailSlot& o = A.ts[l];
+  TLevel v;
+  v.n = A.L[l].m.n_nodes;
+  v.nbr = reinterpret_cast<const int*>(sm + o.nbr);
+  v.rid = reinterpret_cast<const int*>(sm + o.rid);
+  v.pid = reinterpret_cast<const int*>(sm + o.pid);
+  v.S = reinterpret_cast<const double*>(sm + o.S);
+  v.dinv = reinterpret_cast<const double*>(sm + o.dinv);
+  v.b = reinterpret_cast<double*>(sm + o.b);
+  v.t = reinterpret_cast<double*>(sm + o.t);
+  v.e = reinterpret_cast<double*>(sm + o.e);
   return v;
 }
-__device__ __forceinline__ void mg_stage(void* dst, const void* src, size_t bytes) {
-  const int4* s4 = reinterpret_cast<const int4*>(src);
-  int4* d4 = reinterpret_cast<int4*>(dst);
-  for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) d4[i] = __ldcg(s4 + i);
+// TMA bulk copies global -> shared completing on one mbarrier (sizes and addresses are
+// multiples of 16 B: the host pads every multigrid array)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
 }
-__global__ void __launch_bounds__(MG_TAIL_NT) k_mg_tail(MgArgs A) {
-  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nl = A.n_levels, l0 = A.n_tail, c = nl - 1;
-  for (int l = l0; l < nl; ++l) {
-    const LView v = mg_tail_view(A, l);
-    const MgLevel& G = A.L[l];
-    mg_stage((void*)v.m.nrow, G.m.nrow, sizeof(int4) * (G.m.ny + 1));
-    mg_stage((void*)v.m.erow, G.m.erow, sizeof(int4) * G.m.ny);
-    mg_stage((void*)v.K, G.K, sizeof(double) * 64 * (size_t)G.m.n_elems);
-    mg_stage((void*)v.dinv, G.dinv, sizeof(double) * 2 * (size_t)G.m.n_nodes);
+__device__ __forceinline__ void mg_bulk_g2s(const void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mg_mbar_init_expect(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mg_mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ unsigned mg_r16(size_t b) { return (unsigned)((b + 15) & ~size_t(15)); }
+__device__ __forceinline__ double2 ts2(const double* p, int i) {
+  return reinterpret_cast<const double2*>(p)[i];
+}
+// S x at node id of a tail level: 4 lanes per node, lane q takes slots q, q+4, q+8
+template <class X>
+__device__ __forceinline__ double2 mg_tapply(const TLevel& L, int id, X&& xval) {
+  const int q = threadIdx.x & 3, n = L.n;
+  double2 v = make_double2(0.0, 0.0);
+  if (id < n) {
+#pragma unroll
+    for (int s2 = q; s2 < MG_NS; s2 += 4) {
+      const int k = L.nbr[s2 * n + id];
+      if (k >= 0) {
+        const double* Sp = L.S + (4 * s2) * n + id;
+        const double2 x = xval(k);
+        v.x += Sp[0] * x.x + Sp[n] * x.y;
+        v.y += Sp[2 * n] * x.x + Sp[3 * n] * x.y;
+      }
+    }
   }
+  return hw_sum<4>(v);
+}
+#define MG_TAIL_NODES(n) \
+  for (int id = threadIdx.x >> 2, _e = (((n) + 7) >> 3) << 3; id < _e; id += blockDim.x >> 2)
+constexpr int MG_TAIL_PASS = MG_TAIL_NT / 4;  // nodes per pass
+
+__global__ void __launch_bounds__(MG_TAIL_NT) k_mg_tail(MgArgs A) {
+  const int nl = A.n_levels, l0 = A.n_tail, c = nl - 1;
+  const int q = threadIdx.x & 3;
+  int tk = 0;
+  auto TCLK = [&]() {
+    if (A.tclk && threadIdx.x == 0 && tk < 32) A.tclk[tk++] = clock64();
+  };
+  TCLK();
   const int nd = 2 * A.L[c].m.n_nodes;
   double* Ainv = reinterpret_cast<double*>(mg_tail_smem + A.ts_ainv);
-  if (A.dense) mg_stage(Ainv, A.Ainv, sizeof(double) * nd * nd);
+  __shared__ __align__(8) unsigned long long bar;
+  if (threadIdx.x == 0) {  // stage the tables and this hierarchy's operators with TMA bulk copies
+    unsigned total = 0;
+    for (int l = l0; l < nl; ++l) {
+      const size_t n = A.L[l].m.n_nodes;
+      total += mg_r16(4 * MG_NS * n) + mg_r16(4 * 12 * n) + (l < c ? mg_r16(4 * 4 * n) : 0) +
+               mg_r16(8 * 4 * MG_NS * n) + mg_r16(16 * n);
+    }
+    if (A.dense) total += mg_r16(8 * (size_t)nd * nd);
+    mg_mbar_init_expect(&bar, total);
+    for (int l = l0; l < nl; ++l) {
+      const TLevel v = mg_tl(A, l);
+      const MgLevel& G = A.L[l];
+      const size_t n = v.n;
+      mg_bulk_g2s(v.nbr, G.nbr, mg_r16(4 * MG_NS * n), &bar);
+      mg_bulk_g2s(v.rid, G.rid, mg_r16(4 * 12 * n), &bar);
+      if (l < c) mg_bulk_g2s(v.pid, G.pid, mg_r16(4 * 4 * n), &bar);
+      mg_bulk_g2s(v.S, G.S, mg_r16(8 * 4 * MG_NS * n), &bar);
+      mg_bulk_g2s(v.dinv, G.dinv, mg_r16(16 * n), &bar);
+    }
+    if (A.dense) mg_bulk_g2s(Ainv, A.Ainv, mg_r16(8 * (size_t)nd * nd), &bar);
+  }
+  __shared__ double om_s[MG_MAXL];
+  if (threadIdx.x < MG_MAXL) om_s[threadIdx.x] = __ldcg(&A.ctl->omega[threadIdx.x]);
+  // restriction sources of level n_tail (global memory), loaded while the bulk copies fly:
+  // pass p, slot q + 4 k of node (threadIdx.x >> 2) + p * MG_TAIL_PASS
+  double2 tg[MG_TAIL_P][3];
+  {
+    const MgLevel& G0 = A.L[l0];
+    const int n0 = G0.m.n_nodes;
+    const double* tf = A.L[l0 - 1].t;
+#pragma unroll
+    for (int p = 0; p < MG_TAIL_P; ++p)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int id = (threadIdx.x >> 2) + p * MG_TAIL_PASS, s2 = q + 4 * k;
+        const int f = (s2 < 12 && id < n0) ? __ldg(G0.rid + s2 * n0 + id) : -1;
+        tg[p][k] = f >= 0 ? GMem::v2(tf, f) : make_double2(0.0, 0.0);
+      }
+  }
   __syncthreads();
-  for (int l = l0; l < nl; ++l) {
-    const LView v = mg_tail_view(A, l);
-    if (l == l0) mg_restrict<GMem, SMem>(v, A.L[l - 1].m, A.L[l - 1].t, w, nw);
-    else {
-      const LView f = mg_tail_view(A, l - 1);
-      mg_restrict<SMem, SMem>(v, f.m, f.t, w, nw);
+  mg_mbar_wait(&bar, 0);
+  TCLK();
+  for (int l = l0; l <= c; ++l) {
+    const TLevel v = mg_tl(A, l);
+    const int n = v.n;
+    const double* tf = l == l0 ? nullptr : mg_tl(A, l - 1).t;  // l0 - 1: pre-loaded in tg
+    int pass = 0;
+    MG_TAIL_NODES(n) {  // b = P^T t_f
+      double2 r = make_double2(0.0, 0.0);
+      if (id < n) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int s2 = q + 4 * k;
+          if (s2 >= 12) break;
+          const int f = v.rid[s2 * n + id];
+          if (f < 0) continue;
+          double2 t = make_double2(0.0, 0.0);
+          if (l == l0) {
+#pragma unroll
+            for (int p = 0; p < MG_TAIL_P; ++p)
+              if (p == pass) t = tg[p][k];
+          } else {
+            t = ts2(tf, f);
+          }
+          const double w = mg_rw(s2);
+          r.x += w * t.x;
+          r.y += w * t.y;
+        }
+      }
+      ++pass;
+      r = hw_sum<4>(r);
+      if (q == 0 && id < n) d2st(v.b, id, mask2(r, ts2(v.dinv, id)));
     }
     __syncthreads();
-    if (l < c) {
-      mg_resid<SMem>(v, __ldcg(&A.ctl->omega[l]), w, nw);
-      __syncthreads();
+    TCLK();
+    if (l == c) break;
+    const double om = om_s[l];
+    MG_TAIL_NODES(n) {  // t = b - A (omega D^-1 b)
+      const double2 Av = mg_tapply(v, id, [&](int k) -> double2 {
+        const double2 di = ts2(v.dinv, k), bv = ts2(v.b, k);
+        return make_double2(om * di.x * bv.x, om * di.y * bv.y);
+      });
+      if (q == 0 && id < n) {
+        const double2 di = ts2(v.dinv, id), bv = ts2(v.b, id);
+        d2st(v.t, id, mask2(make_double2(bv.x - Av.x, bv.y - Av.y), di));
+      }
     }
+    __syncthreads();
+    TCLK();
   }
   {  // coarsest solve
-    const LView v = mg_tail_view(A, c);
+    const TLevel v = mg_tl(A, c);
     if (A.dense) {
       for (int i = threadIdx.x; i < nd; i += blockDim.x) {
-        double s = 0.0;
-        for (int j = 0; j < nd; ++j) s += Ainv[i * nd + j] * v.b[j];
-        v.e[i] = s;
+        double sacc = 0.0;
+        for (int j = 0; j < nd; ++j) sacc += Ainv[i * nd + j] * v.b[j];
+        v.e[i] = sacc;
       }
       __syncthreads();
     } else {
-      const double om = __ldcg(&A.ctl->omega[c]);
+      const double om = om_s[c];
       double* bufs[2] = {v.e, v.t};
       int cur = (A.nu_c - 1) % 2 == 0 ? 0 : 1;  // the last sweep lands in e
       for (int i = threadIdx.x; i < nd; i += blockDim.x) bufs[cur][i] = om * v.dinv[i] * v.b[i];
       __syncthreads();
-      for (int s2 = 1; s2 < A.nu_c; ++s2) {
-        mg_sweep<SMem>(v, om, bufs[cur], bufs[cur ^ 1], w, nw);
+      for (int sw = 1; sw < A.nu_c; ++sw) {
+        const double* in = bufs[cur];
+        double* out = bufs[cur ^ 1];
+        MG_TAIL_NODES(v.n) {
+          const double2 Ax = mg_tapply(v, id, [&](int k) -> double2 { return ts2(in, k); });
+          if (q == 0 && id < v.n) {
+            const double2 x = ts2(in, id), di = ts2(v.dinv, id), bv = ts2(v.b, id);
+            d2st(out, id, make_double2(x.x + om * di.x * (bv.x - Ax.x), x.y + om * di.y * (bv.y - Ax.y)));
+          }
+        }
         cur ^= 1;
         __syncthreads();
       }
     }
+    TCLK();
     if (l0 == c)  // only the coarsest level in the tail: hand its result to the grid
       for (int i = threadIdx.x; i < nd; i += blockDim.x) A.L[c].e[i] = v.e[i];
   }
   for (int l = c - 1; l >= l0; --l) {
-    const LView v = mg_tail_view(A, l);
-    const LView cv = mg_tail_view(A, l + 1);
-    const double om = __ldcg(&A.ctl->omega[l]);
-    mg_prolongate<SMem, SMem>(v, cv.m, cv.e, om, w, nw);
+    const TLevel v = mg_tl(A, l), vc = mg_tl(A, l + 1);
+    const int n = v.n;
+    const double om = om_s[l];
+    MG_TAIL_NODES(n) {  // y = omega D^-1 b + P e_c (into t)
+      double2 r = make_double2(0.0, 0.0), cnt = make_double2(0.0, 0.0);
+      if (id < n) {
+        const int k = v.pid[q * n + id];
+        if (k >= 0) {
+          r = ts2(vc.e, k);
+          cnt.x = 1.0;
+        }
+      }
+      r = hw_sum<4>(r);
+      cnt = hw_sum<4>(cnt);
+      if (q == 0 && id < n) {
+        const double w = 1.0 / cnt.x;
+        const double2 di = ts2(v.dinv, id), bv = ts2(v.b, id);
+        d2st(v.t, id, mask2(make_double2(om * di.x * bv.x + w * r.x, om * di.y * bv.y + w * r.y), di));
+      }
+    }
     __syncthreads();
-    mg_smooth<SMem>(v, l == l0 ? A.L[l].e : v.e, om, w, nw);
+    TCLK();
+    double* eout = (l == l0) ? A.L[l].e : v.e;
+    MG_TAIL_NODES(n) {  // e = y + omega D^-1 (b - A y)
+      const double2 Ay = mg_tapply(v, id, [&](int k) -> double2 { return ts2(v.t, k); });
+      if (q == 0 && id < n) {
+        const double2 y = ts2(v.t, id), di = ts2(v.dinv, id), bv = ts2(v.b, id);
+        d2st(eout, id, make_double2(y.x + om * di.x * (bv.x - Ay.x), y.y + om * di.y * (bv.y - Ay.y)));
+      }
+    }
     __syncthreads();
+    TCLK();
   }
 }
 
