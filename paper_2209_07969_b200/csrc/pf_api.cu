@@ -628,14 +628,16 @@ static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
   A.L[0].e = A.z;
   const int ndc = 2 * lv.back().n_nodes;
   if (A.dense && mg_alloc(h, &A.Ainv, (size_t)ndc * ndc) != cudaSuccess) return oom();
-  const size_t npart = std::max<size_t>((size_t)2 * h->mg_gf + h->mg_gflat,
-                                        (size_t)h->mg_gflat * 2 * pfb::MG_MAXL);
+  const size_t npart = std::max<size_t>(
+      std::max<size_t>((size_t)2 * h->mg_gf + h->mg_gflat, (size_t)h->mg_gflat * 2 * pfb::MG_MAXL),
+      (size_t)pfb::MG_WP * h->mg_gf + h->mg_gflat);
   if (mg_alloc(h, &A.part, npart) != cudaSuccess || mg_alloc(h, &A.ctl, 1) != cudaSuccess)
     return oom();
-  if (cudaHostAlloc((void**)&h->mg_in, sizeof(pfb::MgIn), cudaHostAllocMapped) != cudaSuccess)
+  // per-solve inputs: written on the host (pinned), copied to the device before each solve
+  if (cudaHostAlloc((void**)&h->mg_in, sizeof(pfb::MgIn), cudaHostAllocDefault) != cudaSuccess)
     return oom();
   pfb::MgIn* din = nullptr;
-  cudaHostGetDevicePointer((void**)&din, h->mg_in, 0);
+  if (mg_alloc(h, &din, 1) != cudaSuccess) return oom();
   A.in = din;
   A.d = h->d;
   A.flags = h->flags;
@@ -719,7 +721,8 @@ static pf_status mg_build_graphs(pf_handle* h) {
     cudaGraph_t g = nullptr;
     A.use_cond = 0;
     PF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    pfb::k_mg_init<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A);
+    for (int k = 0; k < pfb::MG_WARM; ++k) pfb::k_mg_warm_q<<<h->mg_gf, pfb::MG_NT, 0, s>>>(A, k);
+    pfb::k_mg_init<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A, h->mg_gf);
     for (int it = 0; it < unroll; ++it) body_kernels(A);
     pfb::k_mg_finish<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A);
     PF_CUDA(cudaStreamEndCapture(s, &g));
@@ -736,14 +739,20 @@ static pf_status mg_build_graphs(pf_handle* h) {
     cudaGraphNode_t n_init = nullptr, n_while = nullptr, n_fin = nullptr;
     {
       PF_CUDA(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-      pfb::k_mg_init<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A);
+      for (int k = 0; k < pfb::MG_WARM; ++k) pfb::k_mg_warm_q<<<h->mg_gf, pfb::MG_NT, 0, s>>>(A, k);
+      pfb::k_mg_init<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A, h->mg_gf);
       cudaGraph_t gg = g;
       PF_CUDA(cudaStreamEndCapture(s, &gg));
       size_t nn = 0;
       PF_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
       std::vector<cudaGraphNode_t> nodes(nn);
       PF_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
-      n_init = nodes[0];
+      for (cudaGraphNode_t nd : nodes) {  // the WHILE node follows k_mg_init
+        cudaKernelNodeParams kp{};
+        if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func == (void*)pfb::k_mg_init)
+          n_init = nd;
+      }
+      if (!n_init) return fail(h, PF_ERR_CUDA, "MG solve graph: init node not found");
     }
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
@@ -1063,7 +1072,8 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
       if (om >= 1) {
         pf_status ms = mg_setup(h, om * dev_sms * pfb::MG_WARPS);
         if (ms != PF_OK) return bail(ms);
-        if (h->mg) h->warm = false;  // the MG solves start cold (x0 = 0, like the reference CG)
+        const char* mw = getenv("PFB200_MG_WARM");  // "0": MG solves start cold (x0 = 0)
+        if (h->mg && mw && std::string(mw) == "0") h->warm = false;
         const char* ru = getenv("PFB200_MG_REUSE");
         h->mg_reuse = !(ru && std::string(ru) == "0");
       }
@@ -1626,7 +1636,10 @@ static pf_status run_cg_dist(pf_handle* h, bool mom, double* target, bool probe,
 // PCG loop is a device-side WHILE node; the host waits once, at the end
 static pf_status run_mg(pf_handle* h, double* target, int* status, long long* iters,
                         int setup_only = 0, long long maxiter = -1, double rtol = -1.0,
-                        bool check = true, bool force_setup = false) {
+                        bool check = true, bool force_setup = false,
+                        double* const* guess = nullptr, int n_guess = 0) {
+  h->mg_in->n_guess = std::min(n_guess, pfb::MG_WARM);
+  for (int k = 0; k < pfb::MG_WARM; ++k) h->mg_in->guess[k] = k < h->mg_in->n_guess ? guess[k] : nullptr;
   h->mg_in->rtol = rtol >= 0.0 ? rtol : h->cfg.cg_rtol;
   h->mg_in->maxiter = maxiter > 0 ? maxiter
                                   : (long long)h->cfg.cg_maxiter_factor * 2LL * h->n_nodes;
@@ -1635,6 +1648,8 @@ static pf_status run_mg(pf_handle* h, double* target, int* status, long long* it
                        h->mg_age >= h->mg_max_age ||
                        h->mg_last_iters > (h->mg_ref_iters * 5) / 4 + 2;
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
+  PF_CUDA(cudaMemcpyAsync((void*)h->mga.in, h->mg_in, sizeof(pfb::MgIn), cudaMemcpyHostToDevice,
+                          h->stream));
   if (rebuild) {
     PF_CUDA(cudaGraphLaunch(h->mg_setup_exec, h->stream));
     PF_TRY(launched(h));
@@ -1675,7 +1690,8 @@ static pf_status run_mg(pf_handle* h, double* target, int* status, long long* it
 
 static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
                         long long* iters, double* const* guess = nullptr, int n_guess = 0) {
-  if (mom && h->mg && !probe) return run_mg(h, target, status, iters);
+  if (mom && h->mg && !probe)
+    return run_mg(h, target, status, iters, 0, -1, -1.0, true, false, guess, n_guess);
   if (h->comm) return run_cg_dist(h, mom, target, probe, status, iters);
   return h->split ? run_cg_split(h, mom, target, probe, status, iters)
                   : run_cg_persistent(h, mom, target, probe, status, iters, guess, n_guess);

@@ -58,10 +58,13 @@ struct MgLevel {
 };
 
 // device-side control block of one solve
-struct MgIn {  // per-solve inputs, in mapped pinned host memory (read by k_mg_init)
+constexpr int MG_WARM = 3;  // warm-start directions (backward-difference table, pf_cg.cuh)
+struct MgIn {  // per-solve inputs (device copy of a pinned host struct, refreshed per solve)
   double rtol;
   long long maxiter;
-  double* target;  // optional: target += x at the end
+  double* target;                 // optional: target += x at the end
+  const double* guess[MG_WARM];   // warm start: x0 = sum y_k guess[k], Galerkin-optimal y
+  int n_guess;
 };
 struct MgCtl {
   double omega[MG_MAXL];
@@ -345,6 +348,34 @@ struct FineSmooth : FineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 
                                     y.y + om * dv.y * (bv.y - Av.y));
     d2st(z, id, ev);
     *rz += bv.x * ev.x + bv.y * ev.y;
+  }
+};
+
+struct FineWarm : FineBase {  // q_k = A u_k (masked); u_j.q_k (j <= k), u_k.b (b = r on entry)
+  const double* u;
+  double* qk;
+  const double* uj[MG_WARM];
+  int k;
+  const double* b;
+  double* acc;  // [MG_WARM + 2]: u_0.q_k .. u_k.q_k, u_k.b, b.b
+  __device__ double2 in(int id, int, int, bool, double& aux) const {
+    aux = 0.0;
+    if (id < 0) return make_double2(0.0, 0.0);
+    aux = __ldg(d + id);
+    return mask2(__ldg(reinterpret_cast<const double2*>(u) + id), di(id));
+  }
+  __device__ void out(int id, double2 Av, double2 uv) const {
+    const double2 qv = mask2(Av, di(id));
+    d2st(qk, id, qv);
+#pragma unroll
+    for (int j = 0; j < MG_WARM; ++j) {
+      if (j > k) break;
+      const double2 a = j == k ? uv : mask2(__ldg(reinterpret_cast<const double2*>(uj[j]) + id), di(id));
+      acc[j] += a.x * qv.x + a.y * qv.y;
+    }
+    const double2 bv = __ldg(reinterpret_cast<const double2*>(b) + id);
+    acc[MG_WARM] += uv.x * bv.x + uv.y * bv.y;
+    if (k == 0) acc[MG_WARM + 1] += bv.x * bv.x + bv.y * bv.y;
   }
 };
 
@@ -705,27 +736,124 @@ __device__ __forceinline__ bool mg_publish(double (&v)[NV], double* part, unsign
 // ================================================================================================
 // kernels of one solve: k_mg_init, WHILE { fine resid, (restrict, resid) per grid level, tail,
 // (prolongate, smooth) per grid level, fine smooth, pcg, update }, k_mg_finish
-__global__ void __launch_bounds__(MG_NT) k_mg_init(MgArgs A) {
-  __shared__ double red[MG_WARPS];
+// warm start, step 1 (k = 0 .. MG_WARM-1): q_k = A u_k over the fine march, with the Gram
+// partials u_j.q_k (j <= k), u_k.b and b.b; the guesses come from the mapped per-solve inputs
+// (a kernel with k >= n_guess does nothing).  Partials: [CTA][MG_WARM * (MG_WARM + 1) / 2 + 4].
+constexpr int MG_WP = MG_WARM * (MG_WARM + 1) / 2 + MG_WARM + 1;
+__device__ __forceinline__ int mg_gidx(int j, int k) { return k * (k + 1) / 2 + j; }  // j <= k
+__device__ __forceinline__ double* mg_warm_q(const MgArgs& A, int k) {
+  return k == 0 ? A.L[0].t : (k == 1 ? A.z : A.q);
+}
+__global__ void __launch_bounds__(MG_NT, 2) k_mg_warm_q(MgArgs A, int k) {
+  __shared__ MgWarp ws[MG_WARPS];
+  __shared__ double red[MG_WARPS * (MG_WARM + 2)];
+  const MgIn* in = A.in;
+  if (k >= __ldg(&in->n_guess)) return;
+  double acc[MG_WARM + 2];
+#pragma unroll
+  for (int j = 0; j < MG_WARM + 2; ++j) acc[j] = 0.0;
+  FineWarm op{{&A.C, A.flags, A.d, A.L[0].dinv}, (const double*)in->guess[k], mg_warm_q(A, k),
+              {(const double*)in->guess[0], (const double*)in->guess[1], (const double*)in->guess[2]},
+              k, A.r, acc};
+  const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
+  if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
+  mg_block_sum<MG_WARM + 2>(acc, red);
+  if (threadIdx.x == 0) {
+    double* p = A.part + (size_t)MG_WP * blockIdx.x;
+#pragma unroll
+    for (int j = 0; j < MG_WARM; ++j)
+      if (j <= k) p[mg_gidx(j, k)] = acc[j];
+    p[MG_WARM * (MG_WARM + 1) / 2 + k] = acc[MG_WARM];
+    if (k == 0) p[MG_WP - 1] = acc[MG_WARM + 1];
+  }
+}
+
+// solve init: x0 = U y with (U^T A U) y = U^T b (pivot-dropping Cholesky, identical in every
+// CTA), r0 = b - sum y_k q_k; x0 = 0 without guesses.  ||b|| is the original right-hand side's
+// (scipy: rtol * ||b||).  The last CTA sets the control block and the WHILE condition.
+__global__ void __launch_bounds__(MG_NT) k_mg_init(MgArgs A, int n_wparts) {
+  __shared__ double red[MG_WP];
+  const MgIn* in = A.in;
+  const int m = __ldg(&in->n_guess);
+  double y[MG_WARM] = {0.0, 0.0, 0.0};
+  double bb = -1.0;
+  if (m > 0) {
+    double g[MG_WP];
+    mg_all_reduce<MG_WP>(A.part, n_wparts, red, g);
+    bb = g[MG_WP - 1];
+    double G[MG_WARM][MG_WARM], c[MG_WARM], L[MG_WARM][MG_WARM], z[MG_WARM];
+    bool keep[MG_WARM];
+#pragma unroll
+    for (int i = 0; i < MG_WARM; ++i) {
+      c[i] = i < m ? g[MG_WARM * (MG_WARM + 1) / 2 + i] : 0.0;
+#pragma unroll
+      for (int j = 0; j < MG_WARM; ++j) {
+        G[i][j] = (i < m && j < m) ? g[mg_gidx(min(i, j), max(i, j))] : 0.0;
+        L[i][j] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MG_WARM; ++i) {
+      double dd = G[i][i];
+#pragma unroll
+      for (int k = 0; k < i; ++k) dd -= L[i][k] * L[i][k];
+      keep[i] = i < m && G[i][i] > 0.0 && dd > 1e-6 * G[i][i];
+      const double lii = keep[i] ? sqrt(dd) : 1.0;
+      L[i][i] = keep[i] ? lii : 0.0;
+#pragma unroll
+      for (int j = i + 1; j < MG_WARM; ++j) {
+        double e = G[j][i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) e -= L[j][k] * L[i][k];
+        L[j][i] = keep[i] ? e / lii : 0.0;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MG_WARM; ++i) {
+      double e = c[i];
+#pragma unroll
+      for (int k = 0; k < i; ++k) e -= L[i][k] * z[k];
+      z[i] = keep[i] ? e / L[i][i] : 0.0;
+    }
+#pragma unroll
+    for (int i = MG_WARM - 1; i >= 0; --i) {
+      double e = z[i];
+#pragma unroll
+      for (int k = i + 1; k < MG_WARM; ++k) e -= L[k][i] * y[k];
+      y[i] = keep[i] ? e / L[i][i] : 0.0;
+    }
+  }
   double rr = 0.0;
+  const double* u0 = m > 0 ? (const double*)in->guess[0] : nullptr;
+  const double* u1 = m > 1 ? (const double*)in->guess[1] : nullptr;
+  const double* u2 = m > 2 ? (const double*)in->guess[2] : nullptr;
+  const double* q0 = mg_warm_q(A, 0);
+  const double* q1 = mg_warm_q(A, 1);
+  const double* q2 = mg_warm_q(A, 2);
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < A.ndof;
        i += (long long)gridDim.x * blockDim.x) {
-    const double v = __ldcg(A.r + i);
-    rr += v * v;
-    A.x[i] = 0.0;
+    double rv = __ldcg(A.r + i), xv = 0.0;
+    if (m > 0 && __ldg(A.L[0].dinv + i) != 0.0) {
+      xv = y[0] * __ldg(u0 + i);
+      rv -= y[0] * __ldcg(q0 + i);
+      if (u1) { xv += y[1] * __ldg(u1 + i); rv -= y[1] * __ldcg(q1 + i); }
+      if (u2) { xv += y[2] * __ldg(u2 + i); rv -= y[2] * __ldcg(q2 + i); }
+      A.r[i] = rv;
+    }
+    A.x[i] = xv;
+    rr += rv * rv;
   }
   double v[1] = {rr};
-  if (mg_publish<1>(v, A.part, &A.ctl->count, red)) {
+  if (mg_publish<1>(v, A.part + (size_t)MG_WP * n_wparts, &A.ctl->count, red)) {
     double tot[1];
-    mg_all_reduce<1>(A.part, gridDim.x, red, tot);
+    mg_all_reduce<1>(A.part + (size_t)MG_WP * n_wparts, gridDim.x, red, tot);
     if (threadIdx.x == 0) {
       MgCtl& c = *A.ctl;
       c.count = 0;
       c.rr = tot[0];
-      const volatile MgIn* in = A.in;
       c.maxiter = in->maxiter;
       c.target = in->target;
-      c.bnorm = sqrt(tot[0]);
+      c.bnorm = sqrt(m > 0 ? bb : tot[0]);
       c.atol = in->rtol * c.bnorm;
       c.k = 0;
       c.rho_prev = 0.0;
