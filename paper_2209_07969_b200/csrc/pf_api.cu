@@ -77,6 +77,11 @@ struct pf_handle {
   int warm_depth = 3;
   double* warm_buf[WARM_SLOTS][pfb::WARM_MAX] = {};
   int warm_n[WARM_SLOTS] = {};
+  // phase-field solves without the SPD probe (no gated Gauss point, or ST): the same
+  // difference tables, per staggered pass (1, 2, >= 3)
+  static constexpr int WARM_SLOTS_D = 3;
+  double* warm_d[WARM_SLOTS_D][pfb::WARM_MAX] = {};
+  int warm_nd[WARM_SLOTS_D] = {};
   bool xupd_mom = false, xupd_evo = false;  // lazy-x PCG variants (k_cg<MOM, true>)
   double* stage = nullptr;  // pinned host staging buffer for state transfers
   size_t stage_cap = 0;     // doubles
@@ -247,6 +252,9 @@ extern "C" void pf_destroy(pf_handle* h) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& row : h->warm_buf)
+    for (double* p : row)
+      if (p) cudaFree(p);
+  for (auto& row : h->warm_d)
     for (double* p : row)
       if (p) cudaFree(p);
   for (void* p : h->mg_allocs)
@@ -969,6 +977,9 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
     if (h->warm)
       for (int sl = 0; sl < pf_handle::WARM_SLOTS; ++sl)
         for (int k = 0; k < h->warm_depth; ++k) CREATE_ALLOC(h->warm_buf[sl][k], 2 * nn);
+    if (h->warm)
+      for (int sl = 0; sl < pf_handle::WARM_SLOTS_D; ++sl)
+        for (int k = 0; k < h->warm_depth; ++k) CREATE_ALLOC(h->warm_d[sl][k], nn);
     const char* tr = getenv("PFB200_TRACE");
     h->trace = tr && std::string(tr) == "1";
   }
@@ -1789,7 +1800,8 @@ static pf_status momentum(pf_handle* h, const BcView& bc, bool apply_inc, double
 }
 
 // solve_evolution (schemes.py:242-313)
-static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, int* fallbacks) {
+static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, int* fallbacks,
+                           int pass = 0) {
   const pf_config& cfg = h->cfg;
   int n_nr = 0;
   for (int it = 0; it <= cfg.max_nr; ++it) {
@@ -1846,7 +1858,22 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
       PF_TRY(halo(h, h->xd, 1));
       PF_TRY(axpy(h, h->d, h->xd, h->n_nodes));
     } else {
-      PF_TRY(run_cg(h, false, h->d, false, &status, &iters));
+      // warm start of the first Newton step from the previous solves of the same staggered
+      // pass (no SPD probe here: the system is K_dd without K~)
+      const int ws = std::min(std::max(pass - 1, 0), pf_handle::WARM_SLOTS_D - 1);
+      const bool use_warm = h->warm && n_nr == 0 && pass > 0;
+      double* guess[pfb::WARM_MAX] = {};
+      const int ng = use_warm ? h->warm_nd[ws] : 0;
+      for (int k = 0; k < ng; ++k) guess[k] = h->warm_d[ws][k];
+      PF_TRY(run_cg(h, false, h->d, false, &status, &iters, guess, ng));
+      if (use_warm) {
+        pfb::WarmTable t{};
+        for (int k = 0; k < h->warm_depth; ++k) t.d[k] = h->warm_d[ws][k];
+        pfb::k_warm_push<<<4 * h->sm_count, 256, 0, h->stream>>>(t, h->warm_nd[ws], h->warm_depth,
+                                                              h->xd, (long long)h->n_nodes);
+        PF_TRY(launched(h));
+        h->warm_nd[ws] = std::min(h->warm_nd[ws] + 1, h->warm_depth);
+      }
     }
     if (h->trace)
       fprintf(stderr, "[pfb200] evolution newton %d gated %d iters %lld\n", n_nr, (int)gated,
@@ -1911,7 +1938,7 @@ extern "C" pf_status pf_staggered_step(pf_handle* h, int scheme, const int64_t* 
     st.n_stag += 1;
     t0 = now_s();
     int nd = 0;
-    PF_TRY(evolution(h, scheme, &r0_d, &nd, &st.spd_fallbacks));
+    PF_TRY(evolution(h, scheme, &r0_d, &nd, &st.spd_fallbacks, st.n_stag));
     st.n_nr_d += nd;
     st.wall_d += now_s() - t0;
     t0 = now_s();

@@ -427,8 +427,9 @@ __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO
             nwarps = gridDim.x * (CG_NT / 32);
   double* part = a.partials;
   double bnorm_in = -1.0;
-  if constexpr (MOM)  // phase-field solves start cold (SPD predicate semantics)
-    if (a.n_guess > 0) bnorm_in = warm_start<MOM>(a, S);
+  // warm start (phase-field solves only without the SPD probe: the predicate needs the Krylov
+  // sequence from x0 = 0 that was validated against check_spd)
+  if (a.n_guess > 0 && !a.probe) bnorm_in = warm_start<MOM>(a, S);
   double rr = 0.0, rz = 0.0;
   phase_b<!XUPD>(a, 0.0, nullptr, false, rr, rz);  // ||r0||^2 and r0.D^-1.r0 (r = b on entry)
   {
@@ -536,8 +537,7 @@ __global__ void __launch_bounds__(CG_NT, MOM ? PFB_CG_MINB_MOM : PFB_CG_MINB_EVO
             nwarps = gridDim.x * (CG_NT / 32);
   double* part = a.partials;
   double bnorm_in = -1.0;
-  if constexpr (MOM)
-    if (a.n_guess > 0) bnorm_in = warm_start<MOM>(a, S);
+  if (a.n_guess > 0 && !a.probe) bnorm_in = warm_start<MOM>(a, S);
   SrScal sp;
   long long k = 0;
   int status = CG_CONVERGED;
