@@ -12,8 +12,10 @@ schedule: W untimed warm-up load steps advance the state, then K load steps are 
 * ``e2e``     — the same metric through the reference-facing drop-in
   ``paper_2209_07969_b200.schemes.staggered_step`` with the caller's HOST SolverState: every
   step uploads the state, solves, and downloads the state (all copies inside the timed region).
-* ``roofline``— the dominant kernel (``k_cg``, momentum PCG): algorithmic bytes
-  168 B * N_nodes per PCG iteration / its CUDA-event time.
+* ``roofline``— the dominant single kernel: with the multigrid momentum solver (default) the
+  phase-field Jacobi PCG ``k_cg<false, *>`` (algorithmic bytes 72 B * N_nodes + 32 B * N_cells
+  per PCG iteration); with PFB200_MG=0 the momentum PCG (168 B * N_nodes) /
+  its CUDA-event time.  ``momentum_solver`` summarises the multigrid PCG graph.
 * ``cpu_baseline`` — the CPU oracle port (oracle/phasefield_oracle.py, SuperLU like the
   reference default) on the first load step of the same case, rank 0 only.
 * ``--gpus N`` (torchrun, one process per GPU) — the same cfg2 problem split into N row strips
@@ -243,16 +245,30 @@ def run_ours(args, ws, rank, local):
     peak, peak_src = peaks()
     n_cg = run.n_local
     mom_bytes = MOM_BYTES_PER_NODE * n_cg
-    achieved = (tot["cg_u"] * mom_bytes / 1e9) / (tot["ms_u"] / 1e3) if tot["ms_u"] else 0.0
     evo_bytes = EVO_BYTES_PER_NODE * n_cg + EVO_BYTES_PER_ELEM * n_elems / ws
     evo_achieved = (tot["cg_d"] * evo_bytes / 1e9) / (tot["ms_d"] / 1e3) if tot["ms_d"] else 0.0
+    mg = sess.mg_info() if ws == 1 else {"n_levels": 0}
+    if mg["n_levels"]:
+        # The momentum solves run as the multigrid PCG graph (~30 small kernels per iteration,
+        # no single dominant kernel); the largest single kernel is the phase-field Jacobi PCG
+        # (k_cg<false, *>, one persistent launch per solve): its roofline is reported.
+        rl_kernel = "k_cg<false, *> (phase-field Jacobi PCG, persistent cooperative)"
+        achieved, rl_bytes = evo_achieved, "72 B x N_nodes + 32 B x N_cells per phase-field PCG iteration"
+        tkey, iters_key, launches_key = "k_cg_evo", "cg_d", "cgl_d"
+    else:
+        rl_kernel = ("k_cg<true, *> (momentum PCG, persistent cooperative)" if ws == 1 else
+                     "momentum PCG (k_cg_a/k_cg_b + NCCL, rank 0's strip)")
+        achieved = (tot["cg_u"] * mom_bytes / 1e9) / (tot["ms_u"] / 1e3) if tot["ms_u"] else 0.0
+        rl_bytes = "168 B x N_nodes per momentum PCG iteration"
+        tkey, iters_key, launches_key = "k_cg", "cg_u", "cgl_u"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "k_cg_traffic.json")
     if os.path.exists(tpath) and ws == 1:
         with open(tpath) as f:
             tj = json.load(f)
-        if tj.get("case") == args.case and tot["cgl_u"]:
-            traffic = tj["dram_bytes_per_iter"] * tot["cg_u"] / tot["cgl_u"]
+        ent = tj.get(tkey) if isinstance(tj.get(tkey), dict) else (tj if tkey == "k_cg" else None)
+        if ent and ent.get("case") == args.case and tot[launches_key]:
+            traffic = ent["dram_bytes_per_iter"] * tot[iters_key] / tot[launches_key]
     launches = int(allreduce_sum(ws, float(tot["launches"])))
     res = {
         "metric": "DOF-iterations/s of staggered solve (FP64)",
@@ -283,14 +299,19 @@ def run_ours(args, ws, rank, local):
                       "momentum_launches": tot["cgl_u"], "phase_field_launches": tot["cgl_d"]},
         "kernel_ms": {"momentum_pcg": tot["ms_u"], "phase_field_pcg": tot["ms_d"]},
         "roofline": {
-            "kernel": "k_cg<true, *> (momentum PCG, persistent cooperative)" if ws == 1 else
-                      "momentum PCG (k_cg_a/k_cg_b + NCCL, rank 0's strip)",
+            "kernel": rl_kernel,
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "peak_source": peak_src,
-            "algorithmic_bytes": "168 B x N_nodes per momentum PCG iteration",
-            "phase_field_achieved": evo_achieved,
+            "algorithmic_bytes": rl_bytes,
+            "note": "cfg2's PCG working set (~50 MB) is L2-resident: the fraction mixes L2 and "
+                    "HBM traffic (SURVEY.md 8(d)); cfg3-5 are the HBM-bound sizes",
         },
+        "momentum_solver": ({"kind": "multigrid PCG (Galerkin V(1,1), CUDA graph)",
+                             "levels": mg["n_levels"], "hierarchy_builds": mg.get("setups"),
+                             "iterations": tot["cg_u"], "solves": tot["cgl_u"],
+                             "us_per_iteration": 1e3 * tot["ms_u"] / max(tot["cg_u"], 1)}
+                            if mg["n_levels"] else {"kind": "Jacobi PCG"}),
         "e2e": {"value": ndof * e2e_stag / (e2e_ms / 1e3), "unit": "DOF-iter/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms / args.steps, "path": e2e_path},

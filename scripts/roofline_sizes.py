@@ -51,6 +51,7 @@ def main():
         s.push(u=1e-4 * rng.standard_normal(2 * nn), d=0.5 * rng.random(nn),
                d_prev=np.zeros(nn))
         s.refresh_gp()
+        best_mom = None
         for phys, nbytes in (("momentum", 168.0 * nn), ("evolution", 72.0 * nn + 32.0 * ne)):
             n_iter = args.iters or max(20, int(0.5 / max(nbytes / 4.0e12, 1.2e-5)))
             s.flush_l2()
@@ -68,12 +69,28 @@ def main():
                 us = 1e3 * tot_ms / tot_it
                 best = us if best is None else min(best, us)
             gbs = nbytes / best / 1e3
+            if phys == "momentum":
+                best_mom = best
             print(json.dumps({
                 "case": name, "physics": phys, "n_nodes": nn, "n_cells": ne,
                 "iters": n_iter, "us_per_iter": round(best, 3),
                 "algorithmic_bytes_per_iter": nbytes, "GBs": round(gbs, 1),
                 "frac_of_measured_hbm": round(gbs / peak, 3) if peak else None,
                 **s.device_info()}), flush=True)
+        mg = s.mg_info()
+        if mg["n_levels"]:  # multigrid momentum PCG: per-iteration cost and per-solve setup
+            t = {}
+            for n in (1, 11):
+                s.flush_l2()
+                s.bench_cg("momentum_mg", n)
+                t[n] = min(s.bench_cg("momentum_mg", n)[0] for _ in range(args.repeats))
+            per = (t[11] - t[1]) / 10.0
+            print(json.dumps({
+                "case": name, "physics": "momentum_mg", "n_nodes": nn, "levels": mg["n_levels"],
+                "tail_from_level": mg["n_grid"], "us_per_iter": round(1e3 * per, 2),
+                "setup_us": round(1e3 * (t[1] - per), 1),
+                "jacobi_equivalent_iters": round(1e3 * per / best_mom, 1) if best_mom else None}),
+                flush=True)
         s.close()
 
 
