@@ -217,8 +217,10 @@ def run_ours(args, ws, rank, local):
                                         pb2.config, pb2.pins)
             e2e_stag += s2.n_stag
         e2e_ms = (time.perf_counter() - t0) * 1e3
-        h2d = 8 * (2 * n_nodes + 2 * n_nodes + 4 * 4 * n_elems)  # u, d, d_prev, 4 GP arrays
-        d2h = h2d + 8 * (16 + 4) * n_elems if schemes.SYNC_GP_STRAIN else h2d
+        h2d = 8 * (2 * n_nodes + 2 * n_nodes + 4 * n_elems)  # u, d, d_prev, gp.psi_max
+        d2h = 8 * (4 * n_nodes + 4 * 4 * n_elems)  # u, d, d_prev, 4 GP arrays
+        if schemes.SYNC_GP_STRAIN:
+            d2h += 8 * (16 + 4) * n_elems  # gp.strain, gp.tr_eps
         e2e_path = "paper_2209_07969_b200.schemes.staggered_step with host SolverState"
     else:
         run2 = _Strip(pb2, rank, ws, local)

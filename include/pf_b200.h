@@ -124,6 +124,11 @@ pf_status pf_get_state(pf_handle* h, double* u, double* d, double* d_prev,
 /* gp.strain [n_elems*4*4] Voigt (xx,yy,zz,xy) and gp.tr_eps [n_elems*4] recomputed from u
  * (refresh_gp_from_displacement, assembly.py:260-269). */
 pf_status pf_get_gp_strain(pf_handle* h, double* strain, double* tr_eps);
+/* Page-locked host buffers (cudaHostAlloc): state arrays in them move by direct DMA in
+ * pf_set_state / pf_get_state / pf_get_gp_strain (other host pointers go through the handle's
+ * pinned staging buffer). */
+pf_status pf_host_alloc(int64_t bytes, void** out);
+void pf_host_free(void* p);
 
 /* hot path: one load step (schemes.py:332-392).
  * Boundary pairs: pair k covers bc_dofs[bc_offsets[k] .. bc_offsets[k+1]) with increment

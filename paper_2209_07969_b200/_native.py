@@ -112,6 +112,8 @@ _SIGNATURES = {
                                   C.c_int, C.POINTER(PfStrip), C.POINTER(C.c_void_p)]),
     "pf_bench_cg": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, _f64p, _i64p]),
     "pf_device_info": (C.c_int, [C.c_void_p, _i32p, _i32p, _i64p]),
+    "pf_host_alloc": (C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),
+    "pf_host_free": (None, [C.c_void_p]),
     "pf_mg_info": (C.c_int, [C.c_void_p, _i32p, _i32p, _i32p, _i64p, _f64p]),
     "pf_flush_l2": (C.c_int, [C.c_void_p]),
     "pf_synchronize": (C.c_int, [C.c_void_p]),
@@ -165,3 +167,36 @@ def i32(a):
 def u8(a):
     assert a.dtype == np.uint8 and a.flags["C_CONTIGUOUS"]
     return a.ctypes.data_as(_u8p)
+
+
+class PinnedPool:
+    """Page-locked float64 arrays for the state outputs (pf_host_alloc): the device writes them
+    by direct DMA.  A buffer returns to the pool when its array is garbage collected, so the
+    drop-in's per-step output arrays (rebound like the reference's, schemes.py:391,
+    assembly.py:265-269) cycle through two sets of buffers."""
+
+    def __init__(self):
+        self.free = {}
+
+    def empty(self, shape):
+        import weakref
+
+        lib = load()
+        n = int(np.prod(shape))
+        nbytes = max(8 * n, 8)
+        stack = self.free.setdefault(nbytes, [])
+        if stack:
+            ptr = stack.pop()
+        else:
+            p = C.c_void_p()
+            if lib.pf_host_alloc(nbytes, C.byref(p)) != 0:
+                return np.empty(shape)  # no pinned memory left: pageable (staged) output
+            ptr = p.value
+        buf = (C.c_char * nbytes).from_address(ptr)
+        flat = np.frombuffer(buf, dtype=np.float64, count=n)
+        # every view (reshape included) keeps `flat` alive: numpy collapses view bases to it
+        weakref.finalize(flat, stack.append, ptr)
+        return flat.reshape(shape)
+
+
+PINNED = PinnedPool()

@@ -124,6 +124,7 @@ struct pf_handle {
   long long mg_ref_iters = 0, mg_last_iters = 0;
   int mg_age = 0, mg_max_age = 64;
   long long mg_setups = 0;
+  int mg_setup_kernels = 0, mg_body_kernels = 0;  // kernel nodes per graph (launch accounting)
 
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
@@ -676,6 +677,7 @@ static pf_status mg_build_graphs(pf_handle* h) {
       pfb::k_mg_stencil<<<h->mg_gl[lc], pfb::MG_NT, 0, s>>>(A, lc);
     }
     if (A.dense) pfb::k_mg_dense<<<1, pfb::MG_NT, 0, s>>>(A);
+    h->mg_setup_kernels = 2 * (nl - 1) + (A.dense ? 1 : 0) + pfb::MG_POW + 1;
     const int cb = (16 * A.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
     for (int k = 1; k <= pfb::MG_POW; ++k)
       pfb::k_mg_pow<<<h->mg_gf + cb, pfb::MG_NT, 0, s>>>(A, k, h->mg_gf);
@@ -723,6 +725,11 @@ static pf_status mg_build_graphs(pf_handle* h) {
     pfb::k_mg_pcg<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B, h->mg_gf);
     pfb::k_mg_update<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(B, h->mg_gf, h->mg_gf);
   };
+  {
+    const int c = nl - 1, top = std::min(A.n_tail, c);
+    h->mg_body_kernels = 1 + 4 * (top - 1) + 3 +
+                         (A.n_tail < nl ? 1 : 1 + (A.dense ? 1 : A.nu_c));
+  }
   const char* un = getenv("PFB200_MG_UNROLL");
   const int unroll = un ? std::max(0, atoi(un)) : 0;
   if (unroll > 0) {
@@ -1177,7 +1184,31 @@ static pf_status ensure_stage(pf_handle* h, size_t n) {
 
 static constexpr size_t STAGE_MIN = 1 << 19;  // doubles (4 MB): below, plain pageable copies
 
-static pf_status transfer(pf_handle* h, const std::vector<Xfer>& items, bool to_device) {
+// page-locked host memory (pf_host_alloc, cudaHostAlloc / cudaHostRegister): DMA directly
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+static pf_status transfer(pf_handle* h, const std::vector<Xfer>& items0, bool to_device) {
+  // pinned host buffers go straight to / from the device; the rest through the staging buffer
+  std::vector<Xfer> items;
+  for (const auto& it : items0) {
+    if (!it.host) continue;
+    if (host_pinned(it.host)) {
+      PF_CUDA(cudaMemcpyAsync(to_device ? (void*)it.dev : (void*)it.host,
+                              to_device ? (const void*)it.host : (const void*)it.dev,
+                              it.n * sizeof(double),
+                              to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                              h->stream));
+    } else {
+      items.push_back(it);
+    }
+  }
   size_t total = 0;
   for (const auto& it : items)
     if (it.host) total += it.n;
@@ -1261,6 +1292,20 @@ static pfb::GpArgs gp_args(pf_handle* h) {
   g.psi = h->psi;
   g.psimax = h->psimax;
   return g;
+}
+
+// page-locked host buffers for state outputs (direct DMA in pf_get_state / pf_get_gp_strain)
+extern "C" pf_status pf_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes <= 0) return PF_ERR_INVALID;
+  *out = nullptr;
+  if (cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return PF_ERR_CUDA;
+  }
+  return PF_OK;
+}
+extern "C" void pf_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 extern "C" pf_status pf_get_gp_strain(pf_handle* h, double* strain, double* tr_eps) {
@@ -1683,6 +1728,9 @@ static pf_status run_mg(pf_handle* h, double* target, int* status, long long* it
   *iters = h->h_cgres->iters;
   if (rebuild) h->mg_ref_iters = *iters;
   h->mg_last_iters = *iters;
+  // kernels executed inside the graphs (each graph launch counted one by launched())
+  h->acc.launches += (rebuild ? h->mg_setup_kernels - 1 : 0) +
+                     (setup_only ? 0 : pfb::MG_WARM + 1 + (int)(*iters) * h->mg_body_kernels);
   if (h->trace)
     fprintf(stderr, "[pfb200] mg solve: %lld iterations, %.3f ms%s\n", *iters, ms,
             rebuild ? " (hierarchy rebuilt)" : "");

@@ -81,7 +81,11 @@ class SolverState:
 
 
 def _write_back(sess: DeviceSession, state) -> None:
-    out = sess.pull()
+    """Mirror the device state into the caller's SolverState with the reference's binding
+    semantics: u, d and gp.psi_max are updated in place (schemes.py:390, in-place arithmetic),
+    d_prev and the refreshed GP arrays are rebound to new arrays (schemes.py:391,
+    assembly.py:265-269).  The new arrays are page-locked (direct DMA from the device)."""
+    out = sess.pull(pinned=True)
     state.u[...] = out["u"]
     state.d[...] = out["d"]
     state.d_prev = out["d_prev"]
@@ -91,14 +95,18 @@ def _write_back(sess: DeviceSession, state) -> None:
     gp.psi_plus = out["psi_plus"]
     gp.psi_max[...] = out["psi_max"]
     if SYNC_GP_STRAIN:
-        gp.strain, gp.tr_eps = sess.gp_strain()
+        gp.strain, gp.tr_eps = sess.gp_strain(pinned=True)
 
 
 def staggered_step(disc, state, scheme, bc_increments, params, config,
                    pinned_d_nodes=None) -> StaggeredStats:
     """Advance one loading step with the chosen staggered scheme on the GPU."""
     sess = session_for(disc, params, config)
-    sess.push_state(state)
+    # Inputs of a load step: u, d, d_prev, psi_max.  gp.tr_eps_plus / dev_dot_dev / psi_plus are
+    # overwritten from u by the first momentum pass (refresh_gp_from_displacement at the end of
+    # solve_momentum, schemes.py:237 / assembly.py:260-269) before anything reads them.
+    gp = state.gp
+    sess.push(u=state.u, d=state.d, d_prev=state.d_prev, psi_max=gp.psi_max)
     try:
         st = sess.step(scheme, bc_increments, pinned_d_nodes)
     finally:

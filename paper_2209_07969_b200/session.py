@@ -161,18 +161,21 @@ class DeviceSession:
         self.push(state.u, state.d, state.d_prev, gp.tr_eps_plus, gp.dev_dot_dev, gp.psi_plus,
                   gp.psi_max)
 
-    def pull(self) -> dict:
+    def pull(self, pinned: bool = False) -> dict:
+        """The state arrays (fresh arrays; ``pinned``: page-locked, filled by direct DMA)."""
         nn, ne = self.n_nodes, self.n_elems
-        out = dict(u=np.empty(2 * nn), d=np.empty(nn), d_prev=np.empty(nn),
-                   tr_eps_plus=np.empty((ne, 4)), dev_dot_dev=np.empty((ne, 4)),
-                   psi_plus=np.empty((ne, 4)), psi_max=np.empty((ne, 4)))
+        emp = N.PINNED.empty if pinned else np.empty
+        out = dict(u=emp(2 * nn), d=emp(nn), d_prev=emp(nn),
+                   tr_eps_plus=emp((ne, 4)), dev_dot_dev=emp((ne, 4)),
+                   psi_plus=emp((ne, 4)), psi_max=emp((ne, 4)))
         self._check(self.lib.pf_get_state(self.h, *[N.f64(out[k]) for k in (
             "u", "d", "d_prev", "tr_eps_plus", "dev_dot_dev", "psi_plus", "psi_max")]))
         return out
 
-    def gp_strain(self) -> tuple:
+    def gp_strain(self, pinned: bool = False) -> tuple:
         ne = self.n_elems
-        strain, tr = np.empty((ne, 4, 4)), np.empty((ne, 4))
+        emp = N.PINNED.empty if pinned else np.empty
+        strain, tr = emp((ne, 4, 4)), emp((ne, 4))
         self._check(self.lib.pf_get_gp_strain(self.h, N.f64(strain), N.f64(tr)))
         return strain, tr
 
