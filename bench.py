@@ -268,9 +268,12 @@ def run_ours(args, ws, rank, local):
     if os.path.exists(tpath) and ws == 1:
         with open(tpath) as f:
             tj = json.load(f)
-        ent = tj.get(tkey) if isinstance(tj.get(tkey), dict) else (tj if tkey == "k_cg" else None)
+        ent = tj.get(tkey)
         if ent and ent.get("case") == args.case and tot[launches_key]:
-            traffic = ent["dram_bytes_per_iter"] * tot[iters_key] / tot[launches_key]
+            if "dram_bytes_per_launch" in ent:
+                traffic = ent["dram_bytes_per_launch"]
+            else:
+                traffic = ent["dram_bytes_per_iter"] * tot[iters_key] / tot[launches_key]
     launches = int(allreduce_sum(ws, float(tot["launches"])))
     res = {
         "metric": "DOF-iterations/s of staggered solve (FP64)",
