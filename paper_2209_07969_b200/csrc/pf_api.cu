@@ -125,6 +125,7 @@ struct pf_handle {
   int mg_age = 0, mg_max_age = 64;
   long long mg_setups = 0;
   int mg_setup_kernels = 0, mg_body_kernels = 0;  // kernel nodes per graph (launch accounting)
+  bool mg_fuse = true;  // fused down / up kernels on the half-warp levels (PFB200_MG_FUSE=0: off)
 
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
@@ -496,6 +497,8 @@ static cudaError_t mg_alloc(pf_handle* h, T** p, size_t n) {
 static pf_status mg_build_graphs(pf_handle* h);
 
 static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
+  const char* fz = getenv("PFB200_MG_FUSE");
+  h->mg_fuse = !(fz && std::string(fz) == "0");
 
   const char* tl = getenv("PFB200_MG_TAIL");  // tail levels: at most this many nodes
   const int tail_nodes = tl ? std::max(0, atoi(tl)) : 1 << 30;
@@ -700,8 +703,12 @@ static pf_status mg_build_graphs(pf_handle* h) {
     const int c = nl - 1, top = std::min(B.n_tail, c);  // grid levels [1, top)
     pfb::k_mg_fine_resid<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B);
     for (int l = 1; l < top; ++l) {
-      MG_NODE_KERNEL(k_mg_srestrict, l, B, l);
-      MG_NODE_KERNEL(k_mg_sresid, l, B, l);
+      if (h->mg_lpn[l] == 16 && h->mg_fuse) {  // small levels: one fused kernel per direction
+        pfb::k_mg_sdown<16><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(B, l);
+      } else {
+        MG_NODE_KERNEL(k_mg_srestrict, l, B, l);
+        MG_NODE_KERNEL(k_mg_sresid, l, B, l);
+      }
     }
     if (B.n_tail < nl) {
       pfb::k_mg_tail<<<1, pfb::MG_TAIL_NT, B.ts_bytes, s>>>(B);
@@ -718,8 +725,12 @@ static pf_status mg_build_graphs(pf_handle* h) {
       }
     }
     for (int l = top - 1; l >= 1; --l) {
-      MG_NODE_KERNEL(k_mg_sprolongate, l, B, l);
-      MG_NODE_KERNEL(k_mg_ssmooth, l, B, l);
+      if (h->mg_lpn[l] == 16 && h->mg_fuse) {
+        pfb::k_mg_sup<16><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(B, l);
+      } else {
+        MG_NODE_KERNEL(k_mg_sprolongate, l, B, l);
+        MG_NODE_KERNEL(k_mg_ssmooth, l, B, l);
+      }
     }
     pfb::k_mg_fine_smooth<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B);
     pfb::k_mg_pcg<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B, h->mg_gf);
@@ -727,8 +738,8 @@ static pf_status mg_build_graphs(pf_handle* h) {
   };
   {
     const int c = nl - 1, top = std::min(A.n_tail, c);
-    h->mg_body_kernels = 1 + 4 * (top - 1) + 3 +
-                         (A.n_tail < nl ? 1 : 1 + (A.dense ? 1 : A.nu_c));
+    h->mg_body_kernels = 1 + 3 + (A.n_tail < nl ? 1 : 1 + (A.dense ? 1 : A.nu_c));
+    for (int l = 1; l < top; ++l) h->mg_body_kernels += (h->mg_lpn[l] == 16 && h->mg_fuse) ? 2 : 4;
   }
   const char* un = getenv("PFB200_MG_UNROLL");
   const int unroll = un ? std::max(0, atoi(un)) : 0;

@@ -591,6 +591,99 @@ __global__ void __launch_bounds__(MG_NT) k_mg_ssmooth(MgArgs A, int l) {
     }
   }
 }
+// Fused down-sweep of a small level (one lane per stencil slot): the restriction of t_{l-1} is
+// evaluated at each neighbour by the lane that multiplies it (12 source loads per lane, all in
+// flight), x = omega D^-1 b, t = b - A x; b is stored for the up-sweep.  Saves the separate
+// restriction kernel's launch and dependent rounds.
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mg_sdown(MgArgs A, int l) {
+  const MgLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  const double* tf = A.L[l - 1].t;
+  MG_FOR_NODE_L(n) {
+    double2 acc = make_double2(0.0, 0.0), bc = make_double2(0.0, 0.0);
+    if (id < n) {
+#pragma unroll
+      for (int s2 = NodeMap<LPN>::lane(); s2 < MG_NS; s2 += LPN) {
+        const int k = __ldg(L.nbr + (size_t)s2 * n + id);
+        if (k < 0) continue;
+        int f[12];
+#pragma unroll
+        for (int j = 0; j < 12; ++j) f[j] = __ldg(L.rid + (size_t)j * n + k);
+        double2 b = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < 12; ++j) {
+          if (f[j] < 0) continue;
+          const double2 t = GMem::v2(tf, f[j]);
+          const double w = mg_rw(j);
+          b.x += w * t.x;
+          b.y += w * t.y;
+        }
+        const double2 di = GMem::v2(L.dinv, k);
+        b = mask2(b, di);
+        if (s2 == 4) bc = b;  // the node itself
+        const double* Sp = L.S + (size_t)(4 * s2) * n + id;
+        const double sxx = __ldg(Sp), sxy = __ldg(Sp + n), syx = __ldg(Sp + 2 * (size_t)n),
+                     syy = __ldg(Sp + 3 * (size_t)n);
+        const double2 x = make_double2(om * di.x * b.x, om * di.y * b.y);
+        acc.x += sxx * x.x + sxy * x.y;
+        acc.y += syx * x.x + syy * x.y;
+      }
+    }
+    acc = NodeMap<LPN>::sum(acc);
+    bc = NodeMap<LPN>::sum(bc);
+    if (MG_LEAD) {
+      d2st(L.b, id, bc);
+      d2st(L.t, id, mask2(make_double2(bc.x - acc.x, bc.y - acc.y), GMem::v2(L.dinv, id)));
+    }
+  }
+}
+// Fused up-sweep of a small level: y = omega D^-1 b + P e_{l+1} evaluated at each neighbour by
+// its lane, e = y + omega D^-1 (b - A y)
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mg_sup(MgArgs A, int l) {
+  const MgLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  const double* ec = A.L[l + 1].e;
+  MG_FOR_NODE_L(n) {
+    double2 acc = make_double2(0.0, 0.0), yc = make_double2(0.0, 0.0);
+    if (id < n) {
+#pragma unroll
+      for (int s2 = NodeMap<LPN>::lane(); s2 < MG_NS; s2 += LPN) {
+        const int k = __ldg(L.nbr + (size_t)s2 * n + id);
+        if (k < 0) continue;
+        int c[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = __ldg(L.pid + (size_t)j * n + k);
+        const double w = 1.0 / ((c[0] >= 0) + (c[1] >= 0) + (c[2] >= 0) + (c[3] >= 0));
+        double2 pe = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (c[j] < 0) continue;
+          const double2 e = GMem::v2(ec, c[j]);
+          pe.x += e.x;
+          pe.y += e.y;
+        }
+        const double2 di = GMem::v2(L.dinv, k), bv = GMem::v2(L.b, k);
+        const double2 y = mask2(make_double2(om * di.x * bv.x + w * pe.x, om * di.y * bv.y + w * pe.y), di);
+        if (s2 == 4) yc = y;
+        const double* Sp = L.S + (size_t)(4 * s2) * n + id;
+        const double sxx = __ldg(Sp), sxy = __ldg(Sp + n), syx = __ldg(Sp + 2 * (size_t)n),
+                     syy = __ldg(Sp + 3 * (size_t)n);
+        acc.x += sxx * y.x + sxy * y.y;
+        acc.y += syx * y.x + syy * y.y;
+      }
+    }
+    acc = NodeMap<LPN>::sum(acc);
+    yc = NodeMap<LPN>::sum(yc);
+    if (MG_LEAD) {
+      const double2 di = GMem::v2(L.dinv, id), bv = GMem::v2(L.b, id);
+      d2st(L.e, id, make_double2(yc.x + om * di.x * (bv.x - acc.x), yc.y + om * di.y * (bv.y - acc.y)));
+    }
+  }
+}
 // Jacobi sweep out = in + omega D^-1 (b - A in) (grid coarsest level)
 template <int LPN>
 __global__ void __launch_bounds__(MG_NT) k_mg_ssweep(MgArgs A, int l, const double* in,
