@@ -73,8 +73,10 @@ struct pf_handle {
   static constexpr int WARM_SLOTS = 4;
   bool warm = true;
   bool trace = false;
-  // cfg2 load steps 4..13, momentum PCG iterations: depth 1 69634, 3 52336, 4 52151, 5 51805
-  int warm_depth = 3;
+  // cfg2 load steps 4..13, Jacobi momentum PCG iterations: depth 1 69634, 3 52336, 4 52151,
+  // 5 51805; MG bench (phase-field tables): depth 3 682, 5 538 phase-field iterations.  The
+  // multigrid solves use the first MG_WARM = 3 entries.
+  int warm_depth = 5;
   double* warm_buf[WARM_SLOTS][pfb::WARM_MAX] = {};
   int warm_n[WARM_SLOTS] = {};
   // phase-field solves without the SPD probe (no gated Gauss point, or ST): the same
@@ -86,7 +88,9 @@ struct pf_handle {
   double* stage = nullptr;  // pinned host staging buffer for state transfers
   size_t stage_cap = 0;     // doubles
   bool sr_mom = false;  // momentum solves by the single-reduction PCG (k_cg_sr<true>)
-  bool sr_evo = false;  // phase-field solves by k_cg_sr<false>
+  bool sr_evo = false;  // phase-field solves without the SPD probe by k_cg_sr<false>
+  bool sr_evo_now = false;       // the kernel choice of the current phase-field launch
+  long long evo_last_iters = 0;  // PCG iterations of the last converged phase-field solve
   size_t sr_smem_evo = 0;
   size_t sr_smem = 0;   // its dynamic shared memory (cp.async staging slots)
   pfb::MarchGeom geom_mom{}, geom_evo{}, geom_apply{};
@@ -958,9 +962,12 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
     if (srv) h->sr_mom = std::string(srv) == "1";
     h->sr_mom = h->sr_mom && !strip;  // strips: split-phase kernels
     const char* sre = getenv("PFB200_SR_EVO");
-    // opt-in: on cfg3's first load step the single-reduction phase-field PCG never reached
-    // ||r|| < 1e-12 ||b|| (maxiter 20 n, tests/test_gpu_solver.py::test_full_size_first_step)
-    h->sr_evo = (sre && std::string(sre) == "1") && !strip;
+    // Phase-field solves without the SPD probe use the single-reduction PCG (one grid barrier
+    // per iteration; cfg2 bench: phase-field time -19%).  Its recurrence stalled once (cfg3's
+    // first load step never reached ||r|| < 1e-12 ||b||), so every single-reduction solve runs
+    // with an iteration cap and is redone by the two-barrier PCG when it does not converge
+    // (evolution() below).  PFB200_SR_EVO=0: two-barrier PCG only.
+    h->sr_evo = !(sre && std::string(sre) == "0") && !strip;
     if (h->sr_evo) {
       CREATE_ALLOC(h->r1d, nn);
       CREATE_ALLOC(h->w1d, nn);
@@ -1463,12 +1470,12 @@ static pf_status axpy(pf_handle* h, double* y, const double* x, long long n) {
 }
 
 static size_t cg_smem(const pf_handle* h, bool mom) {  // dynamic smem of the chosen PCG kernel
-  return mom ? (h->sr_mom ? h->sr_smem : 0) : (h->sr_evo ? h->sr_smem_evo : 0);
+  return mom ? (h->sr_mom ? h->sr_smem : 0) : (h->sr_evo_now ? h->sr_smem_evo : 0);
 }
 
 static const void* cg_kernel(pf_handle* h, bool mom) {
   if (mom && h->sr_mom) return (const void*)pfb::k_cg_sr<true>;
-  if (!mom && h->sr_evo) return (const void*)pfb::k_cg_sr<false>;
+  if (!mom && h->sr_evo_now) return (const void*)pfb::k_cg_sr<false>;
   if (mom) return h->xupd_mom ? (const void*)pfb::k_cg<true, true> : (const void*)pfb::k_cg<true, false>;
   return h->xupd_evo ? (const void*)pfb::k_cg<false, true> : (const void*)pfb::k_cg<false, false>;
 }
@@ -1526,8 +1533,9 @@ static pf_status cg_status(pf_handle* h, int status, long long iters) {
 // one persistent PCG solve (single cooperative launch)
 static pf_status run_cg_persistent(pf_handle* h, bool mom, double* target, bool probe,
                                    int* status, long long* iters, double* const* guess,
-                                   int n_guess) {
+                                   int n_guess, long long maxiter_cap = 0) {
   pfb::CgArgs a = cg_args(h, mom);
+  if (maxiter_cap > 0) a.maxiter = std::min(a.maxiter, maxiter_cap);
   a.target = target;
   a.probe = probe ? 1 : 0;
   for (int k = 0; k < n_guess && k < pfb::WARM_MAX; ++k) a.guess[k] = guess[k];
@@ -1924,7 +1932,29 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
       double* guess[pfb::WARM_MAX] = {};
       const int ng = use_warm ? h->warm_nd[ws] : 0;
       for (int k = 0; k < ng; ++k) guess[k] = h->warm_d[ws][k];
-      PF_TRY(run_cg(h, false, h->d, false, &status, &iters, guess, ng));
+      bool done = false;
+      if (h->sr_evo && !h->comm && !h->split) {
+        // single-reduction PCG with an iteration cap (4x the last converged phase-field solve);
+        // d is updated only after it converged
+        const long long cap = std::max(300LL, 4 * h->evo_last_iters);
+        h->sr_evo_now = true;
+        const pf_status sst = run_cg_persistent(h, false, nullptr, false, &status, &iters, guess,
+                                                ng, cap);
+        h->sr_evo_now = false;
+        if (sst == PF_OK) {
+          PF_TRY(axpy(h, h->d, h->xd, h->n_nodes));
+          done = true;
+        } else if (sst != PF_ERR_SINGULAR) {
+          return sst;
+        } else {  // stalled: redo this solve from scratch with the two-barrier PCG
+          if (h->trace)
+            fprintf(stderr, "[pfb200] single-reduction phase-field PCG stalled after %lld "
+                            "iterations: two-barrier PCG\n", iters);
+          PF_TRY(launch_evo_prepare(h, 1, 0));
+        }
+      }
+      if (!done) PF_TRY(run_cg(h, false, h->d, false, &status, &iters, guess, ng));
+      h->evo_last_iters = iters;
       if (use_warm) {
         pfb::WarmTable t{};
         for (int k = 0; k < h->warm_depth; ++k) t.d[k] = h->warm_d[ws][k];
