@@ -156,8 +156,10 @@ __device__ __forceinline__ double mg_q(int c, int k, int K) {
 
 // ----------------------------------------------------------------------------------------
 // Generic warp march (pf_march.cuh march_unit without the PCG specifics).  Op provides
-//   double2 in(int id, int i, int j, bool dup, double& aux)  input value at a node (zero, aux 0
-//                                                             for id < 0)
+//   struct Raw; void fetch(int id, Raw&)                      the node's loads (id >= 0)
+//   double2 finish(const Raw&, int id, int i, int j, bool dup, double& aux)  its input value
+//   double2 in(int id, int i, int j, bool dup, double& aux)  fetch + finish (zero, aux 0 for
+//                                                             id < 0)
 //   void cell(int eid, const double2 (&v)[4], const double (&a)[4], double2 (&f)[4])
 //   void out(int id, double2 Av, double2 vin)                 once per owned node
 template <class Op>
@@ -211,11 +213,20 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
   double2 v_lo = op.in(id_lo, col, r0 - 1, false, a_lo);
   bool lo_slit = (r0 - 1 == R);
   if (lo_slit) load_dup();
+  // the next node row's loads are issued one row step ahead (Op::fetch), so every warp keeps
+  // a row of loads in flight while it does the current row's FP64 work (Op::finish)
+  typename Op::Raw w_hi;
+  int id_hi = nid(r0);
+  if (id_hi >= 0) op.fetch(id_hi, w_hi);
   double2 acc_lo = make_double2(0.0, 0.0);
   for (int cj = r0 - 1; cj < r1; ++cj) {
     const int jh = cj + 1;
-    const int id_hi = nid(jh);
-    const double2 v_hi = op.in(id_hi, col, jh, false, a_hi);
+    a_hi = 0.0;
+    const double2 v_hi = id_hi >= 0 ? op.finish(w_hi, id_hi, col, jh, false, a_hi)
+                                    : make_double2(0.0, 0.0);
+    typename Op::Raw w_nx;
+    const int id_nx = (jh + 1 <= r1) ? nid(jh + 1) : -1;
+    if (id_nx >= 0) op.fetch(id_nx, w_nx);
     const bool hi_slit = (jh == R);
     const int eid = cell_id(cj);
     const bool use_dup = lo_slit && dupcol;
@@ -249,6 +260,8 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
     a_lo = a_hi;
     id_lo = id_hi;
     lo_slit = hi_slit;
+    id_hi = id_nx;
+    w_hi = w_nx;
   }
 }
 
@@ -275,12 +288,25 @@ struct FineResid : FineBase {  // x = omega D^-1 r (pre-smoothing from zero), t 
   double om;
   const double* r;
   double* t;
-  __device__ double2 in(int id, int, int, bool, double& aux) const {
+  struct Raw {
+    double2 dv, bv;
+    double d;
+  };
+  __device__ void fetch(int id, Raw& w) const {
+    w.dv = di(id);
+    w.bv = d2ldcg(r, id);
+    w.d = __ldg(d + id);
+  }
+  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
+    aux = w.d;
+    return make_double2(om * w.dv.x * w.bv.x, om * w.dv.y * w.bv.y);
+  }
+  __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
-    aux = __ldg(d + id);
-    const double2 dv = di(id), bv = d2ldcg(r, id);
-    return make_double2(om * dv.x * bv.x, om * dv.y * bv.y);
+    Raw w;
+    fetch(id, w);
+    return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2) const {
     const double2 bv = d2ldcg(r, id);
@@ -334,13 +360,26 @@ struct FineSmooth : FineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 
   const DMesh* mc;
   const double* ec;
   double* rz;
+  struct Raw {
+    double2 dv, bv;
+    double d;
+  };
+  __device__ void fetch(int id, Raw& w) const {
+    w.dv = di(id);
+    w.bv = d2ldcg(r, id);
+    w.d = __ldg(d + id);
+  }
+  __device__ double2 finish(const Raw& w, int, int i, int j, bool dup, double& aux) const {
+    aux = w.d;
+    const double2 pe = mg_prolong<GMem>(*mf, *mc, ec, i, j, dup);
+    return mask2(make_double2(om * w.dv.x * w.bv.x + pe.x, om * w.dv.y * w.bv.y + pe.y), w.dv);
+  }
   __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
-    aux = __ldg(d + id);
-    const double2 dv = di(id), bv = d2ldcg(r, id);
-    const double2 pe = mg_prolong<GMem>(*mf, *mc, ec, i, j, dup);
-    return mask2(make_double2(om * dv.x * bv.x + pe.x, om * dv.y * bv.y + pe.y), dv);
+    Raw w;
+    fetch(id, w);
+    return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2 y) const {
     const double2 dv = di(id), bv = d2ldcg(r, id);
@@ -358,11 +397,25 @@ struct FineWarm : FineBase {  // q_k = A u_k (masked); u_j.q_k (j <= k), u_k.b (
   int k;
   const double* b;
   double* acc;  // [MG_WARM + 2]: u_0.q_k .. u_k.q_k, u_k.b, b.b
-  __device__ double2 in(int id, int, int, bool, double& aux) const {
+  struct Raw {
+    double2 uv, dv;
+    double d;
+  };
+  __device__ void fetch(int id, Raw& w) const {
+    w.uv = __ldg(reinterpret_cast<const double2*>(u) + id);
+    w.dv = di(id);
+    w.d = __ldg(d + id);
+  }
+  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
+    aux = w.d;
+    return mask2(w.uv, w.dv);
+  }
+  __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
-    aux = __ldg(d + id);
-    return mask2(__ldg(reinterpret_cast<const double2*>(u) + id), di(id));
+    Raw w;
+    fetch(id, w);
+    return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2 uv) const {
     const double2 qv = mask2(Av, di(id));
@@ -387,13 +440,25 @@ __device__ __forceinline__ double mg_hash01(unsigned k) {
 struct FinePow : FineBase {  // power step vout = D^-1 A vin (vin == nullptr: hashed start)
   const double* vin;
   double* vout;
-  __device__ double2 in(int id, int, int, bool, double& aux) const {
+  struct Raw {
+    double2 v, dv;
+    double d;
+  };
+  __device__ void fetch(int id, Raw& w) const {
+    w.v = vin ? d2ldcg(vin, id) : make_double2(mg_hash01(2u * id + 1u), mg_hash01(2u * id + 2u));
+    w.dv = di(id);
+    w.d = __ldg(d + id);
+  }
+  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
+    aux = w.d;
+    return mask2(w.v, w.dv);
+  }
+  __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
-    aux = __ldg(d + id);
-    const double2 v = vin ? d2ldcg(vin, id)
-                          : make_double2(mg_hash01(2u * id + 1u), mg_hash01(2u * id + 2u));
-    return mask2(v, di(id));
+    Raw w;
+    fetch(id, w);
+    return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2) const {
     const double2 dv = di(id);
@@ -408,14 +473,26 @@ struct FinePcg : FineBase {  // p = z + beta p_old (owner stores), q = A p (mask
   double* pnew;
   double* q;
   double* pq;
-  __device__ double2 in(int id, int, int, bool, double& aux) const {
+  struct Raw {
+    double2 zv, po;
+    double d;
+  };
+  __device__ void fetch(int id, Raw& w) const {
+    w.zv = d2ldcg(z, id);
+    w.po = pold ? d2ldcg(pold, id) : make_double2(0.0, 0.0);
+    w.d = __ldg(d + id);
+  }
+  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
+    aux = w.d;
+    if (!pold) return w.zv;
+    return make_double2(w.zv.x + beta * w.po.x, w.zv.y + beta * w.po.y);
+  }
+  __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
-    aux = __ldg(d + id);
-    const double2 zv = d2ldcg(z, id);
-    if (!pold) return zv;
-    const double2 po = d2ldcg(pold, id);
-    return make_double2(zv.x + beta * po.x, zv.y + beta * po.y);
+    Raw w;
+    fetch(id, w);
+    return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2 p) const {
     const double2 qv = mask2(Av, di(id));
