@@ -124,7 +124,7 @@ struct pf_handle {
   // they are rebuilt when the iteration count drifts above the count right after the last
   // rebuild, when the Dirichlet set changes, or after mg_max_age solves (PFB200_MG_REUSE=0:
   // rebuild at every solve).  The fine level always uses the current tangent.
-  bool mg_built = false, mg_reuse = true;
+  bool mg_built = false, mg_reuse = true, mg_reuse_cap = false;
   long long mg_ref_iters = 0, mg_last_iters = 0;
   int mg_age = 0, mg_max_age = 64;
   long long mg_setups = 0;
@@ -1722,6 +1722,10 @@ static pf_status run_mg(pf_handle* h, double* target, int* status, long long* it
   const bool rebuild = force_setup || setup_only || !h->mg_reuse || !h->mg_built ||
                        h->mg_age >= h->mg_max_age ||
                        h->mg_last_iters > (h->mg_ref_iters * 5) / 4 + 2;
+  // a reused hierarchy gets an iteration budget: past it the solve reports CG_MAXITER and the
+  // caller redoes it on a fresh hierarchy (crack steps change the tangent quickly)
+  if (!rebuild && maxiter <= 0 && h->mg_reuse_cap)
+    h->mg_in->maxiter = std::min(h->mg_in->maxiter, std::max(50LL, 3 * h->mg_ref_iters + 20));
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
   PF_CUDA(cudaMemcpyAsync((void*)h->mga.in, h->mg_in, sizeof(pfb::MgIn), cudaMemcpyHostToDevice,
                           h->stream));
@@ -1841,7 +1845,25 @@ static pf_status momentum(pf_handle* h, const BcView& bc, bool apply_inc, double
       double* guess[pfb::WARM_MAX] = {};
       const int ng = (h->warm && n_nr == 0) ? h->warm_n[ws] : 0;
       for (int k = 0; k < ng; ++k) guess[k] = h->warm_buf[ws][k];
-      PF_TRY(run_cg(h, true, h->u, false, &status, &iters, guess, ng));
+      pf_status cst;
+      if (h->mg) {
+        h->mg_reuse_cap = true;
+        cst = run_cg(h, true, h->u, false, &status, &iters, guess, ng);
+        h->mg_reuse_cap = false;
+        if (cst == PF_ERR_SINGULAR && status == pfb::CG_MAXITER && h->mg_age > 1) {
+          // the reused hierarchy was too stale: u is untouched (target is updated only on
+          // convergence); rebuild and redo the solve from the same Newton residual
+          if (h->trace)
+            fprintf(stderr, "[pfb200] mg solve over budget (%lld iterations): rebuild, redo\n", iters);
+          PF_TRY(launch_mom_prepare(h, 1));
+          PF_TRY(finalize(h, 1));
+          h->mg_built = false;
+          cst = run_cg(h, true, h->u, false, &status, &iters, guess, ng);
+        }
+      } else {
+        cst = run_cg(h, true, h->u, false, &status, &iters, guess, ng);
+      }
+      PF_TRY(cst);
       if (h->trace)
         fprintf(stderr, "[pfb200] momentum pass %d newton %d warm %d iters %lld\n", pass, n_nr,
                 ng, iters);
