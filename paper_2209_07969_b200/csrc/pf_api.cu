@@ -23,6 +23,30 @@
 
 using pfb::CgResult;
 
+// One multigrid PCG instance (pf_mg.cuh): the momentum solves (phys 0) and the phase-field
+// solves without the SPD probe (phys 1, the scalar field embedded as the x component of a
+// two-component system) each have their own hierarchy, buffers and graphs.
+struct MgInst {
+  bool on = false;
+  pfb::MgArgs A{};
+  int gf = 1, gflat = 1;            // fine-march grid, flat-kernel grid
+  std::vector<int> gl;              // warp-item grid per level (row-chunk kernels)
+  std::vector<int> gn;              // node-parallel grid per level (assembled form)
+  std::vector<int> lpn;             // lanes per node of the level's node kernels (1 | 4 | 16)
+  pfb::MgIn* in = nullptr;          // pinned per-solve inputs (copied to A.in before a solve)
+  cudaGraphExec_t setup_exec = nullptr, solve_exec = nullptr;
+  // hierarchy reuse: the coarse levels (Galerkin matrices, omegas) are a preconditioner only;
+  // they are rebuilt when the iteration count drifts above the count right after the last
+  // rebuild, when the Dirichlet set changes, or after max_age solves (PFB200_MG_REUSE=0:
+  // rebuild at every solve).  The fine level always uses the current tangent.
+  bool built = false, reuse = true, reuse_cap = false;
+  long long ref_iters = 0, last_iters = 0;
+  int age = 0, max_age = 64;
+  long long setups = 0;
+  int setup_kernels = 0, body_kernels = 0;  // kernel nodes per graph (launch accounting)
+  bool fuse = true;  // fused down / up kernels on the half-warp levels (PFB200_MG_FUSE=0: off)
+};
+
 struct pf_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -110,27 +134,9 @@ struct pf_handle {
   double* gB = nullptr;     // [CG_SLOTS+1][2]  global r.r, r.D^-1.r
   cudaGraphExec_t dgraphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // dist chunks
   long long l2_bytes = 0;
-  // geometric-multigrid PCG for the momentum solves (pf_mg.cuh k_mgcg)
-  bool mg = false;
-  pfb::MgArgs mga{};
+  // geometric-multigrid PCG instances (momentum; phase field on large meshes)
+  MgInst mgu, mgd;
   std::vector<void*> mg_allocs;
-  int mg_gf = 1, mg_gflat = 1;            // fine-march grid, flat-kernel grid
-  std::vector<int> mg_gl;                 // warp-item grid per level (row-chunk kernels)
-  std::vector<int> mg_gn;                 // node-parallel grid per level (assembled form)
-  std::vector<int> mg_lpn;                // lanes per node of the level's node kernels (1 | 16)
-  pfb::MgIn* mg_in = nullptr;             // mapped pinned per-solve inputs
-  cudaGraphExec_t mg_setup_exec = nullptr, mg_solve_exec = nullptr;
-  // hierarchy reuse: the coarse levels (Galerkin matrices, omegas) are a preconditioner only;
-  // they are rebuilt when the iteration count drifts above the count right after the last
-  // rebuild, when the Dirichlet set changes, or after mg_max_age solves (PFB200_MG_REUSE=0:
-  // rebuild at every solve).  The fine level always uses the current tangent.
-  bool mg_built = false, mg_reuse = true, mg_reuse_cap = false;
-  long long mg_ref_iters = 0, mg_last_iters = 0;
-  int mg_age = 0, mg_max_age = 64;
-  long long mg_setups = 0;
-  int mg_setup_kernels = 0, mg_body_kernels = 0;  // kernel nodes per graph (launch accounting)
-  bool mg_fuse = true;  // fused down / up kernels on the half-warp levels (PFB200_MG_FUSE=0: off)
-
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
   bool umask_all_free = true, pmask_all_free = true;
@@ -265,9 +271,11 @@ extern "C" void pf_destroy(pf_handle* h) {
       if (p) cudaFree(p);
   for (void* p : h->mg_allocs)
     if (p) cudaFree(p);
-  if (h->mg_in) cudaFreeHost(h->mg_in);
-  if (h->mg_setup_exec) cudaGraphExecDestroy(h->mg_setup_exec);
-  if (h->mg_solve_exec) cudaGraphExecDestroy(h->mg_solve_exec);
+  for (MgInst* M : {&h->mgu, &h->mgd}) {
+    if (M->in) cudaFreeHost(M->in);
+    if (M->setup_exec) cudaGraphExecDestroy(M->setup_exec);
+    if (M->solve_exec) cudaGraphExecDestroy(M->solve_exec);
+  }
   if (h->stage) cudaFreeHost(h->stage);
   for (auto& row : h->graphs)
     for (auto& g : row)
@@ -498,11 +506,11 @@ static cudaError_t mg_alloc(pf_handle* h, T** p, size_t n) {
   return e;
 }
 
-static pf_status mg_build_graphs(pf_handle* h);
+static pf_status mg_build_graphs(pf_handle* h, MgInst& M);
 
-static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
+static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_warps) {
   const char* fz = getenv("PFB200_MG_FUSE");
-  h->mg_fuse = !(fz && std::string(fz) == "0");
+  M.fuse = !(fz && std::string(fz) == "0");
 
   const char* tl = getenv("PFB200_MG_TAIL");  // tail levels: at most this many nodes
   const int tail_nodes = tl ? std::max(0, atoi(tl)) : 1 << 30;
@@ -522,7 +530,7 @@ static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
   }
   const int nl = (int)lv.size();
   if (nl < 2) return PF_OK;  // nothing to agglomerate: Jacobi PCG
-  pfb::MgArgs& A = h->mga;
+  pfb::MgArgs& A = M.A;
   A = pfb::MgArgs{};
   A.C = h->C;
   A.n_levels = nl;
@@ -571,14 +579,14 @@ static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
       return fail(h, PF_ERR_CUDA, "k_mg_tail shared memory");
   }
   auto oom = [&]() { return fail(h, PF_ERR_CUDA, "multigrid allocation failed"); };
-  h->mg_gl.assign(nl, 1);
-  h->mg_gn.assign(nl, 1);
-  h->mg_lpn.assign(nl, 16);
+  M.gl.assign(nl, 1);
+  M.gn.assign(nl, 1);
+  M.lpn.assign(nl, 16);
   int coarse_items = 0;
   for (int l = 0; l < nl; ++l) {
     const HostLevel& L = lv[l];
-    pfb::MgLevel& M = A.L[l];
-    pfb::DMesh& dm = M.m;
+    pfb::MgLevel& ML = A.L[l];
+    pfb::DMesh& dm = ML.m;
     if (l == 0) {
       dm = h->dm;
     } else {
@@ -598,80 +606,96 @@ static pf_status mg_setup(pf_handle* h, int fine_resident_warps) {
       dm.n_nodes = L.n_nodes; dm.n_elems = L.n_elems;
       dm.own_lo = 0; dm.own_hi = L.n_nodes; dm.dup_lo = L.n_nodes;
       dm.cell_lo = 0; dm.cell_hi = L.n_elems;
-      if (mg_alloc(h, &M.K, 64 * (size_t)L.n_elems) != cudaSuccess ||
-          mg_alloc(h, &M.dinv, 2 * (size_t)L.n_nodes) != cudaSuccess ||
-          mg_alloc(h, &M.b, 2 * (size_t)L.n_nodes) != cudaSuccess ||
-          mg_alloc(h, &M.e, 2 * (size_t)L.n_nodes) != cudaSuccess)
+      if (mg_alloc(h, &ML.K, 64 * (size_t)L.n_elems) != cudaSuccess ||
+          mg_alloc(h, &ML.dinv, 2 * (size_t)L.n_nodes) != cudaSuccess ||
+          mg_alloc(h, &ML.b, 2 * (size_t)L.n_nodes) != cudaSuccess ||
+          mg_alloc(h, &ML.e, 2 * (size_t)L.n_nodes) != cudaSuccess)
         return oom();
-      M.items = pfb::mg_items(L.nx, L.ny, L.notch_row >= 0);
-      M.item_off = coarse_items;  // node offset in the concatenated coarse node space (even)
+      ML.items = pfb::mg_items(L.nx, L.ny, L.notch_row >= 0);
+      ML.item_off = coarse_items;  // node offset in the concatenated coarse node space (even)
       coarse_items += (L.n_nodes + 1) & ~1;
-      h->mg_gl[l] = (M.items + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+      M.gl[l] = (ML.items + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
       // small levels: a half-warp per node (all loads of a node in flight); large levels: a
       // thread per node (latency hidden by occupancy).  Threshold: 16 lanes per node would
       // exceed one wave of resident threads.
       const long long wave = 2048LL * h->sm_count;
-      h->mg_lpn[l] = 16LL * L.n_nodes <= wave ? 16 : (4LL * L.n_nodes <= wave ? 4 : 1);
-      h->mg_gn[l] = std::max(1, std::min((int)((h->mg_lpn[l] * (long long)L.n_nodes + pfb::MG_NT - 1) / pfb::MG_NT),
+      M.lpn[l] = 16LL * L.n_nodes <= wave ? 16 : (4LL * L.n_nodes <= wave ? 4 : 1);
+      M.gn[l] = std::max(1, std::min((int)((M.lpn[l] * (long long)L.n_nodes + pfb::MG_NT - 1) / pfb::MG_NT),
                                          16 * h->sm_count));
       {  // assembled-form index tables (static per handle)
         const std::vector<int> nb = hl_stencil_ids(L), rd = hl_restrict_ids(lv[l - 1], L);
         int *dnb = nullptr, *drd = nullptr;
         if (mg_alloc(h, &dnb, nb.size()) != cudaSuccess || mg_alloc(h, &drd, rd.size()) != cudaSuccess ||
-            mg_alloc(h, &M.S, (size_t)4 * pfb::MG_NS * L.n_nodes) != cudaSuccess)
+            mg_alloc(h, &ML.S, (size_t)4 * pfb::MG_NS * L.n_nodes) != cudaSuccess)
           return oom();
         cudaMemcpy(dnb, nb.data(), nb.size() * sizeof(int), cudaMemcpyHostToDevice);
         cudaMemcpy(drd, rd.data(), rd.size() * sizeof(int), cudaMemcpyHostToDevice);
-        M.nbr = dnb;
-        M.rid = drd;
+        ML.nbr = dnb;
+        ML.rid = drd;
         if (l + 1 < nl) {
           const std::vector<int> pd = hl_prolong_ids(L, lv[l + 1]);
           int* dpd = nullptr;
           if (mg_alloc(h, &dpd, pd.size()) != cudaSuccess) return oom();
           cudaMemcpy(dpd, pd.data(), pd.size() * sizeof(int), cudaMemcpyHostToDevice);
-          M.pid = dpd;
+          ML.pid = dpd;
         }
       }
     }
-    if (mg_alloc(h, &M.t, 2 * (size_t)L.n_nodes) != cudaSuccess) return oom();
+    if (mg_alloc(h, &ML.t, 2 * (size_t)L.n_nodes) != cudaSuccess) return oom();
   }
   A.coarse_items = coarse_items;
   A.g0 = pfb::make_march_geom(h->nx, h->ny, fine_resident_warps);
-  h->mg_gf = (A.g0.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
-  h->mg_gflat = 2 * h->sm_count;
+  M.gf = (A.g0.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+  M.gflat = 2 * h->sm_count;
   if (mg_alloc(h, &A.z, 2 * (size_t)h->n_nodes) != cudaSuccess) return oom();
-  A.L[0].dinv = h->dinvu;
+  A.phys = phys;
+  if (phys == 0) {
+    A.L[0].dinv = h->dinvu;
+  } else {  // phase field: scalar vectors packed as (value, 0) per node (y dofs dead)
+    double* dinv2 = nullptr;
+    if (mg_alloc(h, &dinv2, 2 * (size_t)h->n_nodes) != cudaSuccess) return oom();
+    A.L[0].dinv = dinv2;
+  }
   A.L[0].e = A.z;
   const int ndc = 2 * lv.back().n_nodes;
   if (A.dense && mg_alloc(h, &A.Ainv, (size_t)ndc * ndc) != cudaSuccess) return oom();
   const size_t npart = std::max<size_t>(
-      std::max<size_t>((size_t)2 * h->mg_gf + h->mg_gflat, (size_t)h->mg_gflat * 2 * pfb::MG_MAXL),
-      (size_t)pfb::MG_WP * h->mg_gf + h->mg_gflat);
+      std::max<size_t>((size_t)2 * M.gf + M.gflat, (size_t)M.gflat * 2 * pfb::MG_MAXL),
+      (size_t)pfb::MG_WP * M.gf + M.gflat);
   if (mg_alloc(h, &A.part, npart) != cudaSuccess || mg_alloc(h, &A.ctl, 1) != cudaSuccess)
     return oom();
   // per-solve inputs: written on the host (pinned), copied to the device before each solve
-  if (cudaHostAlloc((void**)&h->mg_in, sizeof(pfb::MgIn), cudaHostAllocDefault) != cudaSuccess)
+  if (cudaHostAlloc((void**)&M.in, sizeof(pfb::MgIn), cudaHostAllocDefault) != cudaSuccess)
     return oom();
   pfb::MgIn* din = nullptr;
   if (mg_alloc(h, &din, 1) != cudaSuccess) return oom();
   A.in = din;
   A.d = h->d;
   A.flags = h->flags;
-  A.x = h->xu; A.r = h->ru; A.p0 = h->p0u; A.p1 = h->p1u; A.q = h->qu;
+  A.bq = h->b;
+  if (phys == 0) {
+    A.x = h->xu; A.r = h->ru; A.p0 = h->p0u; A.p1 = h->p1u; A.q = h->qu;
+  } else {
+    const size_t n2 = 2 * (size_t)h->n_nodes;
+    if (mg_alloc(h, &A.x, n2) != cudaSuccess || mg_alloc(h, &A.r, n2) != cudaSuccess ||
+        mg_alloc(h, &A.p0, n2) != cudaSuccess || mg_alloc(h, &A.p1, n2) != cudaSuccess ||
+        mg_alloc(h, &A.q, n2) != cudaSuccess)
+      return oom();
+  }
   A.result = h->d_cgres;
   A.ndof = 2LL * h->n_nodes;
   if (getenv("PFB200_MG_TAILCLK")) {
     if (mg_alloc(h, &A.tclk, 32) != cudaSuccess) return oom();
   }
-  PF_TRY(mg_build_graphs(h));
-  h->mg = true;
+  PF_TRY(mg_build_graphs(h, M));
+  M.on = true;
   return PF_OK;
 }
 
 // Two graphs per handle: the hierarchy setup (Galerkin levels, diagonals, power steps, omega,
 // dense coarsest inverse) and the solve (init, WHILE {one PCG iteration}, finish).
-static pf_status mg_build_graphs(pf_handle* h) {
-  pfb::MgArgs& A = h->mga;
+static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
+  pfb::MgArgs& A = M.A;
   const int nl = A.n_levels;
   cudaStream_t s = h->stream;
   // ---- setup graph
@@ -681,17 +705,17 @@ static pf_status mg_build_graphs(pf_handle* h) {
     for (int lc = 1; lc < nl; ++lc) {
       const int cells = A.L[lc].m.nx * A.L[lc].m.ny;
       pfb::k_mg_galerkin<<<(cells + pfb::MG_WARPS - 1) / pfb::MG_WARPS, pfb::MG_NT, 0, s>>>(A, lc);
-      pfb::k_mg_stencil<<<h->mg_gl[lc], pfb::MG_NT, 0, s>>>(A, lc);
+      pfb::k_mg_stencil<<<M.gl[lc], pfb::MG_NT, 0, s>>>(A, lc);
     }
     if (A.dense) pfb::k_mg_dense<<<1, pfb::MG_NT, 0, s>>>(A);
-    h->mg_setup_kernels = 2 * (nl - 1) + (A.dense ? 1 : 0) + pfb::MG_POW + 1;
+    M.setup_kernels = 2 * (nl - 1) + (A.dense ? 1 : 0) + pfb::MG_POW + 1;
     const int cb = (16 * A.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
     for (int k = 1; k <= pfb::MG_POW; ++k)
-      pfb::k_mg_pow<<<h->mg_gf + cb, pfb::MG_NT, 0, s>>>(A, k, h->mg_gf);
+      pfb::k_mg_pow<<<M.gf + cb, pfb::MG_NT, 0, s>>>(A, k, M.gf);
     pfb::k_mg_lambda<<<32, pfb::MG_NT, 0, s>>>(A);  // few CTAs: 2 MG_MAXL partials each
     cudaError_t e = cudaStreamEndCapture(s, &g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG setup capture: ") + cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&h->mg_setup_exec, g, 0);
+    e = cudaGraphInstantiate(&M.setup_exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG setup graph: ") + cudaGetErrorString(e));
   }
@@ -699,16 +723,16 @@ static pf_status mg_build_graphs(pf_handle* h) {
   // only): N unconditional iterations instead of the WHILE node, so ncu sees every kernel.
 #define MG_NODE_KERNEL(K, l, ...)                                                   \
   do {                                                                              \
-    if (h->mg_lpn[l] == 16) pfb::K<16><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__); \
-    else if (h->mg_lpn[l] == 4) pfb::K<4><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__); \
-    else pfb::K<1><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__);                     \
+    if (M.lpn[l] == 16) pfb::K<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__); \
+    else if (M.lpn[l] == 4) pfb::K<4><<<M.gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__); \
+    else pfb::K<1><<<M.gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__);                     \
   } while (0)
   auto body_kernels = [&](const pfb::MgArgs& B) {
     const int c = nl - 1, top = std::min(B.n_tail, c);  // grid levels [1, top)
-    pfb::k_mg_fine_resid<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B);
+    pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(B);
     for (int l = 1; l < top; ++l) {
-      if (h->mg_lpn[l] == 16 && h->mg_fuse) {  // small levels: one fused kernel per direction
-        pfb::k_mg_sdown<16><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(B, l);
+      if (M.lpn[l] == 16 && M.fuse) {  // small levels: one fused kernel per direction
+        pfb::k_mg_sdown<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
       } else {
         MG_NODE_KERNEL(k_mg_srestrict, l, B, l);
         MG_NODE_KERNEL(k_mg_sresid, l, B, l);
@@ -723,27 +747,27 @@ static pf_status mg_build_graphs(pf_handle* h) {
       } else {
         double* bufs[2] = {B.L[c].e, B.L[c].t};
         int cur = (B.nu_c - 1) % 2 == 0 ? 0 : 1;
-        pfb::k_mg_jacobi0<<<h->mg_gn[c], pfb::MG_NT, 0, s>>>(B, c, bufs[cur]);
+        pfb::k_mg_jacobi0<<<M.gn[c], pfb::MG_NT, 0, s>>>(B, c, bufs[cur]);
         for (int k = 1; k < B.nu_c; ++k, cur ^= 1)
           MG_NODE_KERNEL(k_mg_ssweep, c, B, c, bufs[cur], bufs[cur ^ 1]);
       }
     }
     for (int l = top - 1; l >= 1; --l) {
-      if (h->mg_lpn[l] == 16 && h->mg_fuse) {
-        pfb::k_mg_sup<16><<<h->mg_gn[l], pfb::MG_NT, 0, s>>>(B, l);
+      if (M.lpn[l] == 16 && M.fuse) {
+        pfb::k_mg_sup<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
       } else {
         MG_NODE_KERNEL(k_mg_sprolongate, l, B, l);
         MG_NODE_KERNEL(k_mg_ssmooth, l, B, l);
       }
     }
-    pfb::k_mg_fine_smooth<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B);
-    pfb::k_mg_pcg<<<h->mg_gf, pfb::MG_NT, 0, s>>>(B, h->mg_gf);
-    pfb::k_mg_update<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(B, h->mg_gf, h->mg_gf);
+    pfb::k_mg_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(B);
+    pfb::k_mg_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(B, M.gf);
+    pfb::k_mg_update<<<M.gflat, pfb::MG_NT, 0, s>>>(B, M.gf, M.gf);
   };
   {
     const int c = nl - 1, top = std::min(A.n_tail, c);
-    h->mg_body_kernels = 1 + 3 + (A.n_tail < nl ? 1 : 1 + (A.dense ? 1 : A.nu_c));
-    for (int l = 1; l < top; ++l) h->mg_body_kernels += (h->mg_lpn[l] == 16 && h->mg_fuse) ? 2 : 4;
+    M.body_kernels = 1 + 3 + (A.n_tail < nl ? 1 : 1 + (A.dense ? 1 : A.nu_c));
+    for (int l = 1; l < top; ++l) M.body_kernels += (M.lpn[l] == 16 && M.fuse) ? 2 : 4;
   }
   const char* un = getenv("PFB200_MG_UNROLL");
   const int unroll = un ? std::max(0, atoi(un)) : 0;
@@ -751,12 +775,12 @@ static pf_status mg_build_graphs(pf_handle* h) {
     cudaGraph_t g = nullptr;
     A.use_cond = 0;
     PF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    for (int k = 0; k < pfb::MG_WARM; ++k) pfb::k_mg_warm_q<<<h->mg_gf, pfb::MG_NT, 0, s>>>(A, k);
-    pfb::k_mg_init<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A, h->mg_gf);
+    for (int k = 0; k < pfb::MG_WARM; ++k) pfb::k_mg_warm_q<<<M.gf, pfb::MG_NT, 0, s>>>(A, k);
+    pfb::k_mg_init<<<M.gflat, pfb::MG_NT, 0, s>>>(A, M.gf);
     for (int it = 0; it < unroll; ++it) body_kernels(A);
-    pfb::k_mg_finish<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A);
+    pfb::k_mg_finish<<<M.gflat, pfb::MG_NT, 0, s>>>(A);
     PF_CUDA(cudaStreamEndCapture(s, &g));
-    cudaError_t e = cudaGraphInstantiate(&h->mg_solve_exec, g, 0);
+    cudaError_t e = cudaGraphInstantiate(&M.solve_exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG solve graph: ") + cudaGetErrorString(e));
     return PF_OK;
@@ -769,8 +793,8 @@ static pf_status mg_build_graphs(pf_handle* h) {
     cudaGraphNode_t n_init = nullptr, n_while = nullptr, n_fin = nullptr;
     {
       PF_CUDA(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-      for (int k = 0; k < pfb::MG_WARM; ++k) pfb::k_mg_warm_q<<<h->mg_gf, pfb::MG_NT, 0, s>>>(A, k);
-      pfb::k_mg_init<<<h->mg_gflat, pfb::MG_NT, 0, s>>>(A, h->mg_gf);
+      for (int k = 0; k < pfb::MG_WARM; ++k) pfb::k_mg_warm_q<<<M.gf, pfb::MG_NT, 0, s>>>(A, k);
+      pfb::k_mg_init<<<M.gflat, pfb::MG_NT, 0, s>>>(A, M.gf);
       cudaGraph_t gg = g;
       PF_CUDA(cudaStreamEndCapture(s, &gg));
       size_t nn = 0;
@@ -802,12 +826,12 @@ static pf_status mg_build_graphs(pf_handle* h) {
       kp.type = cudaGraphNodeTypeKernel;
       void* args[] = {&A};
       kp.kernel.func = (void*)pfb::k_mg_finish;
-      kp.kernel.gridDim = dim3(h->mg_gflat);
+      kp.kernel.gridDim = dim3(M.gflat);
       kp.kernel.blockDim = dim3(pfb::MG_NT);
       kp.kernel.kernelParams = args;
       PF_CUDA(cudaGraphAddNode(&n_fin, g, &n_while, 1, &kp));
     }
-    cudaError_t e = cudaGraphInstantiate(&h->mg_solve_exec, g, 0);
+    cudaError_t e = cudaGraphInstantiate(&M.solve_exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG solve graph: ") + cudaGetErrorString(e));
   }
@@ -1106,12 +1130,21 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
       CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_mg_fine_resid, pfb::MG_NT, 0));
       om = std::min(om, o2);
       if (om >= 1) {
-        pf_status ms = mg_setup(h, om * dev_sms * pfb::MG_WARPS);
+        pf_status ms = mg_setup(h, h->mgu, 0, om * dev_sms * pfb::MG_WARPS);
         if (ms != PF_OK) return bail(ms);
+        // phase-field multigrid (solves without the SPD probe) where Jacobi PCG iteration
+        // counts get large: deep hierarchies on big meshes (PFB200_MG_EVO=1/0: force on/off)
+        const char* me = getenv("PFB200_MG_EVO");
+        const bool evo_auto = h->mgu.on && h->mgu.A.n_levels >= 5 && h->n_nodes >= 500000;
+        const bool evo = me ? std::string(me) == "1" : evo_auto;
+        if (evo && h->mgu.on) {
+          pf_status es = mg_setup(h, h->mgd, 1, om * dev_sms * pfb::MG_WARPS);
+          if (es != PF_OK) return bail(es);
+        }
         const char* mw = getenv("PFB200_MG_WARM");  // "0": MG solves start cold (x0 = 0)
-        if (h->mg && mw && std::string(mw) == "0") h->warm = false;
+        if (h->mgu.on && mw && std::string(mw) == "0") h->warm = false;
         const char* ru = getenv("PFB200_MG_REUSE");
-        h->mg_reuse = !(ru && std::string(ru) == "0");
+        h->mgu.reuse = h->mgd.reuse = !(ru && std::string(ru) == "0");
       }
     }
   }
@@ -1360,7 +1393,7 @@ static pf_status set_umask(pf_handle* h, const std::vector<int64_t>& cons) {
   }
   PF_CUDA(cudaMemcpyAsync(h->umask, m.data(), n, cudaMemcpyHostToDevice, h->stream));
   PF_CUDA(cudaStreamSynchronize(h->stream));
-  h->mg_built = false;  // the Galerkin levels are masked at the Dirichlet dofs
+  h->mgu.built = false;  // the Galerkin levels are masked at the Dirichlet dofs
   h->cons_key = cons;
   h->umask_all_free = cons.empty();
   return PF_OK;
@@ -1378,6 +1411,7 @@ static pf_status set_pmask(pf_handle* h, const int64_t* pins, int64_t n_pins) {
   PF_CUDA(cudaMemcpyAsync(h->pmask, m.data(), n, cudaMemcpyHostToDevice, h->stream));
   PF_CUDA(cudaStreamSynchronize(h->stream));
   h->n_pinned = (int64_t)std::count(m.begin(), m.end(), (uint8_t)0);
+  h->mgd.built = false;  // the phase-field Galerkin levels are masked at the pinned nodes
   h->pins_key = key;
   h->pmask_all_free = key.empty();
   return PF_OK;
@@ -1709,33 +1743,33 @@ static pf_status run_cg_dist(pf_handle* h, bool mom, double* target, bool probe,
 
 // one MG-PCG solve: setup graph (hierarchy at the current tangent), then the solve graph whose
 // PCG loop is a device-side WHILE node; the host waits once, at the end
-static pf_status run_mg(pf_handle* h, double* target, int* status, long long* iters,
+static pf_status run_mg(pf_handle* h, MgInst& M, double* target, int* status, long long* iters,
                         int setup_only = 0, long long maxiter = -1, double rtol = -1.0,
                         bool check = true, bool force_setup = false,
                         double* const* guess = nullptr, int n_guess = 0) {
-  h->mg_in->n_guess = std::min(n_guess, pfb::MG_WARM);
-  for (int k = 0; k < pfb::MG_WARM; ++k) h->mg_in->guess[k] = k < h->mg_in->n_guess ? guess[k] : nullptr;
-  h->mg_in->rtol = rtol >= 0.0 ? rtol : h->cfg.cg_rtol;
-  h->mg_in->maxiter = maxiter > 0 ? maxiter
+  M.in->n_guess = std::min(n_guess, pfb::MG_WARM);
+  for (int k = 0; k < pfb::MG_WARM; ++k) M.in->guess[k] = k < M.in->n_guess ? guess[k] : nullptr;
+  M.in->rtol = rtol >= 0.0 ? rtol : h->cfg.cg_rtol;
+  M.in->maxiter = maxiter > 0 ? maxiter
                                   : (long long)h->cfg.cg_maxiter_factor * 2LL * h->n_nodes;
-  h->mg_in->target = target;
-  const bool rebuild = force_setup || setup_only || !h->mg_reuse || !h->mg_built ||
-                       h->mg_age >= h->mg_max_age ||
-                       h->mg_last_iters > (h->mg_ref_iters * 5) / 4 + 2;
+  M.in->target = target;
+  const bool rebuild = force_setup || setup_only || !M.reuse || !M.built ||
+                       M.age >= M.max_age ||
+                       M.last_iters > (M.ref_iters * 5) / 4 + 2;
   // a reused hierarchy gets an iteration budget: past it the solve reports CG_MAXITER and the
   // caller redoes it on a fresh hierarchy (crack steps change the tangent quickly)
-  if (!rebuild && maxiter <= 0 && h->mg_reuse_cap)
-    h->mg_in->maxiter = std::min(h->mg_in->maxiter, std::max(50LL, 3 * h->mg_ref_iters + 20));
+  if (!rebuild && maxiter <= 0 && M.reuse_cap)
+    M.in->maxiter = std::min(M.in->maxiter, std::max(50LL, 3 * M.ref_iters + 20));
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
-  PF_CUDA(cudaMemcpyAsync((void*)h->mga.in, h->mg_in, sizeof(pfb::MgIn), cudaMemcpyHostToDevice,
+  PF_CUDA(cudaMemcpyAsync((void*)M.A.in, M.in, sizeof(pfb::MgIn), cudaMemcpyHostToDevice,
                           h->stream));
   if (rebuild) {
-    PF_CUDA(cudaGraphLaunch(h->mg_setup_exec, h->stream));
+    PF_CUDA(cudaGraphLaunch(M.setup_exec, h->stream));
     PF_TRY(launched(h));
-    h->mg_setups += 1;
+    M.setups += 1;
   }
   if (!setup_only) {
-    PF_CUDA(cudaGraphLaunch(h->mg_solve_exec, h->stream));
+    PF_CUDA(cudaGraphLaunch(M.solve_exec, h->stream));
     PF_TRY(launched(h));
   }
   PF_CUDA(cudaEventRecord(h->ev1, h->stream));
@@ -1743,37 +1777,37 @@ static pf_status run_mg(pf_handle* h, double* target, int* status, long long* it
   float ms = 0.f;
   PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   if (rebuild) {
-    h->mg_built = true;
-    h->mg_age = 0;
+    M.built = true;
+    M.age = 0;
   }
   if (setup_only) return PF_OK;
   *status = h->h_cgres->status;
   *iters = h->h_cgres->iters;
-  if (rebuild) h->mg_ref_iters = *iters;
-  h->mg_last_iters = *iters;
+  if (rebuild) M.ref_iters = *iters;
+  M.last_iters = *iters;
   // kernels executed inside the graphs (each graph launch counted one by launched())
-  h->acc.launches += (rebuild ? h->mg_setup_kernels - 1 : 0) +
-                     (setup_only ? 0 : pfb::MG_WARM + 1 + (int)(*iters) * h->mg_body_kernels);
+  h->acc.launches += (rebuild ? M.setup_kernels - 1 : 0) +
+                     (setup_only ? 0 : pfb::MG_WARM + 1 + (int)(*iters) * M.body_kernels);
   if (h->trace)
     fprintf(stderr, "[pfb200] mg solve: %lld iterations, %.3f ms%s\n", *iters, ms,
             rebuild ? " (hierarchy rebuilt)" : "");
-  if (h->mga.tclk) {
+  if (M.A.tclk) {
     long long c[32] = {};
-    cudaMemcpy(c, h->mga.tclk, sizeof c, cudaMemcpyDeviceToHost);
+    cudaMemcpy(c, M.A.tclk, sizeof c, cudaMemcpyDeviceToHost);
     fprintf(stderr, "[pfb200] tail phases (cycles):");
     for (int k = 1; k < 32 && c[k]; ++k) fprintf(stderr, " %lld", c[k] - c[k - 1]);
     fprintf(stderr, "\n");
   }
-  h->mg_age += 1;
+  M.age += 1;
   if (!check) return PF_OK;
-  cg_account(h, true, *iters, ms);
+  cg_account(h, M.A.phys == 0, *iters, ms);
   return cg_status(h, *status, *iters);
 }
 
 static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
                         long long* iters, double* const* guess = nullptr, int n_guess = 0) {
-  if (mom && h->mg && !probe)
-    return run_mg(h, target, status, iters, 0, -1, -1.0, true, false, guess, n_guess);
+  if (mom && h->mgu.on && !probe)
+    return run_mg(h, h->mgu, target, status, iters, 0, -1, -1.0, true, false, guess, n_guess);
   if (h->comm) return run_cg_dist(h, mom, target, probe, status, iters);
   return h->split ? run_cg_split(h, mom, target, probe, status, iters)
                   : run_cg_persistent(h, mom, target, probe, status, iters, guess, n_guess);
@@ -1846,18 +1880,18 @@ static pf_status momentum(pf_handle* h, const BcView& bc, bool apply_inc, double
       const int ng = (h->warm && n_nr == 0) ? h->warm_n[ws] : 0;
       for (int k = 0; k < ng; ++k) guess[k] = h->warm_buf[ws][k];
       pf_status cst;
-      if (h->mg) {
-        h->mg_reuse_cap = true;
+      if (h->mgu.on) {
+        h->mgu.reuse_cap = true;
         cst = run_cg(h, true, h->u, false, &status, &iters, guess, ng);
-        h->mg_reuse_cap = false;
-        if (cst == PF_ERR_SINGULAR && status == pfb::CG_MAXITER && h->mg_age > 1) {
+        h->mgu.reuse_cap = false;
+        if (cst == PF_ERR_SINGULAR && status == pfb::CG_MAXITER && h->mgu.age > 1) {
           // the reused hierarchy was too stale: u is untouched (target is updated only on
           // convergence); rebuild and redo the solve from the same Newton residual
           if (h->trace)
             fprintf(stderr, "[pfb200] mg solve over budget (%lld iterations): rebuild, redo\n", iters);
           PF_TRY(launch_mom_prepare(h, 1));
           PF_TRY(finalize(h, 1));
-          h->mg_built = false;
+          h->mgu.built = false;
           cst = run_cg(h, true, h->u, false, &status, &iters, guess, ng);
         }
       } else {
@@ -1955,7 +1989,34 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
       const int ng = use_warm ? h->warm_nd[ws] : 0;
       for (int k = 0; k < ng; ++k) guess[k] = h->warm_d[ws][k];
       bool done = false;
-      if (h->sr_evo && !h->comm && !h->split) {
+      if (h->mgd.on && !h->comm) {
+        // multigrid PCG on the packed two-component layout (pf_mg.cuh, phys 1)
+        const long long n = h->n_nodes;
+        const unsigned gb = (unsigned)std::min<long long>((n + 255) / 256, 8LL * h->sm_count);
+        auto attempt = [&](bool cap) -> pf_status {
+          pfb::k_mg_pack2<<<gb, 256, 0, h->stream>>>(h->mgd.A.r, h->rd, n);
+          pfb::k_mg_pack2<<<gb, 256, 0, h->stream>>>(h->mgd.A.L[0].dinv, h->dinvd, n);
+          PF_TRY(launched(h));
+          h->mgd.reuse_cap = cap;
+          const pf_status st2 = run_mg(h, h->mgd, nullptr, &status, &iters);
+          h->mgd.reuse_cap = false;
+          return st2;
+        };
+        pf_status est = attempt(true);
+        if (est == PF_ERR_SINGULAR && status == pfb::CG_MAXITER && h->mgd.age > 1) {
+          if (h->trace)
+            fprintf(stderr, "[pfb200] phase-field mg solve over budget (%lld iterations): "
+                            "rebuild, redo\n", iters);
+          PF_TRY(launch_evo_prepare(h, 1, 0));
+          h->mgd.built = false;
+          est = attempt(false);
+        }
+        PF_TRY(est);
+        pfb::k_mg_unpack_add<<<gb, 256, 0, h->stream>>>(h->xd, h->d, h->mgd.A.x, n);
+        PF_TRY(launched(h));
+        done = true;
+      }
+      if (!done && h->sr_evo && !h->comm && !h->split) {
         // single-reduction PCG with an iteration cap (4x the last converged phase-field solve);
         // d is updated only after it converged
         const long long cap = std::max(300LL, 4 * h->evo_last_iters);
@@ -2249,11 +2310,11 @@ extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, doub
   PF_CUDA(cudaSetDevice(h->device));
   if (n_iter < 1 || physics < 0 || physics > 2) return fail(h, PF_ERR_INVALID, "bad arguments");
   if (physics == 2) {  // multigrid-preconditioned momentum PCG
-    if (!h->mg) return fail(h, PF_ERR_INVALID, "no multigrid hierarchy on this handle");
+    if (!h->mgu.on) return fail(h, PF_ERR_INVALID, "no multigrid hierarchy on this handle");
     PF_TRY(launch_mom_prepare(h, 1));
     int status = 0;
     long long iters = 0;
-    PF_TRY(run_mg(h, nullptr, &status, &iters, 0, n_iter, 0.0, false, true));
+    PF_TRY(run_mg(h, h->mgu, nullptr, &status, &iters, 0, n_iter, 0.0, false, true));
     float ms = 0.f;
     PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
     if (ms_out) *ms_out = ms;
@@ -2286,16 +2347,16 @@ extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, doub
 extern "C" pf_status pf_mg_info(pf_handle* h, int32_t* n_levels, int32_t* n_grid,
                                 int32_t* dense, int64_t* setups, double* omega) {
   PF_CUDA(cudaSetDevice(h->device));
-  if (setups) *setups = h->mg_setups;
-  if (n_levels) *n_levels = h->mg ? h->mga.n_levels : 0;
-  if (n_grid) *n_grid = h->mg ? h->mga.n_tail : 0;
-  if (dense) *dense = h->mg ? h->mga.dense : 0;
-  if (!h->mg || !omega) return PF_OK;
+  if (setups) *setups = h->mgu.setups;
+  if (n_levels) *n_levels = h->mgu.on ? h->mgu.A.n_levels : 0;
+  if (n_grid) *n_grid = h->mgu.on ? h->mgu.A.n_tail : 0;
+  if (dense) *dense = h->mgu.on ? h->mgu.A.dense : 0;
+  if (!h->mgu.on || !omega) return PF_OK;
   PF_TRY(launch_mom_prepare(h, 1));
   int status = 0;
   long long iters = 0;
-  PF_TRY(run_mg(h, nullptr, &status, &iters, 1));
-  PF_CUDA(cudaMemcpy(omega, h->mga.ctl->omega, h->mga.n_levels * sizeof(double),
+  PF_TRY(run_mg(h, h->mgu, nullptr, &status, &iters, 1));
+  PF_CUDA(cudaMemcpy(omega, h->mgu.A.ctl->omega, h->mgu.A.n_levels * sizeof(double),
                      cudaMemcpyDeviceToHost));
   return PF_OK;
 }

@@ -86,8 +86,10 @@ struct MgArgs {
   MgLevel L[MG_MAXL];
   MarchGeom g0;          // march units of the fine level
   int coarse_items;      // sum of items over levels >= 1
-  const double* d;       // nodal d (level-0 operator)
-  const uint8_t* flags;  // level-0 tangent branch bits
+  int phys;              // 0: momentum K_uu(u, d); 1: phase field (x component, y dead)
+  const double* d;       // nodal d (level-0 momentum operator)
+  const uint8_t* flags;  // level-0 tangent branch bits (momentum)
+  const double* bq;      // level-0 Newton coefficient b per Gauss point [n_elems][4] (phase field)
   double *x, *r, *z, *p0, *p1, *q;
   double* Ainv;          // [nd*nd] dense inverse of the coarsest level
   double* part;          // per-CTA partial sums (>= max grid * 2 * MG_MAXL)
@@ -273,9 +275,22 @@ struct FineBase {
   const uint8_t* flags;
   const double* d;
   const double* dinv;
+  int phys;
+  const double* bq;
   __device__ void cell(int eid, const double2 (&v)[4], const double (&a)[4],
                        double2 (&f)[4]) const {
-    mom_cell_fast(*C, v, a, __ldg(flags + eid), f);
+    if (phys == 0) {
+      mom_cell_fast(*C, v, a, __ldg(flags + eid), f);
+    } else {  // phase field (pf_cg.cuh evo_cell_apply) on the x components
+      const double2 b01 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid);
+      const double2 b23 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid + 1);
+      const double pc[4] = {v[0].x, v[1].x, v[2].x, v[3].x};
+      const double bb[4] = {b01.x, b01.y, b23.x, b23.y};
+      double fx[4];
+      evo_cell_apply(*C, pc, bb, fx);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) f[k] = make_double2(fx[k], 0.0);
+    }
   }
   __device__ double2 di(int id) const { return __ldg(reinterpret_cast<const double2*>(dinv) + id); }
 };
@@ -922,7 +937,7 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_warm_q(MgArgs A, int k) {
   double acc[MG_WARM + 2];
 #pragma unroll
   for (int j = 0; j < MG_WARM + 2; ++j) acc[j] = 0.0;
-  FineWarm op{{&A.C, A.flags, A.d, A.L[0].dinv}, (const double*)in->guess[k], mg_warm_q(A, k),
+  FineWarm op{{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq}, (const double*)in->guess[k], mg_warm_q(A, k),
               {(const double*)in->guess[0], (const double*)in->guess[1], (const double*)in->guess[2]},
               k, A.r, acc};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
@@ -1039,7 +1054,7 @@ __global__ void __launch_bounds__(MG_NT) k_mg_init(MgArgs A, int n_wparts) {
 __global__ void __launch_bounds__(MG_NT, 2) k_mg_fine_resid(MgArgs A) {
   __shared__ MgWarp ws[MG_WARPS];
   const double om = __ldcg(&A.ctl->omega[0]);
-  FineResid op{{&A.C, A.flags, A.d, A.L[0].dinv}, om, A.r, A.L[0].t};
+  FineResid op{{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq}, om, A.r, A.L[0].t};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
 }
@@ -1316,7 +1331,7 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_fine_smooth(MgArgs A) {
   __shared__ double red[MG_WARPS];
   const double om = __ldcg(&A.ctl->omega[0]);
   double rz = 0.0;
-  FineSmooth op{{&A.C, A.flags, A.d, A.L[0].dinv}, om, A.r, A.z, &A.L[0].m, &A.L[1].m,
+  FineSmooth op{{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq}, om, A.r, A.z, &A.L[0].m, &A.L[1].m,
                 A.L[1].e, &rz};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
@@ -1333,7 +1348,7 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_pcg(MgArgs A, int n_rz) {
   const long long k = __ldcg(&A.ctl->k);
   const bool first = k == 0;
   double pq = 0.0;
-  FinePcg op{{&A.C, A.flags, A.d, A.L[0].dinv}, first ? 0.0 : rho[0] / __ldcg(&A.ctl->rho_prev),
+  FinePcg op{{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq}, first ? 0.0 : rho[0] / __ldcg(&A.ctl->rho_prev),
              A.z, first ? nullptr : ((k & 1) ? A.p0 : A.p1), (k & 1) ? A.p1 : A.p0, A.q, &pq};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
@@ -1400,6 +1415,25 @@ __global__ void __launch_bounds__(MG_NT) k_mg_finish(MgArgs A) {
   }
 }
 
+// scalar phase-field vectors <-> the two-component layout of the phys-1 instance
+__global__ void __launch_bounds__(MG_NT) k_mg_pack2(double* __restrict__ dst2,
+                                                    const double* __restrict__ src, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    reinterpret_cast<double2*>(dst2)[i] = make_double2(src[i], 0.0);
+}
+__global__ void __launch_bounds__(MG_NT) k_mg_unpack_add(double* __restrict__ x,
+                                                         double* __restrict__ target,
+                                                         const double* __restrict__ x2,
+                                                         long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = __ldg(x2 + 2 * i);
+    x[i] = v;
+    target[i] += v;
+  }
+}
+
 // ================================================================================================
 // setup kernels: Galerkin cell matrices, inverse diagonals, lambda_max by power steps, dense
 // inverse of the coarsest level
@@ -1443,7 +1477,10 @@ __device__ __forceinline__ void mg_galerkin(const MgArgs& A, int lc, int worker,
         const double fb = (bcol & 1) ? di[bcol >> 1].y : di[bcol >> 1].x;
         double2 f[4];
         f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
-        if (fe >= 0 && fb != 0.0) mom_cell_fast(A.C, v, dc, __ldg(A.flags + fe), f);
+        if (fe >= 0 && fb != 0.0) {
+          const FineBase fop{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq};
+          fop.cell(fe, v, dc, f);
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           col[2 * q] = di[q].x != 0.0 ? f[q].x : 0.0;
@@ -1504,7 +1541,7 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_pow(MgArgs A, int step, int fin
   };
   auto vout = [&](const MgLevel& L) -> double* { return (step & 1) ? L.t : L.e; };
   if ((int)blockIdx.x < fine_blocks) {
-    FinePow op{{&A.C, A.flags, A.d, A.L[0].dinv}, vin(A.L[0]), vout(A.L[0])};
+    FinePow op{{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq}, vin(A.L[0]), vout(A.L[0])};
     const int w = blockIdx.x * MG_WARPS + warp;
     if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[warp]);
     return;
