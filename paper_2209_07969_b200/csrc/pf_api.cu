@@ -1144,7 +1144,10 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
         const char* mw = getenv("PFB200_MG_WARM");  // "0": MG solves start cold (x0 = 0)
         if (h->mgu.on && mw && std::string(mw) == "0") h->warm = false;
         const char* ru = getenv("PFB200_MG_REUSE");
-        h->mgu.reuse = h->mgd.reuse = !(ru && std::string(ru) == "0");
+        h->mgu.reuse = !(ru && std::string(ru) == "0");
+        // the phase-field tangent changes strongly between Newton iterations (cfg5: 10-18
+        // iterations on a fresh hierarchy, 50-74 on the previous one): rebuild every solve
+        h->mgd.reuse = ru && std::string(ru) == "1";
       }
     }
   }
