@@ -254,7 +254,8 @@ def run_ours(args, ws, rank, local):
         # The momentum solves run as the multigrid PCG graph (~30 small kernels per iteration,
         # no single dominant kernel); the largest single kernel is the phase-field Jacobi PCG
         # (k_cg<false, *>, one persistent launch per solve): its roofline is reported.
-        rl_kernel = "k_cg<false, *> (phase-field Jacobi PCG, persistent cooperative)"
+        rl_kernel = ("k_cg_sr<false> (phase-field single-reduction Jacobi PCG, persistent "
+                     "cooperative; solves without the SPD probe)")
         achieved, rl_bytes = evo_achieved, "72 B x N_nodes + 32 B x N_cells per phase-field PCG iteration"
         tkey, iters_key, launches_key = "k_cg_evo", "cg_d", "cgl_d"
     else:
