@@ -731,7 +731,10 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
     const int c = nl - 1, top = std::min(B.n_tail, c);  // grid levels [1, top)
     pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(B);
     for (int l = 1; l < top; ++l) {
-      if (M.lpn[l] == 16 && M.fuse) {  // small levels: one fused kernel per direction
+      // fused down-sweep only on the smallest grid levels: it evaluates 12 restriction sources
+      // per stencil slot (cfg2, ncu: 16.6 k nodes 13.7 us fused vs 11.8 split; <= 4.2 k nodes
+      // 7.5 / 6.4 vs 7.8 / 6.9)
+      if (M.lpn[l] == 16 && M.fuse && B.L[l].m.n_nodes <= 8192) {
         pfb::k_mg_sdown<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
       } else {
         MG_NODE_KERNEL(k_mg_srestrict, l, B, l);
@@ -767,7 +770,7 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
   {
     const int c = nl - 1, top = std::min(A.n_tail, c);
     M.body_kernels = 1 + 3 + (A.n_tail < nl ? 1 : 1 + (A.dense ? 1 : A.nu_c));
-    for (int l = 1; l < top; ++l) M.body_kernels += (M.lpn[l] == 16 && M.fuse) ? 2 : 4;
+    for (int l = 1; l < top; ++l) M.body_kernels += (M.lpn[l] == 16 && M.fuse) ? (A.L[l].m.n_nodes <= 8192 ? 2 : 3) : 4;
   }
   const char* un = getenv("PFB200_MG_UNROLL");
   const int unroll = un ? std::max(0, atoi(un)) : 0;
