@@ -22,6 +22,7 @@ from enum import Enum
 import numpy as np
 
 from .assembly import Discretization, GaussPointState, session_for  # noqa: F401
+from . import _native as N
 from .session import ConvergenceError, DeviceSession  # noqa: F401
 
 #: also download gp.strain / gp.tr_eps after every step (faithful GaussPointState mirror)
@@ -85,15 +86,26 @@ def _write_back(sess: DeviceSession, state) -> None:
     semantics: u, d and gp.psi_max are updated in place (schemes.py:390, in-place arithmetic),
     d_prev and the refreshed GP arrays are rebound to new arrays (schemes.py:391,
     assembly.py:265-269).  The new arrays are page-locked (direct DMA from the device)."""
-    out = sess.pull(pinned=True)
-    state.u[...] = out["u"]
-    state.d[...] = out["d"]
-    state.d_prev = out["d_prev"]
     gp = state.gp
+    nn, ne = sess.n_nodes, sess.n_elems
+    out = {k: N.PINNED.empty(shape) for k, shape in (
+        ("d_prev", (nn,)), ("tr_eps_plus", (ne, 4)), ("dev_dot_dev", (ne, 4)),
+        ("psi_plus", (ne, 4)))}
+    inplace = {}
+    for key, arr in (("u", state.u), ("d", state.d), ("psi_max", gp.psi_max)):
+        ok = (isinstance(arr, np.ndarray) and arr.dtype == np.float64
+              and arr.flags["C_CONTIGUOUS"] and arr.flags["WRITEABLE"])
+        inplace[key] = arr if ok else None
+        if not ok:
+            out[key] = N.PINNED.empty(np.shape(arr))
+    sess.pull_into(**out, **{k: v for k, v in inplace.items() if v is not None})
+    for key, arr in (("u", state.u), ("d", state.d), ("psi_max", gp.psi_max)):
+        if inplace[key] is None:
+            arr[...] = out[key]
+    state.d_prev = out["d_prev"]
     gp.tr_eps_plus = out["tr_eps_plus"]
     gp.dev_dot_dev = out["dev_dot_dev"]
     gp.psi_plus = out["psi_plus"]
-    gp.psi_max[...] = out["psi_max"]
     if SYNC_GP_STRAIN:
         gp.strain, gp.tr_eps = sess.gp_strain(pinned=True)
 

@@ -172,6 +172,21 @@ class DeviceSession:
             "u", "d", "d_prev", "tr_eps_plus", "dev_dot_dev", "psi_plus", "psi_max")]))
         return out
 
+    def pull_into(self, **arrays) -> None:
+        """Download state arrays into existing float64 arrays (e.g. the caller's own
+        SolverState arrays; pageable destinations go through the pinned staging buffer with
+        threaded host copies).  Keys: u, d, d_prev, tr_eps_plus, dev_dot_dev, psi_plus,
+        psi_max."""
+        keys = ("u", "d", "d_prev", "tr_eps_plus", "dev_dot_dev", "psi_plus", "psi_max")
+        ptrs = []
+        for k in keys:
+            a = arrays.get(k)
+            if a is not None:
+                if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"] or not a.flags["WRITEABLE"]:
+                    raise ValueError(f"{k}: expected a writable C-contiguous float64 array")
+            ptrs.append(N.f64(a) if a is not None else None)
+        self._check(self.lib.pf_get_state(self.h, *ptrs))
+
     def gp_strain(self, pinned: bool = False) -> tuple:
         ne = self.n_elems
         emp = N.PINNED.empty if pinned else np.empty
