@@ -1,4 +1,4 @@
-"""Reproducer: cfg3's first load step with the single-reduction phase-field PCG (PFB200_SR_EVO=1)."""
+"""One load step of a case on the device (default cfg3, scheme ST) -- with PFB200_TRACE=1 it prints every inner solve (e.g. the single-reduction phase-field stall and its two-barrier redo on cfg3)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2209_07969_b200 import configs as C

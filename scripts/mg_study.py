@@ -352,3 +352,106 @@ def element_check(name="cfg1", step=65):
               f"lmax power {mg.lmax[l]:.3f} element bound {elem_bound(K):.3f}")
     K0 = fine_cell_mats(orc, u, d, keep)
     print(f"level 0: lmax power {mg.lmax[0]:.3f} element bound {elem_bound(K0):.3f}")
+
+
+# ---- operator-dependent (matrix-dependent) prolongation --------------------------------------
+def md_prolongation(Lf, Lc, A):
+    """Prolongation whose edge / centre weights follow the fine operator's couplings (Dendy-style
+    black-box interpolation, scalar weights shared by both displacement components): a fine node
+    on a coarse edge takes its two coarse endpoints with weights proportional to its coupling
+    strength towards each side; a centre node combines its four edge neighbours' interpolations
+    with weights proportional to its couplings to them."""
+    A = A.tocsr()
+
+    def strength(f, g):  # coupling magnitude between fine nodes f and g (2x2 block)
+        if f < 0 or g < 0:
+            return 0.0
+        blk = A[2 * f:2 * f + 2, 2 * g:2 * g + 2].toarray()
+        return abs(blk[0, 0]) + abs(blk[1, 1])
+
+    P = {}
+
+    def coarse_of(i, j, up):
+        return node_lookup(Lc, i // 2, j // 2, up)
+
+    entries = []
+    for j in range(Lf.ny + 1):
+        for i in range(Lf.node_lo[j], Lf.node_hi[j]):
+            entries.append((node_lookup(Lf, i, j, False), i, j, False))
+            if j == Lf.notch_row and Lf.notch_lo <= i < Lf.notch_hi:
+                entries.append((node_lookup(Lf, i, j, True), i, j, True))
+    rows, cols, vals = [], [], []
+    # pass 1: coarse-coincident and edge nodes
+    for nid, i, j, up in entries:
+        side = up or (Lf.notch_row >= 0 and j > Lf.notch_row)
+        if i % 2 == 0 and j % 2 == 0:
+            P[nid] = {coarse_of(i, j, side): 1.0}
+        elif i % 2 == 1 and j % 2 == 0:  # horizontal coarse edge
+            fl = node_lookup(Lf, i - 1, j, side) if not (j == Lf.notch_row and not up and Lf.notch_lo <= i - 1 < Lf.notch_hi) else node_lookup(Lf, i - 1, j, False)
+            fr = node_lookup(Lf, i + 1, j, side) if not (j == Lf.notch_row and not up and Lf.notch_lo <= i + 1 < Lf.notch_hi) else node_lookup(Lf, i + 1, j, False)
+            if j == Lf.notch_row:
+                fl = node_lookup(Lf, i - 1, j, up)
+                fr = node_lookup(Lf, i + 1, j, up)
+            al, ar = strength(nid, fl), strength(nid, fr)
+            cl = node_lookup(Lc, (i - 1) // 2, j // 2, side)
+            cr = node_lookup(Lc, (i + 1) // 2, j // 2, side)
+            s = al + ar
+            P[nid] = {cl: al / s, cr: ar / s} if s > 0 else {cl: 0.5, cr: 0.5}
+        elif i % 2 == 0 and j % 2 == 1:  # vertical coarse edge
+            fb = node_lookup(Lf, i, j - 1, j - 1 == Lf.notch_row)
+            ft = node_lookup(Lf, i, j + 1, False)
+            ab, at = strength(nid, fb), strength(nid, ft)
+            cb = node_lookup(Lc, i // 2, (j - 1) // 2, side)
+            ct = node_lookup(Lc, i // 2, (j + 1) // 2, side)
+            s = ab + at
+            P[nid] = {cb: ab / s, ct: at / s} if s > 0 else {cb: 0.5, ct: 0.5}
+    # pass 2: centre nodes from their four edge neighbours
+    for nid, i, j, up in entries:
+        if i % 2 == 1 and j % 2 == 1:
+            nb = [node_lookup(Lf, i - 1, j, False), node_lookup(Lf, i + 1, j, False),
+                  node_lookup(Lf, i, j - 1, j - 1 == Lf.notch_row), node_lookup(Lf, i, j + 1, False)]
+            a = [strength(nid, g) for g in nb]
+            s = sum(a)
+            w = {}
+            for g, ag in zip(nb, a):
+                for c, wc in P[g].items():
+                    w[c] = w.get(c, 0.0) + (ag / s if s > 0 else 0.25) * wc
+            P[nid] = w
+    for nid, w in P.items():
+        for c, v in w.items():
+            rows.append(nid); cols.append(c); vals.append(v)
+    return sp.csr_matrix((vals, (rows, cols)), shape=(Lf.n_nodes, Lc.n_nodes))
+
+
+def md_hierarchy(L, keep, A, max_levels=20):
+    """Levels with matrix-dependent prolongation (Galerkin operators built alongside)."""
+    Ls, Ps = [L], []
+    Al = A
+    Lc = coarsen(L)
+    while Lc is not None and len(Ls) < max_levels:
+        P = vec2(md_prolongation(Ls[-1], Lc, Al))
+        if not Ps:
+            P = sp.diags(keep) @ P
+        P = P.tocsr()
+        Ps.append(P)
+        Ls.append(Lc)
+        Al = (P.T @ Al @ P).tocsr()
+        if Al.shape[0] <= 400:
+            break
+        Lc = coarsen(Lc)
+    return Ls, Ps
+
+
+def compare_interp(name="cfg1", steps=(10, 64, 65)):
+    z = np.load("tests/golden/run_cfg1_ST.npz")
+    for step in steps:
+        A, b, keep, L, pb = build_system(name, (z[f"u_step{step}"], z[f"d_step{step}"]))
+        if np.linalg.norm(b) == 0:
+            b = np.random.default_rng(1).standard_normal(A.shape[0]) * keep
+        Ls, Ps = hierarchy(L, keep)
+        mg = MG(A, Ls, Ps, smoother="jacobi")
+        _, it_b = pcg(A, b, lambda r: mg.vcycle(0, r))
+        Ls2, Ps2 = md_hierarchy(L, keep, A)
+        mg2 = MG(A, Ls2, Ps2, smoother="jacobi")
+        _, it_m = pcg(A, b, lambda r: mg2.vcycle(0, r))
+        print(f"cfg1 step {step}: bilinear {it_b} iterations, matrix-dependent {it_m}")
