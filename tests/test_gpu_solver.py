@@ -256,3 +256,40 @@ def test_multicrack256_analogue(cuda_ok):
     pb, recs = run_case("multicrack256", "ST", steps=10)
     check_against_golden(recs, z, pb.state, "multicrack256", "ST", pb.mesh,
                          run_file="run_multicrack256_ST_10steps.npz")
+
+
+def test_dropin_binding_semantics(cuda_ok):
+    """The drop-in mirrors the reference's binding semantics: u, d and gp.psi_max are updated in
+    place (schemes.py:390 and in-place arithmetic), d_prev and the refreshed GP arrays are
+    rebound to new arrays (schemes.py:391, assembly.py:265-269) -- page-locked buffers that
+    stay valid after later steps -- and the values equal a device-resident session's."""
+    from paper_2209_07969_b200 import schemes
+    from paper_2209_07969_b200.session import DeviceSession
+
+    case = C.get_case("tension16")
+    pb = C.setup(case, C.b200_api())
+    st = pb.state
+    u_id, d_id, pm_id = id(st.u), id(st.d), id(st.gp.psi_max)
+    kept = []
+    for _ in range(4):
+        schemes.staggered_step(pb.disc, st, schemes.SchemeKind.S1, pb.bcs, pb.params, pb.config,
+                               pb.pins)
+        kept.append((st.d_prev, st.gp.psi_plus.copy(), st.gp.psi_plus))
+    assert (id(st.u), id(st.d), id(st.gp.psi_max)) == (u_id, d_id, pm_id)
+    assert len({id(k[0]) for k in kept}) == 4 and len({id(k[2]) for k in kept}) == 4
+    for _, copy, arr in kept:  # earlier outputs are not recycled while referenced
+        assert np.array_equal(copy, arr)
+    assert st.gp.strain.shape == (pb.mesh.n_elems, 4, 4) and st.gp.tr_eps.shape == (pb.mesh.n_elems, 4)
+    ref = C.setup(case, C.b200_api())
+    s = DeviceSession(ref.disc.layout, ref.params, ref.config, device=0)
+    s.push_state(ref.state)
+    for _ in range(4):
+        s.step("S1", ref.bcs, ref.pins)
+    got = s.pull()
+    for key in ("u", "d", "d_prev"):
+        assert np.array_equal(got[key], getattr(st, key)), key
+    for key in ("tr_eps_plus", "dev_dot_dev", "psi_plus", "psi_max"):
+        assert np.array_equal(got[key], getattr(st.gp, key)), key
+    strain, tr = s.gp_strain()
+    assert np.array_equal(strain, st.gp.strain) and np.array_equal(tr, st.gp.tr_eps)
+    s.close()
