@@ -712,7 +712,7 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
     const int cb = (16 * A.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
     for (int k = 1; k <= pfb::MG_POW; ++k)
       pfb::k_mg_pow<<<M.gf + cb, pfb::MG_NT, 0, s>>>(A, k, M.gf);
-    pfb::k_mg_lambda<<<32, pfb::MG_NT, 0, s>>>(A);  // few CTAs: 2 MG_MAXL partials each
+    pfb::k_mg_lambda<<<M.gflat, pfb::MG_NT, 0, s>>>(A);
     cudaError_t e = cudaStreamEndCapture(s, &g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG setup capture: ") + cudaGetErrorString(e));
     e = cudaGraphInstantiate(&M.setup_exec, g, 0);
