@@ -612,14 +612,16 @@ static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_w
           mg_alloc(h, &ML.e, 2 * (size_t)L.n_nodes) != cudaSuccess)
         return oom();
       ML.items = pfb::mg_items(L.nx, L.ny, L.notch_row >= 0);
-      ML.item_off = coarse_items;  // node offset in the concatenated coarse node space (even)
-      coarse_items += (L.n_nodes + 1) & ~1;
+      ML.item_off = coarse_items;  // set below, once lpn is known
       M.gl[l] = (ML.items + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
       // small levels: a half-warp per node (all loads of a node in flight); large levels: a
       // thread per node (latency hidden by occupancy).  Threshold: 16 lanes per node would
       // exceed one wave of resident threads.
       const long long wave = 2048LL * h->sm_count;
       M.lpn[l] = 16LL * L.n_nodes <= wave ? 16 : (4LL * L.n_nodes <= wave ? 4 : 1);
+      ML.lpn = M.lpn[l];
+      ML.item_off = coarse_items;  // power steps: lpn threads per node, warp-aligned per level
+      coarse_items += (int)(((long long)M.lpn[l] * L.n_nodes + 31) / 32 * 32);
       M.gn[l] = std::max(1, std::min((int)((M.lpn[l] * (long long)L.n_nodes + pfb::MG_NT - 1) / pfb::MG_NT),
                                          16 * h->sm_count));
       {  // assembled-form index tables (static per handle)
@@ -709,7 +711,7 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
     }
     if (A.dense) pfb::k_mg_dense<<<1, pfb::MG_NT, 0, s>>>(A);
     M.setup_kernels = 2 * (nl - 1) + (A.dense ? 1 : 0) + pfb::MG_POW + 1;
-    const int cb = (16 * A.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
+    const int cb = (A.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
     for (int k = 1; k <= pfb::MG_POW; ++k)
       pfb::k_mg_pow<<<M.gf + cb, pfb::MG_NT, 0, s>>>(A, k, M.gf);
     pfb::k_mg_lambda<<<M.gflat, pfb::MG_NT, 0, s>>>(A);

@@ -47,7 +47,8 @@ struct MgLevel {
   double* t;      // residual / prolongated iterate / power-iteration buffer
   double* e;      // correction / power-iteration buffer
   int items;      // node items (rows x 32-column chunks) of mg_for_nodes
-  int item_off;   // offset of this level in the concatenated coarse item space (power steps)
+  int item_off;   // first thread of this level in the power steps' coarse thread space
+  int lpn;        // lanes per node of the level's node kernels (1 | 4 | 16)
   // assembled form (l >= 1), slot-major: nbr [MG_NS][n] neighbour ids, S [MG_NS*4][n] 2x2
   // blocks (xx, xy, yx, yy); rid [12][n] restriction sources on level l-1; pid [4][n]
   // prolongation sources on level l+1 (l <= n_levels-2)
@@ -793,15 +794,23 @@ __global__ void __launch_bounds__(MG_NT) k_mg_ssweep(MgArgs A, int l, const doub
 }
 // power step at one node of a coarse level (half-warp per node; every lane of the warp must
 // call it: id >= n makes the half-warp idle): vout = D^-1 A vin (vin == nullptr: hashed start)
+template <int LPN>
 __device__ __forceinline__ void mg_spow(const MgLevel& L, const double* vin, double* vout, int id) {
-  const int n = L.m.n_nodes, s2 = (int)(threadIdx.x & 15);
-  const double2 Av = hw_sum(mg_slot_apply(L, n, id, s2, [&](int k) -> double2 {
-    const double2 di = GMem::v2(L.dinv, k);
-    const double2 v = vin ? GMem::v2(vin, k)
-                          : make_double2(mg_hash01(2u * k + 1u), mg_hash01(2u * k + 2u));
-    return mask2(v, di);
-  }));
-  if (s2 == 0 && id < n) {
+  const int n = L.m.n_nodes;
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s2 = NodeMap<LPN>::lane(); s2 < MG_NS; s2 += LPN) {
+    const double2 v = mg_slot_apply(L, n, id, s2, [&](int k) -> double2 {
+      const double2 di = GMem::v2(L.dinv, k);
+      const double2 x = vin ? GMem::v2(vin, k)
+                            : make_double2(mg_hash01(2u * k + 1u), mg_hash01(2u * k + 2u));
+      return mask2(x, di);
+    });
+    acc.x += v.x;
+    acc.y += v.y;
+  }
+  const double2 Av = NodeMap<LPN>::sum(acc);
+  if (NodeMap<LPN>::lane() == 0 && id < n) {
     const double2 di = GMem::v2(L.dinv, id);
     d2st(vout, id, make_double2(di.x * Av.x, di.y * Av.y));
   }
@@ -1546,14 +1555,17 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_pow(MgArgs A, int step, int fin
     if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[warp]);
     return;
   }
-  // concatenated coarse nodes, a half-warp per node (the node pair of a warp shares a level:
-  // level offsets are even)
-  const int t = ((blockIdx.x - fine_blocks) * MG_NT + threadIdx.x) >> 4;
-  if (t >= A.coarse_items) return;  // whole warps (coarse_items is even)
+  // coarse levels: concatenated thread space, lpn threads per node on each level (every
+  // level starts on a warp boundary, so the lanes of a node share a warp)
+  const int t = (blockIdx.x - fine_blocks) * MG_NT + threadIdx.x;
+  if (t >= A.coarse_items) return;
   int l = 1;
   while (l + 1 < A.n_levels && t >= A.L[l + 1].item_off) ++l;
   const MgLevel& L = A.L[l];
-  mg_spow(L, vin(L), vout(L), t - L.item_off);
+  const int q = t - L.item_off;
+  if (L.lpn == 16) mg_spow<16>(L, vin(L), vout(L), q >> 4);
+  else if (L.lpn == 4) mg_spow<4>(L, vin(L), vout(L), q >> 2);
+  else mg_spow<1>(L, vin(L), vout(L), q);
 }
 // omega_l = 4 / (3 lambda_l), lambda_l = ||v_POW|| / ||v_POW-1|| (per-level partials)
 __global__ void __launch_bounds__(MG_NT) k_mg_lambda(MgArgs A) {
