@@ -13,9 +13,10 @@ schedule: W untimed warm-up load steps advance the state, then K load steps are 
   ``paper_2209_07969_b200.schemes.staggered_step`` with the caller's HOST SolverState: every
   step uploads the state, solves, and downloads the state (all copies inside the timed region).
 * ``roofline``— the dominant single kernel: with the multigrid momentum solver (default) the
-  phase-field Jacobi PCG ``k_cg<false, *>`` (algorithmic bytes 72 B * N_nodes + 32 B * N_cells
-  per PCG iteration); with PFB200_MG=0 the momentum PCG (168 B * N_nodes) /
-  its CUDA-event time.  ``momentum_solver`` summarises the multigrid PCG graph.
+  phase-field PCG (``k_cg_st`` on the assembled stencil for L2-resident meshes, else
+  ``k_cg_sr<false>``; algorithmic bytes 72 B * N_nodes + 32 B * N_cells per PCG iteration,
+  SURVEY.md §8(d)); with PFB200_MG=0 the momentum PCG (168 B * N_nodes) / its CUDA-event time.
+  ``momentum_solver`` summarises the multigrid PCG graph.
 * ``cpu_baseline`` — the CPU oracle port (oracle/phasefield_oracle.py, SuperLU like the
   reference default) on the first load step of the same case, rank 0 only.
 * ``--gpus N`` (torchrun, one process per GPU) — the same cfg2 problem split into N row strips
@@ -254,10 +255,17 @@ def run_ours(args, ws, rank, local):
         # The momentum solves run as the multigrid PCG graph (~30 small kernels per iteration,
         # no single dominant kernel); the largest single kernel is the phase-field Jacobi PCG
         # (k_cg<false, *>, one persistent launch per solve): its roofline is reported.
-        rl_kernel = ("k_cg_sr<false> (phase-field single-reduction Jacobi PCG, persistent "
-                     "cooperative; solves without the SPD probe)")
+        kinds = sess.solver_kinds()
+        if kinds["phase_field"] == "stencil_pcg":
+            rl_kernel = ("k_cg_st (phase-field single-reduction Jacobi PCG on the assembled "
+                         "stencil, persistent cooperative; solves without the SPD probe)")
+            tkey = "k_cg_st"
+        else:
+            rl_kernel = ("k_cg_sr<false> (phase-field single-reduction Jacobi PCG, persistent "
+                         "cooperative; solves without the SPD probe)")
+            tkey = "k_cg_evo"
         achieved, rl_bytes = evo_achieved, "72 B x N_nodes + 32 B x N_cells per phase-field PCG iteration"
-        tkey, iters_key, launches_key = "k_cg_evo", "cg_d", "cgl_d"
+        iters_key, launches_key = "cg_d", "cgl_d"
     else:
         rl_kernel = ("k_cg<true, *> (momentum PCG, persistent cooperative)" if ws == 1 else
                      "momentum PCG (k_cg_a/k_cg_b + NCCL, rank 0's strip)")
@@ -311,7 +319,10 @@ def run_ours(args, ws, rank, local):
             "peak_source": peak_src,
             "algorithmic_bytes": rl_bytes,
             "note": "cfg2's PCG working set (~50 MB) is L2-resident: the fraction mixes L2 and "
-                    "HBM traffic (SURVEY.md 8(d)); cfg3-5 are the HBM-bound sizes",
+                    "HBM traffic (SURVEY.md 8(d)); cfg3-5 are the HBM-bound sizes.  k_cg_st "
+                    "moves more than the algorithmic bytes (assembled rows 80 B + neighbour "
+                    "ids 40 B per node instead of 32 B per cell): achieved counts only the "
+                    "algorithmic bytes",
         },
         "momentum_solver": ({"kind": "multigrid PCG (Galerkin V(1,1), CUDA graph)",
                              "levels": mg["n_levels"], "hierarchy_builds": mg.get("setups"),

@@ -204,6 +204,12 @@ pf_status pf_device_info(pf_handle* h, int32_t* cg_grid, int32_t* sm_count, int6
  * with Jacobi PCG (PFB200_MG=0, strips, meshes that do not agglomerate). */
 pf_status pf_mg_info(pf_handle* h, int32_t* n_levels, int32_t* n_grid, int32_t* dense,
                      int64_t* setups, double* omega);
+/* Linear solver of each Newton system on this handle (all solve the reference's CG system of
+ * linsolve.py:48-54 to the same stopping test).  momentum: 0 two-barrier Jacobi PCG (k_cg),
+ * 1 single-reduction Jacobi PCG (k_cg_sr), 2 multigrid PCG.  phase_field (solves without the
+ * SPD probe; probe solves always run k_cg): 0 k_cg, 1 k_cg_sr (matrix-free march), 2 k_cg_st
+ * (assembled stencil, L2-resident meshes), 3 multigrid PCG. */
+pf_status pf_solver_kinds(pf_handle* h, int32_t* momentum, int32_t* phase_field);
 pf_status pf_flush_l2(pf_handle* h);
 pf_status pf_synchronize(pf_handle* h);
 

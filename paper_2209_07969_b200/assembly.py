@@ -33,9 +33,31 @@ class GaussPointState:
 
     @classmethod
     def zeros(cls, n_elems: int, n_gp: int) -> "GaussPointState":
-        return cls(strain=np.zeros((n_elems, n_gp, 4)), tr_eps=np.zeros((n_elems, n_gp)),
-                   tr_eps_plus=np.zeros((n_elems, n_gp)), dev_dot_dev=np.zeros((n_elems, n_gp)),
-                   psi_plus=np.zeros((n_elems, n_gp)), psi_max=np.zeros((n_elems, n_gp)))
+        z = host_zeros
+        return cls(strain=z((n_elems, n_gp, 4)), tr_eps=z((n_elems, n_gp)),
+                   tr_eps_plus=z((n_elems, n_gp)), dev_dot_dev=z((n_elems, n_gp)),
+                   psi_plus=z((n_elems, n_gp)), psi_max=z((n_elems, n_gp)))
+
+
+PINNED_MAX_BYTES = 256 << 20
+
+
+def host_zeros(shape) -> np.ndarray:
+    """Zeroed float64 state array.  Arrays up to PINNED_MAX_BYTES are page-locked
+    (_native.PINNED), so the per-step transfers of the drop-in (staggered_step pushes u, d,
+    d_prev, psi_max and updates u, d, psi_max in place) are direct DMA instead of staged copies;
+    without a CUDA device (or pinned memory) they are ordinary arrays."""
+    n = int(np.prod(shape))
+    if 8 * n <= PINNED_MAX_BYTES:
+        try:
+            from . import _native as N
+
+            a = N.PINNED.empty(shape)
+            a[...] = 0.0
+            return a
+        except Exception:  # no library / no device: pageable state, same semantics
+            pass
+    return np.zeros(shape)
 
 
 class Discretization:

@@ -115,6 +115,10 @@ struct pf_handle {
   bool sr_evo = false;  // phase-field solves without the SPD probe by k_cg_sr<false>
   bool sr_evo_now = false;       // the kernel choice of the current phase-field launch
   long long evo_last_iters = 0;  // PCG iterations of the last converged phase-field solve
+  // phase-field solves on the assembled stencil (pf_st.cuh k_cg_st) where its rows fit in L2
+  bool st_evo = false, st_evo_now = false;
+  pfb::StArgs st{};
+  int cg_grid_st = 1;
   size_t sr_smem_evo = 0;
   size_t sr_smem = 0;   // its dynamic shared memory (cp.async staging slots)
   pfb::MarchGeom geom_mom{}, geom_evo{}, geom_apply{};
@@ -508,6 +512,60 @@ static cudaError_t mg_alloc(pf_handle* h, T** p, size_t n) {
 
 static pf_status mg_build_graphs(pf_handle* h, MgInst& M);
 
+static HostLevel hl_fine(const pf_handle* h) {
+  HostLevel f;
+  f.nx = h->nx; f.ny = h->ny;
+  f.nlo = h->h_nlo; f.nhi = h->h_nhi; f.nst = h->h_nst;
+  f.elo = h->h_elo; f.ehi = h->h_ehi; f.est = h->h_est;
+  f.notch_row = h->dm.notch_row; f.notch_lo = h->dm.notch_lo; f.notch_hi = h->dm.notch_hi;
+  f.dup_start = h->dm.dup_start; f.n_nodes = h->n_nodes; f.n_elems = h->n_elems;
+  return f;
+}
+
+// assembled-stencil tables of the fine layout (pf_st.cuh StArgs): neighbours, and for every
+// node the cells it is a corner of with the stencil slot of each of their corners.  A cell sees
+// the slit row's nodes from its own side (lower face from below, duplicates from above).
+static pf_status st_setup(pf_handle* h) {
+  const HostLevel f = hl_fine(h);
+  const size_t n = f.n_nodes;
+  const std::vector<int> nb = hl_stencil_ids(f);
+  std::vector<int> cc(4 * n, -1), cs(4 * n, -1);
+  static const int dx[4] = {0, 1, 1, 0}, dy[4] = {0, 0, 1, 1};  // evo_cell_apply corner order
+  bool ok = true;
+  hl_for_nodes(f, [&](int id, int i, int j, bool) {
+    for (int a = 0; a < 4; ++a) {
+      const int ci = i - dx[a], cj = j - dy[a];
+      if (!hl_cell(f, ci, cj) || hl_node(f, i, j, cj == j) != id) continue;
+      unsigned sl = 0;
+      for (int b = 0; b < 4; ++b) {
+        const int nbid = hl_node(f, ci + dx[b], cj + dy[b], dy[b] == 0);
+        int slot = -1;
+        for (int s = 0; s < pfb::MG_NS && nbid >= 0; ++s)
+          if (nb[(size_t)s * n + id] == nbid) slot = s;
+        if (slot < 0) ok = false;
+        sl |= (unsigned)(slot < 0 ? 15 : slot) << (4 * b);
+      }
+      cc[(size_t)a * n + id] = f.est[cj] + (ci - f.elo[cj]);
+      cs[(size_t)a * n + id] = (int)sl;
+    }
+  });
+  if (!ok) return fail(h, PF_ERR_INVALID, "assembled phase-field stencil: corner without a slot");
+  int *dnb = nullptr, *dcc = nullptr, *dcs = nullptr;
+  if (mg_alloc(h, &dnb, nb.size()) != cudaSuccess || mg_alloc(h, &dcc, cc.size()) != cudaSuccess ||
+      mg_alloc(h, &dcs, cs.size()) != cudaSuccess ||
+      mg_alloc(h, &h->st.S, (size_t)pfb::MG_NS * n) != cudaSuccess)
+    return fail(h, PF_ERR_CUDA, "assembled phase-field stencil allocation failed");
+  PF_CUDA(cudaMemcpy(dnb, nb.data(), nb.size() * sizeof(int), cudaMemcpyHostToDevice));
+  PF_CUDA(cudaMemcpy(dcc, cc.data(), cc.size() * sizeof(int), cudaMemcpyHostToDevice));
+  PF_CUDA(cudaMemcpy(dcs, cs.data(), cs.size() * sizeof(int), cudaMemcpyHostToDevice));
+  h->st.nbr = dnb;
+  h->st.ccell = dcc;
+  h->st.cslot = dcs;
+  h->st.n = (int)n;
+  return PF_OK;
+}
+
+
 static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_warps) {
   const char* fz = getenv("PFB200_MG_FUSE");
   M.fuse = !(fz && std::string(fz) == "0");
@@ -516,13 +574,7 @@ static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_w
   const int tail_nodes = tl ? std::max(0, atoi(tl)) : 1 << 30;
   const char* nc = getenv("PFB200_MG_NUC");
   const int nu_c = nc ? std::max(1, atoi(nc)) : 16;
-  std::vector<HostLevel> lv(1);
-  HostLevel& f = lv[0];
-  f.nx = h->nx; f.ny = h->ny;
-  f.nlo = h->h_nlo; f.nhi = h->h_nhi; f.nst = h->h_nst;
-  f.elo = h->h_elo; f.ehi = h->h_ehi; f.est = h->h_est;
-  f.notch_row = h->dm.notch_row; f.notch_lo = h->dm.notch_lo; f.notch_hi = h->dm.notch_hi;
-  f.dup_start = h->dm.dup_start; f.n_nodes = h->n_nodes; f.n_elems = h->n_elems;
+  std::vector<HostLevel> lv(1, hl_fine(h));
   while ((int)lv.size() < pfb::MG_MAXL && 2 * lv.back().n_nodes > pfb::MG_DENSE_MAX) {
     HostLevel c;
     if (!mg_coarsen(lv.back(), c)) break;
@@ -1116,9 +1168,28 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
                            sizeof(double) * pfb::CG_SLOTS * std::max(h->gridA_mom, h->gridA_evo)));
     CREATE_CUDA(cudaMalloc((void**)&h->partB, sizeof(double) * (pfb::CG_SLOTS + 1) * h->gridB * 2));
   }
+  {  // assembled-stencil phase-field PCG (pf_st.cuh) while its rows and vectors (~176 B per
+     // node) fit in half of L2; PFB200_ST_EVO=0/1 forces it off/on
+    const char* se = getenv("PFB200_ST_EVO");
+    h->st_evo = h->sr_evo && !h->comm && !h->split && 176.0 * (double)nn <= 0.5 * (double)l2;
+    if (se) h->st_evo = std::string(se) == "1" && h->sr_evo && !h->comm && !h->split;
+    if (h->st_evo) {
+      int os = 0;
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&os, pfb::k_cg_st, pfb::CG_NT, 0));
+      if (os < 1) {
+        h->err = "k_cg_st cannot be resident (occupancy 0)";
+        return bail(PF_ERR_CUDA);
+      }
+      const char* so = getenv("PFB200_ST_OCC");  // CTAs per SM (A/B tests)
+      if (so) os = std::max(1, std::min(os, atoi(so)));
+      h->cg_grid_st = std::max(1, std::min(os * dev_sms, (int)((nn + pfb::CG_NT - 1) / pfb::CG_NT)));
+      if ((s2 = st_setup(h)) != PF_OK) return bail(s2);
+    }
+  }
   const size_t npart =
       std::max<size_t>((size_t)h->n_tiles * 4,
-                       (size_t)std::max(h->cg_grid, h->cg_grid_evo) * pfb::CG_PART_STRIDE);
+                       (size_t)std::max({h->cg_grid, h->cg_grid_evo, h->cg_grid_st}) *
+                           pfb::CG_PART_STRIDE);
   CREATE_ALLOC(h->partials, npart);
   CREATE_CUDA(cudaHostAlloc((void**)&h->h_cgres, sizeof(CgResult), cudaHostAllocMapped));
   CREATE_CUDA(cudaHostGetDevicePointer((void**)&h->d_cgres, h->h_cgres, 0));
@@ -1517,6 +1588,7 @@ static size_t cg_smem(const pf_handle* h, bool mom) {  // dynamic smem of the ch
 
 static const void* cg_kernel(pf_handle* h, bool mom) {
   if (mom && h->sr_mom) return (const void*)pfb::k_cg_sr<true>;
+  if (!mom && h->st_evo_now) return (const void*)pfb::k_cg_st;
   if (!mom && h->sr_evo_now) return (const void*)pfb::k_cg_sr<false>;
   if (mom) return h->xupd_mom ? (const void*)pfb::k_cg<true, true> : (const void*)pfb::k_cg<true, false>;
   return h->xupd_evo ? (const void*)pfb::k_cg<false, true> : (const void*)pfb::k_cg<false, false>;
@@ -1582,9 +1654,9 @@ static pf_status run_cg_persistent(pf_handle* h, bool mom, double* target, bool 
   a.probe = probe ? 1 : 0;
   for (int k = 0; k < n_guess && k < pfb::WARM_MAX; ++k) a.guess[k] = guess[k];
   a.n_guess = guess ? std::min(n_guess, pfb::WARM_MAX) : 0;
-  void* args[] = {&a};
+  void* args[] = {&a, &h->st};  // (k_cg_st only reads the second)
   const void* fn = cg_kernel(h, mom);
-  const int grid = mom ? h->cg_grid : h->cg_grid_evo;
+  const int grid = mom ? h->cg_grid : (h->st_evo_now ? h->cg_grid_st : h->cg_grid_evo);
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
   PF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(pfb::CG_NT), args,
                                       cg_smem(h, mom), h->stream));
@@ -2028,10 +2100,16 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
         // single-reduction PCG with an iteration cap (4x the last converged phase-field solve);
         // d is updated only after it converged
         const long long cap = std::max(300LL, 4 * h->evo_last_iters);
-        h->sr_evo_now = true;
+        if (h->st_evo) {  // assemble this solve's rows (b and D^-1 from launch_evo_prepare)
+          pfb::k_evo_stencil<<<(unsigned)((h->n_nodes + 255) / 256), 256, 0, h->stream>>>(
+              h->st, h->C, h->b, h->dinvd);
+          PF_TRY(launched(h));
+        }
+        h->sr_evo_now = !h->st_evo;
+        h->st_evo_now = h->st_evo;
         const pf_status sst = run_cg_persistent(h, false, nullptr, false, &status, &iters, guess,
                                                 ng, cap);
-        h->sr_evo_now = false;
+        h->sr_evo_now = h->st_evo_now = false;
         if (sst == PF_OK) {
           PF_TRY(axpy(h, h->d, h->xd, h->n_nodes));
           done = true;
@@ -2366,6 +2444,14 @@ extern "C" pf_status pf_mg_info(pf_handle* h, int32_t* n_levels, int32_t* n_grid
   PF_TRY(run_mg(h, h->mgu, nullptr, &status, &iters, 1));
   PF_CUDA(cudaMemcpy(omega, h->mgu.A.ctl->omega, h->mgu.A.n_levels * sizeof(double),
                      cudaMemcpyDeviceToHost));
+  return PF_OK;
+}
+
+extern "C" pf_status pf_solver_kinds(pf_handle* h, int32_t* momentum, int32_t* phase_field) {
+  if (momentum) *momentum = h->mgu.on ? 2 : (h->sr_mom ? 1 : 0);
+  if (phase_field)
+    *phase_field = h->mgd.on && !h->comm ? 3
+                   : (h->sr_evo && !h->comm && !h->split ? (h->st_evo ? 2 : 1) : 0);
   return PF_OK;
 }
 

@@ -21,7 +21,7 @@ from enum import Enum
 
 import numpy as np
 
-from .assembly import Discretization, GaussPointState, session_for  # noqa: F401
+from .assembly import Discretization, GaussPointState, host_zeros, session_for  # noqa: F401
 from . import _native as N
 from .session import ConvergenceError, DeviceSession  # noqa: F401
 
@@ -76,8 +76,8 @@ class SolverState:
 
     @classmethod
     def zeros(cls, disc) -> "SolverState":
-        return cls(u=np.zeros(disc.n_u_dofs), d=np.zeros(disc.n_d_dofs),
-                   d_prev=np.zeros(disc.n_d_dofs),
+        z = host_zeros  # page-locked where possible (assembly.host_zeros)
+        return cls(u=z(disc.n_u_dofs), d=z(disc.n_d_dofs), d_prev=z(disc.n_d_dofs),
                    gp=GaussPointState.zeros(disc.mesh.n_elems, disc.n_gp))
 
 

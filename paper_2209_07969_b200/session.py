@@ -305,6 +305,16 @@ class DeviceSession:
             out["omega"] = om
         return out
 
+    MOMENTUM_SOLVERS = ("jacobi_pcg", "single_reduction_pcg", "multigrid_pcg")
+    PHASE_FIELD_SOLVERS = ("jacobi_pcg", "single_reduction_pcg", "stencil_pcg", "multigrid_pcg")
+
+    def solver_kinds(self) -> dict:
+        """Linear solver of each Newton system (pf_solver_kinds)."""
+        m, d = C.c_int32(), C.c_int32()
+        self._check(self.lib.pf_solver_kinds(self.h, C.byref(m), C.byref(d)))
+        return {"momentum": self.MOMENTUM_SOLVERS[m.value],
+                "phase_field": self.PHASE_FIELD_SOLVERS[d.value]}
+
     def device_info(self) -> dict:
         g, s, l2 = C.c_int32(), C.c_int32(), C.c_int64()
         self._check(self.lib.pf_device_info(self.h, C.byref(g), C.byref(s), C.byref(l2)))

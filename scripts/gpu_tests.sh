@@ -1,5 +1,4 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_mg.py -q > gpurun_out/mg_tests.log 2>&1; echo "mg tests exit $?"; tail -15 gpurun_out/mg_tests.log
-timeout 2400 python -m pytest tests -m gpu -q --durations=6 > gpurun_out/gpu_all.log 2>&1; echo "gpu tests exit $?"; tail -10 gpurun_out/gpu_all.log
-timeout 900 python scripts/cfg5_run.py 3 S1 > gpurun_out/cfg5_run2.jsonl 2>&1; echo "cfg5 exit $?"; cut -c1-300 gpurun_out/cfg5_run2.jsonl
+timeout 1500 python -m pytest tests -m gpu -q -x --durations=8 > gpurun_out/gpu_all.log 2>&1; echo "gpu tests exit $?"; tail -14 gpurun_out/gpu_all.log
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['ms_per_step'], 'pf us/it', 1e3*d['kernel_ms']['phase_field_pcg']/d['pcg_iters']['phase_field'], d['roofline']['kernel'][:8], d['roofline']['frac'])"
