@@ -1982,13 +1982,14 @@ static pf_status momentum(pf_handle* h, const BcView& bc, bool apply_inc, double
         fprintf(stderr, "[pfb200] momentum pass %d newton %d warm %d iters %lld\n", pass, n_nr,
                 ng, iters);
       if (h->warm && n_nr == 0) {  // the solution joins the difference table
+        // (the multigrid solves read only the first MG_WARM entries: deeper ones are not kept)
+        const int depth = h->mgu.on ? std::min(h->warm_depth, pfb::MG_WARM) : h->warm_depth;
         pfb::WarmTable t{};
-        for (int k = 0; k < h->warm_depth; ++k) t.d[k] = h->warm_buf[ws][k];
+        for (int k = 0; k < depth; ++k) t.d[k] = h->warm_buf[ws][k];
         const long long n = 2LL * h->n_nodes;
-        pfb::k_warm_push<<<4 * h->sm_count, 256, 0, h->stream>>>(t, h->warm_n[ws],
-                                                              h->warm_depth, h->xu, n);
+        pfb::k_warm_push<<<4 * h->sm_count, 256, 0, h->stream>>>(t, h->warm_n[ws], depth, h->xu, n);
         PF_TRY(launched(h));
-        h->warm_n[ws] = std::min(h->warm_n[ws] + 1, h->warm_depth);
+        h->warm_n[ws] = std::min(h->warm_n[ws] + 1, depth);
       }
     }
     n_nr += 1;

@@ -83,7 +83,10 @@ __global__ void __launch_bounds__(256) k_evo_stencil(StArgs s, Consts C,
 //   pass 0:  (r.r, r.D^-1.r), w = A D^-1 r, w.D^-1.r
 //   pass k:  s = w + beta s, p = D^-1 r + beta p, x += alpha p, r -= alpha s, then as pass 0
 //   then     beta = g'/g, alpha = g'/(w.u - beta g'/alpha)      (k_cg_sr's recurrence)
-__global__ void __launch_bounds__(CG_NT, 2) k_cg_st(CgArgs a, StArgs st) {
+#ifndef PFB_ST_MINB
+#define PFB_ST_MINB 2
+#endif
+__global__ void __launch_bounds__(CG_NT, PFB_ST_MINB) k_cg_st(CgArgs a, StArgs st) {
   __shared__ CgSmem<false> S;
   cg::grid_group grid = cg::this_grid();
   double* part = a.partials;
