@@ -121,6 +121,14 @@ pf_status pf_set_state(pf_handle* h, const double* u, const double* d, const dou
 pf_status pf_get_state(pf_handle* h, double* u, double* d, double* d_prev,
                        double* tr_eps_plus, double* dev_dot_dev, double* psi_plus,
                        double* psi_max);
+/* Device-side state construction: the zero state of SolverState.zeros
+ * (schemes.py:80-87) and d = d_prev = 1 at every node within `radius` of one of the
+ * n_segments pre-crack segments (segments[4k..4k+3] = ax, ay, bx, by; configs.precrack_nodes),
+ * node (i, j) at (i hx, j hy) with the last column / row at x_last / y_last (np.linspace).
+ * No host state arrays are needed (config 5: 8.6 GB of zero GP arrays otherwise).
+ * Single-GPU handles only. */
+pf_status pf_init_state(pf_handle* h, const double* segments, int64_t n_segments,
+                        double radius, double x_last, double y_last);
 /* gp.strain [n_elems*4*4] Voigt (xx,yy,zz,xy) and gp.tr_eps [n_elems*4] recomputed from u
  * (refresh_gp_from_displacement, assembly.py:260-269). */
 pf_status pf_get_gp_strain(pf_handle* h, double* strain, double* tr_eps);

@@ -116,6 +116,7 @@ _SIGNATURES = {
     "pf_host_free": (None, [C.c_void_p]),
     "pf_mg_info": (C.c_int, [C.c_void_p, _i32p, _i32p, _i32p, _i64p, _f64p]),
     "pf_solver_kinds": (C.c_int, [C.c_void_p, _i32p, _i32p]),
+    "pf_init_state": (C.c_int, [C.c_void_p, _f64p, C.c_int64, C.c_double, C.c_double, C.c_double]),
     "pf_flush_l2": (C.c_int, [C.c_void_p]),
     "pf_synchronize": (C.c_int, [C.c_void_p]),
 }

@@ -213,20 +213,35 @@ def reaction_sets(case: LoadCase, mesh) -> list:
     raise ValueError(case.loading)
 
 
-def precrack_nodes(case: LoadCase, mesh) -> np.ndarray:
-    """Nodes within h/2 of one of the seeded straight pre-cracks.
+def precrack_segments(case: LoadCase) -> tuple:
+    """The seeded straight pre-cracks as end points [(ax, ay, bx, by), ...]
+    and the marking radius h/2.
 
     Draw order from ``np.random.default_rng(seed)``: centres U[0, side]^2, then lengths
     U[len_lo, len_hi], then angles U[0, pi).
     """
     if case.precracks is None:
-        return np.zeros(0, dtype=np.int64)
+        return np.zeros((0, 4)), 0.0
     n, seed, lo, hi = case.precracks
     _, nx, ny, side, _ = case.mesh
     rng = np.random.default_rng(seed)
     centres = rng.uniform(0.0, side, size=(n, 2))
     lengths = rng.uniform(lo, hi, size=n)
     angles = rng.uniform(0.0, np.pi, size=n)
+    segs = []
+    for (cx, cy), ln, th in zip(centres, lengths, angles):
+        dx, dy = 0.5 * ln * np.cos(th), 0.5 * ln * np.sin(th)
+        segs.append((cx - dx, cy - dy, cx + dx, cy + dy))
+    return np.array(segs, dtype=np.float64).reshape(-1, 4), 0.5 * (side / nx)
+
+
+def precrack_nodes(case: LoadCase, mesh) -> np.ndarray:
+    """Nodes within h/2 of one of the seeded straight pre-cracks (precrack_segments); the
+    host reference of the device initialiser (DeviceSession.init_state / pf_init_state)."""
+    if case.precracks is None:
+        return np.zeros(0, dtype=np.int64)
+    _, nx, ny, side, _ = case.mesh
+    segs, _ = precrack_segments(case)
     h = side / nx
     coords = np.asarray(mesh.nodes)
     # regular-grid lookup (column i, row j) -> node id; the multi-crack square has no notch
@@ -235,9 +250,7 @@ def precrack_nodes(case: LoadCase, mesh) -> np.ndarray:
     lut = np.full((ny + 1, nx + 1), -1, dtype=np.int64)
     lut[gj, gi] = np.arange(coords.shape[0])
     hit = np.zeros(coords.shape[0], dtype=bool)
-    for (cx, cy), ln, th in zip(centres, lengths, angles):
-        dx, dy = 0.5 * ln * np.cos(th), 0.5 * ln * np.sin(th)
-        ax, ay, bx, by = cx - dx, cy - dy, cx + dx, cy + dy
+    for ax, ay, bx, by in segs:
         i0 = max(int(np.floor((min(ax, bx) - h) / h)), 0)
         i1 = min(int(np.ceil((max(ax, bx) + h) / h)), nx)
         j0 = max(int(np.floor((min(ay, by) - h) / h)), 0)

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <string>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "../../include/pf_b200.h"
@@ -48,6 +49,7 @@ struct MgInst {
 };
 
 struct pf_handle {
+  double hx = 0.0, hy = 0.0;  // uniform cell size (node (i, j) at (i hx, j hy))
   int device = 0;
   cudaStream_t stream = nullptr;
   pfb::DMesh dm{};
@@ -1016,6 +1018,8 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
     CREATE_CUDA(cudaMalloc((void**)&h->gB, (pfb::CG_SLOTS + 1) * 2 * sizeof(double)));
   }
   build_consts(h, mesh->hx, mesh->hy);
+  h->hx = mesh->hx;
+  h->hy = mesh->hy;
   const size_t nn = h->n_nodes, ne = h->n_elems;
   pf_status s2 = PF_OK;
 #define CREATE_ALLOC(ptr, n) \
@@ -1397,6 +1401,36 @@ extern "C" pf_status pf_set_state(pf_handle* h, const double* u, const double* d
                    {c(trp), h->trp, ng}, {c(dev2), h->dev2, ng}, {c(psi), h->psi, ng},
                    {c(psimax), h->psimax, ng}},
                   true);
+}
+
+// Device-side state construction: the zero state of SolverState.zeros (schemes.py:80-87) plus
+// d = d_prev = 1 at the pre-crack nodes (configs.precrack_nodes), without host arrays.
+extern "C" pf_status pf_init_state(pf_handle* h, const double* segments, int64_t n_segments,
+                                   double radius, double x_last, double y_last) {
+  if (!h) return PF_ERR_INVALID;
+  PF_CUDA(cudaSetDevice(h->device));
+  if (h->comm) return fail(h, PF_ERR_INVALID, "pf_init_state: single-GPU handles only");
+  if (n_segments < 0 || (n_segments > 0 && !segments))
+    return fail(h, PF_ERR_INVALID, "pf_init_state: bad segment list");
+  const size_t nn = h->n_nodes, ng = 4 * (size_t)h->n_elems;
+  for (auto pr : {std::make_pair(h->u, 2 * nn), std::make_pair(h->d, nn),
+                  std::make_pair(h->dprev, nn), std::make_pair(h->trp, ng),
+                  std::make_pair(h->dev2, ng), std::make_pair(h->psi, ng),
+                  std::make_pair(h->psimax, ng)})
+    PF_CUDA(cudaMemsetAsync(pr.first, 0, pr.second * sizeof(double), h->stream));
+  if (n_segments > 0) {
+    double4* dseg = nullptr;
+    PF_CUDA(cudaMallocAsync((void**)&dseg, (size_t)n_segments * sizeof(double4), h->stream));
+    PF_CUDA(cudaMemcpyAsync(dseg, segments, (size_t)n_segments * sizeof(double4),
+                            cudaMemcpyHostToDevice, h->stream));
+    pfb::k_precrack<<<8 * h->sm_count, 256, 0, h->stream>>>(h->dm, h->hx, h->hy, x_last, y_last,
+                                                          dseg, (int)n_segments, radius, h->d,
+                                                          h->dprev);
+    PF_TRY(launched(h));
+    PF_CUDA(cudaFreeAsync(dseg, h->stream));
+  }
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  return PF_OK;
 }
 
 extern "C" pf_status pf_get_state(pf_handle* h, double* u, double* d, double* d_prev,

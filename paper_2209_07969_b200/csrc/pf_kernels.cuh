@@ -664,6 +664,43 @@ __global__ void k_reaction(const double* R, const long long* nodes, long long n,
   if (threadIdx.x == 0) out[0] = s[0];
 }
 
+// Device-side pre-crack initialiser (configs.precrack_nodes): d = d_prev = 1
+// at every node within `radius` of one of the segments (ax, ay, bx, by).  Node (i, j) sits at
+// (i hx, j hy) like np.linspace(0, side, n + 1), the last column / row exactly at x_last /
+// y_last; a slit position marks its duplicate (the host LUT's last write).  The distance is the
+// host's expression in the same operation order, without FMA contraction.
+__global__ void k_precrack(DMesh m, double hx, double hy, double x_last, double y_last,
+                           const double4* __restrict__ seg, int n_seg, double radius,
+                           double* __restrict__ d, double* __restrict__ dprev) {
+  const long long total = (long long)(m.nx + 1) * (m.ny + 1);
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % (m.nx + 1)), j = (int)(t / (m.nx + 1));
+    const int4 rw = __ldg(m.nrow + j);
+    if (i < rw.x || i >= rw.y) continue;
+    const bool dpos = j == m.notch_row && i >= m.notch_lo && i < m.notch_hi;
+    const int id = dpos ? m.dup_start + (i - m.notch_lo) : rw.z + (i - rw.x);
+    const double px = i == m.nx ? x_last : __dmul_rn((double)i, hx);
+    const double py = j == m.ny ? y_last : __dmul_rn((double)j, hy);
+    bool hit = false;
+    for (int k = 0; k < n_seg && !hit; ++k) {
+      const double4 sg = seg[k];
+      const double ex = __dsub_rn(sg.z, sg.x), ey = __dsub_rn(sg.w, sg.y);
+      double tt = __ddiv_rn(__dadd_rn(__dmul_rn(__dsub_rn(px, sg.x), ex),
+                                      __dmul_rn(__dsub_rn(py, sg.y), ey)),
+                            __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)));
+      tt = fmin(fmax(tt, 0.0), 1.0);
+      const double qx = __dsub_rn(px, __dadd_rn(sg.x, __dmul_rn(tt, ex)));
+      const double qy = __dsub_rn(py, __dadd_rn(sg.y, __dmul_rn(tt, ey)));
+      hit = hypot(qx, qy) <= radius;
+    }
+    if (hit) {
+      d[id] = 1.0;
+      dprev[id] = 1.0;
+    }
+  }
+}
+
 __global__ void k_flush(double* buf, long long n, double v) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)

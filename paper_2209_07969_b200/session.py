@@ -156,6 +156,16 @@ class DeviceSession:
                 c(psi_plus, ng), c(psi_max, ng)]
         self._check(self.lib.pf_set_state(self.h, *[N.f64(a) for a in arrs]))
 
+    def init_state(self, segments=None, radius: float = 0.0, x_last: float = 0.0,
+                   y_last: float = 0.0) -> None:
+        """Zero state built on the device, with d = d_prev = 1 within ``radius`` of the pre-crack
+        segments ``[(ax, ay, bx, by), ...]`` (pf_init_state; configs.precrack_segments)."""
+        seg = np.ascontiguousarray(np.zeros((0, 4)) if segments is None else segments,
+                                   dtype=np.float64).reshape(-1, 4)
+        self._check(self.lib.pf_init_state(self.h, N.f64(seg) if seg.size else None,
+                                           seg.shape[0], float(radius), float(x_last),
+                                           float(y_last)))
+
     def push_state(self, state) -> None:
         gp = state.gp
         self.push(state.u, state.d, state.d_prev, gp.tr_eps_plus, gp.dev_dot_dev, gp.psi_plus,

@@ -1,8 +1,8 @@
 """BASELINE configs[4] (8192^2 cells, 67.1 M nodes, 201 M DOFs, 256 seeded pre-cracks, biaxial
 loading) on ONE B200 through the device session, without materialising the reference's element
-arrays: the row-compact layout of the plain square (StructuredLayout.rectangle), node
-coordinates only for the pre-crack initialiser (configs.precrack_nodes), boundary dofs from the
-layout.  Prints one JSON line per load step (n_stag, Newton counts, PCG iterations, step ms,
+arrays: the row-compact layout of the plain square (StructuredLayout.rectangle), boundary dofs
+from the layout, the zero state and the pre-cracks built on the device (DeviceSession.init_state,
+configs.precrack_segments).  Prints one JSON line per load step (n_stag, Newton counts, PCG iterations, step ms,
 reactions).
 
     python scripts/cfg5_run.py [n_steps] [scheme]
@@ -11,7 +11,6 @@ import json
 import os
 import sys
 import time
-from types import SimpleNamespace
 
 import numpy as np
 
@@ -28,10 +27,7 @@ h = side / nx
 t0 = time.perf_counter()
 lay = meshing.StructuredLayout.rectangle(nx, ny, h, h)
 ids = np.arange(lay.n_nodes, dtype=np.int64).reshape(ny + 1, nx + 1)
-gi, gj = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1))
-nodes = np.stack([gi.ravel() * h, gj.ravel() * h], axis=1)
-cracked = C.precrack_nodes(case, SimpleNamespace(nodes=nodes))
-del nodes, gi, gj
+segs, radius = C.precrack_segments(case)
 api = C.b200_api()
 params = C.material(case, api)
 config = api.SolverConfig(tol_st=case.tol_st)
@@ -40,12 +36,12 @@ bcs = [(2 * left, 0.0), (2 * bottom + 1, 0.0), (2 * right, case.inc), (2 * top +
 setup_s = time.perf_counter() - t0
 s = DeviceSession(lay, params, config, device=0)
 nn, ne = lay.n_nodes, lay.n_elems
-d = np.zeros(nn)
-d[cracked] = 1.0
-s.push(u=np.zeros(2 * nn), d=d, d_prev=d.copy(), tr_eps_plus=np.zeros((ne, 4)),
-       dev_dot_dev=np.zeros((ne, 4)), psi_plus=np.zeros((ne, 4)), psi_max=np.zeros((ne, 4)))
+t1 = time.perf_counter()
+s.init_state(segs, radius, side, side)  # zero state + pre-cracks built on the device
+init_s = time.perf_counter() - t1
 print(json.dumps({"case": "cfg5", "n_nodes": nn, "n_cells": ne, "dofs": 3 * nn,
-                  "precracked_nodes": int(cracked.size), "host_setup_s": round(setup_s, 1),
+                  "precrack_segments": int(segs.shape[0]), "host_setup_s": round(setup_s, 2),
+                  "device_init_s": round(init_s, 3),
                   "mg": s.mg_info()}), flush=True)
 for k in range(1, n_steps + 1):
     st = s.step(scheme, bcs)
