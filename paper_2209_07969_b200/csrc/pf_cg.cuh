@@ -169,10 +169,7 @@ __device__ __forceinline__ void grid_reduce(const double* part, int stride, doub
     double s[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) {
-#pragma unroll
-      for (int k = 0; k < NV; ++k) s[k] += __ldcg(part + stride * i + k);
-    }
+    lane_ordered_sum<NV>(part, stride, (int)gridDim.x, s);
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = warp_sum(s[k]);
     if (threadIdx.x == 0) {
@@ -653,10 +650,7 @@ __device__ __forceinline__ void reduce_parts(const double* part, int n, double* 
     double s[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) s[q] = 0.0;
-    for (int i = threadIdx.x; i < n; i += 32) {
-#pragma unroll
-      for (int q = 0; q < NV; ++q) s[q] += __ldcg(part + NV * i + q);
-    }
+    lane_ordered_sum<NV>(part, NV, n, s);
 #pragma unroll
     for (int q = 0; q < NV; ++q) s[q] = warp_sum(s[q]);
     if (threadIdx.x == 0) {

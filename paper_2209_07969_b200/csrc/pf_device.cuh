@@ -83,6 +83,32 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // Block-wide sum of NV values; result valid in thread 0. `red` holds NT/32*NV doubles.
+// Lane's ordered partial sum of part[stride * i + k] over i = lane, lane + 32, ... < n: the
+// loads of LANE_SUM_BATCH rows are issued before their adds, so a grid-wide reduction costs one
+// L2 round trip per batch instead of one per row (the additions, and so the bits, are those of
+// the plain loop).
+constexpr int LANE_SUM_BATCH = 4;
+template <int NV>
+__device__ __forceinline__ void lane_ordered_sum(const double* part, int stride, int n,
+                                                 double (&s)[NV]) {
+  constexpr int B = NV <= 3 ? LANE_SUM_BATCH : 1;  // (wide partial rows: registers)
+  for (int base = (int)(threadIdx.x & 31); base < n; base += 32 * B) {
+    double v[B][NV];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int i = base + 32 * q;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) v[q][k] = i < n ? __ldcg(part + (size_t)stride * i + k) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < B; ++q)
+      if (base + 32 * q < n) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) s[k] += v[q][k];
+      }
+  }
+}
+
 template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

@@ -896,9 +896,7 @@ __device__ __forceinline__ void mg_all_reduce(const double* part, int nparts, do
     double s[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = 0.0;
-    for (int i = threadIdx.x; i < nparts; i += 32)
-#pragma unroll
-      for (int k = 0; k < NV; ++k) s[k] += __ldcg(part + NV * i + k);
+    lane_ordered_sum<NV>(part, NV, nparts, s);
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = warp_sum(s[k]);
     if (threadIdx.x == 0)
