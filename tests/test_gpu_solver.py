@@ -100,12 +100,14 @@ def test_fast_schemes_reduce_crack_step_iterations(cuda_ok):
         assert CFG1_MAX_STAG[scheme] < 0.75 * CFG1_MAX_STAG["ST"], CFG1_MAX_STAG
 
 
-def test_cfg2_first_steps(cuda_ok):
-    """BASELINE configs[1] at full size (512x512, 790k DOFs): first two load steps."""
-    z = golden("run_cfg2_ST_2steps.npz")
-    pb, recs = run_case("cfg2", "ST", steps=2)
-    check_against_golden(recs, z, pb.state, "cfg2", "ST", pb.mesh,
-                         run_file="run_cfg2_ST_2steps.npz")
+@pytest.mark.parametrize("scheme", ["ST", "S1"])
+def test_cfg2_first_steps(cuda_ok, scheme):
+    """BASELINE configs[1] at full size (512x512, 790k DOFs): first two load steps, with the
+    bench's scheme S1 too (multigrid momentum PCG + assembled-stencil phase-field PCG)."""
+    z = golden(f"run_cfg2_{scheme}_2steps.npz")
+    pb, recs = run_case("cfg2", scheme, steps=2)
+    check_against_golden(recs, z, pb.state, "cfg2", scheme, pb.mesh,
+                         run_file=f"run_cfg2_{scheme}_2steps.npz")
 
 
 @pytest.mark.parametrize("case,scheme", [("tension16", "S1"), ("tension16", "S2"),
