@@ -669,9 +669,12 @@ static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_w
       ML.item_off = coarse_items;  // set below, once lpn is known
       M.gl[l] = (ML.items + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
       // small levels: a half-warp per node (all loads of a node in flight); large levels: a
-      // thread per node (latency hidden by occupancy).  Threshold: 16 lanes per node would
-      // exceed one wave of resident threads.
-      const long long wave = 2048LL * h->sm_count;
+      // thread per node (latency hidden by occupancy).  Threshold: the level's lanes stay within
+      // a quarter of one wave of resident threads (measured against a full wave: cfg2 MG
+      // iteration 127.7 -> 121.3 us in the bench, cfg4 273.8 -> 247.2 us, cfg3/cfg5 unchanged;
+      // an eighth of a wave: 132.5 us).  PFB200_MG_WAVE_X scales it (A/B tests).
+      const char* wx = getenv("PFB200_MG_WAVE_X");
+      const long long wave = (long long)(2048.0 * h->sm_count * (wx ? atof(wx) : 0.25));
       M.lpn[l] = 16LL * L.n_nodes <= wave ? 16 : (4LL * L.n_nodes <= wave ? 4 : 1);
       ML.lpn = M.lpn[l];
       ML.item_off = coarse_items;  // power steps: lpn threads per node, warp-aligned per level
