@@ -685,7 +685,8 @@ static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_w
         const std::vector<int> nb = hl_stencil_ids(L), rd = hl_restrict_ids(lv[l - 1], L);
         int *dnb = nullptr, *drd = nullptr;
         if (mg_alloc(h, &dnb, nb.size()) != cudaSuccess || mg_alloc(h, &drd, rd.size()) != cudaSuccess ||
-            mg_alloc(h, &ML.S, (size_t)4 * pfb::MG_NS * L.n_nodes) != cudaSuccess)
+            mg_alloc(h, &ML.S, (size_t)4 * pfb::MG_NS * L.n_nodes) != cudaSuccess ||
+            mg_alloc(h, &ML.Sf, (size_t)4 * pfb::MG_NS * L.n_nodes) != cudaSuccess)
           return oom();
         cudaMemcpy(dnb, nb.data(), nb.size() * sizeof(int), cudaMemcpyHostToDevice);
         cudaMemcpy(drd, rd.data(), rd.size() * sizeof(int), cudaMemcpyHostToDevice);

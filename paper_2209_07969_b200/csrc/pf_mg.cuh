@@ -54,6 +54,7 @@ struct MgLevel {
   // prolongation sources on level l+1 (l <= n_levels-2)
   const int* nbr;
   double* S;
+  float* Sf;      // S rounded to FP32 for the grid-level kernels (PFB_MG_S32; the tail keeps S)
   const int* rid;
   const int* pid;
 };
@@ -558,6 +559,24 @@ __device__ __forceinline__ double2 hw_sum(double2 v) {  // butterfly over W alig
   }
   return v;
 }
+// The 2x2 block of slot s2 at node id.  The grid-level kernels read it in FP32 (PFB_MG_S32,
+// default): the V-cycle is only the preconditioner -- the PCG's operator, residual and stopping
+// test stay FP64 -- and the coarse levels' stencil products are bound by these loads.
+#ifndef PFB_MG_S32
+#define PFB_MG_S32 1
+#endif
+__device__ __forceinline__ void mg_s4(const MgLevel& L, int n, int id, int s2, double& sxx,
+                                      double& sxy, double& syx, double& syy) {
+#if PFB_MG_S32
+  const float* Sp = L.Sf + (size_t)(4 * s2) * n + id;
+#else
+  const double* Sp = L.S + (size_t)(4 * s2) * n + id;
+#endif
+  sxx = __ldg(Sp);
+  sxy = __ldg(Sp + n);
+  syx = __ldg(Sp + 2 * (size_t)n);
+  syy = __ldg(Sp + 3 * (size_t)n);
+}
 // slot s2 of S_s x[nbr_s] at node id (zero for s2 >= MG_NS or no coupling)
 template <class X>
 __device__ __forceinline__ double2 mg_slot_apply(const MgLevel& L, int n, int id, int s2,
@@ -565,9 +584,8 @@ __device__ __forceinline__ double2 mg_slot_apply(const MgLevel& L, int n, int id
   if (s2 >= MG_NS || id >= n) return make_double2(0.0, 0.0);
   const int k = __ldg(L.nbr + (size_t)s2 * n + id);
   if (k < 0) return make_double2(0.0, 0.0);
-  const double* Sp = L.S + (size_t)(4 * s2) * n + id;
-  const double sxx = __ldg(Sp), sxy = __ldg(Sp + n), syx = __ldg(Sp + 2 * (size_t)n),
-               syy = __ldg(Sp + 3 * (size_t)n);
+  double sxx, sxy, syx, syy;
+  mg_s4(L, n, id, s2, sxx, sxy, syx, syy);
   const double2 x = xval(k);
   return make_double2(sxx * x.x + sxy * x.y, syx * x.x + syy * x.y);
 }
@@ -716,9 +734,8 @@ __global__ void __launch_bounds__(MG_NT) k_mg_sdown(MgArgs A, int l) {
         const double2 di = GMem::v2(L.dinv, k);
         b = mask2(b, di);
         if (s2 == 4) bc = b;  // the node itself
-        const double* Sp = L.S + (size_t)(4 * s2) * n + id;
-        const double sxx = __ldg(Sp), sxy = __ldg(Sp + n), syx = __ldg(Sp + 2 * (size_t)n),
-                     syy = __ldg(Sp + 3 * (size_t)n);
+        double sxx, sxy, syx, syy;
+        mg_s4(L, n, id, s2, sxx, sxy, syx, syy);
         const double2 x = make_double2(om * di.x * b.x, om * di.y * b.y);
         acc.x += sxx * x.x + sxy * x.y;
         acc.y += syx * x.x + syy * x.y;
@@ -762,9 +779,8 @@ __global__ void __launch_bounds__(MG_NT) k_mg_sup(MgArgs A, int l) {
         const double2 di = GMem::v2(L.dinv, k), bv = GMem::v2(L.b, k);
         const double2 y = mask2(make_double2(om * di.x * bv.x + w * pe.x, om * di.y * bv.y + w * pe.y), di);
         if (s2 == 4) yc = y;
-        const double* Sp = L.S + (size_t)(4 * s2) * n + id;
-        const double sxx = __ldg(Sp), sxy = __ldg(Sp + n), syx = __ldg(Sp + 2 * (size_t)n),
-                     syy = __ldg(Sp + 3 * (size_t)n);
+        double sxx, sxy, syx, syy;
+        mg_s4(L, n, id, s2, sxx, sxy, syx, syy);
         acc.x += sxx * y.x + sxy * y.y;
         acc.y += syx * y.x + syy * y.y;
       }
@@ -862,7 +878,10 @@ __global__ void __launch_bounds__(MG_NT) k_mg_stencil(MgArgs A, int l) {
 #pragma unroll
     for (int s2 = 0; s2 < MG_NS; ++s2)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) L.S[(size_t)(4 * s2 + q) * n + id] = acc[s2][q];
+      for (int q = 0; q < 4; ++q) {
+        L.S[(size_t)(4 * s2 + q) * n + id] = acc[s2][q];
+        L.Sf[(size_t)(4 * s2 + q) * n + id] = (float)acc[s2][q];
+      }
     d2st(L.dinv, id, make_double2(acc[4][0] > 0.0 ? 1.0 / acc[4][0] : 0.0,
                                   acc[4][3] > 0.0 ? 1.0 / acc[4][3] : 0.0));
   });
