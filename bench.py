@@ -362,6 +362,9 @@ def run_ours(args, ws, rank, local):
                     "algorithmic bytes",
         },
         "momentum_solver": ({"kind": "multigrid PCG (Galerkin V(1,1), CUDA graph)",
+                             "precision": "FP64 operator, residuals, dot products and stopping "
+                                          "test; grid-level coarse stencils stored FP32 "
+                                          "(preconditioner only)",
                              "levels": mg["n_levels"], "hierarchy_builds": mg.get("setups"),
                              "iterations": tot["cg_u"], "solves": tot["cgl_u"],
                              "us_per_iteration": 1e3 * tot["ms_u"] / max(tot["cg_u"], 1)}
