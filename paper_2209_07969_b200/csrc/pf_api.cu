@@ -709,6 +709,7 @@ static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_w
   M.gflat = 2 * h->sm_count;
   if (mg_alloc(h, &A.z, 2 * (size_t)h->n_nodes) != cudaSuccess) return oom();
   A.phys = phys;
+  for (int l = 0; l < nl; ++l) A.L[l].scalar = phys == 1 ? 1 : 0;
   if (phys == 0) {
     A.L[0].dinv = h->dinvu;
   } else {  // phase field: scalar vectors packed as (value, 0) per node (y dofs dead)

@@ -49,6 +49,7 @@ struct MgLevel {
   int items;      // node items (rows x 32-column chunks) of mg_for_nodes
   int item_off;   // first thread of this level in the power steps' coarse thread space
   int lpn;        // lanes per node of the level's node kernels (1 | 4 | 16)
+  int scalar;     // phase field (phys 1): only the xx entry of each 2x2 block is non-zero
   // assembled form (l >= 1), slot-major: nbr [MG_NS][n] neighbour ids, S [MG_NS*4][n] 2x2
   // blocks (xx, xy, yx, yy); rid [12][n] restriction sources on level l-1; pid [4][n]
   // prolongation sources on level l+1 (l <= n_levels-2)
@@ -573,6 +574,10 @@ __device__ __forceinline__ void mg_s4(const MgLevel& L, int n, int id, int s2, d
   const double* Sp = L.S + (size_t)(4 * s2) * n + id;
 #endif
   sxx = __ldg(Sp);
+  if (L.scalar) {  // the packed scalar field: xy, yx, yy are exactly zero (warp-uniform)
+    sxy = syx = syy = 0.0;
+    return;
+  }
   sxy = __ldg(Sp + n);
   syx = __ldg(Sp + 2 * (size_t)n);
   syy = __ldg(Sp + 3 * (size_t)n);
