@@ -1557,7 +1557,13 @@ __device__ __forceinline__ void mg_galerkin(const MgArgs& A, int lc, int worker,
   }
 }
 
-__global__ void __launch_bounds__(MG_NT) k_mg_galerkin(MgArgs A, int lc) {
+// two CTAs per SM (128 registers, 224 B stack): hierarchy setup cfg5 119.9 -> 106.1 ms, cfg3
+// 2.33 -> 2.05 ms (one CTA with 167 registers left the per-cell latency chains exposed; three
+// CTAs at 80 registers spill 464 B and land in between)
+#ifndef PFB_MG_GAL_MINB
+#define PFB_MG_GAL_MINB 2
+#endif
+__global__ void __launch_bounds__(MG_NT, PFB_MG_GAL_MINB) k_mg_galerkin(MgArgs A, int lc) {
   __shared__ MgGal sg[MG_WARPS];
   mg_galerkin(A, lc, blockIdx.x * MG_WARPS + (threadIdx.x >> 5), gridDim.x * MG_WARPS,
               sg[threadIdx.x >> 5]);
