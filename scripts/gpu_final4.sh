@@ -1,7 +1,7 @@
 # Round-1 closing measurement (v10: final code): GPU test suite, smoke, bench line + reference arm,
 # bench launch list.  The k_cg_st ncu capture of v9 (gpu_final3.sh) is of the same kernel.
 cd "${GRAFT_REPO_ROOT:-.}"
-TAG=${TAG:-v14}
+TAG=${TAG:-v15}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm --format=csv,noheader > gpurun_out/gpu.txt
 timeout 1500 python -m pytest tests -m gpu -q -x --durations=5 > gpurun_out/gpu_all.log 2>&1; echo "gpu tests exit $?"; tail -2 gpurun_out/gpu_all.log
