@@ -132,6 +132,9 @@ pf_status pf_init_state(pf_handle* h, const double* segments, int64_t n_segments
 /* gp.strain [n_elems*4*4] Voigt (xx,yy,zz,xy) and gp.tr_eps [n_elems*4] recomputed from u
  * (refresh_gp_from_displacement, assembly.py:260-269). */
 pf_status pf_get_gp_strain(pf_handle* h, double* strain, double* tr_eps);
+/* Discretization.interp_nodal (assembly.py:148-150): the nodal scalar field field[n_nodes]
+ * interpolated at the 4 Gauss points of every cell, out[n_elems*4] (reference GP order). */
+pf_status pf_interp_nodal(pf_handle* h, const double* field, double* out);
 /* Page-locked host buffers (cudaHostAlloc): state arrays in them move by direct DMA in
  * pf_set_state / pf_get_state / pf_get_gp_strain (other host pointers go through the handle's
  * pinned staging buffer). */

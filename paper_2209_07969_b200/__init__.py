@@ -9,8 +9,3 @@ __version__ = "0.1.0"
 
 from . import configs, material, meshing  # noqa: F401  (pure host modules)
 
-
-def _lazy():
-    from . import assembly, schemes, session  # noqa: F401
-
-    return assembly, schemes, session

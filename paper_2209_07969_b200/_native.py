@@ -88,6 +88,7 @@ _SIGNATURES = {
     "pf_set_state": (C.c_int, [C.c_void_p] + [_f64p] * 7),
     "pf_get_state": (C.c_int, [C.c_void_p] + [_f64p] * 7),
     "pf_get_gp_strain": (C.c_int, [C.c_void_p, _f64p, _f64p]),
+    "pf_interp_nodal": (C.c_int, [C.c_void_p, _f64p, _f64p]),
     "pf_staggered_step": (C.c_int, [C.c_void_p, C.c_int, _i64p, _i64p, _f64p, C.c_int32,
                                     _i64p, C.c_int64, C.POINTER(PfStats), _f64p, C.c_int32]),
     "pf_solve_momentum": (C.c_int, [C.c_void_p, _i64p, _i64p, _f64p, C.c_int32, _f64p, _i32p,

@@ -15,7 +15,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .material import material_key
+from .material import MaterialParams, StrainState, material_key
 from .meshing import StructuredLayout
 from .session import DeviceSession
 
@@ -72,6 +72,19 @@ class Discretization:
         self.n_u_dofs = 2 * mesh.n_nodes
         self.n_d_dofs = mesh.n_nodes
 
+    # field evaluation at Gauss points (assembly.py:148-158), on the device
+    def interp_nodal(self, field) -> np.ndarray:
+        """Nodal scalar field interpolated at every Gauss point, (n_elems, 4)."""
+        return _any_session(self).interp_nodal(field)
+
+    def strain_state(self, u) -> StrainState:
+        """Voigt strain at every Gauss point of the displacement ``u`` (eps_zz = 0) and its
+        invariants (reference ``strain_state`` + ``StrainState.from_voigt``)."""
+        sess = _any_session(self)
+        sess.push(u=u)
+        strain, _ = sess.gp_strain()
+        return StrainState.from_voigt(strain)
+
 
 def _layout_of(disc) -> StructuredLayout:
     lay = getattr(disc, "layout", None)
@@ -108,6 +121,15 @@ def session_for(disc, params, config=None) -> DeviceSession:
         sess = DeviceSession(_layout_of(disc), params, config)
         sessions[key] = sess
     return sess
+
+
+def _any_session(disc) -> DeviceSession:
+    """A device session of this discretisation for geometry-only operations (interpolation,
+    strains): any cached one, else one with placeholder material constants (unused by them)."""
+    sessions = disc.__dict__.setdefault("_pfb200_sessions", {})
+    if sessions:
+        return next(iter(sessions.values()))
+    return session_for(disc, MaterialParams(mu=1.0, lam=1.0, g_c=1.0, length_l=1.0))
 
 
 def internal_force(disc, u, d, params) -> np.ndarray:

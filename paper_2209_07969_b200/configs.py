@@ -244,18 +244,25 @@ def precrack_nodes(case: LoadCase, mesh) -> np.ndarray:
     segs, _ = precrack_segments(case)
     h = side / nx
     coords = np.asarray(mesh.nodes)
-    # regular-grid lookup (column i, row j) -> node id; the multi-crack square has no notch
+    # regular-grid lookup (column i, row j) -> node ids; a slit position of a notched square
+    # holds two nodes (the crack faces share the coordinates) and both are tested
     gi = np.rint(coords[:, 0] / h).astype(np.int64)
     gj = np.rint(coords[:, 1] / h).astype(np.int64)
-    lut = np.full((ny + 1, nx + 1), -1, dtype=np.int64)
-    lut[gj, gi] = np.arange(coords.shape[0])
+    key = gj * (nx + 1) + gi
+    order = np.argsort(key, kind="stable")
+    ks = key[order]
+    first = np.r_[True, ks[1:] != ks[:-1]]
+    lut = np.full((2, (ny + 1) * (nx + 1)), -1, dtype=np.int64)
+    lut[0, ks[first]] = order[first]
+    lut[1, ks[~first]] = order[~first]
+    lut = lut.reshape(2, ny + 1, nx + 1)
     hit = np.zeros(coords.shape[0], dtype=bool)
     for ax, ay, bx, by in segs:
         i0 = max(int(np.floor((min(ax, bx) - h) / h)), 0)
         i1 = min(int(np.ceil((max(ax, bx) + h) / h)), nx)
         j0 = max(int(np.floor((min(ay, by) - h) / h)), 0)
         j1 = min(int(np.ceil((max(ay, by) + h) / h)), ny)
-        ids = lut[j0:j1 + 1, i0:i1 + 1].ravel()
+        ids = lut[:, j0:j1 + 1, i0:i1 + 1].ravel()
         ids = ids[ids >= 0]
         px, py = coords[ids, 0], coords[ids, 1]
         ex, ey = bx - ax, by - ay
@@ -311,13 +318,16 @@ class StepRecord:
     wall: float = 0.0
 
 
-def run(problem: Problem, scheme: str, n_steps: int | None = None, on_step=None) -> list:
-    """Advance ``n_steps`` load steps (default: the case's full schedule)."""
+def run(problem: Problem, scheme: str, n_steps: int | None = None, on_step=None,
+        first_step: int = 1) -> list:
+    """Advance ``n_steps`` load steps (default: the case's full schedule), numbering them from
+    ``first_step`` (a restart from a saved state: every load step applies the same increment,
+    so the number is only a label)."""
     api = problem.api
     kind = api.SchemeKind(scheme)
     n = problem.case.n_steps if n_steps is None else n_steps
     out = []
-    for k in range(1, n + 1):
+    for k in range(first_step, first_step + n):
         t0 = time.perf_counter()
         st = api.staggered_step(problem.disc, problem.state, kind, problem.bcs,
                                 problem.params, problem.config, problem.pins)

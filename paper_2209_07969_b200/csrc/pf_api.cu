@@ -1398,6 +1398,7 @@ static pf_status d2h(pf_handle* h, double* dst, const double* src, size_t n) {
 extern "C" pf_status pf_set_state(pf_handle* h, const double* u, const double* d,
                                   const double* d_prev, const double* trp, const double* dev2,
                                   const double* psi, const double* psimax) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   const size_t nn = h->n_nodes, ng = 4 * (size_t)h->n_elems;
   auto c = [](const double* p) { return const_cast<double*>(p); };
@@ -1440,6 +1441,7 @@ extern "C" pf_status pf_init_state(pf_handle* h, const double* segments, int64_t
 
 extern "C" pf_status pf_get_state(pf_handle* h, double* u, double* d, double* d_prev,
                                   double* trp, double* dev2, double* psi, double* psimax) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   const size_t nn = h->n_nodes, ng = 4 * (size_t)h->n_elems;
   return transfer(h,
@@ -1478,6 +1480,7 @@ extern "C" void pf_host_free(void* p) {
 }
 
 extern "C" pf_status pf_get_gp_strain(pf_handle* h, double* strain, double* tr_eps) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   const size_t ne = h->n_elems;
   double* tr_dev = h->scratch;  // tr first (4 ne), then strain needs 16 ne: do two passes
@@ -1497,6 +1500,22 @@ extern "C" pf_status pf_get_gp_strain(pf_handle* h, double* strain, double* tr_e
     PF_TRY(d2h(h, strain, h->scratch, 16 * ne));
   }
   return PF_OK;
+}
+
+// interp_nodal (assembly.py:148-150) of a host nodal field: [n_nodes] -> [n_elems*4]
+extern "C" pf_status pf_interp_nodal(pf_handle* h, const double* field, double* out) {
+  if (!h) return PF_ERR_INVALID;
+  if (!field || !out) return fail(h, PF_ERR_INVALID, "pf_interp_nodal: null array");
+  PF_CUDA(cudaSetDevice(h->device));
+  const size_t nn = h->n_nodes, ne = h->n_elems;
+  double* fd = h->scratch;                        // scratch holds 16 n_elems doubles
+  double* od = h->scratch + ((nn + 1) & ~size_t(1));  // >= nn, 16-byte aligned
+  if (((nn + 1) & ~size_t(1)) + 4 * ne > 16 * ne)
+    return fail(h, PF_ERR_INVALID, "pf_interp_nodal: mesh too small for the scratch buffer");
+  PF_TRY(h2d(h, fd, field, nn));
+  pfb::k_interp_nodal<<<cell_grid(h), 128, 0, h->stream>>>(gp_args(h), fd, od);
+  PF_TRY(launched(h));
+  return d2h(h, out, od, 4 * ne);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -2268,6 +2287,7 @@ extern "C" pf_status pf_solve_momentum(pf_handle* h, const int64_t* bc_dofs,
                                        const int64_t* bc_offsets, const double* bc_incs,
                                        int32_t n_bc, double* r0_u, int32_t* n_nr,
                                        double* last_ratio) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   h->acc = pf_stats{};
   BcView bc{bc_dofs, bc_offsets, bc_incs, n_bc};
@@ -2283,6 +2303,7 @@ extern "C" pf_status pf_solve_momentum(pf_handle* h, const int64_t* bc_dofs,
 extern "C" pf_status pf_solve_evolution(pf_handle* h, int scheme, const int64_t* pins,
                                         int64_t n_pins, double* r0_d, int32_t* n_nr,
                                         int32_t* spd_fallbacks) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   h->acc = pf_stats{};
   PF_TRY(set_pmask(h, pins, n_pins));
@@ -2296,12 +2317,14 @@ extern "C" pf_status pf_solve_evolution(pf_handle* h, int scheme, const int64_t*
 
 extern "C" pf_status pf_evolution_residual_norm(pf_handle* h, const int64_t* pins,
                                                 int64_t n_pins, double* out) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   PF_TRY(set_pmask(h, pins, n_pins));
   return evo_norm(h, out);
 }
 
 extern "C" pf_status pf_commit_step(pf_handle* h) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   PF_TRY(commit(h));
   PF_CUDA(cudaStreamSynchronize(h->stream));
@@ -2311,6 +2334,7 @@ extern "C" pf_status pf_commit_step(pf_handle* h) {
 // ------------------------------------------------------------------------------------------
 // operators at the current state
 extern "C" pf_status pf_internal_force(pf_handle* h, double* f_out) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   PF_TRY(launch_mom_prepare(h, 0));
   PF_TRY(d2h(h, f_out, h->Ru, 2 * (size_t)h->n_nodes));
@@ -2320,6 +2344,7 @@ extern "C" pf_status pf_internal_force(pf_handle* h, double* f_out) {
 
 extern "C" pf_status pf_reaction_force(pf_handle* h, const int64_t* nodes, int64_t n,
                                        int component, double* out) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   if (component < 0 || component > 1) return fail(h, PF_ERR_INVALID, "component must be 0 or 1");
   for (int64_t i = 0; i < n; ++i)
@@ -2345,6 +2370,7 @@ extern "C" pf_status pf_reaction_force(pf_handle* h, const int64_t* nodes, int64
 
 extern "C" pf_status pf_momentum_tangent_apply(pf_handle* h, const double* x, double* y,
                                                double* diag) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   PF_TRY(launch_mom_prepare(h, 1));  // branch flags and raw diagonal at the current u
   PF_TRY(h2d(h, h->p0u, x, 2 * (size_t)h->n_nodes));
@@ -2359,6 +2385,7 @@ extern "C" pf_status pf_momentum_tangent_apply(pf_handle* h, const double* x, do
 }
 
 extern "C" pf_status pf_evolution_residual(pf_handle* h, double* r_out) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   PF_TRY(launch_evo_prepare(h, 0, 0));
   PF_TRY(d2h(h, r_out, h->Rd, (size_t)h->n_nodes));
@@ -2368,6 +2395,7 @@ extern "C" pf_status pf_evolution_residual(pf_handle* h, double* r_out) {
 
 extern "C" pf_status pf_evolution_tangent_apply(pf_handle* h, int scheme, const double* x,
                                                 double* y, double* diag) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   if (scheme < PF_ST || scheme > PF_S3) return fail(h, PF_ERR_INVALID, "unknown scheme");
   PF_TRY(launch_evo_prepare(h, 1, scheme));
@@ -2383,6 +2411,7 @@ extern "C" pf_status pf_evolution_tangent_apply(pf_handle* h, int scheme, const 
 }
 
 extern "C" pf_status pf_refresh_gp(pf_handle* h) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   pfb::GpArgs g = gp_args(h);
   pfb::k_refresh_gp<<<cell_grid(h), 128, 0, h->stream>>>(g);
@@ -2392,6 +2421,7 @@ extern "C" pf_status pf_refresh_gp(pf_handle* h) {
 }
 
 extern "C" pf_status pf_softening_gate(pf_handle* h, uint8_t* gate_out) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   pfb::GpArgs g = gp_args(h);
   g.gate = reinterpret_cast<uint8_t*>(h->scratch);
@@ -2404,6 +2434,7 @@ extern "C" pf_status pf_softening_gate(pf_handle* h, uint8_t* gate_out) {
 }
 
 extern "C" pf_status pf_extra_stiffness(pf_handle* h, int scheme, double* extra_out) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   if (scheme < PF_ST || scheme > PF_S3) return fail(h, PF_ERR_INVALID, "unknown scheme");
   pfb::GpArgs g = gp_args(h);
@@ -2417,6 +2448,7 @@ extern "C" pf_status pf_extra_stiffness(pf_handle* h, int scheme, double* extra_
 }
 
 extern "C" pf_status pf_update_active_energy(pf_handle* h, int scheme, const double* dd) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   if (scheme < PF_ST || scheme > PF_S3) return fail(h, PF_ERR_INVALID, "unknown scheme");
   if (scheme == PF_ST) return PF_OK;  // schemes.py:162-163
@@ -2433,6 +2465,7 @@ extern "C" pf_status pf_update_active_energy(pf_handle* h, int scheme, const dou
 // ------------------------------------------------------------------------------------------
 extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, double* ms_out,
                                  int64_t* iters_out) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   if (n_iter < 1 || physics < 0 || physics > 2) return fail(h, PF_ERR_INVALID, "bad arguments");
   if (physics == 2) {  // multigrid-preconditioned momentum PCG
@@ -2472,6 +2505,7 @@ extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, doub
 
 extern "C" pf_status pf_mg_info(pf_handle* h, int32_t* n_levels, int32_t* n_grid,
                                 int32_t* dense, int64_t* setups, double* omega) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   if (setups) *setups = h->mgu.setups;
   if (n_levels) *n_levels = h->mgu.on ? h->mgu.A.n_levels : 0;
@@ -2488,6 +2522,7 @@ extern "C" pf_status pf_mg_info(pf_handle* h, int32_t* n_levels, int32_t* n_grid
 }
 
 extern "C" pf_status pf_solver_kinds(pf_handle* h, int32_t* momentum, int32_t* phase_field) {
+  if (!h) return PF_ERR_INVALID;
   if (momentum) *momentum = h->mgu.on ? 2 : (h->sr_mom ? 1 : 0);
   if (phase_field)
     *phase_field = h->mgd.on && !h->comm ? 3
@@ -2497,6 +2532,7 @@ extern "C" pf_status pf_solver_kinds(pf_handle* h, int32_t* momentum, int32_t* p
 
 extern "C" pf_status pf_device_info(pf_handle* h, int32_t* cg_grid, int32_t* sm_count,
                                     int64_t* l2_bytes) {
+  if (!h) return PF_ERR_INVALID;
   if (cg_grid) *cg_grid = h->cg_grid;
   if (sm_count) *sm_count = h->sm_count;
   if (l2_bytes) *l2_bytes = h->l2_bytes;
@@ -2504,6 +2540,7 @@ extern "C" pf_status pf_device_info(pf_handle* h, int32_t* cg_grid, int32_t* sm_
 }
 
 extern "C" pf_status pf_flush_l2(pf_handle* h) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   if (!h->flushbuf) {
     h->flush_n = (size_t)std::max<long long>(2 * h->l2_bytes, 256LL << 20) / sizeof(double);
@@ -2516,6 +2553,7 @@ extern "C" pf_status pf_flush_l2(pf_handle* h) {
 }
 
 extern "C" pf_status pf_synchronize(pf_handle* h) {
+  if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
   PF_CUDA(cudaStreamSynchronize(h->stream));
   return PF_OK;

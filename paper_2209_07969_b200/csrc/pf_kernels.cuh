@@ -563,6 +563,19 @@ __global__ void k_refresh_gp(GpArgs a) {
   }
 }
 
+// interp_nodal (assembly.py:148-150): a nodal scalar field at the four Gauss points of each cell
+__global__ void k_interp_nodal(GpArgs a, const double* __restrict__ field,
+                               double* __restrict__ out) {
+  const int ci = blockIdx.x * blockDim.x + threadIdx.x, cj = blockIdx.y;
+  const int eid = cell_at(a.m, ci, cj);
+  if (eid < 0) return;
+  int n[4];
+  cell_nodes(a.m, ci, cj, n);
+  double v[4];
+  interp_q4(a.C, ldro(field + n[0]), ldro(field + n[1]), ldro(field + n[2]), ldro(field + n[3]), v);
+  store4(out, eid, v);
+}
+
 // K9: update_active_energy (schemes.py:145-176) at GPs gated before the solve
 // (gate recomputed from the unchanged pre-solve d, psi+, psi_max).
 __global__ void k_update_energy(GpArgs a) {
@@ -667,8 +680,9 @@ __global__ void k_reaction(const double* R, const long long* nodes, long long n,
 // Device-side pre-crack initialiser (configs.precrack_nodes): d = d_prev = 1
 // at every node within `radius` of one of the segments (ax, ay, bx, by).  Node (i, j) sits at
 // (i hx, j hy) like np.linspace(0, side, n + 1), the last column / row exactly at x_last /
-// y_last; a slit position marks its duplicate (the host LUT's last write).  The distance is the
-// host's expression in the same operation order, without FMA contraction.
+// y_last; a slit position marks both crack faces (the base node and its duplicate share the
+// coordinates).  The distance is the host's expression in the same operation order, without FMA
+// contraction.
 __global__ void k_precrack(DMesh m, double hx, double hy, double x_last, double y_last,
                            const double4* __restrict__ seg, int n_seg, double radius,
                            double* __restrict__ d, double* __restrict__ dprev) {
@@ -679,7 +693,7 @@ __global__ void k_precrack(DMesh m, double hx, double hy, double x_last, double 
     const int4 rw = __ldg(m.nrow + j);
     if (i < rw.x || i >= rw.y) continue;
     const bool dpos = j == m.notch_row && i >= m.notch_lo && i < m.notch_hi;
-    const int id = dpos ? m.dup_start + (i - m.notch_lo) : rw.z + (i - rw.x);
+    const int id = rw.z + (i - rw.x);
     const double px = i == m.nx ? x_last : __dmul_rn((double)i, hx);
     const double py = j == m.ny ? y_last : __dmul_rn((double)j, hy);
     bool hit = false;
@@ -697,6 +711,11 @@ __global__ void k_precrack(DMesh m, double hx, double hy, double x_last, double 
     if (hit) {
       d[id] = 1.0;
       dprev[id] = 1.0;
+      if (dpos) {
+        const int dup = m.dup_start + (i - m.notch_lo);
+        d[dup] = 1.0;
+        dprev[dup] = 1.0;
+      }
     }
   }
 }

@@ -79,6 +79,27 @@ class MaterialParams:
         return self.g_c / (self.c_w * self.length_l) * 2.0 * np.ones_like(d)
 
 
+VOIGT_XX, VOIGT_YY, VOIGT_ZZ, VOIGT_XY = 0, 1, 2, 3
+
+
+@dataclass
+class StrainState:
+    """Voigt strain [xx, yy, zz, xy] (engineering shear) and the two invariants the split uses
+    (interface mirror of the reference's ``StrainState``, ``material.py:99-116``)."""
+
+    eps: np.ndarray
+    tr_eps: np.ndarray
+    dev_dot_dev: np.ndarray
+
+    @classmethod
+    def from_voigt(cls, eps) -> "StrainState":
+        eps = np.asarray(eps, dtype=float)
+        tr = eps[..., VOIGT_XX] + eps[..., VOIGT_YY] + eps[..., VOIGT_ZZ]
+        dev = [eps[..., k] - tr / 3.0 for k in (VOIGT_XX, VOIGT_YY, VOIGT_ZZ)]
+        dev2 = dev[0] ** 2 + dev[1] ** 2 + dev[2] ** 2 + 0.5 * eps[..., VOIGT_XY] ** 2
+        return cls(eps=eps, tr_eps=tr, dev_dot_dev=dev2)
+
+
 def material_key(p) -> tuple:
     """Hashable identity of a params object (ours or the reference's, duck-typed)."""
     return (float(p.mu), float(p.lam), float(p.bulk_k), float(p.g_c), float(p.length_l),

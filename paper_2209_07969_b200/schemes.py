@@ -121,8 +121,15 @@ def staggered_step(disc, state, scheme, bc_increments, params, config,
     sess.push(u=state.u, d=state.d, d_prev=state.d_prev, psi_max=gp.psi_max)
     try:
         st = sess.step(scheme, bc_increments, pinned_d_nodes)
-    finally:
-        _write_back(sess, state)
+    except BaseException:
+        # the reference leaves the state wherever the failed step stopped: mirror it, but never
+        # let a failing download (e.g. after a CUDA fault) replace the solver's own exception
+        try:
+            _write_back(sess, state)
+        except Exception:  # noqa: BLE001
+            pass
+        raise
+    _write_back(sess, state)
     return StaggeredStats(
         n_stag=st.n_stag, n_nr_u=st.n_nr_u, n_nr_d=st.n_nr_d,
         residual_history=list(sess.last_history), final_rd_ratio=st.final_rd_ratio,

@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
+import sys
 
 import numpy as np
 
@@ -36,6 +37,28 @@ class SingularSystemError(RuntimeError):
 
 class DeviceError(RuntimeError):
     """CUDA / NCCL failure inside the native library."""
+
+
+_REF_ERRORS = {ConvergenceError: ("phasefrac.schemes", "ConvergenceError"),
+               SingularSystemError: ("phasefrac.linsolve", "SingularSystemError")}
+_COMBINED: dict = {}
+
+
+def reference_error(cls):
+    """The class to raise for one of the reference's exceptions: when the caller has imported
+    the reference package (``phasefrac``, e.g. a reference runner switched to the drop-in), a
+    subclass of both this package's class and the reference's own (``schemes.py:90-93``,
+    ``linsolve.py:18-21``), so ``except phasefrac.schemes.ConvergenceError`` handlers keep
+    working; otherwise the local class."""
+    modname, name = _REF_ERRORS[cls]
+    ref = getattr(sys.modules.get(modname), name, None)
+    if not isinstance(ref, type) or issubclass(cls, ref):
+        return cls
+    combo = _COMBINED.get((cls, ref))
+    if combo is None:
+        combo = type(cls.__name__, (cls, ref), {"__module__": cls.__module__})
+        _COMBINED[(cls, ref)] = combo
+    return combo
 
 
 def scheme_code(scheme) -> int:
@@ -132,9 +155,9 @@ class DeviceSession:
             return
         msg = self.lib.pf_last_error(self.h).decode(errors="replace")
         if st in (N.PF_ERR_CONV_MOMENTUM, N.PF_ERR_CONV_EVOLUTION, N.PF_ERR_CONV_STAGGERED):
-            raise ConvergenceError(msg, history)
+            raise reference_error(ConvergenceError)(msg, history)
         if st == N.PF_ERR_SINGULAR:
-            raise SingularSystemError(msg)
+            raise reference_error(SingularSystemError)(msg)
         if st == N.PF_ERR_INVALID:
             raise ValueError(msg)
         if st == N.PF_ERR_INDEX:
@@ -203,6 +226,15 @@ class DeviceSession:
         strain, tr = emp((ne, 4, 4)), emp((ne, 4))
         self._check(self.lib.pf_get_gp_strain(self.h, N.f64(strain), N.f64(tr)))
         return strain, tr
+
+    def interp_nodal(self, field) -> np.ndarray:
+        """A nodal scalar field at the Gauss points, (n_elems, 4) (pf_interp_nodal)."""
+        f = np.ascontiguousarray(field, dtype=np.float64)
+        if f.size != self.n_nodes:
+            raise ValueError(f"nodal field has {f.size} entries, expected {self.n_nodes}")
+        out = np.empty((self.n_elems, 4))
+        self._check(self.lib.pf_interp_nodal(self.h, N.f64(f), N.f64(out)))
+        return out
 
     # -- hot path ------------------------------------------------------------------------
     def step(self, scheme, bc_increments, pinned_d_nodes=None) -> N.PfStats:

@@ -135,14 +135,63 @@ def _state_arrays(state) -> dict:
                 psi_plus=gp.psi_plus.copy(), psi_max=gp.psi_max.copy())
 
 
+def restart_state_arrays(state) -> dict:
+    """The part of a SolverState that determines the next load step: u, d, d_prev and
+    gp.psi_max.  The other GP arrays are overwritten from u by the k = 0 momentum pass
+    (``schemes.py:237`` -> ``assembly.py:260-269``) before anything reads them."""
+    return dict(u=state.u.copy(), d=state.d.copy(), d_prev=state.d_prev.copy(),
+                psi_max=state.gp.psi_max.copy())
+
+
+def load_restart(state, path: str) -> int:
+    """Overwrite ``state`` with a restart file; returns the load step it was taken after."""
+    z = np.load(path)
+    state.u[:] = z["u"]
+    state.d[:] = z["d"]
+    state.d_prev = z["d_prev"].copy()
+    state.gp.psi_max = z["psi_max"].copy()
+    return int(z["after_step"])
+
+
 def run(case_name: str, scheme: str, steps: int | None, snaps: list[int],
-        lin_method: str | None) -> None:
+        lin_method: str | None, partial: bool = False, state_snaps: tuple = (),
+        restart: str | None = None, tag_extra: str = "") -> None:
+    """Run the reference on a case.  ``partial``: rewrite the output after every load step
+    (long full-size runs, meta["complete"] tells whether the run finished).  ``state_snaps``:
+    also store the restart state after those steps (``restart_step<k>.npz``).  ``restart``:
+    start from such a restart file (the reference crack step from a given state)."""
     api = C.reference_api(REF_SRC)
     case = C.get_case(case_name)
     pb = C.setup(case, api, lin_method=lin_method)
-    n = case.n_steps if steps is None else steps
+    first = 1
+    if restart:
+        first = load_restart(pb.state, restart) + 1
+    n = case.n_steps - first + 1 if steps is None else steps
     rows, snap = [], {}
     t_loop = 0.0
+    suffix = "" if lin_method in (None, "direct") else f"_{lin_method}"
+    tag = (f"{case_name}_{scheme}{suffix}{tag_extra}"
+           + ("" if steps is None or partial else f"_{n}steps"))
+    path = os.path.join(HERE, f"run_{tag}.npz")
+
+    def meta(complete):
+        return dict(case=case_name, scheme=scheme, steps=len(rows), first_step=first,
+                    complete=complete, restart=os.path.basename(restart) if restart else None,
+                    lin_method=lin_method or "direct",
+                    loop_wall_s=t_loop, n_nodes=int(pb.mesh.n_nodes),
+                    n_elems=int(pb.mesh.n_elems),
+                    columns=["step", "n_stag", "n_nr_u", "n_nr_d", "spd_fallbacks",
+                             "final_rd_ratio", "wall"] + [r[0] for r in pb.reactions],
+                    generator="tests/golden/make_golden.py (unmodified reference, "
+                              "/root/reference/pkg/src/phasefrac)")
+
+    def write(complete):
+        final = _state_arrays(pb.state) if pb.mesh.n_nodes <= 20000 else {
+            "d": pb.state.d.copy(), "u": pb.state.u.copy()}
+        tmp = path + ".tmp.npz"
+        np.savez_compressed(tmp, table=np.array(rows), meta=json.dumps(meta(complete)),
+                            **{f"final_{k}": v for k, v in final.items()}, **snap)
+        os.replace(tmp, path)
 
     def cb(rec, problem):
         nonlocal t_loop
@@ -153,21 +202,15 @@ def run(case_name: str, scheme: str, steps: int | None, snaps: list[int],
         if rec.step in snaps:
             snap[f"d_step{rec.step}"] = problem.state.d.copy()
             snap[f"u_step{rec.step}"] = problem.state.u.copy()
+        if rec.step in state_snaps:
+            rp = os.path.join(HERE, f"restart_{case_name}_{scheme}_step{rec.step}.npz")
+            np.savez_compressed(rp, after_step=rec.step, **restart_state_arrays(problem.state))
+            print("wrote", rp, flush=True)
+        if partial:
+            write(False)
 
-    C.run(pb, scheme, n_steps=n, on_step=cb)
-    meta = dict(case=case_name, scheme=scheme, steps=n, lin_method=lin_method or "direct",
-                loop_wall_s=t_loop, n_nodes=int(pb.mesh.n_nodes), n_elems=int(pb.mesh.n_elems),
-                columns=["step", "n_stag", "n_nr_u", "n_nr_d", "spd_fallbacks",
-                         "final_rd_ratio", "wall"] + [r[0] for r in pb.reactions],
-                generator="tests/golden/make_golden.py (unmodified reference, "
-                          "/root/reference/pkg/src/phasefrac)")
-    suffix = "" if lin_method in (None, "direct") else f"_{lin_method}"
-    tag = f"{case_name}_{scheme}{suffix}" + ("" if steps is None else f"_{n}steps")
-    final = _state_arrays(pb.state) if pb.mesh.n_nodes <= 20000 else {
-        "d": pb.state.d.copy(), "u": pb.state.u.copy()}
-    path = os.path.join(HERE, f"run_{tag}.npz")
-    np.savez_compressed(path, table=np.array(rows), meta=json.dumps(meta),
-                        **{f"final_{k}": v for k, v in final.items()}, **snap)
+    C.run(pb, scheme, n_steps=n, on_step=cb, first_step=first)
+    write(True)
     print("wrote", path, "loop", round(t_loop, 1), "s", flush=True)
 
 
@@ -222,6 +265,10 @@ def main() -> None:
     r.add_argument("--steps", type=int, default=None)
     r.add_argument("--snap", default="")
     r.add_argument("--lin", default=None)
+    r.add_argument("--partial", action="store_true")
+    r.add_argument("--state-snap", default="")
+    r.add_argument("--restart", default=None)
+    r.add_argument("--tag", default="")
     s = sub.add_parser("spd")
     s.add_argument("case")
     s.add_argument("scheme")
@@ -232,7 +279,8 @@ def main() -> None:
         kat(a.only)
     elif a.cmd == "run":
         snaps = [int(x) for x in a.snap.split(",") if x]
-        run(a.case, a.scheme, a.steps, snaps, a.lin)
+        run(a.case, a.scheme, a.steps, snaps, a.lin, a.partial,
+            tuple(int(x) for x in a.state_snap.split(",") if x), a.restart, a.tag)
     else:
         spd(a.case, a.scheme, a.max_each)
     print("elapsed", round(time.time() - t0, 1), "s")

@@ -16,6 +16,7 @@ solver direct (SuperLU) or the reference's own lin_method="cg".  The crack side 
 symmetric tension test ("branch") is recorded too.
 
     OMP_NUM_THREADS=1 python tests/golden/make_sensitivity.py tension16 ST [steps|-] [max_variants|-] [a:b]
+    OMP_NUM_THREADS=1 python tests/golden/make_sensitivity.py cfg1 ST - - exact:0:4   (exact-geometry half)
 """
 
 from __future__ import annotations
@@ -86,10 +87,16 @@ def main() -> None:
     variants = factorial(maxv)
     suffix = ""
     if len(sys.argv) > 5:  # "a:b" slice of the full factorial, written to its own part file
-        a, b = (int(x) for x in sys.argv[5].split(":"))
-        names = list(factorial())[a:b]
-        variants = {n: factorial()[n] for n in names}
-        suffix = f"_part{a}_{b}"
+        spec = sys.argv[5]
+        full = factorial()
+        if spec.startswith("exact:"):  # the exact-geometry half (uniform-cell constants, as
+            spec = spec[len("exact:"):]  # the device path evaluates them)
+            full = {n: kw for n, kw in full.items() if kw.get("geometry") == "exact"}
+            suffix = "_exact"
+        a, b = (int(x) for x in spec.split(":"))
+        names = list(full)[a:b]
+        variants = {n: full[n] for n in names}
+        suffix += f"_part{a}_{b}"
     t0 = time.time()
     stag, branch = {}, {}
     for name, kw in variants.items():
