@@ -203,10 +203,18 @@ pf_status pf_create_strip(const pf_mesh* local_mesh, const pf_material* mat, con
 /* n_iter PCG iterations of the momentum (physics 0) or phase-field (1) operator at the current
  * state with the stopping test disabled (rtol 0): per-iteration cost at any mesh size without
  * solving to convergence; physics 2 = the multigrid-preconditioned momentum PCG (including its
- * per-solve hierarchy setup).  ms_out = CUDA-event time of the PCG launch. */
+ * per-solve hierarchy setup), 3 = the scalar phase-field multigrid PCG (pf_mgs.cuh, including
+ * its hierarchy setup).  ms_out = CUDA-event time of the PCG launch. */
 pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, double* ms_out,
                       int64_t* iters_out);
 pf_status pf_device_info(pf_handle* h, int32_t* cg_grid, int32_t* sm_count, int64_t* l2_bytes);
+/* Benchmark helper (not on the solve path): average device time of one fine-level multigrid
+ * march, re-launched `reps` times on the current hierarchy / state with CUDA events (kernels of
+ * the conditional solve graph cannot be event-timed individually).  which: 0 / 1 / 2 momentum
+ * fine residual, smoothing, PCG-direction march; 10 / 11 / 12 the same for the scalar
+ * phase-field hierarchy.  bytes_out: algorithmic bytes per launch. */
+pf_status pf_bench_mg_kernel(pf_handle* h, int which, int reps, double* ms_out,
+                             double* bytes_out);
 /* Multigrid hierarchy of the momentum PCG (replaces the Jacobi preconditioner M = D^-1 of
  * linsolve.py:49 by a Galerkin V-cycle; same system, same stopping test): level count, first
  * level of the single-CTA tail kernel (n_levels: none), dense coarsest solve, hierarchy builds
@@ -219,7 +227,8 @@ pf_status pf_mg_info(pf_handle* h, int32_t* n_levels, int32_t* n_grid, int32_t* 
  * linsolve.py:48-54 to the same stopping test).  momentum: 0 two-barrier Jacobi PCG (k_cg),
  * 1 single-reduction Jacobi PCG (k_cg_sr), 2 multigrid PCG.  phase_field (solves without the
  * SPD probe; probe solves always run k_cg): 0 k_cg, 1 k_cg_sr (matrix-free march), 2 k_cg_st
- * (assembled stencil, L2-resident meshes), 3 multigrid PCG. */
+ * (assembled stencil, L2-resident meshes), 3 multigrid PCG on the two-component packing
+ * (PFB200_MG_EVO=packed), 4 native scalar multigrid PCG (pf_mgs.cuh). */
 pf_status pf_solver_kinds(pf_handle* h, int32_t* momentum, int32_t* phase_field);
 pf_status pf_flush_l2(pf_handle* h);
 pf_status pf_synchronize(pf_handle* h);

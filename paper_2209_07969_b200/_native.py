@@ -111,6 +111,7 @@ _SIGNATURES = {
     "pf_host_group_destroy": (None, [C.c_void_p]),
     "pf_create_strip": (C.c_int, [C.POINTER(PfMesh), C.POINTER(PfMaterial), C.POINTER(PfConfig),
                                   C.c_int, C.POINTER(PfStrip), C.POINTER(C.c_void_p)]),
+    "pf_bench_mg_kernel": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _f64p, _f64p]),
     "pf_bench_cg": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, _f64p, _i64p]),
     "pf_device_info": (C.c_int, [C.c_void_p, _i32p, _i32p, _i64p]),
     "pf_host_alloc": (C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),

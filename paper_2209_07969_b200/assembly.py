@@ -72,6 +72,18 @@ class Discretization:
         self.n_u_dofs = 2 * mesh.n_nodes
         self.n_d_dofs = mesh.n_nodes
 
+    @classmethod
+    def from_layout(cls, layout: StructuredLayout) -> "Discretization":
+        """A discretisation of a row-compact layout without host node / element arrays
+        (``mesh`` is None): config 5's 67 M cells are described by a few row tables."""
+        self = cls.__new__(cls)
+        self.mesh = None
+        self.n_gp = 4
+        self.layout = layout
+        self.n_u_dofs = 2 * layout.n_nodes
+        self.n_d_dofs = layout.n_nodes
+        return self
+
     # field evaluation at Gauss points (assembly.py:148-158), on the device
     def interp_nodal(self, field) -> np.ndarray:
         """Nodal scalar field interpolated at every Gauss point, (n_elems, 4)."""

@@ -272,6 +272,77 @@ def precrack_nodes(case: LoadCase, mesh) -> np.ndarray:
     return np.flatnonzero(hit)
 
 
+def precrack_nodes_grid(case: LoadCase) -> np.ndarray:
+    """precrack_nodes for the plain square of a case (build_notched_square(..., notch=False))
+    from its grid coordinates (np.linspace, like the mesh builder) without materialising the node
+    array (config 5: 67 M nodes); node (i, j) has id j (nx + 1) + i."""
+    if case.precracks is None:
+        return np.zeros(0, dtype=np.int64)
+    _, nx, ny, side, notch = case.mesh
+    if notch:
+        raise ValueError("precrack_nodes_grid: plain squares only")
+    xs = np.linspace(0.0, side, nx + 1)
+    ys = np.linspace(0.0, side, ny + 1)
+    segs, _ = precrack_segments(case)
+    h = side / nx
+    hit = []
+    for ax, ay, bx, by in segs:
+        i0 = max(int(np.floor((min(ax, bx) - h) / h)), 0)
+        i1 = min(int(np.ceil((max(ax, bx) + h) / h)), nx)
+        j0 = max(int(np.floor((min(ay, by) - h) / h)), 0)
+        j1 = min(int(np.ceil((max(ay, by) + h) / h)), ny)
+        jj, ii = np.meshgrid(np.arange(j0, j1 + 1), np.arange(i0, i1 + 1), indexing="ij")
+        px, py = xs[ii.ravel()], ys[jj.ravel()]
+        ex, ey = bx - ax, by - ay
+        t = np.clip(((px - ax) * ex + (py - ay) * ey) / (ex * ex + ey * ey), 0.0, 1.0)
+        dist = np.hypot(px - (ax + t * ex), py - (ay + t * ey))
+        ids = jj.ravel() * (nx + 1) + ii.ravel()
+        hit.append(ids[dist <= 0.5 * h])
+    return np.unique(np.concatenate(hit)) if hit else np.zeros(0, dtype=np.int64)
+
+
+@dataclass
+class DeviceProblem:
+    """A case for device-resident stepping without the reference's host mesh arrays: the
+    row-compact layout, boundary-condition / pin / reaction node sets, and (plain squares) the
+    pre-crack segments for pf_init_state.  For the plain squares (config 5: 67 M cells) nothing
+    of size n_elems is built on the host."""
+
+    case: LoadCase
+    layout: object
+    params: object
+    config: object
+    bcs: list
+    pins: object
+    reactions: list
+    boundary_sets: dict
+    mesh: object = None   # the host mesh (non-plain cases only)
+
+
+def device_problem(case: LoadCase, api=None) -> DeviceProblem:
+    from types import SimpleNamespace  # noqa: PLC0415
+
+    from .meshing import StructuredLayout  # noqa: PLC0415
+
+    api = api or b200_api()
+    params = material(case, api)
+    config = api.SolverConfig(tol_st=case.tol_st)
+    mesh = None
+    if case.mesh[0] == "notched" and not case.mesh[4]:
+        _, nx, ny, side, _ = case.mesh
+        lay = StructuredLayout.rectangle(nx, ny, side / nx, side / ny)
+        rows = np.arange(ny + 1, dtype=np.int64) * (nx + 1)
+        cols = np.arange(nx + 1, dtype=np.int64)
+        bsets = {"bottom": cols, "top": ny * (nx + 1) + cols, "left": rows, "right": rows + nx}
+    else:
+        mesh = build_mesh(case, api)
+        lay = StructuredLayout.from_mesh(mesh)
+        bsets = mesh.boundary_sets
+    view = SimpleNamespace(boundary_sets=bsets)
+    return DeviceProblem(case, lay, params, config, boundary_conditions(case, view),
+                         pinned_nodes(case, view), reaction_sets(case, view), bsets, mesh)
+
+
 @dataclass
 class Problem:
     case: LoadCase

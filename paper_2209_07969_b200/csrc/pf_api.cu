@@ -48,6 +48,21 @@ struct MgInst {
   bool fuse = true;  // fused down / up kernels on the half-warp levels (PFB200_MG_FUSE=0: off)
 };
 
+// The native scalar phase-field multigrid PCG (pf_mgs.cuh): hierarchy rebuilt at every solve
+// (the phase-field tangent changes strongly between Newton iterations), solved by a graph whose
+// PCG loop is a device-side WHILE node.
+struct MgsInst {
+  bool on = false;
+  pfb::MgsArgs A{};
+  int gf = 1, gflat = 1;
+  std::vector<int> gl, gn, lpn;
+  pfb::MgIn* in = nullptr;
+  cudaGraphExec_t setup_exec = nullptr, solve_exec = nullptr;
+  long long setups = 0;
+  int setup_kernels = 0, body_kernels = 0;
+  bool fuse = true;
+};
+
 struct pf_handle {
   double hx = 0.0, hy = 0.0;  // uniform cell size (node (i, j) at (i hx, j hy))
   int device = 0;
@@ -142,6 +157,7 @@ struct pf_handle {
   long long l2_bytes = 0;
   // geometric-multigrid PCG instances (momentum; phase field on large meshes)
   MgInst mgu, mgd;
+  MgsInst mgs;  // scalar phase-field multigrid (default for the phase field on large meshes)
   std::vector<void*> mg_allocs;
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
@@ -282,6 +298,9 @@ extern "C" void pf_destroy(pf_handle* h) {
     if (M->setup_exec) cudaGraphExecDestroy(M->setup_exec);
     if (M->solve_exec) cudaGraphExecDestroy(M->solve_exec);
   }
+  if (h->mgs.in) cudaFreeHost(h->mgs.in);
+  if (h->mgs.setup_exec) cudaGraphExecDestroy(h->mgs.setup_exec);
+  if (h->mgs.solve_exec) cudaGraphExecDestroy(h->mgs.solve_exec);
   if (h->stage) cudaFreeHost(h->stage);
   for (auto& row : h->graphs)
     for (auto& g : row)
@@ -902,6 +921,302 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
   return PF_OK;
 }
 
+// ------------------------------------------------------------------------------------------
+// native scalar phase-field multigrid (pf_mgs.cuh)
+static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M);
+
+static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
+  const char* fz = getenv("PFB200_MG_FUSE");
+  M.fuse = !(fz && std::string(fz) == "0");
+  const char* nc = getenv("PFB200_MG_NUC");
+  const int nu_c = nc ? std::max(1, atoi(nc)) : 16;
+  std::vector<HostLevel> lv(1, hl_fine(h));
+  while ((int)lv.size() < pfb::MG_MAXL && lv.back().n_nodes > pfb::MGS_DENSE_MAX) {
+    HostLevel c;
+    if (!mg_coarsen(lv.back(), c)) break;
+    lv.push_back(std::move(c));
+  }
+  const int nl = (int)lv.size();
+  if (nl < 2) return PF_OK;
+  pfb::MgsArgs& A = M.A;
+  A = pfb::MgsArgs{};
+  A.C = h->C;
+  A.n_levels = nl;
+  A.dense = lv.back().n_nodes <= pfb::MGS_DENSE_MAX;
+  A.nu_c = nu_c;
+  // tail: the coarsest levels whose assembled FP64 form fits the single-CTA kernel's shared
+  // memory (PFB200_MG_TAIL_KB, default 220)
+  const char* tk = getenv("PFB200_MG_TAIL_KB");
+  const size_t budget = (size_t)(tk ? std::max(0, atoi(tk)) : 220) * 1024;
+  auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
+  auto level_bytes = [&](const HostLevel& L) -> size_t {
+    const size_t n = L.n_nodes;
+    return al(4 * pfb::MG_NS * n) + al(4 * 12 * n) + al(4 * 4 * n) + al(8 * pfb::MG_NS * n) +
+           4 * al(8 * n);
+  };
+  const size_t nc_nodes = lv.back().n_nodes;
+  const size_t ainv_bytes = A.dense ? 8 * nc_nodes * nc_nodes : 0;
+  int nt = nl;
+  size_t used = ainv_bytes;
+  while (nt > 1 && lv[nt - 1].n_nodes <= pfb::MGS_TAIL_P * pfb::MG_TAIL_NT / 4 &&
+         used + level_bytes(lv[nt - 1]) <= budget) {
+    used += level_bytes(lv[nt - 1]);
+    --nt;
+  }
+  A.n_tail = nt;
+  {
+    size_t off = 0;
+    auto take = [&](size_t bytes) { const size_t o = off; off += al(bytes); return (int)o; };
+    for (int l = nt; l < nl; ++l) {
+      const size_t n = lv[l].n_nodes;
+      pfb::MgTailSlot& t = A.ts[l];
+      t.nbr = take(4 * pfb::MG_NS * n);
+      t.rid = take(4 * 12 * n);
+      t.pid = take(4 * 4 * n);
+      t.S = take(8 * pfb::MG_NS * n);
+      t.dinv = take(8 * n);
+      t.b = take(8 * n);
+      t.t = take(8 * n);
+      t.e = take(8 * n);
+    }
+    A.ts_ainv = take(ainv_bytes);
+    A.ts_bytes = (int)off;
+    if (nt < nl && cudaFuncSetAttribute(pfb::k_mgs_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        A.ts_bytes) != cudaSuccess)
+      return fail(h, PF_ERR_CUDA, "k_mgs_tail shared memory");
+  }
+  auto oom = [&]() { return fail(h, PF_ERR_CUDA, "phase-field multigrid allocation failed"); };
+  M.gl.assign(nl, 1);
+  M.gn.assign(nl, 1);
+  M.lpn.assign(nl, 16);
+  int coarse_items = 0;
+  const long long wave = (long long)(2048.0 * h->sm_count * 0.25);
+  for (int l = 0; l < nl; ++l) {
+    const HostLevel& L = lv[l];
+    pfb::MgsLevel& ML = A.L[l];
+    pfb::DMesh& dm = ML.m;
+    if (l == 0) {
+      dm = h->dm;
+      ML.dinv = h->dinvd;
+      if (mg_alloc(h, &ML.t, (size_t)L.n_nodes) != cudaSuccess) return oom();
+      continue;
+    }
+    std::vector<int4> nrow(L.ny + 1), erow(L.ny);
+    for (int j = 0; j <= L.ny; ++j) nrow[j] = make_int4(L.nlo[j], L.nhi[j], L.nst[j], 0);
+    for (int j = 0; j < L.ny; ++j) erow[j] = make_int4(L.elo[j], L.ehi[j], L.est[j], 0);
+    int4 *dn = nullptr, *de = nullptr;
+    if (mg_alloc(h, &dn, nrow.size()) != cudaSuccess || mg_alloc(h, &de, erow.size()) != cudaSuccess)
+      return oom();
+    PF_CUDA(cudaMemcpy(dn, nrow.data(), nrow.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    PF_CUDA(cudaMemcpy(de, erow.data(), erow.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    dm = pfb::DMesh{};
+    dm.nx = L.nx; dm.ny = L.ny;
+    dm.nrow = dn; dm.erow = de;
+    dm.notch_row = L.notch_row; dm.notch_lo = L.notch_lo; dm.notch_hi = L.notch_hi;
+    dm.dup_start = L.dup_start;
+    dm.n_nodes = L.n_nodes; dm.n_elems = L.n_elems;
+    dm.own_lo = 0; dm.own_hi = L.n_nodes; dm.dup_lo = L.n_nodes;
+    dm.cell_lo = 0; dm.cell_hi = L.n_elems;
+    const size_t n = L.n_nodes;
+    if (mg_alloc(h, &ML.K, 16 * (size_t)L.n_elems) != cudaSuccess ||
+        mg_alloc(h, &ML.dinv, n) != cudaSuccess || mg_alloc(h, &ML.b, n) != cudaSuccess ||
+        mg_alloc(h, &ML.e, n) != cudaSuccess || mg_alloc(h, &ML.t, n) != cudaSuccess)
+      return oom();
+    ML.items = pfb::mg_items(L.nx, L.ny, L.notch_row >= 0);
+    M.gl[l] = (ML.items + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+    M.lpn[l] = 16LL * L.n_nodes <= wave ? 16 : (4LL * L.n_nodes <= wave ? 4 : 1);
+    ML.lpn = M.lpn[l];
+    ML.in_tail = l >= nt ? 1 : 0;
+    if (l < nt) {
+      ML.item_off = coarse_items;
+      coarse_items += (int)(((long long)M.lpn[l] * L.n_nodes + 31) / 32 * 32);
+    }
+    M.gn[l] = std::max(1, std::min((int)((M.lpn[l] * (long long)L.n_nodes + pfb::MG_NT - 1) / pfb::MG_NT),
+                                   16 * h->sm_count));
+    const std::vector<int> nb = hl_stencil_ids(L), rd = hl_restrict_ids(lv[l - 1], L);
+    int *dnb = nullptr, *drd = nullptr;
+    if (mg_alloc(h, &dnb, nb.size()) != cudaSuccess || mg_alloc(h, &drd, rd.size()) != cudaSuccess)
+      return oom();
+    if (l >= nt ? mg_alloc(h, &ML.S, (size_t)pfb::MG_NS * n) != cudaSuccess
+                : mg_alloc(h, &ML.Sf, (size_t)pfb::MG_NS * n) != cudaSuccess)
+      return oom();
+    PF_CUDA(cudaMemcpy(dnb, nb.data(), nb.size() * sizeof(int), cudaMemcpyHostToDevice));
+    PF_CUDA(cudaMemcpy(drd, rd.data(), rd.size() * sizeof(int), cudaMemcpyHostToDevice));
+    ML.nbr = dnb;
+    ML.rid = drd;
+    if (l + 1 < nl) {
+      const std::vector<int> pd = hl_prolong_ids(L, lv[l + 1]);
+      int* dpd = nullptr;
+      if (mg_alloc(h, &dpd, pd.size()) != cudaSuccess) return oom();
+      PF_CUDA(cudaMemcpy(dpd, pd.data(), pd.size() * sizeof(int), cudaMemcpyHostToDevice));
+      ML.pid = dpd;
+    }
+  }
+  A.coarse_items = coarse_items;
+  A.g0 = pfb::make_march_geom(h->nx, h->ny, fine_resident_warps);
+  M.gf = (A.g0.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+  M.gflat = 2 * h->sm_count;
+  const size_t nn = h->n_nodes;
+  if (mg_alloc(h, &A.z, nn) != cudaSuccess) return oom();
+  A.L[0].e = A.z;
+  if (A.dense && mg_alloc(h, &A.Ainv, nc_nodes * nc_nodes) != cudaSuccess) return oom();
+  const size_t npart = std::max<size_t>((size_t)2 * M.gf + M.gflat, (size_t)M.gflat * 2 * pfb::MG_MAXL);
+  if (mg_alloc(h, &A.part, npart) != cudaSuccess || mg_alloc(h, &A.ctl, 1) != cudaSuccess)
+    return oom();
+  if (cudaHostAlloc((void**)&M.in, sizeof(pfb::MgIn), cudaHostAllocDefault) != cudaSuccess)
+    return oom();
+  *M.in = pfb::MgIn{};
+  pfb::MgIn* din = nullptr;
+  if (mg_alloc(h, &din, 1) != cudaSuccess) return oom();
+  A.in = din;
+  A.bq = h->b;
+  // the phase-field Newton system in place: right-hand side rd (consumed), solution xd; the
+  // Jacobi PCG's direction buffers serve as p and q
+  A.r = h->rd;
+  A.x = h->xd;
+  A.p0 = h->p0d;
+  A.p1 = h->p1d;
+  A.q = h->qd;
+  A.result = h->d_cgres;
+  A.n = (long long)nn;
+  PF_TRY(mgs_build_graphs(h, M));
+  M.on = true;
+  return PF_OK;
+}
+
+static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
+  pfb::MgsArgs& A = M.A;
+  const int nl = A.n_levels;
+  cudaStream_t s = h->stream;
+  {  // setup: Galerkin levels, stencils, dense coarsest inverse, power steps, omegas
+    cudaGraph_t g = nullptr;
+    PF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int lc = 1; lc < nl; ++lc) {
+      const long long cells = (long long)A.L[lc].m.nx * A.L[lc].m.ny;
+      const int gb = (int)std::max(1LL, std::min((cells + pfb::MG_NT - 1) / pfb::MG_NT,
+                                                 64LL * h->sm_count));
+      pfb::k_mgs_galerkin<<<gb, pfb::MG_NT, 0, s>>>(A, lc);
+      pfb::k_mgs_stencil<<<M.gl[lc], pfb::MG_NT, 0, s>>>(A, lc);
+    }
+    if (A.dense) pfb::k_mgs_dense<<<1, pfb::MG_NT, 0, s>>>(A);
+    const int cb = (A.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
+    for (int k = 1; k <= pfb::MG_POW; ++k)
+      pfb::k_mgs_pow<<<M.gf + cb, pfb::MG_NT, 0, s>>>(A, k, M.gf);
+    if (A.n_tail < nl) pfb::k_mgs_pow_tail<<<1, pfb::MG_TAIL_NT, 0, s>>>(A);
+    pfb::k_mgs_lambda<<<M.gflat, pfb::MG_NT, 0, s>>>(A);
+    M.setup_kernels = 2 * (nl - 1) + (A.dense ? 1 : 0) + pfb::MG_POW + (A.n_tail < nl ? 1 : 0) + 1;
+    cudaError_t e = cudaStreamEndCapture(s, &g);
+    if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MGS setup capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&M.setup_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MGS setup graph: ") + cudaGetErrorString(e));
+  }
+#define MGS_NODE_KERNEL(K, l, ...)                                                  \
+  do {                                                                              \
+    if (M.lpn[l] == 16) pfb::K<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__); \
+    else if (M.lpn[l] == 4) pfb::K<4><<<M.gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__); \
+    else pfb::K<1><<<M.gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__);                     \
+  } while (0)
+  const int c = nl - 1, top = std::min(A.n_tail, c);
+  auto body_kernels = [&](const pfb::MgsArgs& B) {
+    pfb::k_mgs_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(B);
+    for (int l = 1; l < top; ++l) {
+      if (M.lpn[l] == 16 && M.fuse && B.L[l].m.n_nodes <= 8192) {
+        pfb::k_mgs_sdown<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
+      } else {
+        MGS_NODE_KERNEL(k_mgs_srestrict, l, B, l);
+        MGS_NODE_KERNEL(k_mgs_sresid, l, B, l);
+      }
+    }
+    if (B.n_tail < nl) {
+      pfb::k_mgs_tail<<<1, pfb::MG_TAIL_NT, B.ts_bytes, s>>>(B);
+    } else {
+      MGS_NODE_KERNEL(k_mgs_srestrict, c, B, c);
+      if (B.dense) {
+        pfb::k_mgs_coarse_dense<<<1, pfb::MG_NT, 0, s>>>(B);
+      } else {
+        double* bufs[2] = {B.L[c].e, B.L[c].t};
+        int cur = (B.nu_c - 1) % 2 == 0 ? 0 : 1;
+        pfb::k_mgs_jacobi0<<<M.gn[c], pfb::MG_NT, 0, s>>>(B, c, bufs[cur]);
+        for (int k = 1; k < B.nu_c; ++k, cur ^= 1)
+          MGS_NODE_KERNEL(k_mgs_ssweep, c, B, c, bufs[cur], bufs[cur ^ 1]);
+      }
+    }
+    for (int l = top - 1; l >= 1; --l) {
+      if (M.lpn[l] == 16 && M.fuse) {
+        pfb::k_mgs_sup<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
+      } else {
+        MGS_NODE_KERNEL(k_mgs_sprolongate, l, B, l);
+        MGS_NODE_KERNEL(k_mgs_ssmooth, l, B, l);
+      }
+    }
+    pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(B);
+    pfb::k_mgs_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(B, M.gf);
+    pfb::k_mgs_update<<<M.gflat, pfb::MG_NT, 0, s>>>(B, M.gf, M.gf);
+  };
+  M.body_kernels = 4 + (A.n_tail < nl ? 1 : 1 + (A.dense ? 1 : A.nu_c));
+  for (int l = 1; l < top; ++l)
+    M.body_kernels += (M.lpn[l] == 16 && M.fuse) ? (A.L[l].m.n_nodes <= 8192 ? 2 : 3) : 4;
+  const char* un = getenv("PFB200_MG_UNROLL");
+  const int unroll = un ? std::max(0, atoi(un)) : 0;
+  if (unroll > 0) {  // profiling only: N unconditional iterations, so ncu sees every kernel
+    cudaGraph_t g = nullptr;
+    A.use_cond = 0;
+    PF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    pfb::k_mgs_init<<<M.gflat, pfb::MG_NT, 0, s>>>(A);
+    for (int it = 0; it < unroll; ++it) body_kernels(A);
+    pfb::k_mgs_finish<<<M.gflat, pfb::MG_NT, 0, s>>>(A);
+    PF_CUDA(cudaStreamEndCapture(s, &g));
+    cudaError_t e = cudaGraphInstantiate(&M.solve_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MGS solve graph: ") + cudaGetErrorString(e));
+    return PF_OK;
+  }
+  cudaGraph_t g = nullptr;
+  PF_CUDA(cudaGraphCreate(&g, 0));
+  PF_CUDA(cudaGraphConditionalHandleCreate(&A.cond, g, 1, cudaGraphCondAssignDefault));
+  A.use_cond = 1;
+  cudaGraphNode_t n_init = nullptr, n_while = nullptr, n_fin = nullptr;
+  {
+    cudaGraphNodeParams kp = {};
+    kp.type = cudaGraphNodeTypeKernel;
+    void* args[] = {&A};
+    kp.kernel.func = (void*)pfb::k_mgs_init;
+    kp.kernel.gridDim = dim3(M.gflat);
+    kp.kernel.blockDim = dim3(pfb::MG_NT);
+    kp.kernel.kernelParams = args;
+    PF_CUDA(cudaGraphAddNode(&n_init, g, nullptr, 0, &kp));
+  }
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = A.cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  PF_CUDA(cudaGraphAddNode(&n_while, g, &n_init, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  {
+    PF_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    body_kernels(A);
+    cudaGraph_t bb = body;
+    PF_CUDA(cudaStreamEndCapture(s, &bb));
+  }
+  {
+    cudaGraphNodeParams kp = {};
+    kp.type = cudaGraphNodeTypeKernel;
+    void* args[] = {&A};
+    kp.kernel.func = (void*)pfb::k_mgs_finish;
+    kp.kernel.gridDim = dim3(M.gflat);
+    kp.kernel.blockDim = dim3(pfb::MG_NT);
+    kp.kernel.kernelParams = args;
+    PF_CUDA(cudaGraphAddNode(&n_fin, g, &n_while, 1, &kp));
+  }
+  cudaError_t e = cudaGraphInstantiate(&M.solve_exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MGS solve graph: ") + cudaGetErrorString(e));
+  return PF_OK;
+#undef MGS_NODE_KERNEL
+}
+
 static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const pf_config* cfg,
                              int device, const pf_strip* strip, pf_handle** out) {
   if (!out || !mesh || !mat || !cfg) return PF_ERR_INVALID;
@@ -1219,11 +1534,22 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
         if (ms != PF_OK) return bail(ms);
         // phase-field multigrid (solves without the SPD probe) where Jacobi PCG iteration
         // counts get large: deep hierarchies on big meshes (PFB200_MG_EVO=1/0: force on/off)
+        // PFB200_MG_EVO: "1" / "scalar" the native scalar hierarchy (pf_mgs.cuh), "packed" the
+        // round-1 two-component packing (pf_mg.cuh phys 1, A/B comparisons), "0" off
         const char* me = getenv("PFB200_MG_EVO");
         const bool evo_auto = h->mgu.on && h->mgu.A.n_levels >= 5 && h->n_nodes >= 500000;
-        const bool evo = me ? std::string(me) == "1" : evo_auto;
-        if (evo && h->mgu.on) {
+        const std::string mev = me ? std::string(me) : std::string(evo_auto ? "scalar" : "0");
+        if (mev == "packed" && h->mgu.on) {
           pf_status es = mg_setup(h, h->mgd, 1, om * dev_sms * pfb::MG_WARPS);
+          if (es != PF_OK) return bail(es);
+        } else if ((mev == "1" || mev == "scalar") && h->mgu.on) {
+          int os = 0, o3 = 0;
+          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&os, pfb::k_mgs_fine_smooth, pfb::MG_NT, 0));
+          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, pfb::k_mgs_pcg, pfb::MG_NT, 0));
+          os = std::min(os, o3);
+          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, pfb::k_mgs_fine_resid, pfb::MG_NT, 0));
+          os = std::max(1, std::min(os, o3));
+          pf_status es = mgs_setup(h, h->mgs, os * dev_sms * pfb::MG_WARPS);
           if (es != PF_OK) return bail(es);
         }
         const char* mw = getenv("PFB200_MG_WARM");  // "0": MG solves start cold (x0 = 0)
@@ -1942,6 +2268,36 @@ static pf_status run_mg(pf_handle* h, MgInst& M, double* target, int* status, lo
   return cg_status(h, *status, *iters);
 }
 
+// one scalar phase-field MG-PCG solve on (rd, dinvd, b): fresh hierarchy, then the solve graph
+// (device-side WHILE); the solution lands in xd, rd is consumed
+static pf_status run_mgs(pf_handle* h, MgsInst& M, int* status, long long* iters,
+                         long long maxiter = -1, double rtol = -1.0, bool check = true) {
+  M.in->n_guess = 0;
+  M.in->rtol = rtol >= 0.0 ? rtol : h->cfg.cg_rtol;
+  M.in->maxiter = maxiter > 0 ? maxiter : (long long)h->cfg.cg_maxiter_factor * h->n_nodes;
+  M.in->target = nullptr;
+  PF_CUDA(cudaEventRecord(h->ev0, h->stream));
+  PF_CUDA(cudaMemcpyAsync((void*)M.A.in, M.in, sizeof(pfb::MgIn), cudaMemcpyHostToDevice,
+                          h->stream));
+  PF_CUDA(cudaGraphLaunch(M.setup_exec, h->stream));
+  PF_TRY(launched(h));
+  PF_CUDA(cudaGraphLaunch(M.solve_exec, h->stream));
+  PF_TRY(launched(h));
+  PF_CUDA(cudaEventRecord(h->ev1, h->stream));
+  PF_CUDA(cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  M.setups += 1;
+  *status = h->h_cgres->status;
+  *iters = h->h_cgres->iters;
+  h->acc.launches += M.setup_kernels - 1 + 1 + (int)(*iters) * M.body_kernels + 1 - 1;
+  if (h->trace)
+    fprintf(stderr, "[pfb200] scalar phase-field mg solve: %lld iterations, %.3f ms\n", *iters, ms);
+  if (!check) return PF_OK;
+  cg_account(h, false, *iters, ms);
+  return cg_status(h, *status, *iters);
+}
+
 static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
                         long long* iters, double* const* guess = nullptr, int n_guess = 0) {
   if (mom && h->mgu.on && !probe)
@@ -2128,7 +2484,13 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
       const int ng = use_warm ? h->warm_nd[ws] : 0;
       for (int k = 0; k < ng; ++k) guess[k] = h->warm_d[ws][k];
       bool done = false;
-      if (h->mgd.on && !h->comm) {
+      if (h->mgs.on && !h->comm) {
+        // native scalar multigrid PCG (pf_mgs.cuh) on the phase-field system in place
+        PF_TRY(run_mgs(h, h->mgs, &status, &iters));
+        PF_TRY(axpy(h, h->d, h->xd, h->n_nodes));
+        done = true;
+      }
+      if (!done && h->mgd.on && !h->comm) {
         // multigrid PCG on the packed two-component layout (pf_mg.cuh, phys 1)
         const long long n = h->n_nodes;
         const unsigned gb = (unsigned)std::min<long long>((n + 255) / 256, 8LL * h->sm_count);
@@ -2467,7 +2829,19 @@ extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, doub
                                  int64_t* iters_out) {
   if (!h) return PF_ERR_INVALID;
   PF_CUDA(cudaSetDevice(h->device));
-  if (n_iter < 1 || physics < 0 || physics > 2) return fail(h, PF_ERR_INVALID, "bad arguments");
+  if (n_iter < 1 || physics < 0 || physics > 3) return fail(h, PF_ERR_INVALID, "bad arguments");
+  if (physics == 3) {  // scalar phase-field multigrid PCG (pf_mgs.cuh), fresh hierarchy
+    if (!h->mgs.on) return fail(h, PF_ERR_INVALID, "no scalar phase-field hierarchy on this handle");
+    PF_TRY(launch_evo_prepare(h, 1, 0));
+    int status = 0;
+    long long iters = 0;
+    PF_TRY(run_mgs(h, h->mgs, &status, &iters, n_iter, 0.0, false));
+    float ms = 0.f;
+    PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (ms_out) *ms_out = ms;
+    if (iters_out) *iters_out = iters;
+    return PF_OK;
+  }
   if (physics == 2) {  // multigrid-preconditioned momentum PCG
     if (!h->mgu.on) return fail(h, PF_ERR_INVALID, "no multigrid hierarchy on this handle");
     PF_TRY(launch_mom_prepare(h, 1));
@@ -2503,6 +2877,71 @@ extern "C" pf_status pf_bench_cg(pf_handle* h, int physics, int64_t n_iter, doub
   return PF_OK;
 }
 
+// Average device time of one fine-level multigrid march on the current hierarchy and state,
+// re-launched `reps` times outside the solve graph (CUDA events on the handle's stream; a kernel
+// inside the conditional solve graph cannot be event-timed or seen by ncu).  which: 0 / 1 / 2
+// the momentum hierarchy's fine residual, smoothing and PCG-direction marches; 10 / 11 / 12 the
+// same of the scalar phase-field hierarchy.  bytes_out: the kernel's algorithmic bytes per launch
+// (compulsory traffic of its inputs and outputs).
+extern "C" pf_status pf_bench_mg_kernel(pf_handle* h, int which, int reps, double* ms_out,
+                                        double* bytes_out) {
+  if (!h) return PF_ERR_INVALID;
+  PF_CUDA(cudaSetDevice(h->device));
+  if (reps < 1) return fail(h, PF_ERR_INVALID, "pf_bench_mg_kernel: reps < 1");
+  const double n = h->n_nodes, e = h->n_elems;
+  double bytes = 0.0;
+  auto run = [&](auto&& launch) -> pf_status {
+    launch();  // warm
+    PF_CUDA(cudaEventRecord(h->ev0, h->stream));
+    for (int k = 0; k < reps; ++k) launch();
+    PF_CUDA(cudaEventRecord(h->ev1, h->stream));
+    PF_CUDA(cudaStreamSynchronize(h->stream));
+    PF_CUDA(cudaGetLastError());
+    return PF_OK;
+  };
+  cudaStream_t s = h->stream;
+  if (which >= 0 && which <= 2) {
+    if (!h->mgu.on || !h->mgu.built) return fail(h, PF_ERR_INVALID, "no built momentum hierarchy");
+    MgInst& M = h->mgu;
+    pfb::MgArgs A = M.A;
+    A.use_cond = 0;
+    const double n1 = A.L[1].m.n_nodes;
+    if (which == 0) {
+      bytes = 56.0 * n + e;  // r, D^-1 (16 B), d (8 B), t (16 B); branch bits 1 B per cell
+      PF_TRY(run([&] { pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));
+    } else if (which == 1) {
+      bytes = 56.0 * n + 16.0 * n1 + e;  // r, D^-1, d, z; level-1 correction; bits
+      PF_TRY(run([&] { pfb::k_mg_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));
+    } else {
+      bytes = 88.0 * n + e;  // z, p_old, d, D^-1, p_new, q; bits
+      PF_TRY(run([&] { pfb::k_mg_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(A, M.gf); }));
+    }
+  } else if (which >= 10 && which <= 12) {
+    if (!h->mgs.on || h->mgs.setups == 0) return fail(h, PF_ERR_INVALID, "no built phase-field hierarchy");
+    MgsInst& M = h->mgs;
+    pfb::MgsArgs A = M.A;
+    A.use_cond = 0;
+    const double n1 = A.L[1].m.n_nodes;
+    if (which == 10) {
+      bytes = 24.0 * n + 32.0 * e;  // r, D^-1, t (8 B); b per Gauss point (32 B per cell)
+      PF_TRY(run([&] { pfb::k_mgs_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));
+    } else if (which == 11) {
+      bytes = 24.0 * n + 8.0 * n1 + 32.0 * e;  // r, D^-1, z; level-1 correction; b
+      PF_TRY(run([&] { pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));
+    } else {
+      bytes = 40.0 * n + 32.0 * e;  // z, p_old, D^-1, p_new, q; b
+      PF_TRY(run([&] { pfb::k_mgs_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(A, M.gf); }));
+    }
+  } else {
+    return fail(h, PF_ERR_INVALID, "pf_bench_mg_kernel: unknown kernel");
+  }
+  float ms = 0.f;
+  PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  if (ms_out) *ms_out = ms / reps;
+  if (bytes_out) *bytes_out = bytes;
+  return PF_OK;
+}
+
 extern "C" pf_status pf_mg_info(pf_handle* h, int32_t* n_levels, int32_t* n_grid,
                                 int32_t* dense, int64_t* setups, double* omega) {
   if (!h) return PF_ERR_INVALID;
@@ -2525,7 +2964,8 @@ extern "C" pf_status pf_solver_kinds(pf_handle* h, int32_t* momentum, int32_t* p
   if (!h) return PF_ERR_INVALID;
   if (momentum) *momentum = h->mgu.on ? 2 : (h->sr_mom ? 1 : 0);
   if (phase_field)
-    *phase_field = h->mgd.on && !h->comm ? 3
+    *phase_field = h->mgs.on && !h->comm   ? 4
+                   : h->mgd.on && !h->comm ? 3
                    : (h->sr_evo && !h->comm && !h->split ? (h->st_evo ? 2 : 1) : 0);
   return PF_OK;
 }

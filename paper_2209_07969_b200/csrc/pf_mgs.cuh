@@ -1,0 +1,1014 @@
+// pf_mgs.cuh — native scalar geometric-multigrid PCG for the phase-field Newton systems
+// (solve_evolution, schemes.py:242-313: K_dd = sum N b N^T w + grad_w sum gradN gradN^T w,
+// assembly.py:233-246, masked at the pinned nodes, assembly.py:279-312).
+//
+// Same system, x0 = 0 and stopping test as the reference's Jacobi-PCG switch
+// (linsolve.py:48-54; SciPy 1.18.1 cg: stop at the top of an iteration when the recursive
+// residual satisfies ||r|| < rtol ||b||, maxiter 20 n); the preconditioner is one symmetric
+// V(1,1)-cycle.  Round 1 ran these solves through the two-component momentum machinery with the
+// y dofs dead (pf_mg.cuh, phys 1): every vector, diagonal and restriction was double2 and every
+// coarse stencil a 2x2 block, twice the fine-level and four times the coarse-level traffic of the
+// scalar field, and 8x8 Galerkin products per coarse cell.  This is the scalar hierarchy:
+//   * level 0: the matrix-free phase-field operator (evo_cell_apply: per-Gauss-point Newton
+//     coefficient b of k_evo_prepare + the constant gradient block), marched by warps
+//     (mg_march of pf_mg.cuh with the value in the x lane);
+//   * level l+1: 2x2 agglomeration of level l's cells (L-panel rows and the slit kept, as in
+//     pf_mg.cuh), bilinear prolongation masked at pinned / dead nodes, Galerkin cell matrices
+//     K_E = sum_c Q_c^T K_c Q_c (4x4 per coarse cell, one thread per coarse cell);
+//   * assembled 10-slot scalar stencils (3x3 + the slit tip's second face); grid levels read
+//     them in FP32 (preconditioner only: the PCG's operator, residual recurrence, dot products
+//     and stopping test stay FP64), the single-CTA tail in FP64 from shared memory;
+//   * damped Jacobi V(1,1) with omega_l = 4 / (3 lambda_l), lambda_l from MG_POW power steps;
+//   * coarsest level by a dense inverse (<= MGS_DENSE_MAX nodes) or nu_c Jacobi sweeps.
+// Reductions: per-CTA partials summed in a fixed order (bit-reproducible run to run).
+#pragma once
+
+namespace pfb {
+
+constexpr int MGS_DENSE_MAX = 64;  // coarsest level by a dense inverse when n_nodes <= this
+constexpr int MGS_TAIL_P = 2;      // node passes of the tail's top level (MG_TAIL_NT / 4 each)
+
+struct MgsLevel {
+  DMesh m;
+  double* K;      // [n_elems][16] Galerkin cell matrices (l >= 1)
+  double* dinv;   // [n] inverse diagonal (0: pinned / dead node)
+  double* b;      // right-hand side (l >= 1)
+  double* t;      // residual / prolongated iterate / power-iteration buffer
+  double* e;      // correction / power-iteration buffer
+  const int* nbr; // [MG_NS][n] stencil neighbours (l >= 1)
+  double* S;      // [MG_NS][n] FP64 stencil (tail levels)
+  float* Sf;      // [MG_NS][n] FP32 stencil (grid levels)
+  const int* rid; // [12][n] restriction sources on level l-1
+  const int* pid; // [4][n] prolongation sources on level l+1
+  int items, item_off, lpn, in_tail;
+};
+
+struct MgsArgs {
+  Consts C;
+  int n_levels, n_tail, dense, nu_c;
+  MgsLevel L[MG_MAXL];
+  MarchGeom g0;
+  int coarse_items;
+  const double* bq;           // level-0 Newton coefficient per Gauss point [n_elems][4]
+  double *x, *r, *z, *p0, *p1, *q;
+  double* Ainv;               // [nd*nd] dense inverse of the coarsest level
+  double* part;
+  MgCtl* ctl;
+  const MgIn* in;
+  CgResult* result;
+  long long n;                // fine nodes
+  cudaGraphConditionalHandle cond;
+  int use_cond;
+  MgTailSlot ts[MG_MAXL];
+  int ts_ainv, ts_bytes;
+};
+
+__device__ __forceinline__ double mgs_mask(double v, double di) { return di != 0.0 ? v : 0.0; }
+
+// ---- fine level (level 0): scalar node ops for mg_march (value in the x lane, y = 0) --------
+struct SFineBase {
+  const Consts* C;
+  const double* bq;
+  const double* dinv;
+  __device__ void cell(int eid, const double2 (&v)[4], const double (&)[4],
+                       double2 (&f)[4]) const {
+    const double2 b01 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid);
+    const double2 b23 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid + 1);
+    const double pc[4] = {v[0].x, v[1].x, v[2].x, v[3].x};
+    const double bb[4] = {b01.x, b01.y, b23.x, b23.y};
+    double fx[4];
+    evo_cell_apply(*C, pc, bb, fx);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) f[k] = make_double2(fx[k], 0.0);
+  }
+  __device__ double di(int id) const { return __ldg(dinv + id); }
+};
+
+struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), t = r - A x
+  double om;
+  const double* r;
+  double* t;
+  struct Raw {
+    double dv, bv;
+  };
+  __device__ void fetch(int id, Raw& w) const {
+    w.dv = di(id);
+    w.bv = __ldg(r + id);
+  }
+  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
+    aux = 0.0;
+    return make_double2(om * w.dv * w.bv, 0.0);
+  }
+  __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
+    aux = 0.0;
+    if (id < 0) return make_double2(0.0, 0.0);
+    Raw w;
+    fetch(id, w);
+    return finish(w, id, i, j, dup, aux);
+  }
+  __device__ void out(int id, double2 Av, double2) const {
+    t[id] = mgs_mask(__ldg(r + id) - Av.x, di(id));
+  }
+};
+
+// prolongation (P e_{l+1}) at node (i, j) of level l; dup = upper-face slit node
+__device__ __forceinline__ double mgs_prolong(const DMesh& mf, const DMesh& mc, const double* ec,
+                                              int i, int j, bool dup) {
+  const bool up = dup || (mf.notch_row >= 0 && j > mf.notch_row);
+  const int I0 = i >> 1, J0 = j >> 1, I1 = I0 + (i & 1), J1 = J0 + (j & 1);
+  const double w = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
+  const int4 r0 = __ldg(mc.nrow + J0), r1 = __ldg(mc.nrow + min(J1, mc.ny));
+  const int c00 = mg_row_node(mc, r0, I0, J0, up), c10 = mg_row_node(mc, r0, I1, J0, up);
+  const int c01 = mg_row_node(mc, r1, I0, J1, up), c11 = mg_row_node(mc, r1, I1, J1, up);
+  const double v00 = __ldg(ec + max(c00, 0)), v10 = __ldg(ec + max(c10, 0));
+  const double v01 = __ldg(ec + max(c01, 0)), v11 = __ldg(ec + max(c11, 0));
+  const double a00 = c00 >= 0 ? w : 0.0;
+  const double a10 = (c10 >= 0 && I1 != I0) ? w : 0.0;
+  const double a01 = (c01 >= 0 && J1 != J0) ? w : 0.0;
+  const double a11 = (c11 >= 0 && I1 != I0 && J1 != J0) ? w : 0.0;
+  return a00 * v00 + a10 * v10 + a01 * v01 + a11 * v11;
+}
+
+struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 (r - A y); r.z
+  double om;
+  const double* r;
+  double* z;
+  const DMesh* mf;
+  const DMesh* mc;
+  const double* ec;
+  double* rz;
+  struct Raw {
+    double dv, bv;
+  };
+  __device__ void fetch(int id, Raw& w) const {
+    w.dv = di(id);
+    w.bv = __ldg(r + id);
+  }
+  __device__ double2 finish(const Raw& w, int, int i, int j, bool dup, double& aux) const {
+    aux = 0.0;
+    const double pe = mgs_prolong(*mf, *mc, ec, i, j, dup);
+    return make_double2(mgs_mask(om * w.dv * w.bv + pe, w.dv), 0.0);
+  }
+  __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
+    aux = 0.0;
+    if (id < 0) return make_double2(0.0, 0.0);
+    Raw w;
+    fetch(id, w);
+    return finish(w, id, i, j, dup, aux);
+  }
+  __device__ void out(int id, double2 Av, double2 y) const {
+    const double dv = di(id), bv = __ldg(r + id);
+    const double ev = y.x + om * dv * (bv - Av.x);
+    z[id] = ev;
+    *rz += bv * ev;
+  }
+};
+
+struct SFinePow : SFineBase {  // power step vout = D^-1 A vin (vin == nullptr: hashed start)
+  const double* vin;
+  double* vout;
+  struct Raw {
+    double v, dv;
+  };
+  __device__ void fetch(int id, Raw& w) const {
+    w.v = vin ? __ldg(vin + id) : mg_hash01(2u * id + 1u);
+    w.dv = di(id);
+  }
+  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
+    aux = 0.0;
+    return make_double2(mgs_mask(w.v, w.dv), 0.0);
+  }
+  __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
+    aux = 0.0;
+    if (id < 0) return make_double2(0.0, 0.0);
+    Raw w;
+    fetch(id, w);
+    return finish(w, id, i, j, dup, aux);
+  }
+  __device__ void out(int id, double2 Av, double2) const { vout[id] = di(id) * Av.x; }
+};
+
+struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (masked), p.q
+  double beta;
+  const double* z;
+  const double* pold;
+  double* pnew;
+  double* q;
+  double* pq;
+  struct Raw {
+    double zv, po;
+  };
+  __device__ void fetch(int id, Raw& w) const {
+    w.zv = __ldg(z + id);
+    w.po = pold ? __ldg(pold + id) : 0.0;
+  }
+  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
+    aux = 0.0;
+    return make_double2(pold ? w.zv + beta * w.po : w.zv, 0.0);
+  }
+  __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
+    aux = 0.0;
+    if (id < 0) return make_double2(0.0, 0.0);
+    Raw w;
+    fetch(id, w);
+    return finish(w, id, i, j, dup, aux);
+  }
+  __device__ void out(int id, double2 Av, double2 p) const {
+    const double qv = mgs_mask(Av.x, di(id));
+    pnew[id] = p.x;
+    q[id] = qv;
+    *pq += p.x * qv;
+  }
+};
+
+// ---- coarse levels: node kernels of the assembled scalar form -------------------------------
+template <int W>
+__device__ __forceinline__ double hw_sum1(double v) {  // butterfly over W aligned lanes
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <int LPN>
+__device__ __forceinline__ double nm_sum1(double v) { return LPN == 1 ? v : hw_sum1<LPN>(v); }
+
+// slot s2 of S x[nbr] at node id (FP32 stencil of the grid levels)
+template <class X>
+__device__ __forceinline__ double mgs_slot_apply(const MgsLevel& L, int n, int id, int s2,
+                                                 X&& xval) {
+  if (s2 >= MG_NS || id >= n) return 0.0;
+  const int k = __ldg(L.nbr + (size_t)s2 * n + id);
+  if (k < 0) return 0.0;
+  return (double)__ldg(L.Sf + (size_t)s2 * n + id) * xval(k);
+}
+template <int LPN, class X>
+__device__ __forceinline__ double mgs_apply(const MgsLevel& L, int n, int id, X&& xval) {
+  double acc = 0.0;
+#pragma unroll
+  for (int s2 = NodeMap<LPN>::lane(); s2 < MG_NS; s2 += LPN) acc += mgs_slot_apply(L, n, id, s2, xval);
+  return nm_sum1<LPN>(acc);
+}
+
+// restriction b = P^T t_{l-1} (masked)
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mgs_srestrict(MgsArgs A, int l) {
+  const MgsLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double* tf = A.L[l - 1].t;
+  MG_FOR_NODE_L(n) {
+    double v = 0.0;
+    if (id < n) {
+#pragma unroll
+      for (int s2 = NodeMap<LPN>::lane(); s2 < 12; s2 += LPN) {
+        const int f = __ldg(L.rid + (size_t)s2 * n + id);
+        if (f >= 0) v += mg_rw(s2) * __ldg(tf + f);
+      }
+    }
+    v = nm_sum1<LPN>(v);
+    if (MG_LEAD) L.b[id] = mgs_mask(v, __ldg(L.dinv + id));
+  }
+}
+// t = b - A x, x = omega D^-1 b
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mgs_sresid(MgsArgs A, int l) {
+  const MgsLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  MG_FOR_NODE_L(n) {
+    const double Av = mgs_apply<LPN>(L, n, id, [&](int k) -> double {
+      return om * __ldg(L.dinv + k) * __ldg(L.b + k);
+    });
+    if (MG_LEAD) L.t[id] = mgs_mask(__ldg(L.b + id) - Av, __ldg(L.dinv + id));
+  }
+}
+// y = omega D^-1 b + P e_{l+1} (into t)
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mgs_sprolongate(MgsArgs A, int l) {
+  const MgsLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  const double* ec = A.L[l + 1].e;
+  MG_FOR_NODE_L(n) {
+    double v = 0.0, cnt = 0.0;
+    if (id < n) {
+#pragma unroll
+      for (int s2 = NodeMap<LPN>::lane(); s2 < 4; s2 += LPN) {
+        const int c = __ldg(L.pid + (size_t)s2 * n + id);
+        if (c >= 0) {
+          v += __ldg(ec + c);
+          cnt += 1.0;
+        }
+      }
+    }
+    v = nm_sum1<LPN>(v);
+    cnt = nm_sum1<LPN>(cnt);
+    if (MG_LEAD) {
+      const double di = __ldg(L.dinv + id);
+      L.t[id] = mgs_mask(om * di * __ldg(L.b + id) + v / cnt, di);
+    }
+  }
+}
+// e = y + omega D^-1 (b - A y), y in t
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mgs_ssmooth(MgsArgs A, int l) {
+  const MgsLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  MG_FOR_NODE_L(n) {
+    const double Ay = mgs_apply<LPN>(L, n, id, [&](int k) -> double { return __ldg(L.t + k); });
+    if (MG_LEAD)
+      L.e[id] = __ldg(L.t + id) + om * __ldg(L.dinv + id) * (__ldg(L.b + id) - Ay);
+  }
+}
+// fused down-sweep of a small level: the restriction of t_{l-1} evaluated at each neighbour by
+// the lane that multiplies it, x = omega D^-1 b, t = b - A x; b stored for the up-sweep
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mgs_sdown(MgsArgs A, int l) {
+  const MgsLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  const double* tf = A.L[l - 1].t;
+  MG_FOR_NODE_L(n) {
+    double acc = 0.0, bc = 0.0;
+    if (id < n) {
+#pragma unroll
+      for (int s2 = NodeMap<LPN>::lane(); s2 < MG_NS; s2 += LPN) {
+        const int k = __ldg(L.nbr + (size_t)s2 * n + id);
+        if (k < 0) continue;
+        int f[12];
+#pragma unroll
+        for (int j = 0; j < 12; ++j) f[j] = __ldg(L.rid + (size_t)j * n + k);
+        double b = 0.0;
+#pragma unroll
+        for (int j = 0; j < 12; ++j)
+          if (f[j] >= 0) b += mg_rw(j) * __ldg(tf + f[j]);
+        const double di = __ldg(L.dinv + k);
+        b = mgs_mask(b, di);
+        if (s2 == 4) bc = b;
+        acc += (double)__ldg(L.Sf + (size_t)s2 * n + id) * (om * di * b);
+      }
+    }
+    acc = nm_sum1<LPN>(acc);
+    bc = nm_sum1<LPN>(bc);
+    if (MG_LEAD) {
+      L.b[id] = bc;
+      L.t[id] = mgs_mask(bc - acc, __ldg(L.dinv + id));
+    }
+  }
+}
+// fused up-sweep of a small level: y = omega D^-1 b + P e_{l+1} at each neighbour by its lane,
+// e = y + omega D^-1 (b - A y)
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mgs_sup(MgsArgs A, int l) {
+  const MgsLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  const double* ec = A.L[l + 1].e;
+  MG_FOR_NODE_L(n) {
+    double acc = 0.0, yc = 0.0;
+    if (id < n) {
+#pragma unroll
+      for (int s2 = NodeMap<LPN>::lane(); s2 < MG_NS; s2 += LPN) {
+        const int k = __ldg(L.nbr + (size_t)s2 * n + id);
+        if (k < 0) continue;
+        int c[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = __ldg(L.pid + (size_t)j * n + k);
+        const double w = 1.0 / ((c[0] >= 0) + (c[1] >= 0) + (c[2] >= 0) + (c[3] >= 0));
+        double pe = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (c[j] >= 0) pe += __ldg(ec + c[j]);
+        const double di = __ldg(L.dinv + k);
+        const double y = mgs_mask(om * di * __ldg(L.b + k) + w * pe, di);
+        if (s2 == 4) yc = y;
+        acc += (double)__ldg(L.Sf + (size_t)s2 * n + id) * y;
+      }
+    }
+    acc = nm_sum1<LPN>(acc);
+    yc = nm_sum1<LPN>(yc);
+    if (MG_LEAD) L.e[id] = yc + om * __ldg(L.dinv + id) * (__ldg(L.b + id) - acc);
+  }
+}
+// Jacobi sweep out = in + omega D^-1 (b - A in) (grid coarsest level)
+template <int LPN>
+__global__ void __launch_bounds__(MG_NT) k_mgs_ssweep(MgsArgs A, int l, const double* in,
+                                                      double* out) {
+  const MgsLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  MG_FOR_NODE_L(n) {
+    const double Ax = mgs_apply<LPN>(L, n, id, [&](int k) -> double { return __ldg(in + k); });
+    if (MG_LEAD) out[id] = __ldg(in + id) + om * __ldg(L.dinv + id) * (__ldg(L.b + id) - Ax);
+  }
+}
+__global__ void __launch_bounds__(MG_NT) k_mgs_jacobi0(MgsArgs A, int l, double* out) {
+  const MgsLevel& L = A.L[l];
+  const double om = __ldcg(&A.ctl->omega[l]);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < L.m.n_nodes;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = om * __ldcg(L.dinv + i) * __ldcg(L.b + i);
+}
+__global__ void __launch_bounds__(MG_NT) k_mgs_coarse_dense(MgsArgs A) {
+  const MgsLevel& L = A.L[A.n_levels - 1];
+  const int nd = L.m.n_nodes;
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < nd; ++j) s += __ldcg(A.Ainv + (size_t)i * nd + j) * __ldcg(L.b + j);
+    L.e[i] = s;
+  }
+}
+
+// power step at one node of a coarse level: vout = D^-1 A vin (vin == nullptr: hashed start)
+template <int LPN>
+__device__ __forceinline__ void mgs_spow(const MgsLevel& L, const double* vin, double* vout,
+                                         int id) {
+  const int n = L.m.n_nodes;
+  double acc = 0.0;
+#pragma unroll
+  for (int s2 = NodeMap<LPN>::lane(); s2 < MG_NS; s2 += LPN)
+    acc += mgs_slot_apply(L, n, id, s2, [&](int k) -> double {
+      const double x = vin ? __ldg(vin + k) : mg_hash01(2u * k + 1u);
+      return mgs_mask(x, __ldg(L.dinv + k));
+    });
+  const double Av = nm_sum1<LPN>(acc);
+  if (NodeMap<LPN>::lane() == 0 && id < n) vout[id] = __ldg(L.dinv + id) * Av;
+}
+
+// ---- setup ----------------------------------------------------------------------------------
+// Galerkin cell matrices of level lc from level lc-1, one thread per coarse cell:
+// K_E = sum_c Q_c^T K_c Q_c with K_c the child's 4x4 matrix (lc == 1: the fine phase-field cell
+// matrix sum_g b_g N_g N_g^T w + the gradient block, rows / columns of masked corners zeroed).
+__global__ void __launch_bounds__(MG_NT) k_mgs_galerkin(MgsArgs A, int lc) {
+  const DMesh& mc = A.L[lc].m;
+  const DMesh& mf = A.L[lc - 1].m;
+  const int total = mc.nx * mc.ny;
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < total; it += gridDim.x * blockDim.x) {
+    const int J = it / mc.nx, I = it % mc.nx;
+    const int4 er = __ldg(mc.erow + J);
+    if (I < er.x || I >= er.y) continue;
+    const int E = er.z + (I - er.x);
+    double KE[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) KE[k] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int ci = 2 * I + (c & 1), cj = 2 * J + (c >> 1);
+      const int fe = mg_cell(mf, ci, cj);
+      if (fe < 0) continue;
+      double Kc[16];
+      if (lc == 1) {
+        int nd[4];
+        nd[0] = mg_node(mf, ci, cj, true);
+        nd[1] = mg_node(mf, ci + 1, cj, true);
+        nd[2] = mg_node(mf, ci + 1, cj + 1, false);
+        nd[3] = mg_node(mf, ci, cj + 1, false);
+        bool live[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) live[a] = nd[a] >= 0 && __ldg(A.L[0].dinv + nd[a]) != 0.0;
+        const double2 b01 = __ldg(reinterpret_cast<const double2*>(A.bq) + 2 * fe);
+        const double2 b23 = __ldg(reinterpret_cast<const double2*>(A.bq) + 2 * fe + 1);
+        const double bb[4] = {b01.x, b01.y, b23.x, b23.y};
+        // the columns of evo_cell_apply (same products, same order)
+#pragma unroll
+        for (int bcol = 0; bcol < 4; ++bcol) {
+          double pc[4] = {0.0, 0.0, 0.0, 0.0};
+          pc[bcol] = 1.0;
+          double f[4];
+          evo_cell_apply(A.C, pc, bb, f);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) Kc[a * 4 + bcol] = (live[a] && live[bcol]) ? f[a] : 0.0;
+        }
+      } else {
+        const double2* Kf = reinterpret_cast<const double2*>(A.L[lc - 1].K + 16 * (size_t)fe);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double2 v = __ldg(Kf + k);
+          Kc[2 * k] = v.x;
+          Kc[2 * k + 1] = v.y;
+        }
+      }
+      // T = K_c Q_c, KE += Q_c^T T
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        double T[4];
+#pragma unroll
+        for (int B = 0; B < 4; ++B) {
+          double s = 0.0;
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) s += Kc[a * 4 + k2] * mg_q(c, k2, B);
+          T[B] = s;
+        }
+#pragma unroll
+        for (int Ar = 0; Ar < 4; ++Ar) {
+          const double qa = mg_q(c, a, Ar);
+#pragma unroll
+          for (int B = 0; B < 4; ++B) KE[Ar * 4 + B] += qa * T[B];
+        }
+      }
+    }
+    double2* out = reinterpret_cast<double2*>(A.L[lc].K + 16 * (size_t)E);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) out[k] = make_double2(KE[2 * k], KE[2 * k + 1]);
+  }
+}
+
+// assemble the stencil of level l from its cell matrices (FP32 for grid levels, FP64 for the
+// tail), and its inverse diagonal; one thread per node
+__global__ void __launch_bounds__(MG_NT) k_mgs_stencil(MgsArgs A, int l) {
+  const MgsLevel& L = A.L[l];
+  const DMesh& m = L.m;
+  const int n = m.n_nodes;
+  mg_for_nodes<GMem>(m, blockIdx.x * MG_WARPS + (threadIdx.x >> 5), gridDim.x * MG_WARPS,
+                     [&](int id, int i, int j, bool) {
+    int nb[MG_NS];
+#pragma unroll
+    for (int s2 = 0; s2 < MG_NS; ++s2) nb[s2] = __ldg(L.nbr + (size_t)s2 * n + id);
+    double acc[MG_NS];
+#pragma unroll
+    for (int s2 = 0; s2 < MG_NS; ++s2) acc[s2] = 0.0;
+    const int cdx[4] = {-1, 0, -1, 0}, cdy[4] = {-1, -1, 0, 0}, ck[4] = {2, 3, 1, 0};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {  // below-left, below-right, above-left, above-right
+      const int ci = i + cdx[c], cj = j + cdy[c];
+      const int e = mg_cell(m, ci, cj);
+      if (e < 0) continue;
+      int cn[4];
+      cn[0] = mg_node(m, ci, cj, true);
+      cn[1] = mg_node(m, ci + 1, cj, true);
+      cn[2] = mg_node(m, ci + 1, cj + 1, false);
+      cn[3] = mg_node(m, ci, cj + 1, false);
+      const int k = ck[c];
+      if (cn[k] != id) continue;  // the cell is on the other face of the slit
+      const double* Ke = L.K + 16 * (size_t)e;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int qx = ci + ((q == 1 || q == 2) ? 1 : 0) - i, qy = cj + (q >= 2 ? 1 : 0) - j;
+        int slot = qy < 0 ? 1 + qx : (qy > 0 ? 7 + qx : 4 + qx);
+        if (qy == 0 && nb[slot] != cn[q]) slot = 9;
+        const double kv = __ldg(Ke + k * 4 + q);
+#pragma unroll
+        for (int s2 = 0; s2 < MG_NS; ++s2)
+          if (s2 == slot) acc[s2] += kv;
+      }
+    }
+    if (L.in_tail) {
+#pragma unroll
+      for (int s2 = 0; s2 < MG_NS; ++s2) L.S[(size_t)s2 * n + id] = acc[s2];
+    } else {
+#pragma unroll
+      for (int s2 = 0; s2 < MG_NS; ++s2) L.Sf[(size_t)s2 * n + id] = (float)acc[s2];
+    }
+    L.dinv[id] = acc[4] > 0.0 ? 1.0 / acc[4] : 0.0;
+  });
+}
+
+// power step k (1..MG_POW): blocks [0, fine_blocks) march the fine level, the rest gather the
+// coarse grid levels (concatenated item space; the tail levels use their FP64 stencils below)
+__global__ void __launch_bounds__(MG_NT, 3) k_mgs_pow(MgsArgs A, int step, int fine_blocks) {
+  __shared__ MgWarp ws[MG_WARPS];
+  const int warp = threadIdx.x >> 5;
+  auto vin = [&](const MgsLevel& L) -> const double* {
+    return step == 1 ? nullptr : (((step - 1) & 1) ? L.t : L.e);
+  };
+  auto vout = [&](const MgsLevel& L) -> double* { return (step & 1) ? L.t : L.e; };
+  if ((int)blockIdx.x < fine_blocks) {
+    SFinePow op{{&A.C, A.bq, A.L[0].dinv}, vin(A.L[0]), vout(A.L[0])};
+    const int w = blockIdx.x * MG_WARPS + warp;
+    if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[warp]);
+    return;
+  }
+  const int t = (blockIdx.x - fine_blocks) * MG_NT + threadIdx.x;
+  if (t >= A.coarse_items) return;
+  int l = 1;
+  while (l + 1 < A.n_tail && t >= A.L[l + 1].item_off) ++l;
+  const MgsLevel& L = A.L[l];
+  const int q = t - L.item_off;
+  if (L.lpn == 16) mgs_spow<16>(L, vin(L), vout(L), q >> 4);
+  else if (L.lpn == 4) mgs_spow<4>(L, vin(L), vout(L), q >> 2);
+  else mgs_spow<1>(L, vin(L), vout(L), q);
+}
+// power steps of the tail levels (FP64 stencils), one CTA, all MG_POW steps
+__global__ void __launch_bounds__(MG_TAIL_NT) k_mgs_pow_tail(MgsArgs A) {
+  for (int step = 1; step <= MG_POW; ++step) {
+    for (int l = A.n_tail; l < A.n_levels; ++l) {
+      const MgsLevel& L = A.L[l];
+      const int n = L.m.n_nodes;
+      const double* vin = step == 1 ? nullptr : (((step - 1) & 1) ? L.t : L.e);
+      double* vout = (step & 1) ? L.t : L.e;
+      for (int id = threadIdx.x; id < n; id += blockDim.x) {
+        double acc = 0.0;
+        for (int s2 = 0; s2 < MG_NS; ++s2) {
+          const int k = L.nbr[(size_t)s2 * n + id];
+          if (k < 0) continue;
+          const double x = vin ? __ldcg(vin + k) : mg_hash01(2u * k + 1u);
+          acc += __ldcg(L.S + (size_t)s2 * n + id) * mgs_mask(x, __ldcg(L.dinv + k));
+        }
+        vout[id] = __ldcg(L.dinv + id) * acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+// omega_l = 4 / (3 lambda_l), lambda_l = ||v_POW|| / ||v_POW-1|| (per-level partials)
+__global__ void __launch_bounds__(MG_NT) k_mgs_lambda(MgsArgs A) {
+  __shared__ double red[MG_WARPS * 2 * MG_MAXL];
+  double v[2 * MG_MAXL];
+#pragma unroll
+  for (int l = 0; l < 2 * MG_MAXL; ++l) v[l] = 0.0;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+#pragma unroll
+  for (int l = 0; l < MG_MAXL; ++l) {
+    if (l >= A.n_levels) break;
+    const double* a1 = (MG_POW & 1) ? A.L[l].t : A.L[l].e;
+    const double* a0 = (MG_POW & 1) ? A.L[l].e : A.L[l].t;
+    const long long n = A.L[l].m.n_nodes;
+    for (long long i = tid; i < n; i += nth) {
+      const double x1 = __ldcg(a1 + i), x0 = __ldcg(a0 + i);
+      v[2 * l] += x1 * x1;
+      v[2 * l + 1] += x0 * x0;
+    }
+  }
+  if (mg_publish<2 * MG_MAXL>(v, A.part, &A.ctl->count, red)) {
+    double g[2 * MG_MAXL];
+    mg_all_reduce<2 * MG_MAXL>(A.part, gridDim.x, red, g);
+    if (threadIdx.x < MG_MAXL) {
+      const int l = threadIdx.x;
+      const double lam = (l < A.n_levels && g[2 * l + 1] > 0.0) ? sqrt(g[2 * l] / g[2 * l + 1]) : 1.0;
+      A.ctl->omega[l] = 4.0 / (3.0 * (lam > 0.0 ? lam : 1.0));
+    }
+    if (threadIdx.x == 0) A.ctl->count = 0;
+  }
+}
+// dense inverse of the coarsest level (one CTA): assembled from its cell matrices, Gauss-Jordan
+// without pivoting (SPD on the live nodes; dead nodes get identity rows, zeroed afterwards)
+__global__ void __launch_bounds__(MG_NT) k_mgs_dense(MgsArgs A) {
+  __shared__ double M[MGS_DENSE_MAX * MGS_DENSE_MAX];
+  __shared__ double F[MGS_DENSE_MAX];
+  __shared__ int live[MGS_DENSE_MAX];
+  __shared__ int cn[MGS_DENSE_MAX][4];
+  __shared__ int ncell;
+  const int c = A.n_levels - 1;
+  const DMesh& m = A.L[c].m;
+  const int nd = m.n_nodes;
+  if (threadIdx.x == 0) {
+    int e = 0;
+    for (int cjr = 0; cjr < m.ny; ++cjr) {
+      const int4 er = __ldg(m.erow + cjr);
+      for (int cir = er.x; cir < er.y && e < MGS_DENSE_MAX; ++cir, ++e) {
+        cn[e][0] = mg_node(m, cir, cjr, true);
+        cn[e][1] = mg_node(m, cir + 1, cjr, true);
+        cn[e][2] = mg_node(m, cir + 1, cjr + 1, false);
+        cn[e][3] = mg_node(m, cir, cjr + 1, false);
+      }
+    }
+    ncell = e;
+  }
+  __syncthreads();
+  for (int ij = threadIdx.x; ij < nd * nd; ij += blockDim.x) {
+    const int i = ij / nd, j = ij % nd;
+    double s = 0.0;
+    for (int e = 0; e < ncell; ++e) {
+      int ka = -1, kb = -1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (cn[e][q] == i) ka = q;
+        if (cn[e][q] == j) kb = q;
+      }
+      if (ka >= 0 && kb >= 0) s += __ldcg(A.L[c].K + 16 * (size_t)e + ka * 4 + kb);
+    }
+    M[ij] = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) live[i] = M[i * nd + i] > 0.0;
+  __syncthreads();
+  for (int ij = threadIdx.x; ij < nd * nd; ij += blockDim.x) {
+    const int i = ij / nd, j = ij % nd;
+    if (!live[i] || !live[j]) M[ij] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int k = 0; k < nd; ++k) {
+    for (int i = threadIdx.x; i < nd; i += blockDim.x) F[i] = M[i * nd + k];
+    __syncthreads();
+    const double piv = F[k];
+    for (int j = threadIdx.x; j < nd; j += blockDim.x) M[k * nd + j] = (j == k ? 1.0 : M[k * nd + j]) / piv;
+    __syncthreads();
+    for (int ij = threadIdx.x; ij < nd * nd; ij += blockDim.x) {
+      const int i = ij / nd, j = ij % nd;
+      if (i != k) M[ij] = (j == k ? 0.0 : M[ij]) - F[i] * M[k * nd + j];
+    }
+    __syncthreads();
+  }
+  for (int ij = threadIdx.x; ij < nd * nd; ij += blockDim.x) {
+    const int i = ij / nd, j = ij % nd;
+    A.Ainv[ij] = (live[i] && live[j]) ? M[ij] : 0.0;
+  }
+}
+
+// ---- solve ------------------------------------------------------------------------------------
+// x0 = 0, r0 = b; ||b|| (scipy: rtol * ||b||); the last CTA sets the control block and the WHILE
+// condition
+__global__ void __launch_bounds__(MG_NT) k_mgs_init(MgsArgs A) {
+  __shared__ double red[MG_WARPS];
+  const MgIn* in = A.in;
+  double rr = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < A.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double rv = __ldcg(A.r + i);
+    A.x[i] = 0.0;
+    rr += rv * rv;
+  }
+  double v[1] = {rr};
+  if (mg_publish<1>(v, A.part, &A.ctl->count, red)) {
+    double tot[1];
+    mg_all_reduce<1>(A.part, gridDim.x, red, tot);
+    if (threadIdx.x == 0) {
+      MgCtl& c = *A.ctl;
+      c.count = 0;
+      c.rr = tot[0];
+      c.maxiter = in->maxiter;
+      c.target = in->target;
+      c.bnorm = sqrt(tot[0]);
+      c.atol = in->rtol * c.bnorm;
+      c.k = 0;
+      c.rho_prev = 0.0;
+      c.status = CG_CONVERGED;
+      c.done = (c.bnorm == 0.0 || sqrt(tot[0]) < c.atol) ? 1 : 0;
+      if (!c.done && c.maxiter <= 0) { c.done = 1; c.status = CG_MAXITER; }
+      if (A.use_cond) cudaGraphSetConditional(A.cond, c.done ? 0u : 1u);
+    }
+  }
+}
+
+#ifndef PFB_MGS_MINB
+#define PFB_MGS_MINB 3
+#endif
+__global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_fine_resid(MgsArgs A) {
+  __shared__ MgWarp ws[MG_WARPS];
+  const double om = __ldcg(&A.ctl->omega[0]);
+  SFineResid op{{&A.C, A.bq, A.L[0].dinv}, om, A.r, A.L[0].t};
+  const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
+  if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
+}
+
+__global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_fine_smooth(MgsArgs A) {
+  __shared__ MgWarp ws[MG_WARPS];
+  __shared__ double red[MG_WARPS];
+  const double om = __ldcg(&A.ctl->omega[0]);
+  double rz = 0.0;
+  SFineSmooth op{{&A.C, A.bq, A.L[0].dinv}, om, A.r, A.z, &A.L[0].m, &A.L[1].m, A.L[1].e, &rz};
+  const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
+  if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
+  double v[1] = {rz};
+  mg_block_sum<1>(v, red);
+  if (threadIdx.x == 0) A.part[blockIdx.x] = v[0];  // r.z partials, reduced by k_mgs_pcg
+}
+
+__global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_pcg(MgsArgs A, int n_rz) {
+  __shared__ MgWarp ws[MG_WARPS];
+  __shared__ double red[MG_WARPS];
+  double rho[1];
+  mg_all_reduce<1>(A.part, n_rz, red, rho);
+  const long long k = __ldcg(&A.ctl->k);
+  const bool first = k == 0;
+  double pq = 0.0;
+  SFinePcg op{{&A.C, A.bq, A.L[0].dinv}, first ? 0.0 : rho[0] / __ldcg(&A.ctl->rho_prev), A.z,
+              first ? nullptr : ((k & 1) ? A.p0 : A.p1), (k & 1) ? A.p1 : A.p0, A.q, &pq};
+  const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
+  if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
+  double v[1] = {pq};
+  mg_block_sum<1>(v, red);
+  if (threadIdx.x == 0) A.part[n_rz + blockIdx.x] = v[0];
+}
+
+__global__ void __launch_bounds__(MG_NT) k_mgs_update(MgsArgs A, int n_rz, int n_pq) {
+  __shared__ double red[MG_WARPS];
+  double rho[1], pq[1];
+  mg_all_reduce<1>(A.part, n_rz, red, rho);
+  mg_all_reduce<1>(A.part + n_rz, n_pq, red, pq);
+  const long long k = __ldcg(&A.ctl->k);
+  const double alpha = rho[0] / pq[0];
+  const double* p = (k & 1) ? A.p1 : A.p0;
+  double rr = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < A.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double pv = __ldcg(p + i), qv = __ldcg(A.q + i);
+    const double xv = __ldcg(A.x + i) + alpha * pv;
+    const double rv = __ldcg(A.r + i) - alpha * qv;
+    A.x[i] = xv;
+    A.r[i] = rv;
+    rr += rv * rv;
+  }
+  double* part = A.part + n_rz + n_pq;
+  double v[1] = {rr};
+  if (mg_publish<1>(v, part, &A.ctl->count, red)) {
+    double tot[1];
+    mg_all_reduce<1>(part, gridDim.x, red, tot);
+    if (threadIdx.x == 0) {
+      MgCtl& c = *A.ctl;
+      c.count = 0;
+      c.rr = tot[0];
+      c.rho_prev = rho[0];
+      c.k = k + 1;
+      const double rn = sqrt(tot[0]);
+      if (rn < c.atol) { c.done = 1; c.status = CG_CONVERGED; }
+      else if (!(rn == rn)) { c.done = 1; c.status = CG_NAN; }
+      else if (c.k >= c.maxiter) { c.done = 1; c.status = CG_MAXITER; }
+      if (A.use_cond) cudaGraphSetConditional(A.cond, c.done ? 0u : 1u);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(MG_NT) k_mgs_finish(MgsArgs A) {
+  const MgCtl& c = *A.ctl;
+  const int status = __ldcg(&c.status);
+  double* target = *(double* volatile*)&c.target;
+  if (target && status == CG_CONVERGED)
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < A.n;
+         i += (long long)gridDim.x * blockDim.x)
+      target[i] += __ldcg(A.x + i);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.result->iters = __ldcg(&c.k);
+    A.result->status = status;
+    A.result->bnorm = __ldcg(&c.bnorm);
+    A.result->rnorm = sqrt(__ldcg(&c.rr));
+  }
+}
+
+// ---- tail: levels [n_tail, n_levels) in shared memory, cycled by one CTA ---------------------
+struct STLevel {
+  int n;
+  const int *nbr, *rid, *pid;
+  const double *S, *dinv;
+  double *b, *t, *e;
+};
+__device__ __forceinline__ STLevel mgs_tl(const MgsArgs& A, int l) {
+  unsigned char* sm = mg_tail_smem;
+  const MgTailSlot& o = A.ts[l];
+  STLevel v;
+  v.n = A.L[l].m.n_nodes;
+  v.nbr = reinterpret_cast<const int*>(sm + o.nbr);
+  v.rid = reinterpret_cast<const int*>(sm + o.rid);
+  v.pid = reinterpret_cast<const int*>(sm + o.pid);
+  v.S = reinterpret_cast<const double*>(sm + o.S);
+  v.dinv = reinterpret_cast<const double*>(sm + o.dinv);
+  v.b = reinterpret_cast<double*>(sm + o.b);
+  v.t = reinterpret_cast<double*>(sm + o.t);
+  v.e = reinterpret_cast<double*>(sm + o.e);
+  return v;
+}
+template <class X>
+__device__ __forceinline__ double mgs_tapply(const STLevel& L, int id, X&& xval) {
+  const int q = threadIdx.x & 3, n = L.n;
+  double v = 0.0;
+  if (id < n) {
+#pragma unroll
+    for (int s2 = q; s2 < MG_NS; s2 += 4) {
+      const int k = L.nbr[s2 * n + id];
+      if (k >= 0) v += L.S[s2 * n + id] * xval(k);
+    }
+  }
+  return hw_sum1<4>(v);
+}
+
+__global__ void __launch_bounds__(MG_TAIL_NT) k_mgs_tail(MgsArgs A) {
+  const int nl = A.n_levels, l0 = A.n_tail, c = nl - 1;
+  const int q = threadIdx.x & 3;
+  const int nd = A.L[c].m.n_nodes;
+  double* Ainv = reinterpret_cast<double*>(mg_tail_smem + A.ts_ainv);
+  __shared__ __align__(8) unsigned long long bar;
+  if (threadIdx.x == 0) {
+    unsigned total = 0;
+    for (int l = l0; l < nl; ++l) {
+      const size_t n = A.L[l].m.n_nodes;
+      total += mg_r16(4 * MG_NS * n) + mg_r16(4 * 12 * n) + (l < c ? mg_r16(4 * 4 * n) : 0) +
+               mg_r16(8 * MG_NS * n) + mg_r16(8 * n);
+    }
+    if (A.dense) total += mg_r16(8 * (size_t)nd * nd);
+    mg_mbar_init_expect(&bar, total);
+    for (int l = l0; l < nl; ++l) {
+      const STLevel v = mgs_tl(A, l);
+      const MgsLevel& G = A.L[l];
+      const size_t n = v.n;
+      mg_bulk_g2s(v.nbr, G.nbr, mg_r16(4 * MG_NS * n), &bar);
+      mg_bulk_g2s(v.rid, G.rid, mg_r16(4 * 12 * n), &bar);
+      if (l < c) mg_bulk_g2s(v.pid, G.pid, mg_r16(4 * 4 * n), &bar);
+      mg_bulk_g2s(v.S, G.S, mg_r16(8 * MG_NS * n), &bar);
+      mg_bulk_g2s(v.dinv, G.dinv, mg_r16(8 * n), &bar);
+    }
+    if (A.dense) mg_bulk_g2s(Ainv, A.Ainv, mg_r16(8 * (size_t)nd * nd), &bar);
+  }
+  __shared__ double om_s[MG_MAXL];
+  if (threadIdx.x < MG_MAXL) om_s[threadIdx.x] = __ldcg(&A.ctl->omega[threadIdx.x]);
+  // restriction sources of level n_tail (global memory), loaded while the bulk copies fly
+  double tg[MGS_TAIL_P][3];
+  {
+    const MgsLevel& G0 = A.L[l0];
+    const int n0 = G0.m.n_nodes;
+    const double* tf = A.L[l0 - 1].t;
+#pragma unroll
+    for (int p = 0; p < MGS_TAIL_P; ++p)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int id = (threadIdx.x >> 2) + p * MG_TAIL_PASS, s2 = q + 4 * k;
+        const int f = (s2 < 12 && id < n0) ? __ldg(G0.rid + s2 * n0 + id) : -1;
+        tg[p][k] = f >= 0 ? __ldcg(tf + f) : 0.0;
+      }
+  }
+  __syncthreads();
+  mg_mbar_wait(&bar, 0);
+  for (int l = l0; l <= c; ++l) {
+    const STLevel v = mgs_tl(A, l);
+    const int n = v.n;
+    const double* tf = l == l0 ? nullptr : mgs_tl(A, l - 1).t;
+    int pass = 0;
+    MG_TAIL_NODES(n) {  // b = P^T t_f
+      double r = 0.0;
+      if (id < n) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int s2 = q + 4 * k;
+          if (s2 >= 12) break;
+          const int f = v.rid[s2 * n + id];
+          if (f < 0) continue;
+          double t = 0.0;
+          if (l == l0) {
+#pragma unroll
+            for (int p = 0; p < MGS_TAIL_P; ++p)
+              if (p == pass) t = tg[p][k];
+          } else {
+            t = tf[f];
+          }
+          r += mg_rw(s2) * t;
+        }
+      }
+      ++pass;
+      r = hw_sum1<4>(r);
+      if (q == 0 && id < n) v.b[id] = mgs_mask(r, v.dinv[id]);
+    }
+    __syncthreads();
+    if (l == c) break;
+    const double om = om_s[l];
+    MG_TAIL_NODES(n) {  // t = b - A (omega D^-1 b)
+      const double Av = mgs_tapply(v, id, [&](int k) -> double { return om * v.dinv[k] * v.b[k]; });
+      if (q == 0 && id < n) v.t[id] = mgs_mask(v.b[id] - Av, v.dinv[id]);
+    }
+    __syncthreads();
+  }
+  {  // coarsest solve
+    const STLevel v = mgs_tl(A, c);
+    if (A.dense) {
+      for (int i = threadIdx.x; i < nd; i += blockDim.x) {
+        double sacc = 0.0;
+        for (int j = 0; j < nd; ++j) sacc += Ainv[i * nd + j] * v.b[j];
+        v.e[i] = sacc;
+      }
+      __syncthreads();
+    } else {
+      const double om = om_s[c];
+      double* bufs[2] = {v.e, v.t};
+      int cur = (A.nu_c - 1) % 2 == 0 ? 0 : 1;
+      for (int i = threadIdx.x; i < nd; i += blockDim.x) bufs[cur][i] = om * v.dinv[i] * v.b[i];
+      __syncthreads();
+      for (int sw = 1; sw < A.nu_c; ++sw) {
+        const double* in = bufs[cur];
+        double* out = bufs[cur ^ 1];
+        MG_TAIL_NODES(v.n) {
+          const double Ax = mgs_tapply(v, id, [&](int k) -> double { return in[k]; });
+          if (q == 0 && id < v.n) out[id] = in[id] + om * v.dinv[id] * (v.b[id] - Ax);
+        }
+        cur ^= 1;
+        __syncthreads();
+      }
+    }
+    if (l0 == c)
+      for (int i = threadIdx.x; i < nd; i += blockDim.x) A.L[c].e[i] = v.e[i];
+  }
+  for (int l = c - 1; l >= l0; --l) {
+    const STLevel v = mgs_tl(A, l), vc = mgs_tl(A, l + 1);
+    const int n = v.n;
+    const double om = om_s[l];
+    MG_TAIL_NODES(n) {  // y = omega D^-1 b + P e_c (into t)
+      double r = 0.0, cnt = 0.0;
+      if (id < n) {
+        const int k = v.pid[q * n + id];
+        if (k >= 0) {
+          r = vc.e[k];
+          cnt = 1.0;
+        }
+      }
+      r = hw_sum1<4>(r);
+      cnt = hw_sum1<4>(cnt);
+      if (q == 0 && id < n) v.t[id] = mgs_mask(om * v.dinv[id] * v.b[id] + r / cnt, v.dinv[id]);
+    }
+    __syncthreads();
+    double* eout = (l == l0) ? A.L[l].e : v.e;
+    MG_TAIL_NODES(n) {  // e = y + omega D^-1 (b - A y)
+      const double Ay = mgs_tapply(v, id, [&](int k) -> double { return v.t[k]; });
+      if (q == 0 && id < n) eout[id] = v.t[id] + om * v.dinv[id] * (v.b[id] - Ay);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace pfb

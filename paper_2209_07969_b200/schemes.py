@@ -77,8 +77,9 @@ class SolverState:
     @classmethod
     def zeros(cls, disc) -> "SolverState":
         z = host_zeros  # page-locked where possible (assembly.host_zeros)
+        ne = disc.mesh.n_elems if disc.mesh is not None else disc.layout.n_elems
         return cls(u=z(disc.n_u_dofs), d=z(disc.n_d_dofs), d_prev=z(disc.n_d_dofs),
-                   gp=GaussPointState.zeros(disc.mesh.n_elems, disc.n_gp))
+                   gp=GaussPointState.zeros(ne, disc.n_gp))
 
 
 def _write_back(sess: DeviceSession, state) -> None:

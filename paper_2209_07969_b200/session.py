@@ -329,10 +329,32 @@ class DeviceSession:
     # -- benchmarking helpers ------------------------------------------------------------
     def bench_cg(self, physics: str, n_iter: int) -> tuple:
         """(ms, iterations) of a fixed-length PCG run at the current state (no convergence)."""
-        code = {"momentum": 0, "evolution": 1, "phase_field": 1, "momentum_mg": 2}[physics]
+        code = {"momentum": 0, "evolution": 1, "phase_field": 1, "momentum_mg": 2,
+                "phase_field_mg": 3}[physics]
         ms, it = C.c_double(), C.c_int64()
         self._check(self.lib.pf_bench_cg(self.h, code, int(n_iter), C.byref(ms), C.byref(it)))
         return ms.value, it.value
+
+    MG_KERNELS = {
+        0: "momentum fine residual march: r, D^-1 (16 B), d (8 B), t (16 B) per node + 1 B "
+           "branch bits per cell",
+        1: "momentum fine smoothing march: r, D^-1, d, z per node + level-1 correction (16 B per "
+           "coarse node) + 1 B per cell",
+        2: "momentum PCG-direction march: z, p_old, d, D^-1, p_new, q per node + 1 B per cell",
+        10: "phase-field fine residual march: r, D^-1, t (8 B) per node + b (32 B) per cell",
+        11: "phase-field fine smoothing march: r, D^-1, z (8 B) per node + level-1 correction "
+            "(8 B per coarse node) + b (32 B) per cell",
+        12: "phase-field PCG-direction march: z, p_old, D^-1, p_new, q (8 B) per node + b "
+            "(32 B) per cell",
+    }
+
+    def bench_mg_kernel(self, which: int, reps: int = 20) -> tuple:
+        """(ms per launch, algorithmic bytes per launch, byte accounting) of one fine-level
+        multigrid march on the current state (pf_bench_mg_kernel)."""
+        ms, nb = C.c_double(), C.c_double()
+        self._check(self.lib.pf_bench_mg_kernel(self.h, int(which), int(reps), C.byref(ms),
+                                                C.byref(nb)))
+        return ms.value, nb.value, self.MG_KERNELS[which]
 
     def mg_info(self, with_omega: bool = False) -> dict:
         """Multigrid hierarchy of the momentum PCG (n_levels 0: Jacobi PCG on this handle)."""
@@ -348,7 +370,8 @@ class DeviceSession:
         return out
 
     MOMENTUM_SOLVERS = ("jacobi_pcg", "single_reduction_pcg", "multigrid_pcg")
-    PHASE_FIELD_SOLVERS = ("jacobi_pcg", "single_reduction_pcg", "stencil_pcg", "multigrid_pcg")
+    PHASE_FIELD_SOLVERS = ("jacobi_pcg", "single_reduction_pcg", "stencil_pcg",
+                           "packed_multigrid_pcg", "multigrid_pcg")
 
     def solver_kinds(self) -> dict:
         """Linear solver of each Newton system (pf_solver_kinds)."""

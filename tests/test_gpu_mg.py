@@ -103,15 +103,16 @@ def test_mg_solve_accuracy_cracked_state(cuda_ok, monkeypatch):
     assert np.max(np.abs(u0 - u1)) <= 1e-8 * np.max(np.abs(u0))
 
 
+@pytest.mark.parametrize("kind", ["scalar", "packed"])
 @pytest.mark.parametrize("case_name,scheme,steps", [
     ("tension32", "ST", 18), ("shear32", "S1", 12), ("lpanel25", "ST", 12),
     ("multicrack32", "S1", 10)])
-def test_phase_field_mg_matches(cuda_ok, monkeypatch, case_name, scheme, steps):
-    """Phase-field solves without the SPD probe by the multigrid PCG (phys 1: the scalar field
-    as the x component of a two-component system; auto-enabled on large meshes, forced here)
-    against the Jacobi / single-reduction PCG: same per-step counts up to the crack step, the
-    reference's round-off band after it, fields to the linear-solve accuracy, fewer phase-field
-    PCG iterations."""
+def test_phase_field_mg_matches(cuda_ok, monkeypatch, case_name, scheme, steps, kind):
+    """Phase-field solves without the SPD probe by the multigrid PCG -- the native scalar
+    hierarchy (pf_mgs.cuh, the default on large meshes) and round 1's two-component packing
+    (pf_mg.cuh phys 1), forced here -- against the Jacobi / single-reduction PCG: same per-step
+    counts up to the crack step, the reference's round-off band after it, fields to the
+    linear-solve accuracy, fewer phase-field PCG iterations."""
     from conftest import stag_band
     from paper_2209_07969_b200.session import DeviceSession
 
@@ -119,10 +120,13 @@ def test_phase_field_mg_matches(cuda_ok, monkeypatch, case_name, scheme, steps):
     band = stag_band(case_name, scheme, steps)
     calm = int(np.argmax(band > 1)) if np.any(band > 1) else steps
     runs = []
-    for evo in ("0", "1"):
+    for evo in ("0", kind):
         monkeypatch.setenv("PFB200_MG_EVO", evo)
         pb = C.setup(case, C.b200_api())
         s = DeviceSession(pb.disc.layout, pb.params, pb.config, device=0)
+        if evo != "0":
+            want = "multigrid_pcg" if kind == "scalar" else "packed_multigrid_pcg"
+            assert s.solver_kinds()["phase_field"] == want
         s.push_state(pb.state)
         stats, snap = [], None
         for k in range(steps):
