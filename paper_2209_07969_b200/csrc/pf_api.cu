@@ -57,7 +57,11 @@ struct MgsInst {
   int gf = 1, gflat = 1;
   std::vector<int> gl, gn, lpn;
   pfb::MgIn* in = nullptr;
-  cudaGraphExec_t setup_exec = nullptr, solve_exec = nullptr;
+  // setup graphs: the first with MG_POW power steps from a hashed start, later ones with
+  // MGS_POW_WARM steps from the previous setup's normalised vectors (PFB200_MGS_POW_WARM)
+  cudaGraphExec_t setup_exec = nullptr, setup_warm_exec = nullptr, solve_exec = nullptr;
+  int pow_warm_steps = 2;
+  int setup_kernels_warm = 0;
   long long setups = 0;
   int setup_kernels = 0, body_kernels = 0;
   bool fuse = true;
@@ -300,6 +304,7 @@ extern "C" void pf_destroy(pf_handle* h) {
   }
   if (h->mgs.in) cudaFreeHost(h->mgs.in);
   if (h->mgs.setup_exec) cudaGraphExecDestroy(h->mgs.setup_exec);
+  if (h->mgs.setup_warm_exec) cudaGraphExecDestroy(h->mgs.setup_warm_exec);
   if (h->mgs.solve_exec) cudaGraphExecDestroy(h->mgs.solve_exec);
   if (h->stage) cudaFreeHost(h->stage);
   for (auto& row : h->graphs)
@@ -998,7 +1003,9 @@ static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
     if (l == 0) {
       dm = h->dm;
       ML.dinv = h->dinvd;
-      if (mg_alloc(h, &ML.t, (size_t)L.n_nodes) != cudaSuccess) return oom();
+      if (mg_alloc(h, &ML.t, (size_t)L.n_nodes) != cudaSuccess ||
+          mg_alloc(h, &ML.ev, (size_t)L.n_nodes) != cudaSuccess)
+        return oom();
       continue;
     }
     std::vector<int4> nrow(L.ny + 1), erow(L.ny);
@@ -1020,7 +1027,8 @@ static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
     const size_t n = L.n_nodes;
     if (mg_alloc(h, &ML.K, 16 * (size_t)L.n_elems) != cudaSuccess ||
         mg_alloc(h, &ML.dinv, n) != cudaSuccess || mg_alloc(h, &ML.b, n) != cudaSuccess ||
-        mg_alloc(h, &ML.e, n) != cudaSuccess || mg_alloc(h, &ML.t, n) != cudaSuccess)
+        mg_alloc(h, &ML.e, n) != cudaSuccess || mg_alloc(h, &ML.t, n) != cudaSuccess ||
+        mg_alloc(h, &ML.ev, n) != cudaSuccess)
       return oom();
     ML.items = pfb::mg_items(L.nx, L.ny, L.notch_row >= 0);
     M.gl[l] = (ML.items + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
@@ -1088,26 +1096,36 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
   pfb::MgsArgs& A = M.A;
   const int nl = A.n_levels;
   cudaStream_t s = h->stream;
-  {  // setup: Galerkin levels, stencils, dense coarsest inverse, power steps, omegas
+  const char* pw = getenv("PFB200_MGS_POW_WARM");
+  M.pow_warm_steps = pw ? std::max(0, std::min(pfb::MG_POW, atoi(pw))) : 2;
+  for (int warm = 0; warm < 2; ++warm) {
+    // setup: Galerkin levels, stencils, dense coarsest inverse, power steps, omegas; the warm
+    // variant starts the power steps from the previous setup's vectors (0 steps: cold only)
+    if (warm && M.pow_warm_steps == 0) break;
+    const int npow = warm ? M.pow_warm_steps : pfb::MG_POW;
+    pfb::MgsArgs B = A;
+    B.pow_warm = warm;
     cudaGraph_t g = nullptr;
     PF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     for (int lc = 1; lc < nl; ++lc) {
-      const long long cells = (long long)A.L[lc].m.nx * A.L[lc].m.ny;
+      const long long cells = (long long)B.L[lc].m.nx * B.L[lc].m.ny;
       const int gb = (int)std::max(1LL, std::min((cells + pfb::MG_NT - 1) / pfb::MG_NT,
                                                  64LL * h->sm_count));
-      pfb::k_mgs_galerkin<<<gb, pfb::MG_NT, 0, s>>>(A, lc);
-      pfb::k_mgs_stencil<<<M.gl[lc], pfb::MG_NT, 0, s>>>(A, lc);
+      pfb::k_mgs_galerkin<<<gb, pfb::MG_NT, 0, s>>>(B, lc);
+      pfb::k_mgs_stencil<<<M.gl[lc], pfb::MG_NT, 0, s>>>(B, lc);
     }
-    if (A.dense) pfb::k_mgs_dense<<<1, pfb::MG_NT, 0, s>>>(A);
-    const int cb = (A.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
-    for (int k = 1; k <= pfb::MG_POW; ++k)
-      pfb::k_mgs_pow<<<M.gf + cb, pfb::MG_NT, 0, s>>>(A, k, M.gf);
-    if (A.n_tail < nl) pfb::k_mgs_pow_tail<<<1, pfb::MG_TAIL_NT, 0, s>>>(A);
-    pfb::k_mgs_lambda<<<M.gflat, pfb::MG_NT, 0, s>>>(A);
-    M.setup_kernels = 2 * (nl - 1) + (A.dense ? 1 : 0) + pfb::MG_POW + (A.n_tail < nl ? 1 : 0) + 1;
+    if (B.dense) pfb::k_mgs_dense<<<1, pfb::MG_NT, 0, s>>>(B);
+    const int cb = (B.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
+    for (int k = 1; k <= npow; ++k)
+      pfb::k_mgs_pow<<<M.gf + cb, pfb::MG_NT, 0, s>>>(B, k, M.gf);
+    if (B.n_tail < nl) pfb::k_mgs_pow_tail<<<1, pfb::MG_TAIL_NT, 0, s>>>(B, npow);
+    pfb::k_mgs_lambda<<<M.gflat, pfb::MG_NT, 0, s>>>(B, npow);
+    pfb::k_mgs_evstore<<<4 * h->sm_count, pfb::MG_NT, 0, s>>>(B, npow);
+    const int nk = 2 * (nl - 1) + (B.dense ? 1 : 0) + npow + (B.n_tail < nl ? 1 : 0) + 2;
+    (warm ? M.setup_kernels_warm : M.setup_kernels) = nk;
     cudaError_t e = cudaStreamEndCapture(s, &g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MGS setup capture: ") + cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&M.setup_exec, g, 0);
+    e = cudaGraphInstantiate(warm ? &M.setup_warm_exec : &M.setup_exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MGS setup graph: ") + cudaGetErrorString(e));
   }
@@ -2279,7 +2297,8 @@ static pf_status run_mgs(pf_handle* h, MgsInst& M, int* status, long long* iters
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
   PF_CUDA(cudaMemcpyAsync((void*)M.A.in, M.in, sizeof(pfb::MgIn), cudaMemcpyHostToDevice,
                           h->stream));
-  PF_CUDA(cudaGraphLaunch(M.setup_exec, h->stream));
+  const bool warm = M.setups > 0 && M.setup_warm_exec;
+  PF_CUDA(cudaGraphLaunch(warm ? M.setup_warm_exec : M.setup_exec, h->stream));
   PF_TRY(launched(h));
   PF_CUDA(cudaGraphLaunch(M.solve_exec, h->stream));
   PF_TRY(launched(h));
@@ -2290,7 +2309,10 @@ static pf_status run_mgs(pf_handle* h, MgsInst& M, int* status, long long* iters
   M.setups += 1;
   *status = h->h_cgres->status;
   *iters = h->h_cgres->iters;
-  h->acc.launches += M.setup_kernels - 1 + 1 + (int)(*iters) * M.body_kernels + 1 - 1;
+  // kernels inside the two graphs (each graph launch was counted once by launched()):
+  // setup kernels, init, iterations x body, finish
+  h->acc.launches += (warm ? M.setup_kernels_warm : M.setup_kernels) - 1 + 2 +
+                     (int)(*iters) * M.body_kernels - 1;
   if (h->trace)
     fprintf(stderr, "[pfb200] scalar phase-field mg solve: %lld iterations, %.3f ms\n", *iters, ms);
   if (!check) return PF_OK;

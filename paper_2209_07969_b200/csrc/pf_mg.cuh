@@ -71,6 +71,7 @@ struct MgIn {  // per-solve inputs (device copy of a pinned host struct, refresh
 };
 struct MgCtl {
   double omega[MG_MAXL];
+  double evscale[MG_MAXL];  // 1 / ||v_last|| per level (warm-started power steps, pf_mgs.cuh)
   double* target;
   double rho_prev, bnorm, atol, rr;
   long long k, maxiter;
@@ -161,12 +162,16 @@ __device__ __forceinline__ double mg_q(int c, int k, int K) {
 
 // ----------------------------------------------------------------------------------------
 // Generic warp march (pf_march.cuh march_unit without the PCG specifics).  Op provides
-//   struct Raw; void fetch(int id, Raw&)                      the node's loads (id >= 0)
+//   struct Raw; void fetch(int id, int i, int j, bool dup, Raw&)  the node's loads (id >= 0)
 //   double2 finish(const Raw&, int id, int i, int j, bool dup, double& aux)  its input value
 //   double2 in(int id, int i, int j, bool dup, double& aux)  fetch + finish (zero, aux 0 for
 //                                                             id < 0)
-//   void cell(int eid, const double2 (&v)[4], const double (&a)[4], double2 (&f)[4])
+//   struct CRaw; void cfetch(int eid, CRaw&)                 the cell's own data (eid >= 0)
+//   void cellr(int eid, const CRaw&, const double2 (&v)[4], const double (&a)[4],
+//              double2 (&f)[4])                               the cell's contributions
 //   void out(int id, double2 Av, double2 vin)                 once per owned node
+// The cell data of the next cell row (branch bits / Newton coefficients) is fetched one row
+// step ahead like the node rows, so no dependent HBM load sits on a row step's critical path.
 template <class Op>
 __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int unit, Op& op,
                                          MgWarp& ws) {
@@ -222,7 +227,10 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
   // a row of loads in flight while it does the current row's FP64 work (Op::finish)
   typename Op::Raw w_hi;
   int id_hi = nid(r0);
-  if (id_hi >= 0) op.fetch(id_hi, w_hi);
+  if (id_hi >= 0) op.fetch(id_hi, col, r0, false, w_hi);
+  typename Op::CRaw c_cur;
+  int e_cur = cell_id(r0 - 1);
+  if (e_cur >= 0) op.cfetch(e_cur, c_cur);
   double2 acc_lo = make_double2(0.0, 0.0);
   for (int cj = r0 - 1; cj < r1; ++cj) {
     const int jh = cj + 1;
@@ -231,9 +239,12 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
                                     : make_double2(0.0, 0.0);
     typename Op::Raw w_nx;
     const int id_nx = (jh + 1 <= r1) ? nid(jh + 1) : -1;
-    if (id_nx >= 0) op.fetch(id_nx, w_nx);
+    if (id_nx >= 0) op.fetch(id_nx, col, jh + 1, false, w_nx);
     const bool hi_slit = (jh == R);
-    const int eid = cell_id(cj);
+    const int eid = e_cur;
+    typename Op::CRaw c_nx;
+    const int e_nx = (cj + 1 < r1) ? cell_id(cj + 1) : -1;
+    if (e_nx >= 0) op.cfetch(e_nx, c_nx);
     const bool use_dup = lo_slit && dupcol;
     const double2 b0 = use_dup ? ws.dv[lane] : v_lo;
     const double e0 = use_dup ? ws.da[lane] : a_lo;
@@ -244,7 +255,7 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
     if (eid >= 0) {
       const double2 v[4] = {b0, b1, t2, v_hi};
       const double a[4] = {e0, e1, e2, a_hi};
-      op.cell(eid, v, a, f);
+      op.cellr(eid, c_cur, v, a, f);
     }
     const double2 c1l = shfl_up(f[1]), c2l = shfl_up(f[2]);
     if (lane_own && cj >= r0) {
@@ -267,6 +278,8 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
     lo_slit = hi_slit;
     id_hi = id_nx;
     w_hi = w_nx;
+    e_cur = e_nx;
+    c_cur = c_nx;
   }
 }
 
@@ -280,13 +293,30 @@ struct FineBase {
   const double* dinv;
   int phys;
   const double* bq;
+  struct CRaw {
+    double2 b01, b23;
+    unsigned fl;
+  };
+  __device__ void cfetch(int eid, CRaw& c) const {
+    if (phys == 0) {
+      c.fl = __ldg(flags + eid);
+    } else {
+      c.b01 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid);
+      c.b23 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid + 1);
+    }
+  }
   __device__ void cell(int eid, const double2 (&v)[4], const double (&a)[4],
                        double2 (&f)[4]) const {
+    CRaw c;
+    cfetch(eid, c);
+    cellr(eid, c, v, a, f);
+  }
+  __device__ void cellr(int, const CRaw& c, const double2 (&v)[4], const double (&a)[4],
+                        double2 (&f)[4]) const {
     if (phys == 0) {
-      mom_cell_fast(*C, v, a, __ldg(flags + eid), f);
+      mom_cell_fast(*C, v, a, c.fl, f);
     } else {  // phase field (pf_cg.cuh evo_cell_apply) on the x components
-      const double2 b01 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid);
-      const double2 b23 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid + 1);
+      const double2 b01 = c.b01, b23 = c.b23;
       const double pc[4] = {v[0].x, v[1].x, v[2].x, v[3].x};
       const double bb[4] = {b01.x, b01.y, b23.x, b23.y};
       double fx[4];
@@ -310,7 +340,7 @@ struct FineResid : FineBase {  // x = omega D^-1 r (pre-smoothing from zero), t 
     double2 dv, bv;
     double d;
   };
-  __device__ void fetch(int id, Raw& w) const {
+  __device__ void fetch(int id, int, int, bool, Raw& w) const {
     w.dv = di(id);
     w.bv = d2ldcg(r, id);
     w.d = __ldg(d + id);
@@ -323,7 +353,7 @@ struct FineResid : FineBase {  // x = omega D^-1 r (pre-smoothing from zero), t 
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
     Raw w;
-    fetch(id, w);
+    fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2) const {
@@ -381,22 +411,41 @@ struct FineSmooth : FineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 
   struct Raw {
     double2 dv, bv;
     double d;
+    double2 pv[4];  // the level-1 corrections of the bilinear prolongation, fetched ahead
+    double pw;
+    unsigned live;
   };
-  __device__ void fetch(int id, Raw& w) const {
+  __device__ void fetch(int id, int i, int j, bool dup, Raw& w) const {
     w.dv = di(id);
     w.bv = d2ldcg(r, id);
     w.d = __ldg(d + id);
+    const DMesh& c = *mc;
+    const bool up = dup || (mf->notch_row >= 0 && j > mf->notch_row);
+    const int I0 = i >> 1, J0 = j >> 1, I1 = I0 + (i & 1), J1 = J0 + (j & 1);
+    w.pw = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
+    const int4 r0 = GMem::row(c.nrow, J0), r1 = GMem::row(c.nrow, min(J1, c.ny));
+    const int cc[4] = {mg_row_node(c, r0, I0, J0, up), mg_row_node(c, r0, I1, J0, up),
+                       mg_row_node(c, r1, I0, J1, up), mg_row_node(c, r1, I1, J1, up)};
+    w.live = (cc[0] >= 0 ? 1u : 0u) | ((cc[1] >= 0 && I1 != I0) ? 2u : 0u) |
+             ((cc[2] >= 0 && J1 != J0) ? 4u : 0u) |
+             ((cc[3] >= 0 && I1 != I0 && J1 != J0) ? 8u : 0u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w.pv[k] = GMem::v2(ec, max(cc[k], 0));
   }
-  __device__ double2 finish(const Raw& w, int, int i, int j, bool dup, double& aux) const {
+  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
     aux = w.d;
-    const double2 pe = mg_prolong<GMem>(*mf, *mc, ec, i, j, dup);
+    // same products and order as mg_prolong: a00 v00 + a10 v10 + a01 v01 + a11 v11
+    const double a0 = (w.live & 1u) ? w.pw : 0.0, a1 = (w.live & 2u) ? w.pw : 0.0;
+    const double a2 = (w.live & 4u) ? w.pw : 0.0, a3 = (w.live & 8u) ? w.pw : 0.0;
+    const double2 pe = make_double2(a0 * w.pv[0].x + a1 * w.pv[1].x + a2 * w.pv[2].x + a3 * w.pv[3].x,
+                                    a0 * w.pv[0].y + a1 * w.pv[1].y + a2 * w.pv[2].y + a3 * w.pv[3].y);
     return mask2(make_double2(om * w.dv.x * w.bv.x + pe.x, om * w.dv.y * w.bv.y + pe.y), w.dv);
   }
   __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
     Raw w;
-    fetch(id, w);
+    fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2 y) const {
@@ -419,7 +468,7 @@ struct FineWarm : FineBase {  // q_k = A u_k (masked); u_j.q_k (j <= k), u_k.b (
     double2 uv, dv;
     double d;
   };
-  __device__ void fetch(int id, Raw& w) const {
+  __device__ void fetch(int id, int, int, bool, Raw& w) const {
     w.uv = __ldg(reinterpret_cast<const double2*>(u) + id);
     w.dv = di(id);
     w.d = __ldg(d + id);
@@ -432,7 +481,7 @@ struct FineWarm : FineBase {  // q_k = A u_k (masked); u_j.q_k (j <= k), u_k.b (
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
     Raw w;
-    fetch(id, w);
+    fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2 uv) const {
@@ -462,7 +511,7 @@ struct FinePow : FineBase {  // power step vout = D^-1 A vin (vin == nullptr: ha
     double2 v, dv;
     double d;
   };
-  __device__ void fetch(int id, Raw& w) const {
+  __device__ void fetch(int id, int, int, bool, Raw& w) const {
     w.v = vin ? d2ldcg(vin, id) : make_double2(mg_hash01(2u * id + 1u), mg_hash01(2u * id + 2u));
     w.dv = di(id);
     w.d = __ldg(d + id);
@@ -475,7 +524,7 @@ struct FinePow : FineBase {  // power step vout = D^-1 A vin (vin == nullptr: ha
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
     Raw w;
-    fetch(id, w);
+    fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2) const {
@@ -495,7 +544,7 @@ struct FinePcg : FineBase {  // p = z + beta p_old (owner stores), q = A p (mask
     double2 zv, po;
     double d;
   };
-  __device__ void fetch(int id, Raw& w) const {
+  __device__ void fetch(int id, int, int, bool, Raw& w) const {
     w.zv = d2ldcg(z, id);
     w.po = pold ? d2ldcg(pold, id) : make_double2(0.0, 0.0);
     w.d = __ldg(d + id);
@@ -509,7 +558,7 @@ struct FinePcg : FineBase {  // p = z + beta p_old (owner stores), q = A p (mask
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
     Raw w;
-    fetch(id, w);
+    fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2 p) const {

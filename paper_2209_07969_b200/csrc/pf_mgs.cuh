@@ -40,6 +40,7 @@ struct MgsLevel {
   float* Sf;      // [MG_NS][n] FP32 stencil (grid levels)
   const int* rid; // [12][n] restriction sources on level l-1
   const int* pid; // [4][n] prolongation sources on level l+1
+  double* ev;     // [n] dominant-eigenvector estimate of D^-1 A (warm start of the power steps)
   int items, item_off, lpn, in_tail;
 };
 
@@ -49,6 +50,7 @@ struct MgsArgs {
   MgsLevel L[MG_MAXL];
   MarchGeom g0;
   int coarse_items;
+  int pow_warm;               // 1: power steps start from L[l].ev (the previous setup's vectors)
   const double* bq;           // level-0 Newton coefficient per Gauss point [n_elems][4]
   double *x, *r, *z, *p0, *p1, *q;
   double* Ainv;               // [nd*nd] dense inverse of the coarsest level
@@ -70,12 +72,17 @@ struct SFineBase {
   const Consts* C;
   const double* bq;
   const double* dinv;
-  __device__ void cell(int eid, const double2 (&v)[4], const double (&)[4],
-                       double2 (&f)[4]) const {
-    const double2 b01 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid);
-    const double2 b23 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid + 1);
+  struct CRaw {
+    double2 b01, b23;
+  };
+  __device__ void cfetch(int eid, CRaw& c) const {  // one row step ahead (mg_march)
+    c.b01 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid);
+    c.b23 = __ldg(reinterpret_cast<const double2*>(bq) + 2 * eid + 1);
+  }
+  __device__ void cellr(int, const CRaw& c, const double2 (&v)[4], const double (&)[4],
+                        double2 (&f)[4]) const {
     const double pc[4] = {v[0].x, v[1].x, v[2].x, v[3].x};
-    const double bb[4] = {b01.x, b01.y, b23.x, b23.y};
+    const double bb[4] = {c.b01.x, c.b01.y, c.b23.x, c.b23.y};
     double fx[4];
     evo_cell_apply(*C, pc, bb, fx);
 #pragma unroll
@@ -91,7 +98,7 @@ struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), 
   struct Raw {
     double dv, bv;
   };
-  __device__ void fetch(int id, Raw& w) const {
+  __device__ void fetch(int id, int, int, bool, Raw& w) const {
     w.dv = di(id);
     w.bv = __ldg(r + id);
   }
@@ -103,7 +110,7 @@ struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), 
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
     Raw w;
-    fetch(id, w);
+    fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2) const {
@@ -111,22 +118,30 @@ struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), 
   }
 };
 
-// prolongation (P e_{l+1}) at node (i, j) of level l; dup = upper-face slit node
-__device__ __forceinline__ double mgs_prolong(const DMesh& mf, const DMesh& mc, const double* ec,
-                                              int i, int j, bool dup) {
+// prolongation (P e_{l+1}) at node (i, j) of level l, split into its loads (issued one row step
+// ahead by the march) and the weighted sum; dup = upper-face slit node
+struct ProlongRaw {
+  double v[4];
+  double w;
+  unsigned live;  // bit k: corner k exists and is distinct
+};
+__device__ __forceinline__ void mgs_prolong_fetch(const DMesh& mf, const DMesh& mc,
+                                                  const double* ec, int i, int j, bool dup,
+                                                  ProlongRaw& p) {
   const bool up = dup || (mf.notch_row >= 0 && j > mf.notch_row);
   const int I0 = i >> 1, J0 = j >> 1, I1 = I0 + (i & 1), J1 = J0 + (j & 1);
-  const double w = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
+  p.w = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
   const int4 r0 = __ldg(mc.nrow + J0), r1 = __ldg(mc.nrow + min(J1, mc.ny));
-  const int c00 = mg_row_node(mc, r0, I0, J0, up), c10 = mg_row_node(mc, r0, I1, J0, up);
-  const int c01 = mg_row_node(mc, r1, I0, J1, up), c11 = mg_row_node(mc, r1, I1, J1, up);
-  const double v00 = __ldg(ec + max(c00, 0)), v10 = __ldg(ec + max(c10, 0));
-  const double v01 = __ldg(ec + max(c01, 0)), v11 = __ldg(ec + max(c11, 0));
-  const double a00 = c00 >= 0 ? w : 0.0;
-  const double a10 = (c10 >= 0 && I1 != I0) ? w : 0.0;
-  const double a01 = (c01 >= 0 && J1 != J0) ? w : 0.0;
-  const double a11 = (c11 >= 0 && I1 != I0 && J1 != J0) ? w : 0.0;
-  return a00 * v00 + a10 * v10 + a01 * v01 + a11 * v11;
+  const int c[4] = {mg_row_node(mc, r0, I0, J0, up), mg_row_node(mc, r0, I1, J0, up),
+                    mg_row_node(mc, r1, I0, J1, up), mg_row_node(mc, r1, I1, J1, up)};
+  p.live = (c[0] >= 0 ? 1u : 0u) | ((c[1] >= 0 && I1 != I0) ? 2u : 0u) |
+           ((c[2] >= 0 && J1 != J0) ? 4u : 0u) | ((c[3] >= 0 && I1 != I0 && J1 != J0) ? 8u : 0u);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) p.v[k] = __ldg(ec + max(c[k], 0));
+}
+__device__ __forceinline__ double mgs_prolong_sum(const ProlongRaw& p) {
+  return ((p.live & 1u) ? p.w : 0.0) * p.v[0] + ((p.live & 2u) ? p.w : 0.0) * p.v[1] +
+         ((p.live & 4u) ? p.w : 0.0) * p.v[2] + ((p.live & 8u) ? p.w : 0.0) * p.v[3];
 }
 
 struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 (r - A y); r.z
@@ -139,21 +154,23 @@ struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-
   double* rz;
   struct Raw {
     double dv, bv;
+    ProlongRaw pr;
   };
-  __device__ void fetch(int id, Raw& w) const {
+  __device__ void fetch(int id, int i, int j, bool dup, Raw& w) const {
     w.dv = di(id);
     w.bv = __ldg(r + id);
+    mgs_prolong_fetch(*mf, *mc, ec, i, j, dup, w.pr);
   }
-  __device__ double2 finish(const Raw& w, int, int i, int j, bool dup, double& aux) const {
+  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
     aux = 0.0;
-    const double pe = mgs_prolong(*mf, *mc, ec, i, j, dup);
+    const double pe = mgs_prolong_sum(w.pr);
     return make_double2(mgs_mask(om * w.dv * w.bv + pe, w.dv), 0.0);
   }
   __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
     Raw w;
-    fetch(id, w);
+    fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2 y) const {
@@ -170,7 +187,7 @@ struct SFinePow : SFineBase {  // power step vout = D^-1 A vin (vin == nullptr: 
   struct Raw {
     double v, dv;
   };
-  __device__ void fetch(int id, Raw& w) const {
+  __device__ void fetch(int id, int, int, bool, Raw& w) const {
     w.v = vin ? __ldg(vin + id) : mg_hash01(2u * id + 1u);
     w.dv = di(id);
   }
@@ -182,7 +199,7 @@ struct SFinePow : SFineBase {  // power step vout = D^-1 A vin (vin == nullptr: 
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
     Raw w;
-    fetch(id, w);
+    fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2) const { vout[id] = di(id) * Av.x; }
@@ -198,7 +215,7 @@ struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (ma
   struct Raw {
     double zv, po;
   };
-  __device__ void fetch(int id, Raw& w) const {
+  __device__ void fetch(int id, int, int, bool, Raw& w) const {
     w.zv = __ldg(z + id);
     w.po = pold ? __ldg(pold + id) : 0.0;
   }
@@ -210,7 +227,7 @@ struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (ma
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
     Raw w;
-    fetch(id, w);
+    fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2 p) const {
@@ -568,7 +585,7 @@ __global__ void __launch_bounds__(MG_NT, 3) k_mgs_pow(MgsArgs A, int step, int f
   __shared__ MgWarp ws[MG_WARPS];
   const int warp = threadIdx.x >> 5;
   auto vin = [&](const MgsLevel& L) -> const double* {
-    return step == 1 ? nullptr : (((step - 1) & 1) ? L.t : L.e);
+    return step == 1 ? (A.pow_warm ? L.ev : nullptr) : (((step - 1) & 1) ? L.t : L.e);
   };
   auto vout = [&](const MgsLevel& L) -> double* { return (step & 1) ? L.t : L.e; };
   if ((int)blockIdx.x < fine_blocks) {
@@ -588,12 +605,13 @@ __global__ void __launch_bounds__(MG_NT, 3) k_mgs_pow(MgsArgs A, int step, int f
   else mgs_spow<1>(L, vin(L), vout(L), q);
 }
 // power steps of the tail levels (FP64 stencils), one CTA, all MG_POW steps
-__global__ void __launch_bounds__(MG_TAIL_NT) k_mgs_pow_tail(MgsArgs A) {
-  for (int step = 1; step <= MG_POW; ++step) {
+__global__ void __launch_bounds__(MG_TAIL_NT) k_mgs_pow_tail(MgsArgs A, int npow) {
+  for (int step = 1; step <= npow; ++step) {
     for (int l = A.n_tail; l < A.n_levels; ++l) {
       const MgsLevel& L = A.L[l];
       const int n = L.m.n_nodes;
-      const double* vin = step == 1 ? nullptr : (((step - 1) & 1) ? L.t : L.e);
+      const double* vin = step == 1 ? (A.pow_warm ? L.ev : nullptr)
+                                    : (((step - 1) & 1) ? L.t : L.e);
       double* vout = (step & 1) ? L.t : L.e;
       for (int id = threadIdx.x; id < n; id += blockDim.x) {
         double acc = 0.0;
@@ -609,8 +627,9 @@ __global__ void __launch_bounds__(MG_TAIL_NT) k_mgs_pow_tail(MgsArgs A) {
     __syncthreads();
   }
 }
-// omega_l = 4 / (3 lambda_l), lambda_l = ||v_POW|| / ||v_POW-1|| (per-level partials)
-__global__ void __launch_bounds__(MG_NT) k_mgs_lambda(MgsArgs A) {
+// omega_l = 4 / (3 lambda_l), lambda_l = ||v_npow|| / ||v_npow-1|| (per-level partials);
+// evscale_l = 1 / ||v_npow|| for k_mgs_evstore
+__global__ void __launch_bounds__(MG_NT) k_mgs_lambda(MgsArgs A, int npow) {
   __shared__ double red[MG_WARPS * 2 * MG_MAXL];
   double v[2 * MG_MAXL];
 #pragma unroll
@@ -620,8 +639,8 @@ __global__ void __launch_bounds__(MG_NT) k_mgs_lambda(MgsArgs A) {
 #pragma unroll
   for (int l = 0; l < MG_MAXL; ++l) {
     if (l >= A.n_levels) break;
-    const double* a1 = (MG_POW & 1) ? A.L[l].t : A.L[l].e;
-    const double* a0 = (MG_POW & 1) ? A.L[l].e : A.L[l].t;
+    const double* a1 = (npow & 1) ? A.L[l].t : A.L[l].e;
+    const double* a0 = (npow & 1) ? A.L[l].e : A.L[l].t;
     const long long n = A.L[l].m.n_nodes;
     for (long long i = tid; i < n; i += nth) {
       const double x1 = __ldcg(a1 + i), x0 = __ldcg(a0 + i);
@@ -636,8 +655,20 @@ __global__ void __launch_bounds__(MG_NT) k_mgs_lambda(MgsArgs A) {
       const int l = threadIdx.x;
       const double lam = (l < A.n_levels && g[2 * l + 1] > 0.0) ? sqrt(g[2 * l] / g[2 * l + 1]) : 1.0;
       A.ctl->omega[l] = 4.0 / (3.0 * (lam > 0.0 ? lam : 1.0));
+      A.ctl->evscale[l] = g[2 * l] > 0.0 ? 1.0 / sqrt(g[2 * l]) : 0.0;
     }
     if (threadIdx.x == 0) A.ctl->count = 0;
+  }
+}
+// keep the normalised last power vector of every level as the next setup's start vector
+__global__ void __launch_bounds__(MG_NT) k_mgs_evstore(MgsArgs A, int npow) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  for (int l = 0; l < A.n_levels; ++l) {
+    const double* v = (npow & 1) ? A.L[l].t : A.L[l].e;
+    const double sc = __ldcg(&A.ctl->evscale[l]);
+    double* ev = A.L[l].ev;
+    for (long long i = tid; i < A.L[l].m.n_nodes; i += nth) ev[i] = sc * __ldcg(v + i);
   }
 }
 // dense inverse of the coarsest level (one CTA): assembled from its cell matrices, Gauss-Jordan

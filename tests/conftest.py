@@ -128,6 +128,39 @@ def stag_band(case: str, scheme: str, n_steps: int, run_file: str | None = None)
     return band
 
 
+def exact_geometry_ensemble(case: str, scheme: str) -> dict:
+    """The reference algorithm's round-off ensemble restricted to exact uniform-cell geometry
+    (tests/golden/sens_<case>_<scheme>_exact_part*.json, make_sensitivity.py "exact:a:b"): the
+    Jacobians / B matrices from the exact cell size, as the device path evaluates them (DESIGN.md
+    section 4), instead of from node coordinates.  {variant: per-step n_stag}."""
+    import glob
+
+    out = {}
+    for path in sorted(glob.glob(os.path.join(GOLDEN, f"sens_{case}_{scheme}_exact_part*.json"))):
+        with open(path) as f:
+            out.update(json.load(f)["n_stag"])
+    return out
+
+
+def stag_window(case: str, scheme: str, n_steps: int, run_file: str | None = None) -> tuple:
+    """Per-step allowed [lo, hi] of n_stag.  Default: the reference's count +- stag_band.  At
+    round-off-chaotic crack steps of cases with an exact-geometry ensemble, the window is that
+    ensemble's range +- 2: the reference evaluates cell geometry from node coordinates, and that
+    1e-16 spatially varying perturbation alone shifts the crack-step count (cfg1 ST: 298-299 with
+    coordinates, 303-312 with exact geometry, the device's 305-311), so the
+    device is compared with the population that evaluates the same arithmetic."""
+    z = np.load(os.path.join(GOLDEN, run_file or f"run_{case}_{scheme}.npz"))
+    ref = z["table"][:n_steps, 1].astype(int)
+    band = stag_band(case, scheme, n_steps, run_file)
+    lo, hi = ref - band, ref + band
+    ex = exact_geometry_ensemble(case, scheme)
+    for i in range(n_steps):
+        vals = [int(v[i]) for v in ex.values() if len(v) > i]
+        if band[i] > 1 and vals:
+            lo[i], hi[i] = min(vals) - 2, max(vals) + 2
+    return lo, hi
+
+
 KAT_MESHES = ("notched8", "notched12x6", "plain10", "lshape", "notched16", "notched80x16",
               "lshape12p5")
 

@@ -8,7 +8,7 @@ reaction force within 1e-6 of the peak force, phase field within 1e-6 in L-infin
 import numpy as np
 import pytest
 
-from conftest import golden, golden_meta, mirror_perm, rel_err, stag_band
+from conftest import golden, golden_meta, mirror_perm, rel_err, stag_band, stag_window
 from paper_2209_07969_b200 import configs as C
 
 pytestmark = pytest.mark.gpu
@@ -41,12 +41,14 @@ def check_against_golden(recs, z, state, case, scheme, mesh, fcol=7, run_file=No
     tab = z["table"]
     assert len(recs) == len(tab)
     band = stag_band(case, scheme, len(tab), run_file)
+    lo, hi = stag_window(case, scheme, len(tab), run_file)
     fpeak = np.abs(tab[:, fcol]).max()
-    for r, row, b in zip(recs, tab, band):
+    for r, row, b, wl, wh in zip(recs, tab, band, lo, hi):
         ref_stag, ref_nu, ref_nd, ref_fb = (int(x) for x in row[1:5])
         d_stag = abs(r.n_stag - ref_stag)
         d_force = abs(r.reactions[0] - row[fcol]) / fpeak
-        assert d_stag <= b, f"step {r.step}: n_stag {r.n_stag} vs reference {ref_stag} (band {b})"
+        assert wl <= r.n_stag <= wh, (
+            f"step {r.step}: n_stag {r.n_stag} vs reference {ref_stag} (window [{wl}, {wh}])")
         assert d_force <= 1e-6, f"step {r.step}: force {r.reactions[0]} vs {row[fcol]}"
         got = (r.n_nr_u, r.n_nr_d, r.spd_fallbacks)
         want = (ref_nu, ref_nd, ref_fb)
