@@ -74,3 +74,47 @@ def bar_problem(api, at_model: str, n_cells: int = 32):
 def bar_bcs(nodes, inc: float):
     left, right, every = nodes
     return [(2 * every + 1, 0.0), (2 * left, 0.0), (2 * right, inc)]
+
+
+# ---------------------------------------------------------------------------------------------
+# Localizing bar: SPEC.md Appendix C / acceptance #1
+LOC_E, LOC_GC, LOC_L, LOC_CELLS = 1.0, 0.1, 0.01, 100
+LOC_SEED, LOC_U0, LOC_INC = 0.6, 1.0, 0.01
+
+
+def localizing_bar_problem(api):
+    """The Appendix C bar on any API namespace: a 100-cell Q4 strip of length 1 (cells
+    0.01 x 0.5), E = 1, nu = 0 (so psi+ = E eps^2 / 2, the 1-D energy), G_c = 0.1, l = 0.01,
+    AT2, u_y = 0 everywhere, u_x = 0 at x = 0.  The imperfection that makes the crack localize
+    at a definite place is an initial damage d = d_prev = 0.6 on the mid-length node column
+    (the reference has no spatially varying material; an initial damage field is how it takes
+    an imperfection, like config 5's pre-cracks).  Returns (disc, state, params, config, nodes,
+    mesh)."""
+    mesh = api.build_notched_square(LOC_CELLS, 2, 1.0, notch_from_left_to_center=False)
+    disc = api.Discretization(mesh)
+    params = api.MaterialParams.from_young_poisson(LOC_E, 0.0, g_c=LOC_GC, length_l=LOC_L,
+                                                   at_model="AT2")
+    config = api.SolverConfig(tol_st=1.0e-5)
+    state = api.SolverState.zeros(disc)
+    x = np.asarray(mesh.nodes)[:, 0]
+    mid = np.flatnonzero(np.abs(x - 0.5) < 1e-9)
+    state.d[mid] = LOC_SEED
+    state.d_prev[mid] = LOC_SEED
+    left = np.flatnonzero(np.abs(x) < 1e-12)
+    right = np.flatnonzero(np.abs(x - 1.0) < 1e-12)
+    every = np.arange(np.asarray(mesh.nodes).shape[0], dtype=np.int64)
+    return disc, state, params, config, (left, right, every), mesh
+
+
+def run_localizing_bar(api, scheme: str, max_steps: int = 120):
+    """Load steps u(1) = LOC_U0, then +LOC_INC per step, until the crack has formed (max d >
+    0.95).  Returns (per-step n_stag, index of the crack step, final d)."""
+    disc, state, params, config, nodes, mesh = localizing_bar_problem(api)
+    counts = []
+    for k in range(max_steps):
+        bcs = bar_bcs(nodes, LOC_U0 if k == 0 else LOC_INC)
+        st = api.staggered_step(disc, state, api.SchemeKind(scheme), bcs, params, config)
+        counts.append(int(st.n_stag))
+        if float(np.max(state.d)) > 0.95:
+            return counts, k, np.asarray(state.d).copy()
+    raise RuntimeError("the bar did not crack")

@@ -8,6 +8,7 @@ box; the fixtures it writes are committed and travel instead):
     OMP_NUM_THREADS=1 python tests/golden/make_golden.py run cfg1 S1 --snap 10,40,60,64,65
     OMP_NUM_THREADS=1 python tests/golden/make_golden.py run cfg2 ST --steps 2
     OMP_NUM_THREADS=1 python tests/golden/make_golden.py spd tension16 S1
+    OMP_NUM_THREADS=1 python tests/golden/make_golden.py bar
 
 Outputs (``tests/golden/``):
   * ``kat_<mesh>.npz``   — seeded random states and the reference's assembled residuals,
@@ -254,6 +255,24 @@ def spd(case_name: str, scheme: str, max_each: int) -> None:
     print("wrote", path, counter, flush=True)
 
 
+def bar() -> None:
+    """The localizing bar of SPEC.md Appendix C (oracle/bar_analytic.py) on the unmodified
+    reference: per-step staggered counts and the final phase field per scheme."""
+    from oracle import bar_analytic as B
+
+    api = C.reference_api(REF_SRC)
+    out = {}
+    for scheme in ("ST", "S1", "S3"):
+        counts, k, d = B.run_localizing_bar(api, scheme)
+        out[f"{scheme}_n_stag"] = np.array(counts)
+        out[f"{scheme}_crack_step"] = np.array(k)
+        out[f"{scheme}_d"] = d
+        print("bar", scheme, "crack step", k, "n_stag", counts[k], flush=True)
+    path = os.path.join(HERE, "bar_localizing.npz")
+    np.savez_compressed(path, **out)
+    print("wrote", path)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -269,6 +288,7 @@ def main() -> None:
     r.add_argument("--state-snap", default="")
     r.add_argument("--restart", default=None)
     r.add_argument("--tag", default="")
+    sub.add_parser("bar")
     s = sub.add_parser("spd")
     s.add_argument("case")
     s.add_argument("scheme")
@@ -277,6 +297,8 @@ def main() -> None:
     t0 = time.time()
     if a.cmd == "kat":
         kat(a.only)
+    elif a.cmd == "bar":
+        bar()
     elif a.cmd == "run":
         snaps = [int(x) for x in a.snap.split(",") if x]
         run(a.case, a.scheme, a.steps, snaps, a.lin, a.partial,

@@ -1,7 +1,9 @@
-"""The 1-D bar oracle: a strip under uniform uniaxial strain whose
+"""The 1-D bar oracle.  (1) A strip under uniform uniaxial strain whose
 staggered fixed point has a closed form per load step (oracle/bar_analytic.py), for AT1 (elastic
 phase, then damage) and AT2.  The CPU oracle and the B200 path must both reproduce it: the
-phase field stays uniform and equals the closed form after every load step."""
+phase field stays uniform and equals the closed form after every load step.  (2) The
+localizing bar of SPEC.md Appendix C (acceptance #1): the staggered-iteration counts at the
+crack step, ST against the fast schemes."""
 
 import numpy as np
 import pytest
@@ -48,3 +50,51 @@ def test_b200_bar_matches_closed_form(cuda_ok, at_model, scheme):
 
     got, want, params = _run(C.b200_api(), at_model, scheme)
     _check(got, want, params, at_model)
+
+
+# ---- the localizing bar (SPEC.md Appendix C, acceptance #1: SPEC.md:522) ------
+def _check_localizing(res):
+    """The crack forms within one load step; at that step ST needs 15..35 staggered iterations
+    (paper: 25) and the fast schemes 10..24 (paper: 17), strictly fewer than ST."""
+    (st_counts, st_k, _), fast = res["ST"], [res[s] for s in ("S1", "S3")]
+    n_st = st_counts[st_k]
+    assert 15 <= n_st <= 35, st_counts
+    for counts, k, _ in fast:
+        assert abs(k - st_k) <= 1, (k, st_k)  # same load step (+-1)
+        assert 10 <= counts[k] <= 24, counts
+        assert counts[k] < n_st, (counts[k], n_st)
+
+
+def test_oracle_localizing_bar():
+    """The oracle reproduces the unmodified reference's bar (tests/golden/bar_localizing.npz,
+    make_golden.py bar: ST 23, S1 17, S3 16 staggered iterations at the crack step 40) and
+    meets the acceptance bands."""
+    from conftest import golden
+    from oracle.phasefield_oracle import oracle_api
+
+    api = oracle_api()
+    res = {s: B.run_localizing_bar(api, s) for s in ("ST", "S1", "S3")}
+    _check_localizing(res)
+    z = golden("bar_localizing.npz")
+    for s, (counts, k, d) in res.items():
+        assert counts == z[f"{s}_n_stag"].tolist() and k == int(z[f"{s}_crack_step"])
+        assert np.abs(d - z[f"{s}_d"]).max() <= 1e-9
+
+
+@pytest.mark.gpu
+def test_b200_localizing_bar(cuda_ok):
+    from oracle.phasefield_oracle import oracle_api
+    from paper_2209_07969_b200 import configs as C
+
+    from conftest import golden
+
+    res = {s: B.run_localizing_bar(C.b200_api(), s) for s in ("ST", "S1", "S3")}
+    _check_localizing(res)
+    # against the unmodified reference's run: the same crack step, the same localized phase
+    # field, staggered counts within +-1 per step
+    z = golden("bar_localizing.npz")
+    for s, (counts, k, d) in res.items():
+        assert k == int(z[f"{s}_crack_step"])
+        ref = z[f"{s}_n_stag"]
+        assert len(counts) == len(ref) and np.abs(np.array(counts) - ref).max() <= 1, (s, counts)
+        assert np.abs(d - z[f"{s}_d"]).max() <= 1e-6
