@@ -400,6 +400,68 @@ __device__ __forceinline__ double2 mg_prolong(const DMesh& mf, const DMesh& mc,
                       a00 * v00.y + a10 * v10.y + a01 * v01.y + a11 * v11.y);
 }
 
+// The bilinear prolongation of a fine-level march: a lane keeps its fine column i, so its
+// coarse sources are the fixed columns I0 = i/2, I1 = I0 + (i odd) of coarse rows J0 = j/2,
+// J1 = J0 + (j odd).  Two coarse rows are cached per lane (keyed by row and slit face): each
+// coarse row is loaded once per two fine rows, in fetch (one row step ahead of its use in
+// finish; fetch(j+1) always follows finish(j)), instead of four row-table lookups and four
+// gathers per fine node.
+template <class V>
+struct ProlongCache {
+  int aJ = -0x4000, bJ = -0x4000;
+  bool aUp = false, bUp = false;
+  V a0, a1, b0, b1;
+  __device__ static V zero();
+  __device__ static V load(const double* e, int c);
+  __device__ void fill(const DMesh& mc, const double* ec, int J, bool up, int I0, int I1,
+                       V& v0, V& v1) {
+    const int4 rw = __ldg(mc.nrow + J);
+    const int c0 = mg_row_node(mc, rw, I0, J, up);
+    const int c1 = I1 != I0 ? mg_row_node(mc, rw, I1, J, up) : -1;
+    v0 = c0 >= 0 ? load(ec, c0) : zero();
+    v1 = c1 >= 0 ? load(ec, c1) : zero();
+  }
+  __device__ bool has(int J, bool up) const {
+    return (aJ == J && aUp == up) || (bJ == J && bUp == up);
+  }
+  // make rows (J0, up) and (J1, up) resident
+  __device__ void need(const DMesh& mc, const double* ec, int I0, int I1, int J0, int J1,
+                       bool up) {
+    if (!has(J0, up)) {
+      const bool keep_a = aJ == J1 && aUp == up;  // slot a holds the other needed row
+      if (keep_a) { bJ = J0; bUp = up; fill(mc, ec, J0, up, I0, I1, b0, b1); }
+      else { aJ = J0; aUp = up; fill(mc, ec, J0, up, I0, I1, a0, a1); }
+    }
+    if (!has(J1, up)) {
+      const bool keep_a = aJ == J0 && aUp == up;
+      if (keep_a) { bJ = J1; bUp = up; fill(mc, ec, J1, up, I0, I1, b0, b1); }
+      else { aJ = J1; aUp = up; fill(mc, ec, J1, up, I0, I1, a0, a1); }
+    }
+  }
+  __device__ void get(int J, bool up, V& v0, V& v1) const {
+    const bool in_a = aJ == J && aUp == up;
+    v0 = in_a ? a0 : b0;
+    v1 = in_a ? a1 : b1;
+  }
+};
+template <> __device__ __forceinline__ double ProlongCache<double>::zero() { return 0.0; }
+template <> __device__ __forceinline__ double ProlongCache<double>::load(const double* e, int c) {
+  return __ldg(e + c);
+}
+template <> __device__ __forceinline__ double2 ProlongCache<double2>::zero() {
+  return make_double2(0.0, 0.0);
+}
+template <> __device__ __forceinline__ double2 ProlongCache<double2>::load(const double* e, int c) {
+  return __ldg(reinterpret_cast<const double2*>(e) + c);
+}
+// fine row j of a node (dup: upper slit face) -> coarse rows and face of its sources
+__device__ __forceinline__ void prolong_rows(const DMesh& mf, int j, bool dup, int& J0, int& J1,
+                                             bool& up) {
+  up = dup || (mf.notch_row >= 0 && j > mf.notch_row);
+  J0 = j >> 1;
+  J1 = J0 + (j & 1);
+}
+
 struct FineSmooth : FineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 (r - A y); r.z
   double om;
   const double* r;

@@ -102,9 +102,11 @@ struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), 
     w.dv = di(id);
     w.bv = __ldg(r + id);
   }
+  // the march carries (value, node datum) pairs; the scalar field leaves the y lane free, so
+  // it brings each node's own residual (NaN at masked nodes) from fetch to out: no reload there
   __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
     aux = 0.0;
-    return make_double2(om * w.dv * w.bv, 0.0);
+    return make_double2(om * w.dv * w.bv, w.dv != 0.0 ? w.bv : __longlong_as_double(~0LL));
   }
   __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
@@ -113,36 +115,10 @@ struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), 
     fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
-  __device__ void out(int id, double2 Av, double2) const {
-    t[id] = mgs_mask(__ldg(r + id) - Av.x, di(id));
+  __device__ void out(int id, double2 Av, double2 v) const {
+    t[id] = v.y == v.y ? v.y - Av.x : 0.0;
   }
 };
-
-// prolongation (P e_{l+1}) at node (i, j) of level l, split into its loads (issued one row step
-// ahead by the march) and the weighted sum; dup = upper-face slit node
-struct ProlongRaw {
-  double v[4];
-  double w;
-  unsigned live;  // bit k: corner k exists and is distinct
-};
-__device__ __forceinline__ void mgs_prolong_fetch(const DMesh& mf, const DMesh& mc,
-                                                  const double* ec, int i, int j, bool dup,
-                                                  ProlongRaw& p) {
-  const bool up = dup || (mf.notch_row >= 0 && j > mf.notch_row);
-  const int I0 = i >> 1, J0 = j >> 1, I1 = I0 + (i & 1), J1 = J0 + (j & 1);
-  p.w = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
-  const int4 r0 = __ldg(mc.nrow + J0), r1 = __ldg(mc.nrow + min(J1, mc.ny));
-  const int c[4] = {mg_row_node(mc, r0, I0, J0, up), mg_row_node(mc, r0, I1, J0, up),
-                    mg_row_node(mc, r1, I0, J1, up), mg_row_node(mc, r1, I1, J1, up)};
-  p.live = (c[0] >= 0 ? 1u : 0u) | ((c[1] >= 0 && I1 != I0) ? 2u : 0u) |
-           ((c[2] >= 0 && J1 != J0) ? 4u : 0u) | ((c[3] >= 0 && I1 != I0 && J1 != J0) ? 8u : 0u);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) p.v[k] = __ldg(ec + max(c[k], 0));
-}
-__device__ __forceinline__ double mgs_prolong_sum(const ProlongRaw& p) {
-  return ((p.live & 1u) ? p.w : 0.0) * p.v[0] + ((p.live & 2u) ? p.w : 0.0) * p.v[1] +
-         ((p.live & 4u) ? p.w : 0.0) * p.v[2] + ((p.live & 8u) ? p.w : 0.0) * p.v[3];
-}
 
 struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 (r - A y); r.z
   double om;
@@ -152,19 +128,31 @@ struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-
   const DMesh* mc;
   const double* ec;
   double* rz;
+  mutable ProlongCache<double> pc;  // coarse sources of the bilinear prolongation (pf_mg.cuh)
   struct Raw {
     double dv, bv;
-    ProlongRaw pr;
   };
   __device__ void fetch(int id, int i, int j, bool dup, Raw& w) const {
     w.dv = di(id);
     w.bv = __ldg(r + id);
-    mgs_prolong_fetch(*mf, *mc, ec, i, j, dup, w.pr);
+    int J0, J1;
+    bool up;
+    prolong_rows(*mf, j, dup, J0, J1, up);
+    pc.need(*mc, ec, i >> 1, (i >> 1) + (i & 1), J0, J1, up);
   }
-  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
+  __device__ double2 finish(const Raw& w, int, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
-    const double pe = mgs_prolong_sum(w.pr);
-    return make_double2(mgs_mask(om * w.dv * w.bv + pe, w.dv), 0.0);
+    int J0, J1;
+    bool up;
+    prolong_rows(*mf, j, dup, J0, J1, up);
+    double v00, v10, v01, v11;
+    pc.get(J0, up, v00, v10);
+    pc.get(J1, up, v01, v11);
+    const double w0 = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
+    const double a10 = (i & 1) ? w0 : 0.0, a01 = (j & 1) ? w0 : 0.0;
+    const double a11 = ((i & 1) && (j & 1)) ? w0 : 0.0;
+    const double pe = w0 * v00 + a10 * v10 + a01 * v01 + a11 * v11;
+    return make_double2(mgs_mask(om * w.dv * w.bv + pe, w.dv), om * w.dv);  // y, omega D^-1
   }
   __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
@@ -174,8 +162,8 @@ struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-
     return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2 y) const {
-    const double dv = di(id), bv = __ldg(r + id);
-    const double ev = y.x + om * dv * (bv - Av.x);
+    const double bv = __ldg(r + id);
+    const double ev = y.x + y.y * (bv - Av.x);
     z[id] = ev;
     *rz += bv * ev;
   }
@@ -193,7 +181,7 @@ struct SFinePow : SFineBase {  // power step vout = D^-1 A vin (vin == nullptr: 
   }
   __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
     aux = 0.0;
-    return make_double2(mgs_mask(w.v, w.dv), 0.0);
+    return make_double2(mgs_mask(w.v, w.dv), w.dv);
   }
   __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
@@ -202,7 +190,7 @@ struct SFinePow : SFineBase {  // power step vout = D^-1 A vin (vin == nullptr: 
     fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
-  __device__ void out(int id, double2 Av, double2) const { vout[id] = di(id) * Av.x; }
+  __device__ void out(int id, double2 Av, double2 v) const { vout[id] = v.y * Av.x; }
 };
 
 struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (masked), p.q
@@ -213,15 +201,16 @@ struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (ma
   double* q;
   double* pq;
   struct Raw {
-    double zv, po;
+    double zv, po, dv;
   };
   __device__ void fetch(int id, int, int, bool, Raw& w) const {
     w.zv = __ldg(z + id);
     w.po = pold ? __ldg(pold + id) : 0.0;
+    w.dv = di(id);
   }
   __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
     aux = 0.0;
-    return make_double2(pold ? w.zv + beta * w.po : w.zv, 0.0);
+    return make_double2(pold ? w.zv + beta * w.po : w.zv, w.dv);  // p, D^-1 (the mask)
   }
   __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
@@ -231,7 +220,7 @@ struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (ma
     return finish(w, id, i, j, dup, aux);
   }
   __device__ void out(int id, double2 Av, double2 p) const {
-    const double qv = mgs_mask(Av.x, di(id));
+    const double qv = mgs_mask(Av.x, p.y);
     pnew[id] = p.x;
     q[id] = qv;
     *pq += p.x * qv;
@@ -787,7 +776,7 @@ __global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_fine_smooth(MgsArgs
   __shared__ double red[MG_WARPS];
   const double om = __ldcg(&A.ctl->omega[0]);
   double rz = 0.0;
-  SFineSmooth op{{&A.C, A.bq, A.L[0].dinv}, om, A.r, A.z, &A.L[0].m, &A.L[1].m, A.L[1].e, &rz};
+  SFineSmooth op{{&A.C, A.bq, A.L[0].dinv}, om, A.r, A.z, &A.L[0].m, &A.L[1].m, A.L[1].e, &rz, {}};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
   double v[1] = {rz};
