@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", "pf_api.cu")]
 DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in (
-    "pf_device.cuh", "pf_kernels.cuh", "pf_cg.cuh", "pf_march.cuh", "pf_mg.cuh", "pf_mgs.cuh", "pf_st.cuh",
+    "pf_device.cuh", "pf_kernels.cuh", "pf_cg.cuh", "pf_march.cuh", "pf_mg.cuh", "pf_mgs.cuh", "pf_mgd.cuh", "pf_st.cuh",
     "pf_comm.h")] + [
     os.path.join(ROOT, "include", "pf_b200.h")]
 OUT = os.path.join(HERE, "libpfb200.so")

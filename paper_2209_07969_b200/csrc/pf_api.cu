@@ -46,6 +46,8 @@ struct MgInst {
   long long setups = 0;
   int setup_kernels = 0, body_kernels = 0;  // kernel nodes per graph (launch accounting)
   bool fuse = true;  // fused down / up kernels on the half-warp levels (PFB200_MG_FUSE=0: off)
+  cudaGraphExec_t vcycle_exec = nullptr;  // row strips: one V-cycle z = M^-1 r (pf_mgd.cuh)
+  int vcycle_kernels = 0;
 };
 
 // The native scalar phase-field multigrid PCG (pf_mgs.cuh): hierarchy rebuilt at every solve
@@ -62,6 +64,8 @@ struct MgsInst {
   cudaGraphExec_t setup_exec = nullptr, setup_warm_exec = nullptr, solve_exec = nullptr;
   int pow_warm_steps = 2;
   int setup_kernels_warm = 0;
+  cudaGraphExec_t vcycle_exec = nullptr;  // row strips: one V-cycle z = M^-1 r (pf_mgd.cuh)
+  int vcycle_kernels = 0;
   long long setups = 0;
   int setup_kernels = 0, body_kernels = 0;
   bool fuse = true;
@@ -162,6 +166,14 @@ struct pf_handle {
   // geometric-multigrid PCG instances (momentum; phase field on large meshes)
   MgInst mgu, mgd;
   MgsInst mgs;  // scalar phase-field multigrid (default for the phase field on large meshes)
+  // row strips: the multigrid PCG with strip-local V-cycles (pf_mgd.cuh).  The hierarchies live
+  // on the sub-mesh of the owned node rows (local rows mgd_row0 ..), the ghost row above masked.
+  int mgd_row0 = 0;
+  double* d_mgd = nullptr;      // [8] all-reduced scalars (pfb::MGD_*)
+  double* h_mgd = nullptr;      // pinned copy of r.r
+  double* mgd_part = nullptr;   // per-CTA partials
+  int mgd_gflat = 1, mgd_gdir_u = 1, mgd_gdir_d = 1;
+  pfb::MarchGeom mgd_geom_u{}, mgd_geom_d{};
   std::vector<void*> mg_allocs;
   // cached masks
   std::vector<int64_t> cons_key, pins_key;
@@ -301,7 +313,12 @@ extern "C" void pf_destroy(pf_handle* h) {
     if (M->in) cudaFreeHost(M->in);
     if (M->setup_exec) cudaGraphExecDestroy(M->setup_exec);
     if (M->solve_exec) cudaGraphExecDestroy(M->solve_exec);
+    if (M->vcycle_exec) cudaGraphExecDestroy(M->vcycle_exec);
   }
+  if (h->mgs.vcycle_exec) cudaGraphExecDestroy(h->mgs.vcycle_exec);
+  if (h->d_mgd) cudaFree(h->d_mgd);
+  if (h->h_mgd) cudaFreeHost(h->h_mgd);
+  if (h->mgd_part) cudaFree(h->mgd_part);
   if (h->mgs.in) cudaFreeHost(h->mgs.in);
   if (h->mgs.setup_exec) cudaGraphExecDestroy(h->mgs.setup_exec);
   if (h->mgs.setup_warm_exec) cudaGraphExecDestroy(h->mgs.setup_warm_exec);
@@ -538,6 +555,38 @@ static cudaError_t mg_alloc(pf_handle* h, T** p, size_t n) {
 
 static pf_status mg_build_graphs(pf_handle* h, MgInst& M);
 
+// Level 0 of a multigrid hierarchy: the whole mesh on one GPU; on a row strip the sub-mesh of
+// the owned node rows (local rows mgd_row0 .. ny: the ghost row below and its cell row are left
+// out, the ghost row above is masked by the V-cycle's inverse diagonal).  Node and cell ids stay
+// the strip's local ids, so the hierarchy reads and writes the strip's own vectors.
+static HostLevel hl_level0(const pf_handle* h) {
+  const int rb = h->comm ? h->mgd_row0 : 0;
+  HostLevel f;
+  f.nx = h->nx; f.ny = h->ny - rb;
+  f.nlo.assign(h->h_nlo.begin() + rb, h->h_nlo.end());
+  f.nhi.assign(h->h_nhi.begin() + rb, h->h_nhi.end());
+  f.nst.assign(h->h_nst.begin() + rb, h->h_nst.end());
+  f.elo.assign(h->h_elo.begin() + rb, h->h_elo.end());
+  f.ehi.assign(h->h_ehi.begin() + rb, h->h_ehi.end());
+  f.est.assign(h->h_est.begin() + rb, h->h_est.end());
+  f.notch_row = h->dm.notch_row >= 0 ? h->dm.notch_row - rb : -1;
+  f.notch_lo = h->dm.notch_lo; f.notch_hi = h->dm.notch_hi;
+  f.dup_start = h->dm.dup_start; f.n_nodes = h->n_nodes;
+  f.n_elems = 0;
+  for (int j = 0; j < f.ny; ++j) f.n_elems += f.ehi[j] - f.elo[j];
+  return f;
+}
+static pfb::DMesh dm_level0(const pf_handle* h) {
+  const int rb = h->comm ? h->mgd_row0 : 0;
+  pfb::DMesh m = h->dm;
+  if (rb == 0) return m;
+  m.ny -= rb;
+  m.nrow += rb; m.erow += rb;
+  m.nlo += rb; m.nhi += rb; m.nst += rb; m.elo += rb; m.ehi += rb; m.est += rb;
+  if (m.notch_row >= 0) m.notch_row -= rb;
+  return m;
+}
+
 static HostLevel hl_fine(const pf_handle* h) {
   HostLevel f;
   f.nx = h->nx; f.ny = h->ny;
@@ -600,7 +649,7 @@ static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_w
   const int tail_nodes = tl ? std::max(0, atoi(tl)) : 1 << 30;
   const char* nc = getenv("PFB200_MG_NUC");
   const int nu_c = nc ? std::max(1, atoi(nc)) : 16;
-  std::vector<HostLevel> lv(1, hl_fine(h));
+  std::vector<HostLevel> lv(1, hl_level0(h));
   while ((int)lv.size() < pfb::MG_MAXL && 2 * lv.back().n_nodes > pfb::MG_DENSE_MAX) {
     HostLevel c;
     if (!mg_coarsen(lv.back(), c)) break;
@@ -666,7 +715,7 @@ static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_w
     pfb::MgLevel& ML = A.L[l];
     pfb::DMesh& dm = ML.m;
     if (l == 0) {
-      dm = h->dm;
+      dm = dm_level0(h);
     } else {
       std::vector<int4> nrow(L.ny + 1), erow(L.ny);
       for (int j = 0; j <= L.ny; ++j) nrow[j] = make_int4(L.nlo[j], L.nhi[j], L.nst[j], 0);
@@ -728,13 +777,15 @@ static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_w
     if (mg_alloc(h, &ML.t, 2 * (size_t)L.n_nodes) != cudaSuccess) return oom();
   }
   A.coarse_items = coarse_items;
-  A.g0 = pfb::make_march_geom(h->nx, h->ny, fine_resident_warps);
+  A.g0 = pfb::make_march_geom(h->nx, lv[0].ny, fine_resident_warps);
   M.gf = (A.g0.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
   M.gflat = 2 * h->sm_count;
   if (mg_alloc(h, &A.z, 2 * (size_t)h->n_nodes) != cudaSuccess) return oom();
   A.phys = phys;
   for (int l = 0; l < nl; ++l) A.L[l].scalar = phys == 1 ? 1 : 0;
-  if (phys == 0) {
+  if (phys == 0 && h->comm) {  // strips: the V-cycle's own inverse diagonal, ghost rows masked
+    if (mg_alloc(h, &A.L[0].dinv, 2 * (size_t)h->n_nodes) != cudaSuccess) return oom();
+  } else if (phys == 0) {
     A.L[0].dinv = h->dinvu;
   } else {  // phase field: scalar vectors packed as (value, 0) per node (y dofs dead)
     double* dinv2 = nullptr;
@@ -812,7 +863,7 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
     else if (M.lpn[l] == 4) pfb::K<4><<<M.gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__); \
     else pfb::K<1><<<M.gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__);                     \
   } while (0)
-  auto body_kernels = [&](const pfb::MgArgs& B) {
+  auto body_kernels = [&](const pfb::MgArgs& B, bool krylov = true) {
     const int c = nl - 1, top = std::min(B.n_tail, c);  // grid levels [1, top)
     pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(B);
     for (int l = 1; l < top; ++l) {
@@ -849,6 +900,7 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
       }
     }
     pfb::k_mg_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(B);
+    if (!krylov) return;
     pfb::k_mg_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(B, M.gf);
     pfb::k_mg_update<<<M.gflat, pfb::MG_NT, 0, s>>>(B, M.gf, M.gf);
   };
@@ -856,6 +908,18 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
     const int c = nl - 1, top = std::min(A.n_tail, c);
     M.body_kernels = 1 + 3 + (A.n_tail < nl ? 1 : 1 + (A.dense ? 1 : A.nu_c));
     for (int l = 1; l < top; ++l) M.body_kernels += (M.lpn[l] == 16 && M.fuse) ? (A.L[l].m.n_nodes <= 8192 ? 2 : 3) : 4;
+  }
+  if (h->comm) {  // row strips: the preconditioner only, one V-cycle (pf_mgd.cuh drives the PCG)
+    cudaGraph_t g = nullptr;
+    A.use_cond = 0;
+    PF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    body_kernels(A, false);
+    PF_CUDA(cudaStreamEndCapture(s, &g));
+    cudaError_t e = cudaGraphInstantiate(&M.vcycle_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG V-cycle graph: ") + cudaGetErrorString(e));
+    M.vcycle_kernels = M.body_kernels - 2;
+    return PF_OK;
   }
   const char* un = getenv("PFB200_MG_UNROLL");
   const int unroll = un ? std::max(0, atoi(un)) : 0;
@@ -935,7 +999,7 @@ static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
   M.fuse = !(fz && std::string(fz) == "0");
   const char* nc = getenv("PFB200_MG_NUC");
   const int nu_c = nc ? std::max(1, atoi(nc)) : 16;
-  std::vector<HostLevel> lv(1, hl_fine(h));
+  std::vector<HostLevel> lv(1, hl_level0(h));
   while ((int)lv.size() < pfb::MG_MAXL && lv.back().n_nodes > pfb::MGS_DENSE_MAX) {
     HostLevel c;
     if (!mg_coarsen(lv.back(), c)) break;
@@ -1001,8 +1065,9 @@ static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
     pfb::MgsLevel& ML = A.L[l];
     pfb::DMesh& dm = ML.m;
     if (l == 0) {
-      dm = h->dm;
+      dm = dm_level0(h);
       ML.dinv = h->dinvd;
+      if (h->comm && mg_alloc(h, &ML.dinv, (size_t)L.n_nodes) != cudaSuccess) return oom();
       if (mg_alloc(h, &ML.t, (size_t)L.n_nodes) != cudaSuccess ||
           mg_alloc(h, &ML.ev, (size_t)L.n_nodes) != cudaSuccess)
         return oom();
@@ -1061,7 +1126,7 @@ static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
     }
   }
   A.coarse_items = coarse_items;
-  A.g0 = pfb::make_march_geom(h->nx, h->ny, fine_resident_warps);
+  A.g0 = pfb::make_march_geom(h->nx, lv[0].ny, fine_resident_warps);
   M.gf = (A.g0.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
   M.gflat = 2 * h->sm_count;
   const size_t nn = h->n_nodes;
@@ -1136,7 +1201,7 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
     else pfb::K<1><<<M.gn[l], pfb::MG_NT, 0, s>>>(__VA_ARGS__);                     \
   } while (0)
   const int c = nl - 1, top = std::min(A.n_tail, c);
-  auto body_kernels = [&](const pfb::MgsArgs& B) {
+  auto body_kernels = [&](const pfb::MgsArgs& B, bool krylov = true) {
     pfb::k_mgs_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(B);
     for (int l = 1; l < top; ++l) {
       if (M.lpn[l] == 16 && M.fuse && B.L[l].m.n_nodes <= 8192) {
@@ -1169,12 +1234,25 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
       }
     }
     pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(B);
+    if (!krylov) return;
     pfb::k_mgs_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(B, M.gf);
     pfb::k_mgs_update<<<M.gflat, pfb::MG_NT, 0, s>>>(B, M.gf, M.gf);
   };
   M.body_kernels = 4 + (A.n_tail < nl ? 1 : 1 + (A.dense ? 1 : A.nu_c));
   for (int l = 1; l < top; ++l)
     M.body_kernels += (M.lpn[l] == 16 && M.fuse) ? (A.L[l].m.n_nodes <= 8192 ? 2 : 3) : 4;
+  if (h->comm) {  // row strips: the preconditioner only, one V-cycle (pf_mgd.cuh drives the PCG)
+    cudaGraph_t g = nullptr;
+    A.use_cond = 0;
+    PF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    body_kernels(A, false);
+    PF_CUDA(cudaStreamEndCapture(s, &g));
+    cudaError_t e = cudaGraphInstantiate(&M.vcycle_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MGS V-cycle graph: ") + cudaGetErrorString(e));
+    M.vcycle_kernels = M.body_kernels - 2;
+    return PF_OK;
+  }
   const char* un = getenv("PFB200_MG_UNROLL");
   const int unroll = un ? std::max(0, atoi(un)) : 0;
   if (unroll > 0) {  // profiling only: N unconditional iterations, so ncu sees every kernel
@@ -1539,7 +1617,15 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
   CREATE_CUDA(cudaHostGetDevicePointer((void**)&h->d_scal, h->h_scal, 0));
   {  // geometric-multigrid PCG for the momentum solves (single GPU; PFB200_MG=0: Jacobi PCG)
     const char* mgv = getenv("PFB200_MG");
-    const bool want = !(mgv && std::string(mgv) == "0") && !strip;
+    // row strips: strip-local V-cycles as a block-Jacobi preconditioner (pf_mgd.cuh;
+    // PFB200_DIST_MG=0: the split-phase Jacobi PCG)
+    const char* dmg = getenv("PFB200_DIST_MG");
+    const bool dist_mg = !(dmg && std::string(dmg) == "0");
+    const bool want = !(mgv && std::string(mgv) == "0") && (!strip || dist_mg);
+    if (strip) {  // level 0 of the strip hierarchies: the first owned node row onwards
+      for (int j = 0; j <= ny; ++j)
+        if (h->h_nst[j] == (int)strip->own_lo) { h->mgd_row0 = j; break; }
+    }
     if (want) {
       int om = 0, o2 = 0;
       CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, pfb::k_mg_fine_smooth, pfb::MG_NT, 0));
@@ -1569,6 +1655,21 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
           os = std::max(1, std::min(os, o3));
           pf_status es = mgs_setup(h, h->mgs, os * dev_sms * pfb::MG_WARPS);
           if (es != PF_OK) return bail(es);
+        }
+        if (strip && (h->mgu.on || h->mgs.on)) {  // the strip PCG's scalars, partials, marches
+          CREATE_CUDA(cudaMalloc((void**)&h->d_mgd, 8 * sizeof(double)));
+          CREATE_CUDA(cudaMemset(h->d_mgd, 0, 8 * sizeof(double)));
+          CREATE_CUDA(cudaMallocHost((void**)&h->h_mgd, 8 * sizeof(double)));
+          int ou = 0, od = 0;
+          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ou, pfb::k_mgd_dir_mom, pfb::MG_NT, 0));
+          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&od, pfb::k_mgd_dir_pf, pfb::MG_NT, 0));
+          h->mgd_geom_u = pfb::make_march_geom(nx, ny, std::max(1, ou) * dev_sms * pfb::MG_WARPS);
+          h->mgd_geom_d = pfb::make_march_geom(nx, ny, std::max(1, od) * dev_sms * pfb::MG_WARPS);
+          h->mgd_gdir_u = (h->mgd_geom_u.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+          h->mgd_gdir_d = (h->mgd_geom_d.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+          h->mgd_gflat = 2 * dev_sms;
+          const int np = std::max({h->mgd_gflat, h->mgd_gdir_u, h->mgd_gdir_d});
+          CREATE_CUDA(cudaMalloc((void**)&h->mgd_part, np * sizeof(double)));
         }
         const char* mw = getenv("PFB200_MG_WARM");  // "0": MG solves start cold (x0 = 0)
         if (h->mgu.on && mw && std::string(mw) == "0") h->warm = false;
@@ -2320,8 +2421,100 @@ static pf_status run_mgs(pf_handle* h, MgsInst& M, int* status, long long* iters
   return cg_status(h, *status, *iters);
 }
 
+// The multigrid PCG on a row strip (pf_mgd.cuh): local V-cycles as a block-Jacobi
+// preconditioner, the Krylov recurrence with NCCL (or host-group) all-reduces and halo rows;
+// x ends up in xu / xd (ghost rows to be refreshed by the caller's halo exchange).
+static pf_status run_mgd(pf_handle* h, bool mom, int* status, long long* iters) {
+  const int comps = mom ? 2 : 1;
+  cudaStream_t s = h->stream;
+  double* g = h->d_mgd;
+  double* r = mom ? h->ru : h->rd;
+  double* x = mom ? h->xu : h->xd;
+  double* q = mom ? h->qu : h->qd;
+  double* p0 = mom ? h->p0u : h->p0d;
+  double* p1 = mom ? h->p1u : h->p1d;
+  const double* dinv = mom ? h->dinvu : h->dinvd;
+  double* vdinv = mom ? h->mgu.A.L[0].dinv : h->mgs.A.L[0].dinv;
+  double* z = mom ? h->mgu.A.z : h->mgs.A.z;
+  const double* rzpart = mom ? h->mgu.A.part : h->mgs.A.part;
+  const int n_rz = mom ? h->mgu.gf : h->mgs.gf;
+  const int gfl = h->mgd_gflat;
+  PF_CUDA(cudaEventRecord(h->ev0, s));
+  pfb::k_mgd_mask<<<gfl, 256, 0, s>>>(vdinv, dinv, comps, h->dm);
+  if (mom) {
+    PF_CUDA(cudaGraphLaunch(h->mgu.setup_exec, s));
+    h->acc.launches += h->mgu.setup_kernels;
+    h->mgu.setups += 1;
+  } else {
+    MgsInst& M = h->mgs;
+    const bool warm = M.setups > 0 && M.setup_warm_exec;
+    PF_CUDA(cudaGraphLaunch(warm ? M.setup_warm_exec : M.setup_exec, s));
+    h->acc.launches += warm ? M.setup_kernels_warm : M.setup_kernels;
+    M.setups += 1;
+  }
+  pfb::k_mgd_init<<<gfl, pfb::MG_NT, 0, s>>>(x, r, comps, h->dm, h->mgd_part);
+  pfb::k_finalize<<<1, 256, 0, s>>>(h->mgd_part, gfl, 1, g + pfb::MGD_RR);
+  h->acc.launches += 3;
+  PF_TRY(comm_check(h, h->comm->allreduce(g + pfb::MGD_RR, 1, s)));
+  PF_CUDA(cudaMemcpyAsync(h->h_mgd, g + pfb::MGD_RR, sizeof(double), cudaMemcpyDeviceToHost, s));
+  PF_CUDA(cudaStreamSynchronize(s));
+  const double bnorm = std::sqrt(h->h_mgd[0]);
+  const double atol = h->cfg.cg_rtol * bnorm;
+  const long long maxiter = (long long)h->cfg.cg_maxiter_factor * comps * h->n_nodes *
+                            std::max(1, h->comm->spec.nranks);
+  long long k = 0;
+  int st = pfb::CG_CONVERGED;
+  if (bnorm > 0.0 && !(bnorm < atol)) {
+    const pfb::MarchGeom& gd = mom ? h->mgd_geom_u : h->mgd_geom_d;
+    const int gdir = mom ? h->mgd_gdir_u : h->mgd_gdir_d;
+    for (k = 0;; ++k) {
+      PF_CUDA(cudaGraphLaunch(mom ? h->mgu.vcycle_exec : h->mgs.vcycle_exec, s));  // z = M^-1 r
+      if (k > 0) pfb::k_mgd_shift<<<1, 1, 0, s>>>(g);
+      pfb::k_finalize<<<1, 256, 0, s>>>(rzpart, n_rz, 1, g + pfb::MGD_RZ);
+      PF_TRY(comm_check(h, h->comm->allreduce(g + pfb::MGD_RZ, 1, s)));
+      PF_TRY(halo(h, z, comps));
+      const double* pold = (k & 1) ? p0 : p1;
+      double* pnew = (k & 1) ? p1 : p0;
+      if (mom)
+        pfb::k_mgd_dir_mom<<<gdir, pfb::MG_NT, 0, s>>>(h->mgu.A, h->dm, gd, dinv, g, k == 0, pold,
+                                                        pnew, h->mgd_part);
+      else
+        pfb::k_mgd_dir_pf<<<gdir, pfb::MG_NT, 0, s>>>(h->mgs.A, h->dm, gd, dinv, g, k == 0, pold,
+                                                       pnew, h->mgd_part);
+      pfb::k_finalize<<<1, 256, 0, s>>>(h->mgd_part, gdir, 1, g + pfb::MGD_PQ);
+      PF_TRY(comm_check(h, h->comm->allreduce(g + pfb::MGD_PQ, 1, s)));
+      pfb::k_mgd_update<<<gfl, pfb::MG_NT, 0, s>>>(x, r, pnew, q, comps, h->dm, g, h->mgd_part);
+      pfb::k_finalize<<<1, 256, 0, s>>>(h->mgd_part, gfl, 1, g + pfb::MGD_RR);
+      PF_TRY(comm_check(h, h->comm->allreduce(g + pfb::MGD_RR, 1, s)));
+      PF_CUDA(cudaMemcpyAsync(h->h_mgd, g + pfb::MGD_RR, sizeof(double), cudaMemcpyDeviceToHost, s));
+      PF_CUDA(cudaStreamSynchronize(s));
+      PF_CUDA(cudaGetLastError());
+      h->acc.launches += (mom ? h->mgu.vcycle_kernels : h->mgs.vcycle_kernels) + 6 + (k > 0);
+      const double rn = std::sqrt(h->h_mgd[0]);
+      if (rn < atol) { ++k; st = pfb::CG_CONVERGED; break; }
+      if (!(rn == rn)) { ++k; st = pfb::CG_NAN; break; }
+      if (k + 1 >= maxiter) { ++k; st = pfb::CG_MAXITER; break; }
+    }
+  }
+  PF_CUDA(cudaEventRecord(h->ev1, s));
+  PF_CUDA(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  PF_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  *status = st;
+  *iters = k;
+  if (h->trace)
+    fprintf(stderr, "[pfb200] strip mg-pcg (%s): %lld iterations, %.3f ms\n",
+            mom ? "momentum" : "phase field", k, ms);
+  cg_account(h, mom, k, ms);
+  return cg_status(h, st, k);
+}
+
 static pf_status run_cg(pf_handle* h, bool mom, double* target, bool probe, int* status,
                         long long* iters, double* const* guess = nullptr, int n_guess = 0) {
+  if (h->comm && !probe && (mom ? h->mgu.on : h->mgs.on)) {
+    if (target) return fail(h, PF_ERR_INVALID, "strip multigrid PCG: no target update");
+    return run_mgd(h, mom, status, iters);
+  }
   if (mom && h->mgu.on && !probe)
     return run_mg(h, h->mgu, target, status, iters, 0, -1, -1.0, true, false, guess, n_guess);
   if (h->comm) return run_cg_dist(h, mom, target, probe, status, iters);

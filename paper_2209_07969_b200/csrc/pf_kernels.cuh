@@ -729,4 +729,5 @@ __global__ void k_flush(double* buf, long long n, double v) {
 }  // namespace pfb
 #include "pf_mg.cuh"
 #include "pf_mgs.cuh"
+#include "pf_mgd.cuh"
 #include "pf_st.cuh"

@@ -602,6 +602,7 @@ struct FinePcg : FineBase {  // p = z + beta p_old (owner stores), q = A p (mask
   double* pnew;
   double* q;
   double* pq;
+  const DMesh* own = nullptr;  // row strips: p.q over owned nodes only (pf_mgd.cuh)
   struct Raw {
     double2 zv, po;
     double d;
@@ -627,7 +628,7 @@ struct FinePcg : FineBase {  // p = z + beta p_old (owner stores), q = A p (mask
     const double2 qv = mask2(Av, di(id));
     d2st(pnew, id, p);
     d2st(q, id, qv);
-    *pq += p.x * qv.x + p.y * qv.y;
+    if (!own || node_owned(*own, id)) *pq += p.x * qv.x + p.y * qv.y;
   }
 };
 

@@ -200,6 +200,7 @@ struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (ma
   double* pnew;
   double* q;
   double* pq;
+  const DMesh* own = nullptr;  // row strips: p.q over owned nodes only (pf_mgd.cuh)
   struct Raw {
     double zv, po, dv;
   };
@@ -223,7 +224,7 @@ struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (ma
     const double qv = mgs_mask(Av.x, p.y);
     pnew[id] = p.x;
     q[id] = qv;
-    *pq += p.x * qv;
+    if (!own || node_owned(*own, id)) *pq += p.x * qv;
   }
 };
 

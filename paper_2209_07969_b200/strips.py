@@ -54,29 +54,48 @@ class Strip:
         return self.local_to_global[idx]
 
 
-def partition_rows(lay: StructuredLayout, nranks: int) -> list:
-    """Node-row cuts ``[c_0=0, c_1, ..., c_n=ny+1]`` balancing cell counts."""
+def partition_rows(lay: StructuredLayout, nranks: int, align: int | None = None) -> list:
+    """Node-row cuts ``[c_0=0, c_1, ..., c_n=ny+1]`` balancing cell counts.
+
+    Cuts are rounded to a multiple of ``align`` (default: the largest power of two not above a
+    quarter of the balanced strip height, at most 512) when that keeps the constraints, so
+    every strip's owned sub-mesh coarsens deeply for its local multigrid V-cycle (pf_mgd.cuh);
+    a cut never makes the first owned row the slit row or the row directly above it (the rank
+    would need the duplicates as ghosts, or its V-cycle would see the lower crack face without
+    its cells)."""
     if nranks < 1:
         raise ValueError("nranks must be >= 1")
     ny = lay.ny
     if nranks > (ny + 1) // 2:
         raise ValueError(f"{nranks} strips need at least {2 * nranks} node rows")
+    if align is None:
+        h = max(1, (ny + 1) // (4 * nranks))
+        align = 1
+        while align * 2 <= min(h, 512):
+            align *= 2
     cells = (lay.elem_hi - lay.elem_lo).astype(np.int64)  # cells of cell row j (owner: row j)
     w = np.r_[cells, 0].astype(float) + 1e-9               # weight of node row j
     cum = np.cumsum(w)
     cuts = [0]
-    for r in range(1, nranks):
-        c = int(np.searchsorted(cum, cum[-1] * r / nranks)) + 1
+
+    def ok(c, r):
         hi_lim = ny + 1 - 2 * (nranks - r)
-        c = min(max(c, cuts[-1] + 2), hi_lim)
-        if lay.notch_row >= 0 and c == lay.notch_row + 1:
-            # first owned row directly above the slit: move the cut by one row
-            if c + 1 <= hi_lim:
-                c += 1
-            elif c - 1 >= cuts[-1] + 2:
-                c -= 1
-            else:
-                raise ValueError(f"cannot cut around the slit row with {nranks} strips")
+        if c < cuts[-1] + 2 or c > hi_lim:
+            return False
+        return not (lay.notch_row >= 0 and c in (lay.notch_row, lay.notch_row + 1))
+
+    for r in range(1, nranks):
+        c0 = int(np.searchsorted(cum, cum[-1] * r / nranks)) + 1
+        cands = []
+        if align > 1:
+            base = int(round(c0 / align)) * align
+            cands += [base, base + align, base - align]
+        cands += [c0, c0 + 1, c0 - 1, c0 + 2, c0 - 2]
+        hi_lim = ny + 1 - 2 * (nranks - r)
+        cands += [min(max(c0, cuts[-1] + 2), hi_lim)]
+        c = next((x for x in cands if ok(x, r)), None)
+        if c is None:
+            raise ValueError(f"cannot cut {ny + 1} node rows into {nranks} strips around the slit")
         cuts.append(c)
     cuts.append(ny + 1)
     if any(b - a < 2 for a, b in zip(cuts, cuts[1:])):

@@ -26,6 +26,7 @@ def run_strips(case_name, scheme, nranks, steps=None):
     n = case.n_steps if steps is None else steps
     group = HostGroup(nranks)
     results = [None] * nranks
+    kinds = [None] * nranks
     errors = []
 
     def worker(rank):
@@ -39,7 +40,9 @@ def run_strips(case_name, scheme, nranks, steps=None):
             for _ in range(n):
                 st = ss.step(scheme, pb.bcs, pb.pins)
                 reac = [ss.reaction_force(nodes, comp) for _, nodes, comp in pb.reactions]
-                rec.append((st.n_stag, st.n_nr_u, st.n_nr_d, st.spd_fallbacks, reac))
+                rec.append((st.n_stag, st.n_nr_u, st.n_nr_d, st.spd_fallbacks, reac,
+                            st.cg_iters_u, st.cg_iters_d))
+            kinds[rank] = ss.sess.solver_kinds()
             results[rank] = (rec, ss.owned_state())
             ss.close()
         except Exception as exc:  # noqa: BLE001
@@ -57,6 +60,7 @@ def run_strips(case_name, scheme, nranks, steps=None):
     d = np.empty(pb.mesh.n_nodes)
     for _, own in results:
         d[own["nodes"]] = own["d"]
+    run_strips.kinds = kinds
     return pb, results[0][0], [r[0] for r in results], d
 
 
@@ -128,3 +132,26 @@ def test_nccl_graph_path_single_rank(case, scheme, cuda_ok):
         err = min(err, float(np.abs(d - z["final_d"][mirror_perm(pb.mesh)]).max()))
     assert err <= 1e-6, err
     ss.close()
+
+
+def test_strips_multigrid_preconditioner(cuda_ok, monkeypatch):
+    """The strips' multigrid PCG (pf_mgd.cuh: strip-local V-cycles as a block-Jacobi
+    preconditioner, ghost rows masked, Krylov recurrence with all-reduces and halo rows) against
+    the strips' Jacobi PCG (PFB200_DIST_MG=0): the same load steps, fields to the linear-solve
+    accuracy, far fewer momentum PCG iterations; and against the reference's table."""
+    case, scheme, nranks, steps = "multicrack32", "ST", 2, 6
+    runs = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PFB200_DIST_MG", flag)
+        pb, rec, _, d = run_strips(case, scheme, nranks, steps=steps)
+        runs[flag] = (rec, d, list(run_strips.kinds))
+    (rj, dj, kj), (rm, dm, km) = runs["0"], runs["1"]
+    assert all(k["momentum"] == "jacobi_pcg" for k in kj)
+    assert all(k["momentum"] == "multigrid_pcg" for k in km)
+    assert [x[:2] for x in rj] == [x[:2] for x in rm]
+    assert np.abs(dj - dm).max() <= 1e-8
+    assert sum(x[5] for x in rm) < 0.25 * sum(x[5] for x in rj)
+    z = golden(f"run_{case}_{scheme}.npz")
+    fpeak = np.abs(z["table"][:, 7]).max()
+    for row, x in zip(z["table"], rm):
+        assert abs(x[0] - int(row[1])) <= 1 and abs(x[4][0] - row[7]) <= 1e-6 * fpeak
