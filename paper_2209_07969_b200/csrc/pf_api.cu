@@ -1656,6 +1656,20 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
           pf_status es = mgs_setup(h, h->mgs, os * dev_sms * pfb::MG_WARPS);
           if (es != PF_OK) return bail(es);
         }
+        if (strip) {  // every strip must take the same solver path (collectives): agree
+          double* d_flag = nullptr;
+          CREATE_CUDA(cudaMalloc((void**)&d_flag, 2 * sizeof(double)));
+          const double miss[2] = {h->mgu.on ? 0.0 : 1.0, h->mgs.on ? 0.0 : 1.0};
+          CREATE_CUDA(cudaMemcpy(d_flag, miss, sizeof miss, cudaMemcpyHostToDevice));
+          const std::string ce = h->comm->allreduce(d_flag, 2, h->stream);
+          double tot[2] = {0.0, 0.0};
+          cudaMemcpyAsync(tot, d_flag, sizeof tot, cudaMemcpyDeviceToHost, h->stream);
+          cudaStreamSynchronize(h->stream);
+          cudaFree(d_flag);
+          if (!ce.empty()) { h->err = ce; return bail(PF_ERR_NCCL); }
+          if (tot[0] > 0.0) h->mgu.on = false;  // some strip's rows do not coarsen: Jacobi PCG
+          if (tot[1] > 0.0) h->mgs.on = false;
+        }
         if (strip && (h->mgu.on || h->mgs.on)) {  // the strip PCG's scalars, partials, marches
           CREATE_CUDA(cudaMalloc((void**)&h->d_mgd, 8 * sizeof(double)));
           CREATE_CUDA(cudaMemset(h->d_mgd, 0, 8 * sizeof(double)));

@@ -138,7 +138,9 @@ struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-
     int J0, J1;
     bool up;
     prolong_rows(*mf, j, dup, J0, J1, up);
+#if PFB_MGS_NOPROL != 2
     pc.need(*mc, ec, i >> 1, (i >> 1) + (i & 1), J0, J1, up);
+#endif
   }
   __device__ double2 finish(const Raw& w, int, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
@@ -151,7 +153,11 @@ struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-
     const double w0 = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
     const double a10 = (i & 1) ? w0 : 0.0, a01 = (j & 1) ? w0 : 0.0;
     const double a11 = ((i & 1) && (j & 1)) ? w0 : 0.0;
+#if PFB_MGS_NOPROL + 0  // timing experiments only: the smoothing march without the prolongation
+    const double pe = 0.0 * (w0 * v00 + a10 * v10 + a01 * v01 + a11 * v11);
+#else
     const double pe = w0 * v00 + a10 * v10 + a01 * v01 + a11 * v11;
+#endif
     return make_double2(mgs_mask(om * w.dv * w.bv + pe, w.dv), om * w.dv);  // y, omega D^-1
   }
   __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
