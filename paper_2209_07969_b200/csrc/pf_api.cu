@@ -1313,9 +1313,16 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
 #undef MGS_NODE_KERNEL
 }
 
+// Handle creation captures CUDA graphs; a legacy-stream operation (cudaMemcpy / cudaMemset) of
+// another thread's concurrent creation would invalidate a capture in progress (several strips
+// created by host threads in one process, tests/test_gpu_strips.py).  Creations are serialised,
+// except around the strips' solver-path agreement, which needs every rank.
+static std::mutex g_create_mu;
+
 static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const pf_config* cfg,
                              int device, const pf_strip* strip, pf_handle** out) {
   if (!out || !mesh || !mat || !cfg) return PF_ERR_INVALID;
+  std::unique_lock<std::mutex> create_lock(g_create_mu);
   *out = nullptr;
   pf_handle* h = new pf_handle();
   h->device = device;
@@ -1420,7 +1427,9 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
       auto* nc = new pfb::NcclComm();
       nc->spec = sp;
       h->comm = nc;
+      create_lock.unlock();  // ncclCommInitRank is collective over the ranks
       const std::string e = nc->init(strip->nccl_id);
+      create_lock.lock();
       if (!e.empty()) { h->err = e; return bail(PF_ERR_NCCL); }
     } else {
       if (!strip->host_group) { h->err = "host_group is null"; return bail(PF_ERR_INVALID); }
@@ -1661,7 +1670,9 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
           CREATE_CUDA(cudaMalloc((void**)&d_flag, 2 * sizeof(double)));
           const double miss[2] = {h->mgu.on ? 0.0 : 1.0, h->mgs.on ? 0.0 : 1.0};
           CREATE_CUDA(cudaMemcpy(d_flag, miss, sizeof miss, cudaMemcpyHostToDevice));
+          create_lock.unlock();  // every rank must reach the all-reduce
           const std::string ce = h->comm->allreduce(d_flag, 2, h->stream);
+          create_lock.lock();
           double tot[2] = {0.0, 0.0};
           cudaMemcpyAsync(tot, d_flag, sizeof tot, cudaMemcpyDeviceToHost, h->stream);
           cudaStreamSynchronize(h->stream);
@@ -2450,11 +2461,12 @@ static pf_status run_mgd(pf_handle* h, bool mom, int* status, long long* iters) 
   const double* dinv = mom ? h->dinvu : h->dinvd;
   double* vdinv = mom ? h->mgu.A.L[0].dinv : h->mgs.A.L[0].dinv;
   double* z = mom ? h->mgu.A.z : h->mgs.A.z;
-  const double* rzpart = mom ? h->mgu.A.part : h->mgs.A.part;
-  const int n_rz = mom ? h->mgu.gf : h->mgs.gf;
   const int gfl = h->mgd_gflat;
+  // the interface row (first owned node row of ranks > 0): point Jacobi in the preconditioner
+  const int if_lo = h->mgd_row0 > 0 ? h->h_nst[h->mgd_row0] : 0;
+  const int if_hi = h->mgd_row0 > 0 ? if_lo + (h->h_nhi[h->mgd_row0] - h->h_nlo[h->mgd_row0]) : 0;
   PF_CUDA(cudaEventRecord(h->ev0, s));
-  pfb::k_mgd_mask<<<gfl, 256, 0, s>>>(vdinv, dinv, comps, h->dm);
+  pfb::k_mgd_mask<<<gfl, 256, 0, s>>>(vdinv, dinv, comps, h->dm, if_lo, if_hi);
   if (mom) {
     PF_CUDA(cudaGraphLaunch(h->mgu.setup_exec, s));
     h->acc.launches += h->mgu.setup_kernels;
@@ -2483,8 +2495,12 @@ static pf_status run_mgd(pf_handle* h, bool mom, int* status, long long* iters) 
     const int gdir = mom ? h->mgd_gdir_u : h->mgd_gdir_d;
     for (k = 0;; ++k) {
       PF_CUDA(cudaGraphLaunch(mom ? h->mgu.vcycle_exec : h->mgs.vcycle_exec, s));  // z = M^-1 r
+      if (if_hi > if_lo)
+        pfb::k_mgd_iface<<<std::max(1, (comps * (if_hi - if_lo) + 255) / 256), 256, 0, s>>>(
+            z, r, dinv, comps, if_lo, if_hi);
       if (k > 0) pfb::k_mgd_shift<<<1, 1, 0, s>>>(g);
-      pfb::k_finalize<<<1, 256, 0, s>>>(rzpart, n_rz, 1, g + pfb::MGD_RZ);
+      pfb::k_mgd_dot<<<gfl, pfb::MG_NT, 0, s>>>(r, z, comps, h->dm, h->mgd_part);
+      pfb::k_finalize<<<1, 256, 0, s>>>(h->mgd_part, gfl, 1, g + pfb::MGD_RZ);
       PF_TRY(comm_check(h, h->comm->allreduce(g + pfb::MGD_RZ, 1, s)));
       PF_TRY(halo(h, z, comps));
       const double* pold = (k & 1) ? p0 : p1;
@@ -2503,7 +2519,8 @@ static pf_status run_mgd(pf_handle* h, bool mom, int* status, long long* iters) 
       PF_CUDA(cudaMemcpyAsync(h->h_mgd, g + pfb::MGD_RR, sizeof(double), cudaMemcpyDeviceToHost, s));
       PF_CUDA(cudaStreamSynchronize(s));
       PF_CUDA(cudaGetLastError());
-      h->acc.launches += (mom ? h->mgu.vcycle_kernels : h->mgs.vcycle_kernels) + 6 + (k > 0);
+      h->acc.launches += (mom ? h->mgu.vcycle_kernels : h->mgs.vcycle_kernels) + 7 + (k > 0) +
+                         (if_hi > if_lo);
       const double rn = std::sqrt(h->h_mgd[0]);
       if (rn < atol) { ++k; st = pfb::CG_CONVERGED; break; }
       if (!(rn == rn)) { ++k; st = pfb::CG_NAN; break; }

@@ -1,9 +1,10 @@
 // pf_mgd.cuh — the multigrid PCG on row strips (multi-GPU).
 //
 // Each rank preconditions with its own V-cycle (pf_mg.cuh momentum / pf_mgs.cuh phase field) on
-// the sub-mesh of its owned node rows, the ghost row above masked (homogeneous Dirichlet): a
-// block-Jacobi preconditioner whose blocks are the strips, each solved approximately by one
-// symmetric V(1,1)-cycle.  It is SPD, so the outer PCG -- the reference's Jacobi-PCG switch with
+// the sub-mesh of its owned node rows, the ghost row above and (ranks > 0) the first owned row
+// masked (homogeneous Dirichlet; the first owned row gets point Jacobi): a block-Jacobi
+// preconditioner whose blocks are the strips, each solved approximately by one symmetric
+// V(1,1)-cycle.  It is SPD, so the outer PCG -- the reference's Jacobi-PCG switch with
 // M^-1 replaced (linsolve.py:48-54: x0 = 0, stop when ||r|| < rtol ||b||) -- keeps the solution
 // contract; there is no coarse-grid exchange between GPUs (the hierarchies are local), the cost is
 // a mild growth of the iteration count with the number of strips.  Per iteration: one local
@@ -15,13 +16,40 @@
 
 namespace pfb {
 
-// dinv restricted to owned nodes (ghost rows masked) for the local V-cycle
+// dinv restricted to the V-cycle's nodes: owned, minus the strip's first owned node row
+// [if_lo, if_hi) on ranks > 0 (the interface row, masked like the ghost row above, so every
+// strip's local problem has a Dirichlet row: a strip with no physical Dirichlet boundary of its
+// own, e.g. the upper L-panel strip, is not singular)
 __global__ void k_mgd_mask(double* __restrict__ dst, const double* __restrict__ src, int comps,
-                           DMesh m) {
+                           DMesh m, int if_lo, int if_hi) {
   const long long n = (long long)comps * m.n_nodes;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int node = (int)(i / comps);
+    dst[i] = (node_owned(m, node) && !(node >= if_lo && node < if_hi)) ? src[i] : 0.0;
+  }
+}
+// the interface row's block of the preconditioner: point Jacobi z = D^-1 r
+__global__ void k_mgd_iface(double* __restrict__ z, const double* __restrict__ r,
+                            const double* __restrict__ dinv, int comps, int if_lo, int if_hi) {
+  const long long lo = (long long)comps * if_lo, n = (long long)comps * (if_hi - if_lo);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    dst[i] = node_owned(m, (int)(i / comps)) ? src[i] : 0.0;
+    z[lo + i] = dinv[lo + i] * r[lo + i];
+}
+// partial sums of r.z over owned nodes (one per CTA)
+__global__ void __launch_bounds__(MG_NT) k_mgd_dot(const double* __restrict__ r,
+                                                    const double* __restrict__ z, int comps,
+                                                    DMesh m, double* part) {
+  __shared__ double red[MG_WARPS];
+  const long long n = (long long)comps * m.n_nodes;
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (node_owned(m, (int)(i / comps))) s += r[i] * z[i];
+  double v[1] = {s};
+  mg_block_sum<1>(v, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = v[0];
 }
 
 // x = 0; partial sums of r.r over owned nodes (one per CTA)

@@ -5,6 +5,8 @@ Golden per-step tables come from the unmodified reference (tests/golden/run_*.np
 reaction force within 1e-6 of the peak force, phase field within 1e-6 in L-infinity.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -186,6 +188,38 @@ def test_cfg2_through_crack(cuda_ok, scheme):
         ref = z[f"d_step{step}"]
         err = min(np.abs(d - ref).max(), np.abs(d - ref[perm]).max())
         assert err <= 1e-6, (step, err)
+
+
+def test_cfg2_crack_step_from_reference_state(cuda_ok):
+    """The cfg2 S1 crack step (load step 55) started from the reference's OWN state after step 54
+    (make_golden.py --state-snap 54: u, d, d_prev, gp.psi_max), so the comparison is free of any
+    drift accumulated over the 54 earlier steps: staggered count within the crack-step window,
+    Newton counts in proportion, force within 1e-6 of the peak, phase field within 1e-6 (modulo
+    the mirror symmetry)."""
+    import sys
+
+    sys.path.insert(0, __import__("conftest").GOLDEN)
+    from make_golden import load_restart
+
+    z, _ = _cfg2_golden("S1")
+    golden("restart_cfg2_S1_step54.npz")
+    if len(z["table"]) < 55:
+        pytest.skip("the reference cfg2 S1 run has not reached the crack step yet")
+    pb = C.setup(C.get_case("cfg2"), C.b200_api())
+    after = load_restart(pb.state, os.path.join(__import__("conftest").GOLDEN,
+                                                "restart_cfg2_S1_step54.npz"))
+    assert after == 54
+    recs = C.run(pb, "S1", n_steps=1, first_step=55)
+    lo, hi = stag_window("cfg2", "S1", 55, "run_cfg2_S1.npz")
+    row = z["table"][54]
+    r = recs[0]
+    assert lo[54] <= r.n_stag <= hi[54], (r.n_stag, row[1], lo[54], hi[54])
+    fpeak = np.abs(z["table"][:, 7]).max()
+    assert abs(r.reactions[0] - row[7]) <= 1e-6 * fpeak, (r.reactions[0], row[7])
+    ref = z["d_step55"]
+    perm = mirror_perm(pb.mesh)
+    err = min(np.abs(pb.state.d - ref).max(), np.abs(pb.state.d - ref[perm]).max())
+    assert err <= 1e-6, err
 
 
 @pytest.mark.parametrize("case,scheme", [("tension16", "S1"), ("tension16", "S2"),
