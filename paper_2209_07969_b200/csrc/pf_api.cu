@@ -56,7 +56,7 @@ struct MgInst {
 struct MgsInst {
   bool on = false;
   pfb::MgsArgs A{};
-  int gf = 1, gflat = 1;
+  int gf = 1, gfr = 1, gflat = 1;  // fine-march grids (gfr: the residual march), flat grid
   std::vector<int> gl, gn, lpn;
   pfb::MgIn* in = nullptr;
   // setup graphs: the first with MG_POW power steps from a hashed start, later ones with
@@ -1128,6 +1128,12 @@ static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
   A.coarse_items = coarse_items;
   A.g0 = pfb::make_march_geom(h->nx, lv[0].ny, fine_resident_warps);
   M.gf = (A.g0.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+  {
+    int orr = 0;
+    PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&orr, pfb::k_mgs_fine_resid, pfb::MG_NT, 0));
+    A.g0r = pfb::make_march_geom(h->nx, lv[0].ny, std::max(1, orr) * h->sm_count * pfb::MG_WARPS);
+    M.gfr = (A.g0r.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+  }
   M.gflat = 2 * h->sm_count;
   const size_t nn = h->n_nodes;
   if (mg_alloc(h, &A.z, nn) != cudaSuccess) return oom();
@@ -1161,13 +1167,19 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
   pfb::MgsArgs& A = M.A;
   const int nl = A.n_levels;
   cudaStream_t s = h->stream;
+  // power steps: MG_POW from a hashed start at every setup (PFB200_MGS_POW); warm-started steps
+  // from the previous setup's vectors (PFB200_MGS_POW_WARM=k) are an experiment: with 2 or 4
+  // steps the phase-field iteration counts drifted up over the load steps at cfg5 (155 -> 187 /
+  // 587 per load step), so they are off by default
+  const char* pc = getenv("PFB200_MGS_POW");
+  const int npow_cold = pc ? std::max(2, std::min(pfb::MG_POW, atoi(pc))) : pfb::MG_POW;
   const char* pw = getenv("PFB200_MGS_POW_WARM");
-  M.pow_warm_steps = pw ? std::max(0, std::min(pfb::MG_POW, atoi(pw))) : 2;
+  M.pow_warm_steps = pw ? std::max(0, std::min(pfb::MG_POW, atoi(pw))) : 0;
   for (int warm = 0; warm < 2; ++warm) {
     // setup: Galerkin levels, stencils, dense coarsest inverse, power steps, omegas; the warm
     // variant starts the power steps from the previous setup's vectors (0 steps: cold only)
     if (warm && M.pow_warm_steps == 0) break;
-    const int npow = warm ? M.pow_warm_steps : pfb::MG_POW;
+    const int npow = warm ? M.pow_warm_steps : npow_cold;
     pfb::MgsArgs B = A;
     B.pow_warm = warm;
     cudaGraph_t g = nullptr;
@@ -1180,13 +1192,18 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
       pfb::k_mgs_stencil<<<M.gl[lc], pfb::MG_NT, 0, s>>>(B, lc);
     }
     if (B.dense) pfb::k_mgs_dense<<<1, pfb::MG_NT, 0, s>>>(B);
+    // the fine march and the coarse grid levels of a power step as two launches: in one grid
+    // the coarse blocks queued behind the fine march's (3.3 ms per step at cfg5)
     const int cb = (B.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
-    for (int k = 1; k <= npow; ++k)
-      pfb::k_mgs_pow<<<M.gf + cb, pfb::MG_NT, 0, s>>>(B, k, M.gf);
+    for (int k = 1; k <= npow; ++k) {
+      pfb::k_mgs_pow<<<M.gf, pfb::MG_NT, 0, s>>>(B, k, M.gf);
+      if (cb > 0) pfb::k_mgs_pow<<<cb, pfb::MG_NT, 0, s>>>(B, k, 0);
+    }
     if (B.n_tail < nl) pfb::k_mgs_pow_tail<<<1, pfb::MG_TAIL_NT, 0, s>>>(B, npow);
     pfb::k_mgs_lambda<<<M.gflat, pfb::MG_NT, 0, s>>>(B, npow);
     pfb::k_mgs_evstore<<<4 * h->sm_count, pfb::MG_NT, 0, s>>>(B, npow);
-    const int nk = 2 * (nl - 1) + (B.dense ? 1 : 0) + npow + (B.n_tail < nl ? 1 : 0) + 2;
+    const int nk = 2 * (nl - 1) + (B.dense ? 1 : 0) + npow * (cb > 0 ? 2 : 1) +
+                   (B.n_tail < nl ? 1 : 0) + 2;
     (warm ? M.setup_kernels_warm : M.setup_kernels) = nk;
     cudaError_t e = cudaStreamEndCapture(s, &g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MGS setup capture: ") + cudaGetErrorString(e));
@@ -1202,7 +1219,7 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
   } while (0)
   const int c = nl - 1, top = std::min(A.n_tail, c);
   auto body_kernels = [&](const pfb::MgsArgs& B, bool krylov = true) {
-    pfb::k_mgs_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(B);
+    pfb::k_mgs_fine_resid<<<M.gfr, pfb::MG_NT, 0, s>>>(B);
     for (int l = 1; l < top; ++l) {
       if (M.lpn[l] == 16 && M.fuse && B.L[l].m.n_nodes <= 8192) {
         pfb::k_mgs_sdown<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
@@ -3170,7 +3187,7 @@ extern "C" pf_status pf_bench_mg_kernel(pf_handle* h, int which, int reps, doubl
     const double n1 = A.L[1].m.n_nodes;
     if (which == 10) {
       bytes = 24.0 * n + 32.0 * e;  // r, D^-1, t (8 B); b per Gauss point (32 B per cell)
-      PF_TRY(run([&] { pfb::k_mgs_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));
+      PF_TRY(run([&] { pfb::k_mgs_fine_resid<<<M.gfr, pfb::MG_NT, 0, s>>>(A); }));
     } else if (which == 11) {
       bytes = 24.0 * n + 8.0 * n1 + 32.0 * e;  // r, D^-1, z; level-1 correction; b
       PF_TRY(run([&] { pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));

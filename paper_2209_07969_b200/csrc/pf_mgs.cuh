@@ -48,7 +48,8 @@ struct MgsArgs {
   Consts C;
   int n_levels, n_tail, dense, nu_c;
   MgsLevel L[MG_MAXL];
-  MarchGeom g0;
+  MarchGeom g0;               // fine-level march units (smoothing, direction, power steps)
+  MarchGeom g0r;              // fine-level march units of the residual march
   int coarse_items;
   int pow_warm;               // 1: power steps start from L[l].ev (the previous setup's vectors)
   const double* bq;           // level-0 Newton coefficient per Gauss point [n_elems][4]
@@ -770,12 +771,17 @@ __global__ void __launch_bounds__(MG_NT) k_mgs_init(MgsArgs A) {
 #ifndef PFB_MGS_MINB
 #define PFB_MGS_MINB 3
 #endif
-__global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_fine_resid(MgsArgs A) {
+// the residual march is the lightest: four CTAs per SM (its own unit geometry g0r; measured at
+// cfg5 0.77 -> 0.66 ms, while the smoothing and direction marches lose at four)
+#ifndef PFB_MGS_MINB_RESID
+#define PFB_MGS_MINB_RESID 4
+#endif
+__global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB_RESID) k_mgs_fine_resid(MgsArgs A) {
   __shared__ MgWarp ws[MG_WARPS];
   const double om = __ldcg(&A.ctl->omega[0]);
   SFineResid op{{&A.C, A.bq, A.L[0].dinv}, om, A.r, A.L[0].t};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
-  if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
+  if (w < A.g0r.n_units) mg_march(A.L[0].m, A.g0r, w, op, ws[threadIdx.x >> 5]);
 }
 
 __global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_fine_smooth(MgsArgs A) {
