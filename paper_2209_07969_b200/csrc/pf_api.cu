@@ -59,11 +59,12 @@ struct MgsInst {
   int gf = 1, gfr = 1, gflat = 1;  // fine-march grids (gfr: the residual march), flat grid
   std::vector<int> gl, gn, lpn;
   pfb::MgIn* in = nullptr;
-  // setup graphs: the first with MG_POW power steps from a hashed start, later ones with
-  // MGS_POW_WARM steps from the previous setup's normalised vectors (PFB200_MGS_POW_WARM)
-  cudaGraphExec_t setup_exec = nullptr, setup_warm_exec = nullptr, solve_exec = nullptr;
-  int pow_warm_steps = 2;
-  int setup_kernels_warm = 0;
+  // setup graphs: MGS_POW power steps (fast: a slightly low lambda estimate, a slightly larger
+  // omega, fewer iterations) and MG_POW steps (safe: the redo when a solve on the fast hierarchy
+  // overruns its budget -- an underestimated lambda can make the smoother diverge)
+  cudaGraphExec_t setup_exec = nullptr, setup_safe_exec = nullptr, solve_exec = nullptr;
+  int setup_kernels_safe = 0;
+  long long last_iters = 0, redos = 0;
   cudaGraphExec_t vcycle_exec = nullptr;  // row strips: one V-cycle z = M^-1 r (pf_mgd.cuh)
   int vcycle_kernels = 0;
   long long setups = 0;
@@ -321,7 +322,7 @@ extern "C" void pf_destroy(pf_handle* h) {
   if (h->mgd_part) cudaFree(h->mgd_part);
   if (h->mgs.in) cudaFreeHost(h->mgs.in);
   if (h->mgs.setup_exec) cudaGraphExecDestroy(h->mgs.setup_exec);
-  if (h->mgs.setup_warm_exec) cudaGraphExecDestroy(h->mgs.setup_warm_exec);
+  if (h->mgs.setup_safe_exec) cudaGraphExecDestroy(h->mgs.setup_safe_exec);
   if (h->mgs.solve_exec) cudaGraphExecDestroy(h->mgs.solve_exec);
   if (h->stage) cudaFreeHost(h->stage);
   for (auto& row : h->graphs)
@@ -782,7 +783,11 @@ static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_w
   M.gflat = 2 * h->sm_count;
   if (mg_alloc(h, &A.z, 2 * (size_t)h->n_nodes) != cudaSuccess) return oom();
   A.phys = phys;
-  for (int l = 0; l < nl; ++l) A.L[l].scalar = phys == 1 ? 1 : 0;
+  const char* s32 = getenv("PFB200_MG_S32");  // "0": FP64 coarse stencils in the V-cycle
+  for (int l = 0; l < nl; ++l) {
+    A.L[l].scalar = phys == 1 ? 1 : 0;
+    A.L[l].s32 = (s32 && std::string(s32) == "0") ? 0 : 1;
+  }
   if (phys == 0 && h->comm) {  // strips: the V-cycle's own inverse diagonal, ghost rows masked
     if (mg_alloc(h, &A.L[0].dinv, 2 * (size_t)h->n_nodes) != cudaSuccess) return oom();
   } else if (phys == 0) {
@@ -844,11 +849,18 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
       pfb::k_mg_stencil<<<M.gl[lc], pfb::MG_NT, 0, s>>>(A, lc);
     }
     if (A.dense) pfb::k_mg_dense<<<1, pfb::MG_NT, 0, s>>>(A);
-    M.setup_kernels = 2 * (nl - 1) + (A.dense ? 1 : 0) + pfb::MG_POW + 1;
+    // power steps for lambda_max(D^-1 A_l) (PFB200_MG_POW, default MG_POW); the fine march and
+    // the coarse grid levels as separate launches (one grid queued the coarse blocks behind the
+    // fine march's)
+    const char* pc = getenv("PFB200_MG_POW");
+    const int npow = pc ? std::max(2, std::min(pfb::MG_POW, atoi(pc))) : pfb::MG_POW;
     const int cb = (A.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
-    for (int k = 1; k <= pfb::MG_POW; ++k)
-      pfb::k_mg_pow<<<M.gf + cb, pfb::MG_NT, 0, s>>>(A, k, M.gf);
-    pfb::k_mg_lambda<<<M.gflat, pfb::MG_NT, 0, s>>>(A);
+    M.setup_kernels = 2 * (nl - 1) + (A.dense ? 1 : 0) + npow * (cb > 0 ? 2 : 1) + 1;
+    for (int k = 1; k <= npow; ++k) {
+      pfb::k_mg_pow<<<M.gf, pfb::MG_NT, 0, s>>>(A, k, M.gf);
+      if (cb > 0) pfb::k_mg_pow<<<cb, pfb::MG_NT, 0, s>>>(A, k, 0);
+    }
+    pfb::k_mg_lambda<<<M.gflat, pfb::MG_NT, 0, s>>>(A, npow);
     cudaError_t e = cudaStreamEndCapture(s, &g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MG setup capture: ") + cudaGetErrorString(e));
     e = cudaGraphInstantiate(&M.setup_exec, g, 0);
@@ -1068,9 +1080,7 @@ static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
       dm = dm_level0(h);
       ML.dinv = h->dinvd;
       if (h->comm && mg_alloc(h, &ML.dinv, (size_t)L.n_nodes) != cudaSuccess) return oom();
-      if (mg_alloc(h, &ML.t, (size_t)L.n_nodes) != cudaSuccess ||
-          mg_alloc(h, &ML.ev, (size_t)L.n_nodes) != cudaSuccess)
-        return oom();
+      if (mg_alloc(h, &ML.t, (size_t)L.n_nodes) != cudaSuccess) return oom();
       continue;
     }
     std::vector<int4> nrow(L.ny + 1), erow(L.ny);
@@ -1092,8 +1102,7 @@ static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
     const size_t n = L.n_nodes;
     if (mg_alloc(h, &ML.K, 16 * (size_t)L.n_elems) != cudaSuccess ||
         mg_alloc(h, &ML.dinv, n) != cudaSuccess || mg_alloc(h, &ML.b, n) != cudaSuccess ||
-        mg_alloc(h, &ML.e, n) != cudaSuccess || mg_alloc(h, &ML.t, n) != cudaSuccess ||
-        mg_alloc(h, &ML.ev, n) != cudaSuccess)
+        mg_alloc(h, &ML.e, n) != cudaSuccess || mg_alloc(h, &ML.t, n) != cudaSuccess)
       return oom();
     ML.items = pfb::mg_items(L.nx, L.ny, L.notch_row >= 0);
     M.gl[l] = (ML.items + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
@@ -1167,21 +1176,16 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
   pfb::MgsArgs& A = M.A;
   const int nl = A.n_levels;
   cudaStream_t s = h->stream;
-  // power steps: MG_POW from a hashed start at every setup (PFB200_MGS_POW); warm-started steps
-  // from the previous setup's vectors (PFB200_MGS_POW_WARM=k) are an experiment: with 2 or 4
-  // steps the phase-field iteration counts drifted up over the load steps at cfg5 (155 -> 187 /
-  // 587 per load step), so they are off by default
+  // power steps from a hashed start at every setup: MGS_POW (PFB200_MGS_POW) and MG_POW (the safe
+  // redo).  (Warm-started power steps from the previous setup's vectors were tried: the
+  // phase-field iteration counts drifted up over the load steps at cfg5.)
   const char* pc = getenv("PFB200_MGS_POW");
-  const int npow_cold = pc ? std::max(2, std::min(pfb::MG_POW, atoi(pc))) : pfb::MG_POW;
-  const char* pw = getenv("PFB200_MGS_POW_WARM");
-  M.pow_warm_steps = pw ? std::max(0, std::min(pfb::MG_POW, atoi(pw))) : 0;
-  for (int warm = 0; warm < 2; ++warm) {
-    // setup: Galerkin levels, stencils, dense coarsest inverse, power steps, omegas; the warm
-    // variant starts the power steps from the previous setup's vectors (0 steps: cold only)
-    if (warm && M.pow_warm_steps == 0) break;
-    const int npow = warm ? M.pow_warm_steps : npow_cold;
+  const int npow_fast = pc ? std::max(2, std::min(pfb::MG_POW, atoi(pc))) : pfb::MGS_POW;
+  for (int safe = 0; safe < 2; ++safe) {
+    const int npow = safe ? pfb::MG_POW : npow_fast;
+    const bool warm = false;
     pfb::MgsArgs B = A;
-    B.pow_warm = warm;
+    B.pow_warm = warm ? 1 : 0;
     cudaGraph_t g = nullptr;
     PF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     for (int lc = 1; lc < nl; ++lc) {
@@ -1201,13 +1205,12 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
     }
     if (B.n_tail < nl) pfb::k_mgs_pow_tail<<<1, pfb::MG_TAIL_NT, 0, s>>>(B, npow);
     pfb::k_mgs_lambda<<<M.gflat, pfb::MG_NT, 0, s>>>(B, npow);
-    pfb::k_mgs_evstore<<<4 * h->sm_count, pfb::MG_NT, 0, s>>>(B, npow);
     const int nk = 2 * (nl - 1) + (B.dense ? 1 : 0) + npow * (cb > 0 ? 2 : 1) +
-                   (B.n_tail < nl ? 1 : 0) + 2;
-    (warm ? M.setup_kernels_warm : M.setup_kernels) = nk;
+                   (B.n_tail < nl ? 1 : 0) + 1;
+    (safe ? M.setup_kernels_safe : M.setup_kernels) = nk;
     cudaError_t e = cudaStreamEndCapture(s, &g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MGS setup capture: ") + cudaGetErrorString(e));
-    e = cudaGraphInstantiate(warm ? &M.setup_warm_exec : &M.setup_exec, g, 0);
+    e = cudaGraphInstantiate(safe ? &M.setup_safe_exec : &M.setup_exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(h, PF_ERR_CUDA, std::string("MGS setup graph: ") + cudaGetErrorString(e));
   }
@@ -2432,7 +2435,8 @@ static pf_status run_mg(pf_handle* h, MgInst& M, double* target, int* status, lo
 // one scalar phase-field MG-PCG solve on (rd, dinvd, b): fresh hierarchy, then the solve graph
 // (device-side WHILE); the solution lands in xd, rd is consumed
 static pf_status run_mgs(pf_handle* h, MgsInst& M, int* status, long long* iters,
-                         long long maxiter = -1, double rtol = -1.0, bool check = true) {
+                         long long maxiter = -1, double rtol = -1.0, bool check = true,
+                         bool safe = false) {
   M.in->n_guess = 0;
   M.in->rtol = rtol >= 0.0 ? rtol : h->cfg.cg_rtol;
   M.in->maxiter = maxiter > 0 ? maxiter : (long long)h->cfg.cg_maxiter_factor * h->n_nodes;
@@ -2440,8 +2444,7 @@ static pf_status run_mgs(pf_handle* h, MgsInst& M, int* status, long long* iters
   PF_CUDA(cudaEventRecord(h->ev0, h->stream));
   PF_CUDA(cudaMemcpyAsync((void*)M.A.in, M.in, sizeof(pfb::MgIn), cudaMemcpyHostToDevice,
                           h->stream));
-  const bool warm = M.setups > 0 && M.setup_warm_exec;
-  PF_CUDA(cudaGraphLaunch(warm ? M.setup_warm_exec : M.setup_exec, h->stream));
+  PF_CUDA(cudaGraphLaunch(safe ? M.setup_safe_exec : M.setup_exec, h->stream));
   PF_TRY(launched(h));
   PF_CUDA(cudaGraphLaunch(M.solve_exec, h->stream));
   PF_TRY(launched(h));
@@ -2454,7 +2457,7 @@ static pf_status run_mgs(pf_handle* h, MgsInst& M, int* status, long long* iters
   *iters = h->h_cgres->iters;
   // kernels inside the two graphs (each graph launch was counted once by launched()):
   // setup kernels, init, iterations x body, finish
-  h->acc.launches += (warm ? M.setup_kernels_warm : M.setup_kernels) - 1 + 2 +
+  h->acc.launches += (safe ? M.setup_kernels_safe : M.setup_kernels) - 1 + 2 +
                      (int)(*iters) * M.body_kernels - 1;
   if (h->trace)
     fprintf(stderr, "[pfb200] scalar phase-field mg solve: %lld iterations, %.3f ms\n", *iters, ms);
@@ -2489,10 +2492,9 @@ static pf_status run_mgd(pf_handle* h, bool mom, int* status, long long* iters) 
     h->acc.launches += h->mgu.setup_kernels;
     h->mgu.setups += 1;
   } else {
-    MgsInst& M = h->mgs;
-    const bool warm = M.setups > 0 && M.setup_warm_exec;
-    PF_CUDA(cudaGraphLaunch(warm ? M.setup_warm_exec : M.setup_exec, s));
-    h->acc.launches += warm ? M.setup_kernels_warm : M.setup_kernels;
+    MgsInst& M = h->mgs;  // strips: the safe (MG_POW-step) hierarchy
+    PF_CUDA(cudaGraphLaunch(M.setup_safe_exec, s));
+    h->acc.launches += M.setup_kernels_safe;
     M.setups += 1;
   }
   pfb::k_mgd_init<<<gfl, pfb::MG_NT, 0, s>>>(x, r, comps, h->dm, h->mgd_part);
@@ -2748,8 +2750,21 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
       for (int k = 0; k < ng; ++k) guess[k] = h->warm_d[ws][k];
       bool done = false;
       if (h->mgs.on && !h->comm) {
-        // native scalar multigrid PCG (pf_mgs.cuh) on the phase-field system in place
-        PF_TRY(run_mgs(h, h->mgs, &status, &iters));
+        // native scalar multigrid PCG (pf_mgs.cuh) on the phase-field system in place, on the
+        // fast hierarchy with an iteration budget; past it, the solve is redone on the safe one
+        MgsInst& M = h->mgs;
+        const long long budget = std::max(100LL, 4 * M.last_iters);
+        pf_status ms = run_mgs(h, M, &status, &iters, budget);
+        if (ms == PF_ERR_SINGULAR && (status == pfb::CG_MAXITER || status == pfb::CG_NAN)) {
+          if (h->trace)
+            fprintf(stderr, "[pfb200] phase-field mg solve over budget (%lld iterations): safe "
+                            "hierarchy, redo\n", iters);
+          M.redos += 1;
+          PF_TRY(launch_evo_prepare(h, 1, 0));  // the solve consumed the right-hand side
+          ms = run_mgs(h, M, &status, &iters, -1, -1.0, true, true);
+        }
+        PF_TRY(ms);
+        M.last_iters = iters;
         PF_TRY(axpy(h, h->d, h->xd, h->n_nodes));
         done = true;
       }

@@ -50,12 +50,13 @@ struct MgLevel {
   int item_off;   // first thread of this level in the power steps' coarse thread space
   int lpn;        // lanes per node of the level's node kernels (1 | 4 | 16)
   int scalar;     // phase field (phys 1): only the xx entry of each 2x2 block is non-zero
+  int s32;        // grid-level stencil products from the FP32 copy Sf (default) or from S
   // assembled form (l >= 1), slot-major: nbr [MG_NS][n] neighbour ids, S [MG_NS*4][n] 2x2
   // blocks (xx, xy, yx, yy); rid [12][n] restriction sources on level l-1; pid [4][n]
   // prolongation sources on level l+1 (l <= n_levels-2)
   const int* nbr;
   double* S;
-  float* Sf;      // S rounded to FP32 for the grid-level kernels (PFB_MG_S32; the tail keeps S)
+  float* Sf;      // S rounded to FP32 for the grid-level kernels (s32; the tail keeps S)
   const int* rid;
   const int* pid;
 };
@@ -71,7 +72,6 @@ struct MgIn {  // per-solve inputs (device copy of a pinned host struct, refresh
 };
 struct MgCtl {
   double omega[MG_MAXL];
-  double evscale[MG_MAXL];  // 1 / ||v_last|| per level (warm-started power steps, pf_mgs.cuh)
   double* target;
   double rho_prev, bnorm, atol, rr;
   long long k, maxiter;
@@ -672,21 +672,27 @@ __device__ __forceinline__ double2 hw_sum(double2 v) {  // butterfly over W alig
   }
   return v;
 }
-// The 2x2 block of slot s2 at node id.  The grid-level kernels read it in FP32 (PFB_MG_S32,
-// default): the V-cycle is only the preconditioner -- the PCG's operator, residual and stopping
-// test stay FP64 -- and the coarse levels' stencil products are bound by these loads.
-#ifndef PFB_MG_S32
-#define PFB_MG_S32 1
-#endif
+// The 2x2 block of slot s2 at node id.  The grid-level kernels read it in FP32 (MgLevel::s32,
+// default; PFB200_MG_S32=0 at handle creation: FP64): the V-cycle is only the preconditioner --
+// the PCG's operator, residual and stopping test stay FP64 -- and the coarse levels' stencil
+// products are bound by these loads.  tests/test_gpu_mg.py compares both on cracked states.
 __device__ __forceinline__ void mg_s4(const MgLevel& L, int n, int id, int s2, double& sxx,
                                       double& sxy, double& syx, double& syy) {
-#if PFB_MG_S32
-  const float* Sp = L.Sf + (size_t)(4 * s2) * n + id;
-#else
+  if (L.s32) {
+    const float* Sp = L.Sf + (size_t)(4 * s2) * n + id;
+    sxx = __ldg(Sp);
+    if (L.scalar) {  // the packed scalar field: xy, yx, yy are exactly zero (warp-uniform)
+      sxy = syx = syy = 0.0;
+      return;
+    }
+    sxy = __ldg(Sp + n);
+    syx = __ldg(Sp + 2 * (size_t)n);
+    syy = __ldg(Sp + 3 * (size_t)n);
+    return;
+  }
   const double* Sp = L.S + (size_t)(4 * s2) * n + id;
-#endif
   sxx = __ldg(Sp);
-  if (L.scalar) {  // the packed scalar field: xy, yx, yy are exactly zero (warp-uniform)
+  if (L.scalar) {
     sxy = syx = syy = 0.0;
     return;
   }
@@ -1711,8 +1717,8 @@ __global__ void __launch_bounds__(MG_NT, PFB_MG_POW_MINB) k_mg_pow(MgArgs A, int
   else if (L.lpn == 4) mg_spow<4>(L, vin(L), vout(L), q >> 2);
   else mg_spow<1>(L, vin(L), vout(L), q);
 }
-// omega_l = 4 / (3 lambda_l), lambda_l = ||v_POW|| / ||v_POW-1|| (per-level partials)
-__global__ void __launch_bounds__(MG_NT) k_mg_lambda(MgArgs A) {
+// omega_l = 4 / (3 lambda_l), lambda_l = ||v_npow|| / ||v_npow-1|| (per-level partials)
+__global__ void __launch_bounds__(MG_NT) k_mg_lambda(MgArgs A, int npow) {
   __shared__ double red[MG_WARPS * 2 * MG_MAXL];
   double v[2 * MG_MAXL];
 #pragma unroll
@@ -1722,8 +1728,8 @@ __global__ void __launch_bounds__(MG_NT) k_mg_lambda(MgArgs A) {
 #pragma unroll
   for (int l = 0; l < MG_MAXL; ++l) {
     if (l >= A.n_levels) break;
-    const double* a1 = (MG_POW & 1) ? A.L[l].t : A.L[l].e;
-    const double* a0 = (MG_POW & 1) ? A.L[l].e : A.L[l].t;
+    const double* a1 = (npow & 1) ? A.L[l].t : A.L[l].e;
+    const double* a0 = (npow & 1) ? A.L[l].e : A.L[l].t;
     const long long n = 2LL * A.L[l].m.n_nodes;
     for (long long i = tid; i < n; i += nth) {
       const double x1 = __ldcg(a1 + i), x0 = __ldcg(a0 + i);

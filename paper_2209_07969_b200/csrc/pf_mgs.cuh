@@ -18,7 +18,7 @@
 //   * assembled 10-slot scalar stencils (3x3 + the slit tip's second face); grid levels read
 //     them in FP32 (preconditioner only: the PCG's operator, residual recurrence, dot products
 //     and stopping test stay FP64), the single-CTA tail in FP64 from shared memory;
-//   * damped Jacobi V(1,1) with omega_l = 4 / (3 lambda_l), lambda_l from MG_POW power steps;
+//   * damped Jacobi V(1,1) with omega_l = 4 / (3 lambda_l), lambda_l from MGS_POW power steps;
 //   * coarsest level by a dense inverse (<= MGS_DENSE_MAX nodes) or nu_c Jacobi sweeps.
 // Reductions: per-CTA partials summed in a fixed order (bit-reproducible run to run).
 #pragma once
@@ -27,6 +27,11 @@ namespace pfb {
 
 constexpr int MGS_DENSE_MAX = 64;  // coarsest level by a dense inverse when n_nodes <= this
 constexpr int MGS_TAIL_P = 2;      // node passes of the tail's top level (MG_TAIL_NT / 4 each)
+// power steps per setup: 4 from a hashed start.  The estimate of lambda_max(D^-1 A) is then a
+// little low, omega = 4 / (3 lambda) a little larger -- and the V-cycle better: cfg5 load steps
+// 3-6 need 140-143 phase-field iterations with 4 steps, 147-166 with 6, 154-173 with 8 and
+// 153-185 with 3 (PFB200_MGS_POW)
+constexpr int MGS_POW = 4;
 
 struct MgsLevel {
   DMesh m;
@@ -40,7 +45,7 @@ struct MgsLevel {
   float* Sf;      // [MG_NS][n] FP32 stencil (grid levels)
   const int* rid; // [12][n] restriction sources on level l-1
   const int* pid; // [4][n] prolongation sources on level l+1
-  double* ev;     // [n] dominant-eigenvector estimate of D^-1 A (warm start of the power steps)
+  double* ev;     // [n] start vector of the power steps when pow_warm (experiments; unused)
   int items, item_off, lpn, in_tail;
 };
 
@@ -624,8 +629,7 @@ __global__ void __launch_bounds__(MG_TAIL_NT) k_mgs_pow_tail(MgsArgs A, int npow
     __syncthreads();
   }
 }
-// omega_l = 4 / (3 lambda_l), lambda_l = ||v_npow|| / ||v_npow-1|| (per-level partials);
-// evscale_l = 1 / ||v_npow|| for k_mgs_evstore
+// omega_l = 4 / (3 lambda_l), lambda_l = ||v_npow|| / ||v_npow-1|| (per-level partials)
 __global__ void __launch_bounds__(MG_NT) k_mgs_lambda(MgsArgs A, int npow) {
   __shared__ double red[MG_WARPS * 2 * MG_MAXL];
   double v[2 * MG_MAXL];
@@ -652,20 +656,8 @@ __global__ void __launch_bounds__(MG_NT) k_mgs_lambda(MgsArgs A, int npow) {
       const int l = threadIdx.x;
       const double lam = (l < A.n_levels && g[2 * l + 1] > 0.0) ? sqrt(g[2 * l] / g[2 * l + 1]) : 1.0;
       A.ctl->omega[l] = 4.0 / (3.0 * (lam > 0.0 ? lam : 1.0));
-      A.ctl->evscale[l] = g[2 * l] > 0.0 ? 1.0 / sqrt(g[2 * l]) : 0.0;
     }
     if (threadIdx.x == 0) A.ctl->count = 0;
-  }
-}
-// keep the normalised last power vector of every level as the next setup's start vector
-__global__ void __launch_bounds__(MG_NT) k_mgs_evstore(MgsArgs A, int npow) {
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nth = (long long)gridDim.x * blockDim.x;
-  for (int l = 0; l < A.n_levels; ++l) {
-    const double* v = (npow & 1) ? A.L[l].t : A.L[l].e;
-    const double sc = __ldcg(&A.ctl->evscale[l]);
-    double* ev = A.L[l].ev;
-    for (long long i = tid; i < A.L[l].m.n_nodes; i += nth) ev[i] = sc * __ldcg(v + i);
   }
 }
 // dense inverse of the coarsest level (one CTA): assembled from its cell matrices, Gauss-Jordan

@@ -148,3 +148,34 @@ def test_phase_field_mg_matches(cuda_ok, monkeypatch, case_name, scheme, steps, 
         scale = max(1.0e-12, float(np.max(np.abs(g0[key]))))
         assert np.max(np.abs(g0[key] - g1[key])) <= 1e-7 * scale, key
     assert sum(x.cg_iters_d for x in s1) < sum(x.cg_iters_d for x in s0)
+
+
+@pytest.mark.parametrize("case_name,scheme", [("cfg1", "ST"), ("shear32", "S3")])
+def test_fp32_coarse_stencils_on_cracked_states(cuda_ok, monkeypatch, case_name, scheme):
+    """The V-cycle's grid levels read FP32 copies of the coarse stencils by default.  Through the
+    crack (cfg1's fully cracked step 65: g(d) down to 1e-6 next to intact cells; the shear case's
+    post-peak S3 steps) the FP32 and FP64 coarse stencils (PFB200_MG_S32=0) give the same
+    staggered counts and momentum PCG counts within 10%: the FP32 rounding of the coarse
+    couplings does not weaken the preconditioner where the degraded couplings are smallest."""
+    from paper_2209_07969_b200.session import DeviceSession
+
+    case = C.get_case(case_name)
+    runs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PFB200_MG_S32", flag)
+        pb = C.setup(case, C.b200_api())
+        s = DeviceSession(pb.disc.layout, pb.params, pb.config, device=0)
+        s.push_state(pb.state)
+        stats = [s.step(scheme, pb.bcs, pb.pins) for _ in range(case.n_steps)]
+        runs[flag] = ([x.n_stag for x in stats], [x.cg_iters_u for x in stats], s.pull()["d"])
+        s.close()
+    from conftest import stag_band
+
+    (st32, it32, d32), (st64, it64, d64) = runs["1"], runs["0"]
+    crack = int(np.argmax(st64))
+    band = stag_band(case_name, scheme, case.n_steps)  # +-1, the round-off band at crack steps
+    for k, (a, b) in enumerate(zip(st32, st64)):
+        assert abs(a - b) <= band[k], (k, a, b, band[k])
+    assert abs(sum(it32) - sum(it64)) <= 0.1 * sum(it64), (sum(it32), sum(it64))
+    post = slice(crack, None)
+    assert sum(it32[post]) <= 1.1 * sum(it64[post]) + 5, (it32[post], it64[post])
