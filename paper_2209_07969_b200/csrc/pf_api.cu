@@ -46,6 +46,7 @@ struct MgInst {
   long long setups = 0;
   int setup_kernels = 0, body_kernels = 0;  // kernel nodes per graph (launch accounting)
   bool fuse = true;  // fused down / up kernels on the half-warp levels (PFB200_MG_FUSE=0: off)
+  bool rows = true;  // row-table kernels on the one-thread-per-node levels (PFB200_MG_ROWS=0)
   cudaGraphExec_t vcycle_exec = nullptr;  // row strips: one V-cycle z = M^-1 r (pf_mgd.cuh)
   int vcycle_kernels = 0;
 };
@@ -64,6 +65,7 @@ struct MgsInst {
   // overruns its budget -- an underestimated lambda can make the smoother diverge)
   cudaGraphExec_t setup_exec = nullptr, setup_safe_exec = nullptr, solve_exec = nullptr;
   int setup_kernels_safe = 0;
+  bool rows = true;  // row-table kernels on the one-thread-per-node levels (PFB200_MGS_ROWS=0: off)
   long long last_iters = 0, redos = 0;
   cudaGraphExec_t vcycle_exec = nullptr;  // row strips: one V-cycle z = M^-1 r (pf_mgd.cuh)
   int vcycle_kernels = 0;
@@ -645,6 +647,8 @@ static pf_status st_setup(pf_handle* h) {
 static pf_status mg_setup(pf_handle* h, MgInst& M, int phys, int fine_resident_warps) {
   const char* fz = getenv("PFB200_MG_FUSE");
   M.fuse = !(fz && std::string(fz) == "0");
+  const char* rz = getenv("PFB200_MG_ROWS");
+  M.rows = !(rz && std::string(rz) == "0");
 
   const char* tl = getenv("PFB200_MG_TAIL");  // tail levels: at most this many nodes
   const int tail_nodes = tl ? std::max(0, atoi(tl)) : 1 << 30;
@@ -884,6 +888,9 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
       // 7.5 / 6.4 vs 7.8 / 6.9)
       if (M.lpn[l] == 16 && M.fuse && B.L[l].m.n_nodes <= 8192) {
         pfb::k_mg_sdown<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
+      } else if (M.lpn[l] == 1 && M.rows) {  // large levels: row-table ids (bitwise equal)
+        pfb::k_mg_rrestrict<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l);
+        pfb::k_mg_rresid<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l);
       } else {
         MG_NODE_KERNEL(k_mg_srestrict, l, B, l);
         MG_NODE_KERNEL(k_mg_sresid, l, B, l);
@@ -906,6 +913,10 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
     for (int l = top - 1; l >= 1; --l) {
       if (M.lpn[l] == 16 && M.fuse) {
         pfb::k_mg_sup<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
+      } else if (M.lpn[l] == 1 && M.rows) {
+        // (the prolongation keeps its 16-byte index table: the row-table version measured slower)
+        MG_NODE_KERNEL(k_mg_sprolongate, l, B, l);
+        pfb::k_mg_rsmooth<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l);
       } else {
         MG_NODE_KERNEL(k_mg_sprolongate, l, B, l);
         MG_NODE_KERNEL(k_mg_ssmooth, l, B, l);
@@ -1009,6 +1020,8 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M);
 static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
   const char* fz = getenv("PFB200_MG_FUSE");
   M.fuse = !(fz && std::string(fz) == "0");
+  const char* rz = getenv("PFB200_MGS_ROWS");
+  M.rows = !(rz && std::string(rz) == "0");
   const char* nc = getenv("PFB200_MG_NUC");
   const int nu_c = nc ? std::max(1, atoi(nc)) : 16;
   std::vector<HostLevel> lv(1, hl_level0(h));
@@ -1201,7 +1214,7 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
     const int cb = (B.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
     for (int k = 1; k <= npow; ++k) {
       pfb::k_mgs_pow<<<M.gf, pfb::MG_NT, 0, s>>>(B, k, M.gf);
-      if (cb > 0) pfb::k_mgs_pow<<<cb, pfb::MG_NT, 0, s>>>(B, k, 0);
+      if (cb > 0) pfb::k_mgs_pow_coarse<<<cb, pfb::MG_NT, 0, s>>>(B, k);
     }
     if (B.n_tail < nl) pfb::k_mgs_pow_tail<<<1, pfb::MG_TAIL_NT, 0, s>>>(B, npow);
     pfb::k_mgs_lambda<<<M.gflat, pfb::MG_NT, 0, s>>>(B, npow);
@@ -1226,6 +1239,9 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
     for (int l = 1; l < top; ++l) {
       if (M.lpn[l] == 16 && M.fuse && B.L[l].m.n_nodes <= 8192) {
         pfb::k_mgs_sdown<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
+      } else if (M.lpn[l] == 1 && M.rows) {  // large levels: row-table ids (bitwise equal)
+        pfb::k_mgs_rrestrict<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l);
+        pfb::k_mgs_rresid<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l);
       } else {
         MGS_NODE_KERNEL(k_mgs_srestrict, l, B, l);
         MGS_NODE_KERNEL(k_mgs_sresid, l, B, l);
@@ -1248,6 +1264,11 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
     for (int l = top - 1; l >= 1; --l) {
       if (M.lpn[l] == 16 && M.fuse) {
         pfb::k_mgs_sup<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
+      } else if (M.lpn[l] == 1 && M.rows) {
+        // (the prolongation keeps its 16-byte index table: the row-table version measured
+        // 160 us against 131 us at cfg5's level 1)
+        MGS_NODE_KERNEL(k_mgs_sprolongate, l, B, l);
+        pfb::k_mgs_rsmooth<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l);
       } else {
         MGS_NODE_KERNEL(k_mgs_sprolongate, l, B, l);
         MGS_NODE_KERNEL(k_mgs_ssmooth, l, B, l);

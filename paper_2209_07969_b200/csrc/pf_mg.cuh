@@ -916,6 +916,108 @@ __global__ void __launch_bounds__(MG_NT) k_mg_sup(MgArgs A, int l) {
     }
   }
 }
+// ---- large coarse levels, one thread per node over (row, 32-column chunk) items: neighbour /
+// restriction / prolongation ids from the row tables where the stencil is regular (as
+// pf_mgs.cuh's k_mgs_r*: the same products in the same order as the table kernels, bitwise
+// equal; 40 B per node less index traffic per stencil product, 48 B per restriction)
+__device__ __forceinline__ bool mg_regular(const DMesh& m, int i, int j, int4 rw) {
+  if (j <= 0 || j >= m.ny || i <= rw.x || i >= rw.y - 1) return false;
+  if (m.notch_row >= 0 && j >= m.notch_row - 1 && j <= m.notch_row + 1) return false;
+  const int4 a = __ldg(m.nrow + j - 1), b = __ldg(m.nrow + j + 1);
+  return a.x == rw.x && a.y == rw.y && b.x == rw.x && b.y == rw.y;
+}
+template <class X>
+__device__ __forceinline__ double2 mg_row_apply(const MgLevel& L, int n, int id, int i, int j,
+                                                bool dup, X&& xval) {
+  double2 acc = make_double2(0.0, 0.0);
+  const int4 rw = __ldg(L.m.nrow + j);
+  if (!dup && mg_regular(L.m, i, j, rw)) {
+    const int len = rw.y - rw.x;
+#pragma unroll
+    for (int s2 = 0; s2 < 9; ++s2) {
+      const int k = id + (s2 / 3 - 1) * len + (s2 % 3 - 1);
+      double sxx, sxy, syx, syy;
+      mg_s4(L, n, id, s2, sxx, sxy, syx, syy);
+      const double2 x = xval(k);
+      acc.x += sxx * x.x + sxy * x.y;
+      acc.y += syx * x.x + syy * x.y;
+    }
+  } else {
+#pragma unroll
+    for (int s2 = 0; s2 < MG_NS; ++s2) {
+      const double2 v = mg_slot_apply(L, n, id, s2, xval);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+  }
+  return acc;
+}
+__global__ void __launch_bounds__(MG_NT) k_mg_rrestrict(MgArgs A, int l) {
+  const MgLevel& L = A.L[l];
+  const DMesh& mf = A.L[l - 1].m;
+  const int n = L.m.n_nodes;
+  const double* tf = A.L[l - 1].t;
+  mg_for_nodes<GMem>(L.m, (int)(blockIdx.x * MG_WARPS + (threadIdx.x >> 5)), (int)(gridDim.x * MG_WARPS), [&](int id, int I, int J, bool dup) {
+    double2 v = make_double2(0.0, 0.0);
+    const int j0 = 2 * J, i0 = 2 * I;
+    bool reg = !dup && j0 >= 1 && j0 < mf.ny &&
+               !(mf.notch_row >= 0 && j0 >= mf.notch_row - 1 && j0 <= mf.notch_row + 1);
+    int4 r0 = make_int4(0, 0, 0, 0), rm = r0, rp = r0;
+    if (reg) {
+      r0 = __ldg(mf.nrow + j0);
+      rm = __ldg(mf.nrow + j0 - 1);
+      rp = __ldg(mf.nrow + j0 + 1);
+      reg = rm.x == r0.x && rm.y == r0.y && rp.x == r0.x && rp.y == r0.y && i0 - 1 >= r0.x &&
+            i0 + 1 <= r0.y - 1;
+    }
+    if (reg) {
+      const int st[3] = {rm.z, r0.z, rp.z};
+#pragma unroll
+      for (int s2 = 0; s2 < 9; ++s2) {
+        const double2 t = GMem::v2(tf, st[s2 / 3] + (i0 + (s2 % 3 - 1) - r0.x));
+        const double w = mg_rw(s2);
+        v.x += w * t.x;
+        v.y += w * t.y;
+      }
+    } else {
+#pragma unroll
+      for (int s2 = 0; s2 < 12; ++s2) {
+        const int f = __ldg(L.rid + (size_t)s2 * n + id);
+        if (f >= 0) {
+          const double2 t = GMem::v2(tf, f);
+          const double w = mg_rw(s2);
+          v.x += w * t.x;
+          v.y += w * t.y;
+        }
+      }
+    }
+    d2st(L.b, id, mask2(v, GMem::v2(L.dinv, id)));
+  });
+}
+__global__ void __launch_bounds__(MG_NT) k_mg_rresid(MgArgs A, int l) {
+  const MgLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  mg_for_nodes<GMem>(L.m, (int)(blockIdx.x * MG_WARPS + (threadIdx.x >> 5)), (int)(gridDim.x * MG_WARPS), [&](int id, int i, int j, bool dup) {
+    const double2 Av = mg_row_apply(L, n, id, i, j, dup, [&](int k) -> double2 {
+      const double2 di = GMem::v2(L.dinv, k), bv = GMem::v2(L.b, k);
+      return make_double2(om * di.x * bv.x, om * di.y * bv.y);
+    });
+    const double2 di = GMem::v2(L.dinv, id), bv = GMem::v2(L.b, id);
+    d2st(L.t, id, mask2(make_double2(bv.x - Av.x, bv.y - Av.y), di));
+  });
+}
+__global__ void __launch_bounds__(MG_NT) k_mg_rsmooth(MgArgs A, int l) {
+  const MgLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  mg_for_nodes<GMem>(L.m, (int)(blockIdx.x * MG_WARPS + (threadIdx.x >> 5)), (int)(gridDim.x * MG_WARPS), [&](int id, int i, int j, bool dup) {
+    const double2 Ay = mg_row_apply(L, n, id, i, j, dup, [&](int k) -> double2 { return GMem::v2(L.t, k); });
+    const double2 y = GMem::v2(L.t, id), di = GMem::v2(L.dinv, id), bv = GMem::v2(L.b, id);
+    d2st(L.e, id, make_double2(y.x + om * di.x * (bv.x - Ay.x), y.y + om * di.y * (bv.y - Ay.y)));
+  });
+}
+
 // Jacobi sweep out = in + omega D^-1 (b - A in) (grid coarsest level)
 template <int LPN>
 __global__ void __launch_bounds__(MG_NT) k_mg_ssweep(MgArgs A, int l, const double* in,

@@ -437,6 +437,93 @@ __global__ void __launch_bounds__(MG_NT) k_mgs_coarse_dense(MgsArgs A) {
   }
 }
 
+// ---- large coarse levels, one thread per node over (row, 32-column chunk) items: the
+// neighbour and restriction ids follow from the row tables where the stencil is
+// regular (interior rows of equal extent away from the slit, interior columns); only boundary
+// and slit nodes read the index tables.  Same products in the same order as the table kernels
+// (bitwise-identical results), about 40 B per node less traffic per stencil product (the
+// neighbour ids) and 48 B per restriction.  The prolongation keeps its 16-byte table.
+__device__ __forceinline__ bool mgs_regular(const DMesh& m, int i, int j, int4 rw) {
+  if (j <= 0 || j >= m.ny || i <= rw.x || i >= rw.y - 1) return false;
+  if (m.notch_row >= 0 && j >= m.notch_row - 1 && j <= m.notch_row + 1) return false;
+  const int4 a = __ldg(m.nrow + j - 1), b = __ldg(m.nrow + j + 1);
+  return a.x == rw.x && a.y == rw.y && b.x == rw.x && b.y == rw.y;
+}
+template <class X>
+__device__ __forceinline__ double mgs_row_apply(const MgsLevel& L, int n, int id, int i, int j,
+                                                bool dup, X&& xval) {
+  double acc = 0.0;
+  const int4 rw = __ldg(L.m.nrow + j);
+  if (!dup && mgs_regular(L.m, i, j, rw)) {
+    const int len = rw.y - rw.x;
+#pragma unroll
+    for (int s2 = 0; s2 < 9; ++s2) {
+      const int k = id + (s2 / 3 - 1) * len + (s2 % 3 - 1);
+      acc += (double)__ldg(L.Sf + (size_t)s2 * n + id) * xval(k);
+    }
+  } else {
+#pragma unroll
+    for (int s2 = 0; s2 < MG_NS; ++s2) acc += mgs_slot_apply(L, n, id, s2, xval);
+  }
+  return acc;
+}
+#define MGS_GW (int)(blockIdx.x * MG_WARPS + (threadIdx.x >> 5)), (int)(gridDim.x * MG_WARPS)
+__global__ void __launch_bounds__(MG_NT) k_mgs_rrestrict(MgsArgs A, int l) {
+  const MgsLevel& L = A.L[l];
+  const DMesh& mf = A.L[l - 1].m;
+  const int n = L.m.n_nodes;
+  const double* tf = A.L[l - 1].t;
+  mg_for_nodes<GMem>(L.m, MGS_GW, [&](int id, int I, int J, bool dup) {
+    double v = 0.0;
+    const int j0 = 2 * J, i0 = 2 * I;
+    bool reg = !dup && j0 >= 1 && j0 < mf.ny &&
+               !(mf.notch_row >= 0 && j0 >= mf.notch_row - 1 && j0 <= mf.notch_row + 1);
+    int4 r0 = make_int4(0, 0, 0, 0), rm = r0, rp = r0;
+    if (reg) {
+      r0 = __ldg(mf.nrow + j0);
+      rm = __ldg(mf.nrow + j0 - 1);
+      rp = __ldg(mf.nrow + j0 + 1);
+      reg = rm.x == r0.x && rm.y == r0.y && rp.x == r0.x && rp.y == r0.y && i0 - 1 >= r0.x &&
+            i0 + 1 <= r0.y - 1;
+    }
+    if (reg) {
+      const int st[3] = {rm.z, r0.z, rp.z};
+#pragma unroll
+      for (int s2 = 0; s2 < 9; ++s2) {
+        const int f = st[s2 / 3] + (i0 + (s2 % 3 - 1) - r0.x);
+        v += mg_rw(s2) * __ldg(tf + f);
+      }
+    } else {
+#pragma unroll
+      for (int s2 = 0; s2 < 12; ++s2) {
+        const int f = __ldg(L.rid + (size_t)s2 * n + id);
+        if (f >= 0) v += mg_rw(s2) * __ldg(tf + f);
+      }
+    }
+    L.b[id] = mgs_mask(v, __ldg(L.dinv + id));
+  });
+}
+__global__ void __launch_bounds__(MG_NT) k_mgs_rresid(MgsArgs A, int l) {
+  const MgsLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  mg_for_nodes<GMem>(L.m, MGS_GW, [&](int id, int i, int j, bool dup) {
+    const double Av = mgs_row_apply(L, n, id, i, j, dup, [&](int k) -> double {
+      return om * __ldg(L.dinv + k) * __ldg(L.b + k);
+    });
+    L.t[id] = mgs_mask(__ldg(L.b + id) - Av, __ldg(L.dinv + id));
+  });
+}
+__global__ void __launch_bounds__(MG_NT) k_mgs_rsmooth(MgsArgs A, int l) {
+  const MgsLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double om = __ldcg(&A.ctl->omega[l]);
+  mg_for_nodes<GMem>(L.m, MGS_GW, [&](int id, int i, int j, bool dup) {
+    const double Ay = mgs_row_apply(L, n, id, i, j, dup, [&](int k) -> double { return __ldg(L.t + k); });
+    L.e[id] = __ldg(L.t + id) + om * __ldg(L.dinv + id) * (__ldg(L.b + id) - Ay);
+  });
+}
+
 // power step at one node of a coarse level: vout = D^-1 A vin (vin == nullptr: hashed start)
 template <int LPN>
 __device__ __forceinline__ void mgs_spow(const MgsLevel& L, const double* vin, double* vout,
@@ -605,6 +692,21 @@ __global__ void __launch_bounds__(MG_NT, 3) k_mgs_pow(MgsArgs A, int step, int f
   if (L.lpn == 16) mgs_spow<16>(L, vin(L), vout(L), q >> 4);
   else if (L.lpn == 4) mgs_spow<4>(L, vin(L), vout(L), q >> 2);
   else mgs_spow<1>(L, vin(L), vout(L), q);
+}
+// the coarse grid levels' power step on its own (a light kernel at full occupancy: inside the
+// march kernel's register budget it took 2.0 ms per step at cfg5)
+__global__ void __launch_bounds__(MG_NT) k_mgs_pow_coarse(MgsArgs A, int step) {
+  const int t = blockIdx.x * MG_NT + threadIdx.x;
+  if (t >= A.coarse_items) return;
+  int l = 1;
+  while (l + 1 < A.n_tail && t >= A.L[l + 1].item_off) ++l;
+  const MgsLevel& L = A.L[l];
+  const double* vin = step == 1 ? (A.pow_warm ? L.ev : nullptr) : (((step - 1) & 1) ? L.t : L.e);
+  double* vout = (step & 1) ? L.t : L.e;
+  const int q = t - L.item_off;
+  if (L.lpn == 16) mgs_spow<16>(L, vin, vout, q >> 4);
+  else if (L.lpn == 4) mgs_spow<4>(L, vin, vout, q >> 2);
+  else mgs_spow<1>(L, vin, vout, q);
 }
 // power steps of the tail levels (FP64 stencils), one CTA, all MG_POW steps
 __global__ void __launch_bounds__(MG_TAIL_NT) k_mgs_pow_tail(MgsArgs A, int npow) {
