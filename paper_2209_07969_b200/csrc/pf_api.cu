@@ -888,7 +888,7 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
       // 7.5 / 6.4 vs 7.8 / 6.9)
       if (M.lpn[l] == 16 && M.fuse && B.L[l].m.n_nodes <= 8192) {
         pfb::k_mg_sdown<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
-      } else if (M.lpn[l] == 1 && M.rows) {  // large levels: row-table ids (bitwise equal)
+      } else if (M.lpn[l] == 1 && M.rows && B.L[l].m.n_nodes >= (1 << 20)) {  // large levels: row-table ids (bitwise equal)
         pfb::k_mg_rrestrict<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l);
         pfb::k_mg_rresid<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l);
       } else {
@@ -913,7 +913,7 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
     for (int l = top - 1; l >= 1; --l) {
       if (M.lpn[l] == 16 && M.fuse) {
         pfb::k_mg_sup<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
-      } else if (M.lpn[l] == 1 && M.rows) {
+      } else if (M.lpn[l] == 1 && M.rows && B.L[l].m.n_nodes >= (1 << 20)) {
         // (the prolongation keeps its 16-byte index table: the row-table version measured slower)
         MG_NODE_KERNEL(k_mg_sprolongate, l, B, l);
         pfb::k_mg_rsmooth<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l);
@@ -1239,7 +1239,7 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
     for (int l = 1; l < top; ++l) {
       if (M.lpn[l] == 16 && M.fuse && B.L[l].m.n_nodes <= 8192) {
         pfb::k_mgs_sdown<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
-      } else if (M.lpn[l] == 1 && M.rows) {  // large levels: row-table ids (bitwise equal)
+      } else if (M.lpn[l] == 1 && M.rows && B.L[l].m.n_nodes >= (1 << 20)) {  // large levels: row-table ids (bitwise equal)
         pfb::k_mgs_rrestrict<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l);
         pfb::k_mgs_rresid<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l);
       } else {
@@ -1264,7 +1264,7 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
     for (int l = top - 1; l >= 1; --l) {
       if (M.lpn[l] == 16 && M.fuse) {
         pfb::k_mgs_sup<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
-      } else if (M.lpn[l] == 1 && M.rows) {
+      } else if (M.lpn[l] == 1 && M.rows && B.L[l].m.n_nodes >= (1 << 20)) {
         // (the prolongation keeps its 16-byte index table: the row-table version measured
         // 160 us against 131 us at cfg5's level 1)
         MGS_NODE_KERNEL(k_mgs_sprolongate, l, B, l);
