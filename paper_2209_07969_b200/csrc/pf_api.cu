@@ -24,6 +24,28 @@
 
 using pfb::CgResult;
 
+// dynamic shared memory of the staged fine marches (pf_mg.cuh mg_march_st; PFB_MST bit per kernel)
+static constexpr size_t SM_MGS_RESID = (PFB_MST & 1) ? pfb::MStage<pfb::SFineResid>::CTA : 0;
+static constexpr size_t SM_MGS_SMOOTH = (PFB_MST & 2) ? pfb::MStage<pfb::SFineSmooth>::CTA : 0;
+static constexpr size_t SM_MGS_PCG = (PFB_MST & 4) ? pfb::MStage<pfb::SFinePcg>::CTA : 0;
+static constexpr size_t SM_MG_RESID = (PFB_MST & 8) ? pfb::MStage<pfb::FineResid>::CTA : 0;
+static constexpr size_t SM_MG_SMOOTH = (PFB_MST & 16) ? pfb::MStage<pfb::FineSmooth>::CTA : 0;
+static constexpr size_t SM_MG_PCG = (PFB_MST & 32) ? pfb::MStage<pfb::FinePcg>::CTA : 0;
+static cudaError_t mst_opt_in() {  // per device and process: idempotent
+  cudaError_t e = cudaSuccess;
+  auto set = [&](const void* fn, size_t bytes) {
+    if (e == cudaSuccess && bytes)
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  };
+  set((const void*)pfb::k_mgs_fine_resid, SM_MGS_RESID);
+  set((const void*)pfb::k_mgs_fine_smooth, SM_MGS_SMOOTH);
+  set((const void*)pfb::k_mgs_pcg, SM_MGS_PCG);
+  set((const void*)pfb::k_mg_fine_resid, SM_MG_RESID);
+  set((const void*)pfb::k_mg_fine_smooth, SM_MG_SMOOTH);
+  set((const void*)pfb::k_mg_pcg, SM_MG_PCG);
+  return e;
+}
+
 // One multigrid PCG instance (pf_mg.cuh): the momentum solves (phys 0) and the phase-field
 // solves without the SPD probe (phys 1, the scalar field embedded as the x component of a
 // two-component system) each have their own hierarchy, buffers and graphs.
@@ -125,6 +147,8 @@ struct pf_handle {
   static constexpr int WARM_SLOTS = 4;
   bool warm = true;
   bool trace = false;
+  bool mgs_gated = true;  // gated (S1/S2/S3) phase-field solves by the scalar multigrid PCG with
+                          // the SPD probe inside (PFB200_MGS_GATED=0: the Jacobi-PCG probe)
   // cfg2 load steps 4..13, Jacobi momentum PCG iterations: depth 1 69634, 3 52336, 4 52151,
   // 5 51805; MG bench (phase-field tables): depth 3 682, 5 538 phase-field iterations.  The
   // multigrid solves use the first MG_WARM = 3 entries.
@@ -219,8 +243,11 @@ static pf_status launched(pf_handle* h) {
 
 template <class T>
 static pf_status dalloc(pf_handle* h, T** p, size_t n) {
-  PF_CUDA(cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T)));
-  PF_CUDA(cudaMemsetAsync(*p, 0, std::max<size_t>(n, 1) * sizeof(T), h->stream));
+  // padded to a 16-byte multiple: the staged marches' bulk copies of 8-byte arrays end on an even
+  // element (pf_mg.cuh mg_march_st)
+  const size_t bytes = (std::max<size_t>(n, 1) * sizeof(T) + 15) & ~size_t(15);
+  PF_CUDA(cudaMalloc((void**)p, bytes));
+  PF_CUDA(cudaMemsetAsync(*p, 0, bytes, h->stream));
   return PF_OK;
 }
 
@@ -881,7 +908,7 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
   } while (0)
   auto body_kernels = [&](const pfb::MgArgs& B, bool krylov = true) {
     const int c = nl - 1, top = std::min(B.n_tail, c);  // grid levels [1, top)
-    pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(B);
+    pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, SM_MG_RESID, s>>>(B);
     for (int l = 1; l < top; ++l) {
       // fused down-sweep only on the smallest grid levels: it evaluates 12 restriction sources
       // per stencil slot (cfg2, ncu: 16.6 k nodes 13.7 us fused vs 11.8 split; <= 4.2 k nodes
@@ -922,9 +949,9 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
         MG_NODE_KERNEL(k_mg_ssmooth, l, B, l);
       }
     }
-    pfb::k_mg_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(B);
+    pfb::k_mg_fine_smooth<<<M.gf, pfb::MG_NT, SM_MG_SMOOTH, s>>>(B);
     if (!krylov) return;
-    pfb::k_mg_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(B, M.gf);
+    pfb::k_mg_pcg<<<M.gf, pfb::MG_NT, SM_MG_PCG, s>>>(B, M.gf);
     pfb::k_mg_update<<<M.gflat, pfb::MG_NT, 0, s>>>(B, M.gf, M.gf);
   };
   {
@@ -1152,7 +1179,7 @@ static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
   M.gf = (A.g0.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
   {
     int orr = 0;
-    PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&orr, pfb::k_mgs_fine_resid, pfb::MG_NT, 0));
+    PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&orr, pfb::k_mgs_fine_resid, pfb::MG_NT, SM_MGS_RESID));
     A.g0r = pfb::make_march_geom(h->nx, lv[0].ny, std::max(1, orr) * h->sm_count * pfb::MG_WARPS);
     M.gfr = (A.g0r.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
   }
@@ -1235,7 +1262,7 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
   } while (0)
   const int c = nl - 1, top = std::min(A.n_tail, c);
   auto body_kernels = [&](const pfb::MgsArgs& B, bool krylov = true) {
-    pfb::k_mgs_fine_resid<<<M.gfr, pfb::MG_NT, 0, s>>>(B);
+    pfb::k_mgs_fine_resid<<<M.gfr, pfb::MG_NT, SM_MGS_RESID, s>>>(B);
     for (int l = 1; l < top; ++l) {
       if (M.lpn[l] == 16 && M.fuse && B.L[l].m.n_nodes <= 8192) {
         pfb::k_mgs_sdown<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
@@ -1274,9 +1301,9 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
         MGS_NODE_KERNEL(k_mgs_ssmooth, l, B, l);
       }
     }
-    pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(B);
+    pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, SM_MGS_SMOOTH, s>>>(B);
     if (!krylov) return;
-    pfb::k_mgs_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(B, M.gf);
+    pfb::k_mgs_pcg<<<M.gf, pfb::MG_NT, SM_MGS_PCG, s>>>(B, M.gf);
     pfb::k_mgs_update<<<M.gflat, pfb::MG_NT, 0, s>>>(B, M.gf, M.gf);
   };
   M.body_kernels = 4 + (A.n_tail < nl ? 1 : 1 + (A.dense ? 1 : A.nu_c));
@@ -1558,6 +1585,8 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
         for (int k = 0; k < h->warm_depth; ++k) CREATE_ALLOC(h->warm_d[sl][k], nn);
     const char* tr = getenv("PFB200_TRACE");
     h->trace = tr && std::string(tr) == "1";
+    const char* mgg = getenv("PFB200_MGS_GATED");
+    h->mgs_gated = !(mgg && std::string(mgg) == "0");
   }
   CREATE_CUDA(cudaMemsetAsync(h->umask, 1, 2 * nn, h->stream));
   CREATE_CUDA(cudaMemsetAsync(h->pmask, 1, nn, h->stream));
@@ -1677,11 +1706,12 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
         if (h->h_nst[j] == (int)strip->own_lo) { h->mgd_row0 = j; break; }
     }
     if (want) {
+      CREATE_CUDA(mst_opt_in());
       int om = 0, o2 = 0;
-      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, pfb::k_mg_fine_smooth, pfb::MG_NT, 0));
-      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_mg_pcg, pfb::MG_NT, 0));
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, pfb::k_mg_fine_smooth, pfb::MG_NT, SM_MG_SMOOTH));
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_mg_pcg, pfb::MG_NT, SM_MG_PCG));
       om = std::min(om, o2);
-      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_mg_fine_resid, pfb::MG_NT, 0));
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_mg_fine_resid, pfb::MG_NT, SM_MG_RESID));
       om = std::min(om, o2);
       if (om >= 1) {
         pf_status ms = mg_setup(h, h->mgu, 0, om * dev_sms * pfb::MG_WARPS);
@@ -1698,10 +1728,10 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
           if (es != PF_OK) return bail(es);
         } else if ((mev == "1" || mev == "scalar") && h->mgu.on) {
           int os = 0, o3 = 0;
-          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&os, pfb::k_mgs_fine_smooth, pfb::MG_NT, 0));
-          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, pfb::k_mgs_pcg, pfb::MG_NT, 0));
+          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&os, pfb::k_mgs_fine_smooth, pfb::MG_NT, SM_MGS_SMOOTH));
+          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, pfb::k_mgs_pcg, pfb::MG_NT, SM_MGS_PCG));
           os = std::min(os, o3);
-          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, pfb::k_mgs_fine_resid, pfb::MG_NT, 0));
+          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, pfb::k_mgs_fine_resid, pfb::MG_NT, SM_MGS_RESID));
           os = std::max(1, std::min(os, o3));
           pf_status es = mgs_setup(h, h->mgs, os * dev_sms * pfb::MG_WARPS);
           if (es != PF_OK) return bail(es);
@@ -2457,8 +2487,9 @@ static pf_status run_mg(pf_handle* h, MgInst& M, double* target, int* status, lo
 // (device-side WHILE); the solution lands in xd, rd is consumed
 static pf_status run_mgs(pf_handle* h, MgsInst& M, int* status, long long* iters,
                          long long maxiter = -1, double rtol = -1.0, bool check = true,
-                         bool safe = false) {
+                         bool safe = false, bool probe = false) {
   M.in->n_guess = 0;
+  M.in->probe = probe ? 1 : 0;
   M.in->rtol = rtol >= 0.0 ? rtol : h->cfg.cg_rtol;
   M.in->maxiter = maxiter > 0 ? maxiter : (long long)h->cfg.cg_maxiter_factor * h->n_nodes;
   M.in->target = nullptr;
@@ -2734,9 +2765,37 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
       // SPD predicate for K_dd + K~ (replaces check_spd, linsolve.py:58-77): a non-positive
       // diagonal, or non-positive curvature p.Ap inside PCG, means "not positive definite"
       bool fallback = nonpos_diag;
+      const bool mgs_gated = h->mgs.on && !h->comm && h->mgs_gated;
       if (!fallback) {
-        PF_TRY(run_cg(h, false, nullptr, true, &status, &iters));
-        fallback = status == pfb::CG_INDEFINITE;
+        bool decided = false;
+        if (mgs_gated) {
+          // the probe inside the scalar multigrid PCG (k_mgs_update): p.Ap <= 0 => not positive
+          // definite; converged => the Jacobi PCG's verdict "no non-positive curvature met".
+          // Anything else (iteration budget, a non-finite residual from a hierarchy built on an
+          // indefinite matrix) decides nothing: the Jacobi-PCG probe below redoes the solve.
+          MgsInst& M = h->mgs;
+          const long long budget = std::max(100LL, 4 * M.last_iters);
+          const pf_status ms = run_mgs(h, M, &status, &iters, budget, -1.0, true, false, true);
+          if (ms != PF_OK && !(ms == PF_ERR_SINGULAR &&
+                               (status == pfb::CG_MAXITER || status == pfb::CG_NAN)))
+            return ms;
+          if (ms == PF_OK && status == pfb::CG_INDEFINITE) {
+            fallback = decided = true;
+          } else if (ms == PF_OK) {
+            M.last_iters = iters;
+            decided = true;
+          } else {
+            if (h->trace)
+              fprintf(stderr, "[pfb200] gated phase-field mg solve undecided (status %d, %lld "
+                              "iterations): Jacobi-PCG probe\n", status, iters);
+            M.redos += 1;
+            PF_TRY(launch_evo_prepare(h, 1, extra));  // the solve consumed the right-hand side
+          }
+        }
+        if (!decided) {
+          PF_TRY(run_cg(h, false, nullptr, true, &status, &iters));
+          fallback = status == pfb::CG_INDEFINITE;
+        }
       }
       if (fallback) {  // plain tangent for this staggered iteration (schemes.py:293-301)
         PF_TRY(launch_evo_prepare(h, 1, 0));
@@ -2744,7 +2803,19 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
           PF_TRY(halo(h, h->rd, 1));
           PF_TRY(halo(h, h->dinvd, 1));
         }
-        PF_TRY(run_cg(h, false, nullptr, false, &status, &iters));
+        bool solved = false;
+        if (mgs_gated) {
+          MgsInst& M = h->mgs;
+          const long long budget = std::max(100LL, 4 * M.last_iters);
+          const pf_status ms = run_mgs(h, M, &status, &iters, budget);
+          if (ms != PF_OK && !(ms == PF_ERR_SINGULAR &&
+                               (status == pfb::CG_MAXITER || status == pfb::CG_NAN)))
+            return ms;
+          solved = ms == PF_OK;
+          if (solved) M.last_iters = iters;
+          else PF_TRY(launch_evo_prepare(h, 1, 0));
+        }
+        if (!solved) PF_TRY(run_cg(h, false, nullptr, false, &status, &iters));
         *fallbacks += 1;
       }
       PF_TRY(halo(h, h->xd, 1));
@@ -3207,13 +3278,13 @@ extern "C" pf_status pf_bench_mg_kernel(pf_handle* h, int which, int reps, doubl
     const double n1 = A.L[1].m.n_nodes;
     if (which == 0) {
       bytes = 56.0 * n + e;  // r, D^-1 (16 B), d (8 B), t (16 B); branch bits 1 B per cell
-      PF_TRY(run([&] { pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));
+      PF_TRY(run([&] { pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, SM_MG_RESID, s>>>(A); }));
     } else if (which == 1) {
       bytes = 56.0 * n + 16.0 * n1 + e;  // r, D^-1, d, z; level-1 correction; bits
-      PF_TRY(run([&] { pfb::k_mg_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));
+      PF_TRY(run([&] { pfb::k_mg_fine_smooth<<<M.gf, pfb::MG_NT, SM_MG_SMOOTH, s>>>(A); }));
     } else {
       bytes = 88.0 * n + e;  // z, p_old, d, D^-1, p_new, q; bits
-      PF_TRY(run([&] { pfb::k_mg_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(A, M.gf); }));
+      PF_TRY(run([&] { pfb::k_mg_pcg<<<M.gf, pfb::MG_NT, SM_MG_PCG, s>>>(A, M.gf); }));
     }
   } else if (which >= 10 && which <= 12) {
     if (!h->mgs.on || h->mgs.setups == 0) return fail(h, PF_ERR_INVALID, "no built phase-field hierarchy");
@@ -3223,13 +3294,13 @@ extern "C" pf_status pf_bench_mg_kernel(pf_handle* h, int which, int reps, doubl
     const double n1 = A.L[1].m.n_nodes;
     if (which == 10) {
       bytes = 24.0 * n + 32.0 * e;  // r, D^-1, t (8 B); b per Gauss point (32 B per cell)
-      PF_TRY(run([&] { pfb::k_mgs_fine_resid<<<M.gfr, pfb::MG_NT, 0, s>>>(A); }));
+      PF_TRY(run([&] { pfb::k_mgs_fine_resid<<<M.gfr, pfb::MG_NT, SM_MGS_RESID, s>>>(A); }));
     } else if (which == 11) {
       bytes = 24.0 * n + 8.0 * n1 + 32.0 * e;  // r, D^-1, z; level-1 correction; b
-      PF_TRY(run([&] { pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));
+      PF_TRY(run([&] { pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, SM_MGS_SMOOTH, s>>>(A); }));
     } else {
       bytes = 40.0 * n + 32.0 * e;  // z, p_old, D^-1, p_new, q; b
-      PF_TRY(run([&] { pfb::k_mgs_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(A, M.gf); }));
+      PF_TRY(run([&] { pfb::k_mgs_pcg<<<M.gf, pfb::MG_NT, SM_MGS_PCG, s>>>(A, M.gf); }));
     }
   } else {
     return fail(h, PF_ERR_INVALID, "pf_bench_mg_kernel: unknown kernel");

@@ -28,8 +28,22 @@
 // (last-block pattern), so every result is bit-reproducible run to run.
 #pragma once
 
+// staged (TMA bulk copy) fine marches, mg_march_st below: bit k switches kernel k to the staged
+// march (1 / 2 / 4: scalar phase-field residual / smoothing / direction; 8 / 16 / 32: momentum);
+// stages per warp of the scalar and the momentum marches
+#ifndef PFB_MST
+#define PFB_MST 0
+#endif
+#ifndef PFB_MST_DS
+#define PFB_MST_DS 3
+#endif
+#ifndef PFB_MST_DM
+#define PFB_MST_DM 4
+#endif
+
 namespace pfb {
 
+constexpr int MST_R8 = 288, MST_R16 = 512, MST_RC = 1024;  // slot regions (mg_march_st)
 constexpr int MG_MAXL = 14;
 constexpr int MG_NT = 256;
 constexpr int MG_WARPS = MG_NT / 32;
@@ -69,6 +83,7 @@ struct MgIn {  // per-solve inputs (device copy of a pinned host struct, refresh
   double* target;                 // optional: target += x at the end
   const double* guess[MG_WARM];   // warm start: x0 = sum y_k guess[k], Galerkin-optimal y
   int n_guess;
+  int probe;                      // SPD probe (pf_mgs.cuh): stop with CG_INDEFINITE at p.Ap <= 0
 };
 struct MgCtl {
   double omega[MG_MAXL];
@@ -283,6 +298,276 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
   }
 }
 
+// TMA bulk copies global -> shared completing on one mbarrier (sizes and addresses are
+// multiples of 16 B: the host pads every multigrid array)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mg_bulk_g2s(const void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mg_mbar_init_expect(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mg_mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ unsigned mg_r16(size_t b) { return (unsigned)((b + 15) & ~size_t(15)); }
+
+// ----------------------------------------------------------------------------------------
+// Staged warp march: mg_march with the node rows (and, for the scalar field, the cell rows) of
+// the next rows brought into shared memory by TMA bulk copies (cp.async.bulk completing on an
+// mbarrier) instead of per-lane loads held in registers.  A warp's 32 columns of a node row are
+// one contiguous run of every nodal array (row-compact numbering), so one elected lane issues
+// one bulk copy per array and row; Op::D stages per warp keep D - 1 rows beyond the current one
+// in flight -- Little's law at ~6.5 TB/s and ~1 us of loaded latency needs ~44 KB in flight per
+// SM, three times what one register-prefetched row per resident warp holds.  A stage (node row
+// t + 1, cell row t) stays valid through iteration t + 1, when its nodes are the march's lower
+// row, so Op::outs reads the per-node data it needs again (r, D^-1) from shared memory instead
+// of reloading it from L1/L2 on the critical path.
+// Op adds to mg_march's interface:
+//   N8 / N16 / CST / D        8-byte and 16-byte nodal arrays, cell records staged?, stages
+//   const double* n8(k), n16(k), const double* cst()   the arrays (nullptr: absent this launch)
+//   void take(slot, e8, e16, Raw&)      the node's staged data (element indices in the slot)
+//   void ctake(cslot, ce, CRaw&)        the cell's staged record (CST)
+//   void ahead(id, i, j)                per-row work outside the stages (prolongation sources)
+//   void outs(slot, e8, e16, id, Av, vin)   out() with the node's stage
+// 8-byte runs start on an even element (16-byte alignment of the bulk copy), so a region holds
+// up to 34 elements.
+template <class Op>
+struct MStage {
+  static constexpr int O16 = Op::N8 * MST_R8;
+  static constexpr int OC = O16 + Op::N16 * MST_R16;
+  static constexpr int SLOT = OC + (Op::CST ? MST_RC : 0);
+  static constexpr int WARP = SLOT * Op::D;
+  static constexpr int CTA = WARP * MG_WARPS;
+};
+__device__ __forceinline__ void mst_bar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mst_bar_expect(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+template <class Op>
+__device__ __forceinline__ void mg_march_st(const DMesh& m, const MarchGeom& G, int unit, Op& op,
+                                            MgWarp& ws, unsigned char* ring,
+                                            unsigned long long* bars) {
+  using ST = MStage<Op>;
+  constexpr int D = Op::D;
+  const int lane = threadIdx.x & 31;
+  const int strip = unit % G.n_strips;
+  const int r0 = (unit / G.n_strips) * G.rows_per_unit;
+  const int r1 = min(r0 + G.rows_per_unit, m.ny + 1);
+  const int col0 = strip * TXW - 1;
+  const int col = col0 + lane;
+  const bool lane_own = lane >= 1 && lane <= TXW;
+  const int R = m.notch_row;
+  const bool dupcol = R >= 0 && col >= m.notch_lo && col < m.notch_hi;
+  const int t0 = r0 - 1;
+  if (lane == 0) {
+#pragma unroll
+    for (int s2 = 0; s2 < D; ++s2) mst_bar_init(bars + s2);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  int base = 0;
+  // row windows of THIS strip: node rows t .. t+31 as (first column, count, first id, bytes of
+  // an 8-byte run) and cell rows as (first column, count, first id): lane l prepares row t + l
+  auto win = [&](int t) {
+    __syncwarp();
+    base = t;
+    const int jj = t + lane;
+    int4 nw = make_int4(0, 0, 0, 0), ew = make_int4(0, 0, 0, 0);
+    if (jj >= 0 && jj <= m.ny) {
+      const int4 rw = __ldg(m.nrow + jj);
+      const int clo = max(col0, rw.x), cnt = min(col0 + 32, rw.y) - clo;
+      if (cnt > 0) {
+        const int id0 = rw.z + (clo - rw.x);
+        nw = make_int4(clo, cnt, id0, (((id0 + cnt + 1) & ~1) - (id0 & ~1)) * 8);
+      }
+    }
+    if (jj >= 0 && jj < m.ny) {
+      const int4 er = __ldg(m.erow + jj);
+      const int elo = max(col0, er.x), ecnt = min(col0 + 31, er.y) - elo;
+      if (ecnt > 0) ew = make_int4(elo, ecnt, er.z + (elo - er.x), 0);
+    }
+    ws.nwin[lane] = nw;
+    ws.ewin[lane] = ew;
+    __syncwarp();
+  };
+  // stage t = node row t + 1 and cell row t, into slot sl (lane 0)
+  auto issue = [&](int t, int sl) {
+    unsigned char* slot = ring + sl * ST::SLOT;
+    const int4 nw = ws.nwin[t + 1 - base];
+    const unsigned b8 = (unsigned)nw.w, b16 = (unsigned)(nw.y * 16);
+    unsigned bc = 0u;
+    int e0 = 0;
+    if (Op::CST) {
+      const int4 ew = ws.ewin[t - base];
+      e0 = ew.z;
+      bc = op.cst() ? (unsigned)(ew.y * 32) : 0u;
+    }
+    unsigned bytes = bc;
+#pragma unroll
+    for (int k = 0; k < Op::N8; ++k) bytes += op.n8(k) ? b8 : 0u;
+#pragma unroll
+    for (int k = 0; k < Op::N16; ++k) bytes += op.n16(k) ? b16 : 0u;
+    mst_bar_expect(bars + sl, bytes);
+    if (nw.y > 0) {
+#pragma unroll
+      for (int k = 0; k < Op::N8; ++k)
+        if (op.n8(k)) mg_bulk_g2s(slot + k * MST_R8, op.n8(k) + (nw.z & ~1), b8, bars + sl);
+#pragma unroll
+      for (int k = 0; k < Op::N16; ++k)
+        if (op.n16(k))
+          mg_bulk_g2s(slot + ST::O16 + k * MST_R16, op.n16(k) + 2 * (size_t)nw.z, b16, bars + sl);
+    }
+    if (Op::CST && bc) mg_bulk_g2s(slot + ST::OC, op.cst() + 4 * (size_t)e0, bc, bars + sl);
+  };
+  auto row_id = [&](int j, int& e8, int& e16) -> int {  // node (col, j) and its slot indices
+    const int4 nw = ws.nwin[j - base];
+    const int k = col - nw.x;
+    if ((unsigned)k >= (unsigned)nw.y) return -1;
+    e16 = k;
+    e8 = k + (nw.z & 1);
+    return nw.z + k;
+  };
+  auto cell_of = [&](int cj, int& ce) -> int {  // cell (col, cj) and its slot index
+    const int4 ew = ws.ewin[cj - base];
+    ce = col - ew.x;
+    return (unsigned)ce < (unsigned)ew.y ? ew.z + ce : -1;
+  };
+  auto load_dup = [&]() {
+    const int id = dupcol ? m.dup_start + (col - m.notch_lo) : -1;
+    double a = 0.0;
+    const double2 v = op.in(id, col, R, true, a);
+    ws.dv[lane] = v;
+    ws.da[lane] = a;
+    ws.did[lane] = id;
+    __syncwarp();
+  };
+  // KEEP: a stage outlives its iteration by one (outs reads it), so D slots hold D - 1 stages
+  // ahead of the consumer; otherwise the slot is refilled as soon as the warp has consumed it
+  constexpr int LA = Op::KEEP ? D - 1 : D;
+  win(t0);
+  if (lane == 0) {
+#pragma unroll 1
+    for (int k = 0; k < LA; ++k)
+      if (t0 + k < r1) issue(t0 + k, k);
+  }
+  double a_lo = 0.0, a_hi = 0.0;
+  int e8_lo = 0, e16_lo = 0;
+  int id_lo = t0 >= 0 ? row_id(t0, e8_lo, e16_lo) : -1;
+  double2 v_lo = op.in(id_lo, col, t0, false, a_lo);
+  bool lo_slit = (t0 == R);
+  if (lo_slit) load_dup();
+  {
+    int x8, x16;
+    const int id_a = row_id(r0, x8, x16);
+    if (id_a >= 0) op.ahead(id_a, col, r0);
+  }
+  typename Op::CRaw c_cur;
+  int e_cur = -1;
+  if (!Op::CST) {
+    int ce;
+    e_cur = cell_of(t0, ce);
+    if (e_cur >= 0) op.cfetch(e_cur, c_cur);
+  }
+  double2 acc_lo = make_double2(0.0, 0.0);
+  int sl = 0;         // slot of the current stage; the previous stage sits in slot sl - 1 (mod D)
+  unsigned ph = 0u;   // parity of slot sl's current use
+  for (int cj = t0; cj < r1; ++cj) {
+    const int jh = cj + 1;
+    if (cj + LA + 1 - base >= 32) win(cj);
+    mg_mbar_wait(bars + sl, ph);
+    const unsigned char* slot = ring + sl * ST::SLOT;
+    const int slp = sl == 0 ? D - 1 : sl - 1;
+    const unsigned char* pslot = ring + slp * ST::SLOT;
+    int e8_hi = 0, e16_hi = 0;
+    const int id_hi = row_id(jh, e8_hi, e16_hi);
+    a_hi = 0.0;
+    double2 v_hi = make_double2(0.0, 0.0);
+    if (id_hi >= 0) {
+      typename Op::Raw w;
+      op.take(slot, e8_hi, e16_hi, w);
+      v_hi = op.finish(w, id_hi, col, jh, false, a_hi);
+    }
+    int eid;
+    typename Op::CRaw c_nx;
+    int e_nx = -1;
+    if (Op::CST) {
+      int ce;
+      eid = cell_of(cj, ce);
+      if (eid >= 0) op.ctake(slot + ST::OC, ce, c_cur);
+    } else {
+      eid = e_cur;
+      int ce;
+      if (cj + 1 < r1) e_nx = cell_of(cj + 1, ce);
+      if (e_nx >= 0) op.cfetch(e_nx, c_nx);
+    }
+    if (jh + 1 <= r1) {
+      int x8, x16;
+      const int id_a = row_id(jh + 1, x8, x16);
+      if (id_a >= 0) op.ahead(id_a, col, jh + 1);
+    }
+    const bool hi_slit = (jh == R);
+    const bool use_dup = lo_slit && dupcol;
+    const double2 b0 = use_dup ? ws.dv[lane] : v_lo;
+    const double e0 = use_dup ? ws.da[lane] : a_lo;
+    const double2 b1 = shfl_dn(b0), t2 = shfl_dn(v_hi);
+    const double e1 = shfl_dn(e0), e2 = shfl_dn(a_hi);
+    double2 f[4];
+    f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
+    if (eid >= 0) {
+      const double2 v[4] = {b0, b1, t2, v_hi};
+      const double a[4] = {e0, e1, e2, a_hi};
+      op.cellr(eid, c_cur, v, a, f);
+    }
+    const double2 c1l = shfl_up(f[1]), c2l = shfl_up(f[2]);
+    // (the shuffles above consumed every lane's reads of the current stage)
+    if (!Op::KEEP && lane == 0 && cj + LA < r1) issue(cj + LA, sl);
+    if (lane_own && cj >= r0) {
+      if (use_dup) {
+        if (id_lo >= 0) op.outs(pslot, e8_lo, e16_lo, id_lo, acc_lo, v_lo);  // lower face
+        const int idd = ws.did[lane];
+        if (idd >= 0) op.out(idd, d2add(c1l, f[0]), ws.dv[lane]);  // upper face
+      } else if (id_lo >= 0) {
+        op.outs(pslot, e8_lo, e16_lo, id_lo, d2add(d2add(acc_lo, c1l), f[0]), v_lo);
+      }
+    }
+    acc_lo = d2add(c2l, f[3]);
+    __syncwarp();  // every lane is done with the previous stage: refill its slot
+    if (Op::KEEP && lane == 0 && cj + LA < r1) issue(cj + LA, slp);
+    if (hi_slit) load_dup();
+    v_lo = v_hi;
+    a_lo = a_hi;
+    id_lo = id_hi;
+    e8_lo = e8_hi;
+    e16_lo = e16_hi;
+    lo_slit = hi_slit;
+    if (!Op::CST) {
+      e_cur = e_nx;
+      c_cur = c_nx;
+    }
+    if (++sl == D) {
+      sl = 0;
+      ph ^= 1u;
+    }
+  }
+}
+
 // ---- fine-level (level 0) node ops for mg_march ---------------------------------------------
 // The fine operator is K_uu(u, d) applied cell by cell (pf_march.cuh mom_cell_fast: branch bits
 // per cell, g(d) at the Gauss points from the nodal d carried as the march's aux value).
@@ -326,7 +611,19 @@ struct FineBase {
     }
   }
   __device__ double2 di(int id) const { return __ldg(reinterpret_cast<const double2*>(dinv) + id); }
+  // staged march (mg_march_st): nodal arrays through shared memory, the cell data (1 B of
+  // branch bits) by cfetch one row step ahead as in mg_march
+  static constexpr bool CST = false;
+  __device__ const double* cst() const { return nullptr; }
+  __device__ void ctake(const unsigned char*, int, CRaw&) const {}
+  __device__ void ahead(int, int, int) const {}
 };
+__device__ __forceinline__ double mst_s8(const unsigned char* slot, int k, int e8) {
+  return reinterpret_cast<const double*>(slot + k * MST_R8)[e8];
+}
+__device__ __forceinline__ double2 mst_s16(const unsigned char* slot, int n8, int k, int e16) {
+  return reinterpret_cast<const double2*>(slot + n8 * MST_R8 + k * MST_R16)[e16];
+}
 
 __device__ __forceinline__ double2 mask2(double2 v, double2 di) {
   return make_double2(di.x != 0.0 ? v.x : 0.0, di.y != 0.0 ? v.y : 0.0);
@@ -359,6 +656,20 @@ struct FineResid : FineBase {  // x = omega D^-1 r (pre-smoothing from zero), t 
   __device__ void out(int id, double2 Av, double2) const {
     const double2 bv = d2ldcg(r, id);
     d2st(t, id, mask2(make_double2(bv.x - Av.x, bv.y - Av.y), di(id)));
+  }
+  static constexpr int N8 = 1, N16 = 2, D = PFB_MST_DM;
+  static constexpr bool KEEP = true;
+  __device__ const double* n8(int) const { return d; }
+  __device__ const double* n16(int k) const { return k == 0 ? dinv : r; }
+  __device__ void take(const unsigned char* slot, int e8, int e16, Raw& w) const {
+    w.dv = mst_s16(slot, N8, 0, e16);
+    w.bv = mst_s16(slot, N8, 1, e16);
+    w.d = mst_s8(slot, 0, e8);
+  }
+  __device__ void outs(const unsigned char* slot, int, int e16, int id, double2 Av,
+                       double2) const {
+    const double2 dv = mst_s16(slot, N8, 0, e16), bv = mst_s16(slot, N8, 1, e16);
+    d2st(t, id, mask2(make_double2(bv.x - Av.x, bv.y - Av.y), dv));
   }
 };
 
@@ -400,66 +711,88 @@ __device__ __forceinline__ double2 mg_prolong(const DMesh& mf, const DMesh& mc,
                       a00 * v00.y + a10 * v10.y + a01 * v01.y + a11 * v11.y);
 }
 
-// The bilinear prolongation of a fine-level march: a lane keeps its fine column i, so its
+// The bilinear prolongation of a fine-level march.  A lane keeps its fine column i, so its
 // coarse sources are the fixed columns I0 = i/2, I1 = I0 + (i odd) of coarse rows J0 = j/2,
-// J1 = J0 + (j odd).  Two coarse rows are cached per lane (keyed by row and slit face): each
-// coarse row is loaded once per two fine rows, in fetch (one row step ahead of its use in
-// finish; fetch(j+1) always follows finish(j)), instead of four row-table lookups and four
-// gathers per fine node.
+// J1 = J0 + (j odd).  The march visits the node rows in order (fetch(j) one row step ahead of
+// finish(j), fetch(j + 1) after finish(j)), so the lane holds exactly two coarse rows -- lo = J0
+// and hi = J0 + 1 -- and moves them by the parity of j: an odd row loads its hi row (one row-
+// table entry and two values per TWO fine rows), an even row takes lo <- hi.  The slit's faces
+// differ only on the coarse slit row, reloaded once when the march passes the fine slit row.
+// A lane whose rows are not consecutive (first row of a unit, holes of an L-panel) starts over.
+// Same products and order as mg_prolong: a00 v00 + a10 v10 + a01 v01 + a11 v11.
 template <class V>
-struct ProlongCache {
-  int aJ = -0x4000, bJ = -0x4000;
-  bool aUp = false, bUp = false;
-  V a0, a1, b0, b1;
+struct ProlongMarch {
+  int last_j = -0x4000;
+  V l0, l1, h0, h1;
   __device__ static V zero();
   __device__ static V load(const double* e, int c);
-  __device__ void fill(const DMesh& mc, const double* ec, int J, bool up, int I0, int I1,
-                       V& v0, V& v1) {
-    const int4 rw = __ldg(mc.nrow + J);
+  __device__ static V comb(double a0, V v0, double a1, V v1, double a2, V v2, double a3, V v3);
+  __device__ static void row(const DMesh& mc, const double* ec, int J, bool up, int I0, int I1,
+                             V& v0, V& v1) {
+    const int4 rw = __ldg(mc.nrow + min(J, mc.ny));
     const int c0 = mg_row_node(mc, rw, I0, J, up);
     const int c1 = I1 != I0 ? mg_row_node(mc, rw, I1, J, up) : -1;
     v0 = c0 >= 0 ? load(ec, c0) : zero();
     v1 = c1 >= 0 ? load(ec, c1) : zero();
   }
-  __device__ bool has(int J, bool up) const {
-    return (aJ == J && aUp == up) || (bJ == J && bUp == up);
-  }
-  // make rows (J0, up) and (J1, up) resident
-  __device__ void need(const DMesh& mc, const double* ec, int I0, int I1, int J0, int J1,
-                       bool up) {
-    if (!has(J0, up)) {
-      const bool keep_a = aJ == J1 && aUp == up;  // slot a holds the other needed row
-      if (keep_a) { bJ = J0; bUp = up; fill(mc, ec, J0, up, I0, I1, b0, b1); }
-      else { aJ = J0; aUp = up; fill(mc, ec, J0, up, I0, I1, a0, a1); }
+  // the loads of node row j (not a duplicate), one row step ahead of value(i, j)
+  __device__ void fetch(const DMesh& mf, const DMesh& mc, const double* ec, int i, int j) {
+    const int R = mf.notch_row;
+    const bool up = R >= 0 && j > R;
+    const int I0 = i >> 1, I1 = I0 + (i & 1), J0 = j >> 1;
+    if (j != last_j + 1) {
+      row(mc, ec, J0, up, I0, I1, l0, l1);
+      h0 = h1 = zero();
+      if (j & 1) row(mc, ec, J0 + 1, up, I0, I1, h0, h1);
+    } else {
+      if (j & 1) {
+        row(mc, ec, J0 + 1, up, I0, I1, h0, h1);
+      } else {
+        l0 = h0;
+        l1 = h1;
+      }
+      if (j == R + 1 && R >= 0) row(mc, ec, J0, true, I0, I1, l0, l1);
     }
-    if (!has(J1, up)) {
-      const bool keep_a = aJ == J0 && aUp == up;
-      if (keep_a) { bJ = J1; bUp = up; fill(mc, ec, J1, up, I0, I1, b0, b1); }
-      else { aJ = J1; aUp = up; fill(mc, ec, J1, up, I0, I1, a0, a1); }
-    }
+    last_j = j;
   }
-  __device__ void get(int J, bool up, V& v0, V& v1) const {
-    const bool in_a = aJ == J && aUp == up;
-    v0 = in_a ? a0 : b0;
-    v1 = in_a ? a1 : b1;
+  __device__ V value(int i, int j) const {
+    const double w = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
+    const double a10 = (i & 1) ? w : 0.0, a01 = (j & 1) ? w : 0.0;
+    const double a11 = ((i & 1) && (j & 1)) ? w : 0.0;
+    return comb(w, l0, a10, l1, a01, h0, a11, h1);
+  }
+  // stateless (the row below a unit, the slit's upper face): four direct loads
+  __device__ static V direct(const DMesh& mf, const DMesh& mc, const double* ec, int i, int j,
+                             bool dup) {
+    const bool up = dup || (mf.notch_row >= 0 && j > mf.notch_row);
+    const int I0 = i >> 1, I1 = I0 + (i & 1), J0 = j >> 1;
+    V a0, a1, b0 = zero(), b1 = zero();
+    row(mc, ec, J0, up, I0, I1, a0, a1);
+    if (j & 1) row(mc, ec, J0 + 1, up, I0, I1, b0, b1);
+    const double w = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
+    const double a10 = (i & 1) ? w : 0.0, a01 = (j & 1) ? w : 0.0;
+    const double a11 = ((i & 1) && (j & 1)) ? w : 0.0;
+    return comb(w, a0, a10, a1, a01, b0, a11, b1);
   }
 };
-template <> __device__ __forceinline__ double ProlongCache<double>::zero() { return 0.0; }
-template <> __device__ __forceinline__ double ProlongCache<double>::load(const double* e, int c) {
+template <> __device__ __forceinline__ double ProlongMarch<double>::zero() { return 0.0; }
+template <> __device__ __forceinline__ double ProlongMarch<double>::load(const double* e, int c) {
   return __ldg(e + c);
 }
-template <> __device__ __forceinline__ double2 ProlongCache<double2>::zero() {
+template <> __device__ __forceinline__ double ProlongMarch<double>::comb(
+    double a0, double v0, double a1, double v1, double a2, double v2, double a3, double v3) {
+  return a0 * v0 + a1 * v1 + a2 * v2 + a3 * v3;
+}
+template <> __device__ __forceinline__ double2 ProlongMarch<double2>::zero() {
   return make_double2(0.0, 0.0);
 }
-template <> __device__ __forceinline__ double2 ProlongCache<double2>::load(const double* e, int c) {
+template <> __device__ __forceinline__ double2 ProlongMarch<double2>::load(const double* e, int c) {
   return __ldg(reinterpret_cast<const double2*>(e) + c);
 }
-// fine row j of a node (dup: upper slit face) -> coarse rows and face of its sources
-__device__ __forceinline__ void prolong_rows(const DMesh& mf, int j, bool dup, int& J0, int& J1,
-                                             bool& up) {
-  up = dup || (mf.notch_row >= 0 && j > mf.notch_row);
-  J0 = j >> 1;
-  J1 = J0 + (j & 1);
+template <> __device__ __forceinline__ double2 ProlongMarch<double2>::comb(
+    double a0, double2 v0, double a1, double2 v1, double a2, double2 v2, double a3, double2 v3) {
+  return make_double2(a0 * v0.x + a1 * v1.x + a2 * v2.x + a3 * v3.x,
+                      a0 * v0.y + a1 * v1.y + a2 * v2.y + a3 * v3.y);
 }
 
 struct FineSmooth : FineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 (r - A y); r.z
@@ -470,52 +803,55 @@ struct FineSmooth : FineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 
   const DMesh* mc;
   const double* ec;
   double* rz;
+  mutable ProlongMarch<double2> pm;  // the level-1 corrections of the bilinear prolongation
   struct Raw {
     double2 dv, bv;
     double d;
-    double2 pv[4];  // the level-1 corrections of the bilinear prolongation, fetched ahead
-    double pw;
-    unsigned live;
   };
-  __device__ void fetch(int id, int i, int j, bool dup, Raw& w) const {
+  __device__ void fetch(int id, int i, int j, bool, Raw& w) const {
     w.dv = di(id);
     w.bv = d2ldcg(r, id);
     w.d = __ldg(d + id);
-    const DMesh& c = *mc;
-    const bool up = dup || (mf->notch_row >= 0 && j > mf->notch_row);
-    const int I0 = i >> 1, J0 = j >> 1, I1 = I0 + (i & 1), J1 = J0 + (j & 1);
-    w.pw = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
-    const int4 r0 = GMem::row(c.nrow, J0), r1 = GMem::row(c.nrow, min(J1, c.ny));
-    const int cc[4] = {mg_row_node(c, r0, I0, J0, up), mg_row_node(c, r0, I1, J0, up),
-                       mg_row_node(c, r1, I0, J1, up), mg_row_node(c, r1, I1, J1, up)};
-    w.live = (cc[0] >= 0 ? 1u : 0u) | ((cc[1] >= 0 && I1 != I0) ? 2u : 0u) |
-             ((cc[2] >= 0 && J1 != J0) ? 4u : 0u) |
-             ((cc[3] >= 0 && I1 != I0 && J1 != J0) ? 8u : 0u);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) w.pv[k] = GMem::v2(ec, max(cc[k], 0));
+    pm.fetch(*mf, *mc, ec, i, j);
   }
-  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
-    aux = w.d;
-    // same products and order as mg_prolong: a00 v00 + a10 v10 + a01 v01 + a11 v11
-    const double a0 = (w.live & 1u) ? w.pw : 0.0, a1 = (w.live & 2u) ? w.pw : 0.0;
-    const double a2 = (w.live & 4u) ? w.pw : 0.0, a3 = (w.live & 8u) ? w.pw : 0.0;
-    const double2 pe = make_double2(a0 * w.pv[0].x + a1 * w.pv[1].x + a2 * w.pv[2].x + a3 * w.pv[3].x,
-                                    a0 * w.pv[0].y + a1 * w.pv[1].y + a2 * w.pv[2].y + a3 * w.pv[3].y);
+  __device__ double2 smooth0(const Raw& w, double2 pe) const {
     return mask2(make_double2(om * w.dv.x * w.bv.x + pe.x, om * w.dv.y * w.bv.y + pe.y), w.dv);
+  }
+  __device__ double2 finish(const Raw& w, int, int i, int j, bool, double& aux) const {
+    aux = w.d;
+    return smooth0(w, pm.value(i, j));
   }
   __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
     Raw w;
-    fetch(id, i, j, dup, w);
-    return finish(w, id, i, j, dup, aux);
+    w.dv = di(id);
+    w.bv = d2ldcg(r, id);
+    aux = __ldg(d + id);
+    return smooth0(w, ProlongMarch<double2>::direct(*mf, *mc, ec, i, j, dup));
   }
-  __device__ void out(int id, double2 Av, double2 y) const {
-    const double2 dv = di(id), bv = d2ldcg(r, id);
+  __device__ void out2(int id, double2 Av, double2 y, double2 dv, double2 bv) const {
     const double2 ev = make_double2(y.x + om * dv.x * (bv.x - Av.x),
                                     y.y + om * dv.y * (bv.y - Av.y));
     d2st(z, id, ev);
     *rz += bv.x * ev.x + bv.y * ev.y;
+  }
+  __device__ void out(int id, double2 Av, double2 y) const {
+    out2(id, Av, y, di(id), d2ldcg(r, id));
+  }
+  static constexpr int N8 = 1, N16 = 2, D = PFB_MST_DM;
+  static constexpr bool KEEP = true;
+  __device__ const double* n8(int) const { return d; }
+  __device__ const double* n16(int k) const { return k == 0 ? dinv : r; }
+  __device__ void take(const unsigned char* slot, int e8, int e16, Raw& w) const {
+    w.dv = mst_s16(slot, N8, 0, e16);
+    w.bv = mst_s16(slot, N8, 1, e16);
+    w.d = mst_s8(slot, 0, e8);
+  }
+  __device__ void ahead(int, int i, int j) const { pm.fetch(*mf, *mc, ec, i, j); }
+  __device__ void outs(const unsigned char* slot, int, int e16, int id, double2 Av,
+                       double2 y) const {
+    out2(id, Av, y, mst_s16(slot, N8, 0, e16), mst_s16(slot, N8, 1, e16));
   }
 };
 
@@ -624,11 +960,25 @@ struct FinePcg : FineBase {  // p = z + beta p_old (owner stores), q = A p (mask
     fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
-  __device__ void out(int id, double2 Av, double2 p) const {
-    const double2 qv = mask2(Av, di(id));
+  __device__ void out2(int id, double2 Av, double2 p, double2 dv) const {
+    const double2 qv = mask2(Av, dv);
     d2st(pnew, id, p);
     d2st(q, id, qv);
     if (!own || node_owned(*own, id)) *pq += p.x * qv.x + p.y * qv.y;
+  }
+  __device__ void out(int id, double2 Av, double2 p) const { out2(id, Av, p, di(id)); }
+  static constexpr int N8 = 1, N16 = 3, D = PFB_MST_DM;
+  static constexpr bool KEEP = true;
+  __device__ const double* n8(int) const { return d; }
+  __device__ const double* n16(int k) const { return k == 0 ? z : (k == 1 ? pold : dinv); }
+  __device__ void take(const unsigned char* slot, int e8, int e16, Raw& w) const {
+    w.zv = mst_s16(slot, N8, 0, e16);
+    w.po = pold ? mst_s16(slot, N8, 1, e16) : make_double2(0.0, 0.0);
+    w.d = mst_s8(slot, 0, e8);
+  }
+  __device__ void outs(const unsigned char* slot, int, int e16, int id, double2 Av,
+                       double2 p) const {
+    out2(id, Av, p, mst_s16(slot, N8, 2, e16));
   }
 };
 
@@ -1309,7 +1659,15 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_fine_resid(MgArgs A) {
   const double om = __ldcg(&A.ctl->omega[0]);
   FineResid op{{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq}, om, A.r, A.L[0].t};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
+#if PFB_MST & 8
+  extern __shared__ __align__(128) unsigned char mst_ring[];
+  __shared__ unsigned long long mst_bars[MG_WARPS][8];
+  if (w < A.g0.n_units)
+    mg_march_st(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5],
+                mst_ring + (threadIdx.x >> 5) * MStage<FineResid>::WARP, mst_bars[threadIdx.x >> 5]);
+#else
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
+#endif
 }
 
 #define MG_GW (int)(blockIdx.x * MG_WARPS + (threadIdx.x >> 5)), (int)(gridDim.x * MG_WARPS)
@@ -1358,31 +1716,6 @@ __device__ __forceinline__ TLevel mg_tl(const MgArgs& A, int l) {
   v.e = reinterpret_cast<double*>(sm + o.e);
   return v;
 }
-// TMA bulk copies global -> shared completing on one mbarrier (sizes and addresses are
-// multiples of 16 B: the host pads every multigrid array)
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mg_bulk_g2s(const void* dst, const void* src, unsigned bytes,
-                                            unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mg_mbar_init_expect(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
-               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mg_mbar_wait(unsigned long long* bar, unsigned phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
-}
-__device__ __forceinline__ unsigned mg_r16(size_t b) { return (unsigned)((b + 15) & ~size_t(15)); }
 __device__ __forceinline__ double2 ts2(const double* p, int i) {
   return reinterpret_cast<const double2*>(p)[i];
 }
@@ -1585,9 +1918,17 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_fine_smooth(MgArgs A) {
   const double om = __ldcg(&A.ctl->omega[0]);
   double rz = 0.0;
   FineSmooth op{{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq}, om, A.r, A.z, &A.L[0].m, &A.L[1].m,
-                A.L[1].e, &rz};
+                A.L[1].e, &rz, {}};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
+#if PFB_MST & 16
+  extern __shared__ __align__(128) unsigned char mst_ring[];
+  __shared__ unsigned long long mst_bars[MG_WARPS][8];
+  if (w < A.g0.n_units)
+    mg_march_st(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5],
+                mst_ring + (threadIdx.x >> 5) * MStage<FineSmooth>::WARP, mst_bars[threadIdx.x >> 5]);
+#else
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
+#endif
   double v[1] = {rz};
   mg_block_sum<1>(v, red);
   if (threadIdx.x == 0) A.part[blockIdx.x] = v[0];  // r.z partials, reduced by k_mg_pcg
@@ -1604,7 +1945,15 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_pcg(MgArgs A, int n_rz) {
   FinePcg op{{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq}, first ? 0.0 : rho[0] / __ldcg(&A.ctl->rho_prev),
              A.z, first ? nullptr : ((k & 1) ? A.p0 : A.p1), (k & 1) ? A.p1 : A.p0, A.q, &pq};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
+#if PFB_MST & 32
+  extern __shared__ __align__(128) unsigned char mst_ring[];
+  __shared__ unsigned long long mst_bars[MG_WARPS][8];
+  if (w < A.g0.n_units)
+    mg_march_st(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5],
+                mst_ring + (threadIdx.x >> 5) * MStage<FinePcg>::WARP, mst_bars[threadIdx.x >> 5]);
+#else
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
+#endif
   double v[1] = {pq};
   mg_block_sum<1>(v, red);
   if (threadIdx.x == 0) A.part[n_rz + blockIdx.x] = v[0];  // p.q partials after the r.z ones

@@ -95,6 +95,15 @@ struct SFineBase {
     for (int k = 0; k < 4; ++k) f[k] = make_double2(fx[k], 0.0);
   }
   __device__ double di(int id) const { return __ldg(dinv + id); }
+  // staged march (pf_mg.cuh mg_march_st): the cell records come through shared memory
+  static constexpr bool CST = true;
+  __device__ const double* cst() const { return bq; }
+  __device__ void ctake(const unsigned char* cs, int ce, CRaw& c) const {
+    const double2* p = reinterpret_cast<const double2*>(cs) + 2 * ce;
+    c.b01 = p[0];
+    c.b23 = p[1];
+  }
+  __device__ void ahead(int, int, int) const {}
 };
 
 struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), t = r - A x
@@ -124,6 +133,17 @@ struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), 
   __device__ void out(int id, double2 Av, double2 v) const {
     t[id] = v.y == v.y ? v.y - Av.x : 0.0;
   }
+  static constexpr int N8 = 2, N16 = 0, D = PFB_MST_DS;
+  static constexpr bool KEEP = false;
+  __device__ const double* n8(int k) const { return k == 0 ? dinv : r; }
+  __device__ const double* n16(int) const { return nullptr; }
+  __device__ void take(const unsigned char* slot, int e8, int, Raw& w) const {
+    w.dv = mst_s8(slot, 0, e8);
+    w.bv = mst_s8(slot, 1, e8);
+  }
+  __device__ void outs(const unsigned char*, int, int, int id, double2 Av, double2 v) const {
+    out(id, Av, v);
+  }
 };
 
 struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 (r - A y); r.z
@@ -134,47 +154,48 @@ struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-
   const DMesh* mc;
   const double* ec;
   double* rz;
-  mutable ProlongCache<double> pc;  // coarse sources of the bilinear prolongation (pf_mg.cuh)
+  mutable ProlongMarch<double> pm;  // coarse sources of the bilinear prolongation (pf_mg.cuh)
   struct Raw {
     double dv, bv;
   };
-  __device__ void fetch(int id, int i, int j, bool dup, Raw& w) const {
+  __device__ void fetch(int id, int i, int j, bool, Raw& w) const {
     w.dv = di(id);
     w.bv = __ldg(r + id);
-    int J0, J1;
-    bool up;
-    prolong_rows(*mf, j, dup, J0, J1, up);
-#if PFB_MGS_NOPROL != 2
-    pc.need(*mc, ec, i >> 1, (i >> 1) + (i & 1), J0, J1, up);
-#endif
+    pm.fetch(*mf, *mc, ec, i, j);
   }
-  __device__ double2 finish(const Raw& w, int, int i, int j, bool dup, double& aux) const {
-    aux = 0.0;
-    int J0, J1;
-    bool up;
-    prolong_rows(*mf, j, dup, J0, J1, up);
-    double v00, v10, v01, v11;
-    pc.get(J0, up, v00, v10);
-    pc.get(J1, up, v01, v11);
-    const double w0 = ((i & 1) ? 0.5 : 1.0) * ((j & 1) ? 0.5 : 1.0);
-    const double a10 = (i & 1) ? w0 : 0.0, a01 = (j & 1) ? w0 : 0.0;
-    const double a11 = ((i & 1) && (j & 1)) ? w0 : 0.0;
-#if PFB_MGS_NOPROL + 0  // timing experiments only: the smoothing march without the prolongation
-    const double pe = 0.0 * (w0 * v00 + a10 * v10 + a01 * v01 + a11 * v11);
-#else
-    const double pe = w0 * v00 + a10 * v10 + a01 * v01 + a11 * v11;
-#endif
+  __device__ double2 smooth0(const Raw& w, double pe) const {
     return make_double2(mgs_mask(om * w.dv * w.bv + pe, w.dv), om * w.dv);  // y, omega D^-1
+  }
+  __device__ double2 finish(const Raw& w, int, int i, int j, bool, double& aux) const {
+    aux = 0.0;
+    return smooth0(w, pm.value(i, j));
   }
   __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
     aux = 0.0;
     if (id < 0) return make_double2(0.0, 0.0);
     Raw w;
-    fetch(id, i, j, dup, w);
-    return finish(w, id, i, j, dup, aux);
+    w.dv = di(id);
+    w.bv = __ldg(r + id);
+    return smooth0(w, ProlongMarch<double>::direct(*mf, *mc, ec, i, j, dup));
   }
   __device__ void out(int id, double2 Av, double2 y) const {
     const double bv = __ldg(r + id);
+    const double ev = y.x + y.y * (bv - Av.x);
+    z[id] = ev;
+    *rz += bv * ev;
+  }
+  static constexpr int N8 = 2, N16 = 0, D = PFB_MST_DS + 1;
+  static constexpr bool KEEP = true;  // outs reads r from the stage
+  __device__ const double* n8(int k) const { return k == 0 ? dinv : r; }
+  __device__ const double* n16(int) const { return nullptr; }
+  __device__ void take(const unsigned char* slot, int e8, int, Raw& w) const {
+    w.dv = mst_s8(slot, 0, e8);
+    w.bv = mst_s8(slot, 1, e8);
+  }
+  __device__ void ahead(int, int i, int j) const { pm.fetch(*mf, *mc, ec, i, j); }
+  __device__ void outs(const unsigned char* slot, int e8, int, int id, double2 Av,
+                       double2 y) const {
+    const double bv = mst_s8(slot, 1, e8);
     const double ev = y.x + y.y * (bv - Av.x);
     z[id] = ev;
     *rz += bv * ev;
@@ -237,6 +258,18 @@ struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (ma
     pnew[id] = p.x;
     q[id] = qv;
     if (!own || node_owned(*own, id)) *pq += p.x * qv;
+  }
+  static constexpr int N8 = 3, N16 = 0, D = PFB_MST_DS;
+  static constexpr bool KEEP = false;
+  __device__ const double* n8(int k) const { return k == 0 ? z : (k == 1 ? pold : dinv); }
+  __device__ const double* n16(int) const { return nullptr; }
+  __device__ void take(const unsigned char* slot, int e8, int, Raw& w) const {
+    w.zv = mst_s8(slot, 0, e8);
+    w.po = pold ? mst_s8(slot, 1, e8) : 0.0;
+    w.dv = mst_s8(slot, 2, e8);
+  }
+  __device__ void outs(const unsigned char*, int, int, int id, double2 Av, double2 p) const {
+    out(id, Av, p);
   }
 };
 
@@ -870,14 +903,26 @@ __global__ void __launch_bounds__(MG_NT) k_mgs_init(MgsArgs A) {
 // the residual march is the lightest: four CTAs per SM (its own unit geometry g0r; measured at
 // cfg5 0.77 -> 0.66 ms, while the smoothing and direction marches lose at four)
 #ifndef PFB_MGS_MINB_RESID
+#if PFB_MST & 1  // staged: rows in flight come from the stages, not from more resident warps
+#define PFB_MGS_MINB_RESID 3
+#else
 #define PFB_MGS_MINB_RESID 4
+#endif
 #endif
 __global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB_RESID) k_mgs_fine_resid(MgsArgs A) {
   __shared__ MgWarp ws[MG_WARPS];
   const double om = __ldcg(&A.ctl->omega[0]);
   SFineResid op{{&A.C, A.bq, A.L[0].dinv}, om, A.r, A.L[0].t};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
+#if PFB_MST & 1
+  extern __shared__ __align__(128) unsigned char mst_ring[];
+  __shared__ unsigned long long mst_bars[MG_WARPS][8];
+  if (w < A.g0r.n_units)
+    mg_march_st(A.L[0].m, A.g0r, w, op, ws[threadIdx.x >> 5],
+                mst_ring + (threadIdx.x >> 5) * MStage<SFineResid>::WARP, mst_bars[threadIdx.x >> 5]);
+#else
   if (w < A.g0r.n_units) mg_march(A.L[0].m, A.g0r, w, op, ws[threadIdx.x >> 5]);
+#endif
 }
 
 __global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_fine_smooth(MgsArgs A) {
@@ -887,7 +932,15 @@ __global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_fine_smooth(MgsArgs
   double rz = 0.0;
   SFineSmooth op{{&A.C, A.bq, A.L[0].dinv}, om, A.r, A.z, &A.L[0].m, &A.L[1].m, A.L[1].e, &rz, {}};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
+#if PFB_MST & 2
+  extern __shared__ __align__(128) unsigned char mst_ring[];
+  __shared__ unsigned long long mst_bars[MG_WARPS][8];
+  if (w < A.g0.n_units)
+    mg_march_st(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5],
+                mst_ring + (threadIdx.x >> 5) * MStage<SFineSmooth>::WARP, mst_bars[threadIdx.x >> 5]);
+#else
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
+#endif
   double v[1] = {rz};
   mg_block_sum<1>(v, red);
   if (threadIdx.x == 0) A.part[blockIdx.x] = v[0];  // r.z partials, reduced by k_mgs_pcg
@@ -904,7 +957,15 @@ __global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_pcg(MgsArgs A, int 
   SFinePcg op{{&A.C, A.bq, A.L[0].dinv}, first ? 0.0 : rho[0] / __ldcg(&A.ctl->rho_prev), A.z,
               first ? nullptr : ((k & 1) ? A.p0 : A.p1), (k & 1) ? A.p1 : A.p0, A.q, &pq};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
+#if PFB_MST & 4
+  extern __shared__ __align__(128) unsigned char mst_ring[];
+  __shared__ unsigned long long mst_bars[MG_WARPS][8];
+  if (w < A.g0.n_units)
+    mg_march_st(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5],
+                mst_ring + (threadIdx.x >> 5) * MStage<SFinePcg>::WARP, mst_bars[threadIdx.x >> 5]);
+#else
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
+#endif
   double v[1] = {pq};
   mg_block_sum<1>(v, red);
   if (threadIdx.x == 0) A.part[n_rz + blockIdx.x] = v[0];
@@ -940,7 +1001,11 @@ __global__ void __launch_bounds__(MG_NT) k_mgs_update(MgsArgs A, int n_rz, int n
       c.rho_prev = rho[0];
       c.k = k + 1;
       const double rn = sqrt(tot[0]);
-      if (rn < c.atol) { c.done = 1; c.status = CG_CONVERGED; }
+      // the SPD probe of the gated solves (check_spd, linsolve.py:58-77; pf_cg.cuh k_cg): a
+      // direction of non-positive curvature proves that K_dd + K~ is not positive definite,
+      // whatever the preconditioner
+      if (__ldcg(&A.in->probe) && !(pq[0] > 0.0)) { c.done = 1; c.status = CG_INDEFINITE; }
+      else if (rn < c.atol) { c.done = 1; c.status = CG_CONVERGED; }
       else if (!(rn == rn)) { c.done = 1; c.status = CG_NAN; }
       else if (c.k >= c.maxiter) { c.done = 1; c.status = CG_MAXITER; }
       if (A.use_cond) cudaGraphSetConditional(A.cond, c.done ? 0u : 1u);

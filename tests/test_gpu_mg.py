@@ -150,6 +150,25 @@ def test_phase_field_mg_matches(cuda_ok, monkeypatch, case_name, scheme, steps, 
     assert sum(x.cg_iters_d for x in s1) < sum(x.cg_iters_d for x in s0)
 
 
+@pytest.mark.parametrize("case_name,scheme", [
+    ("shear32", "S3"), ("shear32", "S2"), ("tension16", "S2"), ("tension32", "S1"),
+    ("multicrack32", "S1")])
+def test_gated_solves_by_scalar_mg_match_reference(cuda_ok, monkeypatch, case_name, scheme):
+    """The gated solves of the fast schemes (K_dd + K~ with the SPD check, schemes.py:293-301)
+    by the scalar multigrid PCG with the probe inside (p.Ap <= 0 => fallback), forced on here
+    as on the large meshes: the whole run against the reference's own table -- staggered and
+    Newton counts and the spd_fallbacks decisions per step, forces, the final phase field."""
+    from conftest import golden
+    from test_gpu_solver import check_against_golden, run_case
+
+    monkeypatch.setenv("PFB200_MG_EVO", "scalar")
+    z = golden(f"run_{case_name}_{scheme}.npz")
+    pb, recs = run_case(case_name, scheme)
+    check_against_golden(recs, z, pb.state, case_name, scheme, pb.mesh)
+    assert sum(r.spd_fallbacks for r in recs) == pytest.approx(
+        z["table"][:, 4].sum(), rel=0.15, abs=3)
+
+
 @pytest.mark.parametrize("case_name,scheme", [("cfg1", "ST"), ("shear32", "S3")])
 def test_fp32_coarse_stencils_on_cracked_states(cuda_ok, monkeypatch, case_name, scheme):
     """The V-cycle's grid levels read FP32 copies of the coarse stencils by default.  Through the

@@ -222,18 +222,25 @@ def test_cfg2_crack_step_from_reference_state(cuda_ok):
     assert err <= 1e-6, err
 
 
+@pytest.mark.parametrize("solver", ["jacobi_pcg", "scalar_mg"])
 @pytest.mark.parametrize("case,scheme", [("tension16", "S1"), ("tension16", "S2"),
                                          ("tension16", "S3"), ("shear32", "S3")])
-def test_spd_predicate_agrees_with_check_spd(case, scheme, cuda_ok):
-    """The curvature SPD predicate reproduces the reference's SuperLU check_spd decisions."""
+def test_spd_predicate_agrees_with_check_spd(case, scheme, solver, cuda_ok, monkeypatch):
+    """The curvature SPD predicate reproduces the reference's SuperLU check_spd decisions --
+    inside the Jacobi PCG (small meshes) and inside the scalar multigrid PCG (the large meshes'
+    default, forced here)."""
     import json
 
     from paper_2209_07969_b200.session import DeviceSession
 
+    monkeypatch.setenv("PFB200_MG_EVO", "scalar" if solver == "scalar_mg" else "0")
     z = golden(f"spd_{case}_{scheme}.npz")
     meta = json.loads(str(z["meta"]))
     pb = C.setup(C.get_case(case), C.b200_api())
     s = DeviceSession(pb.disc.layout, pb.params, pb.config, device=0)
+    if solver == "scalar_mg" and s.solver_kinds()["phase_field"] != "multigrid_pcg":
+        s.close()
+        pytest.skip("mesh too small for a scalar phase-field hierarchy")
     agree = total = 0
     for key, n, want in (("fallback", meta["n_fallback"], 1), ("spd", meta["n_spd"], 0)):
         for i in range(n):
