@@ -147,6 +147,9 @@ struct pf_handle {
   static constexpr int WARM_SLOTS = 4;
   bool warm = true;
   bool trace = false;
+  bool evo_march = false;      // k_evo_prepare as a warp march (big single-GPU meshes)
+  pfb::MarchGeom geom_prep{};
+  int parts_n = 0;             // partial triples written by the last prepare kernel (0: n_tiles)
   bool mgs_gated = true;  // gated (S1/S2/S3) phase-field solves by the scalar multigrid PCG with
                           // the SPD probe inside (PFB200_MGS_GATED=0: the Jacobi-PCG probe)
   // cfg2 load steps 4..13, Jacobi momentum PCG iterations: depth 1 69634, 3 52336, 4 52151,
@@ -1238,14 +1241,19 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
     if (B.dense) pfb::k_mgs_dense<<<1, pfb::MG_NT, 0, s>>>(B);
     // the fine march and the coarse grid levels of a power step as two launches: in one grid
     // the coarse blocks queued behind the fine march's (3.3 ms per step at cfg5)
-    const int cb = (B.coarse_items + pfb::MG_NT - 1) / pfb::MG_NT;
+    // the large one-thread-per-node levels (the first ones) by the row-table kernel
+    int lr = 1;
+    while (lr < B.n_tail && M.lpn[lr] == 1 && M.rows && B.L[lr].m.n_nodes >= (1 << 20)) ++lr;
+    const int off0 = lr < B.n_tail ? B.L[lr].item_off : B.coarse_items;
+    const int cb = (B.coarse_items - off0 + pfb::MG_NT - 1) / pfb::MG_NT;
     for (int k = 1; k <= npow; ++k) {
       pfb::k_mgs_pow<<<M.gf, pfb::MG_NT, 0, s>>>(B, k, M.gf);
-      if (cb > 0) pfb::k_mgs_pow_coarse<<<cb, pfb::MG_NT, 0, s>>>(B, k);
+      for (int l = 1; l < lr; ++l) pfb::k_mgs_rpow<<<M.gl[l], pfb::MG_NT, 0, s>>>(B, l, k);
+      if (cb > 0) pfb::k_mgs_pow_coarse<<<cb, pfb::MG_NT, 0, s>>>(B, k, off0);
     }
     if (B.n_tail < nl) pfb::k_mgs_pow_tail<<<1, pfb::MG_TAIL_NT, 0, s>>>(B, npow);
     pfb::k_mgs_lambda<<<M.gflat, pfb::MG_NT, 0, s>>>(B, npow);
-    const int nk = 2 * (nl - 1) + (B.dense ? 1 : 0) + npow * (cb > 0 ? 2 : 1) +
+    const int nk = 2 * (nl - 1) + (B.dense ? 1 : 0) + npow * ((cb > 0 ? 2 : 1) + (lr - 1)) +
                    (B.n_tail < nl ? 1 : 0) + 1;
     (safe ? M.setup_kernels_safe : M.setup_kernels) = nk;
     cudaError_t e = cudaStreamEndCapture(s, &g);
@@ -1593,6 +1601,14 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
   int dev_sms = 0, occ = 0, occ_evo = 0, l2 = 0;
   CREATE_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
   CREATE_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+  {  // PFB200_EVO_MARCH=1/0 forces the march form of k_evo_prepare on / off
+    const char* em = getenv("PFB200_EVO_MARCH");
+    h->evo_march = !strip && (em ? std::string(em) == "1" : h->n_tiles > 65536);
+    int oc = 0;
+    CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, pfb::k_evo_prepare_march,
+                                                              pfb::MG_NT, 0));
+    h->geom_prep = pfb::make_march_geom(nx, ny, std::max(1, oc) * dev_sms * pfb::MG_WARPS);
+  }
   {  // both variants of each persistent kernel must be co-resident at the same grid size
     int o1 = 0, o2 = 0;
     CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, pfb::k_cg<true, false>,
@@ -2144,7 +2160,14 @@ static pf_status launch_evo_prepare(pf_handle* h, int full, int extra_scheme) {
   a.partials = h->partials;
   a.full = full;
   a.extra_scheme = extra_scheme;
+  if (h->evo_march) {  // big meshes: one warp march (pf_mgs.cuh k_evo_prepare_march)
+    const int grid = (h->geom_prep.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
+    pfb::k_evo_prepare_march<<<grid, pfb::MG_NT, 0, h->stream>>>(a, h->geom_prep);
+    h->parts_n = grid;
+    return launched(h);
+  }
   pfb::k_evo_prepare<<<h->n_tiles, pfb::NT, 0, h->stream>>>(a);
+  h->parts_n = h->n_tiles;
   return launched(h);
 }
 
@@ -2156,13 +2179,18 @@ static pf_status comm_check(pf_handle* h, const std::string& e) {
 // sums nv partial streams of n_tiles CTAs into h_scal[0..nv) (all-reduced over the strips) and
 // waits for them
 static pf_status finalize(pf_handle* h, int nv) {
+  // one CTA sums the per-tile partials in a fixed order; 1024 threads on the big meshes (the
+  // 256-thread order is kept below 2^16 tiles: the small cases' norms stay bit-identical)
+  const int np = h->parts_n > 0 ? h->parts_n : h->n_tiles;
+  const int nt = np > 65536 ? 1024 : 256;
+  h->parts_n = 0;
   if (!h->comm) {
-    pfb::k_finalize<<<1, 256, 0, h->stream>>>(h->partials, h->n_tiles, nv, h->d_scal);
+    pfb::k_finalize<<<1, nt, 0, h->stream>>>(h->partials, np, nv, h->d_scal);
     PF_TRY(launched(h));
     PF_CUDA(cudaStreamSynchronize(h->stream));
     return PF_OK;
   }
-  pfb::k_finalize<<<1, 256, 0, h->stream>>>(h->partials, h->n_tiles, nv, h->d_red);
+  pfb::k_finalize<<<1, nt, 0, h->stream>>>(h->partials, np, nv, h->d_red);
   PF_TRY(launched(h));
   PF_TRY(comm_check(h, h->comm->allreduce(h->d_red, nv, h->stream)));
   PF_CUDA(cudaMemcpyAsync(h->h_scal, h->d_red, nv * sizeof(double), cudaMemcpyDeviceToHost,
@@ -2718,7 +2746,7 @@ static pf_status momentum(pf_handle* h, const BcView& bc, bool apply_inc, double
         pfb::WarmTable t{};
         for (int k = 0; k < depth; ++k) t.d[k] = h->warm_buf[ws][k];
         const long long n = 2LL * h->n_nodes;
-        pfb::k_warm_push<<<4 * h->sm_count, 256, 0, h->stream>>>(t, h->warm_n[ws], depth, h->xu, n);
+        pfb::k_warm_push<<<16 * h->sm_count, 256, 0, h->stream>>>(t, h->warm_n[ws], depth, h->xu, n);
         PF_TRY(launched(h));
         h->warm_n[ws] = std::min(h->warm_n[ws] + 1, depth);
       }
@@ -2918,7 +2946,7 @@ static pf_status evolution(pf_handle* h, int scheme, double* r0, int* n_nr_out, 
       if (use_warm) {
         pfb::WarmTable t{};
         for (int k = 0; k < h->warm_depth; ++k) t.d[k] = h->warm_d[ws][k];
-        pfb::k_warm_push<<<4 * h->sm_count, 256, 0, h->stream>>>(t, h->warm_nd[ws], h->warm_depth,
+        pfb::k_warm_push<<<16 * h->sm_count, 256, 0, h->stream>>>(t, h->warm_nd[ws], h->warm_depth,
                                                               h->xd, (long long)h->n_nodes);
         PF_TRY(launched(h));
         h->warm_nd[ws] = std::min(h->warm_nd[ws] + 1, h->warm_depth);

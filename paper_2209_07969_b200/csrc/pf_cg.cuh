@@ -400,16 +400,19 @@ __device__ __forceinline__ double warm_start(const CgArgs& a, CgSmem<MOM>& S) {
 // guess[k] = k-th backward difference) absorbs x in place; n_valid = entries before the push
 __global__ void k_warm_push(WarmTable t, int n_valid, int depth, const double* __restrict__ x,
                             long long n) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+  // two entries per thread (16-byte accesses; every array is a 16-byte-padded allocation)
+  const long long n2 = (n + 1) >> 1;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
        i += (long long)gridDim.x * blockDim.x) {
-    double cur = x[i];
+    double2 cur = reinterpret_cast<const double2*>(x)[i];
 #pragma unroll
     for (int k = 0; k < WARM_MAX; ++k) {
       if (k >= depth) break;
-      const double old = k < n_valid ? t.d[k][i] : 0.0;
-      t.d[k][i] = cur;
+      double2* tk = reinterpret_cast<double2*>(t.d[k]) + i;
+      const double2 old = k < n_valid ? *tk : make_double2(0.0, 0.0);
+      *tk = cur;
       if (k >= n_valid) break;
-      cur = cur - old;
+      cur = make_double2(cur.x - old.x, cur.y - old.y);
     }
   }
 }

@@ -34,6 +34,10 @@
 #ifndef PFB_MST
 #define PFB_MST 0
 #endif
+// rows ahead of the fine marches' L2 prefetch hints (0: none)
+#ifndef PFB_L2PF
+#define PFB_L2PF 0
+#endif
 #ifndef PFB_MST_DS
 #define PFB_MST_DS 3
 #endif
@@ -187,6 +191,37 @@ __device__ __forceinline__ double mg_q(int c, int k, int K) {
 //   void out(int id, double2 Av, double2 vin)                 once per owned node
 // The cell data of the next cell row (branch bits / Newton coefficients) is fetched one row
 // step ahead like the node rows, so no dependent HBM load sits on a row step's critical path.
+// optional parts of an Op (overload rank by the last argument):
+//   void outa(int id, double2 Av, double2 vin, double aux)   out() with the node's aux value
+//   void l2pf(int id, int lane) / void cl2pf(int eid, int lane)   L2 prefetch of the node's /
+//                                                                  cell's lines, rows ahead
+template <class Op>
+__device__ __forceinline__ auto mg_out(Op& op, int id, double2 Av, double2 v, double a, int)
+    -> decltype(op.outa(id, Av, v, a), void()) {
+  op.outa(id, Av, v, a);
+}
+template <class Op>
+__device__ __forceinline__ void mg_out(Op& op, int id, double2 Av, double2 v, double, long) {
+  op.out(id, Av, v);
+}
+template <class Op>
+__device__ __forceinline__ auto mg_l2pf(Op& op, int id, int lane, int)
+    -> decltype(op.l2pf(id, lane), void()) {
+  op.l2pf(id, lane);
+}
+template <class Op>
+__device__ __forceinline__ void mg_l2pf(Op&, int, int, long) {}
+template <class Op>
+__device__ __forceinline__ auto mg_cl2pf(Op& op, int eid, int lane, int)
+    -> decltype(op.cl2pf(eid, lane), void()) {
+  op.cl2pf(eid, lane);
+}
+template <class Op>
+__device__ __forceinline__ void mg_cl2pf(Op&, int, int, long) {}
+__device__ __forceinline__ void l2_prefetch(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+
 template <class Op>
 __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int unit, Op& op,
                                          MgWarp& ws) {
@@ -260,6 +295,15 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
     typename Op::CRaw c_nx;
     const int e_nx = (cj + 1 < r1) ? cell_id(cj + 1) : -1;
     if (e_nx >= 0) op.cfetch(e_nx, c_nx);
+#if PFB_L2PF
+    // the lines PFB_L2PF rows further up into L2 (the row stride of the last two rows: exact on
+    // regular rows, a harmless wrong line elsewhere), so the register prefetch one row ahead
+    // meets L2 latency instead of HBM latency
+    if (id_nx >= 0 && id_hi >= 0)
+      mg_l2pf(op, min(max(id_nx + PFB_L2PF * (id_nx - id_hi), 0), m.n_nodes - 1), lane, 0);
+    if (e_nx >= 0 && eid >= 0)
+      mg_cl2pf(op, min(max(e_nx + PFB_L2PF * (e_nx - eid), 0), m.n_elems - 1), lane, 0);
+#endif
     const bool use_dup = lo_slit && dupcol;
     const double2 b0 = use_dup ? ws.dv[lane] : v_lo;
     const double e0 = use_dup ? ws.da[lane] : a_lo;
@@ -275,11 +319,11 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
     const double2 c1l = shfl_up(f[1]), c2l = shfl_up(f[2]);
     if (lane_own && cj >= r0) {
       if (use_dup) {
-        if (id_lo >= 0) op.out(id_lo, acc_lo, v_lo);  // lower face: cells below only
+        if (id_lo >= 0) mg_out(op, id_lo, acc_lo, v_lo, a_lo, 0);  // lower face: cells below only
         const int idd = ws.did[lane];
-        if (idd >= 0) op.out(idd, d2add(c1l, f[0]), ws.dv[lane]);  // upper face
+        if (idd >= 0) mg_out(op, idd, d2add(c1l, f[0]), ws.dv[lane], ws.da[lane], 0);  // upper face
       } else if (id_lo >= 0) {
-        op.out(id_lo, d2add(d2add(acc_lo, c1l), f[0]), v_lo);
+        mg_out(op, id_lo, d2add(d2add(acc_lo, c1l), f[0]), v_lo, a_lo, 0);
       }
     }
     acc_lo = d2add(c2l, f[3]);
@@ -613,6 +657,13 @@ struct FineBase {
   __device__ double2 di(int id) const { return __ldg(reinterpret_cast<const double2*>(dinv) + id); }
   // staged march (mg_march_st): nodal arrays through shared memory, the cell data (1 B of
   // branch bits) by cfetch one row step ahead as in mg_march
+  __device__ void l2pf3(int id, int lane, const double* a16, const double* b16) const {
+    if ((lane & 7) == 0) {
+      l2_prefetch(reinterpret_cast<const double2*>(a16) + id);
+      if (b16) l2_prefetch(reinterpret_cast<const double2*>(b16) + id);
+    }
+    if ((lane & 15) == 0) l2_prefetch(d + id);
+  }
   static constexpr bool CST = false;
   __device__ const double* cst() const { return nullptr; }
   __device__ void ctake(const unsigned char*, int, CRaw&) const {}
@@ -657,6 +708,7 @@ struct FineResid : FineBase {  // x = omega D^-1 r (pre-smoothing from zero), t 
     const double2 bv = d2ldcg(r, id);
     d2st(t, id, mask2(make_double2(bv.x - Av.x, bv.y - Av.y), di(id)));
   }
+  __device__ void l2pf(int id, int lane) const { l2pf3(id, lane, dinv, r); }
   static constexpr int N8 = 1, N16 = 2, D = PFB_MST_DM;
   static constexpr bool KEEP = true;
   __device__ const double* n8(int) const { return d; }
@@ -839,6 +891,7 @@ struct FineSmooth : FineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 
   __device__ void out(int id, double2 Av, double2 y) const {
     out2(id, Av, y, di(id), d2ldcg(r, id));
   }
+  __device__ void l2pf(int id, int lane) const { l2pf3(id, lane, dinv, r); }
   static constexpr int N8 = 1, N16 = 2, D = PFB_MST_DM;
   static constexpr bool KEEP = true;
   __device__ const double* n8(int) const { return d; }
@@ -967,6 +1020,10 @@ struct FinePcg : FineBase {  // p = z + beta p_old (owner stores), q = A p (mask
     if (!own || node_owned(*own, id)) *pq += p.x * qv.x + p.y * qv.y;
   }
   __device__ void out(int id, double2 Av, double2 p) const { out2(id, Av, p, di(id)); }
+  __device__ void l2pf(int id, int lane) const {
+    l2pf3(id, lane, z, pold);
+    if ((lane & 7) == 0) l2_prefetch(reinterpret_cast<const double2*>(dinv) + id);
+  }
   static constexpr int N8 = 1, N16 = 3, D = PFB_MST_DM;
   static constexpr bool KEEP = true;
   __device__ const double* n8(int) const { return d; }

@@ -95,6 +95,17 @@ struct SFineBase {
     for (int k = 0; k < 4; ++k) f[k] = make_double2(fx[k], 0.0);
   }
   __device__ double di(int id) const { return __ldg(dinv + id); }
+  __device__ void cl2pf(int eid, int lane) const {  // 32 B per cell: a 128-byte line per 4 lanes
+    if ((lane & 3) == 0) l2_prefetch(bq + 4 * (size_t)eid);
+  }
+  __device__ void l2pf3(int id, int lane, const double* a, const double* b,
+                        const double* c) const {
+    if ((lane & 15) == 0) {
+      l2_prefetch(a + id);
+      if (b) l2_prefetch(b + id);
+      if (c) l2_prefetch(c + id);
+    }
+  }
   // staged march (pf_mg.cuh mg_march_st): the cell records come through shared memory
   static constexpr bool CST = true;
   __device__ const double* cst() const { return bq; }
@@ -133,6 +144,7 @@ struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), 
   __device__ void out(int id, double2 Av, double2 v) const {
     t[id] = v.y == v.y ? v.y - Av.x : 0.0;
   }
+  __device__ void l2pf(int id, int lane) const { l2pf3(id, lane, dinv, r, nullptr); }
   static constexpr int N8 = 2, N16 = 0, D = PFB_MST_DS;
   static constexpr bool KEEP = false;
   __device__ const double* n8(int k) const { return k == 0 ? dinv : r; }
@@ -166,8 +178,9 @@ struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-
   __device__ double2 smooth0(const Raw& w, double pe) const {
     return make_double2(mgs_mask(om * w.dv * w.bv + pe, w.dv), om * w.dv);  // y, omega D^-1
   }
+  // the scalar march's aux value is free: it carries the node's own r from fetch to out
   __device__ double2 finish(const Raw& w, int, int i, int j, bool, double& aux) const {
-    aux = 0.0;
+    aux = w.bv;
     return smooth0(w, pm.value(i, j));
   }
   __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
@@ -176,14 +189,16 @@ struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-
     Raw w;
     w.dv = di(id);
     w.bv = __ldg(r + id);
+    aux = w.bv;
     return smooth0(w, ProlongMarch<double>::direct(*mf, *mc, ec, i, j, dup));
   }
-  __device__ void out(int id, double2 Av, double2 y) const {
-    const double bv = __ldg(r + id);
+  __device__ void outa(int id, double2 Av, double2 y, double bv) const {
     const double ev = y.x + y.y * (bv - Av.x);
     z[id] = ev;
     *rz += bv * ev;
   }
+  __device__ void out(int id, double2 Av, double2 y) const { outa(id, Av, y, __ldg(r + id)); }
+  __device__ void l2pf(int id, int lane) const { l2pf3(id, lane, dinv, r, nullptr); }
   static constexpr int N8 = 2, N16 = 0, D = PFB_MST_DS + 1;
   static constexpr bool KEEP = true;  // outs reads r from the stage
   __device__ const double* n8(int k) const { return k == 0 ? dinv : r; }
@@ -259,6 +274,7 @@ struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (ma
     q[id] = qv;
     if (!own || node_owned(*own, id)) *pq += p.x * qv;
   }
+  __device__ void l2pf(int id, int lane) const { l2pf3(id, lane, z, pold, dinv); }
   static constexpr int N8 = 3, N16 = 0, D = PFB_MST_DS;
   static constexpr bool KEEP = false;
   __device__ const double* n8(int k) const { return k == 0 ? z : (k == 1 ? pold : dinv); }
@@ -272,6 +288,135 @@ struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (ma
     out(id, Av, p);
   }
 };
+
+// ---- k_evo_prepare as a warp march (big meshes) ---------------------------------------------
+// The tile kernel k_evo_prepare (pf_kernels.cuh) stages a node tile with its halo in shared
+// memory, passes twice over the tile's cells and runs at ~0.2 of the HBM rate on meshes far
+// beyond L2; on those the same quantities come out of one warp march: the value pair is
+// (d, d_prev), the cell contributions carry the residual in x and the diagonal in y, each node
+// sums them in the reference's element order, the free-node flag rides in the aux value.
+// b of a cell in two units' halo is written by both (identical values).
+struct EvoPrepOp {
+  const Consts* C;
+  const double *d, *dprev, *psi, *trp, *dev2, *psimax;
+  const uint8_t* pmask;
+  double *R, *r, *x, *dinv, *b, *diag;
+  int full, extra;
+  double *rr, *ngate, *nonpos;
+  struct Raw {
+    double dv, pv;
+    unsigned fr;
+  };
+  struct CRaw {
+    double2 p01, p23;
+  };
+  __device__ void fetch(int id, int, int, bool, Raw& w) const {
+    w.dv = __ldg(d + id);
+    w.pv = __ldg(dprev + id);
+    w.fr = __ldg(pmask + id);
+  }
+  __device__ double2 finish(const Raw& w, int, int, int, bool, double& aux) const {
+    aux = w.fr ? 1.0 : 0.0;
+    return make_double2(w.dv, w.pv);
+  }
+  __device__ double2 in(int id, int i, int j, bool dup, double& aux) const {
+    aux = 0.0;
+    if (id < 0) return make_double2(0.0, 0.0);
+    Raw w;
+    fetch(id, i, j, dup, w);
+    return finish(w, id, i, j, dup, aux);
+  }
+  __device__ void cfetch(int eid, CRaw& c) const {
+    c.p01 = __ldg(reinterpret_cast<const double2*>(psi) + 2 * eid);
+    c.p23 = __ldg(reinterpret_cast<const double2*>(psi) + 2 * eid + 1);
+  }
+  // residual (assembly.py:217-228), b (:233-239, schemes.py:112-142), diagonal of K_dd (+ K~)
+  __device__ void cellr(int eid, const CRaw& c, const double2 (&v)[4], const double (&)[4],
+                        double2 (&f)[4]) const {
+    const Consts& K = *C;
+    const double dc[4] = {v[0].x, v[1].x, v[2].x, v[3].x};
+    const double ps[4] = {c.p01.x, c.p01.y, c.p23.x, c.p23.y};
+    double dg[4], pg[4], aw[4];
+    interp_q4(K, dc[0], dc[1], dc[2], dc[3], dg);
+    interp_q4(K, v[0].y, v[1].y, v[2].y, v[3].y, pg);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double xq = dg[q] - pg[q];
+      const double pen = K.gamma * (0.5 * (xq - fabs(xq)));
+      const double src = K.at2 ? (K.src_base * 2.0) * dg[q] : K.src_base;
+      aw[q] = (-2.0 * (1.0 - dg[q]) * ps[q] + src + pen) * K.w;
+    }
+    double res[4], dia[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int aa = 0; aa < 4; ++aa) {
+      double s2 = K.N[0][aa] * aw[0] + K.N[1][aa] * aw[1] + K.N[2][aa] * aw[2] +
+                  K.N[3][aa] * aw[3];
+      s2 += K.lap[aa][0] * dc[0] + K.lap[aa][1] * dc[1] + K.lap[aa][2] * dc[2] +
+            K.lap[aa][3] * dc[3];
+      res[aa] = s2;
+    }
+    if (full) {
+      double bq[4], tp[4], dv2[4], pm[4];
+      const double srcd = K.at2 ? K.src_base * 2.0 : 0.0;
+      if (extra) {
+        load4(trp, eid, tp);
+        load4(dev2, eid, dv2);
+        load4(psimax, eid, pm);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        bq[q] = 2.0 * ps[q] + srcd + K.gamma * (dg[q] < pg[q] ? 1.0 : 0.0);
+        if (extra && gate_gp(K, ps[q], pm[q], dg[q])) {
+          bq[q] = bq[q] + extra_gp(K, extra, dg[q], tp[q], dv2[q]);
+          *ngate += 1.0;  // only its sign is used (cells in a halo count twice)
+        }
+      }
+      store4(b, eid, bq);
+#pragma unroll
+      for (int aa = 0; aa < 4; ++aa)
+        dia[aa] = K.Nw[0][aa] * K.N[0][aa] * bq[0] + K.Nw[1][aa] * K.N[1][aa] * bq[1] +
+                  K.Nw[2][aa] * K.N[2][aa] * bq[2] + K.Nw[3][aa] * K.N[3][aa] * bq[3] +
+                  K.lap[aa][aa];
+    }
+#pragma unroll
+    for (int aa = 0; aa < 4; ++aa) f[aa] = make_double2(res[aa], dia[aa]);
+  }
+  __device__ void outa(int id, double2 Av, double2, double aux) const {
+    const bool fr = aux != 0.0;
+    const double Rv = Av.x;
+    if (R) R[id] = Rv;
+    if (fr) *rr += Rv * Rv;
+    if (full) {
+      r[id] = fr ? -Rv : 0.0;
+      x[id] = 0.0;
+      if (diag) diag[id] = Av.y;
+      if (fr && !(Av.y > 0.0)) *nonpos += 1.0;
+      dinv[id] = fr ? 1.0 / Av.y : 0.0;
+    }
+  }
+  __device__ void out(int id, double2 Av, double2 v) const {
+    outa(id, Av, v, __ldg(pmask + id) ? 1.0 : 0.0);
+  }
+};
+
+// partials[3 * block + {0, 1, 2}] = (sum of free R^2, gated Gauss points, free nodes with a
+// non-positive diagonal), like k_evo_prepare
+__global__ void __launch_bounds__(MG_NT, 2) k_evo_prepare_march(EvoPrepArgs a, MarchGeom g) {
+  __shared__ MgWarp ws[MG_WARPS];
+  __shared__ double red[MG_WARPS * 3];
+  double rr = 0.0, ngate = 0.0, nonpos = 0.0;
+  EvoPrepOp op{&a.C, a.d, a.dprev, a.psi, a.trp, a.dev2, a.psimax, a.pmask, a.R, a.r, a.x,
+               a.dinv, a.b, a.diag, a.full, a.extra_scheme, &rr, &ngate, &nonpos};
+  const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
+  if (w < g.n_units) mg_march(a.m, g, w, op, ws[threadIdx.x >> 5]);
+  double v[3] = {rr, ngate, nonpos};
+  mg_block_sum<3>(v, red);
+  if (threadIdx.x == 0) {
+    a.partials[3 * blockIdx.x + 0] = v[0];
+    a.partials[3 * blockIdx.x + 1] = v[1];
+    a.partials[3 * blockIdx.x + 2] = v[2];
+  }
+}
 
 // ---- coarse levels: node kernels of the assembled scalar form -------------------------------
 template <int W>
@@ -559,6 +704,22 @@ __global__ void __launch_bounds__(MG_NT) k_mgs_rsmooth(MgsArgs A, int l) {
   });
 }
 
+// power step of a large one-thread-per-node level with the row-table stencil ids (same sums as
+// mgs_spow<1>)
+__global__ void __launch_bounds__(MG_NT) k_mgs_rpow(MgsArgs A, int l, int step) {
+  const MgsLevel& L = A.L[l];
+  const int n = L.m.n_nodes;
+  const double* vin = step == 1 ? (A.pow_warm ? L.ev : nullptr) : (((step - 1) & 1) ? L.t : L.e);
+  double* vout = (step & 1) ? L.t : L.e;
+  mg_for_nodes<GMem>(L.m, MGS_GW, [&](int id, int i, int j, bool dup) {
+    const double Av = mgs_row_apply(L, n, id, i, j, dup, [&](int k) -> double {
+      const double x = vin ? __ldg(vin + k) : mg_hash01(2u * k + 1u);
+      return mgs_mask(x, __ldg(L.dinv + k));
+    });
+    vout[id] = __ldg(L.dinv + id) * Av;
+  });
+}
+
 // power step at one node of a coarse level: vout = D^-1 A vin (vin == nullptr: hashed start)
 template <int LPN>
 __device__ __forceinline__ void mgs_spow(const MgsLevel& L, const double* vin, double* vout,
@@ -730,8 +891,9 @@ __global__ void __launch_bounds__(MG_NT, 3) k_mgs_pow(MgsArgs A, int step, int f
 }
 // the coarse grid levels' power step on its own (a light kernel at full occupancy: inside the
 // march kernel's register budget it took 2.0 ms per step at cfg5)
-__global__ void __launch_bounds__(MG_NT) k_mgs_pow_coarse(MgsArgs A, int step) {
-  const int t = blockIdx.x * MG_NT + threadIdx.x;
+// (levels by the row-table kernel k_mgs_rpow come first in the item space: skipped by off0)
+__global__ void __launch_bounds__(MG_NT) k_mgs_pow_coarse(MgsArgs A, int step, int off0) {
+  const int t = off0 + blockIdx.x * MG_NT + threadIdx.x;
   if (t >= A.coarse_items) return;
   int l = 1;
   while (l + 1 < A.n_tail && t >= A.L[l + 1].item_off) ++l;

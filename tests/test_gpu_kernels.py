@@ -19,11 +19,15 @@ class _Cfg:
         1e-7, 1e-6, 50, 2000, 0.95, 1e-12, "direct")
 
 
+@pytest.mark.parametrize("prep", ["tile", "march"])
 @pytest.mark.parametrize("mesh", KAT_MESHES)
 @pytest.mark.parametrize("tag", ["at2", "at1"])
-def test_kernels_match_reference(mesh, tag, cuda_ok):
+def test_kernels_match_reference(mesh, tag, prep, cuda_ok, monkeypatch):
+    """prep: the phase-field residual / coefficient / diagonal kernel as the tile kernel (small
+    meshes' default) or as the warp march (big meshes' default, forced here)."""
     from paper_2209_07969_b200.session import DeviceSession
 
+    monkeypatch.setenv("PFB200_EVO_MARCH", "1" if prep == "march" else "0")
     z = golden(f"kat_{mesh}.npz")
     m = kat_mesh(mesh)
     s = DeviceSession(m, kat_params(tag), _Cfg(), device=0)

@@ -97,6 +97,18 @@ def test_end_to_end_matches_reference(case, scheme, cuda_ok):
             z["table"][:, 4].sum(), rel=0.15, abs=3)
 
 
+@pytest.mark.parametrize("case,scheme", [
+    ("shear32", "S3"), ("tension32", "S1"), ("lpanel25", "S1"), ("multicrack32", "ST"),
+    ("tension16_at1", "S3")])
+def test_end_to_end_with_evo_prepare_march(case, scheme, cuda_ok, monkeypatch):
+    """The big meshes' march form of the phase-field prepare kernel (k_evo_prepare_march),
+    forced on reduced cases: whole runs against the reference's tables."""
+    monkeypatch.setenv("PFB200_EVO_MARCH", "1")
+    z = golden(f"run_{case}_{scheme}.npz")
+    pb, recs = run_case(case, scheme)
+    check_against_golden(recs, z, pb.state, case, scheme, pb.mesh)
+
+
 CFG1_MAX_STAG = {}
 
 
