@@ -24,28 +24,6 @@
 
 using pfb::CgResult;
 
-// dynamic shared memory of the staged fine marches (pf_mg.cuh mg_march_st; PFB_MST bit per kernel)
-static constexpr size_t SM_MGS_RESID = (PFB_MST & 1) ? pfb::MStage<pfb::SFineResid>::CTA : 0;
-static constexpr size_t SM_MGS_SMOOTH = (PFB_MST & 2) ? pfb::MStage<pfb::SFineSmooth>::CTA : 0;
-static constexpr size_t SM_MGS_PCG = (PFB_MST & 4) ? pfb::MStage<pfb::SFinePcg>::CTA : 0;
-static constexpr size_t SM_MG_RESID = (PFB_MST & 8) ? pfb::MStage<pfb::FineResid>::CTA : 0;
-static constexpr size_t SM_MG_SMOOTH = (PFB_MST & 16) ? pfb::MStage<pfb::FineSmooth>::CTA : 0;
-static constexpr size_t SM_MG_PCG = (PFB_MST & 32) ? pfb::MStage<pfb::FinePcg>::CTA : 0;
-static cudaError_t mst_opt_in() {  // per device and process: idempotent
-  cudaError_t e = cudaSuccess;
-  auto set = [&](const void* fn, size_t bytes) {
-    if (e == cudaSuccess && bytes)
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  };
-  set((const void*)pfb::k_mgs_fine_resid, SM_MGS_RESID);
-  set((const void*)pfb::k_mgs_fine_smooth, SM_MGS_SMOOTH);
-  set((const void*)pfb::k_mgs_pcg, SM_MGS_PCG);
-  set((const void*)pfb::k_mg_fine_resid, SM_MG_RESID);
-  set((const void*)pfb::k_mg_fine_smooth, SM_MG_SMOOTH);
-  set((const void*)pfb::k_mg_pcg, SM_MG_PCG);
-  return e;
-}
-
 // One multigrid PCG instance (pf_mg.cuh): the momentum solves (phys 0) and the phase-field
 // solves without the SPD probe (phys 1, the scalar field embedded as the x component of a
 // two-component system) each have their own hierarchy, buffers and graphs.
@@ -911,7 +889,7 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
   } while (0)
   auto body_kernels = [&](const pfb::MgArgs& B, bool krylov = true) {
     const int c = nl - 1, top = std::min(B.n_tail, c);  // grid levels [1, top)
-    pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, SM_MG_RESID, s>>>(B);
+    pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(B);
     for (int l = 1; l < top; ++l) {
       // fused down-sweep only on the smallest grid levels: it evaluates 12 restriction sources
       // per stencil slot (cfg2, ncu: 16.6 k nodes 13.7 us fused vs 11.8 split; <= 4.2 k nodes
@@ -952,9 +930,9 @@ static pf_status mg_build_graphs(pf_handle* h, MgInst& M) {
         MG_NODE_KERNEL(k_mg_ssmooth, l, B, l);
       }
     }
-    pfb::k_mg_fine_smooth<<<M.gf, pfb::MG_NT, SM_MG_SMOOTH, s>>>(B);
+    pfb::k_mg_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(B);
     if (!krylov) return;
-    pfb::k_mg_pcg<<<M.gf, pfb::MG_NT, SM_MG_PCG, s>>>(B, M.gf);
+    pfb::k_mg_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(B, M.gf);
     pfb::k_mg_update<<<M.gflat, pfb::MG_NT, 0, s>>>(B, M.gf, M.gf);
   };
   {
@@ -1182,7 +1160,7 @@ static pf_status mgs_setup(pf_handle* h, MgsInst& M, int fine_resident_warps) {
   M.gf = (A.g0.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
   {
     int orr = 0;
-    PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&orr, pfb::k_mgs_fine_resid, pfb::MG_NT, SM_MGS_RESID));
+    PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&orr, pfb::k_mgs_fine_resid, pfb::MG_NT, 0));
     A.g0r = pfb::make_march_geom(h->nx, lv[0].ny, std::max(1, orr) * h->sm_count * pfb::MG_WARPS);
     M.gfr = (A.g0r.n_units + pfb::MG_WARPS - 1) / pfb::MG_WARPS;
   }
@@ -1270,7 +1248,7 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
   } while (0)
   const int c = nl - 1, top = std::min(A.n_tail, c);
   auto body_kernels = [&](const pfb::MgsArgs& B, bool krylov = true) {
-    pfb::k_mgs_fine_resid<<<M.gfr, pfb::MG_NT, SM_MGS_RESID, s>>>(B);
+    pfb::k_mgs_fine_resid<<<M.gfr, pfb::MG_NT, 0, s>>>(B);
     for (int l = 1; l < top; ++l) {
       if (M.lpn[l] == 16 && M.fuse && B.L[l].m.n_nodes <= 8192) {
         pfb::k_mgs_sdown<16><<<M.gn[l], pfb::MG_NT, 0, s>>>(B, l);
@@ -1309,9 +1287,9 @@ static pf_status mgs_build_graphs(pf_handle* h, MgsInst& M) {
         MGS_NODE_KERNEL(k_mgs_ssmooth, l, B, l);
       }
     }
-    pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, SM_MGS_SMOOTH, s>>>(B);
+    pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(B);
     if (!krylov) return;
-    pfb::k_mgs_pcg<<<M.gf, pfb::MG_NT, SM_MGS_PCG, s>>>(B, M.gf);
+    pfb::k_mgs_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(B, M.gf);
     pfb::k_mgs_update<<<M.gflat, pfb::MG_NT, 0, s>>>(B, M.gf, M.gf);
   };
   M.body_kernels = 4 + (A.n_tail < nl ? 1 : 1 + (A.dense ? 1 : A.nu_c));
@@ -1722,12 +1700,11 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
         if (h->h_nst[j] == (int)strip->own_lo) { h->mgd_row0 = j; break; }
     }
     if (want) {
-      CREATE_CUDA(mst_opt_in());
       int om = 0, o2 = 0;
-      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, pfb::k_mg_fine_smooth, pfb::MG_NT, SM_MG_SMOOTH));
-      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_mg_pcg, pfb::MG_NT, SM_MG_PCG));
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, pfb::k_mg_fine_smooth, pfb::MG_NT, 0));
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_mg_pcg, pfb::MG_NT, 0));
       om = std::min(om, o2);
-      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_mg_fine_resid, pfb::MG_NT, SM_MG_RESID));
+      CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pfb::k_mg_fine_resid, pfb::MG_NT, 0));
       om = std::min(om, o2);
       if (om >= 1) {
         pf_status ms = mg_setup(h, h->mgu, 0, om * dev_sms * pfb::MG_WARPS);
@@ -1744,10 +1721,10 @@ static pf_status create_impl(const pf_mesh* mesh, const pf_material* mat, const 
           if (es != PF_OK) return bail(es);
         } else if ((mev == "1" || mev == "scalar") && h->mgu.on) {
           int os = 0, o3 = 0;
-          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&os, pfb::k_mgs_fine_smooth, pfb::MG_NT, SM_MGS_SMOOTH));
-          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, pfb::k_mgs_pcg, pfb::MG_NT, SM_MGS_PCG));
+          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&os, pfb::k_mgs_fine_smooth, pfb::MG_NT, 0));
+          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, pfb::k_mgs_pcg, pfb::MG_NT, 0));
           os = std::min(os, o3);
-          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, pfb::k_mgs_fine_resid, pfb::MG_NT, SM_MGS_RESID));
+          CREATE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, pfb::k_mgs_fine_resid, pfb::MG_NT, 0));
           os = std::max(1, std::min(os, o3));
           pf_status es = mgs_setup(h, h->mgs, os * dev_sms * pfb::MG_WARPS);
           if (es != PF_OK) return bail(es);
@@ -3306,13 +3283,13 @@ extern "C" pf_status pf_bench_mg_kernel(pf_handle* h, int which, int reps, doubl
     const double n1 = A.L[1].m.n_nodes;
     if (which == 0) {
       bytes = 56.0 * n + e;  // r, D^-1 (16 B), d (8 B), t (16 B); branch bits 1 B per cell
-      PF_TRY(run([&] { pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, SM_MG_RESID, s>>>(A); }));
+      PF_TRY(run([&] { pfb::k_mg_fine_resid<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));
     } else if (which == 1) {
       bytes = 56.0 * n + 16.0 * n1 + e;  // r, D^-1, d, z; level-1 correction; bits
-      PF_TRY(run([&] { pfb::k_mg_fine_smooth<<<M.gf, pfb::MG_NT, SM_MG_SMOOTH, s>>>(A); }));
+      PF_TRY(run([&] { pfb::k_mg_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));
     } else {
       bytes = 88.0 * n + e;  // z, p_old, d, D^-1, p_new, q; bits
-      PF_TRY(run([&] { pfb::k_mg_pcg<<<M.gf, pfb::MG_NT, SM_MG_PCG, s>>>(A, M.gf); }));
+      PF_TRY(run([&] { pfb::k_mg_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(A, M.gf); }));
     }
   } else if (which >= 10 && which <= 12) {
     if (!h->mgs.on || h->mgs.setups == 0) return fail(h, PF_ERR_INVALID, "no built phase-field hierarchy");
@@ -3322,13 +3299,13 @@ extern "C" pf_status pf_bench_mg_kernel(pf_handle* h, int which, int reps, doubl
     const double n1 = A.L[1].m.n_nodes;
     if (which == 10) {
       bytes = 24.0 * n + 32.0 * e;  // r, D^-1, t (8 B); b per Gauss point (32 B per cell)
-      PF_TRY(run([&] { pfb::k_mgs_fine_resid<<<M.gfr, pfb::MG_NT, SM_MGS_RESID, s>>>(A); }));
+      PF_TRY(run([&] { pfb::k_mgs_fine_resid<<<M.gfr, pfb::MG_NT, 0, s>>>(A); }));
     } else if (which == 11) {
       bytes = 24.0 * n + 8.0 * n1 + 32.0 * e;  // r, D^-1, z; level-1 correction; b
-      PF_TRY(run([&] { pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, SM_MGS_SMOOTH, s>>>(A); }));
+      PF_TRY(run([&] { pfb::k_mgs_fine_smooth<<<M.gf, pfb::MG_NT, 0, s>>>(A); }));
     } else {
       bytes = 40.0 * n + 32.0 * e;  // z, p_old, D^-1, p_new, q; b
-      PF_TRY(run([&] { pfb::k_mgs_pcg<<<M.gf, pfb::MG_NT, SM_MGS_PCG, s>>>(A, M.gf); }));
+      PF_TRY(run([&] { pfb::k_mgs_pcg<<<M.gf, pfb::MG_NT, 0, s>>>(A, M.gf); }));
     }
   } else {
     return fail(h, PF_ERR_INVALID, "pf_bench_mg_kernel: unknown kernel");

@@ -28,26 +28,8 @@
 // (last-block pattern), so every result is bit-reproducible run to run.
 #pragma once
 
-// staged (TMA bulk copy) fine marches, mg_march_st below: bit k switches kernel k to the staged
-// march (1 / 2 / 4: scalar phase-field residual / smoothing / direction; 8 / 16 / 32: momentum);
-// stages per warp of the scalar and the momentum marches
-#ifndef PFB_MST
-#define PFB_MST 0
-#endif
-// rows ahead of the fine marches' L2 prefetch hints (0: none)
-#ifndef PFB_L2PF
-#define PFB_L2PF 0
-#endif
-#ifndef PFB_MST_DS
-#define PFB_MST_DS 3
-#endif
-#ifndef PFB_MST_DM
-#define PFB_MST_DM 4
-#endif
-
 namespace pfb {
 
-constexpr int MST_R8 = 288, MST_R16 = 512, MST_RC = 1024;  // slot regions (mg_march_st)
 constexpr int MG_MAXL = 14;
 constexpr int MG_NT = 256;
 constexpr int MG_WARPS = MG_NT / 32;
@@ -191,10 +173,8 @@ __device__ __forceinline__ double mg_q(int c, int k, int K) {
 //   void out(int id, double2 Av, double2 vin)                 once per owned node
 // The cell data of the next cell row (branch bits / Newton coefficients) is fetched one row
 // step ahead like the node rows, so no dependent HBM load sits on a row step's critical path.
-// optional parts of an Op (overload rank by the last argument):
+// optional part of an Op (overload rank by the last argument):
 //   void outa(int id, double2 Av, double2 vin, double aux)   out() with the node's aux value
-//   void l2pf(int id, int lane) / void cl2pf(int eid, int lane)   L2 prefetch of the node's /
-//                                                                  cell's lines, rows ahead
 template <class Op>
 __device__ __forceinline__ auto mg_out(Op& op, int id, double2 Av, double2 v, double a, int)
     -> decltype(op.outa(id, Av, v, a), void()) {
@@ -204,24 +184,6 @@ template <class Op>
 __device__ __forceinline__ void mg_out(Op& op, int id, double2 Av, double2 v, double, long) {
   op.out(id, Av, v);
 }
-template <class Op>
-__device__ __forceinline__ auto mg_l2pf(Op& op, int id, int lane, int)
-    -> decltype(op.l2pf(id, lane), void()) {
-  op.l2pf(id, lane);
-}
-template <class Op>
-__device__ __forceinline__ void mg_l2pf(Op&, int, int, long) {}
-template <class Op>
-__device__ __forceinline__ auto mg_cl2pf(Op& op, int eid, int lane, int)
-    -> decltype(op.cl2pf(eid, lane), void()) {
-  op.cl2pf(eid, lane);
-}
-template <class Op>
-__device__ __forceinline__ void mg_cl2pf(Op&, int, int, long) {}
-__device__ __forceinline__ void l2_prefetch(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-}
-
 template <class Op>
 __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int unit, Op& op,
                                          MgWarp& ws) {
@@ -295,15 +257,6 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
     typename Op::CRaw c_nx;
     const int e_nx = (cj + 1 < r1) ? cell_id(cj + 1) : -1;
     if (e_nx >= 0) op.cfetch(e_nx, c_nx);
-#if PFB_L2PF
-    // the lines PFB_L2PF rows further up into L2 (the row stride of the last two rows: exact on
-    // regular rows, a harmless wrong line elsewhere), so the register prefetch one row ahead
-    // meets L2 latency instead of HBM latency
-    if (id_nx >= 0 && id_hi >= 0)
-      mg_l2pf(op, min(max(id_nx + PFB_L2PF * (id_nx - id_hi), 0), m.n_nodes - 1), lane, 0);
-    if (e_nx >= 0 && eid >= 0)
-      mg_cl2pf(op, min(max(e_nx + PFB_L2PF * (e_nx - eid), 0), m.n_elems - 1), lane, 0);
-#endif
     const bool use_dup = lo_slit && dupcol;
     const double2 b0 = use_dup ? ws.dv[lane] : v_lo;
     const double e0 = use_dup ? ws.da[lane] : a_lo;
@@ -368,250 +321,6 @@ __device__ __forceinline__ void mg_mbar_wait(unsigned long long* bar, unsigned p
 }
 __device__ __forceinline__ unsigned mg_r16(size_t b) { return (unsigned)((b + 15) & ~size_t(15)); }
 
-// ----------------------------------------------------------------------------------------
-// Staged warp march: mg_march with the node rows (and, for the scalar field, the cell rows) of
-// the next rows brought into shared memory by TMA bulk copies (cp.async.bulk completing on an
-// mbarrier) instead of per-lane loads held in registers.  A warp's 32 columns of a node row are
-// one contiguous run of every nodal array (row-compact numbering), so one elected lane issues
-// one bulk copy per array and row; Op::D stages per warp keep D - 1 rows beyond the current one
-// in flight -- Little's law at ~6.5 TB/s and ~1 us of loaded latency needs ~44 KB in flight per
-// SM, three times what one register-prefetched row per resident warp holds.  A stage (node row
-// t + 1, cell row t) stays valid through iteration t + 1, when its nodes are the march's lower
-// row, so Op::outs reads the per-node data it needs again (r, D^-1) from shared memory instead
-// of reloading it from L1/L2 on the critical path.
-// Op adds to mg_march's interface:
-//   N8 / N16 / CST / D        8-byte and 16-byte nodal arrays, cell records staged?, stages
-//   const double* n8(k), n16(k), const double* cst()   the arrays (nullptr: absent this launch)
-//   void take(slot, e8, e16, Raw&)      the node's staged data (element indices in the slot)
-//   void ctake(cslot, ce, CRaw&)        the cell's staged record (CST)
-//   void ahead(id, i, j)                per-row work outside the stages (prolongation sources)
-//   void outs(slot, e8, e16, id, Av, vin)   out() with the node's stage
-// 8-byte runs start on an even element (16-byte alignment of the bulk copy), so a region holds
-// up to 34 elements.
-template <class Op>
-struct MStage {
-  static constexpr int O16 = Op::N8 * MST_R8;
-  static constexpr int OC = O16 + Op::N16 * MST_R16;
-  static constexpr int SLOT = OC + (Op::CST ? MST_RC : 0);
-  static constexpr int WARP = SLOT * Op::D;
-  static constexpr int CTA = WARP * MG_WARPS;
-};
-__device__ __forceinline__ void mst_bar_init(unsigned long long* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mst_bar_expect(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
-               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-template <class Op>
-__device__ __forceinline__ void mg_march_st(const DMesh& m, const MarchGeom& G, int unit, Op& op,
-                                            MgWarp& ws, unsigned char* ring,
-                                            unsigned long long* bars) {
-  using ST = MStage<Op>;
-  constexpr int D = Op::D;
-  const int lane = threadIdx.x & 31;
-  const int strip = unit % G.n_strips;
-  const int r0 = (unit / G.n_strips) * G.rows_per_unit;
-  const int r1 = min(r0 + G.rows_per_unit, m.ny + 1);
-  const int col0 = strip * TXW - 1;
-  const int col = col0 + lane;
-  const bool lane_own = lane >= 1 && lane <= TXW;
-  const int R = m.notch_row;
-  const bool dupcol = R >= 0 && col >= m.notch_lo && col < m.notch_hi;
-  const int t0 = r0 - 1;
-  if (lane == 0) {
-#pragma unroll
-    for (int s2 = 0; s2 < D; ++s2) mst_bar_init(bars + s2);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  }
-  int base = 0;
-  // row windows of THIS strip: node rows t .. t+31 as (first column, count, first id, bytes of
-  // an 8-byte run) and cell rows as (first column, count, first id): lane l prepares row t + l
-  auto win = [&](int t) {
-    __syncwarp();
-    base = t;
-    const int jj = t + lane;
-    int4 nw = make_int4(0, 0, 0, 0), ew = make_int4(0, 0, 0, 0);
-    if (jj >= 0 && jj <= m.ny) {
-      const int4 rw = __ldg(m.nrow + jj);
-      const int clo = max(col0, rw.x), cnt = min(col0 + 32, rw.y) - clo;
-      if (cnt > 0) {
-        const int id0 = rw.z + (clo - rw.x);
-        nw = make_int4(clo, cnt, id0, (((id0 + cnt + 1) & ~1) - (id0 & ~1)) * 8);
-      }
-    }
-    if (jj >= 0 && jj < m.ny) {
-      const int4 er = __ldg(m.erow + jj);
-      const int elo = max(col0, er.x), ecnt = min(col0 + 31, er.y) - elo;
-      if (ecnt > 0) ew = make_int4(elo, ecnt, er.z + (elo - er.x), 0);
-    }
-    ws.nwin[lane] = nw;
-    ws.ewin[lane] = ew;
-    __syncwarp();
-  };
-  // stage t = node row t + 1 and cell row t, into slot sl (lane 0)
-  auto issue = [&](int t, int sl) {
-    unsigned char* slot = ring + sl * ST::SLOT;
-    const int4 nw = ws.nwin[t + 1 - base];
-    const unsigned b8 = (unsigned)nw.w, b16 = (unsigned)(nw.y * 16);
-    unsigned bc = 0u;
-    int e0 = 0;
-    if (Op::CST) {
-      const int4 ew = ws.ewin[t - base];
-      e0 = ew.z;
-      bc = op.cst() ? (unsigned)(ew.y * 32) : 0u;
-    }
-    unsigned bytes = bc;
-#pragma unroll
-    for (int k = 0; k < Op::N8; ++k) bytes += op.n8(k) ? b8 : 0u;
-#pragma unroll
-    for (int k = 0; k < Op::N16; ++k) bytes += op.n16(k) ? b16 : 0u;
-    mst_bar_expect(bars + sl, bytes);
-    if (nw.y > 0) {
-#pragma unroll
-      for (int k = 0; k < Op::N8; ++k)
-        if (op.n8(k)) mg_bulk_g2s(slot + k * MST_R8, op.n8(k) + (nw.z & ~1), b8, bars + sl);
-#pragma unroll
-      for (int k = 0; k < Op::N16; ++k)
-        if (op.n16(k))
-          mg_bulk_g2s(slot + ST::O16 + k * MST_R16, op.n16(k) + 2 * (size_t)nw.z, b16, bars + sl);
-    }
-    if (Op::CST && bc) mg_bulk_g2s(slot + ST::OC, op.cst() + 4 * (size_t)e0, bc, bars + sl);
-  };
-  auto row_id = [&](int j, int& e8, int& e16) -> int {  // node (col, j) and its slot indices
-    const int4 nw = ws.nwin[j - base];
-    const int k = col - nw.x;
-    if ((unsigned)k >= (unsigned)nw.y) return -1;
-    e16 = k;
-    e8 = k + (nw.z & 1);
-    return nw.z + k;
-  };
-  auto cell_of = [&](int cj, int& ce) -> int {  // cell (col, cj) and its slot index
-    const int4 ew = ws.ewin[cj - base];
-    ce = col - ew.x;
-    return (unsigned)ce < (unsigned)ew.y ? ew.z + ce : -1;
-  };
-  auto load_dup = [&]() {
-    const int id = dupcol ? m.dup_start + (col - m.notch_lo) : -1;
-    double a = 0.0;
-    const double2 v = op.in(id, col, R, true, a);
-    ws.dv[lane] = v;
-    ws.da[lane] = a;
-    ws.did[lane] = id;
-    __syncwarp();
-  };
-  // KEEP: a stage outlives its iteration by one (outs reads it), so D slots hold D - 1 stages
-  // ahead of the consumer; otherwise the slot is refilled as soon as the warp has consumed it
-  constexpr int LA = Op::KEEP ? D - 1 : D;
-  win(t0);
-  if (lane == 0) {
-#pragma unroll 1
-    for (int k = 0; k < LA; ++k)
-      if (t0 + k < r1) issue(t0 + k, k);
-  }
-  double a_lo = 0.0, a_hi = 0.0;
-  int e8_lo = 0, e16_lo = 0;
-  int id_lo = t0 >= 0 ? row_id(t0, e8_lo, e16_lo) : -1;
-  double2 v_lo = op.in(id_lo, col, t0, false, a_lo);
-  bool lo_slit = (t0 == R);
-  if (lo_slit) load_dup();
-  {
-    int x8, x16;
-    const int id_a = row_id(r0, x8, x16);
-    if (id_a >= 0) op.ahead(id_a, col, r0);
-  }
-  typename Op::CRaw c_cur;
-  int e_cur = -1;
-  if (!Op::CST) {
-    int ce;
-    e_cur = cell_of(t0, ce);
-    if (e_cur >= 0) op.cfetch(e_cur, c_cur);
-  }
-  double2 acc_lo = make_double2(0.0, 0.0);
-  int sl = 0;         // slot of the current stage; the previous stage sits in slot sl - 1 (mod D)
-  unsigned ph = 0u;   // parity of slot sl's current use
-  for (int cj = t0; cj < r1; ++cj) {
-    const int jh = cj + 1;
-    if (cj + LA + 1 - base >= 32) win(cj);
-    mg_mbar_wait(bars + sl, ph);
-    const unsigned char* slot = ring + sl * ST::SLOT;
-    const int slp = sl == 0 ? D - 1 : sl - 1;
-    const unsigned char* pslot = ring + slp * ST::SLOT;
-    int e8_hi = 0, e16_hi = 0;
-    const int id_hi = row_id(jh, e8_hi, e16_hi);
-    a_hi = 0.0;
-    double2 v_hi = make_double2(0.0, 0.0);
-    if (id_hi >= 0) {
-      typename Op::Raw w;
-      op.take(slot, e8_hi, e16_hi, w);
-      v_hi = op.finish(w, id_hi, col, jh, false, a_hi);
-    }
-    int eid;
-    typename Op::CRaw c_nx;
-    int e_nx = -1;
-    if (Op::CST) {
-      int ce;
-      eid = cell_of(cj, ce);
-      if (eid >= 0) op.ctake(slot + ST::OC, ce, c_cur);
-    } else {
-      eid = e_cur;
-      int ce;
-      if (cj + 1 < r1) e_nx = cell_of(cj + 1, ce);
-      if (e_nx >= 0) op.cfetch(e_nx, c_nx);
-    }
-    if (jh + 1 <= r1) {
-      int x8, x16;
-      const int id_a = row_id(jh + 1, x8, x16);
-      if (id_a >= 0) op.ahead(id_a, col, jh + 1);
-    }
-    const bool hi_slit = (jh == R);
-    const bool use_dup = lo_slit && dupcol;
-    const double2 b0 = use_dup ? ws.dv[lane] : v_lo;
-    const double e0 = use_dup ? ws.da[lane] : a_lo;
-    const double2 b1 = shfl_dn(b0), t2 = shfl_dn(v_hi);
-    const double e1 = shfl_dn(e0), e2 = shfl_dn(a_hi);
-    double2 f[4];
-    f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
-    if (eid >= 0) {
-      const double2 v[4] = {b0, b1, t2, v_hi};
-      const double a[4] = {e0, e1, e2, a_hi};
-      op.cellr(eid, c_cur, v, a, f);
-    }
-    const double2 c1l = shfl_up(f[1]), c2l = shfl_up(f[2]);
-    // (the shuffles above consumed every lane's reads of the current stage)
-    if (!Op::KEEP && lane == 0 && cj + LA < r1) issue(cj + LA, sl);
-    if (lane_own && cj >= r0) {
-      if (use_dup) {
-        if (id_lo >= 0) op.outs(pslot, e8_lo, e16_lo, id_lo, acc_lo, v_lo);  // lower face
-        const int idd = ws.did[lane];
-        if (idd >= 0) op.out(idd, d2add(c1l, f[0]), ws.dv[lane]);  // upper face
-      } else if (id_lo >= 0) {
-        op.outs(pslot, e8_lo, e16_lo, id_lo, d2add(d2add(acc_lo, c1l), f[0]), v_lo);
-      }
-    }
-    acc_lo = d2add(c2l, f[3]);
-    __syncwarp();  // every lane is done with the previous stage: refill its slot
-    if (Op::KEEP && lane == 0 && cj + LA < r1) issue(cj + LA, slp);
-    if (hi_slit) load_dup();
-    v_lo = v_hi;
-    a_lo = a_hi;
-    id_lo = id_hi;
-    e8_lo = e8_hi;
-    e16_lo = e16_hi;
-    lo_slit = hi_slit;
-    if (!Op::CST) {
-      e_cur = e_nx;
-      c_cur = c_nx;
-    }
-    if (++sl == D) {
-      sl = 0;
-      ph ^= 1u;
-    }
-  }
-}
-
 // ---- fine-level (level 0) node ops for mg_march ---------------------------------------------
 // The fine operator is K_uu(u, d) applied cell by cell (pf_march.cuh mom_cell_fast: branch bits
 // per cell, g(d) at the Gauss points from the nodal d carried as the march's aux value).
@@ -655,26 +364,7 @@ struct FineBase {
     }
   }
   __device__ double2 di(int id) const { return __ldg(reinterpret_cast<const double2*>(dinv) + id); }
-  // staged march (mg_march_st): nodal arrays through shared memory, the cell data (1 B of
-  // branch bits) by cfetch one row step ahead as in mg_march
-  __device__ void l2pf3(int id, int lane, const double* a16, const double* b16) const {
-    if ((lane & 7) == 0) {
-      l2_prefetch(reinterpret_cast<const double2*>(a16) + id);
-      if (b16) l2_prefetch(reinterpret_cast<const double2*>(b16) + id);
-    }
-    if ((lane & 15) == 0) l2_prefetch(d + id);
-  }
-  static constexpr bool CST = false;
-  __device__ const double* cst() const { return nullptr; }
-  __device__ void ctake(const unsigned char*, int, CRaw&) const {}
-  __device__ void ahead(int, int, int) const {}
 };
-__device__ __forceinline__ double mst_s8(const unsigned char* slot, int k, int e8) {
-  return reinterpret_cast<const double*>(slot + k * MST_R8)[e8];
-}
-__device__ __forceinline__ double2 mst_s16(const unsigned char* slot, int n8, int k, int e16) {
-  return reinterpret_cast<const double2*>(slot + n8 * MST_R8 + k * MST_R16)[e16];
-}
 
 __device__ __forceinline__ double2 mask2(double2 v, double2 di) {
   return make_double2(di.x != 0.0 ? v.x : 0.0, di.y != 0.0 ? v.y : 0.0);
@@ -707,21 +397,6 @@ struct FineResid : FineBase {  // x = omega D^-1 r (pre-smoothing from zero), t 
   __device__ void out(int id, double2 Av, double2) const {
     const double2 bv = d2ldcg(r, id);
     d2st(t, id, mask2(make_double2(bv.x - Av.x, bv.y - Av.y), di(id)));
-  }
-  __device__ void l2pf(int id, int lane) const { l2pf3(id, lane, dinv, r); }
-  static constexpr int N8 = 1, N16 = 2, D = PFB_MST_DM;
-  static constexpr bool KEEP = true;
-  __device__ const double* n8(int) const { return d; }
-  __device__ const double* n16(int k) const { return k == 0 ? dinv : r; }
-  __device__ void take(const unsigned char* slot, int e8, int e16, Raw& w) const {
-    w.dv = mst_s16(slot, N8, 0, e16);
-    w.bv = mst_s16(slot, N8, 1, e16);
-    w.d = mst_s8(slot, 0, e8);
-  }
-  __device__ void outs(const unsigned char* slot, int, int e16, int id, double2 Av,
-                       double2) const {
-    const double2 dv = mst_s16(slot, N8, 0, e16), bv = mst_s16(slot, N8, 1, e16);
-    d2st(t, id, mask2(make_double2(bv.x - Av.x, bv.y - Av.y), dv));
   }
 };
 
@@ -891,21 +566,6 @@ struct FineSmooth : FineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 
   __device__ void out(int id, double2 Av, double2 y) const {
     out2(id, Av, y, di(id), d2ldcg(r, id));
   }
-  __device__ void l2pf(int id, int lane) const { l2pf3(id, lane, dinv, r); }
-  static constexpr int N8 = 1, N16 = 2, D = PFB_MST_DM;
-  static constexpr bool KEEP = true;
-  __device__ const double* n8(int) const { return d; }
-  __device__ const double* n16(int k) const { return k == 0 ? dinv : r; }
-  __device__ void take(const unsigned char* slot, int e8, int e16, Raw& w) const {
-    w.dv = mst_s16(slot, N8, 0, e16);
-    w.bv = mst_s16(slot, N8, 1, e16);
-    w.d = mst_s8(slot, 0, e8);
-  }
-  __device__ void ahead(int, int i, int j) const { pm.fetch(*mf, *mc, ec, i, j); }
-  __device__ void outs(const unsigned char* slot, int, int e16, int id, double2 Av,
-                       double2 y) const {
-    out2(id, Av, y, mst_s16(slot, N8, 0, e16), mst_s16(slot, N8, 1, e16));
-  }
 };
 
 struct FineWarm : FineBase {  // q_k = A u_k (masked); u_j.q_k (j <= k), u_k.b (b = r on entry)
@@ -1020,23 +680,6 @@ struct FinePcg : FineBase {  // p = z + beta p_old (owner stores), q = A p (mask
     if (!own || node_owned(*own, id)) *pq += p.x * qv.x + p.y * qv.y;
   }
   __device__ void out(int id, double2 Av, double2 p) const { out2(id, Av, p, di(id)); }
-  __device__ void l2pf(int id, int lane) const {
-    l2pf3(id, lane, z, pold);
-    if ((lane & 7) == 0) l2_prefetch(reinterpret_cast<const double2*>(dinv) + id);
-  }
-  static constexpr int N8 = 1, N16 = 3, D = PFB_MST_DM;
-  static constexpr bool KEEP = true;
-  __device__ const double* n8(int) const { return d; }
-  __device__ const double* n16(int k) const { return k == 0 ? z : (k == 1 ? pold : dinv); }
-  __device__ void take(const unsigned char* slot, int e8, int e16, Raw& w) const {
-    w.zv = mst_s16(slot, N8, 0, e16);
-    w.po = pold ? mst_s16(slot, N8, 1, e16) : make_double2(0.0, 0.0);
-    w.d = mst_s8(slot, 0, e8);
-  }
-  __device__ void outs(const unsigned char* slot, int, int e16, int id, double2 Av,
-                       double2 p) const {
-    out2(id, Av, p, mst_s16(slot, N8, 2, e16));
-  }
 };
 
 // ---- coarse levels: node-parallel phases ----------------------------------------------------
@@ -1716,15 +1359,7 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_fine_resid(MgArgs A) {
   const double om = __ldcg(&A.ctl->omega[0]);
   FineResid op{{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq}, om, A.r, A.L[0].t};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
-#if PFB_MST & 8
-  extern __shared__ __align__(128) unsigned char mst_ring[];
-  __shared__ unsigned long long mst_bars[MG_WARPS][8];
-  if (w < A.g0.n_units)
-    mg_march_st(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5],
-                mst_ring + (threadIdx.x >> 5) * MStage<FineResid>::WARP, mst_bars[threadIdx.x >> 5]);
-#else
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
-#endif
 }
 
 #define MG_GW (int)(blockIdx.x * MG_WARPS + (threadIdx.x >> 5)), (int)(gridDim.x * MG_WARPS)
@@ -1977,15 +1612,7 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_fine_smooth(MgArgs A) {
   FineSmooth op{{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq}, om, A.r, A.z, &A.L[0].m, &A.L[1].m,
                 A.L[1].e, &rz, {}};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
-#if PFB_MST & 16
-  extern __shared__ __align__(128) unsigned char mst_ring[];
-  __shared__ unsigned long long mst_bars[MG_WARPS][8];
-  if (w < A.g0.n_units)
-    mg_march_st(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5],
-                mst_ring + (threadIdx.x >> 5) * MStage<FineSmooth>::WARP, mst_bars[threadIdx.x >> 5]);
-#else
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
-#endif
   double v[1] = {rz};
   mg_block_sum<1>(v, red);
   if (threadIdx.x == 0) A.part[blockIdx.x] = v[0];  // r.z partials, reduced by k_mg_pcg
@@ -2002,15 +1629,7 @@ __global__ void __launch_bounds__(MG_NT, 2) k_mg_pcg(MgArgs A, int n_rz) {
   FinePcg op{{&A.C, A.flags, A.d, A.L[0].dinv, A.phys, A.bq}, first ? 0.0 : rho[0] / __ldcg(&A.ctl->rho_prev),
              A.z, first ? nullptr : ((k & 1) ? A.p0 : A.p1), (k & 1) ? A.p1 : A.p0, A.q, &pq};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
-#if PFB_MST & 32
-  extern __shared__ __align__(128) unsigned char mst_ring[];
-  __shared__ unsigned long long mst_bars[MG_WARPS][8];
-  if (w < A.g0.n_units)
-    mg_march_st(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5],
-                mst_ring + (threadIdx.x >> 5) * MStage<FinePcg>::WARP, mst_bars[threadIdx.x >> 5]);
-#else
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
-#endif
   double v[1] = {pq};
   mg_block_sum<1>(v, red);
   if (threadIdx.x == 0) A.part[n_rz + blockIdx.x] = v[0];  // p.q partials after the r.z ones

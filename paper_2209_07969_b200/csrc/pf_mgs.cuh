@@ -95,26 +95,6 @@ struct SFineBase {
     for (int k = 0; k < 4; ++k) f[k] = make_double2(fx[k], 0.0);
   }
   __device__ double di(int id) const { return __ldg(dinv + id); }
-  __device__ void cl2pf(int eid, int lane) const {  // 32 B per cell: a 128-byte line per 4 lanes
-    if ((lane & 3) == 0) l2_prefetch(bq + 4 * (size_t)eid);
-  }
-  __device__ void l2pf3(int id, int lane, const double* a, const double* b,
-                        const double* c) const {
-    if ((lane & 15) == 0) {
-      l2_prefetch(a + id);
-      if (b) l2_prefetch(b + id);
-      if (c) l2_prefetch(c + id);
-    }
-  }
-  // staged march (pf_mg.cuh mg_march_st): the cell records come through shared memory
-  static constexpr bool CST = true;
-  __device__ const double* cst() const { return bq; }
-  __device__ void ctake(const unsigned char* cs, int ce, CRaw& c) const {
-    const double2* p = reinterpret_cast<const double2*>(cs) + 2 * ce;
-    c.b01 = p[0];
-    c.b23 = p[1];
-  }
-  __device__ void ahead(int, int, int) const {}
 };
 
 struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), t = r - A x
@@ -143,18 +123,6 @@ struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), 
   }
   __device__ void out(int id, double2 Av, double2 v) const {
     t[id] = v.y == v.y ? v.y - Av.x : 0.0;
-  }
-  __device__ void l2pf(int id, int lane) const { l2pf3(id, lane, dinv, r, nullptr); }
-  static constexpr int N8 = 2, N16 = 0, D = PFB_MST_DS;
-  static constexpr bool KEEP = false;
-  __device__ const double* n8(int k) const { return k == 0 ? dinv : r; }
-  __device__ const double* n16(int) const { return nullptr; }
-  __device__ void take(const unsigned char* slot, int e8, int, Raw& w) const {
-    w.dv = mst_s8(slot, 0, e8);
-    w.bv = mst_s8(slot, 1, e8);
-  }
-  __device__ void outs(const unsigned char*, int, int, int id, double2 Av, double2 v) const {
-    out(id, Av, v);
   }
 };
 
@@ -198,23 +166,6 @@ struct SFineSmooth : SFineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-
     *rz += bv * ev;
   }
   __device__ void out(int id, double2 Av, double2 y) const { outa(id, Av, y, __ldg(r + id)); }
-  __device__ void l2pf(int id, int lane) const { l2pf3(id, lane, dinv, r, nullptr); }
-  static constexpr int N8 = 2, N16 = 0, D = PFB_MST_DS + 1;
-  static constexpr bool KEEP = true;  // outs reads r from the stage
-  __device__ const double* n8(int k) const { return k == 0 ? dinv : r; }
-  __device__ const double* n16(int) const { return nullptr; }
-  __device__ void take(const unsigned char* slot, int e8, int, Raw& w) const {
-    w.dv = mst_s8(slot, 0, e8);
-    w.bv = mst_s8(slot, 1, e8);
-  }
-  __device__ void ahead(int, int i, int j) const { pm.fetch(*mf, *mc, ec, i, j); }
-  __device__ void outs(const unsigned char* slot, int e8, int, int id, double2 Av,
-                       double2 y) const {
-    const double bv = mst_s8(slot, 1, e8);
-    const double ev = y.x + y.y * (bv - Av.x);
-    z[id] = ev;
-    *rz += bv * ev;
-  }
 };
 
 struct SFinePow : SFineBase {  // power step vout = D^-1 A vin (vin == nullptr: hashed start)
@@ -273,19 +224,6 @@ struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (ma
     pnew[id] = p.x;
     q[id] = qv;
     if (!own || node_owned(*own, id)) *pq += p.x * qv;
-  }
-  __device__ void l2pf(int id, int lane) const { l2pf3(id, lane, z, pold, dinv); }
-  static constexpr int N8 = 3, N16 = 0, D = PFB_MST_DS;
-  static constexpr bool KEEP = false;
-  __device__ const double* n8(int k) const { return k == 0 ? z : (k == 1 ? pold : dinv); }
-  __device__ const double* n16(int) const { return nullptr; }
-  __device__ void take(const unsigned char* slot, int e8, int, Raw& w) const {
-    w.zv = mst_s8(slot, 0, e8);
-    w.po = pold ? mst_s8(slot, 1, e8) : 0.0;
-    w.dv = mst_s8(slot, 2, e8);
-  }
-  __device__ void outs(const unsigned char*, int, int, int id, double2 Av, double2 p) const {
-    out(id, Av, p);
   }
 };
 
@@ -1065,26 +1003,14 @@ __global__ void __launch_bounds__(MG_NT) k_mgs_init(MgsArgs A) {
 // the residual march is the lightest: four CTAs per SM (its own unit geometry g0r; measured at
 // cfg5 0.77 -> 0.66 ms, while the smoothing and direction marches lose at four)
 #ifndef PFB_MGS_MINB_RESID
-#if PFB_MST & 1  // staged: rows in flight come from the stages, not from more resident warps
-#define PFB_MGS_MINB_RESID 3
-#else
 #define PFB_MGS_MINB_RESID 4
-#endif
 #endif
 __global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB_RESID) k_mgs_fine_resid(MgsArgs A) {
   __shared__ MgWarp ws[MG_WARPS];
   const double om = __ldcg(&A.ctl->omega[0]);
   SFineResid op{{&A.C, A.bq, A.L[0].dinv}, om, A.r, A.L[0].t};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
-#if PFB_MST & 1
-  extern __shared__ __align__(128) unsigned char mst_ring[];
-  __shared__ unsigned long long mst_bars[MG_WARPS][8];
-  if (w < A.g0r.n_units)
-    mg_march_st(A.L[0].m, A.g0r, w, op, ws[threadIdx.x >> 5],
-                mst_ring + (threadIdx.x >> 5) * MStage<SFineResid>::WARP, mst_bars[threadIdx.x >> 5]);
-#else
   if (w < A.g0r.n_units) mg_march(A.L[0].m, A.g0r, w, op, ws[threadIdx.x >> 5]);
-#endif
 }
 
 __global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_fine_smooth(MgsArgs A) {
@@ -1094,15 +1020,7 @@ __global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_fine_smooth(MgsArgs
   double rz = 0.0;
   SFineSmooth op{{&A.C, A.bq, A.L[0].dinv}, om, A.r, A.z, &A.L[0].m, &A.L[1].m, A.L[1].e, &rz, {}};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
-#if PFB_MST & 2
-  extern __shared__ __align__(128) unsigned char mst_ring[];
-  __shared__ unsigned long long mst_bars[MG_WARPS][8];
-  if (w < A.g0.n_units)
-    mg_march_st(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5],
-                mst_ring + (threadIdx.x >> 5) * MStage<SFineSmooth>::WARP, mst_bars[threadIdx.x >> 5]);
-#else
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
-#endif
   double v[1] = {rz};
   mg_block_sum<1>(v, red);
   if (threadIdx.x == 0) A.part[blockIdx.x] = v[0];  // r.z partials, reduced by k_mgs_pcg
@@ -1119,15 +1037,7 @@ __global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_pcg(MgsArgs A, int 
   SFinePcg op{{&A.C, A.bq, A.L[0].dinv}, first ? 0.0 : rho[0] / __ldcg(&A.ctl->rho_prev), A.z,
               first ? nullptr : ((k & 1) ? A.p0 : A.p1), (k & 1) ? A.p1 : A.p0, A.q, &pq};
   const int w = blockIdx.x * MG_WARPS + (threadIdx.x >> 5);
-#if PFB_MST & 4
-  extern __shared__ __align__(128) unsigned char mst_ring[];
-  __shared__ unsigned long long mst_bars[MG_WARPS][8];
-  if (w < A.g0.n_units)
-    mg_march_st(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5],
-                mst_ring + (threadIdx.x >> 5) * MStage<SFinePcg>::WARP, mst_bars[threadIdx.x >> 5]);
-#else
   if (w < A.g0.n_units) mg_march(A.L[0].m, A.g0, w, op, ws[threadIdx.x >> 5]);
-#endif
   double v[1] = {pq};
   mg_block_sum<1>(v, red);
   if (threadIdx.x == 0) A.part[n_rz + blockIdx.x] = v[0];
