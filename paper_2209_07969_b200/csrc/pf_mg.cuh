@@ -56,7 +56,8 @@ struct MgLevel {
   // prolongation sources on level l+1 (l <= n_levels-2)
   const int* nbr;
   double* S;
-  float* Sf;      // S rounded to FP32 for the grid-level kernels (s32; the tail keeps S)
+  float* Sf;      // S rounded to FP32 for the grid-level kernels, [MG_NS][n] float4 blocks (s32;
+                  // the tail keeps S)
   const int* rid;
   const int* pid;
 };
@@ -728,16 +729,16 @@ __device__ __forceinline__ double2 hw_sum(double2 v) {  // butterfly over W alig
 // products are bound by these loads.  tests/test_gpu_mg.py compares both on cracked states.
 __device__ __forceinline__ void mg_s4(const MgLevel& L, int n, int id, int s2, double& sxx,
                                       double& sxy, double& syx, double& syy) {
-  if (L.s32) {
-    const float* Sp = L.Sf + (size_t)(4 * s2) * n + id;
-    sxx = __ldg(Sp);
+  if (L.s32) {  // one 16-byte load per block: Sf is [MG_NS][n] float4 (xx, xy, yx, yy)
+    const float4 b = __ldg(reinterpret_cast<const float4*>(L.Sf) + (size_t)s2 * n + id);
+    sxx = b.x;
     if (L.scalar) {  // the packed scalar field: xy, yx, yy are exactly zero (warp-uniform)
       sxy = syx = syy = 0.0;
       return;
     }
-    sxy = __ldg(Sp + n);
-    syx = __ldg(Sp + 2 * (size_t)n);
-    syy = __ldg(Sp + 3 * (size_t)n);
+    sxy = b.y;
+    syx = b.z;
+    syy = b.w;
     return;
   }
   const double* Sp = L.S + (size_t)(4 * s2) * n + id;
@@ -1153,12 +1154,12 @@ __global__ void __launch_bounds__(MG_NT) k_mg_stencil(MgArgs A, int l) {
       }
     }
 #pragma unroll
-    for (int s2 = 0; s2 < MG_NS; ++s2)
+    for (int s2 = 0; s2 < MG_NS; ++s2) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        L.S[(size_t)(4 * s2 + q) * n + id] = acc[s2][q];
-        L.Sf[(size_t)(4 * s2 + q) * n + id] = (float)acc[s2][q];
-      }
+      for (int q = 0; q < 4; ++q) L.S[(size_t)(4 * s2 + q) * n + id] = acc[s2][q];
+      reinterpret_cast<float4*>(L.Sf)[(size_t)s2 * n + id] = make_float4(
+          (float)acc[s2][0], (float)acc[s2][1], (float)acc[s2][2], (float)acc[s2][3]);
+    }
     d2st(L.dinv, id, make_double2(acc[4][0] > 0.0 ? 1.0 / acc[4][0] : 0.0,
                                   acc[4][3] > 0.0 ? 1.0 / acc[4][3] : 0.0));
   });

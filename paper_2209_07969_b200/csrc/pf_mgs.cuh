@@ -1026,7 +1026,10 @@ __global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_fine_smooth(MgsArgs
   if (threadIdx.x == 0) A.part[blockIdx.x] = v[0];  // r.z partials, reduced by k_mgs_pcg
 }
 
-__global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB) k_mgs_pcg(MgsArgs A, int n_rz) {
+#ifndef PFB_MGS_MINB_PCG
+#define PFB_MGS_MINB_PCG PFB_MGS_MINB
+#endif
+__global__ void __launch_bounds__(MG_NT, PFB_MGS_MINB_PCG) k_mgs_pcg(MgsArgs A, int n_rz) {
   __shared__ MgWarp ws[MG_WARPS];
   __shared__ double red[MG_WARPS];
   double rho[1];
