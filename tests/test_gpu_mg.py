@@ -169,6 +169,37 @@ def test_gated_solves_by_scalar_mg_match_reference(cuda_ok, monkeypatch, case_na
         z["table"][:, 4].sum(), rel=0.15, abs=3)
 
 
+@pytest.mark.parametrize("case_name,scheme,steps", [("cfg3", "S3", 40), ("cfg3", "S2", 40)])
+def test_gated_mg_against_jacobi_probe_full_size(cuda_ok, monkeypatch, case_name, scheme, steps):
+    """BASELINE configs[2] (1024^2 shear, where S2 / S3 fall back often) at full size, where the
+    scalar hierarchy is the default: the gated solves with the probe inside the multigrid PCG
+    against the Jacobi-PCG probe -- per-step staggered, Newton and fallback counts identical,
+    forces to 1e-9."""
+    from paper_2209_07969_b200.session import DeviceSession
+
+    dp = C.device_problem(C.get_case(case_name))
+    runs = []
+    for gated in ("1", "0"):
+        monkeypatch.setenv("PFB200_MGS_GATED", gated)
+        s = DeviceSession(dp.layout, dp.params, dp.config, device=0)
+        assert s.solver_kinds()["phase_field"] == "multigrid_pcg"
+        s.init_state()
+        rows = []
+        for _ in range(steps):
+            st = s.step(scheme, dp.bcs, dp.pins)
+            f = s.reaction_force(dp.reactions[0][1], dp.reactions[0][2])
+            rows.append((st.n_stag, st.n_nr_u, st.n_nr_d, st.spd_fallbacks, f, st.cg_iters_d))
+        runs.append(rows)
+        s.close()
+    a, b = runs
+    # the gate did open: the Jacobi-PCG probe solves cost hundreds of iterations each
+    assert sum(r[5] for r in b) > 2 * sum(r[5] for r in a)
+    fpeak = max(abs(r[4]) for r in b)
+    for k, (ra, rb) in enumerate(zip(a, b)):
+        assert ra[:4] == rb[:4], (k, ra, rb)
+        assert abs(ra[4] - rb[4]) <= 1e-9 * fpeak, (k, ra[4], rb[4])
+
+
 @pytest.mark.parametrize("case_name,scheme", [("cfg1", "ST"), ("shear32", "S3")])
 def test_fp32_coarse_stencils_on_cracked_states(cuda_ok, monkeypatch, case_name, scheme):
     """The V-cycle's grid levels read FP32 copies of the coarse stencils by default.  Through the
