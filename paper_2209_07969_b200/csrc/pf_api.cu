@@ -2114,6 +2114,7 @@ static pf_status launch_mom_prepare(pf_handle* h, int full) {
   a.partials = h->partials;
   a.full = full;
   pfb::k_mom_prepare<<<h->n_tiles, pfb::NT, 0, h->stream>>>(a);
+  h->parts_n = h->n_tiles;  // (a prepare kernel without a finalize may have left its own count)
   return launched(h);
 }
 
