@@ -172,8 +172,19 @@ __device__ __forceinline__ double mg_q(int c, int k, int K) {
 //   void cellr(int eid, const CRaw&, const double2 (&v)[4], const double (&a)[4],
 //              double2 (&f)[4])                               the cell's contributions
 //   void out(int id, double2 Av, double2 vin)                 once per owned node
+//   static constexpr bool VY, AUX                             the cells read the value pair's y
+//                                                             lane / the aux value of a node
 // The cell data of the next cell row (branch bits / Newton coefficients) is fetched one row
 // step ahead like the node rows, so no dependent HBM load sits on a row step's critical path.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ int4 lds_int4(unsigned addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+  return v;
+}
 // optional part of an Op (overload rank by the last argument):
 //   void outa(int id, double2 Av, double2 vin, double aux)   out() with the node's aux value
 template <class Op>
@@ -197,6 +208,9 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
   const int R = m.notch_row;
   const bool dupcol = R >= 0 && col >= m.notch_lo && col < m.notch_hi;
   int nbase = -1000000, ebase = -1000000;
+  // the row windows are read twice per row step: from 32-bit shared addresses kept in a
+  // register (the generic form recomputes the warp's window address every time)
+  const unsigned nwin_a = smem_u32(ws.nwin), ewin_a = smem_u32(ws.ewin);
   auto nid = [&](int j) -> int {
     if (j < 0 || j > m.ny) return -1;
     if (j - nbase >= 32 || j < nbase) {
@@ -206,7 +220,7 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
       ws.nwin[lane] = jj <= m.ny ? __ldg(m.nrow + jj) : make_int4(0, 0, 0, 0);
       __syncwarp();
     }
-    const int4 rw = ws.nwin[j - nbase];
+    const int4 rw = lds_int4(nwin_a + 16u * (unsigned)(j - nbase));
     return (col >= rw.x && col < rw.y) ? rw.z + (col - rw.x) : -1;
   };
   auto cell_id = [&](int cj) -> int {
@@ -219,7 +233,7 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
       __syncwarp();
     }
     if (lane >= 31) return -1;
-    const int4 er = ws.ewin[cj - ebase];
+    const int4 er = lds_int4(ewin_a + 16u * (unsigned)(cj - ebase));
     return (col >= er.x && col < er.y) ? er.z + (col - er.x) : -1;
   };
   auto load_dup = [&]() {
@@ -261,8 +275,11 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
     const bool use_dup = lo_slit && dupcol;
     const double2 b0 = use_dup ? ws.dv[lane] : v_lo;
     const double e0 = use_dup ? ws.da[lane] : a_lo;
-    const double2 b1 = shfl_dn(b0), t2 = shfl_dn(v_hi);
-    const double e1 = shfl_dn(e0), e2 = shfl_dn(a_hi);
+    // only the lanes of the value pair / the aux value that the Op's cells read travel between
+    // lanes (every warp shuffle costs a convergence check as well, dead or not)
+    const double2 b1 = Op::VY ? shfl_dn(b0) : make_double2(shfl_dn(b0.x), 0.0);
+    const double2 t2 = Op::VY ? shfl_dn(v_hi) : make_double2(shfl_dn(v_hi.x), 0.0);
+    const double e1 = Op::AUX ? shfl_dn(e0) : 0.0, e2 = Op::AUX ? shfl_dn(a_hi) : 0.0;
     double2 f[4];
     f[0] = f[1] = f[2] = f[3] = make_double2(0.0, 0.0);
     if (eid >= 0) {
@@ -270,7 +287,8 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
       const double a[4] = {e0, e1, e2, a_hi};
       op.cellr(eid, c_cur, v, a, f);
     }
-    const double2 c1l = shfl_up(f[1]), c2l = shfl_up(f[2]);
+    const double2 c1l = Op::VY ? shfl_up(f[1]) : make_double2(shfl_up(f[1].x), 0.0);
+    const double2 c2l = Op::VY ? shfl_up(f[2]) : make_double2(shfl_up(f[2].x), 0.0);
     if (lane_own && cj >= r0) {
       if (use_dup) {
         if (id_lo >= 0) mg_out(op, id_lo, acc_lo, v_lo, a_lo, 0);  // lower face: cells below only
@@ -298,9 +316,6 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
 
 // TMA bulk copies global -> shared completing on one mbarrier (sizes and addresses are
 // multiples of 16 B: the host pads every multigrid array)
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
 __device__ __forceinline__ void mg_bulk_g2s(const void* dst, const void* src, unsigned bytes,
                                             unsigned long long* bar) {
   asm volatile(
@@ -365,6 +380,7 @@ struct FineBase {
     }
   }
   __device__ double2 di(int id) const { return __ldg(reinterpret_cast<const double2*>(dinv) + id); }
+  static constexpr bool VY = true, AUX = true;  // (ux, uy) per node, d as the aux value
 };
 
 __device__ __forceinline__ double2 mask2(double2 v, double2 di) {

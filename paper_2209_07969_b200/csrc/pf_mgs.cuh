@@ -95,6 +95,8 @@ struct SFineBase {
     for (int k = 0; k < 4; ++k) f[k] = make_double2(fx[k], 0.0);
   }
   __device__ double di(int id) const { return __ldg(dinv + id); }
+  // the cells read only the x lane: y and aux carry a node's own data from fetch to out
+  static constexpr bool VY = false, AUX = false;
 };
 
 struct SFineResid : SFineBase {  // x = omega D^-1 r (pre-smoothing from zero), t = r - A x
@@ -235,6 +237,7 @@ struct SFinePcg : SFineBase {  // p = z + beta p_old (owner stores), q = A p (ma
 // sums them in the reference's element order, the free-node flag rides in the aux value.
 // b of a cell in two units' halo is written by both (identical values).
 struct EvoPrepOp {
+  static constexpr bool VY = true, AUX = false;  // (d, d_prev) per node; aux: the free-node flag
   const Consts* C;
   const double *d, *dprev, *psi, *trp, *dev2, *psimax;
   const uint8_t* pmask;
