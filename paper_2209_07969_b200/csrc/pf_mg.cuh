@@ -27,6 +27,12 @@
 // single-CTA kernel with CTA barriers.  Reductions are per-CTA partials summed in a fixed order
 // (last-block pattern), so every result is bit-reproducible run to run.
 #pragma once
+#include <type_traits>
+
+// FineSmooth with its out() data prefetched (124 registers already: off unless it fits)
+#ifndef PFB_SMOOTH_OPRE
+#define PFB_SMOOTH_OPRE 1
+#endif
 
 namespace pfb {
 
@@ -196,6 +202,26 @@ template <class Op>
 __device__ __forceinline__ void mg_out(Op& op, int id, double2 Av, double2 v, double, long) {
   op.out(id, Av, v);
 }
+// Ops whose out() needs per-node data again (r, D^-1 of the momentum marches: both lanes of the
+// value pair are taken) declare ORaw / ofetch / outp: the loads are then issued at the top of
+// the row step, ahead of the cell arithmetic, instead of sitting between it and the store.
+template <class Op, class = void>
+struct MgOutPre {
+  struct Raw {};
+  __device__ static void fetch(Op&, int, Raw&) {}
+  __device__ static void out(Op& op, int id, double2 Av, double2 v, double a, const Raw&) {
+    mg_out(op, id, Av, v, a, 0);
+  }
+};
+template <class Op>
+struct MgOutPre<Op, std::void_t<typename Op::ORaw>> {
+  using Raw = typename Op::ORaw;
+  __device__ static void fetch(Op& op, int id, Raw& r) { op.ofetch(id, r); }
+  __device__ static void out(Op& op, int id, double2 Av, double2 v, double, const Raw& r) {
+    op.outp(id, Av, v, r);
+  }
+};
+
 template <class Op>
 __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int unit, Op& op,
                                          MgWarp& ws) {
@@ -261,6 +287,8 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
   double2 acc_lo = make_double2(0.0, 0.0);
   for (int cj = r0 - 1; cj < r1; ++cj) {
     const int jh = cj + 1;
+    typename MgOutPre<Op>::Raw o_lo;
+    if (lane_own && cj >= r0 && id_lo >= 0) MgOutPre<Op>::fetch(op, id_lo, o_lo);
     a_hi = 0.0;
     const double2 v_hi = id_hi >= 0 ? op.finish(w_hi, id_hi, col, jh, false, a_hi)
                                     : make_double2(0.0, 0.0);
@@ -291,11 +319,11 @@ __device__ __forceinline__ void mg_march(const DMesh& m, const MarchGeom& G, int
     const double2 c2l = Op::VY ? shfl_up(f[2]) : make_double2(shfl_up(f[2].x), 0.0);
     if (lane_own && cj >= r0) {
       if (use_dup) {
-        if (id_lo >= 0) mg_out(op, id_lo, acc_lo, v_lo, a_lo, 0);  // lower face: cells below only
+        if (id_lo >= 0) MgOutPre<Op>::out(op, id_lo, acc_lo, v_lo, a_lo, o_lo);  // lower face: cells below only
         const int idd = ws.did[lane];
         if (idd >= 0) mg_out(op, idd, d2add(c1l, f[0]), ws.dv[lane], ws.da[lane], 0);  // upper face
       } else if (id_lo >= 0) {
-        mg_out(op, id_lo, d2add(d2add(acc_lo, c1l), f[0]), v_lo, a_lo, 0);
+        MgOutPre<Op>::out(op, id_lo, d2add(d2add(acc_lo, c1l), f[0]), v_lo, a_lo, o_lo);
       }
     }
     acc_lo = d2add(c2l, f[3]);
@@ -411,9 +439,20 @@ struct FineResid : FineBase {  // x = omega D^-1 r (pre-smoothing from zero), t 
     fetch(id, i, j, dup, w);
     return finish(w, id, i, j, dup, aux);
   }
-  __device__ void out(int id, double2 Av, double2) const {
-    const double2 bv = d2ldcg(r, id);
-    d2st(t, id, mask2(make_double2(bv.x - Av.x, bv.y - Av.y), di(id)));
+  struct ORaw {
+    double2 bv, dv;
+  };
+  __device__ void ofetch(int id, ORaw& o) const {
+    o.bv = d2ldcg(r, id);
+    o.dv = di(id);
+  }
+  __device__ void outp(int id, double2 Av, double2, const ORaw& o) const {
+    d2st(t, id, mask2(make_double2(o.bv.x - Av.x, o.bv.y - Av.y), o.dv));
+  }
+  __device__ void out(int id, double2 Av, double2 v) const {
+    ORaw o;
+    ofetch(id, o);
+    outp(id, Av, v, o);
   }
 };
 
@@ -580,6 +619,18 @@ struct FineSmooth : FineBase {  // y = omega D^-1 r + P e_1, z = y + omega D^-1 
     d2st(z, id, ev);
     *rz += bv.x * ev.x + bv.y * ev.y;
   }
+#if PFB_SMOOTH_OPRE
+  struct ORaw {
+    double2 bv, dv;
+  };
+  __device__ void ofetch(int id, ORaw& o) const {
+    o.bv = d2ldcg(r, id);
+    o.dv = di(id);
+  }
+  __device__ void outp(int id, double2 Av, double2 y, const ORaw& o) const {
+    out2(id, Av, y, o.dv, o.bv);
+  }
+#endif
   __device__ void out(int id, double2 Av, double2 y) const {
     out2(id, Av, y, di(id), d2ldcg(r, id));
   }
@@ -696,6 +747,11 @@ struct FinePcg : FineBase {  // p = z + beta p_old (owner stores), q = A p (mask
     d2st(q, id, qv);
     if (!own || node_owned(*own, id)) *pq += p.x * qv.x + p.y * qv.y;
   }
+  struct ORaw {
+    double2 dv;
+  };
+  __device__ void ofetch(int id, ORaw& o) const { o.dv = di(id); }
+  __device__ void outp(int id, double2 Av, double2 p, const ORaw& o) const { out2(id, Av, p, o.dv); }
   __device__ void out(int id, double2 Av, double2 p) const { out2(id, Av, p, di(id)); }
 };
 
